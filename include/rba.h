@@ -1,0 +1,166 @@
+/*
+ * rba.h -- C ABI of librba.so, the B200 (sm_100a) FP32 hot path of square-root bundle adjustment
+ * (sqrt-BA; Demmel, Sommer, Cremers, Usenko, arXiv 2103.01843).  Passages are cited as P:<line>
+ * of /root/reference/PAPER.md (LaTeX source of the paper) with the section / equation they fall in.
+ *
+ * Problem statement (Sec. 4 "Square root bundle adjustment"): state x = (x_p, x_l) with
+ * n_p cameras of d_p = 9 parameters each (BAL/Snavely: angle-axis w[3], translation t[3], focal f,
+ * radial k1, k2) and n_l landmarks of 3 coordinates; observations j in O(i) with
+ * residual r_ij = pi(x_i, X_j) - u_ij, energy E = sum |r_ij|^2 (Eq. ba_energy).
+ *
+ * Every call below runs its arithmetic in CUDA kernels of this library; there is no CPU fallback.
+ * All device work is stream-ordered on the context's stream; only calls that return host values
+ * synchronize.  A context is not thread-safe.  Nothing throws across the ABI: every function
+ * returns an rba_status and rba_last_error() gives a thread-local message.
+ *
+ * Multi-GPU (landmark sharding, "parallel for / parallel reduce"): every rank passes the
+ * FULL problem and identical options; the context keeps a deterministic LPT shard of whole
+ * landmarks (cameras replicated) and all-reduces camera-space partial sums over NCCL.  All ranks
+ * must issue the same call sequence (collective semantics).  With world > 1 and
+ * nccl_unique_id == NULL the context runs a "virtual shard": it computes only its partial sums and
+ * performs no collective (used by single-GPU tests of the sharded decomposition).
+ */
+#ifndef RBA_H
+#define RBA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rba_ctx rba_ctx; /* opaque; owns every device buffer it allocates */
+
+typedef enum {
+    RBA_OK = 0,
+    RBA_ERR_INVALID_ARG = 1, /* bad option, lambda < 0, null pointer, out-of-range landmark id   */
+    RBA_ERR_BAD_PROBLEM = 2, /* index out of range, landmark with k < 2, duplicate (cam, pt),
+                                non-finite value, f <= 0, point not in front of a camera (P_z >= -1e-8)
+                                at the initial state, unsupported track length        */
+    RBA_ERR_STATE = 3,       /* call out of order (e.g. PCG before marginalization)              */
+    RBA_ERR_OOM = 4,         /* device allocation failed; rba_last_error() names the bytes       */
+    RBA_ERR_CUDA = 5,        /* CUDA runtime error                                               */
+    RBA_ERR_NCCL = 6         /* NCCL error                                                       */
+} rba_status;
+
+typedef struct {
+    int device;                 /* CUDA device ordinal                                          */
+    void *stream;               /* cudaStream_t to run on; NULL = a stream owned by the context */
+    int world, rank;            /* landmark sharding; world = 1 for a single GPU                */
+    const void *nccl_unique_id; /* 128-byte ncclUniqueId broadcast by the caller, or NULL       */
+    double lambda0;             /* initial LM damping, 1e-4                             */
+    double pcg_rel_tol;         /* PCG: stop when |rho| <= tol |rho_0| (reading C11), 1e-2 */
+    int pcg_max_iters;          /* 500                                                  */
+    double min_rel_decrease;    /* accept a step iff gain ratio > this (reading C9), 1e-3       */
+    double diag_min, diag_max;  /* clamp of D^2 = diag((JS)^T JS) (reading C8), 1e-6/1e32 */
+    /* optional device allocator (e.g. torch's caching allocator); NULL = cudaMalloc/cudaFree   */
+    void *(*alloc)(size_t bytes, void *alloc_ctx);
+    void (*free)(void *ptr, void *alloc_ctx);
+    void *alloc_ctx;
+} rba_options;
+
+typedef struct {
+    int iters;           /* PCG iterations performed                                          */
+    int reason;          /* 0 tolerance reached, 1 max iterations, 2 indefinite (p^T H p <= 0) */
+    double rel_residual; /* |rho_k| / |rho_0|                                                  */
+} rba_pcg_stats;
+
+typedef struct {
+    int64_t iter;        /* LM iteration index; every attempt counts (reading C13)             */
+    int accepted;
+    int pcg_iters;
+    int pcg_reason;
+    double cost;         /* E at the start of the iteration                                   */
+    double cost_trial;   /* E(x + dx); +inf if a point falls behind a camera (C17)            */
+    double cost_after;   /* E after the accept / reject decision                              */
+    double model;        /* L(0) - L(dx), reading C10                                          */
+    double rho;          /* gain ratio (E - E_trial) / model                                   */
+    double lambda;       /* damping used for this attempt                                     */
+    double lambda_next;
+} rba_lm_report;
+
+/* Fill defaults: device 0, own stream, world 1, lambda0 1e-4, tol 1e-2, 500 iters, 1e-3, 1e-6, 1e32. */
+void rba_default_options(rba_options *opt);
+
+/* Create a solver context from the full problem (host FP64, caller-owned, copied; the caller may
+ * free them on return).  cameras: n_cams x 9 row-major [w0 w1 w2 t0 t1 t2 f k1 k2] (BAL order);
+ * points: n_points x 3; obs_cam / obs_pt: camera / landmark index of each observation; obs_uv:
+ * n_obs x 2 pixel coordinates.  Groups observations by landmark into the landmark-block arena
+ * ((2k+3) x (9k+4) FP32 per landmark), uploads, and validates (see
+ * RBA_ERR_BAD_PROBLEM).  *out is NULL on failure. */
+rba_status rba_create(const double *cameras, int64_t n_cams, const double *points, int64_t n_points,
+                      const int32_t *obs_cam, const int32_t *obs_pt, const double *obs_uv, int64_t n_obs,
+                      const rba_options *opt, rba_ctx **out);
+rba_status rba_destroy(rba_ctx *ctx);
+
+/* Linearize at the current state: residuals, E, Jacobian column norms, column scaling
+ * s = 1/(1+|c|) (C7) and D^2 (C8); camera norms are all-reduced across ranks.  Must precede
+ * rba_marginalize_qr whenever the state changed. */
+rba_status rba_linearize(rba_ctx *ctx);
+
+/* Nullspace marginalization of every landmark block: in-place Householder QR
+ * of the landmark columns (3 reflectors), with LM landmark damping sqrt(lambda) D_l folded
+ * in by 6 Givens rotations.  At an unchanged linearization only the damping is
+ * undone and re-applied (backtracking).  lambda >= 0 else RBA_ERR_INVALID_ARG. */
+rba_status rba_marginalize_qr(rba_ctx *ctx, double lambda);
+
+/* Solve the reduced camera system H~ dp = -b~ with block-Jacobi PCG, H~ applied
+ * matrix-free as (Q^_2^T J_p)^T (Q^_2^T J_p) v + lambda D_p^2 v (Eq. cg_mult).  dp stays
+ * on the device.  stats may be NULL. */
+rba_status rba_pcg_solve(rba_ctx *ctx, rba_pcg_stats *stats);
+
+/* Landmark back-substitution dl = -R^_1^-1 (Q^_1^T r + Q^_1^T J_p dp) (Eq. backsub_nm, P:222-226,
+ * P:353-354); forms the trial state x + S dx and the model-decrease terms of reading C10. */
+rba_status rba_backsubstitute(rba_ctx *ctx);
+
+/* E (Eq. ba_energy) at the current state (at_trial = 0) or at the trial state (1).  Synchronizes. */
+rba_status rba_cost(rba_ctx *ctx, int at_trial, double *cost);
+
+/* One LM iteration = linearize (if the state changed) -> marginalize / re-damp -> PCG ->
+ * back-substitute -> trial cost -> accept / reject and lambda update (C9, C10, C13). */
+rba_status rba_lm_step(rba_ctx *ctx, rba_lm_report *report);
+
+/* Full state on every rank (host FP64, caller buffers n_cams x 9 and n_points x 3). */
+rba_status rba_get_state(rba_ctx *ctx, double *cameras, double *points);
+/* Replace the state (host FP64); the next LM step relinearizes.  Resets lambda to lambda0. */
+rba_status rba_set_state(rba_ctx *ctx, const double *cameras, const double *points);
+
+/* ---- test / measurement hooks ----------------------------------------------------------- */
+/* out = H~ v (incl. lambda D_p^2 v at the damping currently folded in); v, out: device FP32 9 n_cams. */
+rba_status rba_matvec(rba_ctx *ctx, const float *v_dev, float *out_dev);
+/* b~ = sum_j A_j^T q_j (host FP64, 9 n_cams), valid after rba_pcg_solve. */
+rba_status rba_get_rhs(rba_ctx *ctx, double *b);
+/* scaled steps dp (9 n_cams) and dl (3 n_points, caller's landmark order; entries of landmarks
+ * owned by other ranks are 0). */
+rba_status rba_get_step(rba_ctx *ctx, double *dp, double *dl);
+/* column scaling and damping diagonals (host FP64): sp, Dp2 (9 n_cams); sl, Dl2 (3 n_points). */
+rba_status rba_get_scaling(rba_ctx *ctx, double *sp, double *Dp2, double *sl, double *Dl2);
+/* Logical (2k+3) x (9k+4) landmark block of landmark `landmark` (caller's index) in its current
+ * state, row-major, into host_buf (capacity `cap` doubles); *rows, *cols receive the shape.
+ * RBA_ERR_INVALID_ARG if the landmark is not owned by this rank or cap is too small. */
+rba_status rba_export_block(rba_ctx *ctx, int64_t landmark, double *host_buf, int64_t cap, int64_t *rows,
+                            int64_t *cols);
+/* Landmark-block bytes: logical = sum (2k+3)(9k+4)*4 + 48 per landmark (6 Givens pairs);
+ * physical = bytes allocated for the arena (16-byte alignment padding included). */
+rba_status rba_arena_bytes(rba_ctx *ctx, int64_t *logical, int64_t *physical);
+/* Number of this library's kernel launches so far. */
+rba_status rba_kernel_launches(rba_ctx *ctx, int64_t *count);
+/* Per-kernel CUDA-event timing on the context stream: enable (1) / disable (0) and reset. */
+rba_status rba_profile(rba_ctx *ctx, int enable);
+/* kernel: 0 linearize(K1), 1 marginalize(K2), 2 damp(K3), 3 precond+rhs(K4), 4 matvec(K5),
+ * 5 pcg update(K6), 6 backsub(K7), 7 cost(K8).  Synchronizes.  Outputs total ms, launch count and
+ * algorithmic bytes moved (per SURVEY §8d-3 / DESIGN.md §5) summed over the recorded launches. */
+rba_status rba_profile_get(rba_ctx *ctx, int kernel, double *total_ms, int64_t *launches, double *bytes);
+/* Deterministic LPT landmark partition (host only, no GPU): owner[j] in [0, world) for track
+ * lengths k[j]; balances block bytes (2k+3)(9k+4). */
+rba_status rba_plan_shards(const int32_t *k, int64_t n_landmarks, int world, int32_t *owner);
+/* NCCL bootstrap helper: writes a fresh 128-byte ncclUniqueId (call on rank 0 only). */
+rba_status rba_nccl_unique_id(void *id128);
+/* Thread-local description of the last error. */
+const char *rba_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RBA_H */

@@ -1,0 +1,760 @@
+// rba_api.cu -- C ABI of librba (include/rba.h): planner (landmark grouping, bucketing by track
+// length, LPT sharding, arena layout), NCCL plumbing and the host-side LM / PCG drivers.  All
+// arithmetic of the method runs in the kernels of rba_kernels.cu.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <queue>
+#include <string>
+#include <vector>
+
+#include "rba_internal.cuh"
+
+using namespace rba;
+
+static thread_local std::string g_err;
+
+static rba_status fail(rba_status s, const std::string &msg) {
+    g_err = msg;
+    return s;
+}
+
+#define CK(call)                                                                                   \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess)                                                                     \
+            return fail(RBA_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));          \
+    } while (0)
+#define CKN(call)                                                                                  \
+    do {                                                                                           \
+        ncclResult_t r_ = (call);                                                                  \
+        if (r_ != ncclSuccess) return fail(RBA_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+    } while (0)
+#define CKS(call)                                                                                  \
+    do {                                                                                           \
+        rba_status s_ = (call);                                                                    \
+        if (s_ != RBA_OK) return s_;                                                               \
+    } while (0)
+
+namespace rba {
+double plan_marg_bytes(rba_ctx *c) { return c->marg_bytes; }
+double plan_matvec_bytes(rba_ctx *c) { return c->matvec_bytes; }
+
+Prof::Prof(rba_ctx *c_, int kid_, double bytes_) : c(c_), kid(kid_), bytes(bytes_) {
+    if (!c->profiling) return;
+    if (c->ev_pool.empty()) {
+        cudaEventCreate(&a);
+    } else {
+        a = c->ev_pool.back();
+        c->ev_pool.pop_back();
+    }
+    cudaEventRecord(a, c->stream);
+}
+void Prof::end() {
+    if (!c->profiling || !a) return;
+    cudaEvent_t b;
+    if (c->ev_pool.empty()) {
+        cudaEventCreate(&b);
+    } else {
+        b = c->ev_pool.back();
+        c->ev_pool.pop_back();
+    }
+    cudaEventRecord(b, c->stream);
+    c->prof.push_back(Launch{kid, a, b, bytes});
+    a = nullptr;
+}
+}  // namespace rba
+
+// ------------------------------------------------------------------------------------ memory
+static rba_status dalloc(rba_ctx *c, void **p, size_t bytes) {
+    *p = nullptr;
+    if (bytes == 0) bytes = 16;
+    if (c->opt.alloc) {
+        *p = c->opt.alloc(bytes, c->opt.alloc_ctx);
+        if (!*p) return fail(RBA_ERR_OOM, "device allocation of " + std::to_string(bytes) + " bytes failed");
+    } else {
+        cudaError_t e = cudaMalloc(p, bytes);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(RBA_ERR_OOM, "cudaMalloc of " + std::to_string(bytes) + " bytes failed: " +
+                                         cudaGetErrorString(e));
+        }
+    }
+    c->allocations.push_back(*p);
+    return RBA_OK;
+}
+template <typename T>
+static rba_status dalloc_n(rba_ctx *c, T **p, int64_t n) {
+    return dalloc(c, reinterpret_cast<void **>(p), sizeof(T) * (size_t)std::max<int64_t>(n, 1));
+}
+
+// ------------------------------------------------------------------------------------ sharding
+// Deterministic LPT on block bytes (2k+3)(9k+4): landmarks by bytes descending (ties by index),
+// each to the least-loaded rank (ties by lowest rank).  SURVEY §8e.
+static void lpt_shards(const int32_t *k, int64_t n, int world, int32_t *owner) {
+    if (world <= 1) {
+        std::fill(owner, owner + n, 0);
+        return;
+    }
+    std::vector<int64_t> idx(n);
+    std::iota(idx.begin(), idx.end(), 0);
+    auto bytes = [&](int64_t j) { return (int64_t)(2 * k[j] + 3) * (9 * k[j] + 4); };
+    std::stable_sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) { return bytes(a) > bytes(b); });
+    using E = std::pair<int64_t, int>;
+    std::priority_queue<E, std::vector<E>, std::greater<E>> pq;
+    for (int r = 0; r < world; r++) pq.push({0, r});
+    for (int64_t j : idx) {
+        E e = pq.top();
+        pq.pop();
+        owner[j] = e.second;
+        e.first += bytes(j);
+        pq.push(e);
+    }
+}
+
+extern "C" rba_status rba_plan_shards(const int32_t *k, int64_t n, int world, int32_t *owner) {
+    if (!k || !owner || n < 0 || world < 1) return fail(RBA_ERR_INVALID_ARG, "rba_plan_shards: bad argument");
+    lpt_shards(k, n, world, owner);
+    return RBA_OK;
+}
+
+extern "C" void rba_default_options(rba_options *o) {
+    std::memset(o, 0, sizeof(*o));
+    o->device = 0;
+    o->world = 1;
+    o->rank = 0;
+    o->lambda0 = 1e-4;
+    o->pcg_rel_tol = 1e-2;
+    o->pcg_max_iters = 500;
+    o->min_rel_decrease = 1e-3;
+    o->diag_min = 1e-6;
+    o->diag_max = 1e32;
+}
+
+extern "C" const char *rba_last_error(void) { return g_err.c_str(); }
+
+extern "C" rba_status rba_nccl_unique_id(void *id128) {
+    if (!id128) return fail(RBA_ERR_INVALID_ARG, "null id");
+    ncclUniqueId id;
+    CKN(ncclGetUniqueId(&id));
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    std::memcpy(id128, &id, 128);
+    return RBA_OK;
+}
+
+static void free_ctx(rba_ctx *c) {
+    if (!c) return;
+    if (c->device >= 0) cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    for (auto &l : c->prof) {
+        cudaEventDestroy(l.a);
+        cudaEventDestroy(l.b);
+    }
+    for (auto e : c->ev_pool) cudaEventDestroy(e);
+    for (void *p : c->allocations) {
+        if (c->opt.free) c->opt.free(p, c->opt.alloc_ctx);
+        else cudaFree(p);
+    }
+    if (c->h_scal) cudaFreeHost(c->h_scal);
+    if (c->h_pcg) cudaFreeHost(c->h_pcg);
+    if (c->have_comm) ncclCommDestroy(c->comm);
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+extern "C" rba_status rba_destroy(rba_ctx *c) {
+    free_ctx(c);
+    return RBA_OK;
+}
+
+// ------------------------------------------------------------------------------------ create
+extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const double *points, int64_t n_points,
+                                 const int32_t *obs_cam, const int32_t *obs_pt, const double *obs_uv,
+                                 int64_t n_obs, const rba_options *opt_in, rba_ctx **out) {
+    if (!out) return fail(RBA_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    rba_options opt;
+    if (opt_in) opt = *opt_in;
+    else rba_default_options(&opt);
+    if (!cameras || !points || (n_obs > 0 && (!obs_cam || !obs_pt || !obs_uv)) || n_cams < 1 || n_points < 0 ||
+        n_obs < 0)
+        return fail(RBA_ERR_INVALID_ARG, "rba_create: null pointer or negative size");
+    if (opt.world < 1 || opt.rank < 0 || opt.rank >= opt.world || !(opt.lambda0 > 0) || !(opt.pcg_rel_tol >= 0) ||
+        opt.pcg_max_iters < 0 || !(opt.diag_min > 0) || !(opt.diag_max >= opt.diag_min))
+        return fail(RBA_ERR_INVALID_ARG, "rba_create: bad options");
+    if (n_obs >= (int64_t)1 << 31 || n_points >= (int64_t)1 << 31 || n_cams >= (int64_t)1 << 28)
+        return fail(RBA_ERR_INVALID_ARG, "rba_create: problem too large for int32 indices");
+    // ---- validation (RBA_ERR_BAD_PROBLEM)
+    for (int64_t i = 0; i < 9 * n_cams; i++)
+        if (!std::isfinite(cameras[i])) return fail(RBA_ERR_BAD_PROBLEM, "non-finite camera parameter at camera " + std::to_string(i / 9));
+    for (int64_t i = 0; i < n_cams; i++)
+        if (!(cameras[9 * i + 6] > 0)) return fail(RBA_ERR_BAD_PROBLEM, "focal length <= 0 at camera " + std::to_string(i));
+    for (int64_t i = 0; i < 3 * n_points; i++)
+        if (!std::isfinite(points[i])) return fail(RBA_ERR_BAD_PROBLEM, "non-finite point at landmark " + std::to_string(i / 3));
+    std::vector<int32_t> kcount(n_points, 0);
+    for (int64_t i = 0; i < n_obs; i++) {
+        if (obs_cam[i] < 0 || obs_cam[i] >= n_cams)
+            return fail(RBA_ERR_BAD_PROBLEM, "observation " + std::to_string(i) + ": camera index out of range");
+        if (obs_pt[i] < 0 || obs_pt[i] >= n_points)
+            return fail(RBA_ERR_BAD_PROBLEM, "observation " + std::to_string(i) + ": landmark index out of range");
+        if (!std::isfinite(obs_uv[2 * i]) || !std::isfinite(obs_uv[2 * i + 1]))
+            return fail(RBA_ERR_BAD_PROBLEM, "observation " + std::to_string(i) + ": non-finite pixel");
+        kcount[obs_pt[i]]++;
+    }
+    for (int64_t j = 0; j < n_points; j++) {
+        if (kcount[j] < 2)
+            return fail(RBA_ERR_BAD_PROBLEM, "landmark " + std::to_string(j) + " has " + std::to_string(kcount[j]) +
+                                                 " < 2 observations (P:469)");
+        if (kcount[j] > KMAX)
+            return fail(RBA_ERR_BAD_PROBLEM, "landmark " + std::to_string(j) + ": track length " +
+                                                 std::to_string(kcount[j]) + " exceeds this build's KMAX " +
+                                                 std::to_string(KMAX));
+    }
+    // observations sorted by (landmark, camera)
+    std::vector<int64_t> ord(n_obs);
+    std::iota(ord.begin(), ord.end(), 0);
+    std::sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) {
+        return obs_pt[a] != obs_pt[b] ? obs_pt[a] < obs_pt[b] : obs_cam[a] < obs_cam[b];
+    });
+    for (int64_t i = 1; i < n_obs; i++)
+        if (obs_pt[ord[i]] == obs_pt[ord[i - 1]] && obs_cam[ord[i]] == obs_cam[ord[i - 1]])
+            return fail(RBA_ERR_BAD_PROBLEM, "duplicate observation of landmark " + std::to_string(obs_pt[ord[i]]) +
+                                                 " by camera " + std::to_string(obs_cam[ord[i]]));
+    std::vector<int64_t> gptr(n_points + 1, 0);
+    for (int64_t j = 0; j < n_points; j++) gptr[j + 1] = gptr[j] + kcount[j];
+
+    rba_ctx *c = new rba_ctx();
+    c->opt = opt;
+    c->device = opt.device;
+    c->world = opt.world;
+    c->rank = opt.rank;
+    c->n_p = n_cams;
+    c->n_l_global = n_points;
+    c->n_obs_global = n_obs;
+    c->lm_lambda = opt.lambda0;
+    auto bail = [&](rba_status s) {
+        free_ctx(c);
+        return s;
+    };
+#define CKC(call)                                                                                  \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess) {                                                                   \
+            g_err = std::string(#call) + ": " + cudaGetErrorString(e_);                            \
+            return bail(RBA_ERR_CUDA);                                                             \
+        }                                                                                          \
+    } while (0)
+#define CKSC(call)                                                                                 \
+    do {                                                                                           \
+        rba_status s_ = (call);                                                                    \
+        if (s_ != RBA_OK) return bail(s_);                                                         \
+    } while (0)
+    CKC(cudaSetDevice(opt.device));
+    if (opt.stream) {
+        c->stream = (cudaStream_t)opt.stream;
+    } else {
+        CKC(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+    }
+    // ---- shard and order the local landmarks: by k, then first camera, then index
+    std::vector<int32_t> owner(n_points);
+    lpt_shards(kcount.data(), n_points, opt.world, owner.data());
+    std::vector<int32_t> loc;
+    for (int64_t j = 0; j < n_points; j++)
+        if (owner[j] == opt.rank) loc.push_back((int32_t)j);
+    std::stable_sort(loc.begin(), loc.end(), [&](int32_t a, int32_t b) {
+        if (kcount[a] != kcount[b]) return kcount[a] < kcount[b];
+        const int32_t ca = obs_cam[ord[gptr[a]]], cb = obs_cam[ord[gptr[b]]];
+        if (ca != cb) return ca < cb;
+        return a < b;
+    });
+    const int64_t nl = (int64_t)loc.size();
+    c->lm_orig = loc;
+    c->orig_to_int.assign(n_points, -1);
+    for (int64_t i = 0; i < nl; i++) c->orig_to_int[loc[i]] = (int32_t)i;
+    c->h_k.resize(nl);
+    c->h_r2.resize(nl);
+    c->h_side.resize(nl);
+    std::vector<int32_t> h_obs0(nl);
+    int64_t nobs_loc = 0, r2_total = 0;
+    for (int64_t i = 0; i < nl; i++) {
+        const int k = kcount[loc[i]];
+        c->h_k[i] = k;
+        h_obs0[i] = (int32_t)nobs_loc;
+        nobs_loc += k;
+        c->h_r2[i] = r2_total;
+        r2_total += r2_floats(k);
+        c->logical_bytes += (int64_t)(2 * k + 3) * (9 * k + 4) * 4 + 48;
+        c->marg_bytes += (double)(2 * k + 3) * (9 * k + 4) * 4 + 48 + 20.0 * k;
+        c->matvec_bytes += 72.0 * k * k;
+    }
+    int64_t side_total = r2_total;
+    for (int64_t i = 0; i < nl; i++) {
+        c->h_side[i] = side_total;
+        side_total += side_floats(c->h_k[i]);
+    }
+    c->arena_floats = side_total;
+    // classes G = 4, 8, 16, 32 and the large-k work items
+    const int bounds[4] = {4, 8, 16, 32};
+    int64_t pos = 0;
+    for (int cls = 0; cls < 4; cls++) {
+        c->small_lo[cls] = pos;
+        while (pos < nl && c->h_k[pos] <= bounds[cls]) pos++;
+        c->small_hi[cls] = pos;
+    }
+    c->large_lo = pos;
+    c->large_hi = nl;
+    std::vector<LargeItem> items;
+    for (int64_t i = pos; i < nl; i++) {
+        const int k = c->h_k[i];
+        c->max_large_k = std::max<int64_t>(c->max_large_k, k);
+        const int T = n_tiles(k);
+        const int tpi = std::max(1, 65536 / (36 * k));
+        for (int t0 = 0; t0 < T; t0 += tpi) items.push_back(LargeItem{(int32_t)i, t0, std::min(T, t0 + tpi), 0});
+    }
+    c->n_large_items = (int64_t)items.size();
+    // ---- device buffers
+    DevProblem &d = c->d;
+    d.n_p = n_cams;
+    d.n_l = nl;
+    d.n_obs = nobs_loc;
+    CKSC(dalloc_n(c, &d.cams, 9 * n_cams));
+    CKSC(dalloc_n(c, &d.cams_trial, 9 * n_cams));
+    CKSC(dalloc_n(c, &d.pts, 3 * nl));
+    CKSC(dalloc_n(c, &d.pts_trial, 3 * nl));
+    CKSC(dalloc_n(c, &d.lm_k, nl));
+    CKSC(dalloc_n(c, &d.lm_obs0, nl));
+    CKSC(dalloc_n(c, &d.lm_r2, nl));
+    CKSC(dalloc_n(c, &d.lm_side, nl));
+    CKSC(dalloc_n(c, &d.obs_cam, nobs_loc));
+    CKSC(dalloc_n(c, &d.obs_lm, nobs_loc));
+    CKSC(dalloc_n(c, &d.obs_uv, nobs_loc));
+    CKSC(dalloc_n(c, &d.cam_n2, 9 * n_cams));
+    CKSC(dalloc_n(c, &d.sp, 9 * n_cams));
+    CKSC(dalloc_n(c, &d.Dp2, 9 * n_cams));
+    CKSC(dalloc_n(c, &d.lm_s, 3 * nl));
+    CKSC(dalloc_n(c, &d.lm_D, 3 * nl));
+    CKSC(dalloc_n(c, &d.arena, c->arena_floats));
+    CKSC(dalloc_n(c, &d.pacc, 54 * n_cams));
+    CKSC(dalloc_n(c, &d.bt, 9 * n_cams));
+    CKSC(dalloc_n(c, &d.Minv, 81 * n_cams));
+    CKSC(dalloc_n(c, &d.x, 9 * n_cams));
+    CKSC(dalloc_n(c, &d.r, 9 * n_cams));
+    CKSC(dalloc_n(c, &d.z, 9 * n_cams));
+    CKSC(dalloc_n(c, &d.p, 9 * n_cams));
+    CKSC(dalloc_n(c, &d.w, 9 * n_cams));
+    CKSC(dalloc_n(c, &d.dl, 3 * nl));
+    CKSC(dalloc_n(c, &d.scal, SC_N));
+    CKSC(dalloc_n(c, &d.pcg, 1));
+    CKSC(dalloc_n(c, &d.large_items, std::max<int64_t>(1, c->n_large_items)));
+    CKC(cudaMallocHost(&c->h_scal, sizeof(double) * SC_N));
+    CKC(cudaMallocHost(&c->h_pcg, sizeof(PcgState)));
+    // ---- upload (host staging in the device layout)
+    {
+        std::vector<float> hc(9 * n_cams), hp(3 * std::max<int64_t>(nl, 1));
+        for (int64_t i = 0; i < 9 * n_cams; i++) hc[i] = (float)cameras[i];
+        for (int64_t i = 0; i < nl; i++)
+            for (int q = 0; q < 3; q++) hp[3 * i + q] = (float)points[3 * (int64_t)loc[i] + q];
+        std::vector<int32_t> ocam(std::max<int64_t>(nobs_loc, 1)), olm(std::max<int64_t>(nobs_loc, 1));
+        std::vector<float2> ouv(std::max<int64_t>(nobs_loc, 1));
+        for (int64_t i = 0; i < nl; i++) {
+            const int64_t g0 = gptr[loc[i]];
+            for (int o = 0; o < c->h_k[i]; o++) {
+                const int64_t src = ord[g0 + o];
+                const int64_t dst = h_obs0[i] + o;
+                ocam[dst] = obs_cam[src];
+                olm[dst] = (int32_t)i;
+                ouv[dst] = make_float2((float)obs_uv[2 * src], (float)obs_uv[2 * src + 1]);
+            }
+        }
+        CKC(cudaMemcpyAsync(d.cams, hc.data(), sizeof(float) * hc.size(), cudaMemcpyHostToDevice, c->stream));
+        CKC(cudaMemcpyAsync(d.pts, hp.data(), sizeof(float) * 3 * nl, cudaMemcpyHostToDevice, c->stream));
+        CKC(cudaMemcpyAsync(d.lm_k, c->h_k.data(), sizeof(int32_t) * nl, cudaMemcpyHostToDevice, c->stream));
+        CKC(cudaMemcpyAsync(d.lm_obs0, h_obs0.data(), sizeof(int32_t) * nl, cudaMemcpyHostToDevice, c->stream));
+        CKC(cudaMemcpyAsync(d.lm_r2, c->h_r2.data(), sizeof(int64_t) * nl, cudaMemcpyHostToDevice, c->stream));
+        CKC(cudaMemcpyAsync(d.lm_side, c->h_side.data(), sizeof(int64_t) * nl, cudaMemcpyHostToDevice, c->stream));
+        CKC(cudaMemcpyAsync(d.obs_cam, ocam.data(), sizeof(int32_t) * nobs_loc, cudaMemcpyHostToDevice, c->stream));
+        CKC(cudaMemcpyAsync(d.obs_lm, olm.data(), sizeof(int32_t) * nobs_loc, cudaMemcpyHostToDevice, c->stream));
+        CKC(cudaMemcpyAsync(d.obs_uv, ouv.data(), sizeof(float2) * nobs_loc, cudaMemcpyHostToDevice, c->stream));
+        if (!items.empty())
+            CKC(cudaMemcpyAsync(d.large_items, items.data(), sizeof(LargeItem) * items.size(),
+                                cudaMemcpyHostToDevice, c->stream));
+        CKC(cudaMemsetAsync(d.scal, 0, sizeof(double) * SC_N, c->stream));
+        // front-of-camera validation at the initial state, in a kernel
+        int *dbad = reinterpret_cast<int *>(d.pcg);  // scratch
+        CKC(cudaMemsetAsync(dbad, 0, sizeof(int), c->stream));
+        CKC(launch_check_depth(c, dbad));
+        int hbad = 0;
+        CKC(cudaMemcpyAsync(&hbad, dbad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        CKC(cudaStreamSynchronize(c->stream));
+        if (hbad) {
+            g_err = std::to_string(hbad) + " observation(s) not in front of their camera (P_z >= -1e-8) at the initial state";
+            return bail(RBA_ERR_BAD_PROBLEM);
+        }
+    }
+    if (opt.world > 1 && opt.nccl_unique_id) {
+        ncclUniqueId id;
+        std::memcpy(&id, opt.nccl_unique_id, sizeof(id));
+        ncclResult_t r = ncclCommInitRank(&c->comm, opt.world, id, opt.rank);
+        if (r != ncclSuccess) {
+            g_err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
+            return bail(RBA_ERR_NCCL);
+        }
+        c->have_comm = true;
+    }
+    *out = c;
+    return RBA_OK;
+#undef CKC
+#undef CKSC
+}
+
+// ------------------------------------------------------------------------------------ helpers
+static rba_status allreduce(rba_ctx *c, void *buf, size_t count, ncclDataType_t t) {
+    if (!c->have_comm || count == 0) return RBA_OK;
+    CKN(ncclAllReduce(buf, buf, count, t, ncclSum, c->comm, c->stream));
+    return RBA_OK;
+}
+
+static rba_status read_scal(rba_ctx *c) {
+    CK(cudaMemcpyAsync(c->h_scal, c->d.scal, sizeof(double) * SC_N, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return RBA_OK;
+}
+
+// ------------------------------------------------------------------------------------ steps
+extern "C" rba_status rba_linearize(rba_ctx *c) {
+    if (!c) return fail(RBA_ERR_INVALID_ARG, "null ctx");
+    CK(cudaSetDevice(c->device));
+    DevProblem &d = c->d;
+    CK(cudaMemsetAsync(d.cam_n2, 0, sizeof(float) * 9 * d.n_p, c->stream));
+    CK(cudaMemsetAsync(d.scal + SC_E, 0, sizeof(double) * 2, c->stream));
+    CK(launch_linearize(c));
+    CKS(allreduce(c, d.cam_n2, 9 * d.n_p, ncclFloat));
+    CKS(allreduce(c, d.scal + SC_E, 2, ncclDouble));
+    CK(launch_cam_scale(c));
+    CKS(read_scal(c));
+    if (c->h_scal[SC_BAD] > 0) return fail(RBA_ERR_BAD_PROBLEM, "a point is not in front of its camera at the current state");
+    c->cost = c->h_scal[SC_E];
+    c->linearized = true;
+    c->marginalized = false;
+    c->solved = false;
+    c->backsubbed = false;
+    return RBA_OK;
+}
+
+extern "C" rba_status rba_marginalize_qr(rba_ctx *c, double lambda) {
+    if (!c) return fail(RBA_ERR_INVALID_ARG, "null ctx");
+    if (!(lambda >= 0) || !std::isfinite(lambda)) return fail(RBA_ERR_INVALID_ARG, "lambda must be finite and >= 0");
+    if (!c->linearized) return fail(RBA_ERR_STATE, "rba_marginalize_qr before rba_linearize");
+    CK(cudaSetDevice(c->device));
+    if (!c->marginalized) {
+        CK(launch_marginalize(c, (float)lambda));
+        c->marginalized = true;
+    } else if ((float)lambda != (float)c->lambda_blocks) {
+        CK(launch_redamp(c, (float)lambda));
+    }
+    c->lambda_blocks = lambda;
+    c->solved = false;
+    c->backsubbed = false;
+    return RBA_OK;
+}
+
+extern "C" rba_status rba_pcg_solve(rba_ctx *c, rba_pcg_stats *stats) {
+    if (!c) return fail(RBA_ERR_INVALID_ARG, "null ctx");
+    if (!c->marginalized) return fail(RBA_ERR_STATE, "rba_pcg_solve before rba_marginalize_qr");
+    CK(cudaSetDevice(c->device));
+    DevProblem &d = c->d;
+    const float lam = (float)c->lambda_blocks;
+    CK(cudaMemsetAsync(d.pacc, 0, sizeof(float) * 54 * d.n_p, c->stream));
+    CK(cudaMemsetAsync(d.scal + SC_BAD, 0, sizeof(double), c->stream));
+    CK(launch_precond_rhs(c));
+    CKS(allreduce(c, d.pacc, 54 * d.n_p, ncclFloat));
+    CK(launch_precond_finalize(c, lam));
+    CK(launch_pcg_init(c, (float)c->opt.pcg_rel_tol, c->opt.pcg_max_iters));
+    int batch = 2;
+    for (;;) {
+        CK(cudaMemcpyAsync(c->h_pcg, d.pcg, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (c->h_pcg->done || c->h_pcg->it >= c->opt.pcg_max_iters) break;
+        const int todo = std::min(batch, c->opt.pcg_max_iters - c->h_pcg->it);
+        for (int b = 0; b < todo; b++) {
+            CK(cudaMemsetAsync(d.w, 0, sizeof(float) * 9 * d.n_p, c->stream));
+            CK(launch_matvec_pcg(c));
+            CKS(allreduce(c, d.w, 9 * d.n_p, ncclFloat));
+            CK(launch_pcg_step(c, lam, (float)c->opt.pcg_rel_tol, c->opt.pcg_max_iters));
+        }
+        batch = std::min(batch * 2, 64);
+    }
+    CKS(read_scal(c));
+    if (stats) {
+        stats->iters = c->h_pcg->it;
+        stats->reason = c->h_pcg->reason;
+        stats->rel_residual = c->h_pcg->r0 > 0 ? c->h_pcg->rn / c->h_pcg->r0 : 0.0;
+        if (c->h_scal[SC_BAD] > 0) stats->reason = 2;  // preconditioner block not SPD
+    }
+    c->solved = true;
+    c->backsubbed = false;
+    return RBA_OK;
+}
+
+extern "C" rba_status rba_backsubstitute(rba_ctx *c) {
+    if (!c) return fail(RBA_ERR_INVALID_ARG, "null ctx");
+    if (!c->solved) return fail(RBA_ERR_STATE, "rba_backsubstitute before rba_pcg_solve");
+    CK(cudaSetDevice(c->device));
+    CK(cudaMemsetAsync(c->d.scal + SC_Q1R2, 0, sizeof(double) * 2, c->stream));
+    CK(launch_backsub(c, (float)c->lambda_blocks));
+    c->backsubbed = true;
+    return RBA_OK;
+}
+
+extern "C" rba_status rba_cost(rba_ctx *c, int at_trial, double *cost) {
+    if (!c || !cost) return fail(RBA_ERR_INVALID_ARG, "null argument");
+    if (at_trial && !c->backsubbed) return fail(RBA_ERR_STATE, "trial cost before rba_backsubstitute");
+    CK(cudaSetDevice(c->device));
+    const int slot = at_trial ? SC_ET : SC_E;
+    CK(cudaMemsetAsync(c->d.scal + slot, 0, sizeof(double) * 2, c->stream));
+    CK(launch_cost(c, at_trial, slot));
+    CKS(allreduce(c, c->d.scal + slot, 2, ncclDouble));
+    CKS(read_scal(c));
+    *cost = c->h_scal[slot + 1] > 0 ? INFINITY : c->h_scal[slot];
+    return RBA_OK;
+}
+
+extern "C" rba_status rba_lm_step(rba_ctx *c, rba_lm_report *rep) {
+    if (!c) return fail(RBA_ERR_INVALID_ARG, "null ctx");
+    rba_lm_report R;
+    std::memset(&R, 0, sizeof(R));
+    R.iter = c->iteration;
+    if (c->need_lin || !c->linearized) {
+        CKS(rba_linearize(c));
+        c->need_lin = false;
+    }
+    CKS(rba_marginalize_qr(c, c->lm_lambda));
+    R.cost = c->cost;
+    R.lambda = c->lm_lambda;
+    rba_pcg_stats st;
+    CKS(rba_pcg_solve(c, &st));
+    R.pcg_iters = st.iters;
+    R.pcg_reason = st.reason;
+    bool accept = false;
+    R.cost_trial = INFINITY;
+    if (st.reason != 2) {
+        CKS(rba_backsubstitute(c));
+        DevProblem &d = c->d;
+        CK(cudaMemsetAsync(d.scal + SC_ET, 0, sizeof(double) * 2, c->stream));
+        CK(launch_trial_cost(c));
+        CKS(allreduce(c, d.scal + SC_ET, 4, ncclDouble));
+        CKS(read_scal(c));
+        const double *s = c->h_scal;
+        const double Et = s[SC_BADT] > 0 ? INFINITY : s[SC_ET];
+        const double model = s[SC_Q1R2] + s[SC_DAMPL] + s[SC_MODELP];
+        const double rho = (c->cost - Et) / model;
+        R.cost_trial = Et;
+        R.model = model;
+        R.rho = rho;
+        accept = model > 0 && std::isfinite(Et) && rho > c->opt.min_rel_decrease;
+        if (accept) {
+            CK(cudaMemcpyAsync(d.cams, d.cams_trial, sizeof(float) * 9 * d.n_p, cudaMemcpyDeviceToDevice, c->stream));
+            CK(cudaMemcpyAsync(d.pts, d.pts_trial, sizeof(float) * 3 * d.n_l, cudaMemcpyDeviceToDevice, c->stream));
+            c->cost = Et;
+            const double t = 2.0 * rho - 1.0;
+            c->lm_lambda *= std::max(1.0 / 3.0, 1.0 - t * t * t);
+            c->lm_nu = 2.0;
+            c->need_lin = true;
+            c->linearized = false;
+        }
+    }
+    if (!accept) {
+        c->lm_lambda *= c->lm_nu;
+        c->lm_nu *= 2.0;
+    }
+    c->lm_lambda = std::min(std::max(c->lm_lambda, 1e-16), 1e16);
+    R.accepted = accept;
+    R.cost_after = c->cost;
+    R.lambda_next = c->lm_lambda;
+    c->iteration++;
+    if (rep) *rep = R;
+    return RBA_OK;
+}
+
+// ------------------------------------------------------------------------------------ state
+extern "C" rba_status rba_get_state(rba_ctx *c, double *cameras, double *points) {
+    if (!c || !cameras || !points) return fail(RBA_ERR_INVALID_ARG, "null argument");
+    CK(cudaSetDevice(c->device));
+    const DevProblem &d = c->d;
+    std::vector<float> hc(9 * d.n_p), hp(3 * c->n_l_global, 0.f), loc(3 * std::max<int64_t>(d.n_l, 1));
+    CK(cudaMemcpyAsync(hc.data(), d.cams, sizeof(float) * hc.size(), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(loc.data(), d.pts, sizeof(float) * 3 * d.n_l, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (int64_t i = 0; i < d.n_l; i++)
+        for (int q = 0; q < 3; q++) hp[3 * (int64_t)c->lm_orig[i] + q] = loc[3 * i + q];
+    if (c->have_comm) {
+        float *buf = nullptr;
+        CK(cudaMalloc(&buf, sizeof(float) * std::max<int64_t>(1, hp.size())));
+        CK(cudaMemcpyAsync(buf, hp.data(), sizeof(float) * hp.size(), cudaMemcpyHostToDevice, c->stream));
+        rba_status s = allreduce(c, buf, hp.size(), ncclFloat);
+        if (s == RBA_OK) {
+            CK(cudaMemcpyAsync(hp.data(), buf, sizeof(float) * hp.size(), cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+        }
+        cudaFree(buf);
+        if (s != RBA_OK) return s;
+    }
+    for (size_t i = 0; i < hc.size(); i++) cameras[i] = hc[i];
+    for (size_t i = 0; i < hp.size(); i++) points[i] = hp[i];
+    return RBA_OK;
+}
+
+extern "C" rba_status rba_set_state(rba_ctx *c, const double *cameras, const double *points) {
+    if (!c || !cameras || !points) return fail(RBA_ERR_INVALID_ARG, "null argument");
+    CK(cudaSetDevice(c->device));
+    const DevProblem &d = c->d;
+    std::vector<float> hc(9 * d.n_p), hp(3 * std::max<int64_t>(d.n_l, 1));
+    for (size_t i = 0; i < hc.size(); i++) hc[i] = (float)cameras[i];
+    for (int64_t i = 0; i < d.n_l; i++)
+        for (int q = 0; q < 3; q++) hp[3 * i + q] = (float)points[3 * (int64_t)c->lm_orig[i] + q];
+    CK(cudaMemcpyAsync(d.cams, hc.data(), sizeof(float) * hc.size(), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(d.pts, hp.data(), sizeof(float) * 3 * d.n_l, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->linearized = c->marginalized = c->solved = c->backsubbed = false;
+    c->need_lin = true;
+    c->lm_lambda = c->opt.lambda0;
+    c->lm_nu = 2.0;
+    return RBA_OK;
+}
+
+// ------------------------------------------------------------------------------------ hooks
+extern "C" rba_status rba_matvec(rba_ctx *c, const float *v, float *outv) {
+    if (!c || !v || !outv) return fail(RBA_ERR_INVALID_ARG, "null argument");
+    if (!c->marginalized) return fail(RBA_ERR_STATE, "rba_matvec before rba_marginalize_qr");
+    CK(cudaSetDevice(c->device));
+    CK(cudaMemsetAsync(outv, 0, sizeof(float) * 9 * c->d.n_p, c->stream));
+    CK(launch_matvec(c, v, outv));
+    CKS(allreduce(c, outv, 9 * c->d.n_p, ncclFloat));
+    CK(launch_add_damping(c, v, outv, (float)c->lambda_blocks));
+    return RBA_OK;
+}
+
+extern "C" rba_status rba_get_rhs(rba_ctx *c, double *b) {
+    if (!c || !b) return fail(RBA_ERR_INVALID_ARG, "null argument");
+    if (!c->solved) return fail(RBA_ERR_STATE, "rba_get_rhs before rba_pcg_solve");
+    std::vector<float> h(9 * c->d.n_p);
+    CK(cudaMemcpyAsync(h.data(), c->d.bt, sizeof(float) * h.size(), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (size_t i = 0; i < h.size(); i++) b[i] = h[i];
+    return RBA_OK;
+}
+
+extern "C" rba_status rba_get_step(rba_ctx *c, double *dp, double *dl) {
+    if (!c || !dp || !dl) return fail(RBA_ERR_INVALID_ARG, "null argument");
+    if (!c->solved) return fail(RBA_ERR_STATE, "rba_get_step before rba_pcg_solve");
+    std::vector<float> h(9 * c->d.n_p), l(3 * std::max<int64_t>(c->d.n_l, 1));
+    CK(cudaMemcpyAsync(h.data(), c->d.x, sizeof(float) * h.size(), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(l.data(), c->d.dl, sizeof(float) * 3 * c->d.n_l, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (size_t i = 0; i < h.size(); i++) dp[i] = h[i];
+    for (int64_t i = 0; i < 3 * c->n_l_global; i++) dl[i] = 0.0;
+    if (c->backsubbed)
+        for (int64_t i = 0; i < c->d.n_l; i++)
+            for (int q = 0; q < 3; q++) dl[3 * (int64_t)c->lm_orig[i] + q] = l[3 * i + q];
+    return RBA_OK;
+}
+
+extern "C" rba_status rba_get_scaling(rba_ctx *c, double *sp, double *Dp2, double *sl, double *Dl2) {
+    if (!c || !sp || !Dp2 || !sl || !Dl2) return fail(RBA_ERR_INVALID_ARG, "null argument");
+    if (!c->linearized) return fail(RBA_ERR_STATE, "rba_get_scaling before rba_linearize");
+    const int64_t n = 9 * c->d.n_p, m = 3 * std::max<int64_t>(c->d.n_l, 1);
+    std::vector<float> a(n), b(n), s(m), D(m);
+    CK(cudaMemcpyAsync(a.data(), c->d.sp, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(b.data(), c->d.Dp2, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(s.data(), c->d.lm_s, sizeof(float) * 3 * c->d.n_l, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(D.data(), c->d.lm_D, sizeof(float) * 3 * c->d.n_l, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (int64_t i = 0; i < n; i++) sp[i] = a[i], Dp2[i] = b[i];
+    for (int64_t i = 0; i < 3 * c->n_l_global; i++) sl[i] = 0.0, Dl2[i] = 0.0;
+    if (c->marginalized)
+        for (int64_t i = 0; i < c->d.n_l; i++)
+            for (int q = 0; q < 3; q++) {
+                sl[3 * (int64_t)c->lm_orig[i] + q] = s[3 * i + q];
+                Dl2[3 * (int64_t)c->lm_orig[i] + q] = (double)D[3 * i + q] * D[3 * i + q];
+            }
+    return RBA_OK;
+}
+
+extern "C" rba_status rba_export_block(rba_ctx *c, int64_t landmark, double *buf, int64_t cap, int64_t *rows,
+                                       int64_t *cols) {
+    if (!c || !buf || !rows || !cols) return fail(RBA_ERR_INVALID_ARG, "null argument");
+    if (landmark < 0 || landmark >= c->n_l_global || c->orig_to_int[landmark] < 0)
+        return fail(RBA_ERR_INVALID_ARG, "landmark not owned by this rank");
+    if (!c->marginalized) return fail(RBA_ERR_STATE, "rba_export_block before rba_marginalize_qr");
+    const int64_t j = c->orig_to_int[landmark];
+    const int k = c->h_k[j];
+    const int64_t R = 2 * k + 3, C = 9 * k + 4;
+    *rows = R;
+    *cols = C;
+    if (cap < R * C) return fail(RBA_ERR_INVALID_ARG, "buffer too small");
+    std::vector<float> r2(r2_floats(k)), side(side_floats(k));
+    CK(cudaMemcpyAsync(r2.data(), c->d.arena + c->h_r2[j], sizeof(float) * r2.size(), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(side.data(), c->d.arena + c->h_side[j], sizeof(float) * side.size(), cudaMemcpyDeviceToHost,
+                       c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    const float *TL = side.data() + side_tl(k);
+    for (int64_t row = 0; row < R; row++) {
+        double *out = buf + row * C;
+        for (int o = 0; o < k; o++)
+            for (int q = 0; q < 9; q++)
+                out[9 * o + q] = row < 3 ? side[row * 9 * k + 9 * o + q] : r2[r2_index(k, (int)row - 3, o, q)];
+        for (int q = 0; q < 4; q++) out[9 * k + q] = TL[4 * row + q];
+    }
+    return RBA_OK;
+}
+
+extern "C" rba_status rba_arena_bytes(rba_ctx *c, int64_t *logical, int64_t *physical) {
+    if (!c || !logical || !physical) return fail(RBA_ERR_INVALID_ARG, "null argument");
+    *logical = c->logical_bytes;
+    *physical = c->arena_floats * 4;
+    return RBA_OK;
+}
+
+extern "C" rba_status rba_kernel_launches(rba_ctx *c, int64_t *count) {
+    if (!c || !count) return fail(RBA_ERR_INVALID_ARG, "null argument");
+    *count = c->launches;
+    return RBA_OK;
+}
+
+extern "C" rba_status rba_profile(rba_ctx *c, int enable) {
+    if (!c) return fail(RBA_ERR_INVALID_ARG, "null ctx");
+    CK(cudaStreamSynchronize(c->stream));
+    for (auto &l : c->prof) {
+        c->ev_pool.push_back(l.a);
+        c->ev_pool.push_back(l.b);
+    }
+    c->prof.clear();
+    c->profiling = enable != 0;
+    return RBA_OK;
+}
+
+extern "C" rba_status rba_profile_get(rba_ctx *c, int kernel, double *total_ms, int64_t *launches, double *bytes) {
+    if (!c || !total_ms || !launches || !bytes || kernel < 0 || kernel >= KID_N)
+        return fail(RBA_ERR_INVALID_ARG, "bad argument");
+    CK(cudaStreamSynchronize(c->stream));
+    double ms = 0, by = 0;
+    int64_t n = 0;
+    for (auto &l : c->prof)
+        if (l.kid == kernel) {
+            float t = 0.f;
+            CK(cudaEventElapsedTime(&t, l.a, l.b));
+            ms += t;
+            by += l.bytes;
+            n++;
+        }
+    *total_ms = ms;
+    *launches = n;
+    *bytes = by;
+    return RBA_OK;
+}

@@ -1,0 +1,1368 @@
+// rba_kernels.cu -- sm_100a kernels of the FP32 sqrt-BA hot path (product path; no oracle code).
+//
+//  K0 k_check_depth       validation: every observation in front of its camera
+//  K1 k_linearize         residuals, E, camera Jacobian column norms (P:348 scaling)
+//  K1b k_cam_scale        s = 1/(1+|c|), D^2 = clamp(|c|^2 s^2) (C7, C8)
+//  K2 k_marg_small<G>     k <= 32: warp-group per landmark: Jacobians, 3 Householder reflectors
+//     k_marg_large        k > 32: CTA per (landmark, tile range); compact-WY emission of
+//                         Q^T [J_p | J_l | r] with the 6 damping Givens rotations folded in
+//
+//  K3 k_redamp            undo / re-apply the 6 damping rotations in place (Fig. 3)
+//  K4 k_precond_rhs       block-Jacobi blocks + b~ = sum A^T q
+//     k_precond_finalize  + lambda D_p^2, Cholesky inverse per camera (C12)
+//  K5 k_matvec_small<G>,  H~ v = sum_j A_j^T (A_j v_j) (Eq. cg_mult), one HBM pass
+//     k_matvec_large
+//  K6 k_pcg_init/step     PCG vector updates, dots in FP64, device-side termination flag
+//  K7 k_backsub           dl = -R^_1^-1 (Q^_1^T r^ + Q^_1^T J_p dp), trial point
+//  K8 k_cost              E at the current or trial state (Eq. ba_energy; C14, C17)
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "rba_internal.cuh"
+
+namespace rba {
+
+// ============================================================================ camera model
+// BAL / Snavely (readings C1, C2, C22): P = R(w) X + t, p = -P_xy / P_z,
+// d = 1 + k1 |p|^2 + k2 |p|^4, pi = f d p, r = pi - u.  Jacobians for the additive update of all
+// 9 camera parameters: dP/dw = -[R X]_x J_left(w).  Returns P_z.
+__device__ __forceinline__ float cam_model(const float *__restrict__ cam, float X0, float X1, float X2, float u,
+                                           float v, float *r, float *Jc, float *Jl) {
+    const float w0 = cam[0], w1 = cam[1], w2 = cam[2];
+    const float th2 = w0 * w0 + w1 * w1 + w2 * w2;
+    float a, b, cc;  // R = I + a K + b K^2, J_left = I + b K + cc K^2
+    if (th2 < 1e-8f) {
+        a = 1.f - th2 * (1.f / 6.f);
+        b = 0.5f - th2 * (1.f / 24.f);
+        cc = 1.f / 6.f - th2 * (1.f / 120.f);
+    } else {
+        const float th = sqrtf(th2);
+        float s, co;
+        sincosf(th, &s, &co);
+        a = s / th;
+        const float hs = sinf(0.5f * th);
+        b = 2.f * hs * hs / th2;  // (1 - cos th) / th^2 without cancellation
+        cc = (th < 0.5f) ? (1.f / 6.f - th2 * (1.f / 120.f) + th2 * th2 * (1.f / 5040.f)) : (th - s) / (th2 * th);
+    }
+    const float cx0 = w1 * X2 - w2 * X1, cx1 = w2 * X0 - w0 * X2, cx2 = w0 * X1 - w1 * X0;
+    const float dx0 = w1 * cx2 - w2 * cx1, dx1 = w2 * cx0 - w0 * cx2, dx2 = w0 * cx1 - w1 * cx0;
+    const float RX0 = X0 + a * cx0 + b * dx0, RX1 = X1 + a * cx1 + b * dx1, RX2 = X2 + a * cx2 + b * dx2;
+    const float P0 = RX0 + cam[3], P1 = RX1 + cam[4], P2 = RX2 + cam[5];
+    const float iz = -1.f / P2;
+    const float px = P0 * iz, py = P1 * iz;
+    const float n = px * px + py * py;
+    const float f = cam[6], k1 = cam[7], k2 = cam[8];
+    const float dd = 1.f + k1 * n + k2 * n * n;
+    r[0] = f * dd * px - u;
+    r[1] = f * dd * py - v;
+    if (!Jc) return P2;
+    // dpi/dP = f (d I + e p p^T) * iz [[1,0,px],[0,1,py]]
+    const float e = 2.f * (k1 + 2.f * k2 * n);
+    const float D00 = f * (dd + e * px * px), D01 = f * e * px * py, D11 = f * (dd + e * py * py);
+    const float A00 = iz * D00, A01 = iz * D01, A02 = iz * (D00 * px + D01 * py);
+    const float A10 = iz * D01, A11 = iz * D11, A12 = iz * (D01 * px + D11 * py);
+    // R = (1 - b th2) I + a K + b w w^T
+    const float rd = 1.f - b * th2;
+    const float R00 = rd + b * w0 * w0, R11 = rd + b * w1 * w1, R22 = rd + b * w2 * w2;
+    const float R01 = -a * w2 + b * w0 * w1, R02 = a * w1 + b * w0 * w2;
+    const float R10 = a * w2 + b * w0 * w1, R12 = -a * w0 + b * w1 * w2;
+    const float R20 = -a * w1 + b * w0 * w2, R21 = a * w0 + b * w1 * w2;
+    Jl[0] = A00 * R00 + A01 * R10 + A02 * R20;
+    Jl[1] = A00 * R01 + A01 * R11 + A02 * R21;
+    Jl[2] = A00 * R02 + A01 * R12 + A02 * R22;
+    Jl[3] = A10 * R00 + A11 * R10 + A12 * R20;
+    Jl[4] = A10 * R01 + A11 * R11 + A12 * R21;
+    Jl[5] = A10 * R02 + A11 * R12 + A12 * R22;
+    // J_left = (1 - cc th2) I + b K + cc w w^T
+    const float jd = 1.f - cc * th2;
+    const float L00 = jd + cc * w0 * w0, L11 = jd + cc * w1 * w1, L22 = jd + cc * w2 * w2;
+    const float L01 = -b * w2 + cc * w0 * w1, L02 = b * w1 + cc * w0 * w2;
+    const float L10 = b * w2 + cc * w0 * w1, L12 = -b * w0 + cc * w1 * w2;
+    const float L20 = -b * w1 + cc * w0 * w2, L21 = b * w0 + cc * w1 * w2;
+    // B = A [RX]_x,  [RX]_x = [[0,-RX2,RX1],[RX2,0,-RX0],[-RX1,RX0,0]]
+    const float B00 = A01 * RX2 - A02 * RX1, B01 = -A00 * RX2 + A02 * RX0, B02 = A00 * RX1 - A01 * RX0;
+    const float B10 = A11 * RX2 - A12 * RX1, B11 = -A10 * RX2 + A12 * RX0, B12 = A10 * RX1 - A11 * RX0;
+    // d/dw = -B J_left
+    Jc[0] = -(B00 * L00 + B01 * L10 + B02 * L20);
+    Jc[1] = -(B00 * L01 + B01 * L11 + B02 * L21);
+    Jc[2] = -(B00 * L02 + B01 * L12 + B02 * L22);
+    Jc[9] = -(B10 * L00 + B11 * L10 + B12 * L20);
+    Jc[10] = -(B10 * L01 + B11 * L11 + B12 * L21);
+    Jc[11] = -(B10 * L02 + B11 * L12 + B12 * L22);
+    Jc[3] = A00; Jc[4] = A01; Jc[5] = A02;
+    Jc[12] = A10; Jc[13] = A11; Jc[14] = A12;
+    Jc[6] = dd * px; Jc[7] = f * n * px; Jc[8] = f * n * n * px;
+    Jc[15] = dd * py; Jc[16] = f * n * py; Jc[17] = f * n * n * py;
+    return P2;
+}
+
+__device__ __forceinline__ void load_cam(const float *__restrict__ cams, int cam, float *c) {
+#pragma unroll
+    for (int q = 0; q < 9; q++) c[q] = __ldg(cams + 9 * cam + q);
+}
+
+// ============================================================================ reductions
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+    for (int m = 16; m; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+    return v;
+}
+__device__ __forceinline__ float warp_sum_f(float v) {
+#pragma unroll
+    for (int m = 16; m; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+    return v;
+}
+template <int G>
+__device__ __forceinline__ float group_sum(float v) {
+#pragma unroll
+    for (int m = G / 2; m; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m, G);
+    return v;
+}
+// block-wide sum of NV floats; every thread gets the result.  scratch: >= 32*NV floats.
+template <int NV>
+__device__ __forceinline__ void block_sum(float *v, float *scratch) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int i = 0; i < NV; i++) v[i] = warp_sum_f(v[i]);
+    __syncthreads();
+    if (lane == 0)
+#pragma unroll
+        for (int i = 0; i < NV; i++) scratch[i * 32 + warp] = v[i];
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < NV; i++) {
+        float s = 0.f;
+        for (int w = 0; w < nw; w++) s += scratch[i * 32 + w];
+        v[i] = s;
+    }
+    __syncthreads();
+}
+__device__ __forceinline__ double block_sum_d(double v, double *scratch) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_sum_d(v);
+    __syncthreads();
+    if (lane == 0) scratch[warp] = v;
+    __syncthreads();
+    double s = 0.0;
+    for (int w = 0; w < nw; w++) s += scratch[w];
+    __syncthreads();
+    return s;
+}
+
+// ============================================================================ K0 / K1
+__global__ void k_check_depth(DevProblem d, int *bad) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= d.n_obs) return;
+    float c[9], r[2];
+    load_cam(d.cams, d.obs_cam[i], c);
+    const float *X = d.pts + 3 * (int64_t)d.obs_lm[i];
+    float2 uv = d.obs_uv[i];
+    float Pz = cam_model(c, X[0], X[1], X[2], uv.x, uv.y, r, nullptr, nullptr);
+    if (!(Pz < -1e-8f) || !isfinite(r[0]) || !isfinite(r[1])) atomicAdd(bad, 1);
+}
+
+// K1: residuals, E and camera column norms^2 (sum over the camera's observations).
+__global__ void __launch_bounds__(256) k_linearize(DevProblem d) {
+    __shared__ double red[32];
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double e = 0.0, bad = 0.0;
+    if (i < d.n_obs) {
+        float c[9], r[2], Jc[18], Jl[6];
+        const int cam = d.obs_cam[i];
+        load_cam(d.cams, cam, c);
+        const float *X = d.pts + 3 * (int64_t)d.obs_lm[i];
+        float2 uv = d.obs_uv[i];
+        float Pz = cam_model(c, X[0], X[1], X[2], uv.x, uv.y, r, Jc, Jl);
+        if (!(Pz < 0.f)) bad = 1.0;
+        e = (double)r[0] * r[0] + (double)r[1] * r[1];
+#pragma unroll
+        for (int q = 0; q < 9; q++) atomicAdd(d.cam_n2 + 9 * cam + q, Jc[q] * Jc[q] + Jc[9 + q] * Jc[9 + q]);
+    }
+    e = block_sum_d(e, red);
+    bad = block_sum_d(bad, red);
+    if (threadIdx.x == 0) {
+        atomicAdd(d.scal + SC_E, e);
+        if (bad > 0) atomicAdd(d.scal + SC_BAD, bad);
+    }
+}
+
+__global__ void k_cam_scale(DevProblem d, float dmin, float dmax) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 9 * d.n_p) return;
+    float n2 = d.cam_n2[i];
+    float s = 1.f / (1.f + sqrtf(n2));
+    d.sp[i] = s;
+    d.Dp2[i] = fminf(fmaxf(n2 * s * s, dmin), dmax);
+}
+
+// ============================================================================ damping rotations
+// 6 Givens rotations (pivot, target) = (0,d0),(1,d0),(2,d0),(1,d1),(2,d1),(2,d2) fold sqrt(lam) D_l
+// into R1 (Fig. 3b).  Reading C5: c = a/rho, s = b/rho, new_p = c p + s t,
+// new_t = -s p + c t; b == 0 -> identity.  In:  R (3x3 upper, row-major), rr[0..2] residual of
+// rows 0..2, sD[3] = sqrt(lam) D_l.  Out: L6 rows 0..2 = damped R1 (rows 3..5 end up exactly 0),
+// Gm (6x3) maps undamped rows 0..2 to the damped rows {0,1,2,d0,d1,d2} in the pose / residual
+// columns, rr6 the damped residual entries, g[12] the (c, s) pairs.
+__host__ __device__ constexpr int damp_p(int m) { return m == 0 ? 0 : ((m == 1 || m == 3) ? 1 : 2); }
+__host__ __device__ constexpr int damp_t(int m) { return m < 3 ? 3 : (m < 5 ? 4 : 5); }
+
+__device__ __forceinline__ void givens(float a, float b, float &c, float &s) {
+    if (b == 0.f) {
+        c = 1.f;
+        s = 0.f;
+    } else {
+        float r = hypotf(a, b);
+        c = a / r;
+        s = b / r;
+    }
+}
+
+__device__ __forceinline__ void damp_rotations(const float *R, const float *rr, const float *sD, float *L6, float *Gm,
+                                               float *rr6, float *g) {
+#pragma unroll
+    for (int i = 0; i < 18; i++) L6[i] = 0.f, Gm[i] = 0.f;
+#pragma unroll
+    for (int i = 0; i < 9; i++) L6[i] = R[i];
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+        L6[(3 + i) * 3 + i] = sD[i];
+        Gm[i * 3 + i] = 1.f;
+        rr6[i] = rr[i];
+        rr6[3 + i] = 0.f;
+    }
+#pragma unroll
+    for (int m = 0; m < 6; m++) {
+        const int p = damp_p(m), t = damp_t(m);
+        float c, s;
+        givens(L6[p * 3 + p], L6[t * 3 + p], c, s);
+        g[2 * m] = c;
+        g[2 * m + 1] = s;
+#pragma unroll
+        for (int q = 0; q < 3; q++) {
+            float a = L6[p * 3 + q], b = L6[t * 3 + q];
+            L6[p * 3 + q] = c * a + s * b;
+            L6[t * 3 + q] = -s * a + c * b;
+            a = Gm[p * 3 + q], b = Gm[t * 3 + q];
+            Gm[p * 3 + q] = c * a + s * b;
+            Gm[t * 3 + q] = -s * a + c * b;
+        }
+        float a = rr6[p], b = rr6[t];
+        rr6[p] = c * a + s * b;
+        rr6[t] = -s * a + c * b;
+        L6[t * 3 + p] = 0.f;
+    }
+}
+
+// ============================================================================ K2 emission
+// Tables (shared memory) describing one marginalized landmark block in compact-WY form:
+//   VR[row]  (float4) row of V (logical rows 3..2k-1) or effective V of the 6 damped rows
+//            (logical rows 0..2 and 2k..2k+2): out[row, c] = Jterm - VR[row] . MC[c]
+//   MC[c]    (float4) column c of M = T^T V^T J_p
+//   JP[a][q] scaled J_p rows (row a lives in camera block a >> 1)
+//   GM[s][m] damping mix of J_p rows 0..2 into special row s
+struct MargTables {
+    const float4 *VR;
+    const float4 *MC;
+    const float *JP;
+    const float *GM;
+};
+
+// value of logical row `row` (0..2k+2), camera block o, param q
+__device__ __forceinline__ float marg_elem(const MargTables &T, int k, int row, int o, int q) {
+    const float4 vr = T.VR[row];
+    const float4 mc = T.MC[9 * o + q];
+    float val = -(vr.x * mc.x + vr.y * mc.y + vr.z * mc.z);
+    if (row >= 3 && row < 2 * k) {
+        if (o == (row >> 1)) val += T.JP[row * 9 + q];
+    } else {
+        const int s = row < 3 ? row : row - 2 * k + 3;
+        if (o == 0)
+            val += T.GM[s * 3 + 0] * T.JP[q] + T.GM[s * 3 + 1] * T.JP[9 + q];
+        else if (o == 1)
+            val += T.GM[s * 3 + 2] * T.JP[18 + q];
+    }
+    return val;
+}
+
+// R2 elements [e_lo, e_hi) (float indices relative to the landmark's R2 region, multiples of 4),
+// written as float4 by `nl` cooperating lanes (lane id `li`).
+__device__ __forceinline__ void emit_r2(const MargTables &T, int k, float *__restrict__ r2, int64_t e_lo, int64_t e_hi,
+                                       int li, int nl) {
+    const int H = tile_h(k);
+    const int T_ = n_tiles(k);
+    const int64_t full = pad4((int64_t)9 * k * H);
+    for (int64_t e4 = e_lo + 4 * li; e4 < e_hi; e4 += 4 * nl) {
+        float4 out;
+        float *ov = &out.x;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int64_t e = e4 + u;
+            int t = (int)(e / full);
+            if (t >= T_) t = T_ - 1;
+            const int h = tile_rows(k, t);
+            const int within = (int)(e - (int64_t)t * full);
+            float val = 0.f;
+            if (within < 9 * k * h) {
+                const int o = within / (9 * h);
+                const int rem = within - o * 9 * h;
+                const int a = (rem * 7282) >> 16;  // rem / 9 for rem < 36000
+                const int q = rem - 9 * a;
+                val = marg_elem(T, k, 3 + t * H + a, o, q);
+            }
+            ov[u] = val;
+        }
+        *reinterpret_cast<float4 *>(r2 + e4) = out;
+    }
+}
+
+// R1 = logical rows 0..2 (3 x 9k, row-major, padded to 4)
+__device__ __forceinline__ void emit_r1(const MargTables &T, int k, float *__restrict__ r1, int li, int nl) {
+    const int n = 27 * k;
+    const int n4 = (int)pad4(n);
+    for (int e4 = 4 * li; e4 < n4; e4 += 4 * nl) {
+        float4 out;
+        float *ov = &out.x;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int e = e4 + u;
+            float val = 0.f;
+            if (e < n) {
+                const int m = e / (9 * k);
+                const int c = e - m * 9 * k;
+                const int o = c / 9;
+                val = marg_elem(T, k, m, o, c - 9 * o);
+            }
+            ov[u] = val;
+        }
+        *reinterpret_cast<float4 *>(r1 + e4) = out;
+    }
+}
+
+// ============================================================================ K2 small (k <= 32)
+template <int G>
+struct SmallTab {
+    static constexpr int VR = 4 * (2 * G + 3);
+    static constexpr int MC = 4 * 9 * G;
+    static constexpr int JP = 9 * 2 * G;
+    static constexpr int GM = 20;
+    static constexpr int FLOATS = VR + MC + JP + GM;
+};
+
+template <int G>
+__global__ void __launch_bounds__(128) k_marg_small(DevProblem d, int64_t lm_lo, int64_t lm_hi, float lam, float dmin,
+                                                    float dmax) {
+    constexpr int NG = 32 / G;
+    using TB = SmallTab<G>;
+    extern __shared__ float4 smem4[];
+    float *smem = reinterpret_cast<float *>(smem4);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int grp = lane / G, gl = lane % G;
+    const int64_t j = lm_lo + ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * NG + grp;
+    const bool valid = j < lm_hi;
+    const int k = valid ? d.lm_k[j] : 0;
+    const bool act = gl < k;
+    float *tab = smem + (warp * NG + grp) * TB::FLOATS;
+    float4 *VR = reinterpret_cast<float4 *>(tab);
+    float4 *MC = reinterpret_cast<float4 *>(tab + TB::VR);
+    float *JP = tab + TB::VR + TB::MC;
+    float *GM = JP + TB::JP;
+
+    // ---- per-observation Jacobians (lane gl <-> observation gl; rows 2gl, 2gl+1)
+    float r[2] = {0.f, 0.f}, Jc[18], Jl[6];
+#pragma unroll
+    for (int i = 0; i < 18; i++) Jc[i] = 0.f;
+#pragma unroll
+    for (int i = 0; i < 6; i++) Jl[i] = 0.f;
+    int cam = 0;
+    if (act) {
+        const int64_t o = d.lm_obs0[j] + gl;
+        cam = d.obs_cam[o];
+        float c[9];
+        load_cam(d.cams, cam, c);
+        const float *X = d.pts + 3 * j;
+        const float2 uv = d.obs_uv[o];
+        cam_model(c, X[0], X[1], X[2], uv.x, uv.y, r, Jc, Jl);
+    }
+    // ---- landmark column scaling (C7, C8) over the landmark's own observations
+    float sl[3], Dl[3];
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+        float n2 = group_sum<G>(Jl[q] * Jl[q] + Jl[3 + q] * Jl[3 + q]);
+        sl[q] = 1.f / (1.f + sqrtf(n2));
+        Dl[q] = sqrtf(fminf(fmaxf(n2 * sl[q] * sl[q], dmin), dmax));
+    }
+    float Jp[2][9], X[2][3], rv[2] = {r[0], r[1]};
+#pragma unroll
+    for (int q = 0; q < 9; q++) {
+        const float s = act ? d.sp[9 * cam + q] : 0.f;
+        Jp[0][q] = Jc[q] * s;
+        Jp[1][q] = Jc[9 + q] * s;
+    }
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+        X[0][q] = Jl[q] * sl[q];
+        X[1][q] = Jl[3 + q] * sl[q];
+    }
+    // ---- Householder QR of the 2k x 3 landmark Jacobian, reading C4 for the sign
+    float V[2][3], tau[3];
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+        for (int rr = 0; rr < 2; rr++) {
+            const int a = 2 * gl + rr;
+            const float x = (act && a >= c) ? X[rr][c] : 0.f;
+            s0 += x * x;
+            s1 += (c + 1 < 3) ? x * X[rr][(c + 1) % 3] : 0.f;
+            s2 += (c + 2 < 3) ? x * X[rr][(c + 2) % 3] : 0.f;
+            s3 += x * rv[rr];
+        }
+        s0 = group_sum<G>(s0);
+        s1 = group_sum<G>(s1);
+        s2 = group_sum<G>(s2);
+        s3 = group_sum<G>(s3);
+        const int pl = c >> 1, pr = c & 1;  // pivot row c lives in lane c>>1, local row c&1
+        const float x0 = __shfl_sync(0xffffffffu, X[pr][c], pl, G);
+        const float y1 = __shfl_sync(0xffffffffu, X[pr][(c + 1) % 3], pl, G);
+        const float y2 = __shfl_sync(0xffffffffu, X[pr][(c + 2) % 3], pl, G);
+        const float yr = __shfl_sync(0xffffffffu, rv[pr], pl, G);
+        const float sig = sqrtf(s0);
+        const float alpha = x0 >= 0.f ? -sig : sig;
+        const float vtv = 2.f * sig * (sig + fabsf(x0));
+        const float tc = vtv > 0.f ? 2.f / vtv : 0.f;
+        tau[c] = tc;
+        const float d1 = s1 - alpha * y1, d2 = s2 - alpha * y2, dr = s3 - alpha * yr;
+#pragma unroll
+        for (int rr = 0; rr < 2; rr++) {
+            const int a = 2 * gl + rr;
+            float vv = 0.f;
+            if (act && a >= c) vv = (a == c) ? x0 - alpha : X[rr][c];
+            V[rr][c] = vv;
+            if (c + 1 < 3) X[rr][(c + 1) % 3] -= tc * vv * d1;
+            if (c + 2 < 3) X[rr][(c + 2) % 3] -= tc * vv * d2;
+            rv[rr] -= tc * vv * dr;
+            if (a == c) X[rr][c] = alpha;
+            else if (a > c) X[rr][c] = 0.f;
+        }
+    }
+    // ---- compact WY: T upper 3x3 (Q = I - V T V^T, Q^T = I - V T^T V^T)
+    float p01 = 0.f, p02 = 0.f, p12 = 0.f;
+#pragma unroll
+    for (int rr = 0; rr < 2; rr++) {
+        p01 += V[rr][0] * V[rr][1];
+        p02 += V[rr][0] * V[rr][2];
+        p12 += V[rr][1] * V[rr][2];
+    }
+    p01 = group_sum<G>(p01);
+    p02 = group_sum<G>(p02);
+    p12 = group_sum<G>(p12);
+    const float T00 = tau[0], T11 = tau[1], T22 = tau[2];
+    const float T01 = -tau[1] * T00 * p01;
+    const float T02 = -tau[2] * (T00 * p02 + T01 * p12);
+    const float T12 = -tau[2] * T11 * p12;
+    // ---- M = T^T V^T J_p for this lane's camera block (o = gl)
+    if (act) {
+#pragma unroll
+        for (int q = 0; q < 9; q++) {
+            const float W0 = V[0][0] * Jp[0][q] + V[1][0] * Jp[1][q];
+            const float W1 = V[0][1] * Jp[0][q] + V[1][1] * Jp[1][q];
+            const float W2 = V[0][2] * Jp[0][q] + V[1][2] * Jp[1][q];
+            MC[9 * gl + q] = make_float4(T00 * W0, T01 * W0 + T11 * W1, T02 * W0 + T12 * W1 + T22 * W2, 0.f);
+            JP[(2 * gl) * 9 + q] = Jp[0][q];
+            JP[(2 * gl + 1) * 9 + q] = Jp[1][q];
+        }
+#pragma unroll
+        for (int rr = 0; rr < 2; rr++) {
+            const int a = 2 * gl + rr;
+            if (a >= 3) VR[a] = make_float4(V[rr][0], V[rr][1], V[rr][2], 0.f);
+        }
+    }
+    // ---- damping (fused): R1 rows 0..2 and V rows 0..2 from lanes 0, 1
+    float R[9], rr3[3], V3[9];
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+        R[q] = __shfl_sync(0xffffffffu, X[0][q], 0, G);
+        R[3 + q] = __shfl_sync(0xffffffffu, X[1][q], 0, G);
+        R[6 + q] = __shfl_sync(0xffffffffu, X[0][q], 1, G);
+        V3[q] = __shfl_sync(0xffffffffu, V[0][q], 0, G);
+        V3[3 + q] = __shfl_sync(0xffffffffu, V[1][q], 0, G);
+        V3[6 + q] = __shfl_sync(0xffffffffu, V[0][q], 1, G);
+    }
+    rr3[0] = __shfl_sync(0xffffffffu, rv[0], 0, G);
+    rr3[1] = __shfl_sync(0xffffffffu, rv[1], 0, G);
+    rr3[2] = __shfl_sync(0xffffffffu, rv[0], 1, G);
+    const float sq = sqrtf(lam);
+    const float sD[3] = {sq * Dl[0], sq * Dl[1], sq * Dl[2]};
+    float L6[18], Gm[18], rr6[6], g[12];
+    damp_rotations(R, rr3, sD, L6, Gm, rr6, g);
+    if (valid && gl == 0) {
+#pragma unroll
+        for (int s = 0; s < 6; s++) {
+            float4 ve;
+            ve.x = Gm[s * 3] * V3[0] + Gm[s * 3 + 1] * V3[3] + Gm[s * 3 + 2] * V3[6];
+            ve.y = Gm[s * 3] * V3[1] + Gm[s * 3 + 1] * V3[4] + Gm[s * 3 + 2] * V3[7];
+            ve.z = Gm[s * 3] * V3[2] + Gm[s * 3 + 1] * V3[5] + Gm[s * 3 + 2] * V3[8];
+            ve.w = 0.f;
+            VR[s < 3 ? s : 2 * k + s - 3] = ve;
+        }
+#pragma unroll
+        for (int i = 0; i < 18; i++) GM[i] = Gm[i];
+    }
+    __syncwarp();
+    if (!valid) return;
+    // ---- emission (write-only stream, Fig. 2c)
+    MargTables Tb{VR, MC, JP, GM};
+    float *blk_side = d.arena + d.lm_side[j];
+    emit_r2(Tb, k, d.arena + d.lm_r2[j], 0, r2_floats(k), gl, G);
+    emit_r1(Tb, k, blk_side, gl, G);
+    float4 *TL = reinterpret_cast<float4 *>(blk_side + side_tl(k));
+    if (act) {
+#pragma unroll
+        for (int rr = 0; rr < 2; rr++) {
+            const int a = 2 * gl + rr;
+            if (a >= 3) TL[a] = make_float4(0.f, 0.f, 0.f, rv[rr]);
+        }
+    }
+    if (gl == 0) {
+#pragma unroll
+        for (int s = 0; s < 3; s++) {
+            TL[s] = make_float4(L6[s * 3], L6[s * 3 + 1], L6[s * 3 + 2], rr6[s]);
+            TL[2 * k + s] = make_float4(0.f, 0.f, 0.f, rr6[3 + s]);
+        }
+        float *gp = blk_side + side_g(k);
+#pragma unroll
+        for (int i = 0; i < 12; i++) gp[i] = g[i];
+#pragma unroll
+        for (int q = 0; q < 3; q++) {
+            d.lm_s[3 * j + q] = sl[q];
+            d.lm_D[3 * j + q] = Dl[q];
+        }
+    }
+}
+
+// ============================================================================ K2 large (k > 32)
+// One CTA per (landmark, tile range).  The O(k) prologue (Jacobians, Householder, WY tables) is
+// recomputed by every CTA of a landmark; the O(k^2) emission is split across CTAs.
+__global__ void __launch_bounds__(256) k_marg_large(DevProblem d, const LargeItem *__restrict__ items, float lam,
+                                                    float dmin, float dmax) {
+    extern __shared__ float4 smem4[];
+    float *smem = reinterpret_cast<float *>(smem4);
+    __shared__ float red[32 * 4];
+    __shared__ float piv[4];
+    const LargeItem it = items[blockIdx.x];
+    const int64_t j = it.lm;
+    const int k = d.lm_k[j];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    float4 *VR = reinterpret_cast<float4 *>(smem);                 // 2k+3
+    float4 *MC = VR + (2 * k + 3);                                  // 9k
+    float *JP = reinterpret_cast<float *>(MC + 9 * k);              // 18k
+    float *SX = JP + 18 * k;                                        // 2k x 3 (landmark Jacobian)
+    float *SR = SX + 6 * k;                                         // 2k residuals
+    float *GM = SR + 2 * k;                                         // 18 (+2 pad)
+    const int64_t obs0 = d.lm_obs0[j];
+    const float *Xp = d.pts + 3 * j;
+    const float P0 = Xp[0], P1 = Xp[1], P2 = Xp[2];
+    float n2[3] = {0.f, 0.f, 0.f};
+    for (int i = tid; i < k; i += nt) {
+        const int cam = d.obs_cam[obs0 + i];
+        float c[9], r[2], Jc[18], Jl[6];
+        load_cam(d.cams, cam, c);
+        const float2 uv = d.obs_uv[obs0 + i];
+        cam_model(c, P0, P1, P2, uv.x, uv.y, r, Jc, Jl);
+#pragma unroll
+        for (int q = 0; q < 9; q++) {
+            const float s = d.sp[9 * cam + q];
+            JP[(2 * i) * 9 + q] = Jc[q] * s;
+            JP[(2 * i + 1) * 9 + q] = Jc[9 + q] * s;
+        }
+#pragma unroll
+        for (int q = 0; q < 3; q++) {
+            SX[(2 * i) * 3 + q] = Jl[q];
+            SX[(2 * i + 1) * 3 + q] = Jl[3 + q];
+            n2[q] += Jl[q] * Jl[q] + Jl[3 + q] * Jl[3 + q];
+        }
+        SR[2 * i] = r[0];
+        SR[2 * i + 1] = r[1];
+    }
+    block_sum<3>(n2, red);
+    float sl[3], Dl[3];
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+        sl[q] = 1.f / (1.f + sqrtf(n2[q]));
+        Dl[q] = sqrtf(fminf(fmaxf(n2[q] * sl[q] * sl[q], dmin), dmax));
+    }
+    for (int a = tid; a < 2 * k; a += nt)
+#pragma unroll
+        for (int q = 0; q < 3; q++) SX[a * 3 + q] *= sl[q];
+    __syncthreads();
+    // Householder, 3 reflectors; V kept in VR rows (all rows 0..2k-1 during the prologue)
+    float tau[3];
+    for (int c = 0; c < 3; c++) {
+        float s[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int a = c + tid; a < 2 * k; a += nt) {
+            const float x = SX[a * 3 + c];
+            s[0] += x * x;
+            if (c + 1 < 3) s[1] += x * SX[a * 3 + c + 1];
+            if (c + 2 < 3) s[2] += x * SX[a * 3 + c + 2];
+            s[3] += x * SR[a];
+        }
+        if (tid == 0) {
+            piv[0] = SX[c * 3 + c];
+            piv[1] = (c + 1 < 3) ? SX[c * 3 + c + 1] : 0.f;
+            piv[2] = (c + 2 < 3) ? SX[c * 3 + c + 2] : 0.f;
+            piv[3] = SR[c];
+        }
+        block_sum<4>(s, red);  // contains __syncthreads
+        const float x0 = piv[0], y1 = piv[1], y2 = piv[2], yr = piv[3];
+        const float sig = sqrtf(s[0]);
+        const float alpha = x0 >= 0.f ? -sig : sig;
+        const float vtv = 2.f * sig * (sig + fabsf(x0));
+        const float tc = vtv > 0.f ? 2.f / vtv : 0.f;
+        tau[c] = tc;
+        const float d1 = s[1] - alpha * y1, d2 = s[2] - alpha * y2, dr = s[3] - alpha * yr;
+        for (int a = tid; a < 2 * k; a += nt) {
+            float vv = 0.f;
+            if (a >= c) vv = (a == c) ? x0 - alpha : SX[a * 3 + c];
+            float *vr = reinterpret_cast<float *>(VR + a);
+            vr[c] = vv;
+            if (c == 0) vr[3] = 0.f;
+            if (c + 1 < 3) SX[a * 3 + c + 1] -= tc * vv * d1;
+            if (c + 2 < 3) SX[a * 3 + c + 2] -= tc * vv * d2;
+            SR[a] -= tc * vv * dr;
+            if (a == c) SX[a * 3 + c] = alpha;
+            else if (a > c) SX[a * 3 + c] = 0.f;
+        }
+        __syncthreads();
+    }
+    float p[3] = {0.f, 0.f, 0.f};
+    for (int a = tid; a < 2 * k; a += nt) {
+        const float4 v = VR[a];
+        p[0] += v.x * v.y;
+        p[1] += v.x * v.z;
+        p[2] += v.y * v.z;
+    }
+    block_sum<3>(p, red);
+    const float T00 = tau[0], T11 = tau[1], T22 = tau[2];
+    const float T01 = -tau[1] * T00 * p[0];
+    const float T02 = -tau[2] * (T00 * p[1] + T01 * p[2]);
+    const float T12 = -tau[2] * T11 * p[2];
+    for (int o = tid; o < k; o += nt) {
+        const float4 v0 = VR[2 * o], v1 = VR[2 * o + 1];
+#pragma unroll
+        for (int q = 0; q < 9; q++) {
+            const float j0 = JP[(2 * o) * 9 + q], j1 = JP[(2 * o + 1) * 9 + q];
+            const float W0 = v0.x * j0 + v1.x * j1, W1 = v0.y * j0 + v1.y * j1, W2 = v0.z * j0 + v1.z * j1;
+            MC[9 * o + q] = make_float4(T00 * W0, T01 * W0 + T11 * W1, T02 * W0 + T12 * W1 + T22 * W2, 0.f);
+        }
+    }
+    // damping (every thread computes the 6 rotations redundantly from smem values)
+    float R[9], rr3[3], V3[9];
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+#pragma unroll
+        for (int q = 0; q < 3; q++) R[i * 3 + q] = SX[i * 3 + q];
+        rr3[i] = SR[i];
+        const float4 v = VR[i];
+        V3[i * 3] = v.x, V3[i * 3 + 1] = v.y, V3[i * 3 + 2] = v.z;
+    }
+    const float sq = sqrtf(lam);
+    const float sD[3] = {sq * Dl[0], sq * Dl[1], sq * Dl[2]};
+    float L6[18], Gm[18], rr6[6], g[12];
+    damp_rotations(R, rr3, sD, L6, Gm, rr6, g);
+    __syncthreads();  // all reads of VR rows 0..2 done
+    if (tid < 6) {
+        const int s = tid;
+        float4 ve;
+        ve.x = Gm[s * 3] * V3[0] + Gm[s * 3 + 1] * V3[3] + Gm[s * 3 + 2] * V3[6];
+        ve.y = Gm[s * 3] * V3[1] + Gm[s * 3 + 1] * V3[4] + Gm[s * 3 + 2] * V3[7];
+        ve.z = Gm[s * 3] * V3[2] + Gm[s * 3 + 1] * V3[5] + Gm[s * 3 + 2] * V3[8];
+        ve.w = 0.f;
+        VR[s < 3 ? s : 2 * k + s - 3] = ve;
+    }
+    if (tid < 18) GM[tid] = Gm[tid];
+    __syncthreads();
+    MargTables Tb{VR, MC, JP, GM};
+    const int T_ = n_tiles(k);
+    const int64_t e_lo = tile_off(k, it.t0);
+    const int64_t e_hi = it.t1 >= T_ ? r2_floats(k) : tile_off(k, it.t1);
+    emit_r2(Tb, k, d.arena + d.lm_r2[j], e_lo, e_hi, tid, nt);
+    if (it.t0 == 0) {
+        float *side = d.arena + d.lm_side[j];
+        emit_r1(Tb, k, side, tid, nt);
+        float4 *TL = reinterpret_cast<float4 *>(side + side_tl(k));
+        for (int a = 3 + tid; a < 2 * k; a += nt) TL[a] = make_float4(0.f, 0.f, 0.f, SR[a]);
+        if (tid < 3) {
+            const int s = tid;
+            TL[s] = make_float4(L6[s * 3], L6[s * 3 + 1], L6[s * 3 + 2], rr6[s]);
+            TL[2 * k + s] = make_float4(0.f, 0.f, 0.f, rr6[3 + s]);
+            d.lm_s[3 * j + s] = sl[s];
+            d.lm_D[3 * j + s] = Dl[s];
+        }
+        if (tid < 12) side[side_g(k) + tid] = g[tid];
+    }
+}
+
+// ============================================================================ K3 re-damping
+// Warp per landmark.  Undo the stored rotations (transposed, reverse order, Fig. 3c), drop the
+// damping rows, and fold sqrt(lam) D_l in again with freshly computed rotations.
+__global__ void __launch_bounds__(256) k_redamp(DevProblem d, float lam) {
+    const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (j >= d.n_l) return;
+    const int k = d.lm_k[j];
+    float *side = d.arena + d.lm_side[j];
+    float *r2 = d.arena + d.lm_r2[j];
+    float4 *TL = reinterpret_cast<float4 *>(side + side_tl(k));
+    float *gp = side + side_g(k);
+    float g[12];
+#pragma unroll
+    for (int i = 0; i < 12; i++) g[i] = gp[i];
+    // landmark + residual columns of the 6 special rows
+    float M6[6][4];
+#pragma unroll
+    for (int s = 0; s < 6; s++) {
+        const float4 t = TL[s < 3 ? s : 2 * k + s - 3];
+        M6[s][0] = t.x, M6[s][1] = t.y, M6[s][2] = t.z, M6[s][3] = t.w;
+    }
+#pragma unroll
+    for (int m = 5; m >= 0; m--) {
+        const int p = damp_p(m), t = damp_t(m);
+        const float c = g[2 * m], s = g[2 * m + 1];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const float a = M6[p][q], b = M6[t][q];
+            M6[p][q] = c * a - s * b;
+            M6[t][q] = s * a + c * b;
+        }
+    }
+    float R[9], rr3[3];
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+        R[i * 3] = M6[i][0], R[i * 3 + 1] = M6[i][1], R[i * 3 + 2] = M6[i][2];
+        rr3[i] = M6[i][3];
+    }
+    // exact upper-triangular R1 after undo
+    R[3] = 0.f, R[6] = 0.f, R[7] = 0.f;
+    const float sq = sqrtf(lam);
+    const float sD[3] = {sq * d.lm_D[3 * j], sq * d.lm_D[3 * j + 1], sq * d.lm_D[3 * j + 2]};
+    float L6[18], Gm[18], rr6[6], gn[12];
+    damp_rotations(R, rr3, sD, L6, Gm, rr6, gn);
+    // pose columns: 3 rows of R1 (side) + last 3 rows of R2
+    const int W = 9 * k;
+    for (int c = lane; c < W; c += 32) {
+        const int o = c / 9, q = c - 9 * o;
+        float x[6];
+        int64_t idx[3];
+#pragma unroll
+        for (int s = 0; s < 3; s++) {
+            x[s] = side[s * W + c];
+            idx[s] = r2_index(k, 2 * k - 3 + s, o, q);
+            x[3 + s] = r2[idx[s]];
+        }
+#pragma unroll
+        for (int m = 5; m >= 0; m--) {
+            const int p = damp_p(m), t = damp_t(m);
+            const float cc = g[2 * m], ss = g[2 * m + 1];
+            const float a = x[p], b = x[t];
+            x[p] = cc * a - ss * b;
+            x[t] = ss * a + cc * b;
+        }
+#pragma unroll
+        for (int s = 0; s < 6; s++) {
+            const float v = Gm[s * 3] * x[0] + Gm[s * 3 + 1] * x[1] + Gm[s * 3 + 2] * x[2];
+            if (s < 3) side[s * W + c] = v;
+            else r2[idx[s - 3]] = v;
+        }
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < 3; s++) {
+            TL[s] = make_float4(L6[s * 3], L6[s * 3 + 1], L6[s * 3 + 2], rr6[s]);
+            TL[2 * k + s] = make_float4(0.f, 0.f, 0.f, rr6[3 + s]);
+        }
+#pragma unroll
+        for (int i = 0; i < 12; i++) gp[i] = gn[i];
+    }
+}
+
+// ============================================================================ K4 preconditioner + rhs
+// Thread per (landmark, camera block o): P_o = sum_a A[a,o,:]^T A[a,o,:] (45 upper entries) and
+// b_o = sum_a A[a,o,:] q_a, accumulated into the camera's 54-float slot.
+__global__ void __launch_bounds__(256) k_precond_rhs(DevProblem d) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= d.n_obs) return;
+    const int64_t j = d.obs_lm[g];
+    const int k = d.lm_k[j];
+    const int o = (int)(g - d.lm_obs0[j]);
+    const int cam = d.obs_cam[g];
+    const float *r2 = d.arena + d.lm_r2[j];
+    const float4 *TL = reinterpret_cast<const float4 *>(d.arena + d.lm_side[j] + side_tl(k));
+    float P[45], b[9];
+#pragma unroll
+    for (int i = 0; i < 45; i++) P[i] = 0.f;
+#pragma unroll
+    for (int i = 0; i < 9; i++) b[i] = 0.f;
+    for (int a = 0; a < 2 * k; a++) {
+        const float *row = r2 + r2_index(k, a, o, 0);
+        float v[9];
+#pragma unroll
+        for (int q = 0; q < 9; q++) v[q] = row[q];
+        const float qa = TL[a + 3].w;
+        int idx = 0;
+#pragma unroll
+        for (int q1 = 0; q1 < 9; q1++) {
+            b[q1] += v[q1] * qa;
+#pragma unroll
+            for (int q2 = q1; q2 < 9; q2++) P[idx++] += v[q1] * v[q2];
+        }
+    }
+    float *acc = d.pacc + 54 * (int64_t)cam;
+#pragma unroll
+    for (int i = 0; i < 45; i++) atomicAdd(acc + i, P[i]);
+#pragma unroll
+    for (int i = 0; i < 9; i++) atomicAdd(acc + 45 + i, b[i]);
+}
+
+// per camera: P_i + lambda D_p^2 -> Cholesky (FP64) -> inverse M^-1 (FP32, 81); b~ copied out.
+__global__ void k_precond_finalize(DevProblem d, float lam, double *bad) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= d.n_p) return;
+    const float *acc = d.pacc + 54 * i;
+    double P[81];
+    int idx = 0;
+    for (int a = 0; a < 9; a++)
+        for (int b = a; b < 9; b++) {
+            P[a * 9 + b] = acc[idx];
+            P[b * 9 + a] = acc[idx];
+            idx++;
+        }
+    for (int a = 0; a < 9; a++) {
+        P[a * 9 + a] += (double)lam * d.Dp2[9 * i + a];
+        d.bt[9 * i + a] = acc[45 + a];
+    }
+    double L[81];
+    for (int a = 0; a < 81; a++) L[a] = 0.0;
+    bool ok = true;
+    for (int a = 0; a < 9; a++)
+        for (int b = 0; b <= a; b++) {
+            double s = P[a * 9 + b];
+            for (int m = 0; m < b; m++) s -= L[a * 9 + m] * L[b * 9 + m];
+            if (a == b) {
+                if (!(s > 0.0)) ok = false, s = 1.0;
+                L[a * 9 + a] = sqrt(s);
+            } else {
+                L[a * 9 + b] = s / L[b * 9 + b];
+            }
+        }
+    if (!ok) atomicAdd(bad, 1.0);
+    // inverse: solve L L^T X = I column by column
+    for (int col = 0; col < 9; col++) {
+        double y[9], x[9];
+        for (int a = 0; a < 9; a++) {
+            double s = (a == col) ? 1.0 : 0.0;
+            for (int m = 0; m < a; m++) s -= L[a * 9 + m] * y[m];
+            y[a] = s / L[a * 9 + a];
+        }
+        for (int a = 8; a >= 0; a--) {
+            double s = y[a];
+            for (int m = a + 1; m < 9; m++) s -= L[m * 9 + a] * x[m];
+            x[a] = s / L[a * 9 + a];
+        }
+        for (int a = 0; a < 9; a++) d.Minv[81 * i + a * 9 + col] = (float)x[a];
+    }
+}
+
+// ============================================================================ K5 matvec
+// small (k <= 32): warp-group of G lanes per landmark.  Pass 1 streams A_j once from HBM with
+// coalesced float4 loads (y = A_j v_j, row runs accumulated in registers then in shared memory);
+// pass 2 re-reads A_j (L1-resident) column-wise: out_c = A_j[:,c]^T y.
+template <int G>
+__global__ void __launch_bounds__(128) k_matvec_small(DevProblem d, int64_t lm_lo, int64_t lm_hi,
+                                                      const float *__restrict__ v, float *__restrict__ out,
+                                                      const PcgState *__restrict__ st) {
+    if (st && st->done) return;
+    constexpr int NG = 32 / G;
+    __shared__ float sv[4][NG][9 * G];
+    __shared__ float sy[4][NG][2 * G];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int grp = lane / G, gl = lane % G;
+    const int64_t j = lm_lo + ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * NG + grp;
+    const bool valid = j < lm_hi;
+    const int k = valid ? d.lm_k[j] : 0;
+    float *vl = sv[warp][grp];
+    float *y = sy[warp][grp];
+    int cam = 0;
+    if (gl < k) {
+        cam = d.obs_cam[d.lm_obs0[j] + gl];
+#pragma unroll
+        for (int q = 0; q < 9; q++) vl[9 * gl + q] = v[9 * cam + q];
+        y[2 * gl] = 0.f;
+        y[2 * gl + 1] = 0.f;
+    }
+    __syncwarp();
+    const float *A = valid ? d.arena + d.lm_r2[j] : d.arena;
+    const int n = 18 * k * k;
+    const int W = 18 * k;  // floats per camera block (2k rows x 9)
+    if (valid) {
+        const float invW = 1.f / (float)W;
+        for (int e4 = 4 * gl; e4 < n; e4 += 4 * G) {
+            const float4 a4 = __ldg(reinterpret_cast<const float4 *>(A + e4));
+            const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+            int o = __float2int_rd(((float)e4 + 0.5f) * invW);
+            int rem = e4 - o * W;
+            int row = (rem * 7282) >> 16;
+            int q = rem - 9 * row;
+            float run = 0.f;
+            int run_row = row;
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                if (e4 + u < n) {
+                    if (row != run_row) {
+                        atomicAdd(y + run_row, run);
+                        run = 0.f;
+                        run_row = row;
+                    }
+                    run += av[u] * vl[9 * o + q];
+                }
+                if (++q == 9) {
+                    q = 0;
+                    if (++row == 2 * k) row = 0, ++o;
+                }
+            }
+            atomicAdd(y + run_row, run);
+        }
+    }
+    __syncwarp();
+    if (valid) {
+        for (int c = gl; c < 9 * k; c += G) {
+            const int o = c / 9, q = c - 9 * o;
+            const float *col = A + o * W + q;
+            float acc = 0.f;
+            for (int a = 0; a < 2 * k; a++) acc += col[9 * a] * y[a];
+            atomicAdd(out + 9 * d.obs_cam[d.lm_obs0[j] + o] + q, acc);
+        }
+    }
+}
+
+// large (k > 32): CTA per (landmark, tile range); per tile y (<= 4 rows) by a block reduction,
+// then out_c accumulated in registers across the CTA's tiles and flushed once.
+constexpr int MV_MAXC = (9 * KMAX + 255) / 256;
+__global__ void __launch_bounds__(256) k_matvec_large(DevProblem d, const LargeItem *__restrict__ items,
+                                                      const float *__restrict__ v, float *__restrict__ out,
+                                                      const PcgState *__restrict__ st) {
+    if (st && st->done) return;
+    extern __shared__ float4 smem4[];
+    float *vl = reinterpret_cast<float *>(smem4);
+    __shared__ float red[32 * 4];
+    const LargeItem it = items[blockIdx.x];
+    const int64_t j = it.lm;
+    const int k = d.lm_k[j];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int64_t obs0 = d.lm_obs0[j];
+    for (int c = tid; c < 9 * k; c += nt) {
+        const int o = c / 9;
+        vl[c] = v[9 * d.obs_cam[obs0 + o] + (c - 9 * o)];
+    }
+    __syncthreads();
+    float acc[MV_MAXC];
+#pragma unroll
+    for (int i = 0; i < MV_MAXC; i++) acc[i] = 0.f;
+    const float *A = d.arena + d.lm_r2[j];
+    for (int t = it.t0; t < it.t1; t++) {
+        const int h = tile_rows(k, t);
+        const float *At = A + tile_off(k, t);
+        const int n = 9 * k * h;
+        float yp[4] = {0.f, 0.f, 0.f, 0.f};
+        const int bw = 9 * h;
+        for (int e4 = 4 * tid; e4 < n; e4 += 4 * nt) {
+            const float4 a4 = __ldg(reinterpret_cast<const float4 *>(At + e4));
+            const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int e = e4 + u;
+                if (e < n) {
+                    const int o = e / bw;
+                    const int rem = e - o * bw;
+                    const int row = (rem * 7282) >> 16;
+                    const int q = rem - 9 * row;
+                    const float pr = av[u] * vl[9 * o + q];
+                    yp[0] += row == 0 ? pr : 0.f;
+                    yp[1] += row == 1 ? pr : 0.f;
+                    yp[2] += row == 2 ? pr : 0.f;
+                    yp[3] += row == 3 ? pr : 0.f;
+                }
+            }
+        }
+        block_sum<4>(yp, red);
+#pragma unroll
+        for (int i = 0; i < MV_MAXC; i++) {
+            const int c = tid + i * nt;
+            if (c < 9 * k) {
+                const int o = c / 9, q = c - 9 * o;
+                const float *col = At + o * bw + q;
+                float s = 0.f;
+                for (int a = 0; a < h; a++) s += col[9 * a] * yp[a];
+                acc[i] += s;
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < MV_MAXC; i++) {
+        const int c = tid + i * nt;
+        if (c < 9 * k) {
+            const int o = c / 9;
+            atomicAdd(out + 9 * d.obs_cam[obs0 + o] + (c - 9 * o), acc[i]);
+        }
+    }
+}
+
+__global__ void k_add_damping(DevProblem d, const float *v, float *out, float lam) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < 9 * d.n_p) out[i] += lam * d.Dp2[i] * v[i];
+}
+
+// ============================================================================ K6 PCG (single CTA)
+// Reading C11: stop when |rho| <= tol |rho_0| or it == max; p^T w <= 0 -> indefinite.
+__device__ __forceinline__ void precond_apply(const DevProblem &d, const float *in, float *outv, int64_t N) {
+    for (int64_t i = threadIdx.x; i < N; i += blockDim.x) {
+        const int64_t cam = i / 9;
+        const int a = (int)(i - 9 * cam);
+        const float *M = d.Minv + 81 * cam + 9 * a;
+        const float *x = in + 9 * cam;
+        float s = 0.f;
+#pragma unroll
+        for (int b = 0; b < 9; b++) s += M[b] * x[b];
+        outv[i] = s;
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_pcg_init(DevProblem d) {
+    __shared__ double red[32];
+    const int64_t N = 9 * d.n_p;
+    double rr = 0.0;
+    for (int64_t i = threadIdx.x; i < N; i += blockDim.x) {
+        const float r = -d.bt[i];
+        d.r[i] = r;
+        d.x[i] = 0.f;
+        rr += (double)r * r;
+    }
+    __syncthreads();
+    precond_apply(d, d.r, d.z, N);
+    __syncthreads();
+    double rz = 0.0;
+    for (int64_t i = threadIdx.x; i < N; i += blockDim.x) {
+        d.p[i] = d.z[i];
+        rz += (double)d.r[i] * d.z[i];
+    }
+    rr = block_sum_d(rr, red);
+    rz = block_sum_d(rz, red);
+    if (threadIdx.x == 0) {
+        d.pcg->rz = rz;
+        d.pcg->r0 = sqrt(rr);
+        d.pcg->rn = sqrt(rr);
+        d.pcg->it = 0;
+        d.pcg->reason = 0;
+        d.pcg->done = (rr == 0.0) ? 1 : 0;
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_pcg_step(DevProblem d, float lam, double tol, int max_iters) {
+    __shared__ double red[32];
+    __shared__ int stop;
+    PcgState *st = d.pcg;
+    if (st->done) return;
+    const int64_t N = 9 * d.n_p;
+    double pw = 0.0;
+    for (int64_t i = threadIdx.x; i < N; i += blockDim.x) {
+        const float w = d.w[i] + lam * d.Dp2[i] * d.p[i];
+        d.w[i] = w;
+        pw += (double)d.p[i] * w;
+    }
+    pw = block_sum_d(pw, red);
+    if (!(pw > 0.0)) {
+        if (threadIdx.x == 0) st->done = 1, st->reason = 2;
+        return;
+    }
+    const float alpha = (float)(st->rz / pw);
+    double rr = 0.0;
+    for (int64_t i = threadIdx.x; i < N; i += blockDim.x) {
+        d.x[i] += alpha * d.p[i];
+        const float r = d.r[i] - alpha * d.w[i];
+        d.r[i] = r;
+        rr += (double)r * r;
+    }
+    rr = block_sum_d(rr, red);
+    if (threadIdx.x == 0) {
+        const int it = st->it + 1;
+        st->it = it;
+        st->rn = sqrt(rr);
+        stop = 0;
+        if (sqrt(rr) <= tol * st->r0) stop = 1, st->reason = 0;
+        else if (it >= max_iters) stop = 1, st->reason = 1;
+        if (stop) st->done = 1;
+    }
+    __syncthreads();
+    if (stop) return;
+    precond_apply(d, d.r, d.z, N);
+    __syncthreads();
+    double rz = 0.0;
+    for (int64_t i = threadIdx.x; i < N; i += blockDim.x) rz += (double)d.r[i] * d.z[i];
+    rz = block_sum_d(rz, red);
+    const float beta = (float)(rz / st->rz);
+    for (int64_t i = threadIdx.x; i < N; i += blockDim.x) d.p[i] = d.z[i] + beta * d.p[i];
+    __syncthreads();
+    if (threadIdx.x == 0) st->rz = rz;
+}
+
+// ============================================================================ K7 back-substitution
+__global__ void __launch_bounds__(256) k_backsub(DevProblem d, float lam) {
+    const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (j >= d.n_l) return;
+    const int k = d.lm_k[j];
+    const float *side = d.arena + d.lm_side[j];
+    const int W = 9 * k;
+    const int64_t obs0 = d.lm_obs0[j];
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+    for (int c = lane; c < W; c += 32) {
+        const int o = c / 9;
+        const float dp = d.x[9 * d.obs_cam[obs0 + o] + (c - 9 * o)];
+        s0 += side[c] * dp;
+        s1 += side[W + c] * dp;
+        s2 += side[2 * W + c] * dp;
+    }
+    s0 = warp_sum_f(s0);
+    s1 = warp_sum_f(s1);
+    s2 = warp_sum_f(s2);
+    if (lane == 0) {
+        const float4 *TL = reinterpret_cast<const float4 *>(side + side_tl(k));
+        const float4 t0 = TL[0], t1 = TL[1], t2 = TL[2];
+        const float b0 = t0.w + s0, b1 = t1.w + s1, b2 = t2.w + s2;
+        const float x2 = b2 / t2.z;
+        const float x1 = (b1 - t1.z * x2) / t1.y;
+        const float x0 = (b0 - t0.y * x1 - t0.z * x2) / t0.x;
+        const float dl[3] = {-x0, -x1, -x2};
+        double q1 = (double)t0.w * t0.w + (double)t1.w * t1.w + (double)t2.w * t2.w;
+        double dd = 0.0;
+#pragma unroll
+        for (int q = 0; q < 3; q++) {
+            d.dl[3 * j + q] = dl[q];
+            d.pts_trial[3 * j + q] = d.pts[3 * j + q] + d.lm_s[3 * j + q] * dl[q];
+            const double Dd = (double)d.lm_D[3 * j + q] * dl[q];
+            dd += Dd * Dd;
+        }
+        atomicAdd(d.scal + SC_Q1R2, q1);
+        atomicAdd(d.scal + SC_DAMPL, (double)lam * dd);
+    }
+}
+
+// trial cameras x_p + S_p dp and the (replicated) camera part of the model decrease (C10):
+// sum_i (-b~_i dp_i + rho_i dp_i + lam D_p,i^2 dp_i^2)
+__global__ void __launch_bounds__(1024) k_trial_cams(DevProblem d, float lam) {
+    __shared__ double red[32];
+    const int64_t N = 9 * d.n_p;
+    double m = 0.0;
+    for (int64_t i = threadIdx.x; i < N; i += blockDim.x) {
+        const float dp = d.x[i];
+        d.cams_trial[i] = d.cams[i] + d.sp[i] * dp;
+        m += -(double)d.bt[i] * dp + (double)d.r[i] * dp + (double)lam * d.Dp2[i] * (double)dp * dp;
+    }
+    m = block_sum_d(m, red);
+    if (threadIdx.x == 0) d.scal[SC_MODELP] = m;
+}
+
+// ============================================================================ K8 cost
+__global__ void __launch_bounds__(256) k_cost(DevProblem d, const float *__restrict__ cams,
+                                              const float *__restrict__ pts, int slot, int bad_slot) {
+    __shared__ double red[32];
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double e = 0.0, bad = 0.0;
+    if (i < d.n_obs) {
+        float c[9], r[2];
+        load_cam(cams, d.obs_cam[i], c);
+        const float *X = pts + 3 * (int64_t)d.obs_lm[i];
+        const float2 uv = d.obs_uv[i];
+        const float Pz = cam_model(c, X[0], X[1], X[2], uv.x, uv.y, r, nullptr, nullptr);
+        if (!(Pz < 0.f) || !isfinite(r[0]) || !isfinite(r[1])) bad = 1.0;
+        else e = (double)r[0] * r[0] + (double)r[1] * r[1];
+    }
+    e = block_sum_d(e, red);
+    bad = block_sum_d(bad, red);
+    if (threadIdx.x == 0) {
+        atomicAdd(d.scal + slot, e);
+        if (bad > 0) atomicAdd(d.scal + bad_slot, bad);
+    }
+}
+
+// ============================================================================ launchers
+static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+
+template <int G>
+static size_t small_marg_smem() {
+    return (size_t)(128 / 32) * (32 / G) * SmallTab<G>::FLOATS * sizeof(float);
+}
+static size_t large_marg_smem(int kmax) {
+    return (size_t)(4 * (2 * kmax + 3) + 4 * 9 * kmax + 18 * kmax + 6 * kmax + 2 * kmax + 20) * sizeof(float);
+}
+
+cudaError_t launch_check_depth(rba_ctx *c, int *d_bad) {
+    if (c->d.n_obs == 0) return cudaSuccess;
+    k_check_depth<<<nblk(c->d.n_obs, 256), 256, 0, c->stream>>>(c->d, d_bad);
+    c->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_linearize(rba_ctx *c) {
+    if (c->d.n_obs == 0) return cudaSuccess;
+    Prof P(c, KID_LIN, 24.0 * c->d.n_obs);
+    k_linearize<<<nblk(c->d.n_obs, 256), 256, 0, c->stream>>>(c->d);
+    P.end();
+    c->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cam_scale(rba_ctx *c) {
+    k_cam_scale<<<nblk(9 * c->d.n_p, 256), 256, 0, c->stream>>>(c->d, (float)c->opt.diag_min,
+                                                                  (float)c->opt.diag_max);
+    c->launches++;
+    return cudaGetLastError();
+}
+
+extern double plan_marg_bytes(rba_ctx *c);
+extern double plan_matvec_bytes(rba_ctx *c);
+
+template <int G>
+static cudaError_t marg_small_cls(rba_ctx *c, int cls, float lam) {
+    const int64_t lo = c->small_lo[cls], hi = c->small_hi[cls];
+    if (hi <= lo) return cudaSuccess;
+    const int64_t per_block = 4 * (32 / G);
+    const size_t sm = small_marg_smem<G>();
+    cudaFuncSetAttribute(k_marg_small<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_marg_small<G><<<nblk(hi - lo, (int)per_block), 128, sm, c->stream>>>(
+        c->d, lo, hi, lam, (float)c->opt.diag_min, (float)c->opt.diag_max);
+    c->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_marginalize(rba_ctx *c, float lam) {
+    Prof P(c, KID_MARG, plan_marg_bytes(c));
+    cudaError_t e;
+    if ((e = marg_small_cls<4>(c, 0, lam))) return e;
+    if ((e = marg_small_cls<8>(c, 1, lam))) return e;
+    if ((e = marg_small_cls<16>(c, 2, lam))) return e;
+    if ((e = marg_small_cls<32>(c, 3, lam))) return e;
+    if (c->n_large_items) {
+        const size_t sm = large_marg_smem((int)c->max_large_k);
+        cudaFuncSetAttribute(k_marg_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k_marg_large<<<(unsigned)c->n_large_items, 256, sm, c->stream>>>(c->d, c->d.large_items, lam,
+                                                                          (float)c->opt.diag_min,
+                                                                          (float)c->opt.diag_max);
+        c->launches++;
+        if ((e = cudaGetLastError())) return e;
+    }
+    P.end();
+    return cudaSuccess;
+}
+
+cudaError_t launch_redamp(rba_ctx *c, float lam) {
+    if (c->d.n_l == 0) return cudaSuccess;
+    Prof P(c, KID_DAMP, 0.0);
+    k_redamp<<<nblk(32 * c->d.n_l, 256), 256, 0, c->stream>>>(c->d, lam);
+    P.end();
+    c->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_precond_rhs(rba_ctx *c) {
+    if (c->d.n_obs == 0) return cudaSuccess;
+    Prof P(c, KID_PRE, plan_matvec_bytes(c));
+    k_precond_rhs<<<nblk(c->d.n_obs, 256), 256, 0, c->stream>>>(c->d);
+    P.end();
+    c->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_precond_finalize(rba_ctx *c, float lam) {
+    k_precond_finalize<<<nblk(c->d.n_p, 128), 128, 0, c->stream>>>(c->d, lam, c->d.scal + SC_BAD);
+    c->launches++;
+    return cudaGetLastError();
+}
+
+template <int G>
+static cudaError_t matvec_small_cls(rba_ctx *c, int cls, const float *v, float *out, const PcgState *st) {
+    const int64_t lo = c->small_lo[cls], hi = c->small_hi[cls];
+    if (hi <= lo) return cudaSuccess;
+    const int64_t per_block = 4 * (32 / G);
+    k_matvec_small<G><<<nblk(hi - lo, (int)per_block), 128, 0, c->stream>>>(c->d, lo, hi, v, out, st);
+    c->launches++;
+    return cudaGetLastError();
+}
+
+static cudaError_t matvec_impl(rba_ctx *c, const float *v, float *out, const PcgState *st) {
+    Prof P(c, KID_MATVEC, plan_matvec_bytes(c));
+    cudaError_t e;
+    if ((e = matvec_small_cls<4>(c, 0, v, out, st))) return e;
+    if ((e = matvec_small_cls<8>(c, 1, v, out, st))) return e;
+    if ((e = matvec_small_cls<16>(c, 2, v, out, st))) return e;
+    if ((e = matvec_small_cls<32>(c, 3, v, out, st))) return e;
+    if (c->n_large_items) {
+        const size_t sm = (size_t)9 * c->max_large_k * sizeof(float);
+        cudaFuncSetAttribute(k_matvec_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k_matvec_large<<<(unsigned)c->n_large_items, 256, sm, c->stream>>>(c->d, c->d.large_items, v, out, st);
+        c->launches++;
+        if ((e = cudaGetLastError())) return e;
+    }
+    P.end();
+    return cudaSuccess;
+}
+
+cudaError_t launch_matvec(rba_ctx *c, const float *v, float *out) { return matvec_impl(c, v, out, nullptr); }
+cudaError_t launch_matvec_pcg(rba_ctx *c) { return matvec_impl(c, c->d.p, c->d.w, c->d.pcg); }
+
+cudaError_t launch_add_damping(rba_ctx *c, const float *v, float *out, float lam) {
+    k_add_damping<<<nblk(9 * c->d.n_p, 256), 256, 0, c->stream>>>(c->d, v, out, lam);
+    c->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pcg_init(rba_ctx *c, float, int) {
+    k_pcg_init<<<1, 1024, 0, c->stream>>>(c->d);
+    c->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pcg_step(rba_ctx *c, float lam, float tol, int max_iters) {
+    Prof P(c, KID_PCG, 0.0);
+    k_pcg_step<<<1, 1024, 0, c->stream>>>(c->d, lam, (double)tol, max_iters);
+    P.end();
+    c->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_backsub(rba_ctx *c, float lam) {
+    Prof P(c, KID_BACKSUB, 0.0);
+    if (c->d.n_l) {
+        k_backsub<<<nblk(32 * c->d.n_l, 256), 256, 0, c->stream>>>(c->d, lam);
+        c->launches++;
+    }
+    k_trial_cams<<<1, 1024, 0, c->stream>>>(c->d, lam);
+    c->launches++;
+    P.end();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cost(rba_ctx *c, int at_trial, int slot) {
+    if (c->d.n_obs == 0) return cudaSuccess;
+    Prof P(c, KID_COST, 20.0 * c->d.n_obs);
+    const int bad_slot = at_trial ? SC_BADT : SC_BAD;
+    k_cost<<<nblk(c->d.n_obs, 256), 256, 0, c->stream>>>(c->d, at_trial ? c->d.cams_trial : c->d.cams,
+                                                          at_trial ? c->d.pts_trial : c->d.pts, slot, bad_slot);
+    P.end();
+    c->launches++;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_trial_cost(rba_ctx *c) { return launch_cost(c, 1, SC_ET); }
+cudaError_t launch_commit(rba_ctx *) { return cudaSuccess; }
+
+}  // namespace rba

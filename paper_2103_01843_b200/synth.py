@@ -305,3 +305,24 @@ def digest(prob: dict) -> str:
     for key in ("cameras_init", "points_init", "obs_cam", "obs_pt", "obs_uv"):
         h.update(np.ascontiguousarray(prob[key]).tobytes())
     return h.hexdigest()
+
+
+def make_tracks(seed: int, ks, n_p: int | None = None, pt_noise: float = 0.05, cam_noise: float = 0.01) -> dict:
+    """Circle-geometry problem with prescribed track lengths `ks` (edge cases: k = 2, bucket
+    boundaries 4/5, 8/9, 16/17, 32/33, long tracks).  Cameras on a circle of radius 10 looking at
+    the origin (like cfg 1) with random intrinsics; landmark j seen by a random ks[j]-subset."""
+    ks = np.asarray(ks, np.int64)
+    n_p = int(max(ks.max(), 16) if n_p is None else n_p)
+    rng = np.random.default_rng(seed)
+    Rs, ts = _circle_cameras(n_p)
+    intr = np.stack([rng.uniform(300, 800, n_p), rng.normal(0, 0.02, n_p), rng.normal(0, 0.005, n_p)], 1)
+    obs_cam = np.concatenate([np.sort(rng.choice(n_p, size=k, replace=False)) for k in ks])
+    obs_pt = np.repeat(np.arange(ks.size), ks)
+    X = rng.uniform(-2.0, 2.0, size=(ks.size, 3))
+    uv, Pz, _ = _project_true(Rs, ts, intr, obs_cam, X[obs_pt])
+    assert np.all(Pz < 0)
+    cams_true = np.concatenate([matrix_to_rotvec(Rs), ts, intr], 1)
+    cams_init = _perturb_poses(Rs, ts, intr, rng, cam_noise, 5 * cam_noise)
+    return dict(cfg=0, seed=seed, cameras_true=cams_true, points_true=X, cameras_init=cams_init,
+                points_init=X + rng.normal(0, pt_noise, X.shape), obs_cam=obs_cam.astype(np.int32),
+                obs_pt=obs_pt.astype(np.int32), obs_uv=uv + rng.normal(0, 1.0, uv.shape), lm_iters=5)

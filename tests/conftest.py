@@ -10,6 +10,11 @@ if ROOT not in sys.path:
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
+    # build the product library (nvcc cross-compiles without a GPU) and the oracle checker
+    from paper_2103_01843_b200 import _build
+    _build.build()
+    import oracle
+    oracle.build()
 
 
 def pytest_collection_modifyitems(config, items):

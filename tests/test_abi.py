@@ -1,0 +1,97 @@
+"""CPU-side checks of the C ABI (no compute calls without a GPU): every symbol declared in
+include/rba.h is exported by librba.so, the host planner (LPT landmark sharding) is a
+deterministic balanced partition, and host-side validation rejects bad problems with the documented
+status codes before touching the device."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2103_01843_b200 import rba, synth
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _header_functions():
+    src = open(os.path.join(ROOT, "include", "rba.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(rba_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_symbols_exported():
+    names = _header_functions()
+    assert len(names) >= 20
+    lib = rba.lib()
+    for n in names:
+        assert hasattr(lib, n), n
+    assert sorted(rba.EXPORTED) == names
+
+
+def test_default_options():
+    o = rba.rba_default_options()
+    assert (o.lambda0, o.pcg_rel_tol, o.pcg_max_iters, o.min_rel_decrease) == (1e-4, 1e-2, 500, 1e-3)
+    assert (o.diag_min, o.diag_max, o.world, o.rank) == (1e-6, 1e32, 1, 0)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_plan_shards_lpt(world):
+    rng = np.random.default_rng(world)
+    k = np.concatenate([rng.integers(2, 9, 5000), rng.integers(50, 400, 40)]).astype(np.int32)
+    o1 = rba.rba_plan_shards(k, world)
+    o2 = rba.rba_plan_shards(k, world)
+    np.testing.assert_array_equal(o1, o2)  # deterministic: every rank computes the same partition
+    assert o1.min() >= 0 and o1.max() < world
+    if world == 1:
+        assert not o1.any()
+        return
+    b = (2 * k.astype(np.int64) + 3) * (9 * k + 4)
+    load = np.bincount(o1, weights=b, minlength=world)
+    # LPT bound: max load <= mean + largest item
+    assert load.max() <= b.sum() / world + b.max()
+
+
+def _prob():
+    return synth.make_random_small(3, n_p=4, n_l=6)
+
+
+@pytest.mark.parametrize("mutate,status", [
+    (lambda p: p.update(obs_pt=np.where(p["obs_pt"] == 0, 1, p["obs_pt"]).astype(np.int32)), rba.RBA_ERR_BAD_PROBLEM),
+    (lambda p: p["obs_cam"].__setitem__(0, 99), rba.RBA_ERR_BAD_PROBLEM),
+    (lambda p: p["cameras_init"].__setitem__((1, 6), -5.0), rba.RBA_ERR_BAD_PROBLEM),
+    (lambda p: p["points_init"].__setitem__((2, 1), np.nan), rba.RBA_ERR_BAD_PROBLEM),
+    (lambda p: p.update(obs_cam=np.r_[p["obs_cam"], p["obs_cam"][:1]].astype(np.int32),
+                        obs_pt=np.r_[p["obs_pt"], p["obs_pt"][:1]].astype(np.int32),
+                        obs_uv=np.r_[p["obs_uv"], p["obs_uv"][:1]]), rba.RBA_ERR_BAD_PROBLEM),
+])
+def test_create_rejects_bad_problems(mutate, status):
+    """k < 2, index out of range, f <= 0, non-finite, duplicate (cam, pt) -> BAD_PROBLEM."""
+    p = _prob()
+    p = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in p.items()}
+    mutate(p)
+    with pytest.raises(rba.RBAError) as ei:
+        rba.rba_create(p["cameras_init"], p["points_init"], p["obs_cam"], p["obs_pt"], p["obs_uv"])
+    assert ei.value.status == status
+
+
+def test_create_rejects_bad_options():
+    p = _prob()
+    o = rba.rba_default_options()
+    o.world, o.rank = 2, 5
+    with pytest.raises(rba.RBAError) as ei:
+        rba.rba_create(p["cameras_init"], p["points_init"], p["obs_cam"], p["obs_pt"], p["obs_uv"], o)
+    assert ei.value.status == rba.RBA_ERR_INVALID_ARG
+
+
+def test_layout_constants_match_paper_block_size():
+    """The arena stores exactly the logical (2k+3) x (9k+4) block per landmark plus
+    16-byte alignment padding: check the layout formulas the planner uses, via a GPU-free
+    reconstruction of the per-landmark float counts."""
+    for k in list(range(2, 40)) + [64, 100, 257, 400, 512]:
+        H = 2 * k if k <= 32 else 4
+        T = 1 if k <= 32 else (2 * k + 3) // 4
+        pad4 = lambda x: (x + 3) // 4 * 4
+        r2 = (T - 1) * pad4(9 * k * H) + pad4(9 * k * (2 * k - (T - 1) * H))
+        side = pad4(27 * k) + 4 * (2 * k + 3) + 12
+        logical = (2 * k + 3) * (9 * k + 4) + 12
+        assert 0 <= r2 + side - logical <= 3 * (T + 1)
