@@ -255,6 +255,7 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
         if (s_ != RBA_OK) return bail(s_);                                                         \
     } while (0)
     CKC(cudaSetDevice(opt.device));
+    CKC(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, opt.device));
     if (opt.stream) {
         c->stream = (cudaStream_t)opt.stream;
     } else {
@@ -280,44 +281,96 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     c->h_k.resize(nl);
     c->h_r2.resize(nl);
     c->h_side.resize(nl);
+    c->h_pk.assign(nl, 0);
     std::vector<int32_t> h_obs0(nl);
-    int64_t nobs_loc = 0, r2_total = 0;
+    int64_t nobs_loc = 0;
     for (int64_t i = 0; i < nl; i++) {
         const int k = kcount[loc[i]];
         c->h_k[i] = k;
         h_obs0[i] = (int32_t)nobs_loc;
         nobs_loc += k;
-        c->h_r2[i] = r2_total;
-        r2_total += r2_floats(k);
         c->logical_bytes += (int64_t)(2 * k + 3) * (9 * k + 4) * 4 + 48;
         c->marg_bytes += (double)(2 * k + 3) * (9 * k + 4) * 4 + 48 + 20.0 * k;
         c->matvec_bytes += 72.0 * k * k;
     }
+    // ---- R2 arena: packs of same-k small landmarks (classes G = 4, 8, 16, 32), then large ones
+    std::vector<Pack> packs;
+    const int bounds[4] = {4, 8, 16, 32};
+    int64_t r2_total = 0, pos = 0;
+    for (int cls = 0; cls < 4; cls++) {
+        const int NG = 32 / bounds[cls];
+        c->pack_lo[cls] = (int64_t)packs.size();
+        while (pos < nl && c->h_k[pos] <= bounds[cls]) {
+            const int k = c->h_k[pos];
+            int np = 0;
+            while (pos + np < nl && np < NG && c->h_k[pos + np] == k) np++;
+            packs.push_back(Pack{(int32_t)pos, np, r2_total});
+            for (int m = 0; m < np; m++) {
+                c->h_r2[pos + m] = r2_total;
+                c->h_pk[pos + m] = m | (np << 8);
+            }
+            r2_total += pad4(small_pack_floats(k, np));
+            pos += np;
+        }
+        c->pack_hi[cls] = (int64_t)packs.size();
+    }
+    std::vector<LargeItem> marg_items;
+    std::vector<TileRef> tiles;
+    std::vector<int64_t> cta_lo;
+    const int ntb[4] = {64, 128, 256, 512};
+    const int64_t large_lo = pos;
+    for (int64_t i = pos; i < nl; i++) {
+        const int k = c->h_k[i];
+        c->h_r2[i] = r2_total;
+        r2_total += large_r2_floats(k);
+        c->max_large_k = std::max<int64_t>(c->max_large_k, k);
+    }
+    for (int cls = 0; cls < 4; cls++) {
+        auto in_cls = [&](int k) { return k <= ntb[cls] && (cls == 0 || k > ntb[cls - 1]); };
+        c->marg_lo[cls] = (int64_t)marg_items.size();
+        const int64_t t_lo = (int64_t)tiles.size();
+        double bytes = 0;
+        for (int64_t i = large_lo; i < nl; i++) {
+            const int k = c->h_k[i];
+            if (!in_cls(k)) continue;
+            const int T = large_tiles(k);
+            const int tpi2 = std::max(1, 262144 / (36 * k));
+            for (int t0 = 0; t0 < T; t0 += tpi2)
+                marg_items.push_back(LargeItem{(int32_t)i, t0, std::min(T, t0 + tpi2), 0});
+            for (int t = 0; t < T; t++) tiles.push_back(TileRef{(int32_t)i, t});
+            bytes += 144.0 * k * T;
+        }
+        c->marg_hi[cls] = (int64_t)marg_items.size();
+        const int64_t t_hi = (int64_t)tiles.size();
+        // persistent CTAs (one per SM) over contiguous tile ranges balanced by bytes
+        c->cta_off[cls] = (int64_t)cta_lo.size();
+        const int64_t ntl = t_hi - t_lo;
+        const int64_t G = std::min<int64_t>(c->num_sms, ntl);
+        c->cta_n[cls] = G;
+        if (G > 0) {
+            cta_lo.push_back(t_lo);
+            double accb = 0;
+            int64_t next = 1;
+            for (int64_t ti = t_lo; ti < t_hi && next < G; ti++) {
+                accb += 144.0 * c->h_k[tiles[ti].lm];
+                if (accb >= bytes * next / G) {
+                    cta_lo.push_back(ti + 1);
+                    next++;
+                }
+            }
+            while ((int64_t)cta_lo.size() - c->cta_off[cls] < G) cta_lo.push_back(t_hi);
+            cta_lo.push_back(t_hi);
+        } else {
+            cta_lo.push_back(t_hi);
+        }
+    }
+    c->n_packs = (int64_t)packs.size();
     int64_t side_total = r2_total;
     for (int64_t i = 0; i < nl; i++) {
         c->h_side[i] = side_total;
         side_total += side_floats(c->h_k[i]);
     }
     c->arena_floats = side_total;
-    // classes G = 4, 8, 16, 32 and the large-k work items
-    const int bounds[4] = {4, 8, 16, 32};
-    int64_t pos = 0;
-    for (int cls = 0; cls < 4; cls++) {
-        c->small_lo[cls] = pos;
-        while (pos < nl && c->h_k[pos] <= bounds[cls]) pos++;
-        c->small_hi[cls] = pos;
-    }
-    c->large_lo = pos;
-    c->large_hi = nl;
-    std::vector<LargeItem> items;
-    for (int64_t i = pos; i < nl; i++) {
-        const int k = c->h_k[i];
-        c->max_large_k = std::max<int64_t>(c->max_large_k, k);
-        const int T = n_tiles(k);
-        const int tpi = std::max(1, 65536 / (36 * k));
-        for (int t0 = 0; t0 < T; t0 += tpi) items.push_back(LargeItem{(int32_t)i, t0, std::min(T, t0 + tpi), 0});
-    }
-    c->n_large_items = (int64_t)items.size();
     // ---- device buffers
     DevProblem &d = c->d;
     d.n_p = n_cams;
@@ -329,6 +382,7 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     CKSC(dalloc_n(c, &d.pts_trial, 3 * nl));
     CKSC(dalloc_n(c, &d.lm_k, nl));
     CKSC(dalloc_n(c, &d.lm_obs0, nl));
+    CKSC(dalloc_n(c, &d.lm_pk, nl));
     CKSC(dalloc_n(c, &d.lm_r2, nl));
     CKSC(dalloc_n(c, &d.lm_side, nl));
     CKSC(dalloc_n(c, &d.obs_cam, nobs_loc));
@@ -351,7 +405,10 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     CKSC(dalloc_n(c, &d.dl, 3 * nl));
     CKSC(dalloc_n(c, &d.scal, SC_N));
     CKSC(dalloc_n(c, &d.pcg, 1));
-    CKSC(dalloc_n(c, &d.large_items, std::max<int64_t>(1, c->n_large_items)));
+    CKSC(dalloc_n(c, &d.packs, std::max<size_t>(1, packs.size())));
+    CKSC(dalloc_n(c, &d.marg_items, std::max<size_t>(1, marg_items.size())));
+    CKSC(dalloc_n(c, &d.tiles, std::max<size_t>(1, tiles.size())));
+    CKSC(dalloc_n(c, &d.cta_lo, std::max<size_t>(1, cta_lo.size())));
     CKC(cudaMallocHost(&c->h_scal, sizeof(double) * SC_N));
     CKC(cudaMallocHost(&c->h_pcg, sizeof(PcgState)));
     // ---- upload (host staging in the device layout)
@@ -381,9 +438,18 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
         CKC(cudaMemcpyAsync(d.obs_cam, ocam.data(), sizeof(int32_t) * nobs_loc, cudaMemcpyHostToDevice, c->stream));
         CKC(cudaMemcpyAsync(d.obs_lm, olm.data(), sizeof(int32_t) * nobs_loc, cudaMemcpyHostToDevice, c->stream));
         CKC(cudaMemcpyAsync(d.obs_uv, ouv.data(), sizeof(float2) * nobs_loc, cudaMemcpyHostToDevice, c->stream));
-        if (!items.empty())
-            CKC(cudaMemcpyAsync(d.large_items, items.data(), sizeof(LargeItem) * items.size(),
+        CKC(cudaMemcpyAsync(d.lm_pk, c->h_pk.data(), sizeof(int32_t) * nl, cudaMemcpyHostToDevice, c->stream));
+        if (!packs.empty())
+            CKC(cudaMemcpyAsync(d.packs, packs.data(), sizeof(Pack) * packs.size(), cudaMemcpyHostToDevice, c->stream));
+        if (!marg_items.empty())
+            CKC(cudaMemcpyAsync(d.marg_items, marg_items.data(), sizeof(LargeItem) * marg_items.size(),
                                 cudaMemcpyHostToDevice, c->stream));
+        if (!tiles.empty())
+            CKC(cudaMemcpyAsync(d.tiles, tiles.data(), sizeof(TileRef) * tiles.size(), cudaMemcpyHostToDevice,
+                                c->stream));
+        if (!cta_lo.empty())
+            CKC(cudaMemcpyAsync(d.cta_lo, cta_lo.data(), sizeof(int64_t) * cta_lo.size(), cudaMemcpyHostToDevice,
+                                c->stream));
         CKC(cudaMemsetAsync(d.scal, 0, sizeof(double) * SC_N, c->stream));
         // front-of-camera validation at the initial state, in a kernel
         int *dbad = reinterpret_cast<int *>(d.pcg);  // scratch
@@ -698,7 +764,9 @@ extern "C" rba_status rba_export_block(rba_ctx *c, int64_t landmark, double *buf
     *rows = R;
     *cols = C;
     if (cap < R * C) return fail(RBA_ERR_INVALID_ARG, "buffer too small");
-    std::vector<float> r2(r2_floats(k)), side(side_floats(k));
+    const int32_t pk = c->h_pk[j];
+    const int64_t r2n = k <= KSMALL ? small_pack_floats(k, pk >> 8) : large_r2_floats(k);
+    std::vector<float> r2(r2n), side(side_floats(k));
     CK(cudaMemcpyAsync(r2.data(), c->d.arena + c->h_r2[j], sizeof(float) * r2.size(), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(side.data(), c->d.arena + c->h_side[j], sizeof(float) * side.size(), cudaMemcpyDeviceToHost,
                        c->stream));
@@ -708,7 +776,7 @@ extern "C" rba_status rba_export_block(rba_ctx *c, int64_t landmark, double *buf
         double *out = buf + row * C;
         for (int o = 0; o < k; o++)
             for (int q = 0; q < 9; q++)
-                out[9 * o + q] = row < 3 ? side[row * 9 * k + 9 * o + q] : r2[r2_index(k, (int)row - 3, o, q)];
+                out[9 * o + q] = row < 3 ? side[row * 9 * k + 9 * o + q] : r2[r2_index(k, pk, (int)row - 3, o, q)];
         for (int q = 0; q < 4; q++) out[9 * k + q] = TL[4 * row + q];
     }
     return RBA_OK;

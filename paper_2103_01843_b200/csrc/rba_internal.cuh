@@ -12,44 +12,51 @@
 
 namespace rba {
 
-constexpr int KSMALL = 32;    // k <= KSMALL: one tile per landmark, warp-group kernels
-constexpr int TILE_H = 4;     // R2 rows per tile for k > KSMALL
+constexpr int KSMALL = 32;    // k <= KSMALL: warp-group kernels over packs of same-k landmarks
 constexpr int KMAX = 512;     // largest track length supported by this build's large-k kernels
 
 // ---- landmark-block arena layout ------------------------------------------
-// Per landmark (internal order), two 16-byte aligned regions:
-//  R2   = A_j = Q^_2^T J_p: logical rows 3..2k+2 (2k rows) x 9k pose columns, stored in row tiles
-//         of height H (H = 2k if k <= KSMALL else TILE_H); inside a tile, camera-block-major:
-//         block o is an H x 9 row-major slab.  The tile is the unit the matvec streams.
-//  side = R1 (logical rows 0..2, 3 x 9k row-major: Q^_1^T J_p)  | pad4
-//         TL ((2k+3) float4: [landmark columns | residual] of every logical row)
-//         G  (6 x (c, s) damping rotations)                       | pad4
+// Logical block of a landmark with k observations: rows 0..2k+2, columns [J_p (9k) | J_l | r].
+// R2 = A_j = Q^_2^T J_p = logical rows 3..2k+2 (2k rows "a" = 0..2k-1) x 9k pose columns is what
+// the PCG matvec streams; it is stored so that every warp load is one contiguous run:
+//  * small k (<= KSMALL): landmarks are grouped in packs of np <= 32/G same-k landmarks (G = lanes
+//    per landmark).  A pack is row-pair major: for row pair p (rows 2p, 2p+1), slab chunk c (9
+//    float2 of the 2 x 9 slab of camera block o), landmark m, block o:
+//       float2 index ((p*9 + c)*np*k + m*k + o)
+//  * large k (> KSMALL): tiles of 4 rows (rows >= 2k are zero padding), tile t at 36 k t; in a
+//    tile, camera blocks in groups of 32 (n_g = min(32, k - 32 g)); the 4 x 9 slab of block o is
+//    9 float4 chunks:  float4 index (36*32*g)/4 + c*n_g + (o & 31)
+// Side region per landmark (16-byte aligned):  R1 = logical rows 0..2 pose columns (3 x 9k
+// row-major) | pad4 | TL: (2k+3) float4 [J_l row | residual] of every logical row | G: 6 x (c, s).
 __host__ __device__ inline int64_t pad4(int64_t x) { return (x + 3) & ~int64_t(3); }
-__host__ __device__ inline int tile_h(int k) { return k <= KSMALL ? 2 * k : TILE_H; }
-__host__ __device__ inline int n_tiles(int k) { return k <= KSMALL ? 1 : (2 * k + TILE_H - 1) / TILE_H; }
-__host__ __device__ inline int tile_rows(int k, int t) {
-    int H = tile_h(k);
-    int r = 2 * k - t * H;
-    return r < H ? r : H;
+__host__ __device__ inline int large_tiles(int k) { return (k + 1) >> 1; }  // ceil(2k / 4)
+__host__ __device__ inline int64_t small_pack_floats(int k, int np) { return (int64_t)18 * k * k * np; }
+__host__ __device__ inline int64_t large_r2_floats(int k) { return (int64_t)36 * k * large_tiles(k); }
+__host__ __device__ inline int64_t small_index(int k, int np, int m, int a, int o, int q) {
+    const int p = a >> 1, e = 9 * (a & 1) + q, c = e >> 1;
+    return ((int64_t)((p * 9 + c) * np + m) * k + o) * 2 + (e & 1);
 }
-// float offset of tile t inside the landmark's R2 region (all tiles but the last are full)
-__host__ __device__ inline int64_t tile_off(int k, int t) { return (int64_t)t * pad4((int64_t)9 * k * tile_h(k)); }
-__host__ __device__ inline int64_t r2_floats(int k) {
-    int T = n_tiles(k);
-    return tile_off(k, T - 1) + pad4((int64_t)9 * k * tile_rows(k, T - 1));
+__host__ __device__ inline int64_t large_index(int k, int a, int o, int q) {
+    const int t = a >> 2, e = 9 * (a & 3) + q, c = e >> 2;
+    const int g = o >> 5, ng = (k - 32 * g) < 32 ? (k - 32 * g) : 32;
+    return (int64_t)36 * k * t + 36 * 32 * g + (c * ng + (o & 31)) * 4 + (e & 3);
 }
-// float offset of element (R2 row a, camera block o, param q)
-__host__ __device__ inline int64_t r2_index(int k, int a, int o, int q) {
-    int H = tile_h(k);
-    int t = a / H;
-    int h = tile_rows(k, t);
-    return tile_off(k, t) + (int64_t)o * 9 * h + (int64_t)(a - t * H) * 9 + q;
+// lm_pk[j] = m | (np << 8) for small landmarks (pack slot, pack size); 0 for large ones.
+__host__ __device__ inline int64_t r2_index(int k, int32_t pk, int a, int o, int q) {
+    return k <= KSMALL ? small_index(k, pk >> 8, pk & 255, a, o, q) : large_index(k, a, o, q);
 }
 __host__ __device__ inline int64_t side_r1_floats(int k) { return pad4(27 * (int64_t)k); }
 __host__ __device__ inline int64_t side_floats(int k) { return side_r1_floats(k) + 4 * (2 * (int64_t)k + 3) + 12; }
-// side sub-offsets
 __host__ __device__ inline int64_t side_tl(int k) { return side_r1_floats(k); }
 __host__ __device__ inline int64_t side_g(int k) { return side_r1_floats(k) + 4 * (2 * (int64_t)k + 3); }
+
+// fast exact n / d for n, d < 2^16:  __umulhi(n, magic(d))
+__host__ __device__ inline uint32_t divmagic(uint32_t d) { return (uint32_t)((0x100000000ull + d - 1) / d); }
+
+struct Pack {
+    int32_t lm0, np;  // first landmark (internal index) and number of landmarks (same k)
+    int64_t base;     // float offset of the pack's R2 region
+};
 
 struct PcgState {
     double rz;  // rho^T z
@@ -64,8 +71,12 @@ enum { SC_E = 0, SC_BAD, SC_ET, SC_BADT, SC_Q1R2, SC_DAMPL, SC_MODELP, SC_N = 8 
 
 enum { KID_LIN = 0, KID_MARG, KID_DAMP, KID_PRE, KID_MATVEC, KID_PCG, KID_BACKSUB, KID_COST, KID_N };
 
+struct TileRef {
+    int32_t lm, t;  // landmark (internal index) and 4-row tile index
+};
+
 struct LargeItem {
-    int32_t lm, t0, t1, pad;
+    int32_t lm, t0, t1, pad;  // landmark (internal index) and tile range [t0, t1)
 };
 
 struct DevProblem {
@@ -73,7 +84,7 @@ struct DevProblem {
     // state
     float *cams, *cams_trial, *pts, *pts_trial;
     // landmark metadata (internal order, sorted by k)
-    int32_t *lm_k, *lm_obs0;
+    int32_t *lm_k, *lm_obs0, *lm_pk;
     int64_t *lm_r2, *lm_side;
     int32_t *obs_cam, *obs_lm;
     float2 *obs_uv;
@@ -89,7 +100,10 @@ struct DevProblem {
     float *dl;
     double *scal;
     PcgState *pcg;
-    LargeItem *large_items;
+    Pack *packs;            // small-k packs, classes G = 4, 8, 16, 32 back to back
+    LargeItem *marg_items;  // K2 work items (~1 MB of output each), classes NT = 64, 128, 256, 512
+    TileRef *tiles;         // K4/K5 tile stream of the large landmarks, classes k <= 64, 128, 256, 512
+    int64_t *cta_lo;        // per class: tile range boundaries of the persistent CTAs (bytes-balanced)
 };
 
 struct Launch {
@@ -115,9 +129,12 @@ struct rba_ctx {
     std::vector<int32_t> orig_to_int; // caller landmark -> internal (-1 if not owned)
     std::vector<int32_t> h_k;
     std::vector<int64_t> h_r2, h_side;
-    int64_t small_lo[4] = {0, 0, 0, 0}, small_hi[4] = {0, 0, 0, 0};  // G = 4, 8, 16, 32 ranges
-    int64_t large_lo = 0, large_hi = 0;
-    int64_t n_large_items = 0, max_large_k = 0;
+    std::vector<int32_t> h_pk;
+    int64_t pack_lo[4] = {0, 0, 0, 0}, pack_hi[4] = {0, 0, 0, 0};  // G = 4, 8, 16, 32 pack ranges
+    int64_t marg_lo[4] = {0, 0, 0, 0}, marg_hi[4] = {0, 0, 0, 0};  // K2 large items per class
+    int64_t cta_off[4] = {0, 0, 0, 0}, cta_n[4] = {0, 0, 0, 0};    // K4/K5 CTA ranges per class
+    int64_t n_packs = 0, max_large_k = 0;
+    int num_sms = 148;
     int64_t arena_floats = 0, logical_bytes = 0;
     double marg_bytes = 0, matvec_bytes = 0;  // algorithmic bytes per launch
     std::vector<void *> allocations;

@@ -254,102 +254,72 @@ __device__ __forceinline__ void damp_rotations(const float *R, const float *rr, 
 }
 
 // ============================================================================ K2 emission
-// Tables (shared memory) describing one marginalized landmark block in compact-WY form:
-//   VR[row]  (float4) row of V (logical rows 3..2k-1) or effective V of the 6 damped rows
-//            (logical rows 0..2 and 2k..2k+2): out[row, c] = Jterm - VR[row] . MC[c]
-//   MC[c]    (float4) column c of M = T^T V^T J_p
-//   JP[a][q] scaled J_p rows (row a lives in camera block a >> 1)
-//   GM[s][m] damping mix of J_p rows 0..2 into special row s
-struct MargTables {
-    const float4 *VR;
-    const float4 *MC;
-    const float *JP;
-    const float *GM;
+// Compact-WY form of the marginalized block (Householder): Q^T = I - V T^T V^T, so every
+// output row L of the pose columns of camera block o is
+//     out[L, 9o+q] = Jterm(L, o, q) - V[L] . M[:, 9o+q],    M = T^T V^T J_p (3 x 9k),
+// and J_p is block diagonal (observation o owns rows 2o, 2o+1).  The thread (lane) that owns
+// camera block o keeps M[:, 9o..9o+8] and its two scaled J_p rows in registers, so each output
+// float costs 3 FMA and is stored coalesced in the matvec layout.  The 6 damped rows (logical
+// 0..2 and 2k..2k+2) use V_eff = Gm V and mix J_p rows 0..2 with the damping rotations Gm.
+struct BlockWY {
+    float m[3][9];   // M[:, 9o + q]
+    float jp[2][9];  // scaled J_p rows 2o, 2o+1
 };
 
-// value of logical row `row` (0..2k+2), camera block o, param q
-__device__ __forceinline__ float marg_elem(const MargTables &T, int k, int row, int o, int q) {
-    const float4 vr = T.VR[row];
-    const float4 mc = T.MC[9 * o + q];
-    float val = -(vr.x * mc.x + vr.y * mc.y + vr.z * mc.z);
-    if (row >= 3 && row < 2 * k) {
-        if (o == (row >> 1)) val += T.JP[row * 9 + q];
+// 9 values of logical row L for camera block o.  VR = V rows (specials already V_eff), GM = Gm.
+__device__ __forceinline__ void wy_row(const BlockWY &B, const float4 *VR, const float *GM, int k, int L, int o,
+                                       float *out9) {
+    const float4 V = VR[L];
+    float c0 = 0.f, c1 = 0.f;
+    if (L >= 3 && L < 2 * k) {
+        if (o == (L >> 1)) {
+            c0 = (L & 1) ? 0.f : 1.f;
+            c1 = (L & 1) ? 1.f : 0.f;
+        }
     } else {
-        const int s = row < 3 ? row : row - 2 * k + 3;
-        if (o == 0)
-            val += T.GM[s * 3 + 0] * T.JP[q] + T.GM[s * 3 + 1] * T.JP[9 + q];
-        else if (o == 1)
-            val += T.GM[s * 3 + 2] * T.JP[18 + q];
+        const int s = L < 3 ? L : L - 2 * k + 3;
+        if (o == 0) c0 = GM[3 * s], c1 = GM[3 * s + 1];
+        else if (o == 1) c0 = GM[3 * s + 2];
     }
-    return val;
+#pragma unroll
+    for (int q = 0; q < 9; q++)
+        out9[q] = c0 * B.jp[0][q] + c1 * B.jp[1][q] - (V.x * B.m[0][q] + V.y * B.m[1][q] + V.z * B.m[2][q]);
 }
 
-// R2 elements [e_lo, e_hi) (float indices relative to the landmark's R2 region, multiples of 4),
-// written as float4 by `nl` cooperating lanes (lane id `li`).
-__device__ __forceinline__ void emit_r2(const MargTables &T, int k, float *__restrict__ r2, int64_t e_lo, int64_t e_hi,
-                                       int li, int nl) {
-    const int H = tile_h(k);
-    const int T_ = n_tiles(k);
-    const int64_t full = pad4((int64_t)9 * k * H);
-    for (int64_t e4 = e_lo + 4 * li; e4 < e_hi; e4 += 4 * nl) {
-        float4 out;
-        float *ov = &out.x;
+// M column block from V rows 2o, 2o+1 and T (upper 3x3, entries T00..T22)
+__device__ __forceinline__ void wy_m(BlockWY &B, float4 v0, float4 v1, float T00, float T01, float T02, float T11,
+                                     float T12, float T22) {
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
-            const int64_t e = e4 + u;
-            int t = (int)(e / full);
-            if (t >= T_) t = T_ - 1;
-            const int h = tile_rows(k, t);
-            const int within = (int)(e - (int64_t)t * full);
-            float val = 0.f;
-            if (within < 9 * k * h) {
-                const int o = within / (9 * h);
-                const int rem = within - o * 9 * h;
-                const int a = (rem * 7282) >> 16;  // rem / 9 for rem < 36000
-                const int q = rem - 9 * a;
-                val = marg_elem(T, k, 3 + t * H + a, o, q);
-            }
-            ov[u] = val;
-        }
-        *reinterpret_cast<float4 *>(r2 + e4) = out;
+    for (int q = 0; q < 9; q++) {
+        const float j0 = B.jp[0][q], j1 = B.jp[1][q];
+        const float W0 = v0.x * j0 + v1.x * j1, W1 = v0.y * j0 + v1.y * j1, W2 = v0.z * j0 + v1.z * j1;
+        B.m[0][q] = T00 * W0;
+        B.m[1][q] = T01 * W0 + T11 * W1;
+        B.m[2][q] = T02 * W0 + T12 * W1 + T22 * W2;
     }
 }
 
-// R1 = logical rows 0..2 (3 x 9k, row-major, padded to 4)
-__device__ __forceinline__ void emit_r1(const MargTables &T, int k, float *__restrict__ r1, int li, int nl) {
-    const int n = 27 * k;
-    const int n4 = (int)pad4(n);
-    for (int e4 = 4 * li; e4 < n4; e4 += 4 * nl) {
-        float4 out;
-        float *ov = &out.x;
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-            const int e = e4 + u;
-            float val = 0.f;
-            if (e < n) {
-                const int m = e / (9 * k);
-                const int c = e - m * 9 * k;
-                const int o = c / 9;
-                val = marg_elem(T, k, m, o, c - 9 * o);
-            }
-            ov[u] = val;
-        }
-        *reinterpret_cast<float4 *>(r1 + e4) = out;
-    }
+// V_eff rows of the 6 damped rows, written to VR[0..2] and VR[2k..2k+2]
+__device__ __forceinline__ float4 veff(const float *Gm, const float *V3, int s) {
+    float4 ve;
+    ve.x = Gm[s * 3] * V3[0] + Gm[s * 3 + 1] * V3[3] + Gm[s * 3 + 2] * V3[6];
+    ve.y = Gm[s * 3] * V3[1] + Gm[s * 3 + 1] * V3[4] + Gm[s * 3 + 2] * V3[7];
+    ve.z = Gm[s * 3] * V3[2] + Gm[s * 3 + 1] * V3[5] + Gm[s * 3 + 2] * V3[8];
+    ve.w = 0.f;
+    return ve;
 }
 
 // ============================================================================ K2 small (k <= 32)
+// Warp <-> pack of np same-k landmarks; group of G lanes <-> landmark; lane o <-> observation o
+// and camera block o.  Per-group shared memory: VR (2G+3 float4) + GM (18, padded to 20).
 template <int G>
 struct SmallTab {
     static constexpr int VR = 4 * (2 * G + 3);
-    static constexpr int MC = 4 * 9 * G;
-    static constexpr int JP = 9 * 2 * G;
-    static constexpr int GM = 20;
-    static constexpr int FLOATS = VR + MC + JP + GM;
+    static constexpr int FLOATS = VR + 20;
 };
 
 template <int G>
-__global__ void __launch_bounds__(128) k_marg_small(DevProblem d, int64_t lm_lo, int64_t lm_hi, float lam, float dmin,
+__global__ void __launch_bounds__(128) k_marg_small(DevProblem d, int64_t pk_lo, int64_t pk_hi, float lam, float dmin,
                                                     float dmax) {
     constexpr int NG = 32 / G;
     using TB = SmallTab<G>;
@@ -357,15 +327,16 @@ __global__ void __launch_bounds__(128) k_marg_small(DevProblem d, int64_t lm_lo,
     float *smem = reinterpret_cast<float *>(smem4);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int grp = lane / G, gl = lane % G;
-    const int64_t j = lm_lo + ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * NG + grp;
-    const bool valid = j < lm_hi;
-    const int k = valid ? d.lm_k[j] : 0;
-    const bool act = gl < k;
+    const int64_t pi = pk_lo + (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    if (pi >= pk_hi) return;  // warp-uniform
+    const Pack pack = d.packs[pi];
+    const bool valid = grp < pack.np;
+    const int64_t j = pack.lm0 + (valid ? grp : 0);
+    const int k = d.lm_k[pack.lm0];
+    const bool act = valid && gl < k;
     float *tab = smem + (warp * NG + grp) * TB::FLOATS;
     float4 *VR = reinterpret_cast<float4 *>(tab);
-    float4 *MC = reinterpret_cast<float4 *>(tab + TB::VR);
-    float *JP = tab + TB::VR + TB::MC;
-    float *GM = JP + TB::JP;
+    float *GM = tab + TB::VR;
 
     // ---- per-observation Jacobians (lane gl <-> observation gl; rows 2gl, 2gl+1)
     float r[2] = {0.f, 0.f}, Jc[18], Jl[6];
@@ -391,12 +362,13 @@ __global__ void __launch_bounds__(128) k_marg_small(DevProblem d, int64_t lm_lo,
         sl[q] = 1.f / (1.f + sqrtf(n2));
         Dl[q] = sqrtf(fminf(fmaxf(n2 * sl[q] * sl[q], dmin), dmax));
     }
-    float Jp[2][9], X[2][3], rv[2] = {r[0], r[1]};
+    BlockWY B;
+    float X[2][3], rv[2] = {r[0], r[1]};
 #pragma unroll
     for (int q = 0; q < 9; q++) {
         const float s = act ? d.sp[9 * cam + q] : 0.f;
-        Jp[0][q] = Jc[q] * s;
-        Jp[1][q] = Jc[9 + q] * s;
+        B.jp[0][q] = Jc[q] * s;
+        B.jp[1][q] = Jc[9 + q] * s;
     }
 #pragma unroll
     for (int q = 0; q < 3; q++) {
@@ -460,17 +432,9 @@ __global__ void __launch_bounds__(128) k_marg_small(DevProblem d, int64_t lm_lo,
     const float T01 = -tau[1] * T00 * p01;
     const float T02 = -tau[2] * (T00 * p02 + T01 * p12);
     const float T12 = -tau[2] * T11 * p12;
-    // ---- M = T^T V^T J_p for this lane's camera block (o = gl)
+    wy_m(B, make_float4(V[0][0], V[0][1], V[0][2], 0.f), make_float4(V[1][0], V[1][1], V[1][2], 0.f), T00, T01,
+         T02, T11, T12, T22);
     if (act) {
-#pragma unroll
-        for (int q = 0; q < 9; q++) {
-            const float W0 = V[0][0] * Jp[0][q] + V[1][0] * Jp[1][q];
-            const float W1 = V[0][1] * Jp[0][q] + V[1][1] * Jp[1][q];
-            const float W2 = V[0][2] * Jp[0][q] + V[1][2] * Jp[1][q];
-            MC[9 * gl + q] = make_float4(T00 * W0, T01 * W0 + T11 * W1, T02 * W0 + T12 * W1 + T22 * W2, 0.f);
-            JP[(2 * gl) * 9 + q] = Jp[0][q];
-            JP[(2 * gl + 1) * 9 + q] = Jp[1][q];
-        }
 #pragma unroll
         for (int rr = 0; rr < 2; rr++) {
             const int a = 2 * gl + rr;
@@ -497,31 +461,35 @@ __global__ void __launch_bounds__(128) k_marg_small(DevProblem d, int64_t lm_lo,
     damp_rotations(R, rr3, sD, L6, Gm, rr6, g);
     if (valid && gl == 0) {
 #pragma unroll
-        for (int s = 0; s < 6; s++) {
-            float4 ve;
-            ve.x = Gm[s * 3] * V3[0] + Gm[s * 3 + 1] * V3[3] + Gm[s * 3 + 2] * V3[6];
-            ve.y = Gm[s * 3] * V3[1] + Gm[s * 3 + 1] * V3[4] + Gm[s * 3 + 2] * V3[7];
-            ve.z = Gm[s * 3] * V3[2] + Gm[s * 3 + 1] * V3[5] + Gm[s * 3 + 2] * V3[8];
-            ve.w = 0.f;
-            VR[s < 3 ? s : 2 * k + s - 3] = ve;
-        }
+        for (int s = 0; s < 6; s++) VR[s < 3 ? s : 2 * k + s - 3] = veff(Gm, V3, s);
 #pragma unroll
         for (int i = 0; i < 18; i++) GM[i] = Gm[i];
     }
     __syncwarp();
-    if (!valid) return;
-    // ---- emission (write-only stream, Fig. 2c)
-    MargTables Tb{VR, MC, JP, GM};
+    if (!act) return;
+    // ---- emission (write-only stream, Fig. 2c) in the pack layout
     float *blk_side = d.arena + d.lm_side[j];
-    emit_r2(Tb, k, d.arena + d.lm_r2[j], 0, r2_floats(k), gl, G);
-    emit_r1(Tb, k, blk_side, gl, G);
-    float4 *TL = reinterpret_cast<float4 *>(blk_side + side_tl(k));
-    if (act) {
+    float2 *A = reinterpret_cast<float2 *>(d.arena + pack.base);
+    const int npk = pack.np * k, mo = grp * k + gl;
+    for (int p = 0; p < k; p++) {
+        float v18[18];
+        wy_row(B, VR, GM, k, 2 * p + 3, gl, v18);
+        wy_row(B, VR, GM, k, 2 * p + 4, gl, v18 + 9);
 #pragma unroll
-        for (int rr = 0; rr < 2; rr++) {
-            const int a = 2 * gl + rr;
-            if (a >= 3) TL[a] = make_float4(0.f, 0.f, 0.f, rv[rr]);
-        }
+        for (int c = 0; c < 9; c++) A[(p * 9 + c) * npk + mo] = make_float2(v18[2 * c], v18[2 * c + 1]);
+    }
+#pragma unroll
+    for (int s = 0; s < 3; s++) {
+        float v9[9];
+        wy_row(B, VR, GM, k, s, gl, v9);
+#pragma unroll
+        for (int q = 0; q < 9; q++) blk_side[s * 9 * k + 9 * gl + q] = v9[q];
+    }
+    float4 *TL = reinterpret_cast<float4 *>(blk_side + side_tl(k));
+#pragma unroll
+    for (int rr = 0; rr < 2; rr++) {
+        const int a = 2 * gl + rr;
+        if (a >= 3) TL[a] = make_float4(0.f, 0.f, 0.f, rv[rr]);
     }
     if (gl == 0) {
 #pragma unroll
@@ -541,48 +509,50 @@ __global__ void __launch_bounds__(128) k_marg_small(DevProblem d, int64_t lm_lo,
 }
 
 // ============================================================================ K2 large (k > 32)
-// One CTA per (landmark, tile range).  The O(k) prologue (Jacobians, Householder, WY tables) is
-// recomputed by every CTA of a landmark; the O(k^2) emission is split across CTAs.
-__global__ void __launch_bounds__(256) k_marg_large(DevProblem d, const LargeItem *__restrict__ items, float lam,
-                                                    float dmin, float dmax) {
+// CTA of NT >= k threads per (landmark, tile range); thread o <-> observation o and camera
+// block o.  The O(k) prologue (Jacobians, Householder, WY) is recomputed by every CTA of a
+// landmark; the O(k^2) emission is split across CTAs (~1 MB each).
+template <int NT>
+__global__ void __launch_bounds__(NT) k_marg_large(DevProblem d, const LargeItem *__restrict__ items, float lam,
+                                                   float dmin, float dmax) {
     extern __shared__ float4 smem4[];
-    float *smem = reinterpret_cast<float *>(smem4);
     __shared__ float red[32 * 4];
     __shared__ float piv[4];
+    __shared__ float GM[20];
     const LargeItem it = items[blockIdx.x];
     const int64_t j = it.lm;
     const int k = d.lm_k[j];
-    const int tid = threadIdx.x, nt = blockDim.x;
-    float4 *VR = reinterpret_cast<float4 *>(smem);                 // 2k+3
-    float4 *MC = VR + (2 * k + 3);                                  // 9k
-    float *JP = reinterpret_cast<float *>(MC + 9 * k);              // 18k
-    float *SX = JP + 18 * k;                                        // 2k x 3 (landmark Jacobian)
-    float *SR = SX + 6 * k;                                         // 2k residuals
-    float *GM = SR + 2 * k;                                         // 18 (+2 pad)
+    const int tid = threadIdx.x;
+    const bool own = tid < k;
+    float4 *VR = smem4;                                         // 2k+3
+    float *SX = reinterpret_cast<float *>(VR + (2 * k + 3));    // 2k x 3 landmark Jacobian
+    float *SR = SX + 6 * k;                                     // 2k residuals
     const int64_t obs0 = d.lm_obs0[j];
     const float *Xp = d.pts + 3 * j;
-    const float P0 = Xp[0], P1 = Xp[1], P2 = Xp[2];
+    BlockWY B;
     float n2[3] = {0.f, 0.f, 0.f};
-    for (int i = tid; i < k; i += nt) {
-        const int cam = d.obs_cam[obs0 + i];
+#pragma unroll
+    for (int q = 0; q < 9; q++) B.jp[0][q] = B.jp[1][q] = 0.f;
+    if (own) {
+        const int cam = d.obs_cam[obs0 + tid];
         float c[9], r[2], Jc[18], Jl[6];
         load_cam(d.cams, cam, c);
-        const float2 uv = d.obs_uv[obs0 + i];
-        cam_model(c, P0, P1, P2, uv.x, uv.y, r, Jc, Jl);
+        const float2 uv = d.obs_uv[obs0 + tid];
+        cam_model(c, Xp[0], Xp[1], Xp[2], uv.x, uv.y, r, Jc, Jl);
 #pragma unroll
         for (int q = 0; q < 9; q++) {
             const float s = d.sp[9 * cam + q];
-            JP[(2 * i) * 9 + q] = Jc[q] * s;
-            JP[(2 * i + 1) * 9 + q] = Jc[9 + q] * s;
+            B.jp[0][q] = Jc[q] * s;
+            B.jp[1][q] = Jc[9 + q] * s;
         }
 #pragma unroll
         for (int q = 0; q < 3; q++) {
-            SX[(2 * i) * 3 + q] = Jl[q];
-            SX[(2 * i + 1) * 3 + q] = Jl[3 + q];
-            n2[q] += Jl[q] * Jl[q] + Jl[3 + q] * Jl[3 + q];
+            SX[(2 * tid) * 3 + q] = Jl[q];
+            SX[(2 * tid + 1) * 3 + q] = Jl[3 + q];
+            n2[q] = Jl[q] * Jl[q] + Jl[3 + q] * Jl[3 + q];
         }
-        SR[2 * i] = r[0];
-        SR[2 * i + 1] = r[1];
+        SR[2 * tid] = r[0];
+        SR[2 * tid + 1] = r[1];
     }
     block_sum<3>(n2, red);
     float sl[3], Dl[3];
@@ -591,15 +561,16 @@ __global__ void __launch_bounds__(256) k_marg_large(DevProblem d, const LargeIte
         sl[q] = 1.f / (1.f + sqrtf(n2[q]));
         Dl[q] = sqrtf(fminf(fmaxf(n2[q] * sl[q] * sl[q], dmin), dmax));
     }
-    for (int a = tid; a < 2 * k; a += nt)
+    for (int a = tid; a < 2 * k; a += NT)
 #pragma unroll
         for (int q = 0; q < 3; q++) SX[a * 3 + q] *= sl[q];
     __syncthreads();
     // Householder, 3 reflectors; V kept in VR rows (all rows 0..2k-1 during the prologue)
     float tau[3];
+#pragma unroll
     for (int c = 0; c < 3; c++) {
         float s[4] = {0.f, 0.f, 0.f, 0.f};
-        for (int a = c + tid; a < 2 * k; a += nt) {
+        for (int a = c + tid; a < 2 * k; a += NT) {
             const float x = SX[a * 3 + c];
             s[0] += x * x;
             if (c + 1 < 3) s[1] += x * SX[a * 3 + c + 1];
@@ -620,7 +591,7 @@ __global__ void __launch_bounds__(256) k_marg_large(DevProblem d, const LargeIte
         const float tc = vtv > 0.f ? 2.f / vtv : 0.f;
         tau[c] = tc;
         const float d1 = s[1] - alpha * y1, d2 = s[2] - alpha * y2, dr = s[3] - alpha * yr;
-        for (int a = tid; a < 2 * k; a += nt) {
+        for (int a = tid; a < 2 * k; a += NT) {
             float vv = 0.f;
             if (a >= c) vv = (a == c) ? x0 - alpha : SX[a * 3 + c];
             float *vr = reinterpret_cast<float *>(VR + a);
@@ -635,7 +606,7 @@ __global__ void __launch_bounds__(256) k_marg_large(DevProblem d, const LargeIte
         __syncthreads();
     }
     float p[3] = {0.f, 0.f, 0.f};
-    for (int a = tid; a < 2 * k; a += nt) {
+    for (int a = tid; a < 2 * k; a += NT) {
         const float4 v = VR[a];
         p[0] += v.x * v.y;
         p[1] += v.x * v.z;
@@ -646,15 +617,7 @@ __global__ void __launch_bounds__(256) k_marg_large(DevProblem d, const LargeIte
     const float T01 = -tau[1] * T00 * p[0];
     const float T02 = -tau[2] * (T00 * p[1] + T01 * p[2]);
     const float T12 = -tau[2] * T11 * p[2];
-    for (int o = tid; o < k; o += nt) {
-        const float4 v0 = VR[2 * o], v1 = VR[2 * o + 1];
-#pragma unroll
-        for (int q = 0; q < 9; q++) {
-            const float j0 = JP[(2 * o) * 9 + q], j1 = JP[(2 * o + 1) * 9 + q];
-            const float W0 = v0.x * j0 + v1.x * j1, W1 = v0.y * j0 + v1.y * j1, W2 = v0.z * j0 + v1.z * j1;
-            MC[9 * o + q] = make_float4(T00 * W0, T01 * W0 + T11 * W1, T02 * W0 + T12 * W1 + T22 * W2, 0.f);
-        }
-    }
+    if (own) wy_m(B, VR[2 * tid], VR[2 * tid + 1], T00, T01, T02, T11, T12, T22);
     // damping (every thread computes the 6 rotations redundantly from smem values)
     float R[9], rr3[3], V3[9];
 #pragma unroll
@@ -670,27 +633,44 @@ __global__ void __launch_bounds__(256) k_marg_large(DevProblem d, const LargeIte
     float L6[18], Gm[18], rr6[6], g[12];
     damp_rotations(R, rr3, sD, L6, Gm, rr6, g);
     __syncthreads();  // all reads of VR rows 0..2 done
-    if (tid < 6) {
-        const int s = tid;
-        float4 ve;
-        ve.x = Gm[s * 3] * V3[0] + Gm[s * 3 + 1] * V3[3] + Gm[s * 3 + 2] * V3[6];
-        ve.y = Gm[s * 3] * V3[1] + Gm[s * 3 + 1] * V3[4] + Gm[s * 3 + 2] * V3[7];
-        ve.z = Gm[s * 3] * V3[2] + Gm[s * 3 + 1] * V3[5] + Gm[s * 3 + 2] * V3[8];
-        ve.w = 0.f;
-        VR[s < 3 ? s : 2 * k + s - 3] = ve;
-    }
+    if (tid < 6) VR[tid < 3 ? tid : 2 * k + tid - 3] = veff(Gm, V3, tid);
     if (tid < 18) GM[tid] = Gm[tid];
     __syncthreads();
-    MargTables Tb{VR, MC, JP, GM};
-    const int T_ = n_tiles(k);
-    const int64_t e_lo = tile_off(k, it.t0);
-    const int64_t e_hi = it.t1 >= T_ ? r2_floats(k) : tile_off(k, it.t1);
-    emit_r2(Tb, k, d.arena + d.lm_r2[j], e_lo, e_hi, tid, nt);
+    if (own) {
+        const int o = tid, g_ = o >> 5, ng = min(32, k - 32 * g_);
+        float *R2 = d.arena + d.lm_r2[j];
+        for (int t = it.t0; t < it.t1; t++) {
+            float4 *S = reinterpret_cast<float4 *>(R2 + (int64_t)36 * k * t + 36 * 32 * g_) + (o & 31);
+            float v36[36];
+#pragma unroll
+            for (int rr = 0; rr < 4; rr++) {
+                const int a = 4 * t + rr;
+                if (a < 2 * k) {
+                    wy_row(B, VR, GM, k, a + 3, o, v36 + 9 * rr);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 9; q++) v36[9 * rr + q] = 0.f;
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < 9; c++)
+                S[c * ng] = make_float4(v36[4 * c], v36[4 * c + 1], v36[4 * c + 2], v36[4 * c + 3]);
+        }
+        if (it.t0 == 0) {
+            float *side = d.arena + d.lm_side[j];
+#pragma unroll
+            for (int s = 0; s < 3; s++) {
+                float v9[9];
+                wy_row(B, VR, GM, k, s, o, v9);
+#pragma unroll
+                for (int q = 0; q < 9; q++) side[s * 9 * k + 9 * o + q] = v9[q];
+            }
+        }
+    }
     if (it.t0 == 0) {
         float *side = d.arena + d.lm_side[j];
-        emit_r1(Tb, k, side, tid, nt);
         float4 *TL = reinterpret_cast<float4 *>(side + side_tl(k));
-        for (int a = 3 + tid; a < 2 * k; a += nt) TL[a] = make_float4(0.f, 0.f, 0.f, SR[a]);
+        for (int a = 3 + tid; a < 2 * k; a += NT) TL[a] = make_float4(0.f, 0.f, 0.f, SR[a]);
         if (tid < 3) {
             const int s = tid;
             TL[s] = make_float4(L6[s * 3], L6[s * 3 + 1], L6[s * 3 + 2], rr6[s]);
@@ -712,6 +692,7 @@ __global__ void __launch_bounds__(256) k_redamp(DevProblem d, float lam) {
     const int k = d.lm_k[j];
     float *side = d.arena + d.lm_side[j];
     float *r2 = d.arena + d.lm_r2[j];
+    const int32_t pk = d.lm_pk[j];
     float4 *TL = reinterpret_cast<float4 *>(side + side_tl(k));
     float *gp = side + side_g(k);
     float g[12];
@@ -756,7 +737,7 @@ __global__ void __launch_bounds__(256) k_redamp(DevProblem d, float lam) {
 #pragma unroll
         for (int s = 0; s < 3; s++) {
             x[s] = side[s * W + c];
-            idx[s] = r2_index(k, 2 * k - 3 + s, o, q);
+            idx[s] = r2_index(k, pk, 2 * k - 3 + s, o, q);
             x[3 + s] = r2[idx[s]];
         }
 #pragma unroll
@@ -786,41 +767,58 @@ __global__ void __launch_bounds__(256) k_redamp(DevProblem d, float lam) {
 }
 
 // ============================================================================ K4 preconditioner + rhs
-// Thread per (landmark, camera block o): P_o = sum_a A[a,o,:]^T A[a,o,:] (45 upper entries) and
-// b_o = sum_a A[a,o,:] q_a, accumulated into the camera's 54-float slot.
-__global__ void __launch_bounds__(256) k_precond_rhs(DevProblem d) {
-    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= d.n_obs) return;
-    const int64_t j = d.obs_lm[g];
-    const int k = d.lm_k[j];
-    const int o = (int)(g - d.lm_obs0[j]);
-    const int cam = d.obs_cam[g];
-    const float *r2 = d.arena + d.lm_r2[j];
+// P_i = sum_j A_j[:,i]^T A_j[:,i] (45 upper entries) and b~_i = sum_j A_j[:,i]^T q_j (P:348,
+// P:647-648): every thread owns one camera block of one landmark, streams its slabs (the same
+// coalesced loads as the matvec), accumulates 54 values in registers and adds them to the
+// camera's slot once.
+__device__ __forceinline__ void acc_rows(float *P, float *b, const float *row, float qa) {
+    int idx = 0;
+#pragma unroll
+    for (int q1 = 0; q1 < 9; q1++) {
+        b[q1] += row[q1] * qa;
+#pragma unroll
+        for (int q2 = q1; q2 < 9; q2++) P[idx++] += row[q1] * row[q2];
+    }
+}
+__device__ __forceinline__ void flush54(float *acc, const float *P, const float *b) {
+#pragma unroll
+    for (int i = 0; i < 45; i++) atomicAdd(acc + i, P[i]);
+#pragma unroll
+    for (int i = 0; i < 9; i++) atomicAdd(acc + 45 + i, b[i]);
+}
+
+__device__ __forceinline__ int group_of_k(int k) { return k <= 4 ? 4 : (k <= 8 ? 8 : (k <= 16 ? 16 : 32)); }
+
+__global__ void __launch_bounds__(128) k_precond_small(DevProblem d, int64_t n_packs) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t pi = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    if (pi >= n_packs) return;
+    const Pack pack = d.packs[pi];
+    const int k = d.lm_k[pack.lm0];
+    const int G = group_of_k(k);
+    const int m = lane / G, o = lane % G;
+    if (m >= pack.np || o >= k) return;
+    const int64_t j = pack.lm0 + m;
+    const float2 *A = reinterpret_cast<const float2 *>(d.arena + pack.base);
     const float4 *TL = reinterpret_cast<const float4 *>(d.arena + d.lm_side[j] + side_tl(k));
+    const int npk = pack.np * k, mo = m * k + o;
     float P[45], b[9];
 #pragma unroll
     for (int i = 0; i < 45; i++) P[i] = 0.f;
 #pragma unroll
     for (int i = 0; i < 9; i++) b[i] = 0.f;
-    for (int a = 0; a < 2 * k; a++) {
-        const float *row = r2 + r2_index(k, a, o, 0);
-        float v[9];
+    for (int p = 0; p < k; p++) {
+        float sl[18];
 #pragma unroll
-        for (int q = 0; q < 9; q++) v[q] = row[q];
-        const float qa = TL[a + 3].w;
-        int idx = 0;
-#pragma unroll
-        for (int q1 = 0; q1 < 9; q1++) {
-            b[q1] += v[q1] * qa;
-#pragma unroll
-            for (int q2 = q1; q2 < 9; q2++) P[idx++] += v[q1] * v[q2];
+        for (int c = 0; c < 9; c++) {
+            const float2 v = __ldg(A + (p * 9 + c) * npk + mo);
+            sl[2 * c] = v.x;
+            sl[2 * c + 1] = v.y;
         }
+        acc_rows(P, b, sl, TL[3 + 2 * p].w);
+        acc_rows(P, b, sl + 9, TL[4 + 2 * p].w);
     }
-    float *acc = d.pacc + 54 * (int64_t)cam;
-#pragma unroll
-    for (int i = 0; i < 45; i++) atomicAdd(acc + i, P[i]);
-#pragma unroll
-    for (int i = 0; i < 9; i++) atomicAdd(acc + 45 + i, b[i]);
+    flush54(d.pacc + 54 * (int64_t)d.obs_cam[d.lm_obs0[j] + o], P, b);
 }
 
 // per camera: P_i + lambda D_p^2 -> Cholesky (FP64) -> inverse M^-1 (FP32, 81); b~ copied out.
@@ -873,147 +871,266 @@ __global__ void k_precond_finalize(DevProblem d, float lam, double *bad) {
 }
 
 // ============================================================================ K5 matvec
-// small (k <= 32): warp-group of G lanes per landmark.  Pass 1 streams A_j once from HBM with
-// coalesced float4 loads (y = A_j v_j, row runs accumulated in registers then in shared memory);
-// pass 2 re-reads A_j (L1-resident) column-wise: out_c = A_j[:,c]^T y.
-template <int G>
-__global__ void __launch_bounds__(128) k_matvec_small(DevProblem d, int64_t lm_lo, int64_t lm_hi,
-                                                      const float *__restrict__ v, float *__restrict__ out,
-                                                      const PcgState *__restrict__ st) {
+// H~ v = sum_j A_j^T (A_j v_j) (Eq. cg_mult).  A_j is read from HBM exactly once: each
+// thread holds the slab of one camera block o (2 or 4 rows x 9) in registers, forms its partial
+// of y = A v for the slab rows, the partials of a row are summed over the landmark's blocks
+// (warp shuffles for small k, a per-slot named barrier for large k), and out_o += slab^T y
+// accumulates in registers; the 9 entries of out_o are added to the camera vector once per
+// landmark (per CTA range for large k).
+
+__device__ __forceinline__ float group_sum_rt(float v, int G) {
+    for (int m = G >> 1; m; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m, G);
+    return v;
+}
+__device__ __forceinline__ int group_of(int k) { return k <= 4 ? 4 : (k <= 8 ? 8 : (k <= 16 ? 16 : 32)); }
+
+// small k: warp <-> pack of np same-k landmarks; lane <-> (m = lane / G, o = lane % G).  One launch
+// for all packs; the next row pair's slab is prefetched while the current one is reduced.
+__global__ void __launch_bounds__(128) k_matvec_small(DevProblem d, int64_t n_packs, const float *__restrict__ v,
+                                                      float *__restrict__ out, const PcgState *__restrict__ st) {
     if (st && st->done) return;
-    constexpr int NG = 32 / G;
-    __shared__ float sv[4][NG][9 * G];
-    __shared__ float sy[4][NG][2 * G];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int grp = lane / G, gl = lane % G;
-    const int64_t j = lm_lo + ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * NG + grp;
-    const bool valid = j < lm_hi;
-    const int k = valid ? d.lm_k[j] : 0;
-    float *vl = sv[warp][grp];
-    float *y = sy[warp][grp];
+    const int64_t pi = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    if (pi >= n_packs) return;  // warp-uniform
+    const Pack pack = d.packs[pi];
+    const int k = d.lm_k[pack.lm0];
+    const int G = group_of(k);
+    const int m = lane / G, o = lane % G;
+    const bool valid = m < pack.np && o < k;
+    const int npk = pack.np * k, mo = m * k + o;
+    const float2 *A = reinterpret_cast<const float2 *>(d.arena + pack.base) + mo;
+    float vo[9], acc[9];
     int cam = 0;
-    if (gl < k) {
-        cam = d.obs_cam[d.lm_obs0[j] + gl];
-#pragma unroll
-        for (int q = 0; q < 9; q++) vl[9 * gl + q] = v[9 * cam + q];
-        y[2 * gl] = 0.f;
-        y[2 * gl + 1] = 0.f;
-    }
-    __syncwarp();
-    const float *A = valid ? d.arena + d.lm_r2[j] : d.arena;
-    const int n = 18 * k * k;
-    const int W = 18 * k;  // floats per camera block (2k rows x 9)
     if (valid) {
-        const float invW = 1.f / (float)W;
-        for (int e4 = 4 * gl; e4 < n; e4 += 4 * G) {
-            const float4 a4 = __ldg(reinterpret_cast<const float4 *>(A + e4));
-            const float av[4] = {a4.x, a4.y, a4.z, a4.w};
-            int o = __float2int_rd(((float)e4 + 0.5f) * invW);
-            int rem = e4 - o * W;
-            int row = (rem * 7282) >> 16;
-            int q = rem - 9 * row;
-            float run = 0.f;
-            int run_row = row;
+        cam = d.obs_cam[d.lm_obs0[pack.lm0 + m] + o];
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
-                if (e4 + u < n) {
-                    if (row != run_row) {
-                        atomicAdd(y + run_row, run);
-                        run = 0.f;
-                        run_row = row;
-                    }
-                    run += av[u] * vl[9 * o + q];
-                }
-                if (++q == 9) {
-                    q = 0;
-                    if (++row == 2 * k) row = 0, ++o;
-                }
-            }
-            atomicAdd(y + run_row, run);
-        }
+        for (int q = 0; q < 9; q++) vo[q] = __ldg(v + 9 * cam + q);
+    } else {
+#pragma unroll
+        for (int q = 0; q < 9; q++) vo[q] = 0.f;
     }
-    __syncwarp();
-    if (valid) {
-        for (int c = gl; c < 9 * k; c += G) {
-            const int o = c / 9, q = c - 9 * o;
-            const float *col = A + o * W + q;
-            float acc = 0.f;
-            for (int a = 0; a < 2 * k; a++) acc += col[9 * a] * y[a];
-            atomicAdd(out + 9 * d.obs_cam[d.lm_obs0[j] + o] + q, acc);
+#pragma unroll
+    for (int q = 0; q < 9; q++) acc[q] = 0.f;
+    float2 cur[9], nxt[9];
+#pragma unroll
+    for (int c = 0; c < 9; c++) cur[c] = valid ? __ldg(A + c * npk) : make_float2(0.f, 0.f);
+    for (int p = 0; p < k; p++) {
+        if (p + 1 < k) {
+#pragma unroll
+            for (int c = 0; c < 9; c++) nxt[c] = valid ? __ldg(A + ((p + 1) * 9 + c) * npk) : make_float2(0.f, 0.f);
         }
+        const float *sl = reinterpret_cast<const float *>(cur);
+        float y0 = 0.f, y1 = 0.f;
+#pragma unroll
+        for (int q = 0; q < 9; q++) {
+            y0 += sl[q] * vo[q];
+            y1 += sl[9 + q] * vo[q];
+        }
+        y0 = group_sum_rt(y0, G);
+        y1 = group_sum_rt(y1, G);
+#pragma unroll
+        for (int q = 0; q < 9; q++) acc[q] += sl[q] * y0 + sl[9 + q] * y1;
+#pragma unroll
+        for (int c = 0; c < 9; c++) cur[c] = nxt[c];
+    }
+    if (valid) {
+#pragma unroll
+        for (int q = 0; q < 9; q++) atomicAdd(out + 9 * cam + q, acc[q]);
     }
 }
 
-// large (k > 32): CTA per (landmark, tile range); per tile y (<= 4 rows) by a block reduction,
-// then out_c accumulated in registers across the CTA's tiles and flushed once.
-constexpr int MV_MAXC = (9 * KMAX + 255) / 256;
-__global__ void __launch_bounds__(256) k_matvec_large(DevProblem d, const LargeItem *__restrict__ items,
-                                                      const float *__restrict__ v, float *__restrict__ out,
-                                                      const PcgState *__restrict__ st) {
-    if (st && st->done) return;
-    extern __shared__ float4 smem4[];
-    float *vl = reinterpret_cast<float *>(smem4);
-    __shared__ float red[32 * 4];
-    const LargeItem it = items[blockIdx.x];
-    const int64_t j = it.lm;
-    const int k = d.lm_k[j];
-    const int tid = threadIdx.x, nt = blockDim.x;
-    const int64_t obs0 = d.lm_obs0[j];
-    for (int c = tid; c < 9 * k; c += nt) {
-        const int o = c / 9;
-        vl[c] = v[9 * d.obs_cam[obs0 + o] + (c - 9 * o)];
+// ---- TMA bulk-copy pipeline for large k (B200: cp.async.bulk + mbarrier, one CTA per SM).
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+template <int NS, int NSLOT>
+struct PipeCfg {
+    static constexpr int NC = NS * NSLOT;           // consumer threads
+    static constexpr int TB = 144 * NS;             // bytes of the largest tile (k <= NS)
+    static constexpr int SB = TB * NSLOT;           // stage bytes
+    static constexpr int STAGES = (200 * 1024) / SB > 8 ? 8 : (200 * 1024) / SB;
+    static constexpr size_t SMEM = (size_t)STAGES * SB + 2 * STAGES * sizeof(uint64_t);
+};
+
+// Consumer slot s of NSLOT processes tiles lo + i*NSLOT + s; NS threads per slot <-> camera blocks.
+// PRECOND = false: matvec (K5); true: block-Jacobi blocks + rhs (K4).
+template <int NS, int NSLOT, bool PRECOND>
+__global__ void __launch_bounds__(NS *NSLOT + 32, 1)
+    k_large_pipe(DevProblem d, const TileRef *__restrict__ tiles, const int64_t *__restrict__ cta_lo,
+                 const float *__restrict__ v, float *__restrict__ out, const PcgState *__restrict__ st) {
+    using C = PipeCfg<NS, NSLOT>;
+    if (!PRECOND && st && st->done) return;
+    extern __shared__ __align__(128) unsigned char sm[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(sm + (size_t)C::STAGES * C::SB);
+    uint64_t *empty = full + C::STAGES;
+    __shared__ float red[2][C::NC / 32][4];
+    const int tid = threadIdx.x;
+    const int64_t lo = cta_lo[blockIdx.x], hi = cta_lo[blockIdx.x + 1];
+    const int64_t nst = (hi - lo + NSLOT - 1) / NSLOT;
+    if (tid == 0) {
+        for (int s = 0; s < C::STAGES; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], C::NC / 32);
+        }
+        fence_mbar_init();
     }
     __syncthreads();
-    float acc[MV_MAXC];
-#pragma unroll
-    for (int i = 0; i < MV_MAXC; i++) acc[i] = 0.f;
-    const float *A = d.arena + d.lm_r2[j];
-    for (int t = it.t0; t < it.t1; t++) {
-        const int h = tile_rows(k, t);
-        const float *At = A + tile_off(k, t);
-        const int n = 9 * k * h;
-        float yp[4] = {0.f, 0.f, 0.f, 0.f};
-        const int bw = 9 * h;
-        for (int e4 = 4 * tid; e4 < n; e4 += 4 * nt) {
-            const float4 a4 = __ldg(reinterpret_cast<const float4 *>(At + e4));
-            const float av[4] = {a4.x, a4.y, a4.z, a4.w};
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                const int e = e4 + u;
-                if (e < n) {
-                    const int o = e / bw;
-                    const int rem = e - o * bw;
-                    const int row = (rem * 7282) >> 16;
-                    const int q = rem - 9 * row;
-                    const float pr = av[u] * vl[9 * o + q];
-                    yp[0] += row == 0 ? pr : 0.f;
-                    yp[1] += row == 1 ? pr : 0.f;
-                    yp[2] += row == 2 ? pr : 0.f;
-                    yp[3] += row == 3 ? pr : 0.f;
+    if (tid >= C::NC) {  // ---------------- producer warp: one elected lane streams the tiles
+        if (tid == C::NC) {
+            for (int64_t i = 0; i < nst; i++) {
+                const int s = (int)(i % C::STAGES);
+                const uint32_t ph = (uint32_t)((i / C::STAGES) & 1);
+                mbar_wait(&empty[s], ph ^ 1);
+                uint32_t total = 0;
+                for (int sl = 0; sl < NSLOT; sl++) {
+                    const int64_t ti = lo + i * NSLOT + sl;
+                    if (ti < hi) total += 144u * (uint32_t)d.lm_k[tiles[ti].lm];
+                }
+                mbar_arrive_expect_tx(&full[s], total);
+                for (int sl = 0; sl < NSLOT; sl++) {
+                    const int64_t ti = lo + i * NSLOT + sl;
+                    if (ti < hi) {
+                        const TileRef tr = tiles[ti];
+                        const int k = d.lm_k[tr.lm];
+                        const float *src = d.arena + d.lm_r2[tr.lm] + (int64_t)36 * k * tr.t;
+                        bulk_g2s(sm + (size_t)s * C::SB + (size_t)sl * C::TB, src, 144u * (uint32_t)k, &full[s]);
+                    }
                 }
             }
         }
-        block_sum<4>(yp, red);
+        return;
+    }
+    // ---------------- consumers
+    const int slot = tid / NS, o = tid % NS, lane = tid & 31, warp = tid >> 5;
+    constexpr int NWS = NS / 32;
+    int cur = -1, k = 0, cam = 0, ng = 1, g = 0;
+    bool valid = false;
+    const float4 *TL = nullptr;
+    float vo[9], acc[9], P[PRECOND ? 45 : 1], b[PRECOND ? 9 : 1];
 #pragma unroll
-        for (int i = 0; i < MV_MAXC; i++) {
-            const int c = tid + i * nt;
-            if (c < 9 * k) {
-                const int o = c / 9, q = c - 9 * o;
-                const float *col = At + o * bw + q;
-                float s = 0.f;
-                for (int a = 0; a < h; a++) s += col[9 * a] * yp[a];
-                acc[i] += s;
+    for (int q = 0; q < 9; q++) vo[q] = 0.f, acc[q] = 0.f;
+    auto flush = [&]() {
+        if (cur < 0 || !valid) return;
+        if (PRECOND) {
+            flush54(d.pacc + 54 * (int64_t)cam, P, b);
+        } else {
+#pragma unroll
+            for (int q = 0; q < 9; q++) atomicAdd(out + 9 * cam + q, acc[q]);
+        }
+    };
+    int buf = 0;
+    for (int64_t i = 0; i < nst; i++) {
+        const int s = (int)(i % C::STAGES);
+        const uint32_t ph = (uint32_t)((i / C::STAGES) & 1);
+        const int64_t ti = lo + i * NSLOT + slot;
+        const bool have = ti < hi;  // uniform over the slot
+        TileRef tr{-1, 0};
+        if (have) {
+            tr = tiles[ti];
+            if (tr.lm != cur) {
+                flush();
+                cur = tr.lm;
+                k = d.lm_k[cur];
+                valid = o < k;
+                g = o >> 5;
+                ng = valid ? min(32, k - 32 * g) : 1;
+                if (valid) cam = d.obs_cam[d.lm_obs0[cur] + o];
+#pragma unroll
+                for (int q = 0; q < 9; q++) vo[q] = (PRECOND || !valid) ? 0.f : __ldg(v + 9 * cam + q);
+                if (PRECOND) {
+                    TL = reinterpret_cast<const float4 *>(d.arena + d.lm_side[cur] + side_tl(k));
+#pragma unroll
+                    for (int q = 0; q < 45; q++) P[q] = 0.f;
+#pragma unroll
+                    for (int q = 0; q < 9; q++) b[q] = 0.f;
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 9; q++) acc[q] = 0.f;
+                }
             }
         }
-    }
+        mbar_wait(&full[s], ph);
+        float sl[36];
+        if (have && valid) {
+            const float4 *S4 =
+                reinterpret_cast<const float4 *>(sm + (size_t)s * C::SB + (size_t)slot * C::TB) + 288 * g + (o & 31);
 #pragma unroll
-    for (int i = 0; i < MV_MAXC; i++) {
-        const int c = tid + i * nt;
-        if (c < 9 * k) {
-            const int o = c / 9;
-            atomicAdd(out + 9 * d.obs_cam[obs0 + o] + (c - 9 * o), acc[i]);
+            for (int c = 0; c < 9; c++) {
+                const float4 x = S4[c * ng];
+                sl[4 * c] = x.x, sl[4 * c + 1] = x.y, sl[4 * c + 2] = x.z, sl[4 * c + 3] = x.w;
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < 36; c++) sl[c] = 0.f;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (!have) continue;
+        if (PRECOND) {
+            if (valid) {
+#pragma unroll
+                for (int r = 0; r < 4; r++) {
+                    const int a = 4 * tr.t + r;
+                    if (a < 2 * k) acc_rows(P, b, sl + 9 * r, TL[3 + a].w);
+                }
+            }
+        } else {
+            float y[4];
+#pragma unroll
+            for (int r = 0; r < 4; r++) {
+                float sacc = 0.f;
+#pragma unroll
+                for (int q = 0; q < 9; q++) sacc += sl[9 * r + q] * vo[q];
+                y[r] = warp_sum_f(sacc);
+            }
+            if (lane == 0) {
+#pragma unroll
+                for (int r = 0; r < 4; r++) red[buf][warp][r] = y[r];
+            }
+            named_sync(1 + slot, NS);
+#pragma unroll
+            for (int r = 0; r < 4; r++) {
+                float sacc = 0.f;
+#pragma unroll
+                for (int w = 0; w < NWS; w++) sacc += red[buf][slot * NWS + w][r];
+                y[r] = sacc;
+            }
+#pragma unroll
+            for (int q = 0; q < 9; q++)
+                acc[q] += sl[q] * y[0] + sl[9 + q] * y[1] + sl[18 + q] * y[2] + sl[27 + q] * y[3];
+            buf ^= 1;
         }
     }
+    flush();
 }
 
 __global__ void k_add_damping(DevProblem d, const float *v, float *out, float lam) {
@@ -1197,13 +1314,6 @@ __global__ void __launch_bounds__(256) k_cost(DevProblem d, const float *__restr
 // ============================================================================ launchers
 static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
 
-template <int G>
-static size_t small_marg_smem() {
-    return (size_t)(128 / 32) * (32 / G) * SmallTab<G>::FLOATS * sizeof(float);
-}
-static size_t large_marg_smem(int kmax) {
-    return (size_t)(4 * (2 * kmax + 3) + 4 * 9 * kmax + 18 * kmax + 6 * kmax + 2 * kmax + 20) * sizeof(float);
-}
 
 cudaError_t launch_check_depth(rba_ctx *c, int *d_bad) {
     if (c->d.n_obs == 0) return cudaSuccess;
@@ -1233,13 +1343,23 @@ extern double plan_matvec_bytes(rba_ctx *c);
 
 template <int G>
 static cudaError_t marg_small_cls(rba_ctx *c, int cls, float lam) {
-    const int64_t lo = c->small_lo[cls], hi = c->small_hi[cls];
+    const int64_t lo = c->pack_lo[cls], hi = c->pack_hi[cls];
     if (hi <= lo) return cudaSuccess;
-    const int64_t per_block = 4 * (32 / G);
-    const size_t sm = small_marg_smem<G>();
-    cudaFuncSetAttribute(k_marg_small<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_marg_small<G><<<nblk(hi - lo, (int)per_block), 128, sm, c->stream>>>(
-        c->d, lo, hi, lam, (float)c->opt.diag_min, (float)c->opt.diag_max);
+    const size_t sm = (size_t)4 * (32 / G) * SmallTab<G>::FLOATS * sizeof(float);
+    k_marg_small<G><<<nblk(hi - lo, 4), 128, sm, c->stream>>>(c->d, lo, hi, lam, (float)c->opt.diag_min,
+                                                              (float)c->opt.diag_max);
+    c->launches++;
+    return cudaGetLastError();
+}
+
+template <int NT>
+static cudaError_t marg_large_cls(rba_ctx *c, int cls, float lam) {
+    const int64_t lo = c->marg_lo[cls], hi = c->marg_hi[cls];
+    if (hi <= lo) return cudaSuccess;
+    const size_t sm = (size_t)(4 * (2 * NT + 3) + 8 * NT) * sizeof(float);
+    cudaFuncSetAttribute(k_marg_large<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_marg_large<NT><<<(unsigned)(hi - lo), NT, sm, c->stream>>>(c->d, c->d.marg_items + lo, lam,
+                                                                  (float)c->opt.diag_min, (float)c->opt.diag_max);
     c->launches++;
     return cudaGetLastError();
 }
@@ -1247,19 +1367,14 @@ static cudaError_t marg_small_cls(rba_ctx *c, int cls, float lam) {
 cudaError_t launch_marginalize(rba_ctx *c, float lam) {
     Prof P(c, KID_MARG, plan_marg_bytes(c));
     cudaError_t e;
-    if ((e = marg_small_cls<4>(c, 0, lam))) return e;
-    if ((e = marg_small_cls<8>(c, 1, lam))) return e;
-    if ((e = marg_small_cls<16>(c, 2, lam))) return e;
+    if ((e = marg_large_cls<512>(c, 3, lam))) return e;
+    if ((e = marg_large_cls<256>(c, 2, lam))) return e;
+    if ((e = marg_large_cls<128>(c, 1, lam))) return e;
+    if ((e = marg_large_cls<64>(c, 0, lam))) return e;
     if ((e = marg_small_cls<32>(c, 3, lam))) return e;
-    if (c->n_large_items) {
-        const size_t sm = large_marg_smem((int)c->max_large_k);
-        cudaFuncSetAttribute(k_marg_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        k_marg_large<<<(unsigned)c->n_large_items, 256, sm, c->stream>>>(c->d, c->d.large_items, lam,
-                                                                          (float)c->opt.diag_min,
-                                                                          (float)c->opt.diag_max);
-        c->launches++;
-        if ((e = cudaGetLastError())) return e;
-    }
+    if ((e = marg_small_cls<16>(c, 2, lam))) return e;
+    if ((e = marg_small_cls<8>(c, 1, lam))) return e;
+    if ((e = marg_small_cls<4>(c, 0, lam))) return e;
     P.end();
     return cudaSuccess;
 }
@@ -1273,12 +1388,33 @@ cudaError_t launch_redamp(rba_ctx *c, float lam) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_precond_rhs(rba_ctx *c) {
-    if (c->d.n_obs == 0) return cudaSuccess;
-    Prof P(c, KID_PRE, plan_matvec_bytes(c));
-    k_precond_rhs<<<nblk(c->d.n_obs, 256), 256, 0, c->stream>>>(c->d);
-    P.end();
+template <int NS, int NSLOT, bool PRE>
+static void large_pipe_cls(rba_ctx *c, int cls, const float *v, float *out, const PcgState *st) {
+    const int64_t n = c->cta_n[cls];
+    if (n <= 0) return;
+    using Cf = PipeCfg<NS, NSLOT>;
+    cudaFuncSetAttribute(k_large_pipe<NS, NSLOT, PRE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
+    k_large_pipe<NS, NSLOT, PRE><<<(unsigned)n, Cf::NC + 32, Cf::SMEM, c->stream>>>(
+        c->d, c->d.tiles, c->d.cta_lo + c->cta_off[cls], v, out, st);
     c->launches++;
+}
+
+template <bool PRE>
+static void large_pipe_all(rba_ctx *c, const float *v, float *out, const PcgState *st) {
+    large_pipe_cls<512, 1, PRE>(c, 3, v, out, st);
+    large_pipe_cls<256, 1, PRE>(c, 2, v, out, st);
+    large_pipe_cls<128, 2, PRE>(c, 1, v, out, st);
+    large_pipe_cls<64, 4, PRE>(c, 0, v, out, st);
+}
+
+cudaError_t launch_precond_rhs(rba_ctx *c) {
+    Prof P(c, KID_PRE, plan_matvec_bytes(c));
+    large_pipe_all<true>(c, nullptr, nullptr, nullptr);
+    if (c->n_packs) {
+        k_precond_small<<<nblk(c->n_packs, 4), 128, 0, c->stream>>>(c->d, c->n_packs);
+        c->launches++;
+    }
+    P.end();
     return cudaGetLastError();
 }
 
@@ -1288,32 +1424,15 @@ cudaError_t launch_precond_finalize(rba_ctx *c, float lam) {
     return cudaGetLastError();
 }
 
-template <int G>
-static cudaError_t matvec_small_cls(rba_ctx *c, int cls, const float *v, float *out, const PcgState *st) {
-    const int64_t lo = c->small_lo[cls], hi = c->small_hi[cls];
-    if (hi <= lo) return cudaSuccess;
-    const int64_t per_block = 4 * (32 / G);
-    k_matvec_small<G><<<nblk(hi - lo, (int)per_block), 128, 0, c->stream>>>(c->d, lo, hi, v, out, st);
-    c->launches++;
-    return cudaGetLastError();
-}
-
 static cudaError_t matvec_impl(rba_ctx *c, const float *v, float *out, const PcgState *st) {
     Prof P(c, KID_MATVEC, plan_matvec_bytes(c));
-    cudaError_t e;
-    if ((e = matvec_small_cls<4>(c, 0, v, out, st))) return e;
-    if ((e = matvec_small_cls<8>(c, 1, v, out, st))) return e;
-    if ((e = matvec_small_cls<16>(c, 2, v, out, st))) return e;
-    if ((e = matvec_small_cls<32>(c, 3, v, out, st))) return e;
-    if (c->n_large_items) {
-        const size_t sm = (size_t)9 * c->max_large_k * sizeof(float);
-        cudaFuncSetAttribute(k_matvec_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        k_matvec_large<<<(unsigned)c->n_large_items, 256, sm, c->stream>>>(c->d, c->d.large_items, v, out, st);
+    large_pipe_all<false>(c, v, out, st);
+    if (c->n_packs) {
+        k_matvec_small<<<nblk(c->n_packs, 4), 128, 0, c->stream>>>(c->d, c->n_packs, v, out, st);
         c->launches++;
-        if ((e = cudaGetLastError())) return e;
     }
     P.end();
-    return cudaSuccess;
+    return cudaGetLastError();
 }
 
 cudaError_t launch_matvec(rba_ctx *c, const float *v, float *out) { return matvec_impl(c, v, out, nullptr); }

@@ -265,7 +265,13 @@ class _TorchAllocator:
             return None
 
     def _free(self, ptr, _ctx):
-        self.torch.cuda.caching_allocator_delete(ptr)
+        torch = self.torch
+        if torch is None or getattr(torch, "cuda", None) is None:  # interpreter shutdown
+            return
+        try:
+            torch.cuda.caching_allocator_delete(ptr)
+        except Exception:
+            pass
 
 
 class Solver:

@@ -84,14 +84,13 @@ def test_create_rejects_bad_options():
 
 
 def test_layout_constants_match_paper_block_size():
-    """The arena stores exactly the logical (2k+3) x (9k+4) block per landmark plus
-    16-byte alignment padding: check the layout formulas the planner uses, via a GPU-free
-    reconstruction of the per-landmark float counts."""
+    """The arena stores the logical (2k+3) x (9k+4) block per landmark: R2 = 2k x 9k
+    (packed without padding for k <= 32; 4-row tiles for k > 32, so odd k pads 2 zero rows), R1
+    (3 x 9k) + TL ((2k+3) x 4) + G (12) in the side region (16-byte alignment padding)."""
+    pad4 = lambda x: (x + 3) // 4 * 4
     for k in list(range(2, 40)) + [64, 100, 257, 400, 512]:
-        H = 2 * k if k <= 32 else 4
-        T = 1 if k <= 32 else (2 * k + 3) // 4
-        pad4 = lambda x: (x + 3) // 4 * 4
-        r2 = (T - 1) * pad4(9 * k * H) + pad4(9 * k * (2 * k - (T - 1) * H))
+        r2 = 18 * k * k if k <= 32 else 36 * k * ((k + 1) // 2)
         side = pad4(27 * k) + 4 * (2 * k + 3) + 12
         logical = (2 * k + 3) * (9 * k + 4) + 12
-        assert 0 <= r2 + side - logical <= 3 * (T + 1)
+        extra = r2 + side - logical
+        assert 0 <= extra <= 3 + (18 * k if (k > 32 and k % 2) else 0)
