@@ -293,9 +293,9 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
         c->marg_bytes += (double)(2 * k + 3) * (9 * k + 4) * 4 + 48 + 20.0 * k;
         c->matvec_bytes += 72.0 * k * k;
     }
-    // ---- R2 arena: packs of same-k small landmarks (classes G = 4, 8, 16, 32), then large ones
+    // ---- R2 arena: packs of same-k small landmarks (classes G = 2, 4, 8, 16), then large ones
     std::vector<Pack> packs;
-    const int bounds[4] = {4, 8, 16, 32};
+    const int bounds[4] = {2, 4, 8, 16};
     int64_t r2_total = 0, pos = 0;
     for (int cls = 0; cls < 4; cls++) {
         const int NG = 32 / bounds[cls];
@@ -304,7 +304,7 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
             const int k = c->h_k[pos];
             int np = 0;
             while (pos + np < nl && np < NG && c->h_k[pos + np] == k) np++;
-            packs.push_back(Pack{(int32_t)pos, np, r2_total});
+            packs.push_back(Pack{(int32_t)pos, np, r2_total, h_obs0[pos], k, 0, 0});
             for (int m = 0; m < np; m++) {
                 c->h_r2[pos + m] = r2_total;
                 c->h_pk[pos + m] = m | (np << 8);
@@ -314,10 +314,66 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
         }
         c->pack_hi[cls] = (int64_t)packs.size();
     }
+    c->n_packs = (int64_t)packs.size();
+    // small-k pipeline stages: consecutive packs up to SMALL_STAGE_BYTES, 320 camera indices and
+    // 64 packs, each with its table of work units (pack slot, 4-row-pair range)
+    std::vector<SmallChunk> chunks;
+    std::vector<uint16_t> units;
+    for (int64_t p0 = 0; p0 < c->n_packs;) {
+        SmallChunk ch{};
+        ch.p0 = (int32_t)p0;
+        ch.base = packs[p0].base;
+        int64_t bytes = 0;
+        const int32_t cam0 = packs[p0].obs0 & ~3;
+        int32_t cam_end = cam0;
+        int64_t q = p0;
+        while (q < c->n_packs) {
+            const int64_t pb = 4 * pad4(small_pack_floats(packs[q].k, packs[q].np));
+            const int32_t ce = (packs[q].obs0 + packs[q].np * packs[q].k + 3) & ~3;
+            if (q > p0 && (bytes + pb > SMALL_STAGE_BYTES || ce - cam0 > 320 || q - p0 >= 64)) break;
+            bytes += pb;
+            cam_end = ce;
+            q++;
+        }
+        ch.np = (int32_t)(q - p0);
+        ch.bytes = (int32_t)bytes;
+        ch.cam0 = cam0;
+        ch.ncam = cam_end - cam0;
+        ch.unit0 = (int32_t)units.size();
+        for (int64_t sl = 0; sl < ch.np; sl++) {
+            const int nr = (packs[p0 + sl].k + 3) / 4;
+            for (int r = 0; r < nr; r++) units.push_back((uint16_t)(sl | (r << 8)));
+        }
+        while ((units.size() - ch.unit0) % 8) units.push_back(0xFFFF);
+        ch.nunit = (int32_t)(units.size() - ch.unit0);
+        chunks.push_back(ch);
+        p0 = q;
+    }
+    c->n_chunks = (int64_t)chunks.size();
+    std::vector<int64_t> chunk_lo;
+    {
+        const int64_t G = std::min<int64_t>(c->num_sms, c->n_chunks);
+        c->chunk_ctas = G;
+        double tot = 0;
+        for (auto &ch : chunks) tot += ch.bytes;
+        chunk_lo.push_back(0);
+        double accb = 0;
+        int64_t next = 1;
+        for (int64_t i = 0; i < c->n_chunks && next < G; i++) {
+            accb += chunks[i].bytes;
+            if (accb >= tot * next / G) {
+                chunk_lo.push_back(i + 1);
+                next++;
+            }
+        }
+        while ((int64_t)chunk_lo.size() < G) chunk_lo.push_back(c->n_chunks);
+        chunk_lo.push_back(c->n_chunks);
+    }
+    r2_total = pad4(r2_total);
     std::vector<LargeItem> marg_items;
     std::vector<TileRef> tiles;
     std::vector<int64_t> cta_lo;
-    const int ntb[4] = {64, 128, 256, 512};
+    const int ntb[5] = {32, 64, 128, 256, 512};
     const int64_t large_lo = pos;
     for (int64_t i = pos; i < nl; i++) {
         const int k = c->h_k[i];
@@ -325,7 +381,7 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
         r2_total += large_r2_floats(k);
         c->max_large_k = std::max<int64_t>(c->max_large_k, k);
     }
-    for (int cls = 0; cls < 4; cls++) {
+    for (int cls = 0; cls < 5; cls++) {
         auto in_cls = [&](int k) { return k <= ntb[cls] && (cls == 0 || k > ntb[cls - 1]); };
         c->marg_lo[cls] = (int64_t)marg_items.size();
         const int64_t t_lo = (int64_t)tiles.size();
@@ -364,7 +420,6 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
             cta_lo.push_back(t_hi);
         }
     }
-    c->n_packs = (int64_t)packs.size();
     int64_t side_total = r2_total;
     for (int64_t i = 0; i < nl; i++) {
         c->h_side[i] = side_total;
@@ -385,7 +440,7 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     CKSC(dalloc_n(c, &d.lm_pk, nl));
     CKSC(dalloc_n(c, &d.lm_r2, nl));
     CKSC(dalloc_n(c, &d.lm_side, nl));
-    CKSC(dalloc_n(c, &d.obs_cam, nobs_loc));
+    CKSC(dalloc_n(c, &d.obs_cam, nobs_loc + 8));  // +8: 16-byte aligned camera-index bulk copies
     CKSC(dalloc_n(c, &d.obs_lm, nobs_loc));
     CKSC(dalloc_n(c, &d.obs_uv, nobs_loc));
     CKSC(dalloc_n(c, &d.cam_n2, 9 * n_cams));
@@ -394,7 +449,7 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     CKSC(dalloc_n(c, &d.lm_s, 3 * nl));
     CKSC(dalloc_n(c, &d.lm_D, 3 * nl));
     CKSC(dalloc_n(c, &d.arena, c->arena_floats));
-    CKSC(dalloc_n(c, &d.pacc, 54 * n_cams));
+    CKSC(dalloc_n(c, &d.pacc, PACC_STRIDE * n_cams));
     CKSC(dalloc_n(c, &d.bt, 9 * n_cams));
     CKSC(dalloc_n(c, &d.Minv, 81 * n_cams));
     CKSC(dalloc_n(c, &d.x, 9 * n_cams));
@@ -409,6 +464,10 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     CKSC(dalloc_n(c, &d.marg_items, std::max<size_t>(1, marg_items.size())));
     CKSC(dalloc_n(c, &d.tiles, std::max<size_t>(1, tiles.size())));
     CKSC(dalloc_n(c, &d.cta_lo, std::max<size_t>(1, cta_lo.size())));
+    CKSC(dalloc_n(c, &d.chunks, std::max<size_t>(1, chunks.size())));
+    CKSC(dalloc_n(c, &d.units, std::max<size_t>(8, units.size())));
+    CKSC(dalloc_n(c, &d.chunk_lo, std::max<size_t>(1, chunk_lo.size())));
+    CKSC(dalloc_n(c, &d.w12, 12 * n_cams));
     CKC(cudaMallocHost(&c->h_scal, sizeof(double) * SC_N));
     CKC(cudaMallocHost(&c->h_pcg, sizeof(PcgState)));
     // ---- upload (host staging in the device layout)
@@ -435,6 +494,7 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
         CKC(cudaMemcpyAsync(d.lm_obs0, h_obs0.data(), sizeof(int32_t) * nl, cudaMemcpyHostToDevice, c->stream));
         CKC(cudaMemcpyAsync(d.lm_r2, c->h_r2.data(), sizeof(int64_t) * nl, cudaMemcpyHostToDevice, c->stream));
         CKC(cudaMemcpyAsync(d.lm_side, c->h_side.data(), sizeof(int64_t) * nl, cudaMemcpyHostToDevice, c->stream));
+        CKC(cudaMemsetAsync(d.obs_cam + nobs_loc, 0, sizeof(int32_t) * 8, c->stream));
         CKC(cudaMemcpyAsync(d.obs_cam, ocam.data(), sizeof(int32_t) * nobs_loc, cudaMemcpyHostToDevice, c->stream));
         CKC(cudaMemcpyAsync(d.obs_lm, olm.data(), sizeof(int32_t) * nobs_loc, cudaMemcpyHostToDevice, c->stream));
         CKC(cudaMemcpyAsync(d.obs_uv, ouv.data(), sizeof(float2) * nobs_loc, cudaMemcpyHostToDevice, c->stream));
@@ -444,6 +504,14 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
         if (!marg_items.empty())
             CKC(cudaMemcpyAsync(d.marg_items, marg_items.data(), sizeof(LargeItem) * marg_items.size(),
                                 cudaMemcpyHostToDevice, c->stream));
+        if (!units.empty())
+            CKC(cudaMemcpyAsync(d.units, units.data(), sizeof(uint16_t) * units.size(), cudaMemcpyHostToDevice,
+                                c->stream));
+        if (!chunks.empty())
+            CKC(cudaMemcpyAsync(d.chunks, chunks.data(), sizeof(SmallChunk) * chunks.size(), cudaMemcpyHostToDevice,
+                                c->stream));
+        CKC(cudaMemcpyAsync(d.chunk_lo, chunk_lo.data(), sizeof(int64_t) * chunk_lo.size(), cudaMemcpyHostToDevice,
+                            c->stream));
         if (!tiles.empty())
             CKC(cudaMemcpyAsync(d.tiles, tiles.data(), sizeof(TileRef) * tiles.size(), cudaMemcpyHostToDevice,
                                 c->stream));
@@ -536,10 +604,10 @@ extern "C" rba_status rba_pcg_solve(rba_ctx *c, rba_pcg_stats *stats) {
     CK(cudaSetDevice(c->device));
     DevProblem &d = c->d;
     const float lam = (float)c->lambda_blocks;
-    CK(cudaMemsetAsync(d.pacc, 0, sizeof(float) * 54 * d.n_p, c->stream));
+    CK(cudaMemsetAsync(d.pacc, 0, sizeof(float) * PACC_STRIDE * d.n_p, c->stream));
     CK(cudaMemsetAsync(d.scal + SC_BAD, 0, sizeof(double), c->stream));
     CK(launch_precond_rhs(c));
-    CKS(allreduce(c, d.pacc, 54 * d.n_p, ncclFloat));
+    CKS(allreduce(c, d.pacc, PACC_STRIDE * d.n_p, ncclFloat));
     CK(launch_precond_finalize(c, lam));
     CK(launch_pcg_init(c, (float)c->opt.pcg_rel_tol, c->opt.pcg_max_iters));
     int batch = 2;
@@ -549,9 +617,9 @@ extern "C" rba_status rba_pcg_solve(rba_ctx *c, rba_pcg_stats *stats) {
         if (c->h_pcg->done || c->h_pcg->it >= c->opt.pcg_max_iters) break;
         const int todo = std::min(batch, c->opt.pcg_max_iters - c->h_pcg->it);
         for (int b = 0; b < todo; b++) {
-            CK(cudaMemsetAsync(d.w, 0, sizeof(float) * 9 * d.n_p, c->stream));
+            CK(cudaMemsetAsync(d.w12, 0, sizeof(float) * 12 * d.n_p, c->stream));
             CK(launch_matvec_pcg(c));
-            CKS(allreduce(c, d.w, 9 * d.n_p, ncclFloat));
+            CKS(allreduce(c, d.w12, 12 * d.n_p, ncclFloat));
             CK(launch_pcg_step(c, lam, (float)c->opt.pcg_rel_tol, c->opt.pcg_max_iters));
         }
         batch = std::min(batch * 2, 64);
@@ -699,9 +767,9 @@ extern "C" rba_status rba_matvec(rba_ctx *c, const float *v, float *outv) {
     if (!c || !v || !outv) return fail(RBA_ERR_INVALID_ARG, "null argument");
     if (!c->marginalized) return fail(RBA_ERR_STATE, "rba_matvec before rba_marginalize_qr");
     CK(cudaSetDevice(c->device));
-    CK(cudaMemsetAsync(outv, 0, sizeof(float) * 9 * c->d.n_p, c->stream));
+    CK(cudaMemsetAsync(c->d.w12, 0, sizeof(float) * 12 * c->d.n_p, c->stream));
     CK(launch_matvec(c, v, outv));
-    CKS(allreduce(c, outv, 9 * c->d.n_p, ncclFloat));
+    CKS(allreduce(c, c->d.w12, 12 * c->d.n_p, ncclFloat));
     CK(launch_add_damping(c, v, outv, (float)c->lambda_blocks));
     return RBA_OK;
 }

@@ -12,7 +12,7 @@
 
 namespace rba {
 
-constexpr int KSMALL = 32;    // k <= KSMALL: warp-group kernels over packs of same-k landmarks
+constexpr int KSMALL = 16;    // k <= KSMALL: warp-group kernels over packs of same-k landmarks
 constexpr int KMAX = 512;     // largest track length supported by this build's large-k kernels
 
 // ---- landmark-block arena layout ------------------------------------------
@@ -56,7 +56,22 @@ __host__ __device__ inline uint32_t divmagic(uint32_t d) { return (uint32_t)((0x
 struct Pack {
     int32_t lm0, np;  // first landmark (internal index) and number of landmarks (same k)
     int64_t base;     // float offset of the pack's R2 region
+    int32_t obs0, k;  // first observation of the pack (its observations are contiguous) and k
+    int32_t pad0, pad1;
 };
+
+// A stage of the small-k pipeline: consecutive packs whose R2 regions are contiguous, their
+// camera indices and a table of work units (pack slot | row-pair range << 8).
+struct SmallChunk {
+    int32_t p0, np;          // packs [p0, p0 + np)
+    int64_t base;            // float offset of the first pack's R2
+    int32_t bytes;           // R2 bytes (multiple of 16)
+    int32_t cam0, ncam;      // obs_cam[cam0 .. cam0 + ncam): 16-byte aligned superset of the packs' cameras
+    int32_t unit0;           // units[unit0 .. unit0 + nunit) (nunit a multiple of 8, 0xFFFF = none)
+    int32_t nunit, pad0, pad1, pad2;
+};
+constexpr int PACC_STRIDE = 56;             // per-camera slot of the preconditioner accumulator
+constexpr int SMALL_STAGE_BYTES = 40 * 1024;  // >= largest pack (k = 16, np = 2: 36,864 B)
 
 struct PcgState {
     double rz;  // rho^T z
@@ -94,15 +109,19 @@ struct DevProblem {
     // arena
     float *arena;
     // reduced system / PCG
-    float *pacc;  // 54 per camera: 45 upper-triangle of P_i + 9 of b~
+    float *pacc;  // PACC_STRIDE per camera: 45 upper-triangle of P_i + 9 of b~ (+2 pad)
     float *bt, *Minv;
     float *x, *r, *z, *p, *w;
     float *dl;
     double *scal;
     PcgState *pcg;
-    Pack *packs;            // small-k packs, classes G = 4, 8, 16, 32 back to back
+    Pack *packs;            // small-k packs, classes G = 2, 4, 8, 16 back to back
+    uint16_t *units;        // small-k work units per stage
     LargeItem *marg_items;  // K2 work items (~1 MB of output each), classes NT = 64, 128, 256, 512
-    TileRef *tiles;         // K4/K5 tile stream of the large landmarks, classes k <= 64, 128, 256, 512
+    TileRef *tiles;         // K4/K5 tile stream of the large landmarks, classes k <= 32, 64, 128, 256, 512
+    SmallChunk *chunks;     // K4/K5 stage stream of the small-k packs
+    int64_t *chunk_lo;      // tile-range boundaries of the persistent CTAs over the chunks
+    float *w12;             // matvec accumulator, camera stride 12 (16-byte aligned float4 atomics)
     int64_t *cta_lo;        // per class: tile range boundaries of the persistent CTAs (bytes-balanced)
 };
 
@@ -130,9 +149,10 @@ struct rba_ctx {
     std::vector<int32_t> h_k;
     std::vector<int64_t> h_r2, h_side;
     std::vector<int32_t> h_pk;
-    int64_t pack_lo[4] = {0, 0, 0, 0}, pack_hi[4] = {0, 0, 0, 0};  // G = 4, 8, 16, 32 pack ranges
-    int64_t marg_lo[4] = {0, 0, 0, 0}, marg_hi[4] = {0, 0, 0, 0};  // K2 large items per class
-    int64_t cta_off[4] = {0, 0, 0, 0}, cta_n[4] = {0, 0, 0, 0};    // K4/K5 CTA ranges per class
+    int64_t pack_lo[4] = {0, 0, 0, 0}, pack_hi[4] = {0, 0, 0, 0};  // G = 2, 4, 8, 16 pack ranges
+    int64_t marg_lo[5] = {0, 0, 0, 0, 0}, marg_hi[5] = {0, 0, 0, 0, 0};  // K2 large items per class
+    int64_t cta_off[5] = {0, 0, 0, 0, 0}, cta_n[5] = {0, 0, 0, 0, 0};    // K4/K5 CTA ranges per class
+    int64_t n_chunks = 0, chunk_ctas = 0;
     int64_t n_packs = 0, max_large_k = 0;
     int num_sms = 148;
     int64_t arena_floats = 0, logical_bytes = 0;

@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 
 #include "rba_internal.cuh"
 
@@ -781,51 +782,20 @@ __device__ __forceinline__ void acc_rows(float *P, float *b, const float *row, f
     }
 }
 __device__ __forceinline__ void flush54(float *acc, const float *P, const float *b) {
+    // acc: 56-float (16-byte aligned) camera slot: 45 upper-triangle entries of P, 9 of b, 2 pad
+    float4 *a4 = reinterpret_cast<float4 *>(acc);
 #pragma unroll
-    for (int i = 0; i < 45; i++) atomicAdd(acc + i, P[i]);
-#pragma unroll
-    for (int i = 0; i < 9; i++) atomicAdd(acc + 45 + i, b[i]);
-}
-
-__device__ __forceinline__ int group_of_k(int k) { return k <= 4 ? 4 : (k <= 8 ? 8 : (k <= 16 ? 16 : 32)); }
-
-__global__ void __launch_bounds__(128) k_precond_small(DevProblem d, int64_t n_packs) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t pi = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-    if (pi >= n_packs) return;
-    const Pack pack = d.packs[pi];
-    const int k = d.lm_k[pack.lm0];
-    const int G = group_of_k(k);
-    const int m = lane / G, o = lane % G;
-    if (m >= pack.np || o >= k) return;
-    const int64_t j = pack.lm0 + m;
-    const float2 *A = reinterpret_cast<const float2 *>(d.arena + pack.base);
-    const float4 *TL = reinterpret_cast<const float4 *>(d.arena + d.lm_side[j] + side_tl(k));
-    const int npk = pack.np * k, mo = m * k + o;
-    float P[45], b[9];
-#pragma unroll
-    for (int i = 0; i < 45; i++) P[i] = 0.f;
-#pragma unroll
-    for (int i = 0; i < 9; i++) b[i] = 0.f;
-    for (int p = 0; p < k; p++) {
-        float sl[18];
-#pragma unroll
-        for (int c = 0; c < 9; c++) {
-            const float2 v = __ldg(A + (p * 9 + c) * npk + mo);
-            sl[2 * c] = v.x;
-            sl[2 * c + 1] = v.y;
-        }
-        acc_rows(P, b, sl, TL[3 + 2 * p].w);
-        acc_rows(P, b, sl + 9, TL[4 + 2 * p].w);
-    }
-    flush54(d.pacc + 54 * (int64_t)d.obs_cam[d.lm_obs0[j] + o], P, b);
+    for (int i = 0; i < 11; i++) atomicAdd(a4 + i, make_float4(P[4 * i], P[4 * i + 1], P[4 * i + 2], P[4 * i + 3]));
+    atomicAdd(a4 + 11, make_float4(P[44], b[0], b[1], b[2]));
+    atomicAdd(a4 + 12, make_float4(b[3], b[4], b[5], b[6]));
+    atomicAdd(a4 + 13, make_float4(b[7], b[8], 0.f, 0.f));
 }
 
 // per camera: P_i + lambda D_p^2 -> Cholesky (FP64) -> inverse M^-1 (FP32, 81); b~ copied out.
 __global__ void k_precond_finalize(DevProblem d, float lam, double *bad) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= d.n_p) return;
-    const float *acc = d.pacc + 54 * i;
+    const float *acc = d.pacc + PACC_STRIDE * i;
     double P[81];
     int idx = 0;
     for (int a = 0; a < 9; a++)
@@ -878,66 +848,39 @@ __global__ void k_precond_finalize(DevProblem d, float lam, double *bad) {
 // accumulates in registers; the 9 entries of out_o are added to the camera vector once per
 // landmark (per CTA range for large k).
 
+// out12: camera stride 12 so the 9 entries of a camera go out as three 16-byte vector atomics
+__device__ __forceinline__ void flush_cam12(float *out12, int cam, const float *acc) {
+    float4 *o4 = reinterpret_cast<float4 *>(out12 + 12 * (int64_t)cam);
+    atomicAdd(o4, make_float4(acc[0], acc[1], acc[2], acc[3]));
+    atomicAdd(o4 + 1, make_float4(acc[4], acc[5], acc[6], acc[7]));
+    atomicAdd(o4 + 2, make_float4(acc[8], 0.f, 0.f, 0.f));
+}
+
+// Sum 4 values over the warp with 6 shuffles (transpose-style butterfly).  Returns the total of
+// value r = (lane >> 3) & 3 in every lane; lanes 0, 8, 16, 24 hold rows 0, 1, 2, 3.
+__device__ __forceinline__ float warp_sum4(float y0, float y1, float y2, float y3, int lane) {
+    const bool hi16 = lane & 16;
+    // step 16: keep rows {2,3} if hi16 else {0,1}
+    float a = hi16 ? y2 : y0, b = hi16 ? y3 : y1;
+    const float sa = hi16 ? y0 : y2, sb = hi16 ? y1 : y3;
+    a += __shfl_xor_sync(0xffffffffu, sa, 16);
+    b += __shfl_xor_sync(0xffffffffu, sb, 16);
+    // step 8: keep one row
+    const bool hi8 = lane & 8;
+    float c = hi8 ? b : a;
+    const float sc = hi8 ? a : b;
+    c += __shfl_xor_sync(0xffffffffu, sc, 8);
+    c += __shfl_xor_sync(0xffffffffu, c, 4);
+    c += __shfl_xor_sync(0xffffffffu, c, 2);
+    c += __shfl_xor_sync(0xffffffffu, c, 1);
+    return c;  // row = 2 * (lane >> 4 & 1) + (lane >> 3 & 1)
+}
+
 __device__ __forceinline__ float group_sum_rt(float v, int G) {
     for (int m = G >> 1; m; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m, G);
     return v;
 }
-__device__ __forceinline__ int group_of(int k) { return k <= 4 ? 4 : (k <= 8 ? 8 : (k <= 16 ? 16 : 32)); }
-
-// small k: warp <-> pack of np same-k landmarks; lane <-> (m = lane / G, o = lane % G).  One launch
-// for all packs; the next row pair's slab is prefetched while the current one is reduced.
-__global__ void __launch_bounds__(128) k_matvec_small(DevProblem d, int64_t n_packs, const float *__restrict__ v,
-                                                      float *__restrict__ out, const PcgState *__restrict__ st) {
-    if (st && st->done) return;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t pi = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-    if (pi >= n_packs) return;  // warp-uniform
-    const Pack pack = d.packs[pi];
-    const int k = d.lm_k[pack.lm0];
-    const int G = group_of(k);
-    const int m = lane / G, o = lane % G;
-    const bool valid = m < pack.np && o < k;
-    const int npk = pack.np * k, mo = m * k + o;
-    const float2 *A = reinterpret_cast<const float2 *>(d.arena + pack.base) + mo;
-    float vo[9], acc[9];
-    int cam = 0;
-    if (valid) {
-        cam = d.obs_cam[d.lm_obs0[pack.lm0 + m] + o];
-#pragma unroll
-        for (int q = 0; q < 9; q++) vo[q] = __ldg(v + 9 * cam + q);
-    } else {
-#pragma unroll
-        for (int q = 0; q < 9; q++) vo[q] = 0.f;
-    }
-#pragma unroll
-    for (int q = 0; q < 9; q++) acc[q] = 0.f;
-    float2 cur[9], nxt[9];
-#pragma unroll
-    for (int c = 0; c < 9; c++) cur[c] = valid ? __ldg(A + c * npk) : make_float2(0.f, 0.f);
-    for (int p = 0; p < k; p++) {
-        if (p + 1 < k) {
-#pragma unroll
-            for (int c = 0; c < 9; c++) nxt[c] = valid ? __ldg(A + ((p + 1) * 9 + c) * npk) : make_float2(0.f, 0.f);
-        }
-        const float *sl = reinterpret_cast<const float *>(cur);
-        float y0 = 0.f, y1 = 0.f;
-#pragma unroll
-        for (int q = 0; q < 9; q++) {
-            y0 += sl[q] * vo[q];
-            y1 += sl[9 + q] * vo[q];
-        }
-        y0 = group_sum_rt(y0, G);
-        y1 = group_sum_rt(y1, G);
-#pragma unroll
-        for (int q = 0; q < 9; q++) acc[q] += sl[q] * y0 + sl[9 + q] * y1;
-#pragma unroll
-        for (int c = 0; c < 9; c++) cur[c] = nxt[c];
-    }
-    if (valid) {
-#pragma unroll
-        for (int q = 0; q < 9; q++) atomicAdd(out + 9 * cam + q, acc[q]);
-    }
-}
+__device__ __forceinline__ int group_of(int k) { return k == 2 ? 2 : (k <= 4 ? 4 : (k <= 8 ? 8 : 16)); }
 
 // ---- TMA bulk-copy pipeline for large k (B200: cp.async.bulk + mbarrier, one CTA per SM).
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -970,6 +913,159 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 }
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// ---- small k (<= KSMALL): TMA stages of consecutive packs (+ their camera indices, pack headers
+// and a work-unit table); warp <-> unit (pack, <= 4 row pairs), lane <-> (landmark m = lane / G,
+// camera block o = lane % G), slabs read from shared memory, row-pair partials reduced with G-lane
+// shuffles, the unit's 9 outputs per lane added to the camera vector with float4 reductions.
+constexpr int SP_WARPS = 12;                        // consumer warps
+constexpr int SP_CAMCAP = 320;                      // camera indices per stage (host guarantees)
+constexpr int SP_PACKCAP = 64;                      // packs per stage (host guarantees)
+constexpr int SP_UNITCAP = 4 * SP_PACKCAP;          // work units per stage
+constexpr int SP_OFF_CAM = SMALL_STAGE_BYTES;
+constexpr int SP_OFF_PACK = SP_OFF_CAM + 4 * SP_CAMCAP;
+constexpr int SP_OFF_UNIT = SP_OFF_PACK + (int)sizeof(Pack) * SP_PACKCAP;
+constexpr int SP_SB = SP_OFF_UNIT + 2 * SP_UNITCAP;
+constexpr int SP_STAGES = 3;
+constexpr int SP_VCAP = 16384;                      // v (9 n_p floats) kept in shared memory if it fits
+constexpr size_t SP_SMEM = (size_t)SP_STAGES * SP_SB + 4 * SP_VCAP + 2 * SP_STAGES * sizeof(uint64_t);
+
+// one work unit: NRP row pairs starting at p0 of the lane's (landmark, camera block)
+template <int NRP, bool PRECOND>
+__device__ __forceinline__ void small_unit(const DevProblem &d, const float2 *A, int npk, int p0, int k, int G,
+                                           bool valid, int cam, const float *vo, const float4 *TL,
+                                           float *__restrict__ out12) {
+    float sl[NRP][18];
+#pragma unroll
+    for (int u = 0; u < NRP; u++)
+#pragma unroll
+        for (int c = 0; c < 9; c++) {
+            const float2 x = valid ? A[((p0 + u) * 9 + c) * npk] : make_float2(0.f, 0.f);
+            sl[u][2 * c] = x.x;
+            sl[u][2 * c + 1] = x.y;
+        }
+    if (PRECOND) {
+        if (!valid) return;
+        float P[45], b[9];
+#pragma unroll
+        for (int q = 0; q < 45; q++) P[q] = 0.f;
+#pragma unroll
+        for (int q = 0; q < 9; q++) b[q] = 0.f;
+#pragma unroll
+        for (int u = 0; u < NRP; u++) {
+            acc_rows(P, b, sl[u], TL[3 + 2 * (p0 + u)].w);
+            acc_rows(P, b, sl[u] + 9, TL[4 + 2 * (p0 + u)].w);
+        }
+        flush54(d.pacc + PACC_STRIDE * (int64_t)cam, P, b);
+    } else {
+        float y[2 * NRP];
+#pragma unroll
+        for (int u = 0; u < NRP; u++) {
+            float y0 = 0.f, y1 = 0.f;
+#pragma unroll
+            for (int q = 0; q < 9; q++) {
+                y0 += sl[u][q] * vo[q];
+                y1 += sl[u][9 + q] * vo[q];
+            }
+            y[2 * u] = y0;
+            y[2 * u + 1] = y1;
+        }
+        for (int mm = G >> 1; mm; mm >>= 1) {
+#pragma unroll
+            for (int i = 0; i < 2 * NRP; i++) y[i] += __shfl_xor_sync(0xffffffffu, y[i], mm, G);
+        }
+        if (!valid) return;
+        float acc[9];
+#pragma unroll
+        for (int q = 0; q < 9; q++) {
+            float a_ = 0.f;
+#pragma unroll
+            for (int u = 0; u < NRP; u++) a_ += sl[u][q] * y[2 * u] + sl[u][9 + q] * y[2 * u + 1];
+            acc[q] = a_;
+        }
+        flush_cam12(out12, cam, acc);
+    }
+}
+
+template <bool PRECOND>
+__global__ void __launch_bounds__(SP_WARPS * 32 + 32, 1)
+    k_small_pipe(DevProblem d, const float *__restrict__ v, float *__restrict__ out12,
+                 const PcgState *__restrict__ st, int dbg) {
+    if (!PRECOND && st && st->done) return;
+    extern __shared__ __align__(128) unsigned char sm[];
+    float *sv = reinterpret_cast<float *>(sm + (size_t)SP_STAGES * SP_SB);
+    uint64_t *full = reinterpret_cast<uint64_t *>(sm + (size_t)SP_STAGES * SP_SB + 4 * SP_VCAP);
+    uint64_t *empty = full + SP_STAGES;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t lo = d.chunk_lo[blockIdx.x], hi = d.chunk_lo[blockIdx.x + 1];
+    const bool vsm = !PRECOND && 9 * d.n_p <= SP_VCAP;
+    if (vsm)
+        for (int64_t i = tid; i < 9 * d.n_p; i += blockDim.x) sv[i] = __ldg(v + i);
+    const float *vv = vsm ? sv : v;
+    if (tid == 0) {
+        for (int s = 0; s < SP_STAGES; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], SP_WARPS);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (warp == SP_WARPS) {  // producer
+        if (lane == 0) {
+            for (int64_t i = lo; i < hi; i++) {
+                const int s = (int)((i - lo) % SP_STAGES);
+                const uint32_t ph = (uint32_t)(((i - lo) / SP_STAGES) & 1);
+                const SmallChunk ch = d.chunks[i];
+                mbar_wait(&empty[s], ph ^ 1);
+                mbar_arrive_expect_tx(&full[s], (uint32_t)ch.bytes + 4u * (uint32_t)ch.ncam +
+                                                    (uint32_t)sizeof(Pack) * (uint32_t)ch.np + 2u * (uint32_t)ch.nunit);
+                unsigned char *dst = sm + (size_t)s * SP_SB;
+                bulk_g2s(dst, d.arena + ch.base, (uint32_t)ch.bytes, &full[s]);
+                bulk_g2s(dst + SP_OFF_CAM, d.obs_cam + ch.cam0, 4u * (uint32_t)ch.ncam, &full[s]);
+                bulk_g2s(dst + SP_OFF_PACK, d.packs + ch.p0, (uint32_t)sizeof(Pack) * ch.np, &full[s]);
+                bulk_g2s(dst + SP_OFF_UNIT, d.units + ch.unit0, 2u * (uint32_t)ch.nunit, &full[s]);
+            }
+        }
+        return;
+    }
+    for (int64_t i = lo; i < hi; i++) {
+        const int s = (int)((i - lo) % SP_STAGES);
+        const uint32_t ph = (uint32_t)(((i - lo) / SP_STAGES) & 1);
+        const SmallChunk ch = d.chunks[i];
+        const unsigned char *stg = sm + (size_t)s * SP_SB;
+        const int *scam = reinterpret_cast<const int *>(stg + SP_OFF_CAM);
+        const Pack *spk = reinterpret_cast<const Pack *>(stg + SP_OFF_PACK);
+        const uint16_t *sun = reinterpret_cast<const uint16_t *>(stg + SP_OFF_UNIT);
+        mbar_wait(&full[s], ph);
+        for (int ui = warp; ui < (dbg == 1 ? 0 : ch.nunit); ui += SP_WARPS) {
+            const int code = sun[ui];
+            if (code == 0xFFFF) continue;
+            const Pack pack = spk[code & 255];
+            const int p0 = 4 * (code >> 8);
+            const int k = pack.k;
+            const int G = group_of(k);
+            const int m = lane / G, o = lane % G;
+            const bool valid = m < pack.np && o < k;
+            const int npk = pack.np * k, mo = m * k + o;
+            const float2 *A = reinterpret_cast<const float2 *>(stg + 4 * (pack.base - ch.base)) + mo;
+            const int cam = valid ? scam[pack.obs0 - ch.cam0 + mo] : 0;
+            float vo[9];
+#pragma unroll
+            for (int q = 0; q < 9; q++) vo[q] = (valid && !PRECOND) ? vv[9 * cam + q] : 0.f;
+            const float4 *TL = (PRECOND && valid)
+                                   ? reinterpret_cast<const float4 *>(d.arena + d.lm_side[pack.lm0 + m] + side_tl(k))
+                                   : nullptr;
+            switch (min(4, k - p0)) {
+                case 1: small_unit<1, PRECOND>(d, A, npk, p0, k, G, valid, cam, vo, TL, out12); break;
+                case 2: small_unit<2, PRECOND>(d, A, npk, p0, k, G, valid, cam, vo, TL, out12); break;
+                case 3: small_unit<3, PRECOND>(d, A, npk, p0, k, G, valid, cam, vo, TL, out12); break;
+                default: small_unit<4, PRECOND>(d, A, npk, p0, k, G, valid, cam, vo, TL, out12); break;
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
 }
 
 template <int NS, int NSLOT>
@@ -1040,12 +1136,8 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
     for (int q = 0; q < 9; q++) vo[q] = 0.f, acc[q] = 0.f;
     auto flush = [&]() {
         if (cur < 0 || !valid) return;
-        if (PRECOND) {
-            flush54(d.pacc + 54 * (int64_t)cam, P, b);
-        } else {
-#pragma unroll
-            for (int q = 0; q < 9; q++) atomicAdd(out + 9 * cam + q, acc[q]);
-        }
+        if (PRECOND) flush54(d.pacc + PACC_STRIDE * (int64_t)cam, P, b);
+        else flush_cam12(out, cam, acc);
     };
     int buf = 0;
     for (int64_t i = 0; i < nst; i++) {
@@ -1110,19 +1202,23 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
                 float sacc = 0.f;
 #pragma unroll
                 for (int q = 0; q < 9; q++) sacc += sl[9 * r + q] * vo[q];
-                y[r] = warp_sum_f(sacc);
-            }
-            if (lane == 0) {
-#pragma unroll
-                for (int r = 0; r < 4; r++) red[buf][warp][r] = y[r];
-            }
-            named_sync(1 + slot, NS);
-#pragma unroll
-            for (int r = 0; r < 4; r++) {
-                float sacc = 0.f;
-#pragma unroll
-                for (int w = 0; w < NWS; w++) sacc += red[buf][slot * NWS + w][r];
                 y[r] = sacc;
+            }
+            const float yr = warp_sum4(y[0], y[1], y[2], y[3], lane);
+            if ((lane & 7) == 0) red[buf][warp][lane >> 3] = yr;
+            if (NS == 32) {
+                __syncwarp();
+#pragma unroll
+                for (int r = 0; r < 4; r++) y[r] = red[buf][warp][r];
+            } else {
+                named_sync(1 + slot, NS);
+#pragma unroll
+                for (int r = 0; r < 4; r++) {
+                    float sacc = 0.f;
+#pragma unroll
+                    for (int w = 0; w < NWS; w++) sacc += red[buf][slot * NWS + w][r];
+                    y[r] = sacc;
+                }
             }
 #pragma unroll
             for (int q = 0; q < 9; q++)
@@ -1133,9 +1229,12 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
     flush();
 }
 
+// out = w12 (stride 12 -> 9) + lambda D_p^2 v
 __global__ void k_add_damping(DevProblem d, const float *v, float *out, float lam) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < 9 * d.n_p) out[i] += lam * d.Dp2[i] * v[i];
+    if (i >= 9 * d.n_p) return;
+    const int64_t cam = i / 9;
+    out[i] = d.w12[12 * cam + (i - 9 * cam)] + lam * d.Dp2[i] * v[i];
 }
 
 // ============================================================================ K6 PCG (single CTA)
@@ -1191,7 +1290,8 @@ __global__ void __launch_bounds__(1024) k_pcg_step(DevProblem d, float lam, doub
     const int64_t N = 9 * d.n_p;
     double pw = 0.0;
     for (int64_t i = threadIdx.x; i < N; i += blockDim.x) {
-        const float w = d.w[i] + lam * d.Dp2[i] * d.p[i];
+        const int64_t cam = i / 9;
+        const float w = d.w12[12 * cam + (i - 9 * cam)] + lam * d.Dp2[i] * d.p[i];
         d.w[i] = w;
         pw += (double)d.p[i] * w;
     }
@@ -1367,14 +1467,15 @@ static cudaError_t marg_large_cls(rba_ctx *c, int cls, float lam) {
 cudaError_t launch_marginalize(rba_ctx *c, float lam) {
     Prof P(c, KID_MARG, plan_marg_bytes(c));
     cudaError_t e;
-    if ((e = marg_large_cls<512>(c, 3, lam))) return e;
-    if ((e = marg_large_cls<256>(c, 2, lam))) return e;
-    if ((e = marg_large_cls<128>(c, 1, lam))) return e;
-    if ((e = marg_large_cls<64>(c, 0, lam))) return e;
-    if ((e = marg_small_cls<32>(c, 3, lam))) return e;
-    if ((e = marg_small_cls<16>(c, 2, lam))) return e;
-    if ((e = marg_small_cls<8>(c, 1, lam))) return e;
-    if ((e = marg_small_cls<4>(c, 0, lam))) return e;
+    if ((e = marg_large_cls<512>(c, 4, lam))) return e;
+    if ((e = marg_large_cls<256>(c, 3, lam))) return e;
+    if ((e = marg_large_cls<128>(c, 2, lam))) return e;
+    if ((e = marg_large_cls<64>(c, 1, lam))) return e;
+    if ((e = marg_large_cls<32>(c, 0, lam))) return e;
+    if ((e = marg_small_cls<16>(c, 3, lam))) return e;
+    if ((e = marg_small_cls<8>(c, 2, lam))) return e;
+    if ((e = marg_small_cls<4>(c, 1, lam))) return e;
+    if ((e = marg_small_cls<2>(c, 0, lam))) return e;
     P.end();
     return cudaSuccess;
 }
@@ -1400,20 +1501,24 @@ static void large_pipe_cls(rba_ctx *c, int cls, const float *v, float *out, cons
 }
 
 template <bool PRE>
-static void large_pipe_all(rba_ctx *c, const float *v, float *out, const PcgState *st) {
-    large_pipe_cls<512, 1, PRE>(c, 3, v, out, st);
-    large_pipe_cls<256, 1, PRE>(c, 2, v, out, st);
-    large_pipe_cls<128, 2, PRE>(c, 1, v, out, st);
-    large_pipe_cls<64, 4, PRE>(c, 0, v, out, st);
+static void pipes_all(rba_ctx *c, const float *v, float *out12, const PcgState *st) {
+    large_pipe_cls<512, 1, PRE>(c, 4, v, out12, st);
+    large_pipe_cls<256, 1, PRE>(c, 3, v, out12, st);
+    large_pipe_cls<128, 2, PRE>(c, 2, v, out12, st);
+    large_pipe_cls<64, 4, PRE>(c, 1, v, out12, st);
+    large_pipe_cls<32, 8, PRE>(c, 0, v, out12, st);
+    if (c->chunk_ctas > 0) {
+        cudaFuncSetAttribute(k_small_pipe<PRE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SP_SMEM);
+        static const int dbg = getenv("RBA_DEBUG_SMALLPIPE") ? atoi(getenv("RBA_DEBUG_SMALLPIPE")) : 0;
+        k_small_pipe<PRE><<<(unsigned)c->chunk_ctas, SP_WARPS * 32 + 32, SP_SMEM, c->stream>>>(c->d, v, out12, st,
+                                                                                               PRE ? 0 : dbg);
+        c->launches++;
+    }
 }
 
 cudaError_t launch_precond_rhs(rba_ctx *c) {
     Prof P(c, KID_PRE, plan_matvec_bytes(c));
-    large_pipe_all<true>(c, nullptr, nullptr, nullptr);
-    if (c->n_packs) {
-        k_precond_small<<<nblk(c->n_packs, 4), 128, 0, c->stream>>>(c->d, c->n_packs);
-        c->launches++;
-    }
+    pipes_all<true>(c, nullptr, nullptr, nullptr);
     P.end();
     return cudaGetLastError();
 }
@@ -1424,19 +1529,16 @@ cudaError_t launch_precond_finalize(rba_ctx *c, float lam) {
     return cudaGetLastError();
 }
 
-static cudaError_t matvec_impl(rba_ctx *c, const float *v, float *out, const PcgState *st) {
+static cudaError_t matvec_impl(rba_ctx *c, const float *v, const PcgState *st) {
     Prof P(c, KID_MATVEC, plan_matvec_bytes(c));
-    large_pipe_all<false>(c, v, out, st);
-    if (c->n_packs) {
-        k_matvec_small<<<nblk(c->n_packs, 4), 128, 0, c->stream>>>(c->d, c->n_packs, v, out, st);
-        c->launches++;
-    }
+    pipes_all<false>(c, v, c->d.w12, st);
     P.end();
     return cudaGetLastError();
 }
 
-cudaError_t launch_matvec(rba_ctx *c, const float *v, float *out) { return matvec_impl(c, v, out, nullptr); }
-cudaError_t launch_matvec_pcg(rba_ctx *c) { return matvec_impl(c, c->d.p, c->d.w, c->d.pcg); }
+// w12 = sum_j A_j^T (A_j v_j)  (callers zero w12 first and all-reduce it afterwards)
+cudaError_t launch_matvec(rba_ctx *c, const float *v, float *) { return matvec_impl(c, v, nullptr); }
+cudaError_t launch_matvec_pcg(rba_ctx *c) { return matvec_impl(c, c->d.p, c->d.pcg); }
 
 cudaError_t launch_add_damping(rba_ctx *c, const float *v, float *out, float lam) {
     k_add_damping<<<nblk(9 * c->d.n_p, 256), 256, 0, c->stream>>>(c->d, v, out, lam);
