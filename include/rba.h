@@ -123,8 +123,10 @@ rba_status rba_lm_step(rba_ctx *ctx, rba_lm_report *report);
 
 /* Full state on every rank (host FP64, caller buffers n_cams x 9 and n_points x 3). */
 rba_status rba_get_state(rba_ctx *ctx, double *cameras, double *points);
-/* Replace the state (host FP64); the next LM step relinearizes.  Resets lambda to lambda0. */
+/* Replace the state (host FP64); the next LM step relinearizes.  LM damping state is kept. */
 rba_status rba_set_state(rba_ctx *ctx, const double *cameras, const double *points);
+/* Restart the LM schedule: lambda = lambda0, nu = 2, iteration counter 0. */
+rba_status rba_reset_lm(rba_ctx *ctx);
 
 /* ---- test / measurement hooks ----------------------------------------------------------- */
 /* out = H~ v (incl. lambda D_p^2 v at the damping currently folded in); v, out: device FP32 9 n_cams. */
@@ -150,7 +152,9 @@ rba_status rba_kernel_launches(rba_ctx *ctx, int64_t *count);
 rba_status rba_profile(rba_ctx *ctx, int enable);
 /* kernel: 0 linearize(K1), 1 marginalize(K2), 2 damp(K3), 3 precond+rhs(K4), 4 matvec(K5),
  * 5 pcg update(K6), 6 backsub(K7), 7 cost(K8).  Synchronizes.  Outputs total ms, launch count and
- * algorithmic bytes moved (per SURVEY §8d-3 / DESIGN.md §5) summed over the recorded launches. */
+ * algorithmic bytes moved (per SURVEY §8d-3 / DESIGN.md §5) summed over the recorded launches.  For
+ * the matvec, `launches` counts only matvecs that did work (PCG iterations run in batches and the
+ * ones issued after convergence exit immediately); total_ms still includes those no-op launches. */
 rba_status rba_profile_get(rba_ctx *ctx, int kernel, double *total_ms, int64_t *launches, double *bytes);
 /* Deterministic LPT landmark partition (host only, no GPU): owner[j] in [0, world) for track
  * lengths k[j]; balances block bytes (2k+3)(9k+4). */

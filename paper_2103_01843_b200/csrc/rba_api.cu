@@ -443,7 +443,7 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     CKSC(dalloc_n(c, &d.obs_cam, nobs_loc + 8));  // +8: 16-byte aligned camera-index bulk copies
     CKSC(dalloc_n(c, &d.obs_lm, nobs_loc));
     CKSC(dalloc_n(c, &d.obs_uv, nobs_loc));
-    CKSC(dalloc_n(c, &d.cam_n2, 9 * n_cams));
+    CKSC(dalloc_n(c, &d.cam_n2, 12 * n_cams));
     CKSC(dalloc_n(c, &d.sp, 9 * n_cams));
     CKSC(dalloc_n(c, &d.Dp2, 9 * n_cams));
     CKSC(dalloc_n(c, &d.lm_s, 3 * nl));
@@ -565,10 +565,10 @@ extern "C" rba_status rba_linearize(rba_ctx *c) {
     if (!c) return fail(RBA_ERR_INVALID_ARG, "null ctx");
     CK(cudaSetDevice(c->device));
     DevProblem &d = c->d;
-    CK(cudaMemsetAsync(d.cam_n2, 0, sizeof(float) * 9 * d.n_p, c->stream));
+    CK(cudaMemsetAsync(d.cam_n2, 0, sizeof(float) * 12 * d.n_p, c->stream));
     CK(cudaMemsetAsync(d.scal + SC_E, 0, sizeof(double) * 2, c->stream));
     CK(launch_linearize(c));
-    CKS(allreduce(c, d.cam_n2, 9 * d.n_p, ncclFloat));
+    CKS(allreduce(c, d.cam_n2, 12 * d.n_p, ncclFloat));
     CKS(allreduce(c, d.scal + SC_E, 2, ncclDouble));
     CK(launch_cam_scale(c));
     CKS(read_scal(c));
@@ -625,6 +625,7 @@ extern "C" rba_status rba_pcg_solve(rba_ctx *c, rba_pcg_stats *stats) {
         batch = std::min(batch * 2, 64);
     }
     CKS(read_scal(c));
+    c->prof_real_matvecs += c->h_pcg->it;
     if (stats) {
         stats->iters = c->h_pcg->it;
         stats->reason = c->h_pcg->reason;
@@ -757,8 +758,14 @@ extern "C" rba_status rba_set_state(rba_ctx *c, const double *cameras, const dou
     CK(cudaStreamSynchronize(c->stream));
     c->linearized = c->marginalized = c->solved = c->backsubbed = false;
     c->need_lin = true;
+    return RBA_OK;
+}
+
+extern "C" rba_status rba_reset_lm(rba_ctx *c) {
+    if (!c) return fail(RBA_ERR_INVALID_ARG, "null ctx");
     c->lm_lambda = c->opt.lambda0;
     c->lm_nu = 2.0;
+    c->iteration = 0;
     return RBA_OK;
 }
 
@@ -771,6 +778,7 @@ extern "C" rba_status rba_matvec(rba_ctx *c, const float *v, float *outv) {
     CK(launch_matvec(c, v, outv));
     CKS(allreduce(c, c->d.w12, 12 * c->d.n_p, ncclFloat));
     CK(launch_add_damping(c, v, outv, (float)c->lambda_blocks));
+    c->prof_real_matvecs++;
     return RBA_OK;
 }
 
@@ -871,6 +879,7 @@ extern "C" rba_status rba_profile(rba_ctx *c, int enable) {
         c->ev_pool.push_back(l.b);
     }
     c->prof.clear();
+    c->prof_real_matvecs = 0;
     c->profiling = enable != 0;
     return RBA_OK;
 }
@@ -889,6 +898,12 @@ extern "C" rba_status rba_profile_get(rba_ctx *c, int kernel, double *total_ms, 
             by += l.bytes;
             n++;
         }
+    if (kernel == KID_MATVEC) {
+        // PCG launches iterations in batches; launches after convergence exit at once (device-side
+        // done flag).  Count only the matvecs that did work; their time includes the no-op ones.
+        n = c->prof_real_matvecs;
+        by = c->matvec_bytes * (double)n;
+    }
     *total_ms = ms;
     *launches = n;
     *bytes = by;

@@ -171,6 +171,7 @@ struct rba_ctx {
     int64_t launches = 0;
     // profiling
     bool profiling = false;
+    int64_t prof_real_matvecs = 0;  // matvecs that did work (PCG iterations + hook calls) since rba_profile
     std::vector<rba::Launch> prof;
     std::vector<cudaEvent_t> ev_pool;
 };

@@ -151,6 +151,14 @@ __device__ __forceinline__ double block_sum_d(double v, double *scratch) {
     return s;
 }
 
+// out12: camera stride 12 so the 9 entries of a camera go out as three 16-byte vector atomics
+__device__ __forceinline__ void flush_cam12(float *out12, int cam, const float *acc) {
+    float4 *o4 = reinterpret_cast<float4 *>(out12 + 12 * (int64_t)cam);
+    atomicAdd(o4, make_float4(acc[0], acc[1], acc[2], acc[3]));
+    atomicAdd(o4 + 1, make_float4(acc[4], acc[5], acc[6], acc[7]));
+    atomicAdd(o4 + 2, make_float4(acc[8], 0.f, 0.f, 0.f));
+}
+
 // ============================================================================ K0 / K1
 __global__ void k_check_depth(DevProblem d, int *bad) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -177,8 +185,10 @@ __global__ void __launch_bounds__(256) k_linearize(DevProblem d) {
         float Pz = cam_model(c, X[0], X[1], X[2], uv.x, uv.y, r, Jc, Jl);
         if (!(Pz < 0.f)) bad = 1.0;
         e = (double)r[0] * r[0] + (double)r[1] * r[1];
+        float n2[9];
 #pragma unroll
-        for (int q = 0; q < 9; q++) atomicAdd(d.cam_n2 + 9 * cam + q, Jc[q] * Jc[q] + Jc[9 + q] * Jc[9 + q]);
+        for (int q = 0; q < 9; q++) n2[q] = Jc[q] * Jc[q] + Jc[9 + q] * Jc[9 + q];
+        flush_cam12(d.cam_n2, cam, n2);  // camera stride 12, three float4 reductions
     }
     e = block_sum_d(e, red);
     bad = block_sum_d(bad, red);
@@ -191,7 +201,8 @@ __global__ void __launch_bounds__(256) k_linearize(DevProblem d) {
 __global__ void k_cam_scale(DevProblem d, float dmin, float dmax) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= 9 * d.n_p) return;
-    float n2 = d.cam_n2[i];
+    const int64_t cam = i / 9;
+    float n2 = d.cam_n2[12 * cam + (i - 9 * cam)];
     float s = 1.f / (1.f + sqrtf(n2));
     d.sp[i] = s;
     d.Dp2[i] = fminf(fmaxf(n2 * s * s, dmin), dmax);
@@ -848,14 +859,6 @@ __global__ void k_precond_finalize(DevProblem d, float lam, double *bad) {
 // accumulates in registers; the 9 entries of out_o are added to the camera vector once per
 // landmark (per CTA range for large k).
 
-// out12: camera stride 12 so the 9 entries of a camera go out as three 16-byte vector atomics
-__device__ __forceinline__ void flush_cam12(float *out12, int cam, const float *acc) {
-    float4 *o4 = reinterpret_cast<float4 *>(out12 + 12 * (int64_t)cam);
-    atomicAdd(o4, make_float4(acc[0], acc[1], acc[2], acc[3]));
-    atomicAdd(o4 + 1, make_float4(acc[4], acc[5], acc[6], acc[7]));
-    atomicAdd(o4 + 2, make_float4(acc[8], 0.f, 0.f, 0.f));
-}
-
 // Sum 4 values over the warp with 6 shuffles (transpose-style butterfly).  Returns the total of
 // value r = (lane >> 3) & 3 in every lane; lanes 0, 8, 16, 24 hold rows 0, 1, 2, 3.
 __device__ __forceinline__ float warp_sum4(float y0, float y1, float y2, float y3, int lane) {
@@ -1341,12 +1344,15 @@ __global__ void __launch_bounds__(256) k_backsub(DevProblem d, float lam) {
     const int W = 9 * k;
     const int64_t obs0 = d.lm_obs0[j];
     float s0 = 0.f, s1 = 0.f, s2 = 0.f;
-    for (int c = lane; c < W; c += 32) {
-        const int o = c / 9;
-        const float dp = d.x[9 * d.obs_cam[obs0 + o] + (c - 9 * o)];
-        s0 += side[c] * dp;
-        s1 += side[W + c] * dp;
-        s2 += side[2 * W + c] * dp;
+    for (int o = lane; o < k; o += 32) {  // lane <-> camera block: one gather of dp per block
+        const float *dp = d.x + 9 * (int64_t)d.obs_cam[obs0 + o];
+#pragma unroll
+        for (int q = 0; q < 9; q++) {
+            const float v = dp[q];
+            s0 += side[9 * o + q] * v;
+            s1 += side[W + 9 * o + q] * v;
+            s2 += side[2 * W + 9 * o + q] * v;
+        }
     }
     s0 = warp_sum_f(s0);
     s1 = warp_sum_f(s1);

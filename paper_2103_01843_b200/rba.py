@@ -68,6 +68,7 @@ def _load():
         "rba_lm_step": (I, [P, C.POINTER(rba_lm_report)]),
         "rba_get_state": (I, [P, P, P]),
         "rba_set_state": (I, [P, P, P]),
+        "rba_reset_lm": (I, [P]),
         "rba_matvec": (I, [P, P, P]),
         "rba_get_rhs": (I, [P, P]),
         "rba_get_step": (I, [P, P, P]),
@@ -90,7 +91,7 @@ def _load():
 
 _lib = _load()
 EXPORTED = ["rba_default_options", "rba_create", "rba_destroy", "rba_linearize", "rba_marginalize_qr",
-            "rba_pcg_solve", "rba_backsubstitute", "rba_cost", "rba_lm_step", "rba_get_state", "rba_set_state",
+            "rba_pcg_solve", "rba_backsubstitute", "rba_cost", "rba_lm_step", "rba_get_state", "rba_set_state", "rba_reset_lm",
             "rba_matvec", "rba_get_rhs", "rba_get_step", "rba_get_scaling", "rba_export_block", "rba_arena_bytes",
             "rba_kernel_launches", "rba_profile", "rba_profile_get", "rba_plan_shards", "rba_nccl_unique_id",
             "rba_last_error"]
@@ -172,6 +173,10 @@ def rba_set_state(h, cameras, points):
     cameras = np.ascontiguousarray(cameras, np.float64)
     points = np.ascontiguousarray(points, np.float64)
     _check(_lib.rba_set_state(h, _p(cameras), _p(points)))
+
+
+def rba_reset_lm(h):
+    _check(_lib.rba_reset_lm(h))
 
 
 def rba_matvec(h, v_dev_ptr: int, out_dev_ptr: int):
@@ -334,6 +339,9 @@ class Solver:
 
     def set_state(self, cams, pts):
         rba_set_state(self.h, cams, pts)
+
+    def reset_lm(self):
+        rba_reset_lm(self.h)
 
     def matvec(self, v):
         """v: torch float32 CUDA tensor (9 n_p) -> H~ v (torch)."""
