@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <queue>
@@ -163,6 +164,8 @@ static void free_ctx(rba_ctx *c) {
     if (c->h_scal) cudaFreeHost(c->h_scal);
     if (c->h_pcg) cudaFreeHost(c->h_pcg);
     if (c->have_comm) ncclCommDestroy(c->comm);
+    if (c->pcg_exec) cudaGraphExecDestroy(c->pcg_exec);
+    if (c->pcg_graph) cudaGraphDestroy(c->pcg_graph);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -610,8 +613,25 @@ extern "C" rba_status rba_pcg_solve(rba_ctx *c, rba_pcg_stats *stats) {
     CKS(allreduce(c, d.pacc, PACC_STRIDE * d.n_p, ncclFloat));
     CK(launch_precond_finalize(c, lam));
     CK(launch_pcg_init(c, (float)c->opt.pcg_rel_tol, c->opt.pcg_max_iters));
+    static const bool no_graph = getenv("RBA_NO_GRAPH") != nullptr;
+    if (!c->have_comm && !no_graph && !c->pcg_exec && !c->pcg_graph_failed) {
+        if (build_pcg_graph(c) != cudaSuccess) {
+            cudaGetLastError();
+            c->pcg_graph_failed = true;
+        }
+    }
+    if (!c->have_comm && c->pcg_exec && !no_graph) {
+        // device-side loop: no host round trip per iteration, no post-convergence launches
+        c->h_scal[SC_LAM] = lam;
+        CK(cudaMemcpyAsync(d.scal + SC_LAM, c->h_scal + SC_LAM, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        Prof P(c, KID_MATVEC, 0.0);
+        CK(cudaGraphLaunch(c->pcg_exec, c->stream));
+        P.end();
+        c->launches += 1;
+        CK(cudaMemcpyAsync(c->h_pcg, d.pcg, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
+    }
     int batch = 2;
-    for (;;) {
+    for (; !(!c->have_comm && c->pcg_exec && !no_graph);) {
         CK(cudaMemcpyAsync(c->h_pcg, d.pcg, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
         if (c->h_pcg->done || c->h_pcg->it >= c->opt.pcg_max_iters) break;

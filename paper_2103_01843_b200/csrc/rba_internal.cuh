@@ -82,7 +82,7 @@ struct PcgState {
 
 // double scalars on the device (single buffer so one all-reduce covers them)
 // [E, BAD] reduced at linearize; [ET, BADT, Q1R2, DAMPL] reduced after a trial; MODELP replicated
-enum { SC_E = 0, SC_BAD, SC_ET, SC_BADT, SC_Q1R2, SC_DAMPL, SC_MODELP, SC_N = 8 };
+enum { SC_E = 0, SC_BAD, SC_ET, SC_BADT, SC_Q1R2, SC_DAMPL, SC_MODELP, SC_LAM, SC_N = 8 };
 
 enum { KID_LIN = 0, KID_MARG, KID_DAMP, KID_PRE, KID_MATVEC, KID_PCG, KID_BACKSUB, KID_COST, KID_N };
 
@@ -170,6 +170,10 @@ struct rba_ctx {
     int64_t iteration = 0;
     int64_t launches = 0;
     // profiling
+    // PCG as a CUDA graph with a device-side while loop (single GPU; NCCL path uses host batches)
+    cudaGraph_t pcg_graph = nullptr;
+    cudaGraphExec_t pcg_exec = nullptr;
+    bool pcg_graph_failed = false;
     bool profiling = false;
     int64_t prof_real_matvecs = 0;  // matvecs that did work (PCG iterations + hook calls) since rba_profile
     std::vector<rba::Launch> prof;
@@ -189,6 +193,7 @@ cudaError_t launch_matvec(rba_ctx *c, const float *v, float *out);
 cudaError_t launch_matvec_pcg(rba_ctx *c);
 cudaError_t launch_pcg_init(rba_ctx *c, float tol, int max_iters);
 cudaError_t launch_pcg_step(rba_ctx *c, float lambda, float tol, int max_iters);
+cudaError_t build_pcg_graph(rba_ctx *c);
 cudaError_t launch_backsub(rba_ctx *c, float lambda);
 cudaError_t launch_trial_cost(rba_ctx *c);
 cudaError_t launch_cost(rba_ctx *c, int at_trial, int slot);

@@ -1285,11 +1285,18 @@ __global__ void __launch_bounds__(1024) k_pcg_init(DevProblem d) {
     }
 }
 
-__global__ void __launch_bounds__(1024) k_pcg_step(DevProblem d, float lam, double tol, int max_iters) {
+// lam < 0: read lambda from d.scal[SC_LAM] (graph launches).  use_h: also drive the graph's
+// while-loop condition (0 once the solve is done).
+__global__ void __launch_bounds__(1024) k_pcg_step(DevProblem d, float lam, double tol, int max_iters,
+                                                   cudaGraphConditionalHandle h, int use_h) {
     __shared__ double red[32];
     __shared__ int stop;
     PcgState *st = d.pcg;
-    if (st->done) return;
+    if (lam < 0.f) lam = (float)d.scal[SC_LAM];
+    if (st->done) {
+        if (use_h && threadIdx.x == 0) cudaGraphSetConditional(h, 0);
+        return;
+    }
     const int64_t N = 9 * d.n_p;
     double pw = 0.0;
     for (int64_t i = threadIdx.x; i < N; i += blockDim.x) {
@@ -1300,7 +1307,10 @@ __global__ void __launch_bounds__(1024) k_pcg_step(DevProblem d, float lam, doub
     }
     pw = block_sum_d(pw, red);
     if (!(pw > 0.0)) {
-        if (threadIdx.x == 0) st->done = 1, st->reason = 2;
+        if (threadIdx.x == 0) {
+            st->done = 1, st->reason = 2;
+            if (use_h) cudaGraphSetConditional(h, 0);
+        }
         return;
     }
     const float alpha = (float)(st->rz / pw);
@@ -1320,6 +1330,7 @@ __global__ void __launch_bounds__(1024) k_pcg_step(DevProblem d, float lam, doub
         if (sqrt(rr) <= tol * st->r0) stop = 1, st->reason = 0;
         else if (it >= max_iters) stop = 1, st->reason = 1;
         if (stop) st->done = 1;
+        if (use_h) cudaGraphSetConditional(h, stop ? 0 : 1);
     }
     __syncthreads();
     if (stop) return;
@@ -1560,10 +1571,49 @@ cudaError_t launch_pcg_init(rba_ctx *c, float, int) {
 
 cudaError_t launch_pcg_step(rba_ctx *c, float lam, float tol, int max_iters) {
     Prof P(c, KID_PCG, 0.0);
-    k_pcg_step<<<1, 1024, 0, c->stream>>>(c->d, lam, (double)tol, max_iters);
+    k_pcg_step<<<1, 1024, 0, c->stream>>>(c->d, lam, (double)tol, max_iters, 0, 0);
     P.end();
     c->launches++;
     return cudaGetLastError();
+}
+
+// PCG loop as a graph: while (cond) { w12 = 0; w12 = sum_j A_j^T A_j p (all pipes); PCG update }
+// The update kernel clears the condition once |rho| <= tol |rho_0|, max iterations or p^T H p <= 0.
+cudaError_t build_pcg_graph(rba_ctx *c) {
+    cudaError_t e;
+    cudaGraph_t g;
+    if ((e = cudaGraphCreate(&g, 0))) return e;
+    cudaGraphConditionalHandle h;
+    if ((e = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault))) return e;
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    if ((e = cudaGraphAddNode(&node, g, nullptr, 0, &np))) return e;
+    cudaGraph_t body = np.conditional.phGraph_out[0];
+    cudaStream_t cs;
+    if ((e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking))) return e;
+    if ((e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed))) return e;
+    cudaStream_t saved = c->stream;
+    const bool prof = c->profiling;
+    const int64_t nl = c->launches;
+    c->stream = cs;
+    c->profiling = false;
+    cudaMemsetAsync(c->d.w12, 0, sizeof(float) * 12 * c->d.n_p, cs);
+    pipes_all<false>(c, c->d.p, c->d.w12, c->d.pcg);
+    k_pcg_step<<<1, 1024, 0, cs>>>(c->d, -1.f, c->opt.pcg_rel_tol, c->opt.pcg_max_iters, h, 1);
+    c->stream = saved;
+    c->profiling = prof;
+    c->launches = nl;
+    cudaGraph_t captured;
+    e = cudaStreamEndCapture(cs, &captured);
+    cudaStreamDestroy(cs);
+    if (e) return e;
+    if ((e = cudaGraphInstantiate(&c->pcg_exec, g, 0))) return e;
+    c->pcg_graph = g;
+    return cudaSuccess;
 }
 
 cudaError_t launch_backsub(rba_ctx *c, float lam) {
