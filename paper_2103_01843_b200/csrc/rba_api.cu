@@ -166,6 +166,11 @@ static void free_ctx(rba_ctx *c) {
     if (c->have_comm) ncclCommDestroy(c->comm);
     if (c->pcg_exec) cudaGraphExecDestroy(c->pcg_exec);
     if (c->pcg_graph) cudaGraphDestroy(c->pcg_graph);
+    for (int i = 0; i < rba_ctx::NAUX; i++) {
+        if (c->aux[i]) cudaStreamDestroy(c->aux[i]);
+        if (c->ev_join[i]) cudaEventDestroy(c->ev_join[i]);
+    }
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -259,6 +264,11 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     } while (0)
     CKC(cudaSetDevice(opt.device));
     CKC(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, opt.device));
+    for (int i = 0; i < rba_ctx::NAUX; i++) {
+        CKC(cudaStreamCreateWithFlags(&c->aux[i], cudaStreamNonBlocking));
+        CKC(cudaEventCreateWithFlags(&c->ev_join[i], cudaEventDisableTiming));
+    }
+    CKC(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     if (opt.stream) {
         c->stream = (cudaStream_t)opt.stream;
     } else {
@@ -396,7 +406,8 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
             const int tpi2 = std::max(1, 262144 / (36 * k));
             for (int t0 = 0; t0 < T; t0 += tpi2)
                 marg_items.push_back(LargeItem{(int32_t)i, t0, std::min(T, t0 + tpi2), 0});
-            for (int t = 0; t < T; t++) tiles.push_back(TileRef{(int32_t)i, t});
+            for (int t = 0; t < T; t++)
+                tiles.push_back(TileRef{(int32_t)i, t, c->h_r2[i] + (int64_t)36 * k * t, k, 0});
             bytes += 144.0 * k * T;
         }
         c->marg_hi[cls] = (int64_t)marg_items.size();
@@ -411,7 +422,7 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
             double accb = 0;
             int64_t next = 1;
             for (int64_t ti = t_lo; ti < t_hi && next < G; ti++) {
-                accb += 144.0 * c->h_k[tiles[ti].lm];
+                accb += 144.0 * tiles[ti].k;
                 if (accb >= bytes * next / G) {
                     cta_lo.push_back(ti + 1);
                     next++;

@@ -87,7 +87,9 @@ enum { SC_E = 0, SC_BAD, SC_ET, SC_BADT, SC_Q1R2, SC_DAMPL, SC_MODELP, SC_LAM, S
 enum { KID_LIN = 0, KID_MARG, KID_DAMP, KID_PRE, KID_MATVEC, KID_PCG, KID_BACKSUB, KID_COST, KID_N };
 
 struct TileRef {
-    int32_t lm, t;  // landmark (internal index) and 4-row tile index
+    int32_t lm, t;   // landmark (internal index) and 4-row tile index
+    int64_t off;     // float offset of the tile in the arena
+    int32_t k, pad;  // track length (tile bytes = 144 k)
 };
 
 struct LargeItem {
@@ -138,6 +140,10 @@ struct rba_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
+    // auxiliary streams: independent per-class kernels fork off the context stream and join back
+    static constexpr int NAUX = 3;
+    cudaStream_t aux[NAUX] = {nullptr, nullptr, nullptr};
+    cudaEvent_t ev_fork = nullptr, ev_join[NAUX] = {nullptr, nullptr, nullptr};
     int world = 1, rank = 0;
     ncclComm_t comm = nullptr;
     bool have_comm = false;

@@ -929,7 +929,8 @@ constexpr int SP_UNITCAP = 4 * SP_PACKCAP;          // work units per stage
 constexpr int SP_OFF_CAM = SMALL_STAGE_BYTES;
 constexpr int SP_OFF_PACK = SP_OFF_CAM + 4 * SP_CAMCAP;
 constexpr int SP_OFF_UNIT = SP_OFF_PACK + (int)sizeof(Pack) * SP_PACKCAP;
-constexpr int SP_SB = SP_OFF_UNIT + 2 * SP_UNITCAP;
+constexpr int SP_OFF_HDR = SP_OFF_UNIT + 2 * SP_UNITCAP;  // stage descriptor (written by the producer)
+constexpr int SP_SB = SP_OFF_HDR + 128;
 constexpr int SP_STAGES = 3;
 constexpr int SP_VCAP = 16384;                      // v (9 n_p floats) kept in shared memory if it fits
 constexpr size_t SP_SMEM = (size_t)SP_STAGES * SP_SB + 4 * SP_VCAP + 2 * SP_STAGES * sizeof(uint64_t);
@@ -1016,11 +1017,15 @@ __global__ void __launch_bounds__(SP_WARPS * 32 + 32, 1)
     __syncthreads();
     if (warp == SP_WARPS) {  // producer
         if (lane == 0) {
+            SmallChunk nxc{};
+            if (lo < hi) nxc = d.chunks[lo];
             for (int64_t i = lo; i < hi; i++) {
                 const int s = (int)((i - lo) % SP_STAGES);
                 const uint32_t ph = (uint32_t)(((i - lo) / SP_STAGES) & 1);
-                const SmallChunk ch = d.chunks[i];
+                const SmallChunk ch = nxc;
+                if (i + 1 < hi) nxc = d.chunks[i + 1];  // prefetch the next stage's descriptor
                 mbar_wait(&empty[s], ph ^ 1);
+                *reinterpret_cast<SmallChunk *>(sm + (size_t)s * SP_SB + SP_OFF_HDR) = ch;
                 mbar_arrive_expect_tx(&full[s], (uint32_t)ch.bytes + 4u * (uint32_t)ch.ncam +
                                                     (uint32_t)sizeof(Pack) * (uint32_t)ch.np + 2u * (uint32_t)ch.nunit);
                 unsigned char *dst = sm + (size_t)s * SP_SB;
@@ -1035,12 +1040,12 @@ __global__ void __launch_bounds__(SP_WARPS * 32 + 32, 1)
     for (int64_t i = lo; i < hi; i++) {
         const int s = (int)((i - lo) % SP_STAGES);
         const uint32_t ph = (uint32_t)(((i - lo) / SP_STAGES) & 1);
-        const SmallChunk ch = d.chunks[i];
         const unsigned char *stg = sm + (size_t)s * SP_SB;
         const int *scam = reinterpret_cast<const int *>(stg + SP_OFF_CAM);
         const Pack *spk = reinterpret_cast<const Pack *>(stg + SP_OFF_PACK);
         const uint16_t *sun = reinterpret_cast<const uint16_t *>(stg + SP_OFF_UNIT);
         mbar_wait(&full[s], ph);
+        const SmallChunk ch = *reinterpret_cast<const SmallChunk *>(stg + SP_OFF_HDR);
         for (int ui = warp; ui < (dbg == 1 ? 0 : ch.nunit); ui += SP_WARPS) {
             const int code = sun[ui];
             if (code == 0xFFFF) continue;
@@ -1105,25 +1110,38 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
     __syncthreads();
     if (tid >= C::NC) {  // ---------------- producer warp: one elected lane streams the tiles
         if (tid == C::NC) {
+            // descriptors (arena offset, k) of the next stage are loaded one stage ahead, as
+            // independent loads, so their latency overlaps the wait and the current copies
+            int64_t noff[NSLOT];
+            int nk[NSLOT];
+#pragma unroll
+            for (int sl = 0; sl < NSLOT; sl++) {
+                const int64_t ti = lo + sl;
+                nk[sl] = ti < hi ? tiles[ti].k : 0;
+                noff[sl] = ti < hi ? tiles[ti].off : 0;
+            }
             for (int64_t i = 0; i < nst; i++) {
                 const int s = (int)(i % C::STAGES);
                 const uint32_t ph = (uint32_t)((i / C::STAGES) & 1);
-                mbar_wait(&empty[s], ph ^ 1);
+                int64_t coff[NSLOT];
+                int ck[NSLOT];
                 uint32_t total = 0;
+#pragma unroll
                 for (int sl = 0; sl < NSLOT; sl++) {
-                    const int64_t ti = lo + i * NSLOT + sl;
-                    if (ti < hi) total += 144u * (uint32_t)d.lm_k[tiles[ti].lm];
+                    coff[sl] = noff[sl];
+                    ck[sl] = nk[sl];
+                    total += 144u * (uint32_t)ck[sl];
+                    const int64_t tn = lo + (i + 1) * NSLOT + sl;
+                    nk[sl] = tn < hi ? tiles[tn].k : 0;
+                    noff[sl] = tn < hi ? tiles[tn].off : 0;
                 }
+                mbar_wait(&empty[s], ph ^ 1);
                 mbar_arrive_expect_tx(&full[s], total);
-                for (int sl = 0; sl < NSLOT; sl++) {
-                    const int64_t ti = lo + i * NSLOT + sl;
-                    if (ti < hi) {
-                        const TileRef tr = tiles[ti];
-                        const int k = d.lm_k[tr.lm];
-                        const float *src = d.arena + d.lm_r2[tr.lm] + (int64_t)36 * k * tr.t;
-                        bulk_g2s(sm + (size_t)s * C::SB + (size_t)sl * C::TB, src, 144u * (uint32_t)k, &full[s]);
-                    }
-                }
+#pragma unroll
+                for (int sl = 0; sl < NSLOT; sl++)
+                    if (ck[sl])
+                        bulk_g2s(sm + (size_t)s * C::SB + (size_t)sl * C::TB, d.arena + coff[sl], 144u * (uint32_t)ck[sl],
+                                 &full[s]);
             }
         }
         return;
@@ -1148,13 +1166,13 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
         const uint32_t ph = (uint32_t)((i / C::STAGES) & 1);
         const int64_t ti = lo + i * NSLOT + slot;
         const bool have = ti < hi;  // uniform over the slot
-        TileRef tr{-1, 0};
+        TileRef tr{-1, 0, 0, 0, 0};
         if (have) {
             tr = tiles[ti];
             if (tr.lm != cur) {
                 flush();
                 cur = tr.lm;
-                k = d.lm_k[cur];
+                k = tr.k;
                 valid = o < k;
                 g = o >> 5;
                 ng = valid ? min(32, k - 32 * g) : 1;
@@ -1458,24 +1476,44 @@ cudaError_t launch_cam_scale(rba_ctx *c) {
 extern double plan_marg_bytes(rba_ctx *c);
 extern double plan_matvec_bytes(rba_ctx *c);
 
+// fork the context stream into the auxiliary streams (independent class kernels) and join back
+struct ForkJoin {
+    rba_ctx *c;
+    int next = 0;
+    explicit ForkJoin(rba_ctx *c_) : c(c_) {
+        cudaEventRecord(c->ev_fork, c->stream);
+        for (int i = 0; i < rba_ctx::NAUX; i++) cudaStreamWaitEvent(c->aux[i], c->ev_fork, 0);
+    }
+    cudaStream_t s() {  // round robin: context stream, aux 0, aux 1, ...
+        const int i = next++ % (rba_ctx::NAUX + 1);
+        return i == 0 ? c->stream : c->aux[i - 1];
+    }
+    void join() {
+        for (int i = 0; i < rba_ctx::NAUX; i++) {
+            cudaEventRecord(c->ev_join[i], c->aux[i]);
+            cudaStreamWaitEvent(c->stream, c->ev_join[i], 0);
+        }
+    }
+};
+
 template <int G>
-static cudaError_t marg_small_cls(rba_ctx *c, int cls, float lam) {
+static cudaError_t marg_small_cls(rba_ctx *c, int cls, float lam, cudaStream_t st) {
     const int64_t lo = c->pack_lo[cls], hi = c->pack_hi[cls];
     if (hi <= lo) return cudaSuccess;
     const size_t sm = (size_t)4 * (32 / G) * SmallTab<G>::FLOATS * sizeof(float);
-    k_marg_small<G><<<nblk(hi - lo, 4), 128, sm, c->stream>>>(c->d, lo, hi, lam, (float)c->opt.diag_min,
+    k_marg_small<G><<<nblk(hi - lo, 4), 128, sm, st>>>(c->d, lo, hi, lam, (float)c->opt.diag_min,
                                                               (float)c->opt.diag_max);
     c->launches++;
     return cudaGetLastError();
 }
 
 template <int NT>
-static cudaError_t marg_large_cls(rba_ctx *c, int cls, float lam) {
+static cudaError_t marg_large_cls(rba_ctx *c, int cls, float lam, cudaStream_t st) {
     const int64_t lo = c->marg_lo[cls], hi = c->marg_hi[cls];
     if (hi <= lo) return cudaSuccess;
     const size_t sm = (size_t)(4 * (2 * NT + 3) + 8 * NT) * sizeof(float);
     cudaFuncSetAttribute(k_marg_large<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_marg_large<NT><<<(unsigned)(hi - lo), NT, sm, c->stream>>>(c->d, c->d.marg_items + lo, lam,
+    k_marg_large<NT><<<(unsigned)(hi - lo), NT, sm, st>>>(c->d, c->d.marg_items + lo, lam,
                                                                   (float)c->opt.diag_min, (float)c->opt.diag_max);
     c->launches++;
     return cudaGetLastError();
@@ -1484,15 +1522,17 @@ static cudaError_t marg_large_cls(rba_ctx *c, int cls, float lam) {
 cudaError_t launch_marginalize(rba_ctx *c, float lam) {
     Prof P(c, KID_MARG, plan_marg_bytes(c));
     cudaError_t e;
-    if ((e = marg_large_cls<512>(c, 4, lam))) return e;
-    if ((e = marg_large_cls<256>(c, 3, lam))) return e;
-    if ((e = marg_large_cls<128>(c, 2, lam))) return e;
-    if ((e = marg_large_cls<64>(c, 1, lam))) return e;
-    if ((e = marg_large_cls<32>(c, 0, lam))) return e;
-    if ((e = marg_small_cls<16>(c, 3, lam))) return e;
-    if ((e = marg_small_cls<8>(c, 2, lam))) return e;
-    if ((e = marg_small_cls<4>(c, 1, lam))) return e;
-    if ((e = marg_small_cls<2>(c, 0, lam))) return e;
+    ForkJoin F(c);
+    if ((e = marg_large_cls<512>(c, 4, lam, F.s()))) return e;
+    if ((e = marg_large_cls<256>(c, 3, lam, F.s()))) return e;
+    if ((e = marg_large_cls<128>(c, 2, lam, F.s()))) return e;
+    if ((e = marg_large_cls<64>(c, 1, lam, F.s()))) return e;
+    if ((e = marg_large_cls<32>(c, 0, lam, F.s()))) return e;
+    if ((e = marg_small_cls<16>(c, 3, lam, F.s()))) return e;
+    if ((e = marg_small_cls<8>(c, 2, lam, F.s()))) return e;
+    if ((e = marg_small_cls<4>(c, 1, lam, F.s()))) return e;
+    if ((e = marg_small_cls<2>(c, 0, lam, F.s()))) return e;
+    F.join();
     P.end();
     return cudaSuccess;
 }
@@ -1507,30 +1547,33 @@ cudaError_t launch_redamp(rba_ctx *c, float lam) {
 }
 
 template <int NS, int NSLOT, bool PRE>
-static void large_pipe_cls(rba_ctx *c, int cls, const float *v, float *out, const PcgState *st) {
+static void large_pipe_cls(rba_ctx *c, int cls, const float *v, float *out, const PcgState *st, cudaStream_t ss) {
     const int64_t n = c->cta_n[cls];
     if (n <= 0) return;
     using Cf = PipeCfg<NS, NSLOT>;
     cudaFuncSetAttribute(k_large_pipe<NS, NSLOT, PRE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
-    k_large_pipe<NS, NSLOT, PRE><<<(unsigned)n, Cf::NC + 32, Cf::SMEM, c->stream>>>(
+    k_large_pipe<NS, NSLOT, PRE><<<(unsigned)n, Cf::NC + 32, Cf::SMEM, ss>>>(
         c->d, c->d.tiles, c->d.cta_lo + c->cta_off[cls], v, out, st);
     c->launches++;
 }
 
 template <bool PRE>
 static void pipes_all(rba_ctx *c, const float *v, float *out12, const PcgState *st) {
-    large_pipe_cls<512, 1, PRE>(c, 4, v, out12, st);
-    large_pipe_cls<256, 1, PRE>(c, 3, v, out12, st);
-    large_pipe_cls<128, 2, PRE>(c, 2, v, out12, st);
-    large_pipe_cls<64, 4, PRE>(c, 1, v, out12, st);
-    large_pipe_cls<32, 8, PRE>(c, 0, v, out12, st);
+    ForkJoin F(c);
+    // longest first so the short classes fill the long ones' tails
+    large_pipe_cls<512, 1, PRE>(c, 4, v, out12, st, F.s());
     if (c->chunk_ctas > 0) {
         cudaFuncSetAttribute(k_small_pipe<PRE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SP_SMEM);
         static const int dbg = getenv("RBA_DEBUG_SMALLPIPE") ? atoi(getenv("RBA_DEBUG_SMALLPIPE")) : 0;
-        k_small_pipe<PRE><<<(unsigned)c->chunk_ctas, SP_WARPS * 32 + 32, SP_SMEM, c->stream>>>(c->d, v, out12, st,
-                                                                                               PRE ? 0 : dbg);
+        k_small_pipe<PRE><<<(unsigned)c->chunk_ctas, SP_WARPS * 32 + 32, SP_SMEM, F.s()>>>(c->d, v, out12, st,
+                                                                                           PRE ? 0 : dbg);
         c->launches++;
     }
+    large_pipe_cls<256, 1, PRE>(c, 3, v, out12, st, F.s());
+    large_pipe_cls<128, 2, PRE>(c, 2, v, out12, st, F.s());
+    large_pipe_cls<64, 4, PRE>(c, 1, v, out12, st, F.s());
+    large_pipe_cls<32, 8, PRE>(c, 0, v, out12, st, F.s());
+    F.join();
 }
 
 cudaError_t launch_precond_rhs(rba_ctx *c) {
