@@ -19,8 +19,10 @@ landmark subsample of the same workload, on rank 0 only.
 from __future__ import annotations
 
 import argparse
+import glob
 import json
 import os
+import re
 import statistics
 import subprocess
 import sys
@@ -50,6 +52,32 @@ def peaks():
         d = json.load(open(p))
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json copy benchmark)"
     return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+MATVEC_KERNELS = re.compile(r"k_large_pipe<\d+, \d+, (0|false)>|k_small_pipe<(0|false)>|k_huge_y|k_huge_out<(0|false)>")
+MARG_KERNELS = re.compile(r"k_marg_(small|large)<")
+
+
+def ncu_traffic(cfg):
+    """DRAM bytes (read + write) of ONE launch of the matvec and of the marginalization, summed over
+    their per-class kernels, from the newest committed `ncu --set full` summary of this config
+    (profiles/r*_cfg<cfg>_ncu_full.json, written by tools/ncu_summary.py).  None if absent."""
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_cfg{cfg}_ncu_full.json")),
+                   key=lambda f: int(re.search(r"/r(\d+)_", f).group(1)))
+    if not files:
+        return None, None, None
+    rows = json.load(open(files[-1]))
+
+    def first_of_each(rx):
+        seen, tot = set(), 0.0
+        for r in rows:
+            name = r["kernel"].split("(")[0].replace("void ", "")
+            if rx.search(name) and name not in seen:
+                seen.add(name)
+                tot += r["dram_read_bytes"] + r["dram_write_bytes"]
+        return tot if seen else None
+
+    return first_of_each(MATVEC_KERNELS), first_of_each(MARG_KERNELS), os.path.relpath(files[-1], ROOT)
 
 
 class ClockSampler:
@@ -262,7 +290,7 @@ def main():
             cams, pts = s.state()
         barrier()
         t_e2e = max_over_ranks(time.perf_counter() - t0)
-        nb = (9 * n_p + 3 * n_l) * 4
+        nb = (9 * n_p + 3 * n_l) * 8  # FP64 state (host and device)
         e2e = {"value": args.steps / t_e2e, "unit": "LM iterations/s", "h2d_bytes_per_step": nb,
                "d2h_bytes_per_step": nb,
                "note": "per step: rba_set_state(host FP64 state) + rba_lm_step + rba_get_state(host); "
@@ -281,11 +309,16 @@ def main():
                 "traffic": None, "peak_source": peak_src, "launches": n, "avg_ms": ms / n,
                 "bytes_per_launch": by / n}
 
+    tr_mv, tr_mg, tr_src = ncu_traffic(args.config)
     roof_mv = roof(*prof["matvec"])
     if roof_mv:
+        roof_mv["traffic"] = tr_mv
+        roof_mv["traffic_source"] = tr_src
         roof_mv["kernel"] = "matvec (K5: k_matvec_small<G> + k_matvec_large), algorithmic 72k^2 B/landmark"
     roof_mg = roof(*mprof)
     if roof_mg:
+        roof_mg["traffic"] = tr_mg
+        roof_mg["traffic_source"] = tr_src
         roof_mg["kernel"] = "marginalize (K2: k_marg_small<G> + k_marg_large), algorithmic (2k+3)(9k+4)*4+48+20k B/landmark"
     total_prof = sum(shares.values())
     line = {

@@ -57,6 +57,7 @@ def lib():
             "orc_block_doubles": (I64, [P]),
             "orc_cost": (D, [P]),
             "orc_linearize": (I, [P]),
+            "orc_scaling": (I, [P]),
             "orc_marginalize": (I, [P]),
             "orc_damp": (I, [P, D]),
             "orc_undamp": (I, [P]),
@@ -138,7 +139,7 @@ class Oracle:
         self.h = L.orc_create(_p(self.cams0), self.n_p, _p(self.pts0), self.n_l, _p(self.obs_cam),
                               _p(self.obs_pt), _p(self.obs_uv), self.n_obs)
         if not self.h:
-            raise MemoryError("oracle: block allocation failed")
+            raise MemoryError("oracle: allocation failed")
         src = np.zeros(self.n_obs, np.int64)
         self.lm_ptr = np.zeros(self.n_l + 1, np.int64)
         L.orc_obs_order(self.h, _p(src), _p(self.lm_ptr))
@@ -152,7 +153,15 @@ class Oracle:
 
     # --- steps
     def linearize(self):
-        if lib().orc_linearize(self.h):
+        rc = lib().orc_linearize(self.h)
+        if rc == 3:
+            raise MemoryError("oracle: landmark-block allocation failed")
+        if rc:
+            raise ValueError("oracle: degenerate projection")
+
+    def linearize_scaling(self):
+        """O1-O2 only (residuals, Jacobians, E, scaling, D^2): no landmark blocks are allocated."""
+        if lib().orc_scaling(self.h):
             raise ValueError("oracle: degenerate projection")
 
     def marginalize(self):

@@ -288,8 +288,7 @@ orc_ctx *orc_create(const double *cams, int64_t n_p, const double *pts, int64_t 
         int64_t k = c->lm_ptr[j + 1] - c->lm_ptr[j];
         c->blk_off[j + 1] = c->blk_off[j] + (2 * k + 3) * (DP * k + 4); /* P:645 */
     }
-    c->blk = malloc(sizeof(double) * (size_t)c->blk_off[n_l]);
-    if (!c->blk) { orc_destroy(c); return NULL; }
+    c->blk = NULL; /* allocated by the first orc_linearize (orc_scaling needs no blocks) */
     c->giv = calloc(12 * n_l, sizeof(double));
     c->bt = malloc(sizeof(double) * DP * n_p);
     c->Lp = malloc(sizeof(double) * 81 * n_p);
@@ -343,9 +342,10 @@ static double cost_at(orc_ctx *c, const double *cams, const double *pts) {
 
 double orc_cost(orc_ctx *c) { return cost_at(c, c->cams, c->pts); }
 
-/* O1-O3: linearize at the current state, compute scaling and damping diagonals, assemble the
- * (undamped, unmarginalized) landmark blocks. */
-int orc_linearize(orc_ctx *c) {
+/* O1-O2: linearize at the current state (residuals, Jacobians, E) and compute the column scaling
+ * and damping diagonals.  Needs no landmark blocks (used alone on problems whose FP64 blocks do
+ * not fit in host memory). */
+int orc_scaling(orc_ctx *c) {
     int bad = 0;
 #pragma omp parallel for schedule(dynamic, 256) reduction(| : bad)
     for (int64_t j = 0; j < c->n_l; j++)
@@ -378,6 +378,20 @@ int orc_linearize(orc_ctx *c) {
             c->sl[3 * j + q] = sc;
             c->Dl2[3 * j + q] = clampd(s * sc * sc, 1e-6, 1e32);
         }
+    }
+    return 0;
+}
+
+/* O1-O3: orc_scaling, then assemble the (undamped, unmarginalized) landmark blocks.
+ * Returns 1 on a degenerate projection, 3 if the blocks cannot be allocated. */
+int orc_linearize(orc_ctx *c) {
+    if (orc_scaling(c)) return 1;
+    if (!c->blk) {
+        c->blk = malloc(sizeof(double) * (size_t)c->blk_off[c->n_l]);
+        if (!c->blk) return 3;
+    }
+#pragma omp parallel for schedule(dynamic, 256)
+    for (int64_t j = 0; j < c->n_l; j++) {
         /* O3: landmark block (Fig. 2b): rows 2i,2i+1 = obs i; pose cols 9i..9i+8;
          * landmark cols 9k..9k+2; residual col 9k+3; 3 zero damping rows at the bottom. */
         int64_t k = c->lm_ptr[j + 1] - c->lm_ptr[j];

@@ -386,7 +386,9 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     std::vector<LargeItem> marg_items;
     std::vector<TileRef> tiles;
     std::vector<int64_t> cta_lo;
-    const int ntb[5] = {32, 64, 128, 256, 512};
+    const int ntb[6] = {32, 64, 128, 256, 512, KMAX};
+    std::vector<HugeItem> huge_y, huge_out;
+    int64_t ybuf_n = 0;
     const int64_t large_lo = pos;
     for (int64_t i = pos; i < nl; i++) {
         const int k = c->h_k[i];
@@ -394,7 +396,7 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
         r2_total += large_r2_floats(k);
         c->max_large_k = std::max<int64_t>(c->max_large_k, k);
     }
-    for (int cls = 0; cls < 5; cls++) {
+    for (int cls = 0; cls < 6; cls++) {
         auto in_cls = [&](int k) { return k <= ntb[cls] && (cls == 0 || k > ntb[cls - 1]); };
         c->marg_lo[cls] = (int64_t)marg_items.size();
         const int64_t t_lo = (int64_t)tiles.size();
@@ -406,11 +408,24 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
             const int tpi2 = std::max(1, 262144 / (36 * k));
             for (int t0 = 0; t0 < T; t0 += tpi2)
                 marg_items.push_back(LargeItem{(int32_t)i, t0, std::min(T, t0 + tpi2), 0});
+            if (cls == 5) {
+                // huge (k > KLARGE): y pass per tile; out / precond pass per (HUGE_NT camera
+                // blocks, ~1 MB of tiles)
+                c->huge_max_k = std::max<int64_t>(c->huge_max_k, k);
+                for (int t = 0; t < T; t++) huge_y.push_back(HugeItem{(int32_t)i, 0, t, t + 1, ybuf_n});
+                const int tpo = std::max(1, (1 << 20) / (144 * HUGE_NT));
+                for (int o0 = 0; o0 < k; o0 += HUGE_NT)
+                    for (int t0 = 0; t0 < T; t0 += tpo)
+                        huge_out.push_back(HugeItem{(int32_t)i, o0, t0, std::min(T, t0 + tpo), ybuf_n});
+                ybuf_n += 4 * (int64_t)T;
+                continue;
+            }
             for (int t = 0; t < T; t++)
                 tiles.push_back(TileRef{(int32_t)i, t, c->h_r2[i] + (int64_t)36 * k * t, k, 0});
             bytes += 144.0 * k * T;
         }
         c->marg_hi[cls] = (int64_t)marg_items.size();
+        if (cls == 5) break;
         const int64_t t_hi = (int64_t)tiles.size();
         // persistent CTAs (one per SM) over contiguous tile ranges balanced by bytes
         c->cta_off[cls] = (int64_t)cta_lo.size();
@@ -463,7 +478,19 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     CKSC(dalloc_n(c, &d.lm_s, 3 * nl));
     CKSC(dalloc_n(c, &d.lm_D, 3 * nl));
     CKSC(dalloc_n(c, &d.arena, c->arena_floats));
-    CKSC(dalloc_n(c, &d.pacc, PACC_STRIDE * n_cams));
+    {
+        int nsm = 0;
+        CKSC(dalloc_n(c, &d.pcg, 1));
+        CKC(query_nsmid(c, reinterpret_cast<int *>(d.pcg), &nsm));
+        d.nslice = std::max(nsm, 1);
+    }
+    CKSC(dalloc_n(c, &d.psl, (int64_t)d.nslice * PACC_STRIDE * n_cams));
+    CKSC(dalloc_n(c, &d.wsl, (int64_t)d.nslice * 12 * n_cams));
+    CKC(cudaMemsetAsync(d.psl, 0, sizeof(float) * d.nslice * PACC_STRIDE * n_cams, c->stream));
+    CKC(cudaMemsetAsync(d.wsl, 0, sizeof(float) * d.nslice * 12 * n_cams, c->stream));
+    CKSC(dalloc_n(c, &d.pd, 54 * n_cams));
+    CKSC(dalloc_n(c, &d.wd, 9 * n_cams));
+    CKSC(dalloc_n(c, &d.p32, 9 * n_cams));
     CKSC(dalloc_n(c, &d.bt, 9 * n_cams));
     CKSC(dalloc_n(c, &d.Minv, 81 * n_cams));
     CKSC(dalloc_n(c, &d.x, 9 * n_cams));
@@ -473,7 +500,6 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     CKSC(dalloc_n(c, &d.w, 9 * n_cams));
     CKSC(dalloc_n(c, &d.dl, 3 * nl));
     CKSC(dalloc_n(c, &d.scal, SC_N));
-    CKSC(dalloc_n(c, &d.pcg, 1));
     CKSC(dalloc_n(c, &d.packs, std::max<size_t>(1, packs.size())));
     CKSC(dalloc_n(c, &d.marg_items, std::max<size_t>(1, marg_items.size())));
     CKSC(dalloc_n(c, &d.tiles, std::max<size_t>(1, tiles.size())));
@@ -481,17 +507,20 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     CKSC(dalloc_n(c, &d.chunks, std::max<size_t>(1, chunks.size())));
     CKSC(dalloc_n(c, &d.units, std::max<size_t>(8, units.size())));
     CKSC(dalloc_n(c, &d.chunk_lo, std::max<size_t>(1, chunk_lo.size())));
-    CKSC(dalloc_n(c, &d.w12, 12 * n_cams));
+    c->n_huge_y = (int64_t)huge_y.size();
+    c->n_huge_out = (int64_t)huge_out.size();
+    CKSC(dalloc_n(c, &d.huge_y, std::max<size_t>(1, huge_y.size())));
+    CKSC(dalloc_n(c, &d.huge_out, std::max<size_t>(1, huge_out.size())));
+    CKSC(dalloc_n(c, &d.ybuf, std::max<int64_t>(4, ybuf_n)));
     CKC(cudaMallocHost(&c->h_scal, sizeof(double) * SC_N));
     CKC(cudaMallocHost(&c->h_pcg, sizeof(PcgState)));
     // ---- upload (host staging in the device layout)
     {
-        std::vector<float> hc(9 * n_cams), hp(3 * std::max<int64_t>(nl, 1));
-        for (int64_t i = 0; i < 9 * n_cams; i++) hc[i] = (float)cameras[i];
+        std::vector<double> hc(cameras, cameras + 9 * n_cams), hp(3 * std::max<int64_t>(nl, 1));
         for (int64_t i = 0; i < nl; i++)
-            for (int q = 0; q < 3; q++) hp[3 * i + q] = (float)points[3 * (int64_t)loc[i] + q];
+            for (int q = 0; q < 3; q++) hp[3 * i + q] = points[3 * (int64_t)loc[i] + q];
         std::vector<int32_t> ocam(std::max<int64_t>(nobs_loc, 1)), olm(std::max<int64_t>(nobs_loc, 1));
-        std::vector<float2> ouv(std::max<int64_t>(nobs_loc, 1));
+        std::vector<double2> ouv(std::max<int64_t>(nobs_loc, 1));
         for (int64_t i = 0; i < nl; i++) {
             const int64_t g0 = gptr[loc[i]];
             for (int o = 0; o < c->h_k[i]; o++) {
@@ -499,11 +528,11 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
                 const int64_t dst = h_obs0[i] + o;
                 ocam[dst] = obs_cam[src];
                 olm[dst] = (int32_t)i;
-                ouv[dst] = make_float2((float)obs_uv[2 * src], (float)obs_uv[2 * src + 1]);
+                ouv[dst] = make_double2(obs_uv[2 * src], obs_uv[2 * src + 1]);
             }
         }
-        CKC(cudaMemcpyAsync(d.cams, hc.data(), sizeof(float) * hc.size(), cudaMemcpyHostToDevice, c->stream));
-        CKC(cudaMemcpyAsync(d.pts, hp.data(), sizeof(float) * 3 * nl, cudaMemcpyHostToDevice, c->stream));
+        CKC(cudaMemcpyAsync(d.cams, hc.data(), sizeof(double) * hc.size(), cudaMemcpyHostToDevice, c->stream));
+        CKC(cudaMemcpyAsync(d.pts, hp.data(), sizeof(double) * 3 * nl, cudaMemcpyHostToDevice, c->stream));
         CKC(cudaMemcpyAsync(d.lm_k, c->h_k.data(), sizeof(int32_t) * nl, cudaMemcpyHostToDevice, c->stream));
         CKC(cudaMemcpyAsync(d.lm_obs0, h_obs0.data(), sizeof(int32_t) * nl, cudaMemcpyHostToDevice, c->stream));
         CKC(cudaMemcpyAsync(d.lm_r2, c->h_r2.data(), sizeof(int64_t) * nl, cudaMemcpyHostToDevice, c->stream));
@@ -511,7 +540,7 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
         CKC(cudaMemsetAsync(d.obs_cam + nobs_loc, 0, sizeof(int32_t) * 8, c->stream));
         CKC(cudaMemcpyAsync(d.obs_cam, ocam.data(), sizeof(int32_t) * nobs_loc, cudaMemcpyHostToDevice, c->stream));
         CKC(cudaMemcpyAsync(d.obs_lm, olm.data(), sizeof(int32_t) * nobs_loc, cudaMemcpyHostToDevice, c->stream));
-        CKC(cudaMemcpyAsync(d.obs_uv, ouv.data(), sizeof(float2) * nobs_loc, cudaMemcpyHostToDevice, c->stream));
+        CKC(cudaMemcpyAsync(d.obs_uv, ouv.data(), sizeof(double2) * nobs_loc, cudaMemcpyHostToDevice, c->stream));
         CKC(cudaMemcpyAsync(d.lm_pk, c->h_pk.data(), sizeof(int32_t) * nl, cudaMemcpyHostToDevice, c->stream));
         if (!packs.empty())
             CKC(cudaMemcpyAsync(d.packs, packs.data(), sizeof(Pack) * packs.size(), cudaMemcpyHostToDevice, c->stream));
@@ -526,6 +555,12 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
                                 c->stream));
         CKC(cudaMemcpyAsync(d.chunk_lo, chunk_lo.data(), sizeof(int64_t) * chunk_lo.size(), cudaMemcpyHostToDevice,
                             c->stream));
+        if (!huge_y.empty())
+            CKC(cudaMemcpyAsync(d.huge_y, huge_y.data(), sizeof(HugeItem) * huge_y.size(), cudaMemcpyHostToDevice,
+                                c->stream));
+        if (!huge_out.empty())
+            CKC(cudaMemcpyAsync(d.huge_out, huge_out.data(), sizeof(HugeItem) * huge_out.size(),
+                                cudaMemcpyHostToDevice, c->stream));
         if (!tiles.empty())
             CKC(cudaMemcpyAsync(d.tiles, tiles.data(), sizeof(TileRef) * tiles.size(), cudaMemcpyHostToDevice,
                                 c->stream));
@@ -618,10 +653,9 @@ extern "C" rba_status rba_pcg_solve(rba_ctx *c, rba_pcg_stats *stats) {
     CK(cudaSetDevice(c->device));
     DevProblem &d = c->d;
     const float lam = (float)c->lambda_blocks;
-    CK(cudaMemsetAsync(d.pacc, 0, sizeof(float) * PACC_STRIDE * d.n_p, c->stream));
     CK(cudaMemsetAsync(d.scal + SC_BAD, 0, sizeof(double), c->stream));
     CK(launch_precond_rhs(c));
-    CKS(allreduce(c, d.pacc, PACC_STRIDE * d.n_p, ncclFloat));
+    CKS(allreduce(c, d.pd, 54 * d.n_p, ncclDouble));
     CK(launch_precond_finalize(c, lam));
     CK(launch_pcg_init(c, (float)c->opt.pcg_rel_tol, c->opt.pcg_max_iters));
     static const bool no_graph = getenv("RBA_NO_GRAPH") != nullptr;
@@ -648,9 +682,8 @@ extern "C" rba_status rba_pcg_solve(rba_ctx *c, rba_pcg_stats *stats) {
         if (c->h_pcg->done || c->h_pcg->it >= c->opt.pcg_max_iters) break;
         const int todo = std::min(batch, c->opt.pcg_max_iters - c->h_pcg->it);
         for (int b = 0; b < todo; b++) {
-            CK(cudaMemsetAsync(d.w12, 0, sizeof(float) * 12 * d.n_p, c->stream));
             CK(launch_matvec_pcg(c));
-            CKS(allreduce(c, d.w12, 12 * d.n_p, ncclFloat));
+            CKS(allreduce(c, d.wd, 9 * d.n_p, ncclDouble));
             CK(launch_pcg_step(c, lam, (float)c->opt.pcg_rel_tol, c->opt.pcg_max_iters));
         }
         batch = std::min(batch * 2, 64);
@@ -725,8 +758,8 @@ extern "C" rba_status rba_lm_step(rba_ctx *c, rba_lm_report *rep) {
         R.rho = rho;
         accept = model > 0 && std::isfinite(Et) && rho > c->opt.min_rel_decrease;
         if (accept) {
-            CK(cudaMemcpyAsync(d.cams, d.cams_trial, sizeof(float) * 9 * d.n_p, cudaMemcpyDeviceToDevice, c->stream));
-            CK(cudaMemcpyAsync(d.pts, d.pts_trial, sizeof(float) * 3 * d.n_l, cudaMemcpyDeviceToDevice, c->stream));
+            CK(cudaMemcpyAsync(d.cams, d.cams_trial, sizeof(double) * 9 * d.n_p, cudaMemcpyDeviceToDevice, c->stream));
+            CK(cudaMemcpyAsync(d.pts, d.pts_trial, sizeof(double) * 3 * d.n_l, cudaMemcpyDeviceToDevice, c->stream));
             c->cost = Et;
             const double t = 2.0 * rho - 1.0;
             c->lm_lambda *= std::max(1.0 / 3.0, 1.0 - t * t * t);
@@ -753,19 +786,19 @@ extern "C" rba_status rba_get_state(rba_ctx *c, double *cameras, double *points)
     if (!c || !cameras || !points) return fail(RBA_ERR_INVALID_ARG, "null argument");
     CK(cudaSetDevice(c->device));
     const DevProblem &d = c->d;
-    std::vector<float> hc(9 * d.n_p), hp(3 * c->n_l_global, 0.f), loc(3 * std::max<int64_t>(d.n_l, 1));
-    CK(cudaMemcpyAsync(hc.data(), d.cams, sizeof(float) * hc.size(), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaMemcpyAsync(loc.data(), d.pts, sizeof(float) * 3 * d.n_l, cudaMemcpyDeviceToHost, c->stream));
+    std::vector<double> hc(9 * d.n_p), hp(3 * c->n_l_global, 0.0), loc(3 * std::max<int64_t>(d.n_l, 1));
+    CK(cudaMemcpyAsync(hc.data(), d.cams, sizeof(double) * hc.size(), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(loc.data(), d.pts, sizeof(double) * 3 * d.n_l, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     for (int64_t i = 0; i < d.n_l; i++)
         for (int q = 0; q < 3; q++) hp[3 * (int64_t)c->lm_orig[i] + q] = loc[3 * i + q];
     if (c->have_comm) {
-        float *buf = nullptr;
-        CK(cudaMalloc(&buf, sizeof(float) * std::max<int64_t>(1, hp.size())));
-        CK(cudaMemcpyAsync(buf, hp.data(), sizeof(float) * hp.size(), cudaMemcpyHostToDevice, c->stream));
-        rba_status s = allreduce(c, buf, hp.size(), ncclFloat);
+        double *buf = nullptr;
+        CK(cudaMalloc(&buf, sizeof(double) * std::max<int64_t>(1, hp.size())));
+        CK(cudaMemcpyAsync(buf, hp.data(), sizeof(double) * hp.size(), cudaMemcpyHostToDevice, c->stream));
+        rba_status s = allreduce(c, buf, hp.size(), ncclDouble);
         if (s == RBA_OK) {
-            CK(cudaMemcpyAsync(hp.data(), buf, sizeof(float) * hp.size(), cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaMemcpyAsync(hp.data(), buf, sizeof(double) * hp.size(), cudaMemcpyDeviceToHost, c->stream));
             CK(cudaStreamSynchronize(c->stream));
         }
         cudaFree(buf);
@@ -780,12 +813,11 @@ extern "C" rba_status rba_set_state(rba_ctx *c, const double *cameras, const dou
     if (!c || !cameras || !points) return fail(RBA_ERR_INVALID_ARG, "null argument");
     CK(cudaSetDevice(c->device));
     const DevProblem &d = c->d;
-    std::vector<float> hc(9 * d.n_p), hp(3 * std::max<int64_t>(d.n_l, 1));
-    for (size_t i = 0; i < hc.size(); i++) hc[i] = (float)cameras[i];
+    std::vector<double> hp(3 * std::max<int64_t>(d.n_l, 1));
     for (int64_t i = 0; i < d.n_l; i++)
-        for (int q = 0; q < 3; q++) hp[3 * i + q] = (float)points[3 * (int64_t)c->lm_orig[i] + q];
-    CK(cudaMemcpyAsync(d.cams, hc.data(), sizeof(float) * hc.size(), cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(d.pts, hp.data(), sizeof(float) * 3 * d.n_l, cudaMemcpyHostToDevice, c->stream));
+        for (int q = 0; q < 3; q++) hp[3 * i + q] = points[3 * (int64_t)c->lm_orig[i] + q];
+    CK(cudaMemcpyAsync(d.cams, cameras, sizeof(double) * 9 * d.n_p, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(d.pts, hp.data(), sizeof(double) * 3 * d.n_l, cudaMemcpyHostToDevice, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     c->linearized = c->marginalized = c->solved = c->backsubbed = false;
     c->need_lin = true;
@@ -805,9 +837,8 @@ extern "C" rba_status rba_matvec(rba_ctx *c, const float *v, float *outv) {
     if (!c || !v || !outv) return fail(RBA_ERR_INVALID_ARG, "null argument");
     if (!c->marginalized) return fail(RBA_ERR_STATE, "rba_matvec before rba_marginalize_qr");
     CK(cudaSetDevice(c->device));
-    CK(cudaMemsetAsync(c->d.w12, 0, sizeof(float) * 12 * c->d.n_p, c->stream));
     CK(launch_matvec(c, v, outv));
-    CKS(allreduce(c, c->d.w12, 12 * c->d.n_p, ncclFloat));
+    CKS(allreduce(c, c->d.wd, 9 * c->d.n_p, ncclDouble));
     CK(launch_add_damping(c, v, outv, (float)c->lambda_blocks));
     c->prof_real_matvecs++;
     return RBA_OK;
@@ -816,21 +847,18 @@ extern "C" rba_status rba_matvec(rba_ctx *c, const float *v, float *outv) {
 extern "C" rba_status rba_get_rhs(rba_ctx *c, double *b) {
     if (!c || !b) return fail(RBA_ERR_INVALID_ARG, "null argument");
     if (!c->solved) return fail(RBA_ERR_STATE, "rba_get_rhs before rba_pcg_solve");
-    std::vector<float> h(9 * c->d.n_p);
-    CK(cudaMemcpyAsync(h.data(), c->d.bt, sizeof(float) * h.size(), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(b, c->d.bt, sizeof(double) * 9 * c->d.n_p, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    for (size_t i = 0; i < h.size(); i++) b[i] = h[i];
     return RBA_OK;
 }
 
 extern "C" rba_status rba_get_step(rba_ctx *c, double *dp, double *dl) {
     if (!c || !dp || !dl) return fail(RBA_ERR_INVALID_ARG, "null argument");
     if (!c->solved) return fail(RBA_ERR_STATE, "rba_get_step before rba_pcg_solve");
-    std::vector<float> h(9 * c->d.n_p), l(3 * std::max<int64_t>(c->d.n_l, 1));
-    CK(cudaMemcpyAsync(h.data(), c->d.x, sizeof(float) * h.size(), cudaMemcpyDeviceToHost, c->stream));
+    std::vector<float> l(3 * std::max<int64_t>(c->d.n_l, 1));
+    CK(cudaMemcpyAsync(dp, c->d.x, sizeof(double) * 9 * c->d.n_p, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(l.data(), c->d.dl, sizeof(float) * 3 * c->d.n_l, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    for (size_t i = 0; i < h.size(); i++) dp[i] = h[i];
     for (int64_t i = 0; i < 3 * c->n_l_global; i++) dl[i] = 0.0;
     if (c->backsubbed)
         for (int64_t i = 0; i < c->d.n_l; i++)

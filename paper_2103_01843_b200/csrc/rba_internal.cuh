@@ -13,7 +13,8 @@
 namespace rba {
 
 constexpr int KSMALL = 16;    // k <= KSMALL: warp-group kernels over packs of same-k landmarks
-constexpr int KMAX = 512;     // largest track length supported by this build's large-k kernels
+constexpr int KLARGE = 512;   // k <= KLARGE: one thread per camera block in the large-k kernels
+constexpr int KMAX = 3072;    // largest track length supported (k > KLARGE: "huge" path, smem-bound)
 
 // ---- landmark-block arena layout ------------------------------------------
 // Logical block of a landmark with k observations: rows 0..2k+2, columns [J_p (9k) | J_l | r].
@@ -96,24 +97,39 @@ struct LargeItem {
     int32_t lm, t0, t1, pad;  // landmark (internal index) and tile range [t0, t1)
 };
 
+// Huge landmarks (k > KLARGE): work item of the two-pass matvec / preconditioner.
+//  y pass:  (lm, t0 = t1 - 1 = tile)            y[yoff + 4t + r] = (A v) of row 4t + r
+//  out pass: (lm, o0 = first camera block, [t0, t1) tiles)   out_o += sum_t slab_{o,t}^T y_t
+struct HugeItem {
+    int32_t lm, o0, t0, t1;
+    int64_t yoff;
+};
+constexpr int HUGE_NT = 256;  // threads per CTA of the huge-k passes (camera blocks per out item)
+
 struct DevProblem {
     int64_t n_p, n_l, n_obs;  // local counts (landmarks / observations of this shard)
     // state
-    float *cams, *cams_trial, *pts, *pts_trial;
+    double *cams, *cams_trial, *pts, *pts_trial;  // FP64 state (reading C23)
     // landmark metadata (internal order, sorted by k)
     int32_t *lm_k, *lm_obs0, *lm_pk;
     int64_t *lm_r2, *lm_side;
     int32_t *obs_cam, *obs_lm;
-    float2 *obs_uv;
+    double2 *obs_uv;
     // scaling / damping
     float *cam_n2, *sp, *Dp2;
     float *lm_s, *lm_D;
     // arena
     float *arena;
     // reduced system / PCG
-    float *pacc;  // PACC_STRIDE per camera: 45 upper-triangle of P_i + 9 of b~ (+2 pad)
-    float *bt, *Minv;
-    float *x, *r, *z, *p, *w;
+    // camera-space sums of K4 / K5: FP32 per-SM slices (nslice of them), FP64 after k_reduce_slices
+    float *psl;   // K4: PACC_STRIDE per camera per slice: 45 upper-triangle of P_i + 9 of b~ (+2 pad)
+    float *wsl;   // K5: 12 per camera per slice (9 used; 16-byte aligned float4 atomics)
+    double *pd;   // K4 reduced: 54 per camera
+    double *wd;   // K5 reduced: 9 per camera
+    int nslice;
+    double *bt, *Minv;                // b~ (9 n_p), block-Jacobi inverse (81 n_p), FP64
+    double *x, *r, *z, *p, *w;        // PCG vectors (FP64, reading C24)
+    float *p32;                       // p rounded to FP32: the matvec input
     float *dl;
     double *scal;
     PcgState *pcg;
@@ -123,8 +139,9 @@ struct DevProblem {
     TileRef *tiles;         // K4/K5 tile stream of the large landmarks, classes k <= 32, 64, 128, 256, 512
     SmallChunk *chunks;     // K4/K5 stage stream of the small-k packs
     int64_t *chunk_lo;      // tile-range boundaries of the persistent CTAs over the chunks
-    float *w12;             // matvec accumulator, camera stride 12 (16-byte aligned float4 atomics)
     int64_t *cta_lo;        // per class: tile range boundaries of the persistent CTAs (bytes-balanced)
+    HugeItem *huge_y, *huge_out;  // k > KLARGE: y-pass items (one per tile), out/precond items
+    float *ybuf;                  // k > KLARGE: y = A v, 4 floats per 4-row tile
 };
 
 struct Launch {
@@ -156,7 +173,8 @@ struct rba_ctx {
     std::vector<int64_t> h_r2, h_side;
     std::vector<int32_t> h_pk;
     int64_t pack_lo[4] = {0, 0, 0, 0}, pack_hi[4] = {0, 0, 0, 0};  // G = 2, 4, 8, 16 pack ranges
-    int64_t marg_lo[5] = {0, 0, 0, 0, 0}, marg_hi[5] = {0, 0, 0, 0, 0};  // K2 large items per class
+    int64_t marg_lo[6] = {0, 0, 0, 0, 0, 0}, marg_hi[6] = {0, 0, 0, 0, 0, 0};  // K2 large items per class
+    int64_t n_huge_y = 0, n_huge_out = 0, huge_max_k = 0;  // k > KLARGE (two-pass matvec)
     int64_t cta_off[5] = {0, 0, 0, 0, 0}, cta_n[5] = {0, 0, 0, 0, 0};    // K4/K5 CTA ranges per class
     int64_t n_chunks = 0, chunk_ctas = 0;
     int64_t n_packs = 0, max_large_k = 0;
@@ -189,6 +207,7 @@ struct rba_ctx {
 namespace rba {
 // kernel launchers (rba_kernels.cu); each returns cudaGetLastError()
 cudaError_t launch_check_depth(rba_ctx *c, int *d_bad);
+cudaError_t query_nsmid(rba_ctx *c, int *d_scratch, int *out);
 cudaError_t launch_linearize(rba_ctx *c);
 cudaError_t launch_cam_scale(rba_ctx *c);
 cudaError_t launch_marginalize(rba_ctx *c, float lambda);

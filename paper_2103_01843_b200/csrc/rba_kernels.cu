@@ -28,77 +28,79 @@ namespace rba {
 // BAL / Snavely (readings C1, C2, C22): P = R(w) X + t, p = -P_xy / P_z,
 // d = 1 + k1 |p|^2 + k2 |p|^4, pi = f d p, r = pi - u.  Jacobians for the additive update of all
 // 9 camera parameters: dP/dw = -[R X]_x J_left(w).  Returns P_z.
-__device__ __forceinline__ float cam_model(const float *__restrict__ cam, float X0, float X1, float X2, float u,
-                                           float v, float *r, float *Jc, float *Jl) {
-    const float w0 = cam[0], w1 = cam[1], w2 = cam[2];
-    const float th2 = w0 * w0 + w1 * w1 + w2 * w2;
-    float a, b, cc;  // R = I + a K + b K^2, J_left = I + b K + cc K^2
-    if (th2 < 1e-8f) {
-        a = 1.f - th2 * (1.f / 6.f);
-        b = 0.5f - th2 * (1.f / 24.f);
-        cc = 1.f / 6.f - th2 * (1.f / 120.f);
+// Evaluated in FP64 from the FP64 state (reading C23): residuals r in FP64, the
+// Jacobians rounded to FP32 on output.  Everything downstream (blocks, QR, RCS, PCG) is FP32.
+__device__ __forceinline__ double cam_model(const double *__restrict__ cam, double X0, double X1, double X2,
+                                            double u, double v, double *r, float *Jc, float *Jl) {
+    const double w0 = cam[0], w1 = cam[1], w2 = cam[2];
+    const double th2 = w0 * w0 + w1 * w1 + w2 * w2;
+    double a, b, cc;  // R = I + a K + b K^2, J_left = I + b K + cc K^2
+    if (th2 < 1e-16) {
+        a = 1. - th2 * (1. / 6.);
+        b = 0.5 - th2 * (1. / 24.);
+        cc = 1. / 6. - th2 * (1. / 120.);
     } else {
-        const float th = sqrtf(th2);
-        float s, co;
-        sincosf(th, &s, &co);
+        const double th = sqrt(th2);
+        double s, co;
+        sincos(th, &s, &co);
         a = s / th;
-        const float hs = sinf(0.5f * th);
-        b = 2.f * hs * hs / th2;  // (1 - cos th) / th^2 without cancellation
-        cc = (th < 0.5f) ? (1.f / 6.f - th2 * (1.f / 120.f) + th2 * th2 * (1.f / 5040.f)) : (th - s) / (th2 * th);
+        const double hs = sin(0.5 * th);
+        b = 2. * hs * hs / th2;  // (1 - cos th) / th^2 without cancellation
+        cc = (th < 1e-2) ? (1.0 / 6.0 - th2 * (1.0 / 120.0) + th2 * th2 * (1.0 / 5040.0)) : (th - s) / (th2 * th);
     }
-    const float cx0 = w1 * X2 - w2 * X1, cx1 = w2 * X0 - w0 * X2, cx2 = w0 * X1 - w1 * X0;
-    const float dx0 = w1 * cx2 - w2 * cx1, dx1 = w2 * cx0 - w0 * cx2, dx2 = w0 * cx1 - w1 * cx0;
-    const float RX0 = X0 + a * cx0 + b * dx0, RX1 = X1 + a * cx1 + b * dx1, RX2 = X2 + a * cx2 + b * dx2;
-    const float P0 = RX0 + cam[3], P1 = RX1 + cam[4], P2 = RX2 + cam[5];
-    const float iz = -1.f / P2;
-    const float px = P0 * iz, py = P1 * iz;
-    const float n = px * px + py * py;
-    const float f = cam[6], k1 = cam[7], k2 = cam[8];
-    const float dd = 1.f + k1 * n + k2 * n * n;
+    const double cx0 = w1 * X2 - w2 * X1, cx1 = w2 * X0 - w0 * X2, cx2 = w0 * X1 - w1 * X0;
+    const double dx0 = w1 * cx2 - w2 * cx1, dx1 = w2 * cx0 - w0 * cx2, dx2 = w0 * cx1 - w1 * cx0;
+    const double RX0 = X0 + a * cx0 + b * dx0, RX1 = X1 + a * cx1 + b * dx1, RX2 = X2 + a * cx2 + b * dx2;
+    const double P0 = RX0 + cam[3], P1 = RX1 + cam[4], P2 = RX2 + cam[5];
+    const double iz = -1. / P2;
+    const double px = P0 * iz, py = P1 * iz;
+    const double n = px * px + py * py;
+    const double f = cam[6], k1 = cam[7], k2 = cam[8];
+    const double dd = 1. + k1 * n + k2 * n * n;
     r[0] = f * dd * px - u;
     r[1] = f * dd * py - v;
     if (!Jc) return P2;
     // dpi/dP = f (d I + e p p^T) * iz [[1,0,px],[0,1,py]]
-    const float e = 2.f * (k1 + 2.f * k2 * n);
-    const float D00 = f * (dd + e * px * px), D01 = f * e * px * py, D11 = f * (dd + e * py * py);
-    const float A00 = iz * D00, A01 = iz * D01, A02 = iz * (D00 * px + D01 * py);
-    const float A10 = iz * D01, A11 = iz * D11, A12 = iz * (D01 * px + D11 * py);
+    const double e = 2. * (k1 + 2. * k2 * n);
+    const double D00 = f * (dd + e * px * px), D01 = f * e * px * py, D11 = f * (dd + e * py * py);
+    const double A00 = iz * D00, A01 = iz * D01, A02 = iz * (D00 * px + D01 * py);
+    const double A10 = iz * D01, A11 = iz * D11, A12 = iz * (D01 * px + D11 * py);
     // R = (1 - b th2) I + a K + b w w^T
-    const float rd = 1.f - b * th2;
-    const float R00 = rd + b * w0 * w0, R11 = rd + b * w1 * w1, R22 = rd + b * w2 * w2;
-    const float R01 = -a * w2 + b * w0 * w1, R02 = a * w1 + b * w0 * w2;
-    const float R10 = a * w2 + b * w0 * w1, R12 = -a * w0 + b * w1 * w2;
-    const float R20 = -a * w1 + b * w0 * w2, R21 = a * w0 + b * w1 * w2;
-    Jl[0] = A00 * R00 + A01 * R10 + A02 * R20;
-    Jl[1] = A00 * R01 + A01 * R11 + A02 * R21;
-    Jl[2] = A00 * R02 + A01 * R12 + A02 * R22;
-    Jl[3] = A10 * R00 + A11 * R10 + A12 * R20;
-    Jl[4] = A10 * R01 + A11 * R11 + A12 * R21;
-    Jl[5] = A10 * R02 + A11 * R12 + A12 * R22;
+    const double rd = 1. - b * th2;
+    const double R00 = rd + b * w0 * w0, R11 = rd + b * w1 * w1, R22 = rd + b * w2 * w2;
+    const double R01 = -a * w2 + b * w0 * w1, R02 = a * w1 + b * w0 * w2;
+    const double R10 = a * w2 + b * w0 * w1, R12 = -a * w0 + b * w1 * w2;
+    const double R20 = -a * w1 + b * w0 * w2, R21 = a * w0 + b * w1 * w2;
+    Jl[0] = (float)(A00 * R00 + A01 * R10 + A02 * R20);
+    Jl[1] = (float)(A00 * R01 + A01 * R11 + A02 * R21);
+    Jl[2] = (float)(A00 * R02 + A01 * R12 + A02 * R22);
+    Jl[3] = (float)(A10 * R00 + A11 * R10 + A12 * R20);
+    Jl[4] = (float)(A10 * R01 + A11 * R11 + A12 * R21);
+    Jl[5] = (float)(A10 * R02 + A11 * R12 + A12 * R22);
     // J_left = (1 - cc th2) I + b K + cc w w^T
-    const float jd = 1.f - cc * th2;
-    const float L00 = jd + cc * w0 * w0, L11 = jd + cc * w1 * w1, L22 = jd + cc * w2 * w2;
-    const float L01 = -b * w2 + cc * w0 * w1, L02 = b * w1 + cc * w0 * w2;
-    const float L10 = b * w2 + cc * w0 * w1, L12 = -b * w0 + cc * w1 * w2;
-    const float L20 = -b * w1 + cc * w0 * w2, L21 = b * w0 + cc * w1 * w2;
+    const double jd = 1. - cc * th2;
+    const double L00 = jd + cc * w0 * w0, L11 = jd + cc * w1 * w1, L22 = jd + cc * w2 * w2;
+    const double L01 = -b * w2 + cc * w0 * w1, L02 = b * w1 + cc * w0 * w2;
+    const double L10 = b * w2 + cc * w0 * w1, L12 = -b * w0 + cc * w1 * w2;
+    const double L20 = -b * w1 + cc * w0 * w2, L21 = b * w0 + cc * w1 * w2;
     // B = A [RX]_x,  [RX]_x = [[0,-RX2,RX1],[RX2,0,-RX0],[-RX1,RX0,0]]
-    const float B00 = A01 * RX2 - A02 * RX1, B01 = -A00 * RX2 + A02 * RX0, B02 = A00 * RX1 - A01 * RX0;
-    const float B10 = A11 * RX2 - A12 * RX1, B11 = -A10 * RX2 + A12 * RX0, B12 = A10 * RX1 - A11 * RX0;
+    const double B00 = A01 * RX2 - A02 * RX1, B01 = -A00 * RX2 + A02 * RX0, B02 = A00 * RX1 - A01 * RX0;
+    const double B10 = A11 * RX2 - A12 * RX1, B11 = -A10 * RX2 + A12 * RX0, B12 = A10 * RX1 - A11 * RX0;
     // d/dw = -B J_left
-    Jc[0] = -(B00 * L00 + B01 * L10 + B02 * L20);
-    Jc[1] = -(B00 * L01 + B01 * L11 + B02 * L21);
-    Jc[2] = -(B00 * L02 + B01 * L12 + B02 * L22);
-    Jc[9] = -(B10 * L00 + B11 * L10 + B12 * L20);
-    Jc[10] = -(B10 * L01 + B11 * L11 + B12 * L21);
-    Jc[11] = -(B10 * L02 + B11 * L12 + B12 * L22);
-    Jc[3] = A00; Jc[4] = A01; Jc[5] = A02;
-    Jc[12] = A10; Jc[13] = A11; Jc[14] = A12;
-    Jc[6] = dd * px; Jc[7] = f * n * px; Jc[8] = f * n * n * px;
-    Jc[15] = dd * py; Jc[16] = f * n * py; Jc[17] = f * n * n * py;
+    Jc[0] = (float)(-(B00 * L00 + B01 * L10 + B02 * L20));
+    Jc[1] = (float)(-(B00 * L01 + B01 * L11 + B02 * L21));
+    Jc[2] = (float)(-(B00 * L02 + B01 * L12 + B02 * L22));
+    Jc[9] = (float)(-(B10 * L00 + B11 * L10 + B12 * L20));
+    Jc[10] = (float)(-(B10 * L01 + B11 * L11 + B12 * L21));
+    Jc[11] = (float)(-(B10 * L02 + B11 * L12 + B12 * L22));
+    Jc[3] = (float)A00; Jc[4] = (float)A01; Jc[5] = (float)A02;
+    Jc[12] = (float)A10; Jc[13] = (float)A11; Jc[14] = (float)A12;
+    Jc[6] = (float)(dd * px); Jc[7] = (float)(f * n * px); Jc[8] = (float)(f * n * n * px);
+    Jc[15] = (float)(dd * py); Jc[16] = (float)(f * n * py); Jc[17] = (float)(f * n * n * py);
     return P2;
 }
 
-__device__ __forceinline__ void load_cam(const float *__restrict__ cams, int cam, float *c) {
+__device__ __forceinline__ void load_cam(const double *__restrict__ cams, int cam, double *c) {
 #pragma unroll
     for (int q = 0; q < 9; q++) c[q] = __ldg(cams + 9 * cam + q);
 }
@@ -151,6 +153,21 @@ __device__ __forceinline__ double block_sum_d(double v, double *scratch) {
     return s;
 }
 
+// Camera-space partial sums of K4/K5 (matvec output, block-Jacobi blocks, b~) are accumulated in
+// FP32 into the slice of the SM that runs the thread and summed across slices in FP64 by
+// k_reduce_slices (reading C24): a single FP32 accumulator per camera summed the
+// contributions of thousands of landmarks in one chain, and its cancellation error was amplified by
+// PCG into a 1e-3 change of the solution.
+__device__ __forceinline__ unsigned smid() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ float *wslice(const DevProblem &d) { return d.wsl + (int64_t)smid() * 12 * d.n_p; }
+__device__ __forceinline__ float *pslice(const DevProblem &d) {
+    return d.psl + (int64_t)smid() * PACC_STRIDE * d.n_p;
+}
+
 // out12: camera stride 12 so the 9 entries of a camera go out as three 16-byte vector atomics
 __device__ __forceinline__ void flush_cam12(float *out12, int cam, const float *acc) {
     float4 *o4 = reinterpret_cast<float4 *>(out12 + 12 * (int64_t)cam);
@@ -163,12 +180,12 @@ __device__ __forceinline__ void flush_cam12(float *out12, int cam, const float *
 __global__ void k_check_depth(DevProblem d, int *bad) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= d.n_obs) return;
-    float c[9], r[2];
+    double c[9], r[2];
     load_cam(d.cams, d.obs_cam[i], c);
-    const float *X = d.pts + 3 * (int64_t)d.obs_lm[i];
-    float2 uv = d.obs_uv[i];
-    float Pz = cam_model(c, X[0], X[1], X[2], uv.x, uv.y, r, nullptr, nullptr);
-    if (!(Pz < -1e-8f) || !isfinite(r[0]) || !isfinite(r[1])) atomicAdd(bad, 1);
+    const double *X = d.pts + 3 * (int64_t)d.obs_lm[i];
+    const double2 uv = d.obs_uv[i];
+    const double Pz = cam_model(c, X[0], X[1], X[2], uv.x, uv.y, r, nullptr, nullptr);
+    if (!(Pz < -1e-8) || !isfinite(r[0]) || !isfinite(r[1])) atomicAdd(bad, 1);
 }
 
 // K1: residuals, E and camera column norms^2 (sum over the camera's observations).
@@ -177,14 +194,15 @@ __global__ void __launch_bounds__(256) k_linearize(DevProblem d) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     double e = 0.0, bad = 0.0;
     if (i < d.n_obs) {
-        float c[9], r[2], Jc[18], Jl[6];
+        double c[9], r[2];
+        float Jc[18], Jl[6];
         const int cam = d.obs_cam[i];
         load_cam(d.cams, cam, c);
-        const float *X = d.pts + 3 * (int64_t)d.obs_lm[i];
-        float2 uv = d.obs_uv[i];
-        float Pz = cam_model(c, X[0], X[1], X[2], uv.x, uv.y, r, Jc, Jl);
-        if (!(Pz < 0.f)) bad = 1.0;
-        e = (double)r[0] * r[0] + (double)r[1] * r[1];
+        const double *X = d.pts + 3 * (int64_t)d.obs_lm[i];
+        const double2 uv = d.obs_uv[i];
+        const double Pz = cam_model(c, X[0], X[1], X[2], uv.x, uv.y, r, Jc, Jl);
+        if (!(Pz < 0.0)) bad = 1.0;
+        e = r[0] * r[0] + r[1] * r[1];
         float n2[9];
 #pragma unroll
         for (int q = 0; q < 9; q++) n2[q] = Jc[q] * Jc[q] + Jc[9 + q] * Jc[9 + q];
@@ -360,11 +378,13 @@ __global__ void __launch_bounds__(128) k_marg_small(DevProblem d, int64_t pk_lo,
     if (act) {
         const int64_t o = d.lm_obs0[j] + gl;
         cam = d.obs_cam[o];
-        float c[9];
+        double c[9], rd[2];
         load_cam(d.cams, cam, c);
-        const float *X = d.pts + 3 * j;
-        const float2 uv = d.obs_uv[o];
-        cam_model(c, X[0], X[1], X[2], uv.x, uv.y, r, Jc, Jl);
+        const double *X = d.pts + 3 * j;
+        const double2 uv = d.obs_uv[o];
+        cam_model(c, X[0], X[1], X[2], uv.x, uv.y, rd, Jc, Jl);
+        r[0] = (float)rd[0];
+        r[1] = (float)rd[1];
     }
     // ---- landmark column scaling (C7, C8) over the landmark's own observations
     float sl[3], Dl[3];
@@ -524,7 +544,24 @@ __global__ void __launch_bounds__(128) k_marg_small(DevProblem d, int64_t pk_lo,
 // CTA of NT >= k threads per (landmark, tile range); thread o <-> observation o and camera
 // block o.  The O(k) prologue (Jacobians, Householder, WY) is recomputed by every CTA of a
 // landmark; the O(k^2) emission is split across CTAs (~1 MB each).
-template <int NT>
+// MULTI (k > KLARGE, "huge"): thread o' owns camera blocks o = o', o' + NT, ...; its two scaled J_p
+// rows are recomputed per block in the emission loop instead of being kept from the prologue.
+__device__ __forceinline__ void block_jp(const DevProblem &d, int64_t obs0, int o, const double *Xp, BlockWY &B) {
+    const int cam = d.obs_cam[obs0 + o];
+    double c[9], r[2];
+    float Jc[18], Jl[6];
+    load_cam(d.cams, cam, c);
+    const double2 uv = d.obs_uv[obs0 + o];
+    cam_model(c, Xp[0], Xp[1], Xp[2], uv.x, uv.y, r, Jc, Jl);
+#pragma unroll
+    for (int q = 0; q < 9; q++) {
+        const float s = d.sp[9 * cam + q];
+        B.jp[0][q] = Jc[q] * s;
+        B.jp[1][q] = Jc[9 + q] * s;
+    }
+}
+
+template <int NT, bool MULTI>
 __global__ void __launch_bounds__(NT) k_marg_large(DevProblem d, const LargeItem *__restrict__ items, float lam,
                                                    float dmin, float dmax) {
     extern __shared__ float4 smem4[];
@@ -540,31 +577,34 @@ __global__ void __launch_bounds__(NT) k_marg_large(DevProblem d, const LargeItem
     float *SX = reinterpret_cast<float *>(VR + (2 * k + 3));    // 2k x 3 landmark Jacobian
     float *SR = SX + 6 * k;                                     // 2k residuals
     const int64_t obs0 = d.lm_obs0[j];
-    const float *Xp = d.pts + 3 * j;
+    const double *Xp = d.pts + 3 * j;
     BlockWY B;
     float n2[3] = {0.f, 0.f, 0.f};
 #pragma unroll
     for (int q = 0; q < 9; q++) B.jp[0][q] = B.jp[1][q] = 0.f;
-    if (own) {
-        const int cam = d.obs_cam[obs0 + tid];
-        float c[9], r[2], Jc[18], Jl[6];
+    for (int o = tid; o < k; o += NT) {  // !MULTI: NT >= k, at most o == tid
+        const int cam = d.obs_cam[obs0 + o];
+        double c[9], r[2];
+        float Jc[18], Jl[6];
         load_cam(d.cams, cam, c);
-        const float2 uv = d.obs_uv[obs0 + tid];
+        const double2 uv = d.obs_uv[obs0 + o];
         cam_model(c, Xp[0], Xp[1], Xp[2], uv.x, uv.y, r, Jc, Jl);
+        if (!MULTI) {
 #pragma unroll
-        for (int q = 0; q < 9; q++) {
-            const float s = d.sp[9 * cam + q];
-            B.jp[0][q] = Jc[q] * s;
-            B.jp[1][q] = Jc[9 + q] * s;
+            for (int q = 0; q < 9; q++) {
+                const float s = d.sp[9 * cam + q];
+                B.jp[0][q] = Jc[q] * s;
+                B.jp[1][q] = Jc[9 + q] * s;
+            }
         }
 #pragma unroll
         for (int q = 0; q < 3; q++) {
-            SX[(2 * tid) * 3 + q] = Jl[q];
-            SX[(2 * tid + 1) * 3 + q] = Jl[3 + q];
-            n2[q] = Jl[q] * Jl[q] + Jl[3 + q] * Jl[3 + q];
+            SX[(2 * o) * 3 + q] = Jl[q];
+            SX[(2 * o + 1) * 3 + q] = Jl[3 + q];
+            n2[q] += Jl[q] * Jl[q] + Jl[3 + q] * Jl[3 + q];
         }
-        SR[2 * tid] = r[0];
-        SR[2 * tid + 1] = r[1];
+        SR[2 * o] = (float)r[0];
+        SR[2 * o + 1] = (float)r[1];
     }
     block_sum<3>(n2, red);
     float sl[3], Dl[3];
@@ -629,7 +669,7 @@ __global__ void __launch_bounds__(NT) k_marg_large(DevProblem d, const LargeItem
     const float T01 = -tau[1] * T00 * p[0];
     const float T02 = -tau[2] * (T00 * p[1] + T01 * p[2]);
     const float T12 = -tau[2] * T11 * p[2];
-    if (own) wy_m(B, VR[2 * tid], VR[2 * tid + 1], T00, T01, T02, T11, T12, T22);
+    if (!MULTI && own) wy_m(B, VR[2 * tid], VR[2 * tid + 1], T00, T01, T02, T11, T12, T22);
     // damping (every thread computes the 6 rotations redundantly from smem values)
     float R[9], rr3[3], V3[9];
 #pragma unroll
@@ -648,8 +688,15 @@ __global__ void __launch_bounds__(NT) k_marg_large(DevProblem d, const LargeItem
     if (tid < 6) VR[tid < 3 ? tid : 2 * k + tid - 3] = veff(Gm, V3, tid);
     if (tid < 18) GM[tid] = Gm[tid];
     __syncthreads();
-    if (own) {
-        const int o = tid, g_ = o >> 5, ng = min(32, k - 32 * g_);
+    for (int o = tid; o < k; o += NT) {
+        if (MULTI) {  // raw V rows 2o, 2o+1 (VR rows 0..2 now hold V_eff of the damped rows)
+            block_jp(d, obs0, o, Xp, B);
+            const float4 v0 = o == 0 ? make_float4(V3[0], V3[1], V3[2], 0.f)
+                                     : (o == 1 ? make_float4(V3[6], V3[7], V3[8], 0.f) : VR[2 * o]);
+            const float4 v1 = o == 0 ? make_float4(V3[3], V3[4], V3[5], 0.f) : VR[2 * o + 1];
+            wy_m(B, v0, v1, T00, T01, T02, T11, T12, T22);
+        }
+        const int g_ = o >> 5, ng = min(32, k - 32 * g_);
         float *R2 = d.arena + d.lm_r2[j];
         for (int t = it.t0; t < it.t1; t++) {
             float4 *S = reinterpret_cast<float4 *>(R2 + (int64_t)36 * k * t + 36 * 32 * g_) + (o & 31);
@@ -806,7 +853,7 @@ __device__ __forceinline__ void flush54(float *acc, const float *P, const float 
 __global__ void k_precond_finalize(DevProblem d, float lam, double *bad) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= d.n_p) return;
-    const float *acc = d.pacc + PACC_STRIDE * i;
+    const double *acc = d.pd + 54 * i;
     double P[81];
     int idx = 0;
     for (int a = 0; a < 9; a++)
@@ -817,7 +864,7 @@ __global__ void k_precond_finalize(DevProblem d, float lam, double *bad) {
         }
     for (int a = 0; a < 9; a++) {
         P[a * 9 + a] += (double)lam * d.Dp2[9 * i + a];
-        d.bt[9 * i + a] = acc[45 + a];
+        d.bt[9 * i + a] = acc[45 + a];  // FP64
     }
     double L[81];
     for (int a = 0; a < 81; a++) L[a] = 0.0;
@@ -847,7 +894,7 @@ __global__ void k_precond_finalize(DevProblem d, float lam, double *bad) {
             for (int m = a + 1; m < 9; m++) s -= L[m * 9 + a] * x[m];
             x[a] = s / L[a * 9 + a];
         }
-        for (int a = 0; a < 9; a++) d.Minv[81 * i + a * 9 + col] = (float)x[a];
+        for (int a = 0; a < 9; a++) d.Minv[81 * i + a * 9 + col] = x[a];
     }
 }
 
@@ -961,7 +1008,7 @@ __device__ __forceinline__ void small_unit(const DevProblem &d, const float2 *A,
             acc_rows(P, b, sl[u], TL[3 + 2 * (p0 + u)].w);
             acc_rows(P, b, sl[u] + 9, TL[4 + 2 * (p0 + u)].w);
         }
-        flush54(d.pacc + PACC_STRIDE * (int64_t)cam, P, b);
+        flush54(pslice(d) + PACC_STRIDE * (int64_t)cam, P, b);
     } else {
         float y[2 * NRP];
 #pragma unroll
@@ -988,7 +1035,7 @@ __device__ __forceinline__ void small_unit(const DevProblem &d, const float2 *A,
             for (int u = 0; u < NRP; u++) a_ += sl[u][q] * y[2 * u] + sl[u][9 + q] * y[2 * u + 1];
             acc[q] = a_;
         }
-        flush_cam12(out12, cam, acc);
+        flush_cam12(wslice(d), cam, acc);
     }
 }
 
@@ -1157,8 +1204,8 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
     for (int q = 0; q < 9; q++) vo[q] = 0.f, acc[q] = 0.f;
     auto flush = [&]() {
         if (cur < 0 || !valid) return;
-        if (PRECOND) flush54(d.pacc + PACC_STRIDE * (int64_t)cam, P, b);
-        else flush_cam12(out, cam, acc);
+        if (PRECOND) flush54(pslice(d) + PACC_STRIDE * (int64_t)cam, P, b);
+        else flush_cam12(wslice(d), cam, acc);
     };
     int buf = 0;
     for (int64_t i = 0; i < nst; i++) {
@@ -1250,38 +1297,137 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
     flush();
 }
 
-// out = w12 (stride 12 -> 9) + lambda D_p^2 v
+// ---- huge k (> KLARGE): a 4 x 9k tile no longer fits on chip twice (k = 1748: 252 KB), so the
+// product takes two passes over the same 4-row tiles: y = A v per tile (CTA-wide reduction), then
+// out_o += sum_t slab_{o,t}^T y_t with thread <-> camera block.  The preconditioner needs no y and
+// uses the second pass alone.  (2x the algorithmic bytes on these landmarks.)
+__device__ __forceinline__ void huge_slab(const float *__restrict__ R2, int k, int t, int o, float *sl) {
+    const int g = o >> 5, ng = min(32, k - 32 * g);
+    const float4 *S4 = reinterpret_cast<const float4 *>(R2 + (int64_t)36 * k * t + 36 * 32 * g) + (o & 31);
+#pragma unroll
+    for (int c = 0; c < 9; c++) {
+        const float4 x = __ldcs(S4 + c * ng);
+        sl[4 * c] = x.x, sl[4 * c + 1] = x.y, sl[4 * c + 2] = x.z, sl[4 * c + 3] = x.w;
+    }
+}
+
+__global__ void __launch_bounds__(HUGE_NT) k_huge_y(DevProblem d, const float *__restrict__ v,
+                                                    const PcgState *__restrict__ st) {
+    if (st && st->done) return;
+    __shared__ float red[32 * 4];
+    const HugeItem it = d.huge_y[blockIdx.x];
+    const int64_t j = it.lm;
+    const int k = d.lm_k[j], t = it.t0;
+    const float *R2 = d.arena + d.lm_r2[j];
+    const int32_t *oc = d.obs_cam + d.lm_obs0[j];
+    float y[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int o = threadIdx.x; o < k; o += HUGE_NT) {
+        float sl[36];
+        huge_slab(R2, k, t, o, sl);
+        const float *vv = v + 9 * (int64_t)oc[o];
+#pragma unroll
+        for (int q = 0; q < 9; q++) {
+            const float x = __ldg(vv + q);
+#pragma unroll
+            for (int r = 0; r < 4; r++) y[r] += sl[9 * r + q] * x;
+        }
+    }
+    block_sum<4>(y, red);
+    if (threadIdx.x == 0) reinterpret_cast<float4 *>(d.ybuf + it.yoff)[t] = make_float4(y[0], y[1], y[2], y[3]);
+}
+
+template <bool PRECOND>
+__global__ void __launch_bounds__(HUGE_NT) k_huge_out(DevProblem d, float *__restrict__ out,
+                                                      const PcgState *__restrict__ st) {
+    if (!PRECOND && st && st->done) return;
+    const HugeItem it = d.huge_out[blockIdx.x];
+    const int64_t j = it.lm;
+    const int k = d.lm_k[j], o = it.o0 + (int)threadIdx.x;
+    if (o >= k) return;
+    const float *R2 = d.arena + d.lm_r2[j];
+    const int cam = d.obs_cam[d.lm_obs0[j] + o];
+    float acc[9], P[PRECOND ? 45 : 1], b[PRECOND ? 9 : 1];
+#pragma unroll
+    for (int q = 0; q < 9; q++) acc[q] = 0.f;
+    if (PRECOND) {
+#pragma unroll
+        for (int q = 0; q < 45; q++) P[q] = 0.f;
+#pragma unroll
+        for (int q = 0; q < 9; q++) b[q] = 0.f;
+    }
+    const float4 *TL = reinterpret_cast<const float4 *>(d.arena + d.lm_side[j] + side_tl(k));
+    const float4 *Y = reinterpret_cast<const float4 *>(d.ybuf + it.yoff);
+    for (int t = it.t0; t < it.t1; t++) {
+        float sl[36];
+        huge_slab(R2, k, t, o, sl);
+        if (PRECOND) {
+#pragma unroll
+            for (int r = 0; r < 4; r++) {
+                const int a = 4 * t + r;
+                if (a < 2 * k) acc_rows(P, b, sl + 9 * r, TL[3 + a].w);
+            }
+        } else {
+            const float4 y = Y[t];
+#pragma unroll
+            for (int q = 0; q < 9; q++) acc[q] += sl[q] * y.x + sl[9 + q] * y.y + sl[18 + q] * y.z + sl[27 + q] * y.w;
+        }
+    }
+    if (PRECOND) flush54(pslice(d) + PACC_STRIDE * (int64_t)cam, P, b);
+    else flush_cam12(wslice(d), cam, acc);
+}
+
+// FP64 sum over the SM slices (stride `stride` floats per camera, `nv` values used), zeroing them
+// for the next launch: out[nv * cam + e] = sum_s slice_s[stride * cam + e].
+__global__ void __launch_bounds__(256) k_reduce_slices(float *__restrict__ sl, int64_t n_p, int stride, int nv,
+                                                       int nslice, double *__restrict__ out,
+                                                       const PcgState *__restrict__ st) {
+    if (st && st->done) return;  // PCG graph: no matvec ran, the slices are still zero
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nv * n_p) return;
+    const int64_t cam = i / nv;
+    const int64_t e = stride * cam + (i - nv * cam);
+    const int64_t S = (int64_t)stride * n_p;
+    double s = 0.0;
+    for (int k = 0; k < nslice; k++) {
+        float *q = sl + k * S + e;
+        s += (double)*q;
+        *q = 0.f;
+    }
+    out[i] = s;
+}
+
+// out = H~ v = wd + lambda D_p^2 v  (test hook, FP32 out)
 __global__ void k_add_damping(DevProblem d, const float *v, float *out, float lam) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= 9 * d.n_p) return;
-    const int64_t cam = i / 9;
-    out[i] = d.w12[12 * cam + (i - 9 * cam)] + lam * d.Dp2[i] * v[i];
+    out[i] = (float)(d.wd[i] + (double)lam * d.Dp2[i] * v[i]);
 }
 
 // ============================================================================ K6 PCG (single CTA)
 // Reading C11: stop when |rho| <= tol |rho_0| or it == max; p^T w <= 0 -> indefinite.
-__device__ __forceinline__ void precond_apply(const DevProblem &d, const float *in, float *outv, int64_t N) {
+__device__ __forceinline__ void precond_apply(const DevProblem &d, const double *in, double *outv, int64_t N) {
     for (int64_t i = threadIdx.x; i < N; i += blockDim.x) {
         const int64_t cam = i / 9;
         const int a = (int)(i - 9 * cam);
-        const float *M = d.Minv + 81 * cam + 9 * a;
-        const float *x = in + 9 * cam;
-        float s = 0.f;
+        const double *M = d.Minv + 81 * cam + 9 * a;
+        const double *x = in + 9 * cam;
+        double s = 0.0;
 #pragma unroll
         for (int b = 0; b < 9; b++) s += M[b] * x[b];
         outv[i] = s;
     }
 }
 
+// PCG vectors (x, rho, z, p, w) are FP64 (9 n_p each, reading C24); the matvec reads p as FP32 (p32).
 __global__ void __launch_bounds__(1024) k_pcg_init(DevProblem d) {
     __shared__ double red[32];
     const int64_t N = 9 * d.n_p;
     double rr = 0.0;
     for (int64_t i = threadIdx.x; i < N; i += blockDim.x) {
-        const float r = -d.bt[i];
+        const double r = -d.bt[i];
         d.r[i] = r;
-        d.x[i] = 0.f;
-        rr += (double)r * r;
+        d.x[i] = 0.0;
+        rr += r * r;
     }
     __syncthreads();
     precond_apply(d, d.r, d.z, N);
@@ -1289,7 +1435,8 @@ __global__ void __launch_bounds__(1024) k_pcg_init(DevProblem d) {
     double rz = 0.0;
     for (int64_t i = threadIdx.x; i < N; i += blockDim.x) {
         d.p[i] = d.z[i];
-        rz += (double)d.r[i] * d.z[i];
+        d.p32[i] = (float)d.z[i];
+        rz += d.r[i] * d.z[i];
     }
     rr = block_sum_d(rr, red);
     rz = block_sum_d(rz, red);
@@ -1305,12 +1452,12 @@ __global__ void __launch_bounds__(1024) k_pcg_init(DevProblem d) {
 
 // lam < 0: read lambda from d.scal[SC_LAM] (graph launches).  use_h: also drive the graph's
 // while-loop condition (0 once the solve is done).
-__global__ void __launch_bounds__(1024) k_pcg_step(DevProblem d, float lam, double tol, int max_iters,
+__global__ void __launch_bounds__(1024) k_pcg_step(DevProblem d, float lam_f, double tol, int max_iters,
                                                    cudaGraphConditionalHandle h, int use_h) {
     __shared__ double red[32];
     __shared__ int stop;
     PcgState *st = d.pcg;
-    if (lam < 0.f) lam = (float)d.scal[SC_LAM];
+    const double lam = lam_f < 0.f ? d.scal[SC_LAM] : (double)lam_f;
     if (st->done) {
         if (use_h && threadIdx.x == 0) cudaGraphSetConditional(h, 0);
         return;
@@ -1318,10 +1465,9 @@ __global__ void __launch_bounds__(1024) k_pcg_step(DevProblem d, float lam, doub
     const int64_t N = 9 * d.n_p;
     double pw = 0.0;
     for (int64_t i = threadIdx.x; i < N; i += blockDim.x) {
-        const int64_t cam = i / 9;
-        const float w = d.w12[12 * cam + (i - 9 * cam)] + lam * d.Dp2[i] * d.p[i];
+        const double w = d.wd[i] + lam * d.Dp2[i] * d.p[i];
         d.w[i] = w;
-        pw += (double)d.p[i] * w;
+        pw += d.p[i] * w;
     }
     pw = block_sum_d(pw, red);
     if (!(pw > 0.0)) {
@@ -1331,13 +1477,13 @@ __global__ void __launch_bounds__(1024) k_pcg_step(DevProblem d, float lam, doub
         }
         return;
     }
-    const float alpha = (float)(st->rz / pw);
+    const double alpha = st->rz / pw;
     double rr = 0.0;
     for (int64_t i = threadIdx.x; i < N; i += blockDim.x) {
         d.x[i] += alpha * d.p[i];
-        const float r = d.r[i] - alpha * d.w[i];
+        const double r = d.r[i] - alpha * d.w[i];
         d.r[i] = r;
-        rr += (double)r * r;
+        rr += r * r;
     }
     rr = block_sum_d(rr, red);
     if (threadIdx.x == 0) {
@@ -1355,10 +1501,14 @@ __global__ void __launch_bounds__(1024) k_pcg_step(DevProblem d, float lam, doub
     precond_apply(d, d.r, d.z, N);
     __syncthreads();
     double rz = 0.0;
-    for (int64_t i = threadIdx.x; i < N; i += blockDim.x) rz += (double)d.r[i] * d.z[i];
+    for (int64_t i = threadIdx.x; i < N; i += blockDim.x) rz += d.r[i] * d.z[i];
     rz = block_sum_d(rz, red);
-    const float beta = (float)(rz / st->rz);
-    for (int64_t i = threadIdx.x; i < N; i += blockDim.x) d.p[i] = d.z[i] + beta * d.p[i];
+    const double beta = rz / st->rz;
+    for (int64_t i = threadIdx.x; i < N; i += blockDim.x) {
+        const double pn = d.z[i] + beta * d.p[i];
+        d.p[i] = pn;
+        d.p32[i] = (float)pn;
+    }
     __syncthreads();
     if (threadIdx.x == 0) st->rz = rz;
 }
@@ -1374,10 +1524,10 @@ __global__ void __launch_bounds__(256) k_backsub(DevProblem d, float lam) {
     const int64_t obs0 = d.lm_obs0[j];
     float s0 = 0.f, s1 = 0.f, s2 = 0.f;
     for (int o = lane; o < k; o += 32) {  // lane <-> camera block: one gather of dp per block
-        const float *dp = d.x + 9 * (int64_t)d.obs_cam[obs0 + o];
+        const double *dp = d.x + 9 * (int64_t)d.obs_cam[obs0 + o];
 #pragma unroll
         for (int q = 0; q < 9; q++) {
-            const float v = dp[q];
+            const float v = (float)dp[q];
             s0 += side[9 * o + q] * v;
             s1 += side[W + 9 * o + q] * v;
             s2 += side[2 * W + 9 * o + q] * v;
@@ -1399,7 +1549,7 @@ __global__ void __launch_bounds__(256) k_backsub(DevProblem d, float lam) {
 #pragma unroll
         for (int q = 0; q < 3; q++) {
             d.dl[3 * j + q] = dl[q];
-            d.pts_trial[3 * j + q] = d.pts[3 * j + q] + d.lm_s[3 * j + q] * dl[q];
+            d.pts_trial[3 * j + q] = d.pts[3 * j + q] + (double)(d.lm_s[3 * j + q] * dl[q]);
             const double Dd = (double)d.lm_D[3 * j + q] * dl[q];
             dd += Dd * Dd;
         }
@@ -1415,28 +1565,28 @@ __global__ void __launch_bounds__(1024) k_trial_cams(DevProblem d, float lam) {
     const int64_t N = 9 * d.n_p;
     double m = 0.0;
     for (int64_t i = threadIdx.x; i < N; i += blockDim.x) {
-        const float dp = d.x[i];
-        d.cams_trial[i] = d.cams[i] + d.sp[i] * dp;
-        m += -(double)d.bt[i] * dp + (double)d.r[i] * dp + (double)lam * d.Dp2[i] * (double)dp * dp;
+        const double dp = d.x[i];
+        d.cams_trial[i] = d.cams[i] + (double)d.sp[i] * dp;
+        m += -d.bt[i] * dp + d.r[i] * dp + (double)lam * d.Dp2[i] * dp * dp;
     }
     m = block_sum_d(m, red);
     if (threadIdx.x == 0) d.scal[SC_MODELP] = m;
 }
 
 // ============================================================================ K8 cost
-__global__ void __launch_bounds__(256) k_cost(DevProblem d, const float *__restrict__ cams,
-                                              const float *__restrict__ pts, int slot, int bad_slot) {
+__global__ void __launch_bounds__(256) k_cost(DevProblem d, const double *__restrict__ cams,
+                                              const double *__restrict__ pts, int slot, int bad_slot) {
     __shared__ double red[32];
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     double e = 0.0, bad = 0.0;
     if (i < d.n_obs) {
-        float c[9], r[2];
+        double c[9], r[2];
         load_cam(cams, d.obs_cam[i], c);
-        const float *X = pts + 3 * (int64_t)d.obs_lm[i];
-        const float2 uv = d.obs_uv[i];
-        const float Pz = cam_model(c, X[0], X[1], X[2], uv.x, uv.y, r, nullptr, nullptr);
-        if (!(Pz < 0.f) || !isfinite(r[0]) || !isfinite(r[1])) bad = 1.0;
-        else e = (double)r[0] * r[0] + (double)r[1] * r[1];
+        const double *X = pts + 3 * (int64_t)d.obs_lm[i];
+        const double2 uv = d.obs_uv[i];
+        const double Pz = cam_model(c, X[0], X[1], X[2], uv.x, uv.y, r, nullptr, nullptr);
+        if (!(Pz < 0.0) || !isfinite(r[0]) || !isfinite(r[1])) bad = 1.0;
+        else e = r[0] * r[0] + r[1] * r[1];
     }
     e = block_sum_d(e, red);
     bad = block_sum_d(bad, red);
@@ -1449,6 +1599,19 @@ __global__ void __launch_bounds__(256) k_cost(DevProblem d, const float *__restr
 // ============================================================================ launchers
 static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
 
+
+__global__ void k_nsmid(int *out) {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%nsmid;" : "=r"(r));
+    *out = (int)r;
+}
+// number of SM-id slots (%nsmid >= any %smid; SM ids need not be dense)
+cudaError_t query_nsmid(rba_ctx *c, int *d_scratch, int *out) {
+    k_nsmid<<<1, 1, 0, c->stream>>>(d_scratch);
+    cudaError_t e = cudaMemcpyAsync(out, d_scratch, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
+    if (e) return e;
+    return cudaStreamSynchronize(c->stream);
+}
 
 cudaError_t launch_check_depth(rba_ctx *c, int *d_bad) {
     if (c->d.n_obs == 0) return cudaSuccess;
@@ -1507,13 +1670,14 @@ static cudaError_t marg_small_cls(rba_ctx *c, int cls, float lam, cudaStream_t s
     return cudaGetLastError();
 }
 
-template <int NT>
+template <int NT, bool MULTI = false>
 static cudaError_t marg_large_cls(rba_ctx *c, int cls, float lam, cudaStream_t st) {
     const int64_t lo = c->marg_lo[cls], hi = c->marg_hi[cls];
     if (hi <= lo) return cudaSuccess;
-    const size_t sm = (size_t)(4 * (2 * NT + 3) + 8 * NT) * sizeof(float);
-    cudaFuncSetAttribute(k_marg_large<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_marg_large<NT><<<(unsigned)(hi - lo), NT, sm, st>>>(c->d, c->d.marg_items + lo, lam,
+    const int64_t K = MULTI ? c->huge_max_k : NT;
+    const size_t sm = (size_t)(4 * (2 * K + 3) + 8 * K) * sizeof(float);
+    cudaFuncSetAttribute(k_marg_large<NT, MULTI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_marg_large<NT, MULTI><<<(unsigned)(hi - lo), NT, sm, st>>>(c->d, c->d.marg_items + lo, lam,
                                                                   (float)c->opt.diag_min, (float)c->opt.diag_max);
     c->launches++;
     return cudaGetLastError();
@@ -1523,6 +1687,7 @@ cudaError_t launch_marginalize(rba_ctx *c, float lam) {
     Prof P(c, KID_MARG, plan_marg_bytes(c));
     cudaError_t e;
     ForkJoin F(c);
+    if ((e = marg_large_cls<512, true>(c, 5, lam, F.s()))) return e;
     if ((e = marg_large_cls<512>(c, 4, lam, F.s()))) return e;
     if ((e = marg_large_cls<256>(c, 3, lam, F.s()))) return e;
     if ((e = marg_large_cls<128>(c, 2, lam, F.s()))) return e;
@@ -1560,6 +1725,16 @@ static void large_pipe_cls(rba_ctx *c, int cls, const float *v, float *out, cons
 template <bool PRE>
 static void pipes_all(rba_ctx *c, const float *v, float *out12, const PcgState *st) {
     ForkJoin F(c);
+    if (c->n_huge_out > 0) {  // k > KLARGE: two passes, same stream
+        cudaStream_t hs = F.s();
+        if (!PRE) {
+            k_huge_y<<<(unsigned)c->n_huge_y, HUGE_NT, 0, hs>>>(c->d, v, st);
+            c->launches++;
+        }
+        if (PRE) k_huge_out<true><<<(unsigned)c->n_huge_out, HUGE_NT, 0, hs>>>(c->d, out12, st);
+        else k_huge_out<false><<<(unsigned)c->n_huge_out, HUGE_NT, 0, hs>>>(c->d, out12, st);
+        c->launches++;
+    }
     // longest first so the short classes fill the long ones' tails
     large_pipe_cls<512, 1, PRE>(c, 4, v, out12, st, F.s());
     if (c->chunk_ctas > 0) {
@@ -1576,9 +1751,15 @@ static void pipes_all(rba_ctx *c, const float *v, float *out12, const PcgState *
     F.join();
 }
 
+static void reduce_slices(rba_ctx *c, float *sl, int stride, int nv, double *out, const PcgState *st) {
+    k_reduce_slices<<<nblk(nv * c->d.n_p, 256), 256, 0, c->stream>>>(sl, c->d.n_p, stride, nv, c->d.nslice, out, st);
+    c->launches++;
+}
+
 cudaError_t launch_precond_rhs(rba_ctx *c) {
     Prof P(c, KID_PRE, plan_matvec_bytes(c));
-    pipes_all<true>(c, nullptr, nullptr, nullptr);
+    pipes_all<true>(c, nullptr, c->d.psl, nullptr);
+    reduce_slices(c, c->d.psl, PACC_STRIDE, 54, c->d.pd, nullptr);
     P.end();
     return cudaGetLastError();
 }
@@ -1591,14 +1772,15 @@ cudaError_t launch_precond_finalize(rba_ctx *c, float lam) {
 
 static cudaError_t matvec_impl(rba_ctx *c, const float *v, const PcgState *st) {
     Prof P(c, KID_MATVEC, plan_matvec_bytes(c));
-    pipes_all<false>(c, v, c->d.w12, st);
+    pipes_all<false>(c, v, c->d.wsl, st);
+    reduce_slices(c, c->d.wsl, 12, 9, c->d.wd, st);
     P.end();
     return cudaGetLastError();
 }
 
-// w12 = sum_j A_j^T (A_j v_j)  (callers zero w12 first and all-reduce it afterwards)
+// wd = sum_j A_j^T (A_j v_j) in FP64 (callers all-reduce it afterwards)
 cudaError_t launch_matvec(rba_ctx *c, const float *v, float *) { return matvec_impl(c, v, nullptr); }
-cudaError_t launch_matvec_pcg(rba_ctx *c) { return matvec_impl(c, c->d.p, c->d.pcg); }
+cudaError_t launch_matvec_pcg(rba_ctx *c) { return matvec_impl(c, c->d.p32, c->d.pcg); }
 
 cudaError_t launch_add_damping(rba_ctx *c, const float *v, float *out, float lam) {
     k_add_damping<<<nblk(9 * c->d.n_p, 256), 256, 0, c->stream>>>(c->d, v, out, lam);
@@ -1620,7 +1802,7 @@ cudaError_t launch_pcg_step(rba_ctx *c, float lam, float tol, int max_iters) {
     return cudaGetLastError();
 }
 
-// PCG loop as a graph: while (cond) { w12 = 0; w12 = sum_j A_j^T A_j p (all pipes); PCG update }
+// PCG loop as a graph: while (cond) { slices += A_j^T A_j p32 (all pipes); wd = sum of slices; PCG update }
 // The update kernel clears the condition once |rho| <= tol |rho_0|, max iterations or p^T H p <= 0.
 cudaError_t build_pcg_graph(rba_ctx *c) {
     cudaError_t e;
@@ -1644,8 +1826,8 @@ cudaError_t build_pcg_graph(rba_ctx *c) {
     const int64_t nl = c->launches;
     c->stream = cs;
     c->profiling = false;
-    cudaMemsetAsync(c->d.w12, 0, sizeof(float) * 12 * c->d.n_p, cs);
-    pipes_all<false>(c, c->d.p, c->d.w12, c->d.pcg);
+    pipes_all<false>(c, c->d.p32, c->d.wsl, c->d.pcg);
+    reduce_slices(c, c->d.wsl, 12, 9, c->d.wd, c->d.pcg);
     k_pcg_step<<<1, 1024, 0, cs>>>(c->d, -1.f, c->opt.pcg_rel_tol, c->opt.pcg_max_iters, h, 1);
     c->stream = saved;
     c->profiling = prof;

@@ -197,3 +197,49 @@ def test_arena_bytes_exact():
     logical, physical = s.arena_bytes()
     assert logical == int(((2 * k + 3) * (9 * k + 4) * 4 + 48).sum())  # P:645 (+ 6 Givens pairs)
     assert physical >= logical
+
+
+def _probe_gram(B, k, z):
+    """(A|q)^T (A|q) z for the reduced rows of a logical block, without forming the Gram."""
+    Aq = np.concatenate([B[3:, :9 * k], B[3:, -1:]], 1)
+    return Aq.T @ (Aq @ z)
+
+
+def test_huge_tracks():
+    """k > 512 ("huge" path: multi-block threads in K2, two-pass matvec / preconditioner), up to
+    k = 1300 (the config-5 law reaches 1727): blocks through random Gram probes, R1^T R1, the
+    reduced product on random vectors and b~, all vs the oracle (<= 1e-4)."""
+    rng = np.random.default_rng(17)
+    ks = list(rng.integers(2, 40, 150)) + [513, 777, 1300]
+    p = synth.make_tracks(23, ks, n_p=1400)
+    s, o = _pair(p, 1e-3)
+    for j in (150, 151, 152):
+        k = ks[j]
+        Bg, Bo = s.block(j), o.block(j)
+        assert np.all(Bg[3:, 9 * k:9 * k + 3] == 0.0)
+        R1g, R1o = Bg[:3, 9 * k:9 * k + 3], Bo[:3, 9 * k:9 * k + 3]
+        assert relf(R1g.T @ R1g, R1o.T @ R1o) <= 1e-4
+        for _ in range(3):
+            z = rng.normal(size=9 * k + 1)
+            assert relf(_probe_gram(Bg, k, z), _probe_gram(Bo, k, z)) <= 1e-4
+    for _ in range(3):
+        v = rng.normal(size=9 * o.n_p)
+        g = s.matvec(torch.tensor(v, dtype=torch.float32, device="cuda")).double().cpu().numpy()
+        assert relf(g, o.matvec(v)) <= 1e-4
+    s.pcg()
+    assert o.precond_rhs() == 0
+    assert relf(s.rhs(), o.rhs()) <= 1e-4
+
+
+def test_huge_tracks_lm():
+    """Three LM iterations on a problem with huge tracks: costs within 1e-4 of the oracle.  Enough
+    short tracks (~30 observations per camera) that every camera's 9 parameters are determined;
+    with ~4 per camera the steps are damping-dominated and FP32 vs FP64 trajectories separate."""
+    rng = np.random.default_rng(19)
+    ks = list(rng.integers(4, 13, 2500)) + [600, 700]
+    p = synth.make_tracks(29, ks, n_p=700)
+    s = _solver(p)
+    o = oracle.Oracle(p)
+    for i in range(3):
+        rg, ro = s.lm_step(), o.lm_step()
+        assert abs(rg["cost_after"] - ro["cost_after"]) <= 1e-4 * ro["cost_after"], (i, rg, ro)
