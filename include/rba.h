@@ -58,6 +58,11 @@ typedef struct {
     void *(*alloc)(size_t bytes, void *alloc_ctx);
     void (*free)(void *ptr, void *alloc_ctx);
     void *alloc_ctx;
+    /* robust loss ("Huber norm with a parameter of 1 pixel ... IRLS as in Ceres"): Huber
+     * parameter delta in pixels; 0 = squared loss (the default; BASELINE's configs use none).  E
+     * becomes sum rho(|r|^2) with rho(s) = s (s <= delta^2) else 2 delta sqrt(s) - delta^2, and every
+     * residual / Jacobian row is weighted by sqrt(rho'(|r|^2)) at linearization (IRLS). */
+    double huber_delta;
 } rba_options;
 
 typedef struct {
@@ -80,7 +85,8 @@ typedef struct {
     double lambda_next;
 } rba_lm_report;
 
-/* Fill defaults: device 0, own stream, world 1, lambda0 1e-4, tol 1e-2, 500 iters, 1e-3, 1e-6, 1e32. */
+/* Fill defaults: device 0, own stream, world 1, lambda0 1e-4, tol 1e-2, 500 iters, 1e-3, 1e-6, 1e32,
+ * no robust loss. */
 void rba_default_options(rba_options *opt);
 
 /* Create a solver context from the full problem (host FP64, caller-owned, copied; the caller may
@@ -163,6 +169,39 @@ rba_status rba_plan_shards(const int32_t *k, int64_t n_landmarks, int world, int
 rba_status rba_nccl_unique_id(void *id128);
 /* Thread-local description of the last error. */
 const char *rba_last_error(void);
+
+/* ---- BAL ingest and the paper's preprocessing (host only, no GPU) ---------------
+ * A BAL problem in host memory, FP64, arrays allocated by librba (release with rba_bal_free).
+ * Layout as rba_create expects: cameras n_cams x 9 [w t f k1 k2], points n_points x 3,
+ * obs_cam / obs_pt n_obs, obs_uv n_obs x 2.  Errors: RBA_ERR_BAD_PROBLEM with the offending line
+ * (rba_bal_last_error), RBA_ERR_INVALID_ARG for null arguments / unreadable files. */
+typedef struct {
+    int64_t n_cams, n_points, n_obs;
+    double *cameras, *points, *obs_uv;
+    int32_t *obs_cam, *obs_pt;
+} rba_bal;
+/* Parse BAL text: header "n_cams n_points n_obs", n_obs lines "cam pt u v", 9 numbers per camera,
+ * 3 per point.  Counts come from the header; observation order is preserved. */
+rba_status rba_bal_parse(const char *text, size_t len, rba_bal *out);
+rba_status rba_bal_read(const char *path, rba_bal *out);
+/* Write BAL text (%.17g, so parse(write(p)) reproduces p exactly). */
+rba_status rba_bal_write(const char *path, const rba_bal *p);
+/* Gauge normalization: subtract the per-axis median of the points and scale so that the
+ * median over points of the L1 distance to it becomes target_mad (100 in the paper; reading C25);
+ * cameras follow the similarity (centre C = -R^T t moved and scaled, rotation kept), so every
+ * reprojection residual is unchanged.  RBA_ERR_BAD_PROBLEM if that median is 0. */
+rba_status rba_bal_normalize(rba_bal *p, double target_mad);
+/* Seeded Gaussian perturbation in FP64: angle-axis += N(0, sigma_rot^2), camera
+ * centre += N(0, sigma_centre^2) (translation recomputed), points += N(0, sigma_point^2); a
+ * counter-based generator, so the result depends only on (problem, sigmas, seed). */
+rba_status rba_bal_perturb(rba_bal *p, double sigma_rot, double sigma_centre, double sigma_point, uint64_t seed);
+/* Observation filter: keep an observation iff its depth -P_z in the camera frame
+ * (BAL cameras look down -z) exceeds z_min; then drop landmarks with fewer than 2 remaining
+ * observations (and their observations), reindexing landmarks densely in their original order.
+ * Counts of what was removed go to *removed_obs / *removed_points (may be NULL). */
+rba_status rba_bal_filter(rba_bal *p, double z_min, int64_t *removed_obs, int64_t *removed_points);
+void rba_bal_free(rba_bal *p);
+const char *rba_bal_last_error(void);
 
 #ifdef __cplusplus
 }

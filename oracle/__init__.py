@@ -72,6 +72,9 @@ def lib():
             "orc_get_state": (None, [P, P, P]),
             "orc_set_state": (None, [P, P, P]),
             "orc_set_lm": (None, [P, D, D]),
+            "orc_set_huber": (None, [P, D]),
+            "orc_huber_rho": (D, [D, D]),
+            "orc_huber_weight": (D, [D, D]),
             "orc_get_lambda": (D, [P]),
             "orc_linearized_cost": (D, [P]),
             "orc_obs_order": (None, [P, P, P]),
@@ -117,6 +120,14 @@ def residual_jacobian(cam, X, u):
     if rc:
         raise ValueError("degenerate projection")
     return r, Jc, Jl
+
+
+def huber_rho(s, delta):
+    return lib().orc_huber_rho(float(s), float(delta))
+
+
+def huber_weight(s, delta):
+    return lib().orc_huber_weight(float(s), float(delta))
 
 
 def givens(a, b):
@@ -225,6 +236,10 @@ class Oracle:
 
     def set_lm(self, lam, nu=2.0):
         lib().orc_set_lm(self.h, lam, nu)
+
+    def set_huber(self, delta):
+        """Huber robust loss with parameter delta px (IRLS); 0 = squared loss."""
+        lib().orc_set_huber(self.h, float(delta))
 
     def linearization(self):
         """(r, Jc, Jl) unscaled, CSR order (use .obs_src / .lm_ptr / .csr_cam)."""

@@ -73,6 +73,8 @@ typedef struct {
     double cost_trial;
     /* LM */
     double lm_lambda, lm_nu;
+    /* robust loss: Huber with parameter delta (pixels), 0 = squared loss */
+    double huber;
     int need_linearize;
     int64_t iteration;
 } orc_ctx;
@@ -190,6 +192,20 @@ int orc_residual_jacobian(const double *cam, const double *X, const double *u, d
         Jc[9 * i + 8] = f * n * n * pi_;  /* d/dk2 */
     }
     return 0;
+}
+
+/* Huber norm ("Huber norm with a parameter of 1 pixel ... implemented with IRLS as in
+ * Ceres"), on the squared residual norm s = |r|^2:  rho(s) = s for s <= delta^2, else
+ * 2 delta sqrt(s) - delta^2.  IRLS weight (Ceres' corrector with rho'' = 0): the residual and its
+ * Jacobian rows are multiplied by sqrt(rho'(s)), rho'(s) = 1 for s <= delta^2, else delta/sqrt(s).
+ * delta <= 0: squared loss. */
+double orc_huber_rho(double s, double delta) {
+    if (delta <= 0.0 || s <= delta * delta) return s;
+    return 2.0 * delta * sqrt(s) - delta * delta;
+}
+double orc_huber_weight(double s, double delta) {
+    if (delta <= 0.0 || s <= delta * delta) return 1.0;
+    return sqrt(delta / sqrt(s));
 }
 
 /* Givens coefficients, reading C5 of the garbled appendix formula:
@@ -318,7 +334,7 @@ int64_t orc_block_doubles(orc_ctx *c) { return c->blk_off[c->n_l]; }
 
 static double clampd(double x, double lo, double hi) { return x < lo ? lo : (x > hi ? hi : x); }
 
-/* E(x) = sum |r_ij|^2 (Eq. ba_energy, no 1/2: C3).  +inf if a point is at or
+/* E(x) = sum rho(|r_ij|^2) (Eq. ba_energy, no 1/2: C3; rho = identity unless Huber).  +inf if a point is at or
  * behind a camera (P_z >= 0, C17). */
 static double cost_at(orc_ctx *c, const double *cams, const double *pts) {
     double *per = malloc(sizeof(double) * c->n_l);
@@ -330,7 +346,7 @@ static double cost_at(orc_ctx *c, const double *cams, const double *pts) {
             orc_project(cams + DP * c->o_cam[o], pts + 3 * j, uv, &Pz);
             if (!(Pz < 0.0)) { s = INFINITY; break; }
             double dx = uv[0] - c->o_uv[2 * o], dy = uv[1] - c->o_uv[2 * o + 1];
-            s += dx * dx + dy * dy;
+            s += orc_huber_rho(dx * dx + dy * dy, c->huber);
         }
         per[j] = s;
     }
@@ -353,6 +369,17 @@ int orc_scaling(orc_ctx *c) {
             bad |= orc_residual_jacobian(c->cams + DP * c->o_cam[o], c->pts + 3 * j, c->o_uv + 2 * o,
                                          c->r + 2 * o, c->Jc + 18 * o, c->Jl + 6 * o);
     if (bad) return 1;
+    /* IRLS: weight residual and Jacobian rows by sqrt(rho'(|r|^2)) */
+    if (c->huber > 0.0) {
+#pragma omp parallel for schedule(static)
+        for (int64_t o = 0; o < c->n_obs; o++) {
+            double *r = c->r + 2 * o;
+            double w = orc_huber_weight(r[0] * r[0] + r[1] * r[1], c->huber);
+            r[0] *= w, r[1] *= w;
+            for (int q = 0; q < 18; q++) c->Jc[18 * o + q] *= w;
+            for (int q = 0; q < 6; q++) c->Jl[6 * o + q] *= w;
+        }
+    }
     c->cost = orc_cost(c);
     /* column norms of the full Jacobian; camera columns summed over the camera's observations */
 #pragma omp parallel for
@@ -804,6 +831,11 @@ void orc_set_state(orc_ctx *c, const double *cams, const double *pts) {
     c->linearized = c->marginalized = c->damped = 0;
 }
 void orc_set_lm(orc_ctx *c, double lambda, double nu) { c->lm_lambda = lambda; c->lm_nu = nu; }
+/* Huber parameter (pixels); 0 = squared loss.  Takes effect at the next linearization. */
+void orc_set_huber(orc_ctx *c, double delta) {
+    c->huber = delta;
+    c->need_linearize = 1;
+}
 double orc_get_lambda(orc_ctx *c) { return c->lm_lambda; }
 double orc_linearized_cost(orc_ctx *c) { return c->cost; }
 void orc_obs_order(orc_ctx *c, int64_t *src, int64_t *lm_ptr) {

@@ -135,6 +135,7 @@ extern "C" void rba_default_options(rba_options *o) {
     o->min_rel_decrease = 1e-3;
     o->diag_min = 1e-6;
     o->diag_max = 1e32;
+    o->huber_delta = 0.0;
 }
 
 extern "C" const char *rba_last_error(void) { return g_err.c_str(); }
@@ -193,7 +194,8 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
         n_obs < 0)
         return fail(RBA_ERR_INVALID_ARG, "rba_create: null pointer or negative size");
     if (opt.world < 1 || opt.rank < 0 || opt.rank >= opt.world || !(opt.lambda0 > 0) || !(opt.pcg_rel_tol >= 0) ||
-        opt.pcg_max_iters < 0 || !(opt.diag_min > 0) || !(opt.diag_max >= opt.diag_min))
+        opt.pcg_max_iters < 0 || !(opt.diag_min > 0) || !(opt.diag_max >= opt.diag_min) ||
+        !(opt.huber_delta >= 0) || !std::isfinite(opt.huber_delta))
         return fail(RBA_ERR_INVALID_ARG, "rba_create: bad options");
     if (n_obs >= (int64_t)1 << 31 || n_points >= (int64_t)1 << 31 || n_cams >= (int64_t)1 << 28)
         return fail(RBA_ERR_INVALID_ARG, "rba_create: problem too large for int32 indices");
@@ -459,6 +461,7 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     DevProblem &d = c->d;
     d.n_p = n_cams;
     d.n_l = nl;
+    d.huber = opt.huber_delta;
     d.n_obs = nobs_loc;
     CKSC(dalloc_n(c, &d.cams, 9 * n_cams));
     CKSC(dalloc_n(c, &d.cams_trial, 9 * n_cams));

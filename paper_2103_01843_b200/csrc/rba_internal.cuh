@@ -108,6 +108,7 @@ constexpr int HUGE_NT = 256;  // threads per CTA of the huge-k passes (camera bl
 
 struct DevProblem {
     int64_t n_p, n_l, n_obs;  // local counts (landmarks / observations of this shard)
+    double huber;             // Huber parameter (px), 0 = squared loss
     // state
     double *cams, *cams_trial, *pts, *pts_trial;  // FP64 state (reading C23)
     // landmark metadata (internal order, sorted by k)

@@ -17,6 +17,7 @@
 //  K8 k_cost              E at the current or trial state (Eq. ba_energy; C14, C17)
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 
@@ -98,6 +99,27 @@ __device__ __forceinline__ double cam_model(const double *__restrict__ cam, doub
     Jc[6] = (float)(dd * px); Jc[7] = (float)(f * n * px); Jc[8] = (float)(f * n * n * px);
     Jc[15] = (float)(dd * py); Jc[16] = (float)(f * n * py); Jc[17] = (float)(f * n * n * py);
     return P2;
+}
+
+// Huber norm on s = |r|^2 and its IRLS weight sqrt(rho'(s)) (Ceres' corrector with
+// rho'' = 0); delta <= 0: squared loss.
+__device__ __forceinline__ double robust_rho(double s, double delta) {
+    return (delta <= 0.0 || s <= delta * delta) ? s : 2.0 * delta * sqrt(s) - delta * delta;
+}
+__device__ __forceinline__ double robust_w(double s, double delta) {
+    return (delta <= 0.0 || s <= delta * delta) ? 1.0 : sqrt(delta / sqrt(s));
+}
+// weight the residual and the Jacobian rows of one observation (IRLS)
+__device__ __forceinline__ void apply_irls(double *r, float *Jc, float *Jl, double delta) {
+    if (delta <= 0.0) return;
+    const double w = robust_w(r[0] * r[0] + r[1] * r[1], delta);
+    const float wf = (float)w;
+    r[0] *= w;
+    r[1] *= w;
+#pragma unroll
+    for (int i = 0; i < 18; i++) Jc[i] *= wf;
+#pragma unroll
+    for (int i = 0; i < 6; i++) Jl[i] *= wf;
 }
 
 __device__ __forceinline__ void load_cam(const double *__restrict__ cams, int cam, double *c) {
@@ -202,7 +224,8 @@ __global__ void __launch_bounds__(256) k_linearize(DevProblem d) {
         const double2 uv = d.obs_uv[i];
         const double Pz = cam_model(c, X[0], X[1], X[2], uv.x, uv.y, r, Jc, Jl);
         if (!(Pz < 0.0)) bad = 1.0;
-        e = r[0] * r[0] + r[1] * r[1];
+        e = robust_rho(r[0] * r[0] + r[1] * r[1], d.huber);
+        apply_irls(r, Jc, Jl, d.huber);
         float n2[9];
 #pragma unroll
         for (int q = 0; q < 9; q++) n2[q] = Jc[q] * Jc[q] + Jc[9 + q] * Jc[9 + q];
@@ -383,6 +406,7 @@ __global__ void __launch_bounds__(128) k_marg_small(DevProblem d, int64_t pk_lo,
         const double *X = d.pts + 3 * j;
         const double2 uv = d.obs_uv[o];
         cam_model(c, X[0], X[1], X[2], uv.x, uv.y, rd, Jc, Jl);
+        apply_irls(rd, Jc, Jl, d.huber);
         r[0] = (float)rd[0];
         r[1] = (float)rd[1];
     }
@@ -553,6 +577,7 @@ __device__ __forceinline__ void block_jp(const DevProblem &d, int64_t obs0, int 
     load_cam(d.cams, cam, c);
     const double2 uv = d.obs_uv[obs0 + o];
     cam_model(c, Xp[0], Xp[1], Xp[2], uv.x, uv.y, r, Jc, Jl);
+    apply_irls(r, Jc, Jl, d.huber);
 #pragma unroll
     for (int q = 0; q < 9; q++) {
         const float s = d.sp[9 * cam + q];
@@ -589,6 +614,7 @@ __global__ void __launch_bounds__(NT) k_marg_large(DevProblem d, const LargeItem
         load_cam(d.cams, cam, c);
         const double2 uv = d.obs_uv[obs0 + o];
         cam_model(c, Xp[0], Xp[1], Xp[2], uv.x, uv.y, r, Jc, Jl);
+        apply_irls(r, Jc, Jl, d.huber);
         if (!MULTI) {
 #pragma unroll
             for (int q = 0; q < 9; q++) {
@@ -1377,23 +1403,41 @@ __global__ void __launch_bounds__(HUGE_NT) k_huge_out(DevProblem d, float *__res
 }
 
 // FP64 sum over the SM slices (stride `stride` floats per camera, `nv` values used), zeroing them
-// for the next launch: out[nv * cam + e] = sum_s slice_s[stride * cam + e].
+// for the next launch: out[nv * cam + e] = sum_s slice_s[stride * cam + e].  CTA = 32 outputs x 8
+// slice phases (each thread sums every 8th slice, loads unrolled), then an 8-way smem reduction.
 __global__ void __launch_bounds__(256) k_reduce_slices(float *__restrict__ sl, int64_t n_p, int stride, int nv,
                                                        int nslice, double *__restrict__ out,
                                                        const PcgState *__restrict__ st) {
     if (st && st->done) return;  // PCG graph: no matvec ran, the slices are still zero
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= nv * n_p) return;
-    const int64_t cam = i / nv;
-    const int64_t e = stride * cam + (i - nv * cam);
-    const int64_t S = (int64_t)stride * n_p;
+    __shared__ double part[8][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int64_t i = (int64_t)blockIdx.x * 32 + tx;
     double s = 0.0;
-    for (int k = 0; k < nslice; k++) {
-        float *q = sl + k * S + e;
-        s += (double)*q;
-        *q = 0.f;
+    if (i < nv * n_p) {
+        const int64_t cam = i / nv;
+        const int64_t e = stride * cam + (i - nv * cam);
+        const int64_t S = (int64_t)stride * n_p;
+        int k = ty;
+        for (; k + 24 < nslice; k += 32) {
+            float *q0 = sl + k * S + e, *q1 = q0 + 8 * S, *q2 = q0 + 16 * S, *q3 = q0 + 24 * S;
+            const float a0 = *q0, a1 = *q1, a2 = *q2, a3 = *q3;
+            *q0 = 0.f, *q1 = 0.f, *q2 = 0.f, *q3 = 0.f;
+            s += ((double)a0 + (double)a1) + ((double)a2 + (double)a3);
+        }
+        for (; k < nslice; k += 8) {
+            float *q = sl + k * S + e;
+            s += (double)*q;
+            *q = 0.f;
+        }
     }
-    out[i] = s;
+    part[ty][tx] = s;
+    __syncthreads();
+    if (ty == 0 && i < nv * n_p) {
+        double t = 0.0;
+#pragma unroll
+        for (int y = 0; y < 8; y++) t += part[y][tx];
+        out[i] = t;
+    }
 }
 
 // out = H~ v = wd + lambda D_p^2 v  (test hook, FP32 out)
@@ -1514,45 +1558,51 @@ __global__ void __launch_bounds__(1024) k_pcg_step(DevProblem d, float lam_f, do
 }
 
 // ============================================================================ K7 back-substitution
+// Warp per landmark (grid-stride), lanes over the flattened 9k pose columns of R1 (coalesced), the
+// three row sums reduced with shuffles; lane 0 solves the 3x3 upper-triangular system.  The
+// model-decrease sums go out once per CTA (not per landmark: same-address FP64 atomics serialize).
 __global__ void __launch_bounds__(256) k_backsub(DevProblem d, float lam) {
-    const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    __shared__ double red[32];
     const int lane = threadIdx.x & 31;
-    if (j >= d.n_l) return;
-    const int k = d.lm_k[j];
-    const float *side = d.arena + d.lm_side[j];
-    const int W = 9 * k;
-    const int64_t obs0 = d.lm_obs0[j];
-    float s0 = 0.f, s1 = 0.f, s2 = 0.f;
-    for (int o = lane; o < k; o += 32) {  // lane <-> camera block: one gather of dp per block
-        const double *dp = d.x + 9 * (int64_t)d.obs_cam[obs0 + o];
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    double q1 = 0.0, dd = 0.0;
+    for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < d.n_l; j += nwarps) {
+        const int k = d.lm_k[j];
+        const float *side = d.arena + d.lm_side[j];
+        const int W = 9 * k;
+        const int32_t *oc = d.obs_cam + d.lm_obs0[j];
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+        for (int c = lane; c < W; c += 32) {
+            const int o = c / 9, q = c - 9 * o;
+            const float v = (float)d.x[9 * (int64_t)oc[o] + q];
+            s0 += side[c] * v;
+            s1 += side[W + c] * v;
+            s2 += side[2 * W + c] * v;
+        }
+        s0 = warp_sum_f(s0);
+        s1 = warp_sum_f(s1);
+        s2 = warp_sum_f(s2);
+        if (lane == 0) {
+            const float4 *TL = reinterpret_cast<const float4 *>(side + side_tl(k));
+            const float4 t0 = TL[0], t1 = TL[1], t2 = TL[2];
+            const float b0 = t0.w + s0, b1 = t1.w + s1, b2 = t2.w + s2;
+            const float x2 = b2 / t2.z;
+            const float x1 = (b1 - t1.z * x2) / t1.y;
+            const float x0 = (b0 - t0.y * x1 - t0.z * x2) / t0.x;
+            const float dl[3] = {-x0, -x1, -x2};
+            q1 += (double)t0.w * t0.w + (double)t1.w * t1.w + (double)t2.w * t2.w;
 #pragma unroll
-        for (int q = 0; q < 9; q++) {
-            const float v = (float)dp[q];
-            s0 += side[9 * o + q] * v;
-            s1 += side[W + 9 * o + q] * v;
-            s2 += side[2 * W + 9 * o + q] * v;
+            for (int q = 0; q < 3; q++) {
+                d.dl[3 * j + q] = dl[q];
+                d.pts_trial[3 * j + q] = d.pts[3 * j + q] + (double)(d.lm_s[3 * j + q] * dl[q]);
+                const double Dd = (double)d.lm_D[3 * j + q] * dl[q];
+                dd += Dd * Dd;
+            }
         }
     }
-    s0 = warp_sum_f(s0);
-    s1 = warp_sum_f(s1);
-    s2 = warp_sum_f(s2);
-    if (lane == 0) {
-        const float4 *TL = reinterpret_cast<const float4 *>(side + side_tl(k));
-        const float4 t0 = TL[0], t1 = TL[1], t2 = TL[2];
-        const float b0 = t0.w + s0, b1 = t1.w + s1, b2 = t2.w + s2;
-        const float x2 = b2 / t2.z;
-        const float x1 = (b1 - t1.z * x2) / t1.y;
-        const float x0 = (b0 - t0.y * x1 - t0.z * x2) / t0.x;
-        const float dl[3] = {-x0, -x1, -x2};
-        double q1 = (double)t0.w * t0.w + (double)t1.w * t1.w + (double)t2.w * t2.w;
-        double dd = 0.0;
-#pragma unroll
-        for (int q = 0; q < 3; q++) {
-            d.dl[3 * j + q] = dl[q];
-            d.pts_trial[3 * j + q] = d.pts[3 * j + q] + (double)(d.lm_s[3 * j + q] * dl[q]);
-            const double Dd = (double)d.lm_D[3 * j + q] * dl[q];
-            dd += Dd * Dd;
-        }
+    q1 = block_sum_d(q1, red);
+    dd = block_sum_d(dd, red);
+    if (threadIdx.x == 0) {
         atomicAdd(d.scal + SC_Q1R2, q1);
         atomicAdd(d.scal + SC_DAMPL, (double)lam * dd);
     }
@@ -1586,7 +1636,7 @@ __global__ void __launch_bounds__(256) k_cost(DevProblem d, const double *__rest
         const double2 uv = d.obs_uv[i];
         const double Pz = cam_model(c, X[0], X[1], X[2], uv.x, uv.y, r, nullptr, nullptr);
         if (!(Pz < 0.0) || !isfinite(r[0]) || !isfinite(r[1])) bad = 1.0;
-        else e = r[0] * r[0] + r[1] * r[1];
+        else e = robust_rho(r[0] * r[0] + r[1] * r[1], d.huber);
     }
     e = block_sum_d(e, red);
     bad = block_sum_d(bad, red);
@@ -1752,7 +1802,7 @@ static void pipes_all(rba_ctx *c, const float *v, float *out12, const PcgState *
 }
 
 static void reduce_slices(rba_ctx *c, float *sl, int stride, int nv, double *out, const PcgState *st) {
-    k_reduce_slices<<<nblk(nv * c->d.n_p, 256), 256, 0, c->stream>>>(sl, c->d.n_p, stride, nv, c->d.nslice, out, st);
+    k_reduce_slices<<<nblk(nv * c->d.n_p, 32), 256, 0, c->stream>>>(sl, c->d.n_p, stride, nv, c->d.nslice, out, st);
     c->launches++;
 }
 
@@ -1844,7 +1894,8 @@ cudaError_t build_pcg_graph(rba_ctx *c) {
 cudaError_t launch_backsub(rba_ctx *c, float lam) {
     Prof P(c, KID_BACKSUB, 0.0);
     if (c->d.n_l) {
-        k_backsub<<<nblk(32 * c->d.n_l, 256), 256, 0, c->stream>>>(c->d, lam);
+        const unsigned g = (unsigned)std::min<int64_t>(nblk(32 * c->d.n_l, 256), (int64_t)c->num_sms * 8);
+        k_backsub<<<g, 256, 0, c->stream>>>(c->d, lam);
         c->launches++;
     }
     k_trial_cams<<<1, 1024, 0, c->stream>>>(c->d, lam);

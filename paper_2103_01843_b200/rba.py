@@ -29,7 +29,8 @@ class rba_options(C.Structure):
     _fields_ = [("device", C.c_int), ("stream", C.c_void_p), ("world", C.c_int), ("rank", C.c_int),
                 ("nccl_unique_id", C.c_void_p), ("lambda0", C.c_double), ("pcg_rel_tol", C.c_double),
                 ("pcg_max_iters", C.c_int), ("min_rel_decrease", C.c_double), ("diag_min", C.c_double),
-                ("diag_max", C.c_double), ("alloc", _ALLOC_T), ("free", _FREE_T), ("alloc_ctx", C.c_void_p)]
+                ("diag_max", C.c_double), ("alloc", _ALLOC_T), ("free", _FREE_T), ("alloc_ctx", C.c_void_p),
+                ("huber_delta", C.c_double)]
 
 
 class rba_pcg_stats(C.Structure):
@@ -43,6 +44,13 @@ class rba_lm_report(C.Structure):
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class rba_bal(C.Structure):
+    _fields_ = [("n_cams", C.c_int64), ("n_points", C.c_int64), ("n_obs", C.c_int64),
+                ("cameras", C.POINTER(C.c_double)), ("points", C.POINTER(C.c_double)),
+                ("obs_uv", C.POINTER(C.c_double)), ("obs_cam", C.POINTER(C.c_int32)),
+                ("obs_pt", C.POINTER(C.c_int32))]
 
 
 class RBAError(RuntimeError):
@@ -81,6 +89,14 @@ def _load():
         "rba_plan_shards": (I, [P, I64, I, P]),
         "rba_nccl_unique_id": (I, [P]),
         "rba_last_error": (C.c_char_p, []),
+        "rba_bal_parse": (I, [C.c_char_p, C.c_size_t, C.POINTER(rba_bal)]),
+        "rba_bal_read": (I, [C.c_char_p, C.POINTER(rba_bal)]),
+        "rba_bal_write": (I, [C.c_char_p, C.POINTER(rba_bal)]),
+        "rba_bal_normalize": (I, [C.POINTER(rba_bal), D]),
+        "rba_bal_perturb": (I, [C.POINTER(rba_bal), D, D, D, C.c_uint64]),
+        "rba_bal_filter": (I, [C.POINTER(rba_bal), D, C.POINTER(I64), C.POINTER(I64)]),
+        "rba_bal_free": (None, [C.POINTER(rba_bal)]),
+        "rba_bal_last_error": (C.c_char_p, []),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -94,7 +110,8 @@ EXPORTED = ["rba_default_options", "rba_create", "rba_destroy", "rba_linearize",
             "rba_pcg_solve", "rba_backsubstitute", "rba_cost", "rba_lm_step", "rba_get_state", "rba_set_state", "rba_reset_lm",
             "rba_matvec", "rba_get_rhs", "rba_get_step", "rba_get_scaling", "rba_export_block", "rba_arena_bytes",
             "rba_kernel_launches", "rba_profile", "rba_profile_get", "rba_plan_shards", "rba_nccl_unique_id",
-            "rba_last_error"]
+            "rba_last_error", "rba_bal_parse", "rba_bal_read", "rba_bal_write", "rba_bal_normalize",
+            "rba_bal_perturb", "rba_bal_filter", "rba_bal_free", "rba_bal_last_error"]
 
 
 def lib():
@@ -249,6 +266,78 @@ def rba_nccl_unique_id() -> bytes:
 
 def rba_last_error() -> str:
     return _lib.rba_last_error().decode()
+
+
+# ------------------------------------------------------------------------- BAL ingest (f1)
+def _bal_check(status):
+    if status != RBA_OK:
+        raise RBAError(status, _lib.rba_bal_last_error().decode())
+
+
+class BalProblem:
+    """A BAL problem owned by librba (host memory); every operation runs in librba's C++."""
+
+    def __init__(self, b: rba_bal):
+        self.b = b
+
+    @classmethod
+    def parse(cls, text: str | bytes):
+        data = text.encode() if isinstance(text, str) else text
+        b = rba_bal()
+        _bal_check(_lib.rba_bal_parse(data, len(data), C.byref(b)))
+        return cls(b)
+
+    @classmethod
+    def read(cls, path: str):
+        b = rba_bal()
+        _bal_check(_lib.rba_bal_read(os.fsencode(path), C.byref(b)))
+        return cls(b)
+
+    def write(self, path: str):
+        _bal_check(_lib.rba_bal_write(os.fsencode(path), C.byref(self.b)))
+
+    def normalize(self, target_mad: float = 100.0):
+        _bal_check(_lib.rba_bal_normalize(C.byref(self.b), float(target_mad)))
+        return self
+
+    def perturb(self, sigma_rot: float, sigma_centre: float, sigma_point: float, seed: int):
+        _bal_check(_lib.rba_bal_perturb(C.byref(self.b), float(sigma_rot), float(sigma_centre), float(sigma_point),
+                                        int(seed) & 0xFFFFFFFFFFFFFFFF))
+        return self
+
+    def filter(self, z_min: float = 1e-8):
+        ro, rp = C.c_int64(), C.c_int64()
+        _bal_check(_lib.rba_bal_filter(C.byref(self.b), float(z_min), C.byref(ro), C.byref(rp)))
+        return ro.value, rp.value
+
+    def as_problem(self) -> dict:
+        """Copies in the dict layout Solver / rba_create take (cameras_init, points_init, obs_*)."""
+        b = self.b
+        arr = lambda ptr, n, shape: np.ctypeslib.as_array(ptr, shape=(max(n, 1),))[:n].reshape(shape).copy()
+        return dict(cameras_init=arr(b.cameras, 9 * b.n_cams, (b.n_cams, 9)),
+                    points_init=arr(b.points, 3 * b.n_points, (b.n_points, 3)),
+                    obs_cam=arr(b.obs_cam, b.n_obs, (b.n_obs,)), obs_pt=arr(b.obs_pt, b.n_obs, (b.n_obs,)),
+                    obs_uv=arr(b.obs_uv, 2 * b.n_obs, (b.n_obs, 2)))
+
+    def __del__(self):
+        try:
+            _lib.rba_bal_free(C.byref(self.b))
+        except Exception:
+            pass
+
+
+def load_bal(path: str, normalize: bool = True, sigma_rot: float = 0.0, sigma_centre: float = 0.0,
+             sigma_point: float = 0.0, seed: int = 0, z_min: float | None = 1e-8) -> dict:
+    """BAL file -> problem dict with the paper's preprocessing: gauge normalization to
+    median absolute deviation 100, seeded perturbation, z-filter."""
+    p = BalProblem.read(path)
+    if normalize:
+        p.normalize(100.0)
+    if sigma_rot or sigma_centre or sigma_point:
+        p.perturb(sigma_rot, sigma_centre, sigma_point, seed)
+    if z_min is not None:
+        p.filter(z_min)
+    return p.as_problem()
 
 
 # ------------------------------------------------------------------------- convenience

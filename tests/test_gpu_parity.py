@@ -243,3 +243,36 @@ def test_huge_tracks_lm():
     for i in range(3):
         rg, ro = s.lm_step(), o.lm_step()
         assert abs(rg["cost_after"] - ro["cost_after"]) <= 1e-4 * ro["cost_after"], (i, rg, ro)
+
+
+# --------------------------------------------------------------------------- robust loss (f1)
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_huber_reduced_system_and_lm(cfg):
+    """Huber (delta = 1 px, IRLS) on the GPU vs the oracle: E, b~ and H~ probes at the
+    first linearization, then the cost after each of 5 LM iterations (<= 1e-4)."""
+    p = synth.make_problem(cfg)
+    s = _solver(p, huber_delta=1.0)
+    s.linearize()
+    s.marginalize(1e-4)
+    o = oracle.Oracle(p)
+    o.set_huber(1.0)
+    o.linearize()
+    o.marginalize()
+    o.damp(1e-4)
+    assert abs(s.cost() - o.cost()) <= 1e-6 * o.cost()
+    rng = np.random.default_rng(4)
+    for _ in range(3):
+        v = rng.normal(size=9 * o.n_p)
+        g = s.matvec(torch.tensor(v, dtype=torch.float32, device="cuda")).double().cpu().numpy()
+        assert relf(g, o.matvec(v)) <= 1e-4
+    s.pcg()
+    assert o.precond_rhs() == 0
+    assert relf(s.rhs(), o.rhs()) <= 1e-4
+    s.close()
+    s = _solver(p, huber_delta=1.0)
+    o = oracle.Oracle(p)
+    o.set_huber(1.0)
+    for i in range(5):
+        rg, ro = s.lm_step(), o.lm_step()
+        assert rg["pcg_reason"] != 2
+        assert abs(rg["cost_after"] - ro["cost_after"]) <= 1e-4 * ro["cost_after"], (i, rg, ro)
