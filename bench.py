@@ -43,6 +43,7 @@ WORKLOADS = {
     4: "cfg4: venice1778-shaped street BA, 1778 cams, 993k lms, ~5.0M obs (0.5% tracks 50-400)",
     5: "cfg5: final13682-shaped street BA, 13682 cams, 4.46M lms, ~30M obs",
 }
+SOLVERS = {"sqrtba": 0, "sc32": 1, "sc64": 2}
 METRIC = "LM iterations/s (FP32 sqrt-BA step) and QR-marginalized obs/s; % of HBM roofline"
 
 
@@ -196,6 +197,9 @@ def main():
     ap.add_argument("--cpu-every", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--solver", default="sqrtba", choices=list(SOLVERS),
+                    help="landmark elimination: sqrt-BA (the paper's method, default) or the explicit "
+                         "Schur-complement baselines explicit-32 / explicit-64 (SURVEY §8f f3)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -217,7 +221,7 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     n_p, n_l, n_obs = prob["cameras_init"].shape[0], prob["points_init"].shape[0], len(prob["obs_cam"])
-    s = rba.Solver(prob, device=local, world=world, rank=rank, nccl_id=nccl_id)
+    s = rba.Solver(prob, device=local, world=world, rank=rank, nccl_id=nccl_id, solver=SOLVERS[args.solver])
     stream = s.stream
 
     def barrier():
@@ -324,8 +328,10 @@ def main():
     line = {
         "metric": METRIC, "value": args.steps / (t_ms * 1e-3), "unit": "LM iterations/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64" if args.solver == "sc64" else "f32", "data": "synthetic",
         "config": {"workload": WORKLOADS[args.config], "cfg": args.config, "n_p": n_p, "n_l": n_l, "n_obs": n_obs,
+                   "solver": {"sqrtba": "sqrt-BA-32 (QR nullspace marginalization)", "sc32": "explicit-32 (Schur complement)",
+                              "sc64": "explicit-64 (Schur complement)"}[args.solver],
                    "parallelism": f"landmark-shard x{world}",
                    "l2": "inputs larger than L2 (landmark-block arena >> 126 MB)" if args.config >= 3 else
                    "working set L2-resident (no flush)"},

@@ -63,7 +63,16 @@ typedef struct {
      * becomes sum rho(|r|^2) with rho(s) = s (s <= delta^2) else 2 delta sqrt(s) - delta^2, and every
      * residual / Jacobian row is weighted by sqrt(rho'(|r|^2)) at linearization (IRLS). */
     double huber_delta;
+    /* landmark elimination: RBA_SOLVER_SQRTBA (default; nullspace
+     * marginalization by QR), or the paper's explicit Schur-complement baselines
+     * "explicit-32" / "explicit-64": H~ formed explicitly as 9 x 9 blocks on
+     * the covisibility graph in FP32 / FP64, solved by the same PCG / LM.  In the SC modes
+     * rba_marginalize_qr forms the Schur complement, rba_export_block is RBA_ERR_STATE and
+     * rba_arena_bytes reports the block-sparse H~. */
+    int solver;
 } rba_options;
+
+enum { RBA_SOLVER_SQRTBA = 0, RBA_SOLVER_EXPLICIT_SC32 = 1, RBA_SOLVER_EXPLICIT_SC64 = 2 };
 
 typedef struct {
     int iters;           /* PCG iterations performed                                          */

@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librba.so")
-SOURCES = ["rba_kernels.cu", "rba_api.cu", "rba_bal.cpp"]
+SOURCES = ["rba_kernels.cu", "rba_sc.cu", "rba_api.cu", "rba_bal.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -35,20 +35,23 @@ def nvcc():
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """Compile librba.so (or, with `defines` / `out`, a tuning variant of it for tools/)."""
+    lib = out or LIB
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    deps = srcs + [os.path.join(CSRC, "rba_internal.cuh"), os.path.join(ROOT, "include", "rba.h")]
-    if not force and os.path.exists(LIB) and all(os.path.getmtime(LIB) >= os.path.getmtime(d) for d in deps):
-        return LIB
+    deps = srcs + [os.path.join(CSRC, h) for h in ("rba_internal.cuh", "rba_model.cuh")] + \
+        [os.path.join(ROOT, "include", "rba.h")]
+    if not force and os.path.exists(lib) and all(os.path.getmtime(lib) >= os.path.getmtime(d) for d in deps):
+        return lib
     inc, libdir = _nccl_dirs()
     common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-              "-I", os.path.join(ROOT, "include"), "-I", inc]
+              "-I", os.path.join(ROOT, "include"), "-I", inc] + [f"-D{x}" for x in defines]
     if verbose:
         common += ["-Xptxas", "-v"]
     objs = []
 
     def comp(src):
-        obj = os.path.join(CSRC, os.path.basename(src) + ".o")
+        obj = os.path.join(CSRC, os.path.basename(src) + f".{os.path.basename(lib)}.o")
         r = subprocess.run(common + ["-c", src, "-o", obj], capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
@@ -58,14 +61,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with ThreadPoolExecutor(len(srcs)) as ex:
         objs = list(ex.map(comp, srcs))
-    link = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-L", libdir, "-l:libnccl.so.2",
+    link = [nvcc(), *ARCH, "-shared", "-o", lib, *objs, "-L", libdir, "-l:libnccl.so.2",
             "-Xlinker", f"-rpath,{libdir}"]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
     for o in objs:
         os.remove(o)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

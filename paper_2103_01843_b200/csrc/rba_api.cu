@@ -195,7 +195,7 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
         return fail(RBA_ERR_INVALID_ARG, "rba_create: null pointer or negative size");
     if (opt.world < 1 || opt.rank < 0 || opt.rank >= opt.world || !(opt.lambda0 > 0) || !(opt.pcg_rel_tol >= 0) ||
         opt.pcg_max_iters < 0 || !(opt.diag_min > 0) || !(opt.diag_max >= opt.diag_min) ||
-        !(opt.huber_delta >= 0) || !std::isfinite(opt.huber_delta))
+        !(opt.huber_delta >= 0) || !std::isfinite(opt.huber_delta) || opt.solver < 0 || opt.solver > 2)
         return fail(RBA_ERR_INVALID_ARG, "rba_create: bad options");
     if (n_obs >= (int64_t)1 << 31 || n_points >= (int64_t)1 << 31 || n_cams >= (int64_t)1 << 28)
         return fail(RBA_ERR_INVALID_ARG, "rba_create: problem too large for int32 indices");
@@ -462,6 +462,7 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     d.n_p = n_cams;
     d.n_l = nl;
     d.huber = opt.huber_delta;
+    d.sc = opt.solver;
     d.n_obs = nobs_loc;
     CKSC(dalloc_n(c, &d.cams, 9 * n_cams));
     CKSC(dalloc_n(c, &d.cams_trial, 9 * n_cams));
@@ -480,6 +481,45 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     CKSC(dalloc_n(c, &d.Dp2, 9 * n_cams));
     CKSC(dalloc_n(c, &d.lm_s, 3 * nl));
     CKSC(dalloc_n(c, &d.lm_D, 3 * nl));
+    if (d.sc) {
+        // explicit SC: no landmark blocks; the covisibility graph of the local landmarks as BSR
+        // (both triangles, columns ascending per camera row)
+        c->arena_floats = 4;
+        std::vector<std::vector<int32_t>> cam_lms(n_cams);
+        std::vector<int32_t> hcam(nobs_loc);
+        for (int64_t i = 0; i < nl; i++) {
+            const int64_t g0 = gptr[loc[i]];
+            for (int o = 0; o < c->h_k[i]; o++) {
+                hcam[h_obs0[i] + o] = obs_cam[ord[g0 + o]];
+                cam_lms[obs_cam[ord[g0 + o]]].push_back((int32_t)i);
+            }
+        }
+        std::vector<int32_t> bptr(n_cams + 1, 0), bcol, mark(n_cams, -1);
+        for (int64_t c1 = 0; c1 < n_cams; c1++) {
+            const size_t r0 = bcol.size();
+            for (int32_t i : cam_lms[c1])
+                for (int o = 0; o < c->h_k[i]; o++) {
+                    const int32_t c2 = hcam[h_obs0[i] + o];
+                    if (mark[c2] != (int32_t)c1) mark[c2] = (int32_t)c1, bcol.push_back(c2);
+                }
+            if (mark[c1] != (int32_t)c1) bcol.push_back((int32_t)c1);  // diagonal block always present
+            std::sort(bcol.begin() + r0, bcol.end());
+            bptr[c1 + 1] = (int32_t)bcol.size();
+            if (bcol.size() >= (size_t)1 << 31) return bail(fail(RBA_ERR_BAD_PROBLEM, "explicit SC: too many blocks"));
+        }
+        d.nnzb = (int64_t)bcol.size();
+        const size_t ts = d.sc == 2 ? sizeof(double) : sizeof(float);
+        CKSC(dalloc_n(c, &d.bsr_ptr, n_cams + 1));
+        CKSC(dalloc_n(c, &d.bsr_col, d.nnzb));
+        CKSC(dalloc(c, &d.bsr_val, ts * 81 * (size_t)d.nnzb));
+        CKSC(dalloc(c, &d.sc_b, ts * 9 * (size_t)n_cams));
+        CKSC(dalloc(c, &d.sc_scratch, ts * 54 * (size_t)std::max<int64_t>(nobs_loc, 1)));
+        CKC(cudaMemcpyAsync(d.bsr_ptr, bptr.data(), sizeof(int32_t) * bptr.size(), cudaMemcpyHostToDevice, c->stream));
+        CKC(cudaMemcpyAsync(d.bsr_col, bcol.data(), sizeof(int32_t) * bcol.size(), cudaMemcpyHostToDevice, c->stream));
+        CKC(cudaStreamSynchronize(c->stream));  // host staging vectors go out of scope
+        c->matvec_bytes = (double)ts * 81 * d.nnzb;       // one read of H~ per product
+        c->marg_bytes = (double)ts * 81 * d.nnzb + 48.0 * nobs_loc;
+    }
     CKSC(dalloc_n(c, &d.arena, c->arena_floats));
     {
         int nsm = 0;
@@ -638,7 +678,10 @@ extern "C" rba_status rba_marginalize_qr(rba_ctx *c, double lambda) {
     if (!(lambda >= 0) || !std::isfinite(lambda)) return fail(RBA_ERR_INVALID_ARG, "lambda must be finite and >= 0");
     if (!c->linearized) return fail(RBA_ERR_STATE, "rba_marginalize_qr before rba_linearize");
     CK(cudaSetDevice(c->device));
-    if (!c->marginalized) {
+    if (c->d.sc) {  // explicit SC: H_ll depends on lambda, so every new lambda re-forms H~
+        if (!c->marginalized || (float)lambda != (float)c->lambda_blocks) CK(launch_sc_build(c, (float)lambda));
+        c->marginalized = true;
+    } else if (!c->marginalized) {
         CK(launch_marginalize(c, (float)lambda));
         c->marginalized = true;
     } else if ((float)lambda != (float)c->lambda_blocks) {
@@ -657,7 +700,7 @@ extern "C" rba_status rba_pcg_solve(rba_ctx *c, rba_pcg_stats *stats) {
     DevProblem &d = c->d;
     const float lam = (float)c->lambda_blocks;
     CK(cudaMemsetAsync(d.scal + SC_BAD, 0, sizeof(double), c->stream));
-    CK(launch_precond_rhs(c));
+    CK(c->d.sc ? launch_sc_precond(c) : launch_precond_rhs(c));
     CKS(allreduce(c, d.pd, 54 * d.n_p, ncclDouble));
     CK(launch_precond_finalize(c, lam));
     CK(launch_pcg_init(c, (float)c->opt.pcg_rel_tol, c->opt.pcg_max_iters));
@@ -896,6 +939,7 @@ extern "C" rba_status rba_export_block(rba_ctx *c, int64_t landmark, double *buf
     if (landmark < 0 || landmark >= c->n_l_global || c->orig_to_int[landmark] < 0)
         return fail(RBA_ERR_INVALID_ARG, "landmark not owned by this rank");
     if (!c->marginalized) return fail(RBA_ERR_STATE, "rba_export_block before rba_marginalize_qr");
+    if (c->d.sc) return fail(RBA_ERR_STATE, "rba_export_block: explicit-SC mode keeps no landmark blocks");
     const int64_t j = c->orig_to_int[landmark];
     const int k = c->h_k[j];
     const int64_t R = 2 * k + 3, C = 9 * k + 4;
@@ -922,6 +966,10 @@ extern "C" rba_status rba_export_block(rba_ctx *c, int64_t landmark, double *buf
 
 extern "C" rba_status rba_arena_bytes(rba_ctx *c, int64_t *logical, int64_t *physical) {
     if (!c || !logical || !physical) return fail(RBA_ERR_INVALID_ARG, "null argument");
+    if (c->d.sc) {  // explicit SC: the block-sparse H~
+        *logical = *physical = (int64_t)(c->d.sc == 2 ? 8 : 4) * 81 * c->d.nnzb;
+        return RBA_OK;
+    }
     *logical = c->logical_bytes;
     *physical = c->arena_floats * 4;
     return RBA_OK;

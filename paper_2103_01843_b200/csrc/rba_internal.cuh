@@ -143,6 +143,13 @@ struct DevProblem {
     int64_t *cta_lo;        // per class: tile range boundaries of the persistent CTAs (bytes-balanced)
     HugeItem *huge_y, *huge_out;  // k > KLARGE: y-pass items (one per tile), out/precond items
     float *ybuf;                  // k > KLARGE: y = A v, 4 floats per 4-row tile
+    // explicit Schur-complement baseline (f3, rba_sc.cu): sc = 0 off (sqrt-BA), 1 FP32, 2 FP64
+    int sc;
+    int64_t nnzb;                 // 9 x 9 blocks of H~ on the covisibility graph (both triangles)
+    int32_t *bsr_ptr, *bsr_col;   // BSR rows per camera, columns ascending
+    void *bsr_val;                // nnzb x 81 (FP32 or FP64), row-major blocks
+    void *sc_b;                   // b~ accumulator, 9 n_p
+    void *sc_scratch;             // per observation: G_a (27) and L_a = G_a H_ll^-1 (27)
 };
 
 struct Launch {
@@ -225,6 +232,11 @@ cudaError_t launch_trial_cost(rba_ctx *c);
 cudaError_t launch_cost(rba_ctx *c, int at_trial, int slot);
 cudaError_t launch_commit(rba_ctx *c);
 cudaError_t launch_add_damping(rba_ctx *c, const float *v, float *out, float lambda);
+// explicit Schur complement (rba_sc.cu)
+cudaError_t launch_sc_build(rba_ctx *c, float lambda);
+cudaError_t launch_sc_precond(rba_ctx *c);
+void launch_sc_spmv(rba_ctx *c, const PcgState *st, const float *v32);
+cudaError_t launch_sc_backsub(rba_ctx *c, float lambda);
 // profiling scope: CUDA events on the context stream around one launch (rba_api.cu)
 struct Prof {
     rba_ctx *c;

@@ -22,181 +22,9 @@
 #include <cstdlib>
 
 #include "rba_internal.cuh"
+#include "rba_model.cuh"
 
 namespace rba {
-
-// ============================================================================ camera model
-// BAL / Snavely (readings C1, C2, C22): P = R(w) X + t, p = -P_xy / P_z,
-// d = 1 + k1 |p|^2 + k2 |p|^4, pi = f d p, r = pi - u.  Jacobians for the additive update of all
-// 9 camera parameters: dP/dw = -[R X]_x J_left(w).  Returns P_z.
-// Evaluated in FP64 from the FP64 state (reading C23): residuals r in FP64, the
-// Jacobians rounded to FP32 on output.  Everything downstream (blocks, QR, RCS, PCG) is FP32.
-__device__ __forceinline__ double cam_model(const double *__restrict__ cam, double X0, double X1, double X2,
-                                            double u, double v, double *r, float *Jc, float *Jl) {
-    const double w0 = cam[0], w1 = cam[1], w2 = cam[2];
-    const double th2 = w0 * w0 + w1 * w1 + w2 * w2;
-    double a, b, cc;  // R = I + a K + b K^2, J_left = I + b K + cc K^2
-    if (th2 < 1e-16) {
-        a = 1. - th2 * (1. / 6.);
-        b = 0.5 - th2 * (1. / 24.);
-        cc = 1. / 6. - th2 * (1. / 120.);
-    } else {
-        const double th = sqrt(th2);
-        double s, co;
-        sincos(th, &s, &co);
-        a = s / th;
-        const double hs = sin(0.5 * th);
-        b = 2. * hs * hs / th2;  // (1 - cos th) / th^2 without cancellation
-        cc = (th < 1e-2) ? (1.0 / 6.0 - th2 * (1.0 / 120.0) + th2 * th2 * (1.0 / 5040.0)) : (th - s) / (th2 * th);
-    }
-    const double cx0 = w1 * X2 - w2 * X1, cx1 = w2 * X0 - w0 * X2, cx2 = w0 * X1 - w1 * X0;
-    const double dx0 = w1 * cx2 - w2 * cx1, dx1 = w2 * cx0 - w0 * cx2, dx2 = w0 * cx1 - w1 * cx0;
-    const double RX0 = X0 + a * cx0 + b * dx0, RX1 = X1 + a * cx1 + b * dx1, RX2 = X2 + a * cx2 + b * dx2;
-    const double P0 = RX0 + cam[3], P1 = RX1 + cam[4], P2 = RX2 + cam[5];
-    const double iz = -1. / P2;
-    const double px = P0 * iz, py = P1 * iz;
-    const double n = px * px + py * py;
-    const double f = cam[6], k1 = cam[7], k2 = cam[8];
-    const double dd = 1. + k1 * n + k2 * n * n;
-    r[0] = f * dd * px - u;
-    r[1] = f * dd * py - v;
-    if (!Jc) return P2;
-    // dpi/dP = f (d I + e p p^T) * iz [[1,0,px],[0,1,py]]
-    const double e = 2. * (k1 + 2. * k2 * n);
-    const double D00 = f * (dd + e * px * px), D01 = f * e * px * py, D11 = f * (dd + e * py * py);
-    const double A00 = iz * D00, A01 = iz * D01, A02 = iz * (D00 * px + D01 * py);
-    const double A10 = iz * D01, A11 = iz * D11, A12 = iz * (D01 * px + D11 * py);
-    // R = (1 - b th2) I + a K + b w w^T
-    const double rd = 1. - b * th2;
-    const double R00 = rd + b * w0 * w0, R11 = rd + b * w1 * w1, R22 = rd + b * w2 * w2;
-    const double R01 = -a * w2 + b * w0 * w1, R02 = a * w1 + b * w0 * w2;
-    const double R10 = a * w2 + b * w0 * w1, R12 = -a * w0 + b * w1 * w2;
-    const double R20 = -a * w1 + b * w0 * w2, R21 = a * w0 + b * w1 * w2;
-    Jl[0] = (float)(A00 * R00 + A01 * R10 + A02 * R20);
-    Jl[1] = (float)(A00 * R01 + A01 * R11 + A02 * R21);
-    Jl[2] = (float)(A00 * R02 + A01 * R12 + A02 * R22);
-    Jl[3] = (float)(A10 * R00 + A11 * R10 + A12 * R20);
-    Jl[4] = (float)(A10 * R01 + A11 * R11 + A12 * R21);
-    Jl[5] = (float)(A10 * R02 + A11 * R12 + A12 * R22);
-    // J_left = (1 - cc th2) I + b K + cc w w^T
-    const double jd = 1. - cc * th2;
-    const double L00 = jd + cc * w0 * w0, L11 = jd + cc * w1 * w1, L22 = jd + cc * w2 * w2;
-    const double L01 = -b * w2 + cc * w0 * w1, L02 = b * w1 + cc * w0 * w2;
-    const double L10 = b * w2 + cc * w0 * w1, L12 = -b * w0 + cc * w1 * w2;
-    const double L20 = -b * w1 + cc * w0 * w2, L21 = b * w0 + cc * w1 * w2;
-    // B = A [RX]_x,  [RX]_x = [[0,-RX2,RX1],[RX2,0,-RX0],[-RX1,RX0,0]]
-    const double B00 = A01 * RX2 - A02 * RX1, B01 = -A00 * RX2 + A02 * RX0, B02 = A00 * RX1 - A01 * RX0;
-    const double B10 = A11 * RX2 - A12 * RX1, B11 = -A10 * RX2 + A12 * RX0, B12 = A10 * RX1 - A11 * RX0;
-    // d/dw = -B J_left
-    Jc[0] = (float)(-(B00 * L00 + B01 * L10 + B02 * L20));
-    Jc[1] = (float)(-(B00 * L01 + B01 * L11 + B02 * L21));
-    Jc[2] = (float)(-(B00 * L02 + B01 * L12 + B02 * L22));
-    Jc[9] = (float)(-(B10 * L00 + B11 * L10 + B12 * L20));
-    Jc[10] = (float)(-(B10 * L01 + B11 * L11 + B12 * L21));
-    Jc[11] = (float)(-(B10 * L02 + B11 * L12 + B12 * L22));
-    Jc[3] = (float)A00; Jc[4] = (float)A01; Jc[5] = (float)A02;
-    Jc[12] = (float)A10; Jc[13] = (float)A11; Jc[14] = (float)A12;
-    Jc[6] = (float)(dd * px); Jc[7] = (float)(f * n * px); Jc[8] = (float)(f * n * n * px);
-    Jc[15] = (float)(dd * py); Jc[16] = (float)(f * n * py); Jc[17] = (float)(f * n * n * py);
-    return P2;
-}
-
-// Huber norm on s = |r|^2 and its IRLS weight sqrt(rho'(s)) (Ceres' corrector with
-// rho'' = 0); delta <= 0: squared loss.
-__device__ __forceinline__ double robust_rho(double s, double delta) {
-    return (delta <= 0.0 || s <= delta * delta) ? s : 2.0 * delta * sqrt(s) - delta * delta;
-}
-__device__ __forceinline__ double robust_w(double s, double delta) {
-    return (delta <= 0.0 || s <= delta * delta) ? 1.0 : sqrt(delta / sqrt(s));
-}
-// weight the residual and the Jacobian rows of one observation (IRLS)
-__device__ __forceinline__ void apply_irls(double *r, float *Jc, float *Jl, double delta) {
-    if (delta <= 0.0) return;
-    const double w = robust_w(r[0] * r[0] + r[1] * r[1], delta);
-    const float wf = (float)w;
-    r[0] *= w;
-    r[1] *= w;
-#pragma unroll
-    for (int i = 0; i < 18; i++) Jc[i] *= wf;
-#pragma unroll
-    for (int i = 0; i < 6; i++) Jl[i] *= wf;
-}
-
-__device__ __forceinline__ void load_cam(const double *__restrict__ cams, int cam, double *c) {
-#pragma unroll
-    for (int q = 0; q < 9; q++) c[q] = __ldg(cams + 9 * cam + q);
-}
-
-// ============================================================================ reductions
-__device__ __forceinline__ double warp_sum_d(double v) {
-#pragma unroll
-    for (int m = 16; m; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
-    return v;
-}
-__device__ __forceinline__ float warp_sum_f(float v) {
-#pragma unroll
-    for (int m = 16; m; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
-    return v;
-}
-template <int G>
-__device__ __forceinline__ float group_sum(float v) {
-#pragma unroll
-    for (int m = G / 2; m; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m, G);
-    return v;
-}
-// block-wide sum of NV floats; every thread gets the result.  scratch: >= 32*NV floats.
-template <int NV>
-__device__ __forceinline__ void block_sum(float *v, float *scratch) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
-    for (int i = 0; i < NV; i++) v[i] = warp_sum_f(v[i]);
-    __syncthreads();
-    if (lane == 0)
-#pragma unroll
-        for (int i = 0; i < NV; i++) scratch[i * 32 + warp] = v[i];
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < NV; i++) {
-        float s = 0.f;
-        for (int w = 0; w < nw; w++) s += scratch[i * 32 + w];
-        v[i] = s;
-    }
-    __syncthreads();
-}
-__device__ __forceinline__ double block_sum_d(double v, double *scratch) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    v = warp_sum_d(v);
-    __syncthreads();
-    if (lane == 0) scratch[warp] = v;
-    __syncthreads();
-    double s = 0.0;
-    for (int w = 0; w < nw; w++) s += scratch[w];
-    __syncthreads();
-    return s;
-}
-
-// Camera-space partial sums of K4/K5 (matvec output, block-Jacobi blocks, b~) are accumulated in
-// FP32 into the slice of the SM that runs the thread and summed across slices in FP64 by
-// k_reduce_slices (reading C24): a single FP32 accumulator per camera summed the
-// contributions of thousands of landmarks in one chain, and its cancellation error was amplified by
-// PCG into a 1e-3 change of the solution.
-__device__ __forceinline__ unsigned smid() {
-    unsigned r;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ float *wslice(const DevProblem &d) { return d.wsl + (int64_t)smid() * 12 * d.n_p; }
-__device__ __forceinline__ float *pslice(const DevProblem &d) {
-    return d.psl + (int64_t)smid() * PACC_STRIDE * d.n_p;
-}
-
-// out12: camera stride 12 so the 9 entries of a camera go out as three 16-byte vector atomics
-__device__ __forceinline__ void flush_cam12(float *out12, int cam, const float *acc) {
-    float4 *o4 = reinterpret_cast<float4 *>(out12 + 12 * (int64_t)cam);
-    atomicAdd(o4, make_float4(acc[0], acc[1], acc[2], acc[3]));
-    atomicAdd(o4 + 1, make_float4(acc[4], acc[5], acc[6], acc[7]));
-    atomicAdd(o4 + 2, make_float4(acc[8], 0.f, 0.f, 0.f));
-}
 
 // ============================================================================ K0 / K1
 __global__ void k_check_depth(DevProblem d, int *bad) {
@@ -206,7 +34,7 @@ __global__ void k_check_depth(DevProblem d, int *bad) {
     load_cam(d.cams, d.obs_cam[i], c);
     const double *X = d.pts + 3 * (int64_t)d.obs_lm[i];
     const double2 uv = d.obs_uv[i];
-    const double Pz = cam_model(c, X[0], X[1], X[2], uv.x, uv.y, r, nullptr, nullptr);
+    const double Pz = cam_model<float>(c, X[0], X[1], X[2], uv.x, uv.y, r, nullptr, nullptr);
     if (!(Pz < -1e-8) || !isfinite(r[0]) || !isfinite(r[1])) atomicAdd(bad, 1);
 }
 
@@ -987,6 +815,21 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
+// streaming variant for the landmark blocks: L2 evict-first, so the read-once R2 stream does not
+// evict the L2-resident camera vectors and per-SM accumulation slices
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void bulk_g2s_stream(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
+                                                uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -1004,8 +847,17 @@ constexpr int SP_OFF_PACK = SP_OFF_CAM + 4 * SP_CAMCAP;
 constexpr int SP_OFF_UNIT = SP_OFF_PACK + (int)sizeof(Pack) * SP_PACKCAP;
 constexpr int SP_OFF_HDR = SP_OFF_UNIT + 2 * SP_UNITCAP;  // stage descriptor (written by the producer)
 constexpr int SP_SB = SP_OFF_HDR + 128;
-constexpr int SP_STAGES = 3;
-constexpr int SP_VCAP = 16384;                      // v (9 n_p floats) kept in shared memory if it fits
+#ifndef RBA_SP_STAGES
+#define RBA_SP_STAGES 3
+#endif
+#ifndef RBA_SP_VCAP
+#define RBA_SP_VCAP 16384
+#endif
+#ifndef RBA_PIPE_SMEM
+#define RBA_PIPE_SMEM 225000  // 3 stages of 4 x 512 x 36-byte tiles (measured +2.3% over 200 KB)
+#endif
+constexpr int SP_STAGES = RBA_SP_STAGES;
+constexpr int SP_VCAP = RBA_SP_VCAP;                // v (9 n_p floats) kept in shared memory if it fits
 constexpr size_t SP_SMEM = (size_t)SP_STAGES * SP_SB + 4 * SP_VCAP + 2 * SP_STAGES * sizeof(uint64_t);
 
 // one work unit: NRP row pairs starting at p0 of the lane's (landmark, camera block)
@@ -1090,6 +942,7 @@ __global__ void __launch_bounds__(SP_WARPS * 32 + 32, 1)
     __syncthreads();
     if (warp == SP_WARPS) {  // producer
         if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
             SmallChunk nxc{};
             if (lo < hi) nxc = d.chunks[lo];
             for (int64_t i = lo; i < hi; i++) {
@@ -1102,7 +955,7 @@ __global__ void __launch_bounds__(SP_WARPS * 32 + 32, 1)
                 mbar_arrive_expect_tx(&full[s], (uint32_t)ch.bytes + 4u * (uint32_t)ch.ncam +
                                                     (uint32_t)sizeof(Pack) * (uint32_t)ch.np + 2u * (uint32_t)ch.nunit);
                 unsigned char *dst = sm + (size_t)s * SP_SB;
-                bulk_g2s(dst, d.arena + ch.base, (uint32_t)ch.bytes, &full[s]);
+                bulk_g2s_stream(dst, d.arena + ch.base, (uint32_t)ch.bytes, &full[s], pol);
                 bulk_g2s(dst + SP_OFF_CAM, d.obs_cam + ch.cam0, 4u * (uint32_t)ch.ncam, &full[s]);
                 bulk_g2s(dst + SP_OFF_PACK, d.packs + ch.p0, (uint32_t)sizeof(Pack) * ch.np, &full[s]);
                 bulk_g2s(dst + SP_OFF_UNIT, d.units + ch.unit0, 2u * (uint32_t)ch.nunit, &full[s]);
@@ -1154,7 +1007,7 @@ struct PipeCfg {
     static constexpr int NC = NS * NSLOT;           // consumer threads
     static constexpr int TB = 144 * NS;             // bytes of the largest tile (k <= NS)
     static constexpr int SB = TB * NSLOT;           // stage bytes
-    static constexpr int STAGES = (200 * 1024) / SB > 8 ? 8 : (200 * 1024) / SB;
+    static constexpr int STAGES = RBA_PIPE_SMEM / SB > 8 ? 8 : RBA_PIPE_SMEM / SB;
     static constexpr size_t SMEM = (size_t)STAGES * SB + 2 * STAGES * sizeof(uint64_t);
 };
 
@@ -1183,6 +1036,7 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
     __syncthreads();
     if (tid >= C::NC) {  // ---------------- producer warp: one elected lane streams the tiles
         if (tid == C::NC) {
+            const uint64_t pol = policy_evict_first();
             // descriptors (arena offset, k) of the next stage are loaded one stage ahead, as
             // independent loads, so their latency overlaps the wait and the current copies
             int64_t noff[NSLOT];
@@ -1213,8 +1067,8 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
 #pragma unroll
                 for (int sl = 0; sl < NSLOT; sl++)
                     if (ck[sl])
-                        bulk_g2s(sm + (size_t)s * C::SB + (size_t)sl * C::TB, d.arena + coff[sl], 144u * (uint32_t)ck[sl],
-                                 &full[s]);
+                        bulk_g2s_stream(sm + (size_t)s * C::SB + (size_t)sl * C::TB, d.arena + coff[sl], 144u * (uint32_t)ck[sl],
+                                 &full[s], pol);
             }
         }
         return;
@@ -1610,7 +1464,7 @@ __global__ void __launch_bounds__(256) k_backsub(DevProblem d, float lam) {
 
 // trial cameras x_p + S_p dp and the (replicated) camera part of the model decrease (C10):
 // sum_i (-b~_i dp_i + rho_i dp_i + lam D_p,i^2 dp_i^2)
-__global__ void __launch_bounds__(1024) k_trial_cams(DevProblem d, float lam) {
+__global__ void __launch_bounds__(1024) k_trial_cams(DevProblem d, float lam, int with_model) {
     __shared__ double red[32];
     const int64_t N = 9 * d.n_p;
     double m = 0.0;
@@ -1620,7 +1474,7 @@ __global__ void __launch_bounds__(1024) k_trial_cams(DevProblem d, float lam) {
         m += -d.bt[i] * dp + d.r[i] * dp + (double)lam * d.Dp2[i] * dp * dp;
     }
     m = block_sum_d(m, red);
-    if (threadIdx.x == 0) d.scal[SC_MODELP] = m;
+    if (threadIdx.x == 0) d.scal[SC_MODELP] = with_model ? m : 0.0;
 }
 
 // ============================================================================ K8 cost
@@ -1634,7 +1488,7 @@ __global__ void __launch_bounds__(256) k_cost(DevProblem d, const double *__rest
         load_cam(cams, d.obs_cam[i], c);
         const double *X = pts + 3 * (int64_t)d.obs_lm[i];
         const double2 uv = d.obs_uv[i];
-        const double Pz = cam_model(c, X[0], X[1], X[2], uv.x, uv.y, r, nullptr, nullptr);
+        const double Pz = cam_model<float>(c, X[0], X[1], X[2], uv.x, uv.y, r, nullptr, nullptr);
         if (!(Pz < 0.0) || !isfinite(r[0]) || !isfinite(r[1])) bad = 1.0;
         else e = robust_rho(r[0] * r[0] + r[1] * r[1], d.huber);
     }
@@ -1820,10 +1674,19 @@ cudaError_t launch_precond_finalize(rba_ctx *c, float lam) {
     return cudaGetLastError();
 }
 
-static cudaError_t matvec_impl(rba_ctx *c, const float *v, const PcgState *st) {
-    Prof P(c, KID_MATVEC, plan_matvec_bytes(c));
+// wd = (H~ - lambda D_p^2) v: sqrt-BA product (Eq. cg_mult) or, in explicit-SC mode, the BSR SpMV
+static void matvec_body(rba_ctx *c, const float *v, const PcgState *st) {
+    if (c->d.sc) {
+        launch_sc_spmv(c, st, st ? nullptr : v);
+        return;
+    }
     pipes_all<false>(c, v, c->d.wsl, st);
     reduce_slices(c, c->d.wsl, 12, 9, c->d.wd, st);
+}
+
+static cudaError_t matvec_impl(rba_ctx *c, const float *v, const PcgState *st) {
+    Prof P(c, KID_MATVEC, plan_matvec_bytes(c));
+    matvec_body(c, v, st);
     P.end();
     return cudaGetLastError();
 }
@@ -1876,8 +1739,7 @@ cudaError_t build_pcg_graph(rba_ctx *c) {
     const int64_t nl = c->launches;
     c->stream = cs;
     c->profiling = false;
-    pipes_all<false>(c, c->d.p32, c->d.wsl, c->d.pcg);
-    reduce_slices(c, c->d.wsl, 12, 9, c->d.wd, c->d.pcg);
+    matvec_body(c, c->d.p32, c->d.pcg);
     k_pcg_step<<<1, 1024, 0, cs>>>(c->d, -1.f, c->opt.pcg_rel_tol, c->opt.pcg_max_iters, h, 1);
     c->stream = saved;
     c->profiling = prof;
@@ -1893,12 +1755,15 @@ cudaError_t build_pcg_graph(rba_ctx *c) {
 
 cudaError_t launch_backsub(rba_ctx *c, float lam) {
     Prof P(c, KID_BACKSUB, 0.0);
-    if (c->d.n_l) {
+    if (c->d.sc) {
+        cudaError_t e = launch_sc_backsub(c, lam);
+        if (e) return e;
+    } else if (c->d.n_l) {
         const unsigned g = (unsigned)std::min<int64_t>(nblk(32 * c->d.n_l, 256), (int64_t)c->num_sms * 8);
         k_backsub<<<g, 256, 0, c->stream>>>(c->d, lam);
         c->launches++;
     }
-    k_trial_cams<<<1, 1024, 0, c->stream>>>(c->d, lam);
+    k_trial_cams<<<1, 1024, 0, c->stream>>>(c->d, lam, c->d.sc ? 0 : 1);
     c->launches++;
     P.end();
     return cudaGetLastError();

@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librba.so")
+LIB_PATH = os.environ.get("RBA_LIB") or os.path.join(_HERE, "librba.so")  # RBA_LIB: build variants (tools/)
 
 RBA_OK, RBA_ERR_INVALID_ARG, RBA_ERR_BAD_PROBLEM, RBA_ERR_STATE, RBA_ERR_OOM, RBA_ERR_CUDA, RBA_ERR_NCCL = range(7)
 STATUS_NAMES = ["OK", "INVALID_ARG", "BAD_PROBLEM", "STATE", "OOM", "CUDA", "NCCL"]
@@ -30,7 +30,8 @@ class rba_options(C.Structure):
                 ("nccl_unique_id", C.c_void_p), ("lambda0", C.c_double), ("pcg_rel_tol", C.c_double),
                 ("pcg_max_iters", C.c_int), ("min_rel_decrease", C.c_double), ("diag_min", C.c_double),
                 ("diag_max", C.c_double), ("alloc", _ALLOC_T), ("free", _FREE_T), ("alloc_ctx", C.c_void_p),
-                ("huber_delta", C.c_double)]
+                ("huber_delta", C.c_double), ("solver", C.c_int)]
+RBA_SOLVER_SQRTBA, RBA_SOLVER_EXPLICIT_SC32, RBA_SOLVER_EXPLICIT_SC64 = 0, 1, 2
 
 
 class rba_pcg_stats(C.Structure):
