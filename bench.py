@@ -197,6 +197,9 @@ def main():
     ap.add_argument("--cpu-every", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--storage", default="dense", choices=["dense", "factored"],
+                    help="landmark-block storage: the paper's dense blocks (default) or the factored "
+                         "form (SURVEY §8f f4, beyond the paper)")
     ap.add_argument("--solver", default="sqrtba", choices=list(SOLVERS),
                     help="landmark elimination: sqrt-BA (the paper's method, default) or the explicit "
                          "Schur-complement baselines explicit-32 / explicit-64 (SURVEY §8f f3)")
@@ -221,7 +224,8 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     n_p, n_l, n_obs = prob["cameras_init"].shape[0], prob["points_init"].shape[0], len(prob["obs_cam"])
-    s = rba.Solver(prob, device=local, world=world, rank=rank, nccl_id=nccl_id, solver=SOLVERS[args.solver])
+    s = rba.Solver(prob, device=local, world=world, rank=rank, nccl_id=nccl_id, solver=SOLVERS[args.solver],
+                   storage=1 if args.storage == "factored" else 0)
     stream = s.stream
 
     def barrier():
@@ -332,6 +336,7 @@ def main():
         "config": {"workload": WORKLOADS[args.config], "cfg": args.config, "n_p": n_p, "n_l": n_l, "n_obs": n_obs,
                    "solver": {"sqrtba": "sqrt-BA-32 (QR nullspace marginalization)", "sc32": "explicit-32 (Schur complement)",
                               "sc64": "explicit-64 (Schur complement)"}[args.solver],
+                   "storage": args.storage,
                    "parallelism": f"landmark-shard x{world}",
                    "l2": "inputs larger than L2 (landmark-block arena >> 126 MB)" if args.config >= 3 else
                    "working set L2-resident (no flush)"},

@@ -70,7 +70,15 @@ typedef struct {
      * rba_marginalize_qr forms the Schur complement, rba_export_block is RBA_ERR_STATE and
      * rba_arena_bytes reports the block-sparse H~. */
     int solver;
+    /* landmark-block storage for RBA_SOLVER_SQRTBA: RBA_STORAGE_DENSE (default;
+     * the paper's (2k+3) x (9k+4) blocks) or RBA_STORAGE_FACTORED (beyond the
+     * paper: Householder vectors, compact-WY T, the 6 damping Givens and the scaled J_p, 176 + 112 k
+     * bytes per landmark; the reduced system is applied in O(k)).  Same results up to
+     * rounding; rba_export_block is RBA_ERR_STATE in factored mode. */
+    int storage;
 } rba_options;
+
+enum { RBA_STORAGE_DENSE = 0, RBA_STORAGE_FACTORED = 1 };
 
 enum { RBA_SOLVER_SQRTBA = 0, RBA_SOLVER_EXPLICIT_SC32 = 1, RBA_SOLVER_EXPLICIT_SC64 = 2 };
 

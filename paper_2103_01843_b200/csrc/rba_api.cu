@@ -195,7 +195,8 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
         return fail(RBA_ERR_INVALID_ARG, "rba_create: null pointer or negative size");
     if (opt.world < 1 || opt.rank < 0 || opt.rank >= opt.world || !(opt.lambda0 > 0) || !(opt.pcg_rel_tol >= 0) ||
         opt.pcg_max_iters < 0 || !(opt.diag_min > 0) || !(opt.diag_max >= opt.diag_min) ||
-        !(opt.huber_delta >= 0) || !std::isfinite(opt.huber_delta) || opt.solver < 0 || opt.solver > 2)
+        !(opt.huber_delta >= 0) || !std::isfinite(opt.huber_delta) || opt.solver < 0 || opt.solver > 2 ||
+        opt.storage < 0 || opt.storage > 1 || (opt.storage == 1 && opt.solver != 0))
         return fail(RBA_ERR_INVALID_ARG, "rba_create: bad options");
     if (n_obs >= (int64_t)1 << 31 || n_points >= (int64_t)1 << 31 || n_cams >= (int64_t)1 << 28)
         return fail(RBA_ERR_INVALID_ARG, "rba_create: problem too large for int32 indices");
@@ -407,7 +408,7 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
             const int k = c->h_k[i];
             if (!in_cls(k)) continue;
             const int T = large_tiles(k);
-            const int tpi2 = std::max(1, 262144 / (36 * k));
+            const int tpi2 = opt.storage ? T : std::max(1, 262144 / (36 * k));  // factored: one item
             for (int t0 = 0; t0 < T; t0 += tpi2)
                 marg_items.push_back(LargeItem{(int32_t)i, t0, std::min(T, t0 + tpi2), 0});
             if (cls == 5) {
@@ -457,12 +458,36 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
         side_total += side_floats(c->h_k[i]);
     }
     c->arena_floats = side_total;
+    if (opt.storage == 1) {  // factored (f4): header 44 + 28 per observation floats per landmark
+        int64_t off = 0;
+        c->matvec_bytes = 0;
+        c->marg_bytes = 0;
+        c->logical_bytes = 0;
+        const int gb[5] = {2, 4, 8, 16, 1 << 30};
+        int cls = 0;
+        for (int64_t i = 0; i < nl; i++) {
+            const int k = c->h_k[i];
+            while (k > gb[cls]) {
+                c->fac_hi[cls] = i;
+                c->fac_lo[++cls] = i;
+            }
+            c->h_r2[i] = off;
+            off += 44 + 28 * (int64_t)k;
+            c->matvec_bytes += 176.0 + 112.0 * k;
+            c->marg_bytes += 176.0 + 112.0 * k + 20.0 * k;
+            c->logical_bytes += 176 + 112 * (int64_t)k;
+        }
+        for (int q = cls; q < 5; q++) c->fac_hi[q] = nl;
+        for (int q = cls + 1; q < 5; q++) c->fac_lo[q] = nl;
+        c->arena_floats = std::max<int64_t>(off, 4);
+    }
     // ---- device buffers
     DevProblem &d = c->d;
     d.n_p = n_cams;
     d.n_l = nl;
     d.huber = opt.huber_delta;
     d.sc = opt.solver;
+    d.fac = opt.storage;
     d.n_obs = nobs_loc;
     CKSC(dalloc_n(c, &d.cams, 9 * n_cams));
     CKSC(dalloc_n(c, &d.cams_trial, 9 * n_cams));
@@ -940,6 +965,7 @@ extern "C" rba_status rba_export_block(rba_ctx *c, int64_t landmark, double *buf
         return fail(RBA_ERR_INVALID_ARG, "landmark not owned by this rank");
     if (!c->marginalized) return fail(RBA_ERR_STATE, "rba_export_block before rba_marginalize_qr");
     if (c->d.sc) return fail(RBA_ERR_STATE, "rba_export_block: explicit-SC mode keeps no landmark blocks");
+    if (c->d.fac) return fail(RBA_ERR_STATE, "rba_export_block: factored storage keeps no dense blocks");
     const int64_t j = c->orig_to_int[landmark];
     const int k = c->h_k[j];
     const int64_t R = 2 * k + 3, C = 9 * k + 4;

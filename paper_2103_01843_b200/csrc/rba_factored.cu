@@ -1,0 +1,454 @@
+// rba_factored.cu -- factored sqrt-BA storage (beyond the paper).  The QR
+// marginalization is the paper's (Householder; 6 damping Givens), but instead of
+// the dense (2k+3) x (9k+4) block a landmark keeps what defines it:
+//   per observation o (28 floats, 112 B):  scaled J_p rows 2o, 2o+1 (2 x 9) | Householder vectors
+//       V rows 2o, 2o+1 (2 x 3) | (Q^T r^) rows 2o, 2o+1 (undamped) | pad
+//   per landmark (44 floats): undamped R (3x3) | compact-WY T (6) | 6 Givens (c, s) | damped R^1
+//       (3x3) | damped special residual entries (6)
+// and applies A_j = (Q^^T [J_p; 0])[3:] and its transpose in O(k) (Q is never formed):
+//   A v  = rows 3..2k+2 of G (Q^T u (+) 0_3),   u = J_p v,   Q^T = I - V T^T V^T
+//   A^T y = J_p^T Q (G^T [0_3; y])[0:2k],       Q = I - V T V^T
+// The reduced camera system is the same matrix as with dense blocks (exact algebra), read from
+// (176 + 112 k) bytes per landmark instead of 72 k^2 (config 4: 0.74 GB vs 14.9 GB per product).
+// Product path only (no oracle code).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "rba_internal.cuh"
+#include "rba_model.cuh"
+
+namespace rba {
+
+// the 6 damping rotations (pivot p in {0,1,2}, target t in {d0,d1,d2}) on a 6-vector
+// [top0 top1 top2 d0 d1 d2] (reading C5 / C6 order) and their inverse in reverse order
+__device__ __forceinline__ int fac_p(int m) { return m == 0 ? 0 : ((m == 1 || m == 3) ? 1 : 2); }
+__device__ __forceinline__ int fac_t(int m) { return m < 3 ? 3 : (m < 5 ? 4 : 5); }
+__device__ __forceinline__ void givens_fwd(const float *g, float *x) {
+#pragma unroll
+    for (int m = 0; m < 6; m++) {
+        const int p = fac_p(m), t = fac_t(m);
+        const float c = g[2 * m], s = g[2 * m + 1], a = x[p], b = x[t];
+        x[p] = c * a + s * b;
+        x[t] = -s * a + c * b;
+    }
+}
+__device__ __forceinline__ void givens_inv(const float *g, float *x) {
+#pragma unroll
+    for (int m = 5; m >= 0; m--) {
+        const int p = fac_p(m), t = fac_t(m);
+        const float c = g[2 * m], s = g[2 * m + 1], a = x[p], b = x[t];
+        x[p] = c * a - s * b;
+        x[t] = s * a + c * b;
+    }
+}
+
+// a group of G lanes (G | 32) per landmark; lane gl handles observations o = gl, gl + G, ...
+template <int G>
+__device__ __forceinline__ float gsum(float v) {
+#pragma unroll
+    for (int m = G / 2; m; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m, G);
+    return v;
+}
+
+struct FacHdr {
+    float R[9], T[6], g[12], Rd[9], rr6[6];
+};
+
+__device__ __forceinline__ void load_hdr(const float *h, FacHdr &H) {
+#pragma unroll
+    for (int i = 0; i < 9; i++) H.R[i] = h[i];
+#pragma unroll
+    for (int i = 0; i < 6; i++) H.T[i] = h[9 + i];
+#pragma unroll
+    for (int i = 0; i < 12; i++) H.g[i] = h[15 + i];
+#pragma unroll
+    for (int i = 0; i < 9; i++) H.Rd[i] = h[27 + i];
+#pragma unroll
+    for (int i = 0; i < 6; i++) H.rr6[i] = h[36 + i];
+}
+
+// per-observation record: jp[18] | V[6] (rows 2o, 2o+1) | qr[2] | pad[2]
+struct FacObs {
+    float jp[18], v[6], qr[2];
+};
+__device__ __forceinline__ void load_obs(const float *rec, FacObs &o) {
+    const float4 *r4 = reinterpret_cast<const float4 *>(rec);
+    float t[28];
+#pragma unroll
+    for (int i = 0; i < 7; i++) {
+        const float4 x = __ldg(r4 + i);
+        t[4 * i] = x.x, t[4 * i + 1] = x.y, t[4 * i + 2] = x.z, t[4 * i + 3] = x.w;
+    }
+#pragma unroll
+    for (int i = 0; i < 18; i++) o.jp[i] = t[i];
+#pragma unroll
+    for (int i = 0; i < 6; i++) o.v[i] = t[18 + i];
+    o.qr[0] = t[24], o.qr[1] = t[25];
+}
+
+// Forward half for landmark j (group of G lanes): s = V^T u with u = J_p v, t = T^T s; returns
+// through the group: the damped top rows top[3] and damping rows dd[3] (G (Q^T u)_special).
+template <int G>
+__device__ __forceinline__ void fac_forward(const float *fac, int k, const int32_t *oc, const float *vv, int gl,
+                                            const FacHdr &H, float *tvec, float *top, float *dd, float *w012) {
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+    for (int o = gl; o < k; o += G) {
+        FacObs ob;
+        load_obs(fac + 28 * o, ob);
+        const float *x = vv + 9 * (int64_t)oc[o];
+        float u0 = 0.f, u1 = 0.f;
+#pragma unroll
+        for (int q = 0; q < 9; q++) {
+            const float xq = x[q];
+            u0 += ob.jp[q] * xq;
+            u1 += ob.jp[9 + q] * xq;
+        }
+        s0 += ob.v[0] * u0 + ob.v[3] * u1;
+        s1 += ob.v[1] * u0 + ob.v[4] * u1;
+        s2 += ob.v[2] * u0 + ob.v[5] * u1;
+    }
+    s0 = gsum<G>(s0), s1 = gsum<G>(s1), s2 = gsum<G>(s2);
+    // t = T^T s  (T upper: T00 T01 T02 T11 T12 T22)
+    tvec[0] = H.T[0] * s0;
+    tvec[1] = H.T[1] * s0 + H.T[3] * s1;
+    tvec[2] = H.T[2] * s0 + H.T[4] * s1 + H.T[5] * s2;
+    // rows 0, 1 (obs 0) and 2 (obs 1) of w = u - V t: every lane recomputes them (L1 hits)
+    FacObs o0 = {}, o1 = {};
+    float u00 = 0.f, u01 = 0.f, u10 = 0.f;
+    if (k > 0) {
+        load_obs(fac, o0);
+        load_obs(fac + 28, o1);
+        const float *x0 = vv + 9 * (int64_t)oc[0], *x1 = vv + 9 * (int64_t)oc[1];
+#pragma unroll
+        for (int q = 0; q < 9; q++) {
+            u00 += o0.jp[q] * x0[q];
+            u01 += o0.jp[9 + q] * x0[q];
+            u10 += o1.jp[q] * x1[q];
+        }
+    }
+    w012[0] = u00 - (o0.v[0] * tvec[0] + o0.v[1] * tvec[1] + o0.v[2] * tvec[2]);
+    w012[1] = u01 - (o0.v[3] * tvec[0] + o0.v[4] * tvec[1] + o0.v[5] * tvec[2]);
+    w012[2] = u10 - (o1.v[0] * tvec[0] + o1.v[1] * tvec[1] + o1.v[2] * tvec[2]);
+    float x6[6] = {w012[0], w012[1], w012[2], 0.f, 0.f, 0.f};
+    givens_fwd(H.g, x6);
+    top[0] = x6[0], top[1] = x6[1], top[2] = x6[2];
+    dd[0] = x6[3], dd[1] = x6[4], dd[2] = x6[5];
+}
+
+// ---- K5F: out_cam += A_j^T (A_j v) for the landmarks [lo, hi) of one group-size class
+template <int G>
+__global__ void __launch_bounds__(256) k_fac_matvec(DevProblem d, int64_t lo, int64_t hi, const float *__restrict__ v,
+                                                    const PcgState *__restrict__ st) {
+    if (st && st->done) return;
+    const float *vv = v;  // camera vector: L1 / L2 resident (gathered per observation)
+    const int lane = threadIdx.x & 31, gl = lane % G;
+    const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / G;  // landmarks per grid sweep
+    float *out = wslice(d);
+    // warp-uniform trip count (the group shuffles need every lane of the warp): a group whose
+    // landmark is past the range runs with k = 0
+    const int64_t wfirst = lo + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * (32 / G);
+    for (int64_t jb = wfirst; jb < hi; jb += ngroups) {
+        const int64_t j = jb + lane / G;
+        const bool valid = j < hi;
+        const int k = valid ? d.lm_k[j] : 0;
+        const float *base = d.arena + (valid ? d.lm_r2[j] : 0);
+        const float *fac = base + 44;
+        const int32_t *oc = d.obs_cam + (valid ? d.lm_obs0[j] : 0);
+        FacHdr H;
+        load_hdr(base, H);
+        float t[3], top[3], dd[3], w012[3];
+        fac_forward<G>(fac, k, oc, vv, gl, H, t, top, dd, w012);
+        // y = rows 3..2k+2 of G(Q^T u): w rows >= 3 and dd.  Transpose: z = G^T [0_3; y] gives
+        // z rows 0..2 from dd (rows >= 3 are w); then s' = V^T z, t' = T s', z' = z - V t'.
+        float z6[6] = {0.f, 0.f, 0.f, dd[0], dd[1], dd[2]};
+        givens_inv(H.g, z6);
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+        for (int o = gl; o < k; o += G) {
+            FacObs ob;
+            load_obs(fac + 28 * o, ob);
+            const float *x = vv + 9 * (int64_t)oc[o];
+            float u0 = 0.f, u1 = 0.f;
+#pragma unroll
+            for (int q = 0; q < 9; q++) {
+                u0 += ob.jp[q] * x[q];
+                u1 += ob.jp[9 + q] * x[q];
+            }
+            float z0 = u0 - (ob.v[0] * t[0] + ob.v[1] * t[1] + ob.v[2] * t[2]);
+            float z1 = u1 - (ob.v[3] * t[0] + ob.v[4] * t[1] + ob.v[5] * t[2]);
+            if (o == 0) z0 = z6[0], z1 = z6[1];
+            else if (o == 1) z0 = z6[2];
+            s0 += ob.v[0] * z0 + ob.v[3] * z1;
+            s1 += ob.v[1] * z0 + ob.v[4] * z1;
+            s2 += ob.v[2] * z0 + ob.v[5] * z1;
+        }
+        s0 = gsum<G>(s0), s1 = gsum<G>(s1), s2 = gsum<G>(s2);
+        const float t0 = H.T[0] * s0 + H.T[1] * s1 + H.T[2] * s2;  // t' = T s'
+        const float t1 = H.T[3] * s1 + H.T[4] * s2;
+        const float t2 = H.T[5] * s2;
+        for (int o = gl; o < k; o += G) {
+            FacObs ob;
+            load_obs(fac + 28 * o, ob);
+            const int cam = oc[o];
+            const float *x = vv + 9 * (int64_t)cam;
+            float u0 = 0.f, u1 = 0.f;
+#pragma unroll
+            for (int q = 0; q < 9; q++) {
+                u0 += ob.jp[q] * x[q];
+                u1 += ob.jp[9 + q] * x[q];
+            }
+            float z0 = u0 - (ob.v[0] * t[0] + ob.v[1] * t[1] + ob.v[2] * t[2]);
+            float z1 = u1 - (ob.v[3] * t[0] + ob.v[4] * t[1] + ob.v[5] * t[2]);
+            if (o == 0) z0 = z6[0], z1 = z6[1];
+            else if (o == 1) z0 = z6[2];
+            z0 -= ob.v[0] * t0 + ob.v[1] * t1 + ob.v[2] * t2;
+            z1 -= ob.v[3] * t0 + ob.v[4] * t1 + ob.v[5] * t2;
+            float acc[9];
+#pragma unroll
+            for (int q = 0; q < 9; q++) acc[q] = ob.jp[q] * z0 + ob.jp[9 + q] * z1;
+            flush_cam12(out, cam, acc);
+        }
+    }
+}
+
+// ---- K4F: block-Jacobi blocks P_o = A[:, o]^T A[:, o] and b~_o = A[:, o]^T q from the rows of A
+// recomputed by the WY formula (A[a, o] = delta(a in {2o, 2o+1}) J_o - V[a] M_o, M_o = T^T V_o^T J_o,
+// damping rows mixed by G), O(k) per block, exact (no SC-style subtraction).
+template <int G>
+__global__ void __launch_bounds__(256) k_fac_precond(DevProblem d, int64_t lo, int64_t hi) {
+    const int lane = threadIdx.x & 31, gl = lane % G;
+    const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / G;  // landmarks per grid sweep
+    float *out = pslice(d);
+    // warp-uniform trip count (the group shuffles need every lane of the warp): a group whose
+    // landmark is past the range runs with k = 0
+    const int64_t wfirst = lo + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * (32 / G);
+    for (int64_t jb = wfirst; jb < hi; jb += ngroups) {
+        const int64_t j = jb + lane / G;
+        const bool valid = j < hi;
+        const int k = valid ? d.lm_k[j] : 0;
+        const float *base = d.arena + (valid ? d.lm_r2[j] : 0);
+        const float *fac = base + 44;
+        const int32_t *oc = d.obs_cam + (valid ? d.lm_obs0[j] : 0);
+        FacHdr H;
+        load_hdr(base, H);
+        // Gm: the 6x3 mixing of undamped rows 0..2 into {top, d0, d1, d2} (columns of G applied to e_i)
+        float Gm[18];
+#pragma unroll
+        for (int i = 0; i < 3; i++) {
+            float x6[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            x6[i] = 1.f;
+            givens_fwd(H.g, x6);
+#pragma unroll
+            for (int s = 0; s < 6; s++) Gm[3 * s + i] = x6[s];
+        }
+        for (int o = gl; o < k; o += G) {
+            FacObs ob;
+            load_obs(fac + 28 * o, ob);
+            float M[27];  // M = T^T (V_o^T J_o), 3 x 9
+#pragma unroll
+            for (int q = 0; q < 9; q++) {
+                const float W0 = ob.v[0] * ob.jp[q] + ob.v[3] * ob.jp[9 + q];
+                const float W1 = ob.v[1] * ob.jp[q] + ob.v[4] * ob.jp[9 + q];
+                const float W2 = ob.v[2] * ob.jp[q] + ob.v[5] * ob.jp[9 + q];
+                M[q] = H.T[0] * W0;
+                M[9 + q] = H.T[1] * W0 + H.T[3] * W1;
+                M[18 + q] = H.T[2] * W0 + H.T[4] * W1 + H.T[5] * W2;
+            }
+            float P[45], b[9];
+#pragma unroll
+            for (int i = 0; i < 45; i++) P[i] = 0.f;
+#pragma unroll
+            for (int i = 0; i < 9; i++) b[i] = 0.f;
+            float X3[27];  // undamped rows 0..2 of X = Q^T E_o (for the damping rows)
+            for (int a2 = 0; a2 < k; a2++) {  // rows 2 a2, 2 a2 + 1 (V rows of observation a2)
+                FacObs oa;
+                load_obs(fac + 28 * a2, oa);
+#pragma unroll
+                for (int rr = 0; rr < 2; rr++) {
+                    const int a = 2 * a2 + rr;
+                    float row[9];
+#pragma unroll
+                    for (int q = 0; q < 9; q++) {
+                        row[q] = -(oa.v[3 * rr] * M[q] + oa.v[3 * rr + 1] * M[9 + q] + oa.v[3 * rr + 2] * M[18 + q]);
+                        if (a2 == o) row[q] += ob.jp[9 * rr + q];
+                    }
+                    if (a < 3) {
+#pragma unroll
+                        for (int q = 0; q < 9; q++) X3[9 * a + q] = row[q];
+                    } else {
+                        const float qa = oa.qr[rr];
+                        int idx = 0;
+#pragma unroll
+                        for (int q1 = 0; q1 < 9; q1++) {
+                            b[q1] += row[q1] * qa;
+#pragma unroll
+                            for (int q2 = q1; q2 < 9; q2++) P[idx++] += row[q1] * row[q2];
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int s = 3; s < 6; s++) {  // damping rows d0..d2 and their residual entries
+                float row[9];
+#pragma unroll
+                for (int q = 0; q < 9; q++) row[q] = Gm[3 * s] * X3[q] + Gm[3 * s + 1] * X3[9 + q] + Gm[3 * s + 2] * X3[18 + q];
+                const float qa = H.rr6[s];
+                int idx = 0;
+#pragma unroll
+                for (int q1 = 0; q1 < 9; q1++) {
+                    b[q1] += row[q1] * qa;
+#pragma unroll
+                    for (int q2 = q1; q2 < 9; q2++) P[idx++] += row[q1] * row[q2];
+                }
+            }
+            float4 *a4 = reinterpret_cast<float4 *>(out + PACC_STRIDE * (int64_t)oc[o]);
+#pragma unroll
+            for (int i = 0; i < 11; i++) atomicAdd(a4 + i, make_float4(P[4 * i], P[4 * i + 1], P[4 * i + 2], P[4 * i + 3]));
+            atomicAdd(a4 + 11, make_float4(P[44], b[0], b[1], b[2]));
+            atomicAdd(a4 + 12, make_float4(b[3], b[4], b[5], b[6]));
+            atomicAdd(a4 + 13, make_float4(b[7], b[8], 0.f, 0.f));
+        }
+    }
+}
+
+// ---- K7F: dl = -R^1^-1 (Q^1^T r^ + (Q^^T [J_p dp; 0])[0:3]) and the C10 terms
+template <int G>
+__global__ void __launch_bounds__(256) k_fac_backsub(DevProblem d, int64_t lo, int64_t hi, float lam) {
+    __shared__ double red[32];
+    const int lane = threadIdx.x & 31, gl = lane % G;
+    const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / G;  // landmarks per grid sweep
+    double q1 = 0.0, dd2 = 0.0;
+    // dp (FP64, 9 n_p) rounded to FP32 per use
+    // warp-uniform trip count (the group shuffles need every lane of the warp): a group whose
+    // landmark is past the range runs with k = 0
+    const int64_t wfirst = lo + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * (32 / G);
+    for (int64_t jb = wfirst; jb < hi; jb += ngroups) {
+        const int64_t j = jb + lane / G;
+        const bool valid = j < hi;
+        const int k = valid ? d.lm_k[j] : 0;
+        const float *base = d.arena + (valid ? d.lm_r2[j] : 0);
+        const float *fac = base + 44;
+        const int32_t *oc = d.obs_cam + (valid ? d.lm_obs0[j] : 0);
+        FacHdr H;
+        load_hdr(base, H);
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, u00 = 0.f, u01 = 0.f, u10 = 0.f;
+        for (int o = gl; o < k; o += G) {
+            FacObs ob;
+            load_obs(fac + 28 * o, ob);
+            const double *x = d.x + 9 * (int64_t)oc[o];
+            float u0 = 0.f, u1 = 0.f;
+#pragma unroll
+            for (int q = 0; q < 9; q++) {
+                const float xq = (float)x[q];
+                u0 += ob.jp[q] * xq;
+                u1 += ob.jp[9 + q] * xq;
+            }
+            if (o == 0) u00 = u0, u01 = u1;
+            if (o == 1) u10 = u0;
+            s0 += ob.v[0] * u0 + ob.v[3] * u1;
+            s1 += ob.v[1] * u0 + ob.v[4] * u1;
+            s2 += ob.v[2] * u0 + ob.v[5] * u1;
+        }
+        s0 = gsum<G>(s0), s1 = gsum<G>(s1), s2 = gsum<G>(s2);
+        u00 = gsum<G>(u00), u01 = gsum<G>(u01), u10 = gsum<G>(u10);  // only one lane holds each
+        if (gl == 0 && valid) {
+            const float t0 = H.T[0] * s0, t1 = H.T[1] * s0 + H.T[3] * s1, t2 = H.T[2] * s0 + H.T[4] * s1 + H.T[5] * s2;
+            FacObs o0, o1;
+            load_obs(fac, o0);
+            load_obs(fac + 28, o1);
+            float x6[6] = {u00 - (o0.v[0] * t0 + o0.v[1] * t1 + o0.v[2] * t2),
+                           u01 - (o0.v[3] * t0 + o0.v[4] * t1 + o0.v[5] * t2),
+                           u10 - (o1.v[0] * t0 + o1.v[1] * t1 + o1.v[2] * t2), 0.f, 0.f, 0.f};
+            givens_fwd(H.g, x6);
+            const float b0 = H.rr6[0] + x6[0], b1 = H.rr6[1] + x6[1], b2 = H.rr6[2] + x6[2];
+            const float *R = H.Rd;  // damped R^1, upper triangular rows
+            const float x2 = b2 / R[8];
+            const float x1 = (b1 - R[5] * x2) / R[4];
+            const float x0 = (b0 - R[1] * x1 - R[2] * x2) / R[0];
+            const float dl[3] = {-x0, -x1, -x2};
+            q1 += (double)H.rr6[0] * H.rr6[0] + (double)H.rr6[1] * H.rr6[1] + (double)H.rr6[2] * H.rr6[2];
+#pragma unroll
+            for (int q = 0; q < 3; q++) {
+                d.dl[3 * j + q] = dl[q];
+                d.pts_trial[3 * j + q] = d.pts[3 * j + q] + (double)(d.lm_s[3 * j + q] * dl[q]);
+                const double Dd = (double)d.lm_D[3 * j + q] * dl[q];
+                dd2 += Dd * Dd;
+            }
+        }
+    }
+    q1 = block_sum_d(q1, red);
+    dd2 = block_sum_d(dd2, red);
+    if (threadIdx.x == 0) {
+        atomicAdd(d.scal + SC_Q1R2, q1);
+        atomicAdd(d.scal + SC_DAMPL, (double)lam * dd2);
+    }
+}
+
+// ---- K3F: re-damping is O(1) per landmark: new Givens from the undamped R and Q1^T r
+__global__ void k_fac_redamp(DevProblem d, float lam) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= d.n_l) return;
+    const int k = d.lm_k[j];
+    float *base = d.arena + d.lm_r2[j];
+    const float *fac = base + 44;
+    float R[9], rr3[3];
+#pragma unroll
+    for (int i = 0; i < 9; i++) R[i] = base[i];
+    rr3[0] = fac[24], rr3[1] = fac[25], rr3[2] = fac[28 + 24];
+    (void)k;
+    const float sq = sqrtf(lam);
+    const float sD[3] = {sq * d.lm_D[3 * j], sq * d.lm_D[3 * j + 1], sq * d.lm_D[3 * j + 2]};
+    float L6[18], Gm[18], rr6[6], g[12];
+    damp_rotations(R, rr3, sD, L6, Gm, rr6, g);
+#pragma unroll
+    for (int i = 0; i < 12; i++) base[15 + i] = g[i];
+#pragma unroll
+    for (int i = 0; i < 9; i++) base[27 + i] = L6[i];
+#pragma unroll
+    for (int i = 0; i < 6; i++) base[36 + i] = rr6[i];
+}
+
+// ============================================================================ launchers
+static inline unsigned nbk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+static const int FAC_G[5] = {2, 4, 8, 16, 32};
+
+template <int G>
+static void fac_cls(rba_ctx *c, int cls, int what, const float *v, const PcgState *st, float lam, cudaStream_t s) {
+    const int64_t lo = c->fac_lo[cls], hi = c->fac_hi[cls];
+    if (hi <= lo) return;
+    const unsigned g = (unsigned)std::min<int64_t>(nbk((hi - lo) * G, 256), (int64_t)c->num_sms * 8);
+    if (what == 0) {
+        k_fac_matvec<G><<<g, 256, 0, s>>>(c->d, lo, hi, v, st);
+    } else if (what == 1) {
+        k_fac_precond<G><<<g, 256, 0, s>>>(c->d, lo, hi);
+    } else {
+        k_fac_backsub<G><<<g, 256, 0, s>>>(c->d, lo, hi, lam);
+    }
+    c->launches++;
+}
+
+static void fac_all(rba_ctx *c, int what, const float *v, const PcgState *st, float lam) {
+    // on the context stream: few launches, the classes are independent but small
+    fac_cls<32>(c, 4, what, v, st, lam, c->stream);
+    fac_cls<16>(c, 3, what, v, st, lam, c->stream);
+    fac_cls<8>(c, 2, what, v, st, lam, c->stream);
+    fac_cls<4>(c, 1, what, v, st, lam, c->stream);
+    fac_cls<2>(c, 0, what, v, st, lam, c->stream);
+}
+
+void launch_fac_matvec(rba_ctx *c, const float *v, const PcgState *st) { fac_all(c, 0, v, st, 0.f); }
+void launch_fac_precond(rba_ctx *c) { fac_all(c, 1, nullptr, nullptr, 0.f); }
+cudaError_t launch_fac_backsub(rba_ctx *c, float lam) {
+    fac_all(c, 2, nullptr, nullptr, lam);
+    return cudaGetLastError();
+}
+cudaError_t launch_fac_redamp(rba_ctx *c, float lam) {
+    if (c->d.n_l) {
+        k_fac_redamp<<<nbk(c->d.n_l, 256), 256, 0, c->stream>>>(c->d, lam);
+        c->launches++;
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace rba

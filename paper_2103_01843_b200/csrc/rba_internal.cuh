@@ -150,6 +150,8 @@ struct DevProblem {
     void *bsr_val;                // nnzb x 81 (FP32 or FP64), row-major blocks
     void *sc_b;                   // b~ accumulator, 9 n_p
     void *sc_scratch;             // per observation: G_a (27) and L_a = G_a H_ll^-1 (27)
+    // factored storage (f4, rba_factored.cu): landmark j's factors at arena + lm_r2[j]
+    int fac;
 };
 
 struct Launch {
@@ -183,6 +185,7 @@ struct rba_ctx {
     int64_t pack_lo[4] = {0, 0, 0, 0}, pack_hi[4] = {0, 0, 0, 0};  // G = 2, 4, 8, 16 pack ranges
     int64_t marg_lo[6] = {0, 0, 0, 0, 0, 0}, marg_hi[6] = {0, 0, 0, 0, 0, 0};  // K2 large items per class
     int64_t n_huge_y = 0, n_huge_out = 0, huge_max_k = 0;  // k > KLARGE (two-pass matvec)
+    int64_t fac_lo[5] = {0, 0, 0, 0, 0}, fac_hi[5] = {0, 0, 0, 0, 0};  // factored: G = 2..32 landmark ranges
     int64_t cta_off[5] = {0, 0, 0, 0, 0}, cta_n[5] = {0, 0, 0, 0, 0};    // K4/K5 CTA ranges per class
     int64_t n_chunks = 0, chunk_ctas = 0;
     int64_t n_packs = 0, max_large_k = 0;
@@ -236,6 +239,11 @@ cudaError_t launch_add_damping(rba_ctx *c, const float *v, float *out, float lam
 cudaError_t launch_sc_build(rba_ctx *c, float lambda);
 cudaError_t launch_sc_precond(rba_ctx *c);
 void launch_sc_spmv(rba_ctx *c, const PcgState *st, const float *v32);
+// factored storage (rba_factored.cu)
+void launch_fac_matvec(rba_ctx *c, const float *v, const PcgState *st);
+void launch_fac_precond(rba_ctx *c);
+cudaError_t launch_fac_backsub(rba_ctx *c, float lambda);
+cudaError_t launch_fac_redamp(rba_ctx *c, float lambda);
 cudaError_t launch_sc_backsub(rba_ctx *c, float lambda);
 // profiling scope: CUDA events on the context stream around one launch (rba_api.cu)
 struct Prof {

@@ -77,63 +77,6 @@ __global__ void k_cam_scale(DevProblem d, float dmin, float dmax) {
     d.Dp2[i] = fminf(fmaxf(n2 * s * s, dmin), dmax);
 }
 
-// ============================================================================ damping rotations
-// 6 Givens rotations (pivot, target) = (0,d0),(1,d0),(2,d0),(1,d1),(2,d1),(2,d2) fold sqrt(lam) D_l
-// into R1 (Fig. 3b).  Reading C5: c = a/rho, s = b/rho, new_p = c p + s t,
-// new_t = -s p + c t; b == 0 -> identity.  In:  R (3x3 upper, row-major), rr[0..2] residual of
-// rows 0..2, sD[3] = sqrt(lam) D_l.  Out: L6 rows 0..2 = damped R1 (rows 3..5 end up exactly 0),
-// Gm (6x3) maps undamped rows 0..2 to the damped rows {0,1,2,d0,d1,d2} in the pose / residual
-// columns, rr6 the damped residual entries, g[12] the (c, s) pairs.
-__host__ __device__ constexpr int damp_p(int m) { return m == 0 ? 0 : ((m == 1 || m == 3) ? 1 : 2); }
-__host__ __device__ constexpr int damp_t(int m) { return m < 3 ? 3 : (m < 5 ? 4 : 5); }
-
-__device__ __forceinline__ void givens(float a, float b, float &c, float &s) {
-    if (b == 0.f) {
-        c = 1.f;
-        s = 0.f;
-    } else {
-        float r = hypotf(a, b);
-        c = a / r;
-        s = b / r;
-    }
-}
-
-__device__ __forceinline__ void damp_rotations(const float *R, const float *rr, const float *sD, float *L6, float *Gm,
-                                               float *rr6, float *g) {
-#pragma unroll
-    for (int i = 0; i < 18; i++) L6[i] = 0.f, Gm[i] = 0.f;
-#pragma unroll
-    for (int i = 0; i < 9; i++) L6[i] = R[i];
-#pragma unroll
-    for (int i = 0; i < 3; i++) {
-        L6[(3 + i) * 3 + i] = sD[i];
-        Gm[i * 3 + i] = 1.f;
-        rr6[i] = rr[i];
-        rr6[3 + i] = 0.f;
-    }
-#pragma unroll
-    for (int m = 0; m < 6; m++) {
-        const int p = damp_p(m), t = damp_t(m);
-        float c, s;
-        givens(L6[p * 3 + p], L6[t * 3 + p], c, s);
-        g[2 * m] = c;
-        g[2 * m + 1] = s;
-#pragma unroll
-        for (int q = 0; q < 3; q++) {
-            float a = L6[p * 3 + q], b = L6[t * 3 + q];
-            L6[p * 3 + q] = c * a + s * b;
-            L6[t * 3 + q] = -s * a + c * b;
-            a = Gm[p * 3 + q], b = Gm[t * 3 + q];
-            Gm[p * 3 + q] = c * a + s * b;
-            Gm[t * 3 + q] = -s * a + c * b;
-        }
-        float a = rr6[p], b = rr6[t];
-        rr6[p] = c * a + s * b;
-        rr6[t] = -s * a + c * b;
-        L6[t * 3 + p] = 0.f;
-    }
-}
-
 // ============================================================================ K2 emission
 // Compact-WY form of the marginalized block (Householder): Q^T = I - V T^T V^T, so every
 // output row L of the pose columns of camera block o is
@@ -188,6 +131,34 @@ __device__ __forceinline__ float4 veff(const float *Gm, const float *V3, int s) 
     ve.z = Gm[s * 3] * V3[2] + Gm[s * 3 + 1] * V3[5] + Gm[s * 3 + 2] * V3[8];
     ve.w = 0.f;
     return ve;
+}
+
+// factored storage (f4): one observation's record (28 floats: scaled J_p rows 2o,
+// 2o+1 | V rows 2o, 2o+1 | (Q^T r^) rows 2o, 2o+1 | pad) and the landmark header (44 floats: R,
+// T, Givens, damped R^1, damped special residual entries)
+__device__ __forceinline__ void fac_write_obs(float *rec, const BlockWY &B, const float *v0, const float *v1, float q0,
+                                              float q1) {
+    float4 *r4 = reinterpret_cast<float4 *>(rec);
+    r4[0] = make_float4(B.jp[0][0], B.jp[0][1], B.jp[0][2], B.jp[0][3]);
+    r4[1] = make_float4(B.jp[0][4], B.jp[0][5], B.jp[0][6], B.jp[0][7]);
+    r4[2] = make_float4(B.jp[0][8], B.jp[1][0], B.jp[1][1], B.jp[1][2]);
+    r4[3] = make_float4(B.jp[1][3], B.jp[1][4], B.jp[1][5], B.jp[1][6]);
+    r4[4] = make_float4(B.jp[1][7], B.jp[1][8], v0[0], v0[1]);
+    r4[5] = make_float4(v0[2], v1[0], v1[1], v1[2]);
+    r4[6] = make_float4(q0, q1, 0.f, 0.f);
+}
+__device__ __forceinline__ void fac_write_hdr(float *h, const float *R, float T00, float T01, float T02, float T11,
+                                              float T12, float T22, const float *g, const float *L6, const float *rr6) {
+#pragma unroll
+    for (int i = 0; i < 9; i++) h[i] = R[i];
+    h[9] = T00, h[10] = T01, h[11] = T02, h[12] = T11, h[13] = T12, h[14] = T22;
+#pragma unroll
+    for (int i = 0; i < 12; i++) h[15 + i] = g[i];
+#pragma unroll
+    for (int i = 0; i < 9; i++) h[27 + i] = L6[i];
+#pragma unroll
+    for (int i = 0; i < 6; i++) h[36 + i] = rr6[i];
+    h[42] = 0.f, h[43] = 0.f;
 }
 
 // ============================================================================ K2 small (k <= 32)
@@ -351,6 +322,19 @@ __global__ void __launch_bounds__(128) k_marg_small(DevProblem d, int64_t pk_lo,
     }
     __syncwarp();
     if (!act) return;
+    if (d.fac) {  // factored storage: the factors instead of the dense block
+        float *base = d.arena + d.lm_r2[j];
+        fac_write_obs(base + 44 + 28 * gl, B, V[0], V[1], rv[0], rv[1]);
+        if (gl == 0) {
+            fac_write_hdr(base, R, T00, T01, T02, T11, T12, T22, g, L6, rr6);
+#pragma unroll
+            for (int q = 0; q < 3; q++) {
+                d.lm_s[3 * j + q] = sl[q];
+                d.lm_D[3 * j + q] = Dl[q];
+            }
+        }
+        return;
+    }
     // ---- emission (write-only stream, Fig. 2c) in the pack layout
     float *blk_side = d.arena + d.lm_side[j];
     float2 *A = reinterpret_cast<float2 *>(d.arena + pack.base);
@@ -542,6 +526,25 @@ __global__ void __launch_bounds__(NT) k_marg_large(DevProblem d, const LargeItem
     if (tid < 6) VR[tid < 3 ? tid : 2 * k + tid - 3] = veff(Gm, V3, tid);
     if (tid < 18) GM[tid] = Gm[tid];
     __syncthreads();
+    if (d.fac) {  // factored storage: the factors instead of the dense block (one item per landmark)
+        float *base = d.arena + d.lm_r2[j];
+        for (int o = tid; o < k; o += NT) {
+            if (MULTI) block_jp(d, obs0, o, Xp, B);
+            float v0[3], v1[3];
+#pragma unroll
+            for (int q = 0; q < 3; q++) {
+                v0[q] = 2 * o < 3 ? V3[3 * (2 * o) + q] : reinterpret_cast<const float *>(VR + 2 * o)[q];
+                v1[q] = 2 * o + 1 < 3 ? V3[3 * (2 * o + 1) + q] : reinterpret_cast<const float *>(VR + 2 * o + 1)[q];
+            }
+            fac_write_obs(base + 44 + 28 * o, B, v0, v1, SR[2 * o], SR[2 * o + 1]);
+        }
+        if (tid == 0) fac_write_hdr(base, R, T00, T01, T02, T11, T12, T22, g, L6, rr6);
+        if (tid < 3) {
+            d.lm_s[3 * j + tid] = sl[tid];
+            d.lm_D[3 * j + tid] = Dl[tid];
+        }
+        return;
+    }
     for (int o = tid; o < k; o += NT) {
         if (MULTI) {  // raw V rows 2o, 2o+1 (VR rows 0..2 now hold V_eff of the damped rows)
             block_jp(d, obs0, o, Xp, B);
@@ -1425,25 +1428,27 @@ __global__ void __launch_bounds__(256) k_backsub(DevProblem d, float lam) {
         const float *side = d.arena + d.lm_side[j];
         const int W = 9 * k;
         const int32_t *oc = d.obs_cam + d.lm_obs0[j];
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+        // FP64 arithmetic on the stored FP32 R^1 | Q^1^T J_p rows (the 3x3 solve amplifies errors by
+        // cond(R^1), large for far / short-baseline landmarks)
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0;
         for (int c = lane; c < W; c += 32) {
             const int o = c / 9, q = c - 9 * o;
-            const float v = (float)d.x[9 * (int64_t)oc[o] + q];
-            s0 += side[c] * v;
-            s1 += side[W + c] * v;
-            s2 += side[2 * W + c] * v;
+            const double v = d.x[9 * (int64_t)oc[o] + q];
+            s0 += (double)side[c] * v;
+            s1 += (double)side[W + c] * v;
+            s2 += (double)side[2 * W + c] * v;
         }
-        s0 = warp_sum_f(s0);
-        s1 = warp_sum_f(s1);
-        s2 = warp_sum_f(s2);
+        s0 = warp_sum_d(s0);
+        s1 = warp_sum_d(s1);
+        s2 = warp_sum_d(s2);
         if (lane == 0) {
             const float4 *TL = reinterpret_cast<const float4 *>(side + side_tl(k));
             const float4 t0 = TL[0], t1 = TL[1], t2 = TL[2];
-            const float b0 = t0.w + s0, b1 = t1.w + s1, b2 = t2.w + s2;
-            const float x2 = b2 / t2.z;
-            const float x1 = (b1 - t1.z * x2) / t1.y;
-            const float x0 = (b0 - t0.y * x1 - t0.z * x2) / t0.x;
-            const float dl[3] = {-x0, -x1, -x2};
+            const double b0 = t0.w + s0, b1 = t1.w + s1, b2 = t2.w + s2;
+            const double x2 = b2 / t2.z;
+            const double x1 = (b1 - t1.z * x2) / t1.y;
+            const double x0 = (b0 - t0.y * x1 - (double)t0.z * x2) / t0.x;
+            const float dl[3] = {(float)-x0, (float)-x1, (float)-x2};
             q1 += (double)t0.w * t0.w + (double)t1.w * t1.w + (double)t2.w * t2.w;
 #pragma unroll
             for (int q = 0; q < 3; q++) {
@@ -1608,6 +1613,7 @@ cudaError_t launch_marginalize(rba_ctx *c, float lam) {
 
 cudaError_t launch_redamp(rba_ctx *c, float lam) {
     if (c->d.n_l == 0) return cudaSuccess;
+    if (c->d.fac) return launch_fac_redamp(c, lam);
     Prof P(c, KID_DAMP, 0.0);
     k_redamp<<<nblk(32 * c->d.n_l, 256), 256, 0, c->stream>>>(c->d, lam);
     P.end();
@@ -1662,7 +1668,8 @@ static void reduce_slices(rba_ctx *c, float *sl, int stride, int nv, double *out
 
 cudaError_t launch_precond_rhs(rba_ctx *c) {
     Prof P(c, KID_PRE, plan_matvec_bytes(c));
-    pipes_all<true>(c, nullptr, c->d.psl, nullptr);
+    if (c->d.fac) launch_fac_precond(c);
+    else pipes_all<true>(c, nullptr, c->d.psl, nullptr);
     reduce_slices(c, c->d.psl, PACC_STRIDE, 54, c->d.pd, nullptr);
     P.end();
     return cudaGetLastError();
@@ -1680,7 +1687,8 @@ static void matvec_body(rba_ctx *c, const float *v, const PcgState *st) {
         launch_sc_spmv(c, st, st ? nullptr : v);
         return;
     }
-    pipes_all<false>(c, v, c->d.wsl, st);
+    if (c->d.fac) launch_fac_matvec(c, v, st);
+    else pipes_all<false>(c, v, c->d.wsl, st);
     reduce_slices(c, c->d.wsl, 12, 9, c->d.wd, st);
 }
 
@@ -1757,6 +1765,9 @@ cudaError_t launch_backsub(rba_ctx *c, float lam) {
     Prof P(c, KID_BACKSUB, 0.0);
     if (c->d.sc) {
         cudaError_t e = launch_sc_backsub(c, lam);
+        if (e) return e;
+    } else if (c->d.fac) {
+        cudaError_t e = launch_fac_backsub(c, lam);
         if (e) return e;
     } else if (c->d.n_l) {
         const unsigned g = (unsigned)std::min<int64_t>(nblk(32 * c->d.n_l, 256), (int64_t)c->num_sms * 8);

@@ -186,4 +186,61 @@ __device__ __forceinline__ void flush_cam12(float *out12, int cam, const float *
     atomicAdd(o4 + 2, make_float4(acc[8], 0.f, 0.f, 0.f));
 }
 
+// ============================================================================ damping rotations
+// 6 Givens rotations (pivot, target) = (0,d0),(1,d0),(2,d0),(1,d1),(2,d1),(2,d2) fold sqrt(lam) D_l
+// into R1 (Fig. 3b).  Reading C5: c = a/rho, s = b/rho, new_p = c p + s t,
+// new_t = -s p + c t; b == 0 -> identity.  In:  R (3x3 upper, row-major), rr[0..2] residual of
+// rows 0..2, sD[3] = sqrt(lam) D_l.  Out: L6 rows 0..2 = damped R1 (rows 3..5 end up exactly 0),
+// Gm (6x3) maps undamped rows 0..2 to the damped rows {0,1,2,d0,d1,d2} in the pose / residual
+// columns, rr6 the damped residual entries, g[12] the (c, s) pairs.
+__host__ __device__ constexpr int damp_p(int m) { return m == 0 ? 0 : ((m == 1 || m == 3) ? 1 : 2); }
+__host__ __device__ constexpr int damp_t(int m) { return m < 3 ? 3 : (m < 5 ? 4 : 5); }
+
+__device__ __forceinline__ void givens(float a, float b, float &c, float &s) {
+    if (b == 0.f) {
+        c = 1.f;
+        s = 0.f;
+    } else {
+        float r = hypotf(a, b);
+        c = a / r;
+        s = b / r;
+    }
+}
+
+__device__ __forceinline__ void damp_rotations(const float *R, const float *rr, const float *sD, float *L6, float *Gm,
+                                               float *rr6, float *g) {
+#pragma unroll
+    for (int i = 0; i < 18; i++) L6[i] = 0.f, Gm[i] = 0.f;
+#pragma unroll
+    for (int i = 0; i < 9; i++) L6[i] = R[i];
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+        L6[(3 + i) * 3 + i] = sD[i];
+        Gm[i * 3 + i] = 1.f;
+        rr6[i] = rr[i];
+        rr6[3 + i] = 0.f;
+    }
+#pragma unroll
+    for (int m = 0; m < 6; m++) {
+        const int p = damp_p(m), t = damp_t(m);
+        float c, s;
+        givens(L6[p * 3 + p], L6[t * 3 + p], c, s);
+        g[2 * m] = c;
+        g[2 * m + 1] = s;
+#pragma unroll
+        for (int q = 0; q < 3; q++) {
+            float a = L6[p * 3 + q], b = L6[t * 3 + q];
+            L6[p * 3 + q] = c * a + s * b;
+            L6[t * 3 + q] = -s * a + c * b;
+            a = Gm[p * 3 + q], b = Gm[t * 3 + q];
+            Gm[p * 3 + q] = c * a + s * b;
+            Gm[t * 3 + q] = -s * a + c * b;
+        }
+        float a = rr6[p], b = rr6[t];
+        rr6[p] = c * a + s * b;
+        rr6[t] = -s * a + c * b;
+        L6[t * 3 + p] = 0.f;
+    }
+}
+
 }  // namespace rba

@@ -86,6 +86,7 @@ def test_full_reduced_system(full):
 def test_full_pcg_and_backsub(full):
     s, o = full.s, full.o
     st = getattr(full, "pcg_gpu", None) or s.pcg()
+    assert o.precond_rhs() == 0
     it, reason, _ = o.pcg(1e-2, 500)
     assert st["reason"] != 2 and reason != 2  # never indefinite
     if st["iters"] != it:  # tolerance edge: rerun the GPU with the oracle's count
