@@ -55,25 +55,31 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-MATVEC_KERNELS = re.compile(r"k_large_pipe<\d+, \d+, (0|false)>|k_small_pipe<(0|false)>|k_huge_y|k_huge_out<(0|false)>")
+MATVEC_KERNELS = re.compile(r"k_large_pipe<\d+, \d+, (0|false)>|k_small_pipe<(0|false)>|k_huge_y|k_huge_out<(0|false)>|"
+                            r"k_fac_matvec|k_sc_spmv|k_reduce_slices")
 MARG_KERNELS = re.compile(r"k_marg_(small|large)<")
 
 
-def ncu_traffic(cfg):
+def ncu_traffic(cfg, variant=""):
     """DRAM bytes (read + write) of ONE launch of the matvec and of the marginalization, summed over
     their per-class kernels, from the newest committed `ncu --set full` summary of this config
     (profiles/r*_cfg<cfg>_ncu_full.json, written by tools/ncu_summary.py).  None if absent."""
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_cfg{cfg}_ncu_full.json")),
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_cfg{cfg}{variant}_ncu_full.json")),
                    key=lambda f: int(re.search(r"/r(\d+)_", f).group(1)))
     if not files:
         return None, None, None
     rows = json.load(open(files[-1]))
 
     def first_of_each(rx):
-        seen, tot = set(), 0.0
+        # one launch of each matching kernel, counted from the first non-reduction match on (the
+        # slice reduction of the preconditioner pass precedes the first product)
+        seen, tot, on = set(), 0.0, False
         for r in rows:
             name = r["kernel"].split("(")[0].replace("void ", "")
-            if rx.search(name) and name not in seen:
+            if not rx.search(name):
+                continue
+            on = on or "reduce" not in name
+            if on and name not in seen:
                 seen.add(name)
                 tot += r["dram_read_bytes"] + r["dram_write_bytes"]
         return tot if seen else None
@@ -197,6 +203,7 @@ def main():
     ap.add_argument("--cpu-every", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-variants", action="store_true", help="skip the factored / explicit-SC context lines")
     ap.add_argument("--storage", default="dense", choices=["dense", "factored"],
                     help="landmark-block storage: the paper's dense blocks (default) or the factored "
                          "form (SURVEY §8f f4, beyond the paper)")
@@ -317,17 +324,25 @@ def main():
                 "traffic": None, "peak_source": peak_src, "launches": n, "avg_ms": ms / n,
                 "bytes_per_launch": by / n}
 
-    tr_mv, tr_mg, tr_src = ncu_traffic(args.config)
+    variant = "" if (args.storage == "dense" and args.solver == "sqrtba") else \
+        ("_factored" if args.solver == "sqrtba" else f"_{args.solver}")
+    tr_mv, tr_mg, tr_src = ncu_traffic(args.config, variant)
     roof_mv = roof(*prof["matvec"])
     if roof_mv:
         roof_mv["traffic"] = tr_mv
         roof_mv["traffic_source"] = tr_src
-        roof_mv["kernel"] = "matvec (K5: k_matvec_small<G> + k_matvec_large), algorithmic 72k^2 B/landmark"
+        roof_mv["kernel"] = {
+            "": "matvec (K5: k_small_pipe + k_large_pipe<NS> + k_huge_*, then k_reduce_slices), algorithmic 72k^2 B/landmark",
+            "_factored": "factored matvec (k_fac_matvec<G> + k_reduce_slices), algorithmic 176+112k B/landmark",
+        }.get(variant, "explicit-SC SpMV (k_sc_spmv), algorithmic 81 x sizeof(T) B per 9x9 block")
     roof_mg = roof(*mprof)
     if roof_mg:
         roof_mg["traffic"] = tr_mg
         roof_mg["traffic_source"] = tr_src
-        roof_mg["kernel"] = "marginalize (K2: k_marg_small<G> + k_marg_large), algorithmic (2k+3)(9k+4)*4+48+20k B/landmark"
+        roof_mg["kernel"] = {
+            "": "marginalize (K2: k_marg_small<G> + k_marg_large<NT>), algorithmic (2k+3)(9k+4)*4+48+20k B/landmark",
+            "_factored": "factored marginalize (K2 writing factors), algorithmic 176+132k B/landmark",
+        }.get(variant, "explicit-SC build (k_sc_build), algorithmic 81 x sizeof(T) B per block + 48 B/obs")
     total_prof = sum(shares.values())
     line = {
         "metric": METRIC, "value": args.steps / (t_ms * 1e-3), "unit": "LM iterations/s", "n_gpus": world,
@@ -354,13 +369,43 @@ def main():
         "clocks": clk,
         "e2e": e2e,
     }
+    # the same workload through the other landmark eliminations / storages of this library (NEXT
+    # rows f3, f4), timed the same way (W warm-up, reset, K steps, CUDA events): context for the
+    # headline, which stays the paper's dense sqrt-BA-32
+    if not args.no_variants and args.solver == "sqrtba" and args.storage == "dense":
+        s.close()
+        variants = {}
+        for vname, kw in (("sqrtba32_factored", dict(storage=1)), ("explicit32", dict(solver=1)),
+                          ("explicit64", dict(solver=2))):
+            if vname.startswith("explicit") and args.config >= 5:
+                continue  # covisibility H~ too large / slow to form for the final13682 shape
+            sv = rba.Solver(prob, device=local, world=world, rank=rank, nccl_id=nccl_id, **kw)
+            for _ in range(args.warmup):
+                sv.lm_step()
+            sv.set_state(prob["cameras_init"], prob["points_init"])
+            sv.reset_lm()
+            barrier()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(sv.stream)
+            vr = [sv.lm_step() for _ in range(args.steps)]
+            a1.record(sv.stream)
+            barrier()
+            vt = max_over_ranks(a0.elapsed_time(a1))
+            variants[vname] = {"value": args.steps / (vt * 1e-3), "unit": "LM iterations/s",
+                               "ms_per_step": vt / args.steps, "costs": [r["cost_after"] for r in vr],
+                               "pcg_iters": [r["pcg_iters"] for r in vr],
+                               "indefinite": sum(r["pcg_reason"] == 2 for r in vr),
+                               "storage_bytes": sv.arena_bytes()[0]}
+            sv.close()
+        line["variants"] = variants
     if rank == 0 and world == 1 and not args.no_cpu:
         every = args.cpu_every or {1: 1, 2: 4, 3: 16, 4: 64, 5: 512}[args.config]
         val, cb = run_oracle(prob, args.config, 2, 0, every, budget_s=30)
         line["cpu_baseline"] = dict(cb, value=val, unit="LM iterations/s")
     if rank == 0:
         print(json.dumps(line), flush=True)
-    s.close()
+    if s.h:
+        s.close()
     if world > 1:
         dist.destroy_process_group()
 

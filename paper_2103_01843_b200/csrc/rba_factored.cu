@@ -158,6 +158,54 @@ __global__ void __launch_bounds__(256) k_fac_matvec(DevProblem d, int64_t lo, in
         const int32_t *oc = d.obs_cam + (valid ? d.lm_obs0[j] : 0);
         FacHdr H;
         load_hdr(base, H);
+        if (G < 32 || __all_sync(0xffffffffu, k <= G)) {
+            // fast path: one observation per lane, its record, u and w kept in registers; two group
+            // reductions (V^T u, V^T z) and one shuffle round for the special rows 0..2
+            const bool act = gl < k;
+            FacObs ob = {};
+            float u0 = 0.f, u1 = 0.f;
+            int cam = 0;
+            if (act) {
+                load_obs(fac + 28 * gl, ob);
+                cam = oc[gl];
+                const float *x = vv + 9 * (int64_t)cam;
+#pragma unroll
+                for (int q = 0; q < 9; q++) {
+                    const float xq = x[q];
+                    u0 += ob.jp[q] * xq;
+                    u1 += ob.jp[9 + q] * xq;
+                }
+            }
+            const float s0 = gsum<G>(ob.v[0] * u0 + ob.v[3] * u1);
+            const float s1 = gsum<G>(ob.v[1] * u0 + ob.v[4] * u1);
+            const float s2 = gsum<G>(ob.v[2] * u0 + ob.v[5] * u1);
+            const float ta = H.T[0] * s0, tb = H.T[1] * s0 + H.T[3] * s1, tc = H.T[2] * s0 + H.T[4] * s1 + H.T[5] * s2;
+            float z0 = u0 - (ob.v[0] * ta + ob.v[1] * tb + ob.v[2] * tc);
+            float z1 = u1 - (ob.v[3] * ta + ob.v[4] * tb + ob.v[5] * tc);
+            const int gbase = lane - gl;
+            float x6[6] = {__shfl_sync(0xffffffffu, z0, gbase), __shfl_sync(0xffffffffu, z1, gbase),
+                           __shfl_sync(0xffffffffu, z0, gbase + 1), 0.f, 0.f, 0.f};
+            givens_fwd(H.g, x6);  // -> [top; dd]; transpose: G^T [0_3; dd]
+            x6[0] = x6[1] = x6[2] = 0.f;
+            givens_inv(H.g, x6);
+            if (gl == 0) z0 = x6[0], z1 = x6[1];
+            else if (gl == 1) z0 = x6[2];
+            const float r0 = gsum<G>(ob.v[0] * z0 + ob.v[3] * z1);
+            const float r1 = gsum<G>(ob.v[1] * z0 + ob.v[4] * z1);
+            const float r2 = gsum<G>(ob.v[2] * z0 + ob.v[5] * z1);
+            const float t0 = H.T[0] * r0 + H.T[1] * r1 + H.T[2] * r2;
+            const float t1 = H.T[3] * r1 + H.T[4] * r2;
+            const float t2 = H.T[5] * r2;
+            if (act) {
+                z0 -= ob.v[0] * t0 + ob.v[1] * t1 + ob.v[2] * t2;
+                z1 -= ob.v[3] * t0 + ob.v[4] * t1 + ob.v[5] * t2;
+                float acc[9];
+#pragma unroll
+                for (int q = 0; q < 9; q++) acc[q] = ob.jp[q] * z0 + ob.jp[9 + q] * z1;
+                flush_cam12(out, cam, acc);
+            }
+            continue;
+        }
         float t[3], top[3], dd[3], w012[3];
         fac_forward<G>(fac, k, oc, vv, gl, H, t, top, dd, w012);
         // y = rows 3..2k+2 of G(Q^T u): w rows >= 3 and dd.  Transpose: z = G^T [0_3; y] gives
@@ -241,6 +289,130 @@ __global__ void __launch_bounds__(256) k_fac_precond(DevProblem d, int64_t lo, i
             givens_fwd(H.g, x6);
 #pragma unroll
             for (int s = 0; s < 6; s++) Gm[3 * s + i] = x6[s];
+        }
+        if (G < 32 || __all_sync(0xffffffffu, k <= G)) {
+            // fast path, one observation per lane, O(k): the rows of A outside the lane's own two
+            // are -V[a] M_o, so their sums are M_o^T C_o M_o and -M_o^T e_o with
+            // C_o = sum_{a >= 3, a not own} V[a]^T V[a], e_o = sum V[a]^T q_a, taken as exclusive
+            // prefix + exclusive suffix scans over the group (sums of non-negative parts, no
+            // subtraction); own rows, the rows 0..2 feeding the damping rows, exactly
+            const bool act = gl < k;
+            FacObs ob = {};
+            if (act) load_obs(fac + 28 * gl, ob);
+            float c9[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // C (6 upper) | e (3)
+#pragma unroll
+            for (int rr = 0; rr < 2; rr++) {
+                if (!act || 2 * gl + rr < 3) continue;
+                const float *v = ob.v + 3 * rr;
+                c9[0] += v[0] * v[0], c9[1] += v[0] * v[1], c9[2] += v[0] * v[2];
+                c9[3] += v[1] * v[1], c9[4] += v[1] * v[2], c9[5] += v[2] * v[2];
+                c9[6] += v[0] * ob.qr[rr], c9[7] += v[1] * ob.qr[rr], c9[8] += v[2] * ob.qr[rr];
+            }
+            float pre[9], suf[9];
+            const int gbase = lane - gl;
+#pragma unroll
+            for (int i = 0; i < 9; i++) {
+                float x = __shfl_up_sync(0xffffffffu, c9[i], 1, G);
+                pre[i] = gl >= 1 ? x : 0.f;
+                float y = __shfl_down_sync(0xffffffffu, c9[i], 1, G);
+                suf[i] = gl + 1 < G ? y : 0.f;
+            }
+#pragma unroll
+            for (int dlt = 1; dlt < G; dlt <<= 1) {
+#pragma unroll
+                for (int i = 0; i < 9; i++) {
+                    const float x = __shfl_up_sync(0xffffffffu, pre[i], dlt, G);
+                    const float y = __shfl_down_sync(0xffffffffu, suf[i], dlt, G);
+                    if (gl >= dlt) pre[i] += x;
+                    if (gl + dlt < G) suf[i] += y;
+                }
+            }
+            // V rows 0, 1 (lane 0) and 2 (lane 1) for the rows feeding the damping rows
+            float V012[9];
+#pragma unroll
+            for (int i = 0; i < 6; i++) V012[i] = __shfl_sync(0xffffffffu, ob.v[i], gbase);
+#pragma unroll
+            for (int i = 0; i < 3; i++) V012[6 + i] = __shfl_sync(0xffffffffu, ob.v[i], gbase + 1);
+            if (!act) continue;
+            float C[9], e[3];
+            C[0] = pre[0] + suf[0], C[1] = pre[1] + suf[1], C[2] = pre[2] + suf[2];
+            C[4] = pre[3] + suf[3], C[5] = pre[4] + suf[4], C[8] = pre[5] + suf[5];
+            C[3] = C[1], C[6] = C[2], C[7] = C[5];
+            e[0] = pre[6] + suf[6], e[1] = pre[7] + suf[7], e[2] = pre[8] + suf[8];
+            float M[27];
+#pragma unroll
+            for (int q = 0; q < 9; q++) {
+                const float W0 = ob.v[0] * ob.jp[q] + ob.v[3] * ob.jp[9 + q];
+                const float W1 = ob.v[1] * ob.jp[q] + ob.v[4] * ob.jp[9 + q];
+                const float W2 = ob.v[2] * ob.jp[q] + ob.v[5] * ob.jp[9 + q];
+                M[q] = H.T[0] * W0;
+                M[9 + q] = H.T[1] * W0 + H.T[3] * W1;
+                M[18 + q] = H.T[2] * W0 + H.T[4] * W1 + H.T[5] * W2;
+            }
+            float P[45], b[9];
+            {
+                float N[27];  // C M
+#pragma unroll
+                for (int m = 0; m < 3; m++)
+#pragma unroll
+                    for (int q = 0; q < 9; q++) N[9 * m + q] = C[3 * m] * M[q] + C[3 * m + 1] * M[9 + q] + C[3 * m + 2] * M[18 + q];
+                int idx = 0;
+#pragma unroll
+                for (int q1 = 0; q1 < 9; q1++) {
+                    b[q1] = -(M[q1] * e[0] + M[9 + q1] * e[1] + M[18 + q1] * e[2]);
+#pragma unroll
+                    for (int q2 = q1; q2 < 9; q2++)
+                        P[idx++] = M[q1] * N[q2] + M[9 + q1] * N[9 + q2] + M[18 + q1] * N[18 + q2];
+                }
+            }
+            float X3[27];  // rows 0..2 of X = Q^T E_o
+#pragma unroll
+            for (int a = 0; a < 3; a++)
+#pragma unroll
+                for (int q = 0; q < 9; q++)
+                    X3[9 * a + q] = -(V012[3 * a] * M[q] + V012[3 * a + 1] * M[9 + q] + V012[3 * a + 2] * M[18 + q]);
+#pragma unroll
+            for (int rr = 0; rr < 2; rr++) {
+                const int a = 2 * gl + rr;
+                float row[9];
+#pragma unroll
+                for (int q = 0; q < 9; q++)
+                    row[q] = ob.jp[9 * rr + q] - (ob.v[3 * rr] * M[q] + ob.v[3 * rr + 1] * M[9 + q] + ob.v[3 * rr + 2] * M[18 + q]);
+                if (a < 3) {
+#pragma unroll
+                    for (int q = 0; q < 9; q++) X3[9 * a + q] = row[q];
+                } else {
+                    int idx = 0;
+#pragma unroll
+                    for (int q1 = 0; q1 < 9; q1++) {
+                        b[q1] += row[q1] * ob.qr[rr];
+#pragma unroll
+                        for (int q2 = q1; q2 < 9; q2++) P[idx++] += row[q1] * row[q2];
+                    }
+                }
+            }
+#pragma unroll
+            for (int s2 = 3; s2 < 6; s2++) {
+                float row[9];
+#pragma unroll
+                for (int q = 0; q < 9; q++)
+                    row[q] = Gm[3 * s2] * X3[q] + Gm[3 * s2 + 1] * X3[9 + q] + Gm[3 * s2 + 2] * X3[18 + q];
+                const float qa = H.rr6[s2];
+                int idx = 0;
+#pragma unroll
+                for (int q1 = 0; q1 < 9; q1++) {
+                    b[q1] += row[q1] * qa;
+#pragma unroll
+                    for (int q2 = q1; q2 < 9; q2++) P[idx++] += row[q1] * row[q2];
+                }
+            }
+            float4 *a4 = reinterpret_cast<float4 *>(out + PACC_STRIDE * (int64_t)oc[gl]);
+#pragma unroll
+            for (int i = 0; i < 11; i++) atomicAdd(a4 + i, make_float4(P[4 * i], P[4 * i + 1], P[4 * i + 2], P[4 * i + 3]));
+            atomicAdd(a4 + 11, make_float4(P[44], b[0], b[1], b[2]));
+            atomicAdd(a4 + 12, make_float4(b[3], b[4], b[5], b[6]));
+            atomicAdd(a4 + 13, make_float4(b[7], b[8], 0.f, 0.f));
+            continue;
         }
         for (int o = gl; o < k; o += G) {
             FacObs ob;
@@ -429,12 +601,18 @@ static void fac_cls(rba_ctx *c, int cls, int what, const float *v, const PcgStat
 }
 
 static void fac_all(rba_ctx *c, int what, const float *v, const PcgState *st, float lam) {
-    // on the context stream: few launches, the classes are independent but small
+    // the classes are independent: fork them over the auxiliary streams and join back
+    cudaEventRecord(c->ev_fork, c->stream);
+    for (int i = 0; i < rba_ctx::NAUX; i++) cudaStreamWaitEvent(c->aux[i], c->ev_fork, 0);
     fac_cls<32>(c, 4, what, v, st, lam, c->stream);
-    fac_cls<16>(c, 3, what, v, st, lam, c->stream);
-    fac_cls<8>(c, 2, what, v, st, lam, c->stream);
-    fac_cls<4>(c, 1, what, v, st, lam, c->stream);
+    fac_cls<16>(c, 3, what, v, st, lam, c->aux[0]);
+    fac_cls<8>(c, 2, what, v, st, lam, c->aux[1]);
+    fac_cls<4>(c, 1, what, v, st, lam, c->aux[2]);
     fac_cls<2>(c, 0, what, v, st, lam, c->stream);
+    for (int i = 0; i < rba_ctx::NAUX; i++) {
+        cudaEventRecord(c->ev_join[i], c->aux[i]);
+        cudaStreamWaitEvent(c->stream, c->ev_join[i], 0);
+    }
 }
 
 void launch_fac_matvec(rba_ctx *c, const float *v, const PcgState *st) { fac_all(c, 0, v, st, 0.f); }
