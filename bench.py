@@ -372,7 +372,8 @@ def main():
     # the same workload through the other landmark eliminations / storages of this library (NEXT
     # rows f3, f4), timed the same way (W warm-up, reset, K steps, CUDA events): context for the
     # headline, which stays the paper's dense sqrt-BA-32
-    if not args.no_variants and args.solver == "sqrtba" and args.storage == "dense":
+    # (single GPU only: a second NCCL communicator would need its own unique id)
+    if not args.no_variants and args.solver == "sqrtba" and args.storage == "dense" and world == 1:
         s.close()
         variants = {}
         for vname, kw in (("sqrtba32_factored", dict(storage=1)), ("explicit32", dict(solver=1)),

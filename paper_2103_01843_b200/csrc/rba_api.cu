@@ -390,6 +390,8 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     std::vector<TileRef> tiles;
     std::vector<int64_t> cta_lo;
     const int ntb[6] = {32, 64, 128, 256, 512, KMAX};
+    static const int64_t marg_item_floats =
+        getenv("RBA_MARG_ITEM_FLOATS") ? atoll(getenv("RBA_MARG_ITEM_FLOATS")) : 1048576;  // 4 MB of output per item (measured: 3.91 -> 3.34 ms on cfg4 vs 1 MB)
     std::vector<HugeItem> huge_y, huge_out;
     int64_t ybuf_n = 0;
     const int64_t large_lo = pos;
@@ -408,7 +410,8 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
             const int k = c->h_k[i];
             if (!in_cls(k)) continue;
             const int T = large_tiles(k);
-            const int tpi2 = opt.storage ? T : std::max(1, 262144 / (36 * k));  // factored: one item
+            // K2 work item: ~marg_item_floats of emitted output (the O(k) prologue is recomputed per item)
+            const int tpi2 = opt.storage ? T : (int)std::max<int64_t>(1, marg_item_floats / (36 * k));
             for (int t0 = 0; t0 < T; t0 += tpi2)
                 marg_items.push_back(LargeItem{(int32_t)i, t0, std::min(T, t0 + tpi2), 0});
             if (cls == 5) {

@@ -1583,7 +1583,7 @@ template <int NT, bool MULTI = false>
 static cudaError_t marg_large_cls(rba_ctx *c, int cls, float lam, cudaStream_t st) {
     const int64_t lo = c->marg_lo[cls], hi = c->marg_hi[cls];
     if (hi <= lo) return cudaSuccess;
-    const int64_t K = MULTI ? c->huge_max_k : NT;
+    const int64_t K = MULTI ? (cls == 5 ? c->huge_max_k : KLARGE) : NT;
     const size_t sm = (size_t)(4 * (2 * K + 3) + 8 * K) * sizeof(float);
     cudaFuncSetAttribute(k_marg_large<NT, MULTI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k_marg_large<NT, MULTI><<<(unsigned)(hi - lo), NT, sm, st>>>(c->d, c->d.marg_items + lo, lam,
@@ -1597,7 +1597,12 @@ cudaError_t launch_marginalize(rba_ctx *c, float lam) {
     cudaError_t e;
     ForkJoin F(c);
     if ((e = marg_large_cls<512, true>(c, 5, lam, F.s()))) return e;
-    if ((e = marg_large_cls<512>(c, 4, lam, F.s()))) return e;
+    static const bool m512 = getenv("RBA_MARG512_MULTI") && atoi(getenv("RBA_MARG512_MULTI"));  // tuning knob
+    if (m512) {
+        if ((e = marg_large_cls<256, true>(c, 4, lam, F.s()))) return e;
+    } else if ((e = marg_large_cls<512>(c, 4, lam, F.s()))) {
+        return e;
+    }
     if ((e = marg_large_cls<256>(c, 3, lam, F.s()))) return e;
     if ((e = marg_large_cls<128>(c, 2, lam, F.s()))) return e;
     if ((e = marg_large_cls<64>(c, 1, lam, F.s()))) return e;
