@@ -67,7 +67,7 @@ typedef struct {
      * marginalization by QR), or the paper's explicit Schur-complement baselines
      * "explicit-32" / "explicit-64": H~ formed explicitly as 9 x 9 blocks on
      * the covisibility graph in FP32 / FP64, solved by the same PCG / LM.  In the SC modes
-     * rba_marginalize_qr forms the Schur complement, rba_export_block is RBA_ERR_STATE and
+     * rba_marginalize_qr forms the Schur complement, rba_export_block is RBA_ERR_STATE, world must be 1 and
      * rba_arena_bytes reports the block-sparse H~. */
     int solver;
     /* landmark-block storage for RBA_SOLVER_SQRTBA: RBA_STORAGE_DENSE (default;

@@ -193,6 +193,8 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     if (!cameras || !points || (n_obs > 0 && (!obs_cam || !obs_pt || !obs_uv)) || n_cams < 1 || n_points < 0 ||
         n_obs < 0)
         return fail(RBA_ERR_INVALID_ARG, "rba_create: null pointer or negative size");
+    if (opt.world > 1 && opt.solver != 0)
+        return fail(RBA_ERR_INVALID_ARG, "rba_create: the explicit-SC baselines are single-GPU (world must be 1)");
     if (opt.world < 1 || opt.rank < 0 || opt.rank >= opt.world || !(opt.lambda0 > 0) || !(opt.pcg_rel_tol >= 0) ||
         opt.pcg_max_iters < 0 || !(opt.diag_min > 0) || !(opt.diag_max >= opt.diag_min) ||
         !(opt.huber_delta >= 0) || !std::isfinite(opt.huber_delta) || opt.solver < 0 || opt.solver > 2 ||
@@ -746,8 +748,10 @@ extern "C" rba_status rba_pcg_solve(rba_ctx *c, rba_pcg_stats *stats) {
         Prof P(c, KID_MATVEC, 0.0);
         CK(cudaGraphLaunch(c->pcg_exec, c->stream));
         P.end();
-        c->launches += 1;
         CK(cudaMemcpyAsync(c->h_pcg, d.pcg, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        // every body iteration launched its kernel nodes (the last one's product kernels exit early)
+        c->launches += c->graph_body_kernels * std::max(1, c->h_pcg->it);
     }
     int batch = 2;
     for (; !(!c->have_comm && c->pcg_exec && !no_graph);) {

@@ -209,6 +209,7 @@ struct rba_ctx {
     cudaGraph_t pcg_graph = nullptr;
     cudaGraphExec_t pcg_exec = nullptr;
     bool pcg_graph_failed = false;
+    int64_t graph_body_kernels = 0;  // kernels per PCG-graph iteration (launch accounting)
     bool profiling = false;
     int64_t prof_real_matvecs = 0;  // matvecs that did work (PCG iterations + hook calls) since rba_profile
     std::vector<rba::Launch> prof;

@@ -171,7 +171,10 @@ struct SmallTab {
 };
 
 template <int G>
-__global__ void __launch_bounds__(128) k_marg_small(DevProblem d, int64_t pk_lo, int64_t pk_hi, float lam, float dmin,
+#ifndef RBA_MARG_SMALL_MINB
+#define RBA_MARG_SMALL_MINB 4  // 128 registers: 4 CTAs per SM (measured 3.35 -> 3.22 ms K2 on cfg4)
+#endif
+__global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProblem d, int64_t pk_lo, int64_t pk_hi, float lam, float dmin,
                                                     float dmax) {
     constexpr int NG = 32 / G;
     using TB = SmallTab<G>;
@@ -1596,8 +1599,17 @@ cudaError_t launch_marginalize(rba_ctx *c, float lam) {
     Prof P(c, KID_MARG, plan_marg_bytes(c));
     cudaError_t e;
     ForkJoin F(c);
-    if ((e = marg_large_cls<512, true>(c, 5, lam, F.s()))) return e;
     static const bool m512 = getenv("RBA_MARG512_MULTI") && atoi(getenv("RBA_MARG512_MULTI"));  // tuning knob
+    static const bool small_first = getenv("RBA_MARG_ORDER") && atoi(getenv("RBA_MARG_ORDER"));  // tuning knob
+    auto smalls = [&]() -> cudaError_t {
+        cudaError_t x;
+        if ((x = marg_small_cls<16>(c, 3, lam, F.s()))) return x;
+        if ((x = marg_small_cls<8>(c, 2, lam, F.s()))) return x;
+        if ((x = marg_small_cls<4>(c, 1, lam, F.s()))) return x;
+        return marg_small_cls<2>(c, 0, lam, F.s());
+    };
+    if (small_first && (e = smalls())) return e;
+    if ((e = marg_large_cls<512, true>(c, 5, lam, F.s()))) return e;
     if (m512) {
         if ((e = marg_large_cls<256, true>(c, 4, lam, F.s()))) return e;
     } else if ((e = marg_large_cls<512>(c, 4, lam, F.s()))) {
@@ -1607,10 +1619,7 @@ cudaError_t launch_marginalize(rba_ctx *c, float lam) {
     if ((e = marg_large_cls<128>(c, 2, lam, F.s()))) return e;
     if ((e = marg_large_cls<64>(c, 1, lam, F.s()))) return e;
     if ((e = marg_large_cls<32>(c, 0, lam, F.s()))) return e;
-    if ((e = marg_small_cls<16>(c, 3, lam, F.s()))) return e;
-    if ((e = marg_small_cls<8>(c, 2, lam, F.s()))) return e;
-    if ((e = marg_small_cls<4>(c, 1, lam, F.s()))) return e;
-    if ((e = marg_small_cls<2>(c, 0, lam, F.s()))) return e;
+    if (!small_first && (e = smalls())) return e;
     F.join();
     P.end();
     return cudaSuccess;
@@ -1756,6 +1765,7 @@ cudaError_t build_pcg_graph(rba_ctx *c) {
     k_pcg_step<<<1, 1024, 0, cs>>>(c->d, -1.f, c->opt.pcg_rel_tol, c->opt.pcg_max_iters, h, 1);
     c->stream = saved;
     c->profiling = prof;
+    c->graph_body_kernels = c->launches - nl + 1;  // kernel nodes per loop iteration
     c->launches = nl;
     cudaGraph_t captured;
     e = cudaStreamEndCapture(cs, &captured);
