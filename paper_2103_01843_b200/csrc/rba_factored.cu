@@ -261,17 +261,140 @@ __global__ void __launch_bounds__(256) k_fac_matvec(DevProblem d, int64_t lo, in
 }
 
 // ---- K4F: block-Jacobi blocks P_o = A[:, o]^T A[:, o] and b~_o = A[:, o]^T q from the rows of A
-// recomputed by the WY formula (A[a, o] = delta(a in {2o, 2o+1}) J_o - V[a] M_o, M_o = T^T V_o^T J_o,
-// damping rows mixed by G), O(k) per block, exact (no SC-style subtraction).
+// given by the WY formula: A[a, o] = delta(a in {2o, 2o+1}) J_o - V[a] M_o, M_o = T^T V_o^T J_o, the
+// damping rows being G-mixtures of rows 0..2.  The rows outside the observation's own two are
+// -V[a] M_o, so their sums are M_o^T C_o M_o and -M_o^T e_o with C_o = sum_{a >= 3, not own}
+// V[a]^T V[a] and e_o = sum V[a]^T q_a, formed as exclusive prefix + exclusive suffix sums over the
+// observations (sums of non-negative parts, no subtraction); the own rows and the rows 0..2 that
+// feed the damping rows exactly.  O(k) per landmark.
+
+// C (6 upper) | e (3) contribution of one observation's rows a >= 3
+__device__ __forceinline__ void fac_c9(const FacObs &ob, int o, bool act, float *c9) {
+#pragma unroll
+    for (int i = 0; i < 9; i++) c9[i] = 0.f;
+#pragma unroll
+    for (int rr = 0; rr < 2; rr++) {
+        if (!act || 2 * o + rr < 3) continue;
+        const float *v = ob.v + 3 * rr;
+        c9[0] += v[0] * v[0], c9[1] += v[0] * v[1], c9[2] += v[0] * v[2];
+        c9[3] += v[1] * v[1], c9[4] += v[1] * v[2], c9[5] += v[2] * v[2];
+        c9[6] += v[0] * ob.qr[rr], c9[7] += v[1] * ob.qr[rr], c9[8] += v[2] * ob.qr[rr];
+    }
+}
+
+// exclusive prefix (pre) and suffix (suf) sums of c9 over the G lanes of the group
+template <int G>
+__device__ __forceinline__ void fac_scans(const float *c9, int gl, float *pre, float *suf) {
+#pragma unroll
+    for (int i = 0; i < 9; i++) {
+        const float x = __shfl_up_sync(0xffffffffu, c9[i], 1, G);
+        pre[i] = gl >= 1 ? x : 0.f;
+        const float y = __shfl_down_sync(0xffffffffu, c9[i], 1, G);
+        suf[i] = gl + 1 < G ? y : 0.f;
+    }
+#pragma unroll
+    for (int dlt = 1; dlt < G; dlt <<= 1) {
+#pragma unroll
+        for (int i = 0; i < 9; i++) {
+            const float x = __shfl_up_sync(0xffffffffu, pre[i], dlt, G);
+            const float y = __shfl_down_sync(0xffffffffu, suf[i], dlt, G);
+            if (gl >= dlt) pre[i] += x;
+            if (gl + dlt < G) suf[i] += y;
+        }
+    }
+}
+
+// P_o, b_o of observation o from its record, C_o | e_o (c9 layout), V rows 0..2, the header and
+// the damping mixing Gm; added to the camera's slot of the SM's accumulation slice
+__device__ __forceinline__ void fac_pre_obs(float *out, int cam, int o, const FacObs &ob, const float *Ce,
+                                            const float *V012, const FacHdr &H, const float *Gm) {
+    float C[9];
+    C[0] = Ce[0], C[1] = Ce[1], C[2] = Ce[2], C[4] = Ce[3], C[5] = Ce[4], C[8] = Ce[5];
+    C[3] = C[1], C[6] = C[2], C[7] = C[5];
+    float M[27];
+#pragma unroll
+    for (int q = 0; q < 9; q++) {
+        const float W0 = ob.v[0] * ob.jp[q] + ob.v[3] * ob.jp[9 + q];
+        const float W1 = ob.v[1] * ob.jp[q] + ob.v[4] * ob.jp[9 + q];
+        const float W2 = ob.v[2] * ob.jp[q] + ob.v[5] * ob.jp[9 + q];
+        M[q] = H.T[0] * W0;
+        M[9 + q] = H.T[1] * W0 + H.T[3] * W1;
+        M[18 + q] = H.T[2] * W0 + H.T[4] * W1 + H.T[5] * W2;
+    }
+    float P[45], b[9];
+    {
+        float N[27];  // C M
+#pragma unroll
+        for (int m = 0; m < 3; m++)
+#pragma unroll
+            for (int q = 0; q < 9; q++) N[9 * m + q] = C[3 * m] * M[q] + C[3 * m + 1] * M[9 + q] + C[3 * m + 2] * M[18 + q];
+        int idx = 0;
+#pragma unroll
+        for (int q1 = 0; q1 < 9; q1++) {
+            b[q1] = -(M[q1] * Ce[6] + M[9 + q1] * Ce[7] + M[18 + q1] * Ce[8]);
+#pragma unroll
+            for (int q2 = q1; q2 < 9; q2++) P[idx++] = M[q1] * N[q2] + M[9 + q1] * N[9 + q2] + M[18 + q1] * N[18 + q2];
+        }
+    }
+    float X3[27];  // rows 0..2 of X = Q^T E_o
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+        for (int q = 0; q < 9; q++)
+            X3[9 * a + q] = -(V012[3 * a] * M[q] + V012[3 * a + 1] * M[9 + q] + V012[3 * a + 2] * M[18 + q]);
+#pragma unroll
+    for (int rr = 0; rr < 2; rr++) {
+        const int a = 2 * o + rr;
+        float row[9];
+#pragma unroll
+        for (int q = 0; q < 9; q++)
+            row[q] = ob.jp[9 * rr + q] - (ob.v[3 * rr] * M[q] + ob.v[3 * rr + 1] * M[9 + q] + ob.v[3 * rr + 2] * M[18 + q]);
+        if (a < 3) {
+#pragma unroll
+            for (int q = 0; q < 9; q++) X3[9 * a + q] = row[q];
+        } else {
+            int idx = 0;
+#pragma unroll
+            for (int q1 = 0; q1 < 9; q1++) {
+                b[q1] += row[q1] * ob.qr[rr];
+#pragma unroll
+                for (int q2 = q1; q2 < 9; q2++) P[idx++] += row[q1] * row[q2];
+            }
+        }
+    }
+#pragma unroll
+    for (int s2 = 3; s2 < 6; s2++) {
+        float row[9];
+#pragma unroll
+        for (int q = 0; q < 9; q++) row[q] = Gm[3 * s2] * X3[q] + Gm[3 * s2 + 1] * X3[9 + q] + Gm[3 * s2 + 2] * X3[18 + q];
+        const float qa = H.rr6[s2];
+        int idx = 0;
+#pragma unroll
+        for (int q1 = 0; q1 < 9; q1++) {
+            b[q1] += row[q1] * qa;
+#pragma unroll
+            for (int q2 = q1; q2 < 9; q2++) P[idx++] += row[q1] * row[q2];
+        }
+    }
+    float4 *a4 = reinterpret_cast<float4 *>(out + PACC_STRIDE * (int64_t)cam);
+#pragma unroll
+    for (int i = 0; i < 11; i++) atomicAdd(a4 + i, make_float4(P[4 * i], P[4 * i + 1], P[4 * i + 2], P[4 * i + 3]));
+    atomicAdd(a4 + 11, make_float4(P[44], b[0], b[1], b[2]));
+    atomicAdd(a4 + 12, make_float4(b[3], b[4], b[5], b[6]));
+    atomicAdd(a4 + 13, make_float4(b[7], b[8], 0.f, 0.f));
+}
+
+constexpr int FAC_MAXCH = (KMAX + 31) / 32;  // 32-observation chunks of the longest track
+
 template <int G>
 __global__ void __launch_bounds__(256) k_fac_precond(DevProblem d, int64_t lo, int64_t hi) {
+    // G = 32: per-warp chunk totals / suffix carries for tracks longer than 32 (k > G path)
+    extern __shared__ float chunk_sm[];
     const int lane = threadIdx.x & 31, gl = lane % G;
     const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / G;  // landmarks per grid sweep
     float *out = pslice(d);
-    // warp-uniform trip count (the group shuffles need every lane of the warp): a group whose
-    // landmark is past the range runs with k = 0
     const int64_t wfirst = lo + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * (32 / G);
-    for (int64_t jb = wfirst; jb < hi; jb += ngroups) {
+    for (int64_t jb = wfirst; jb < hi; jb += ngroups) {  // warp-uniform trip count
         const int64_t j = jb + lane / G;
         const bool valid = j < hi;
         const int k = valid ? d.lm_k[j] : 0;
@@ -280,8 +403,7 @@ __global__ void __launch_bounds__(256) k_fac_precond(DevProblem d, int64_t lo, i
         const int32_t *oc = d.obs_cam + (valid ? d.lm_obs0[j] : 0);
         FacHdr H;
         load_hdr(base, H);
-        // Gm: the 6x3 mixing of undamped rows 0..2 into {top, d0, d1, d2} (columns of G applied to e_i)
-        float Gm[18];
+        float Gm[18];  // the 6x3 mixing of undamped rows 0..2 into {top, d0, d1, d2}
 #pragma unroll
         for (int i = 0; i < 3; i++) {
             float x6[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -290,197 +412,76 @@ __global__ void __launch_bounds__(256) k_fac_precond(DevProblem d, int64_t lo, i
 #pragma unroll
             for (int s = 0; s < 6; s++) Gm[3 * s + i] = x6[s];
         }
-        if (G < 32 || __all_sync(0xffffffffu, k <= G)) {
-            // fast path, one observation per lane, O(k): the rows of A outside the lane's own two
-            // are -V[a] M_o, so their sums are M_o^T C_o M_o and -M_o^T e_o with
-            // C_o = sum_{a >= 3, a not own} V[a]^T V[a], e_o = sum V[a]^T q_a, taken as exclusive
-            // prefix + exclusive suffix scans over the group (sums of non-negative parts, no
-            // subtraction); own rows, the rows 0..2 feeding the damping rows, exactly
+        if (G < 32 || __all_sync(0xffffffffu, k <= G)) {  // one observation per lane
             const bool act = gl < k;
             FacObs ob = {};
             if (act) load_obs(fac + 28 * gl, ob);
-            float c9[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // C (6 upper) | e (3)
-#pragma unroll
-            for (int rr = 0; rr < 2; rr++) {
-                if (!act || 2 * gl + rr < 3) continue;
-                const float *v = ob.v + 3 * rr;
-                c9[0] += v[0] * v[0], c9[1] += v[0] * v[1], c9[2] += v[0] * v[2];
-                c9[3] += v[1] * v[1], c9[4] += v[1] * v[2], c9[5] += v[2] * v[2];
-                c9[6] += v[0] * ob.qr[rr], c9[7] += v[1] * ob.qr[rr], c9[8] += v[2] * ob.qr[rr];
-            }
-            float pre[9], suf[9];
+            float c9[9], pre[9], suf[9];
+            fac_c9(ob, gl, act, c9);
+            fac_scans<G>(c9, gl, pre, suf);
             const int gbase = lane - gl;
-#pragma unroll
-            for (int i = 0; i < 9; i++) {
-                float x = __shfl_up_sync(0xffffffffu, c9[i], 1, G);
-                pre[i] = gl >= 1 ? x : 0.f;
-                float y = __shfl_down_sync(0xffffffffu, c9[i], 1, G);
-                suf[i] = gl + 1 < G ? y : 0.f;
-            }
-#pragma unroll
-            for (int dlt = 1; dlt < G; dlt <<= 1) {
-#pragma unroll
-                for (int i = 0; i < 9; i++) {
-                    const float x = __shfl_up_sync(0xffffffffu, pre[i], dlt, G);
-                    const float y = __shfl_down_sync(0xffffffffu, suf[i], dlt, G);
-                    if (gl >= dlt) pre[i] += x;
-                    if (gl + dlt < G) suf[i] += y;
-                }
-            }
-            // V rows 0, 1 (lane 0) and 2 (lane 1) for the rows feeding the damping rows
             float V012[9];
 #pragma unroll
             for (int i = 0; i < 6; i++) V012[i] = __shfl_sync(0xffffffffu, ob.v[i], gbase);
 #pragma unroll
             for (int i = 0; i < 3; i++) V012[6 + i] = __shfl_sync(0xffffffffu, ob.v[i], gbase + 1);
             if (!act) continue;
-            float C[9], e[3];
-            C[0] = pre[0] + suf[0], C[1] = pre[1] + suf[1], C[2] = pre[2] + suf[2];
-            C[4] = pre[3] + suf[3], C[5] = pre[4] + suf[4], C[8] = pre[5] + suf[5];
-            C[3] = C[1], C[6] = C[2], C[7] = C[5];
-            e[0] = pre[6] + suf[6], e[1] = pre[7] + suf[7], e[2] = pre[8] + suf[8];
-            float M[27];
 #pragma unroll
-            for (int q = 0; q < 9; q++) {
-                const float W0 = ob.v[0] * ob.jp[q] + ob.v[3] * ob.jp[9 + q];
-                const float W1 = ob.v[1] * ob.jp[q] + ob.v[4] * ob.jp[9 + q];
-                const float W2 = ob.v[2] * ob.jp[q] + ob.v[5] * ob.jp[9 + q];
-                M[q] = H.T[0] * W0;
-                M[9 + q] = H.T[1] * W0 + H.T[3] * W1;
-                M[18 + q] = H.T[2] * W0 + H.T[4] * W1 + H.T[5] * W2;
-            }
-            float P[45], b[9];
-            {
-                float N[27];  // C M
-#pragma unroll
-                for (int m = 0; m < 3; m++)
-#pragma unroll
-                    for (int q = 0; q < 9; q++) N[9 * m + q] = C[3 * m] * M[q] + C[3 * m + 1] * M[9 + q] + C[3 * m + 2] * M[18 + q];
-                int idx = 0;
-#pragma unroll
-                for (int q1 = 0; q1 < 9; q1++) {
-                    b[q1] = -(M[q1] * e[0] + M[9 + q1] * e[1] + M[18 + q1] * e[2]);
-#pragma unroll
-                    for (int q2 = q1; q2 < 9; q2++)
-                        P[idx++] = M[q1] * N[q2] + M[9 + q1] * N[9 + q2] + M[18 + q1] * N[18 + q2];
-                }
-            }
-            float X3[27];  // rows 0..2 of X = Q^T E_o
-#pragma unroll
-            for (int a = 0; a < 3; a++)
-#pragma unroll
-                for (int q = 0; q < 9; q++)
-                    X3[9 * a + q] = -(V012[3 * a] * M[q] + V012[3 * a + 1] * M[9 + q] + V012[3 * a + 2] * M[18 + q]);
-#pragma unroll
-            for (int rr = 0; rr < 2; rr++) {
-                const int a = 2 * gl + rr;
-                float row[9];
-#pragma unroll
-                for (int q = 0; q < 9; q++)
-                    row[q] = ob.jp[9 * rr + q] - (ob.v[3 * rr] * M[q] + ob.v[3 * rr + 1] * M[9 + q] + ob.v[3 * rr + 2] * M[18 + q]);
-                if (a < 3) {
-#pragma unroll
-                    for (int q = 0; q < 9; q++) X3[9 * a + q] = row[q];
-                } else {
-                    int idx = 0;
-#pragma unroll
-                    for (int q1 = 0; q1 < 9; q1++) {
-                        b[q1] += row[q1] * ob.qr[rr];
-#pragma unroll
-                        for (int q2 = q1; q2 < 9; q2++) P[idx++] += row[q1] * row[q2];
-                    }
-                }
-            }
-#pragma unroll
-            for (int s2 = 3; s2 < 6; s2++) {
-                float row[9];
-#pragma unroll
-                for (int q = 0; q < 9; q++)
-                    row[q] = Gm[3 * s2] * X3[q] + Gm[3 * s2 + 1] * X3[9 + q] + Gm[3 * s2 + 2] * X3[18 + q];
-                const float qa = H.rr6[s2];
-                int idx = 0;
-#pragma unroll
-                for (int q1 = 0; q1 < 9; q1++) {
-                    b[q1] += row[q1] * qa;
-#pragma unroll
-                    for (int q2 = q1; q2 < 9; q2++) P[idx++] += row[q1] * row[q2];
-                }
-            }
-            float4 *a4 = reinterpret_cast<float4 *>(out + PACC_STRIDE * (int64_t)oc[gl]);
-#pragma unroll
-            for (int i = 0; i < 11; i++) atomicAdd(a4 + i, make_float4(P[4 * i], P[4 * i + 1], P[4 * i + 2], P[4 * i + 3]));
-            atomicAdd(a4 + 11, make_float4(P[44], b[0], b[1], b[2]));
-            atomicAdd(a4 + 12, make_float4(b[3], b[4], b[5], b[6]));
-            atomicAdd(a4 + 13, make_float4(b[7], b[8], 0.f, 0.f));
+            for (int i = 0; i < 9; i++) pre[i] += suf[i];
+            fac_pre_obs(out, oc[gl], gl, ob, pre, V012, H, Gm);
             continue;
         }
-        for (int o = gl; o < k; o += G) {
-            FacObs ob;
-            load_obs(fac + 28 * o, ob);
-            float M[27];  // M = T^T (V_o^T J_o), 3 x 9
+        // G == 32, k > 32 (the whole warp is one landmark): chunks of 32 observations.  Pass 1:
+        // chunk totals; suffix carries built from the last chunk backwards (additions only);
+        // pass 2: in-chunk scans + prefix carry + suffix carry.
+        float *tot = chunk_sm + (threadIdx.x >> 5) * (2 * 9 * FAC_MAXCH), *sc = tot + 9 * FAC_MAXCH;
+        const int nch = (k + 31) / 32;
+        for (int c = 0; c < nch; c++) {
+            const int o = 32 * c + lane;
+            FacObs ob = {};
+            if (o < k) load_obs(fac + 28 * o, ob);
+            float c9[9];
+            fac_c9(ob, o, o < k, c9);
 #pragma unroll
-            for (int q = 0; q < 9; q++) {
-                const float W0 = ob.v[0] * ob.jp[q] + ob.v[3] * ob.jp[9 + q];
-                const float W1 = ob.v[1] * ob.jp[q] + ob.v[4] * ob.jp[9 + q];
-                const float W2 = ob.v[2] * ob.jp[q] + ob.v[5] * ob.jp[9 + q];
-                M[q] = H.T[0] * W0;
-                M[9 + q] = H.T[1] * W0 + H.T[3] * W1;
-                M[18 + q] = H.T[2] * W0 + H.T[4] * W1 + H.T[5] * W2;
+            for (int i = 0; i < 9; i++) {
+                const float t = gsum<32>(c9[i]);
+                if (lane == 0) tot[9 * c + i] = t;
             }
-            float P[45], b[9];
-#pragma unroll
-            for (int i = 0; i < 45; i++) P[i] = 0.f;
-#pragma unroll
-            for (int i = 0; i < 9; i++) b[i] = 0.f;
-            float X3[27];  // undamped rows 0..2 of X = Q^T E_o (for the damping rows)
-            for (int a2 = 0; a2 < k; a2++) {  // rows 2 a2, 2 a2 + 1 (V rows of observation a2)
-                FacObs oa;
-                load_obs(fac + 28 * a2, oa);
-#pragma unroll
-                for (int rr = 0; rr < 2; rr++) {
-                    const int a = 2 * a2 + rr;
-                    float row[9];
-#pragma unroll
-                    for (int q = 0; q < 9; q++) {
-                        row[q] = -(oa.v[3 * rr] * M[q] + oa.v[3 * rr + 1] * M[9 + q] + oa.v[3 * rr + 2] * M[18 + q]);
-                        if (a2 == o) row[q] += ob.jp[9 * rr + q];
-                    }
-                    if (a < 3) {
-#pragma unroll
-                        for (int q = 0; q < 9; q++) X3[9 * a + q] = row[q];
-                    } else {
-                        const float qa = oa.qr[rr];
-                        int idx = 0;
-#pragma unroll
-                        for (int q1 = 0; q1 < 9; q1++) {
-                            b[q1] += row[q1] * qa;
-#pragma unroll
-                            for (int q2 = q1; q2 < 9; q2++) P[idx++] += row[q1] * row[q2];
-                        }
-                    }
-                }
-            }
-#pragma unroll
-            for (int s = 3; s < 6; s++) {  // damping rows d0..d2 and their residual entries
-                float row[9];
-#pragma unroll
-                for (int q = 0; q < 9; q++) row[q] = Gm[3 * s] * X3[q] + Gm[3 * s + 1] * X3[9 + q] + Gm[3 * s + 2] * X3[18 + q];
-                const float qa = H.rr6[s];
-                int idx = 0;
-#pragma unroll
-                for (int q1 = 0; q1 < 9; q1++) {
-                    b[q1] += row[q1] * qa;
-#pragma unroll
-                    for (int q2 = q1; q2 < 9; q2++) P[idx++] += row[q1] * row[q2];
-                }
-            }
-            float4 *a4 = reinterpret_cast<float4 *>(out + PACC_STRIDE * (int64_t)oc[o]);
-#pragma unroll
-            for (int i = 0; i < 11; i++) atomicAdd(a4 + i, make_float4(P[4 * i], P[4 * i + 1], P[4 * i + 2], P[4 * i + 3]));
-            atomicAdd(a4 + 11, make_float4(P[44], b[0], b[1], b[2]));
-            atomicAdd(a4 + 12, make_float4(b[3], b[4], b[5], b[6]));
-            atomicAdd(a4 + 13, make_float4(b[7], b[8], 0.f, 0.f));
         }
+        __syncwarp();
+        if (lane < 9) {
+            float acc = 0.f;
+            for (int c = nch - 1; c >= 0; c--) {
+                sc[9 * c + lane] = acc;
+                acc += tot[9 * c + lane];
+            }
+        }
+        __syncwarp();
+        FacObs o0, o1;
+        load_obs(fac, o0);
+        load_obs(fac + 28, o1);
+        float V012[9];
+#pragma unroll
+        for (int i = 0; i < 6; i++) V012[i] = o0.v[i];
+#pragma unroll
+        for (int i = 0; i < 3; i++) V012[6 + i] = o1.v[i];
+        float pc[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        for (int c = 0; c < nch; c++) {
+            const int o = 32 * c + lane;
+            const bool act = o < k;
+            FacObs ob = {};
+            if (act) load_obs(fac + 28 * o, ob);
+            float c9[9], pre[9], suf[9];
+            fac_c9(ob, o, act, c9);
+            fac_scans<32>(c9, lane, pre, suf);
+#pragma unroll
+            for (int i = 0; i < 9; i++) {
+                pre[i] += pc[i] + (suf[i] + sc[9 * c + i]);
+                pc[i] += tot[9 * c + i];
+            }
+            if (act) fac_pre_obs(out, oc[o], o, ob, pre, V012, H, Gm);
+        }
+        __syncwarp();
     }
 }
 
@@ -593,7 +594,9 @@ static void fac_cls(rba_ctx *c, int cls, int what, const float *v, const PcgStat
     if (what == 0) {
         k_fac_matvec<G><<<g, 256, 0, s>>>(c->d, lo, hi, v, st);
     } else if (what == 1) {
-        k_fac_precond<G><<<g, 256, 0, s>>>(c->d, lo, hi);
+        const size_t sm = G == 32 ? sizeof(float) * 8 * 2 * 9 * FAC_MAXCH : 0;
+        if (G == 32) cudaFuncSetAttribute(k_fac_precond<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k_fac_precond<G><<<g, 256, sm, s>>>(c->d, lo, hi);
     } else {
         k_fac_backsub<G><<<g, 256, 0, s>>>(c->d, lo, hi, lam);
     }
