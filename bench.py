@@ -178,6 +178,18 @@ def run_oracle(prob, cfg, steps, warmup, every, budget_s=None):
     }
 
 
+def bench_config(args, prob, world):
+    """The workload description shared by both arms (ours and --impl reference)."""
+    return {"workload": WORKLOADS[args.config], "cfg": args.config, "n_p": int(prob["cameras_init"].shape[0]),
+            "n_l": int(prob["points_init"].shape[0]), "n_obs": int(len(prob["obs_cam"])),
+            "solver": {"sqrtba": "sqrt-BA-32 (QR nullspace marginalization)", "sc32": "explicit-32 (Schur complement)",
+                       "sc64": "explicit-64 (Schur complement)"}[args.solver],
+            "storage": args.storage,
+            "parallelism": f"landmark-shard x{world}",
+            "l2": "inputs larger than L2 (landmark-block arena >> 126 MB)" if args.config >= 3 else
+            "working set L2-resident (no flush)"}
+
+
 def bench_reference(args, prob, rank):
     if rank != 0:
         return
@@ -186,7 +198,7 @@ def bench_reference(args, prob, rank):
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "LM iterations/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / val,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOADS[args.config], "cfg": args.config},
+            "config": bench_config(args, prob, args.gpus),
             "cpu_baseline": dict(cb, value=val, unit="LM iterations/s"),
             "e2e": {"value": val, "unit": "LM iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -348,13 +360,7 @@ def main():
         "metric": METRIC, "value": args.steps / (t_ms * 1e-3), "unit": "LM iterations/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64" if args.solver == "sc64" else "f32", "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.config], "cfg": args.config, "n_p": n_p, "n_l": n_l, "n_obs": n_obs,
-                   "solver": {"sqrtba": "sqrt-BA-32 (QR nullspace marginalization)", "sc32": "explicit-32 (Schur complement)",
-                              "sc64": "explicit-64 (Schur complement)"}[args.solver],
-                   "storage": args.storage,
-                   "parallelism": f"landmark-shard x{world}",
-                   "l2": "inputs larger than L2 (landmark-block arena >> 126 MB)" if args.config >= 3 else
-                   "working set L2-resident (no flush)"},
+        "config": bench_config(args, prob, world),
         "qr_marginalized_obs_per_s": n_obs / (t_marg * 1e-3),
         "marginalize_ms": t_marg,
         "pcg_iters": [r["pcg_iters"] for r in reps],

@@ -484,6 +484,12 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
         }
         for (int q = cls; q < 5; q++) c->fac_hi[q] = nl;
         for (int q = cls + 1; q < 5; q++) c->fac_lo[q] = nl;
+        c->fac_big = nl;
+        for (int64_t i = 0; i < nl; i++)
+            if (c->h_k[i] > 32) {
+                c->fac_big = i;
+                break;
+            }
         c->arena_floats = std::max<int64_t>(off, 4);
     }
     // ---- device buffers

@@ -260,6 +260,103 @@ __global__ void __launch_bounds__(256) k_fac_matvec(DevProblem d, int64_t lo, in
     }
 }
 
+// ---- K5F for long tracks (k > 32): CTA per landmark, thread <-> observations, the four phases
+// (u = J_p v and V^T u | w = u - V T^T (V^T u) | special rows through G, V^T z | out) separated by
+// CTA reductions; u / w kept in shared memory (2 floats per observation)
+constexpr int FAC_NT = 256;
+__device__ __forceinline__ void cta_sum3(float *v, float *red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int i = 0; i < 3; i++) v[i] = warp_sum_f(v[i]);
+    if (lane == 0)
+#pragma unroll
+        for (int i = 0; i < 3; i++) red[4 * warp + i] = v[i];
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+        float s = 0.f;
+#pragma unroll
+        for (int w = 0; w < FAC_NT / 32; w++) s += red[4 * w + i];
+        v[i] = s;
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(FAC_NT) k_fac_matvec_cta(DevProblem d, int64_t lo, const float *__restrict__ v,
+                                                          const PcgState *__restrict__ st) {
+    if (st && st->done) return;
+    extern __shared__ float wsm[];  // 2k
+    __shared__ float red[4 * (FAC_NT / 32)];
+    __shared__ float zr[3];
+    const int64_t j = lo + blockIdx.x;
+    const int k = d.lm_k[j], tid = threadIdx.x;
+    const float *base = d.arena + d.lm_r2[j];
+    const float *fac = base + 44;
+    const int32_t *oc = d.obs_cam + d.lm_obs0[j];
+    float T[6], g[12];
+#pragma unroll
+    for (int i = 0; i < 6; i++) T[i] = base[9 + i];
+#pragma unroll
+    for (int i = 0; i < 12; i++) g[i] = base[15 + i];
+    float s[3] = {0.f, 0.f, 0.f};
+    for (int o = tid; o < k; o += FAC_NT) {
+        FacObs ob;
+        load_obs(fac + 28 * o, ob);
+        const float *x = v + 9 * (int64_t)oc[o];
+        float u0 = 0.f, u1 = 0.f;
+#pragma unroll
+        for (int q = 0; q < 9; q++) {
+            u0 += ob.jp[q] * x[q];
+            u1 += ob.jp[9 + q] * x[q];
+        }
+        wsm[2 * o] = u0, wsm[2 * o + 1] = u1;
+        s[0] += ob.v[0] * u0 + ob.v[3] * u1;
+        s[1] += ob.v[1] * u0 + ob.v[4] * u1;
+        s[2] += ob.v[2] * u0 + ob.v[5] * u1;
+    }
+    cta_sum3(s, red);
+    const float ta = T[0] * s[0], tb = T[1] * s[0] + T[3] * s[1], tc = T[2] * s[0] + T[4] * s[1] + T[5] * s[2];
+    float r[3] = {0.f, 0.f, 0.f};
+    for (int o = tid; o < k; o += FAC_NT) {  // w = u - V t
+        FacObs ob;
+        load_obs(fac + 28 * o, ob);
+        wsm[2 * o] -= ob.v[0] * ta + ob.v[1] * tb + ob.v[2] * tc;
+        wsm[2 * o + 1] -= ob.v[3] * ta + ob.v[4] * tb + ob.v[5] * tc;
+    }
+    __syncthreads();
+    if (tid == 0) {  // special rows: G on (w0, w1, w2; 0), then G^T on (0; dd)
+        float x6[6] = {wsm[0], wsm[1], wsm[2], 0.f, 0.f, 0.f};
+        givens_fwd(g, x6);
+        x6[0] = x6[1] = x6[2] = 0.f;
+        givens_inv(g, x6);
+        zr[0] = x6[0], zr[1] = x6[1], zr[2] = x6[2];
+    }
+    __syncthreads();
+    if (tid == 0) wsm[0] = zr[0], wsm[1] = zr[1], wsm[2] = zr[2];
+    __syncthreads();
+    for (int o = tid; o < k; o += FAC_NT) {  // s' = V^T z
+        FacObs ob;
+        load_obs(fac + 28 * o, ob);
+        const float z0 = wsm[2 * o], z1 = wsm[2 * o + 1];
+        r[0] += ob.v[0] * z0 + ob.v[3] * z1;
+        r[1] += ob.v[1] * z0 + ob.v[4] * z1;
+        r[2] += ob.v[2] * z0 + ob.v[5] * z1;
+    }
+    cta_sum3(r, red);
+    const float t0 = T[0] * r[0] + T[1] * r[1] + T[2] * r[2], t1 = T[3] * r[1] + T[4] * r[2], t2 = T[5] * r[2];
+    float *out = wslice(d);
+    for (int o = tid; o < k; o += FAC_NT) {
+        FacObs ob;
+        load_obs(fac + 28 * o, ob);
+        const float z0 = wsm[2 * o] - (ob.v[0] * t0 + ob.v[1] * t1 + ob.v[2] * t2);
+        const float z1 = wsm[2 * o + 1] - (ob.v[3] * t0 + ob.v[4] * t1 + ob.v[5] * t2);
+        float acc[9];
+#pragma unroll
+        for (int q = 0; q < 9; q++) acc[q] = ob.jp[q] * z0 + ob.jp[9 + q] * z1;
+        flush_cam12(out, oc[o], acc);
+    }
+}
+
 // ---- K4F: block-Jacobi blocks P_o = A[:, o]^T A[:, o] and b~_o = A[:, o]^T q from the rows of A
 // given by the WY formula: A[a, o] = delta(a in {2o, 2o+1}) J_o - V[a] M_o, M_o = T^T V_o^T J_o, the
 // damping rows being G-mixtures of rows 0..2.  The rows outside the observation's own two are
@@ -592,7 +689,17 @@ static void fac_cls(rba_ctx *c, int cls, int what, const float *v, const PcgStat
     if (hi <= lo) return;
     const unsigned g = (unsigned)std::min<int64_t>(nbk((hi - lo) * G, 256), (int64_t)c->num_sms * 8);
     if (what == 0) {
-        k_fac_matvec<G><<<g, 256, 0, s>>>(c->d, lo, hi, v, st);
+        const int64_t hw = G == 32 ? std::min(hi, std::max(lo, c->fac_big)) : hi;  // warp path up to k = 32
+        if (hw > lo) {
+            const unsigned gw = (unsigned)std::min<int64_t>(nbk((hw - lo) * G, 256), (int64_t)c->num_sms * 8);
+            k_fac_matvec<G><<<gw, 256, 0, s>>>(c->d, lo, hw, v, st);
+        }
+        if (G == 32 && hi > hw) {
+            c->launches++;
+            const size_t sm = sizeof(float) * 2 * (size_t)c->max_large_k;
+            cudaFuncSetAttribute(k_fac_matvec_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(sm, 16));
+            k_fac_matvec_cta<<<(unsigned)(hi - hw), FAC_NT, sm, s>>>(c->d, hw, v, st);
+        }
     } else if (what == 1) {
         const size_t sm = G == 32 ? sizeof(float) * 8 * 2 * 9 * FAC_MAXCH : 0;
         if (G == 32) cudaFuncSetAttribute(k_fac_precond<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

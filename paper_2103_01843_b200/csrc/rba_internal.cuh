@@ -186,6 +186,7 @@ struct rba_ctx {
     int64_t marg_lo[6] = {0, 0, 0, 0, 0, 0}, marg_hi[6] = {0, 0, 0, 0, 0, 0};  // K2 large items per class
     int64_t n_huge_y = 0, n_huge_out = 0, huge_max_k = 0;  // k > KLARGE (two-pass matvec)
     int64_t fac_lo[5] = {0, 0, 0, 0, 0}, fac_hi[5] = {0, 0, 0, 0, 0};  // factored: G = 2..32 landmark ranges
+    int64_t fac_big = 0;  // factored: first landmark with k > 32 (CTA-per-landmark matvec from here)
     int64_t cta_off[5] = {0, 0, 0, 0, 0}, cta_n[5] = {0, 0, 0, 0, 0};    // K4/K5 CTA ranges per class
     int64_t n_chunks = 0, chunk_ctas = 0;
     int64_t n_packs = 0, max_large_k = 0;
