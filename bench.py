@@ -184,7 +184,7 @@ def bench_config(args, prob, world):
             "n_l": int(prob["points_init"].shape[0]), "n_obs": int(len(prob["obs_cam"])),
             "solver": {"sqrtba": "sqrt-BA-32 (QR nullspace marginalization)", "sc32": "explicit-32 (Schur complement)",
                        "sc64": "explicit-64 (Schur complement)"}[args.solver],
-            "storage": args.storage,
+            "storage": args.storage, "precision": args.precision,
             "parallelism": f"landmark-shard x{world}",
             "l2": "inputs larger than L2 (landmark-block arena >> 126 MB)" if args.config >= 3 else
             "working set L2-resident (no flush)"}
@@ -219,6 +219,8 @@ def main():
     ap.add_argument("--storage", default="dense", choices=["dense", "factored"],
                     help="landmark-block storage: the paper's dense blocks (default) or the factored "
                          "form (SURVEY §8f f4, beyond the paper)")
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"],
+                    help="sqrt-BA-32 (default, the paper's headline) or sqrt-BA-64 (SURVEY §8f f2)")
     ap.add_argument("--solver", default="sqrtba", choices=list(SOLVERS),
                     help="landmark elimination: sqrt-BA (the paper's method, default) or the explicit "
                          "Schur-complement baselines explicit-32 / explicit-64 (SURVEY §8f f3)")
@@ -244,7 +246,7 @@ def main():
         nccl_id = obj[0]
     n_p, n_l, n_obs = prob["cameras_init"].shape[0], prob["points_init"].shape[0], len(prob["obs_cam"])
     s = rba.Solver(prob, device=local, world=world, rank=rank, nccl_id=nccl_id, solver=SOLVERS[args.solver],
-                   storage=1 if args.storage == "factored" else 0)
+                   storage=1 if args.storage == "factored" else 0, precision=1 if args.precision == "fp64" else 0)
     stream = s.stream
 
     def barrier():
@@ -336,8 +338,8 @@ def main():
                 "traffic": None, "peak_source": peak_src, "launches": n, "avg_ms": ms / n,
                 "bytes_per_launch": by / n}
 
-    variant = "" if (args.storage == "dense" and args.solver == "sqrtba") else \
-        ("_factored" if args.solver == "sqrtba" else f"_{args.solver}")
+    variant = "" if (args.storage == "dense" and args.solver == "sqrtba" and args.precision == "fp32") else \
+        ("_factored" if args.storage == "factored" else ("_fp64" if args.precision == "fp64" else f"_{args.solver}"))
     tr_mv, tr_mg, tr_src = ncu_traffic(args.config, variant)
     roof_mv = roof(*prof["matvec"])
     if roof_mv:
@@ -346,6 +348,7 @@ def main():
         roof_mv["kernel"] = {
             "": "matvec (K5: k_small_pipe + k_large_pipe<NS> + k_huge_*, then k_reduce_slices), algorithmic 72k^2 B/landmark",
             "_factored": "factored matvec (k_fac_matvec<G> + k_reduce_slices), algorithmic 176+112k B/landmark",
+            "_fp64": "sqrt-BA-64 product (k_rcs64), algorithmic 8 x 2k(9k+1) B/landmark",
         }.get(variant, "explicit-SC SpMV (k_sc_spmv), algorithmic 81 x sizeof(T) B per 9x9 block")
     roof_mg = roof(*mprof)
     if roof_mg:
@@ -354,12 +357,13 @@ def main():
         roof_mg["kernel"] = {
             "": "marginalize (K2: k_marg_small<G> + k_marg_large<NT>), algorithmic (2k+3)(9k+4)*4+48+20k B/landmark",
             "_factored": "factored marginalize (K2 writing factors), algorithmic 176+132k B/landmark",
+            "_fp64": "sqrt-BA-64 marginalize (k_marg64), algorithmic 8 (2k+3)(9k+4) + 96 + 40k B/landmark",
         }.get(variant, "explicit-SC build (k_sc_build), algorithmic 81 x sizeof(T) B per block + 48 B/obs")
     total_prof = sum(shares.values())
     line = {
         "metric": METRIC, "value": args.steps / (t_ms * 1e-3), "unit": "LM iterations/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64" if args.solver == "sc64" else "f32", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64" if (args.solver == "sc64" or args.precision == "fp64") else "f32", "data": "synthetic",
         "config": bench_config(args, prob, world),
         "qr_marginalized_obs_per_s": n_obs / (t_marg * 1e-3),
         "marginalize_ms": t_marg,
@@ -379,11 +383,14 @@ def main():
     # rows f3, f4), timed the same way (W warm-up, reset, K steps, CUDA events): context for the
     # headline, which stays the paper's dense sqrt-BA-32
     # (single GPU only: a second NCCL communicator would need its own unique id)
-    if not args.no_variants and args.solver == "sqrtba" and args.storage == "dense" and world == 1:
+    if not args.no_variants and args.solver == "sqrtba" and args.storage == "dense" and args.precision == "fp32" \
+            and world == 1:
         s.close()
         variants = {}
-        for vname, kw in (("sqrtba32_factored", dict(storage=1)), ("explicit32", dict(solver=1)),
-                          ("explicit64", dict(solver=2))):
+        for vname, kw in (("sqrtba32_factored", dict(storage=1)), ("sqrtba64", dict(precision=1)),
+                          ("explicit32", dict(solver=1)), ("explicit64", dict(solver=2))):
+            if vname == "sqrtba64" and int(np.bincount(prob["obs_pt"]).max()) > 1024:
+                continue  # sqrt-BA-64 supports tracks up to 1024
             if vname.startswith("explicit") and args.config >= 5:
                 continue  # covisibility H~ too large / slow to form for the final13682 shape
             sv = rba.Solver(prob, device=local, world=world, rank=rank, nccl_id=nccl_id, **kw)

@@ -76,7 +76,15 @@ typedef struct {
      * bytes per landmark; the reduced system is applied in O(k)).  Same results up to
      * rounding; rba_export_block is RBA_ERR_STATE in factored mode. */
     int storage;
+    /* arithmetic of the landmark blocks for RBA_SOLVER_SQRTBA with dense storage (SURVEY §8f row
+     * f2): RBA_PRECISION_FP32 (default, the paper's sqrt-BA-32) or RBA_PRECISION_FP64 (sqrt-BA-64:
+     * the (2k+3) x (9k+4) blocks stored row-major in FP64 and every QR / product / back-substitution
+     * operation in FP64; track lengths up to 1024).  The column scaling and damping diagonals are
+     * FP32 in both (shared with K1). */
+    int precision;
 } rba_options;
+
+enum { RBA_PRECISION_FP32 = 0, RBA_PRECISION_FP64 = 1 };
 
 enum { RBA_STORAGE_DENSE = 0, RBA_STORAGE_FACTORED = 1 };
 

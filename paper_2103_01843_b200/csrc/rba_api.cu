@@ -198,7 +198,8 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     if (opt.world < 1 || opt.rank < 0 || opt.rank >= opt.world || !(opt.lambda0 > 0) || !(opt.pcg_rel_tol >= 0) ||
         opt.pcg_max_iters < 0 || !(opt.diag_min > 0) || !(opt.diag_max >= opt.diag_min) ||
         !(opt.huber_delta >= 0) || !std::isfinite(opt.huber_delta) || opt.solver < 0 || opt.solver > 2 ||
-        opt.storage < 0 || opt.storage > 1 || (opt.storage == 1 && opt.solver != 0))
+        opt.storage < 0 || opt.storage > 1 || (opt.storage == 1 && opt.solver != 0) || opt.precision < 0 ||
+        opt.precision > 1 || (opt.precision == 1 && (opt.solver != 0 || opt.storage != 0)))
         return fail(RBA_ERR_INVALID_ARG, "rba_create: bad options");
     if (n_obs >= (int64_t)1 << 31 || n_points >= (int64_t)1 << 31 || n_cams >= (int64_t)1 << 28)
         return fail(RBA_ERR_INVALID_ARG, "rba_create: problem too large for int32 indices");
@@ -223,6 +224,10 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
         if (kcount[j] < 2)
             return fail(RBA_ERR_BAD_PROBLEM, "landmark " + std::to_string(j) + " has " + std::to_string(kcount[j]) +
                                                  " < 2 observations (P:469)");
+        if (opt.precision == 1 && kcount[j] > KMAX64)
+            return fail(RBA_ERR_BAD_PROBLEM, "landmark " + std::to_string(j) + ": track length " +
+                                                 std::to_string(kcount[j]) + " exceeds sqrt-BA-64's " +
+                                                 std::to_string(KMAX64));
         if (kcount[j] > KMAX)
             return fail(RBA_ERR_BAD_PROBLEM, "landmark " + std::to_string(j) + ": track length " +
                                                  std::to_string(kcount[j]) + " exceeds this build's KMAX " +
@@ -499,6 +504,7 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     d.huber = opt.huber_delta;
     d.sc = opt.solver;
     d.fac = opt.storage;
+    d.s64 = opt.precision;
     d.n_obs = nobs_loc;
     CKSC(dalloc_n(c, &d.cams, 9 * n_cams));
     CKSC(dalloc_n(c, &d.cams_trial, 9 * n_cams));
@@ -517,6 +523,34 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     CKSC(dalloc_n(c, &d.Dp2, 9 * n_cams));
     CKSC(dalloc_n(c, &d.lm_s, 3 * nl));
     CKSC(dalloc_n(c, &d.lm_D, 3 * nl));
+    if (d.s64) {
+        // sqrt-BA-64: row-major FP64 logical blocks + 12 Givens doubles; classes k <= 32, <= 128, else
+        int64_t off = 0;
+        c->logical_bytes = 0;
+        c->matvec_bytes = 0;
+        c->marg_bytes = 0;
+        const int lim[3] = {32, 128, KMAX64};
+        int cls = 0;
+        for (int64_t i = 0; i < nl; i++) {
+            const int k = c->h_k[i];
+            while (k > lim[cls]) {
+                c->s64_hi[cls] = i;
+                c->s64_lo[++cls] = i;
+            }
+            c->s64_kmax[cls] = std::max<int64_t>(c->s64_kmax[cls], k);
+            c->h_r2[i] = off;
+            off += (int64_t)(2 * k + 3) * (9 * k + 4) + 12;
+            c->logical_bytes += (int64_t)(2 * k + 3) * (9 * k + 4) * 8 + 96;
+            c->matvec_bytes += 8.0 * 2 * k * (9 * k + 1);  // reduced rows A | q read once
+            c->marg_bytes += 8.0 * (2 * k + 3) * (9 * k + 4) + 96 + 40.0 * k;
+        }
+        for (int q = cls; q < 3; q++) c->s64_hi[q] = nl;
+        for (int q = cls + 1; q < 3; q++) c->s64_lo[q] = nl;
+        c->arena_floats = 4;
+        CKSC(dalloc_n(c, &d.arena64, std::max<int64_t>(off, 1)));
+        CKSC(dalloc_n(c, &d.lm_s64, 3 * std::max<int64_t>(nl, 1)));
+        CKSC(dalloc_n(c, &d.lm_D64, 3 * std::max<int64_t>(nl, 1)));
+    }
     if (d.sc) {
         // explicit SC: no landmark blocks; the covisibility graph of the local landmarks as BSR
         // (both triangles, columns ascending per camera row)
@@ -714,7 +748,11 @@ extern "C" rba_status rba_marginalize_qr(rba_ctx *c, double lambda) {
     if (!(lambda >= 0) || !std::isfinite(lambda)) return fail(RBA_ERR_INVALID_ARG, "lambda must be finite and >= 0");
     if (!c->linearized) return fail(RBA_ERR_STATE, "rba_marginalize_qr before rba_linearize");
     CK(cudaSetDevice(c->device));
-    if (c->d.sc) {  // explicit SC: H_ll depends on lambda, so every new lambda re-forms H~
+    if (c->d.s64) {  // sqrt-BA-64: marginalize once per linearization, then re-damp in place
+        if (!c->marginalized) CK(launch_marg64(c, lambda));
+        else if (lambda != c->lambda_blocks) CK(launch_redamp64(c, lambda));
+        c->marginalized = true;
+    } else if (c->d.sc) {  // explicit SC: H_ll depends on lambda, so every new lambda re-forms H~
         if (!c->marginalized || (float)lambda != (float)c->lambda_blocks) CK(launch_sc_build(c, (float)lambda));
         c->marginalized = true;
     } else if (!c->marginalized) {
@@ -736,7 +774,7 @@ extern "C" rba_status rba_pcg_solve(rba_ctx *c, rba_pcg_stats *stats) {
     DevProblem &d = c->d;
     const float lam = (float)c->lambda_blocks;
     CK(cudaMemsetAsync(d.scal + SC_BAD, 0, sizeof(double), c->stream));
-    CK(c->d.sc ? launch_sc_precond(c) : launch_precond_rhs(c));
+    CK(c->d.sc ? launch_sc_precond(c) : launch_precond_rhs(c));  // (sqrt-BA-64 dispatches inside)
     CKS(allreduce(c, d.pd, 54 * d.n_p, ncclDouble));
     CK(launch_precond_finalize(c, lam));
     CK(launch_pcg_init(c, (float)c->opt.pcg_rel_tol, c->opt.pcg_max_iters));
@@ -979,6 +1017,16 @@ extern "C" rba_status rba_export_block(rba_ctx *c, int64_t landmark, double *buf
     if (!c->marginalized) return fail(RBA_ERR_STATE, "rba_export_block before rba_marginalize_qr");
     if (c->d.sc) return fail(RBA_ERR_STATE, "rba_export_block: explicit-SC mode keeps no landmark blocks");
     if (c->d.fac) return fail(RBA_ERR_STATE, "rba_export_block: factored storage keeps no dense blocks");
+    if (c->d.s64) {
+        const int64_t j = c->orig_to_int[landmark];
+        const int k = c->h_k[j];
+        const int64_t R = 2 * k + 3, C = 9 * k + 4;
+        *rows = R, *cols = C;
+        if (cap < R * C) return fail(RBA_ERR_INVALID_ARG, "buffer too small");
+        CK(cudaMemcpyAsync(buf, c->d.arena64 + c->h_r2[j], sizeof(double) * R * C, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        return RBA_OK;
+    }
     const int64_t j = c->orig_to_int[landmark];
     const int k = c->h_k[j];
     const int64_t R = 2 * k + 3, C = 9 * k + 4;
@@ -1010,7 +1058,7 @@ extern "C" rba_status rba_arena_bytes(rba_ctx *c, int64_t *logical, int64_t *phy
         return RBA_OK;
     }
     *logical = c->logical_bytes;
-    *physical = c->arena_floats * 4;
+    *physical = c->d.s64 ? c->logical_bytes : c->arena_floats * 4;
     return RBA_OK;
 }
 

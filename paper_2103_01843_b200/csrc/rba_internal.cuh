@@ -15,6 +15,7 @@ namespace rba {
 constexpr int KSMALL = 16;    // k <= KSMALL: warp-group kernels over packs of same-k landmarks
 constexpr int KLARGE = 512;   // k <= KLARGE: one thread per camera block in the large-k kernels
 constexpr int KMAX = 3072;    // largest track length supported (k > KLARGE: "huge" path, smem-bound)
+constexpr int KMAX64 = 1024;  // sqrt-BA-64 (f2): largest track length (registers of the FP64 product)
 
 // ---- landmark-block arena layout ------------------------------------------
 // Logical block of a landmark with k observations: rows 0..2k+2, columns [J_p (9k) | J_l | r].
@@ -152,6 +153,9 @@ struct DevProblem {
     void *sc_scratch;             // per observation: G_a (27) and L_a = G_a H_ll^-1 (27)
     // factored storage (f4, rba_factored.cu): landmark j's factors at arena + lm_r2[j]
     int fac;
+    // sqrt-BA-64 (f2, rba_sqrtba64.cu): row-major FP64 blocks at arena64 + lm_r2[j]
+    int s64;
+    double *arena64, *lm_s64, *lm_D64;
 };
 
 struct Launch {
@@ -187,6 +191,7 @@ struct rba_ctx {
     int64_t n_huge_y = 0, n_huge_out = 0, huge_max_k = 0;  // k > KLARGE (two-pass matvec)
     int64_t fac_lo[5] = {0, 0, 0, 0, 0}, fac_hi[5] = {0, 0, 0, 0, 0};  // factored: G = 2..32 landmark ranges
     int64_t fac_big = 0;  // factored: first landmark with k > 32 (CTA-per-landmark matvec from here)
+    int64_t s64_lo[3] = {0, 0, 0}, s64_hi[3] = {0, 0, 0}, s64_kmax[3] = {2, 2, 2};  // sqrt-BA-64 classes
     int64_t cta_off[5] = {0, 0, 0, 0, 0}, cta_n[5] = {0, 0, 0, 0, 0};    // K4/K5 CTA ranges per class
     int64_t n_chunks = 0, chunk_ctas = 0;
     int64_t n_packs = 0, max_large_k = 0;
@@ -246,6 +251,13 @@ void launch_fac_matvec(rba_ctx *c, const float *v, const PcgState *st);
 void launch_fac_precond(rba_ctx *c);
 cudaError_t launch_fac_backsub(rba_ctx *c, float lambda);
 cudaError_t launch_fac_redamp(rba_ctx *c, float lambda);
+// sqrt-BA-64 (rba_sqrtba64.cu)
+cudaError_t launch_marg64(rba_ctx *c, double lambda);
+cudaError_t launch_redamp64(rba_ctx *c, double lambda);
+void launch_rcs64(rba_ctx *c, const double *v, const PcgState *st);
+void launch_pre64(rba_ctx *c);
+cudaError_t launch_backsub64(rba_ctx *c, float lambda);
+void launch_f2d64(rba_ctx *c, const float *a, double *b, int64_t n);
 cudaError_t launch_sc_backsub(rba_ctx *c, float lambda);
 // profiling scope: CUDA events on the context stream around one launch (rba_api.cu)
 struct Prof {

@@ -1699,6 +1699,11 @@ static void reduce_slices(rba_ctx *c, float *sl, int stride, int nv, double *out
 
 cudaError_t launch_precond_rhs(rba_ctx *c) {
     Prof P(c, KID_PRE, plan_matvec_bytes(c));
+    if (c->d.s64) {
+        launch_pre64(c);
+        P.end();
+        return cudaGetLastError();
+    }
     if (c->d.fac) launch_fac_precond(c);
     else pipes_all<true>(c, nullptr, c->d.psl, nullptr);
     reduce_slices(c, c->d.psl, PACC_STRIDE, 54, c->d.pd, nullptr);
@@ -1716,6 +1721,15 @@ cudaError_t launch_precond_finalize(rba_ctx *c, float lam) {
 static void matvec_body(rba_ctx *c, const float *v, const PcgState *st) {
     if (c->d.sc) {
         launch_sc_spmv(c, st, st ? nullptr : v);
+        return;
+    }
+    if (c->d.s64) {  // sqrt-BA-64: FP64 product straight into wd
+        const double *v64 = c->d.p;
+        if (!st) {  // test hook: FP32 input
+            launch_f2d64(c, v, c->d.z, 9 * c->d.n_p);
+            v64 = c->d.z;
+        }
+        launch_rcs64(c, v64, st);
         return;
     }
     if (c->d.fac) launch_fac_matvec(c, v, st);
@@ -1800,6 +1814,9 @@ cudaError_t launch_backsub(rba_ctx *c, float lam) {
         if (e) return e;
     } else if (c->d.fac) {
         cudaError_t e = launch_fac_backsub(c, lam);
+        if (e) return e;
+    } else if (c->d.s64) {
+        cudaError_t e = launch_backsub64(c, lam);
         if (e) return e;
     } else if (c->d.n_l) {
         const unsigned g = (unsigned)std::min<int64_t>(nblk(32 * c->d.n_l, 256), (int64_t)c->num_sms * 8);

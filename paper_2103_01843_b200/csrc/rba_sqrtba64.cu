@@ -1,0 +1,514 @@
+// rba_sqrtba64.cu -- sqrt-BA-64 (the paper's double-precision variant, P:407,
+// Table 1): the same QR nullspace marginalization (Householder + compact WY, 6 damping Givens),
+// reduced-camera-system product, block-Jacobi blocks and back-substitution as the FP32 path, with
+// the landmark blocks stored and all their arithmetic done in FP64.  Storage is the paper's logical
+// block itself: (2k+3) x (9k+4) doubles per landmark, row-major (Fig. 2c), followed by the 6
+// Givens pairs.  Camera-space sums use FP64 atomics directly (no FP32 slices).
+// Product path only (no oracle code).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "rba_internal.cuh"
+#include "rba_model.cuh"
+
+namespace rba {
+
+// block of landmark j: B + row * W + col, W = 9k + 4; Givens after the (2k+3) rows
+__device__ __forceinline__ double *blk64(const DevProblem &d, int64_t j) { return d.arena64 + d.lm_r2[j]; }
+
+__device__ __forceinline__ void givens64(double a, double b, double &c, double &s) {
+    if (b == 0.0) {
+        c = 1.0, s = 0.0;
+    } else {
+        const double r = hypot(a, b);
+        c = a / r, s = b / r;
+    }
+}
+
+// the 6 damping rotations on rows {0,1,2} x {2k, 2k+1, 2k+2} (reading C5 / C6), FP64
+__device__ __forceinline__ void damp64(const double *R, const double *sD, double *g) {
+    double L6[18] = {};
+#pragma unroll
+    for (int i = 0; i < 9; i++) L6[i] = R[i];
+#pragma unroll
+    for (int i = 0; i < 3; i++) L6[(3 + i) * 3 + i] = sD[i];
+#pragma unroll
+    for (int m = 0; m < 6; m++) {
+        const int p = damp_p(m), t = damp_t(m);
+        double c, s;
+        givens64(L6[p * 3 + p], L6[t * 3 + p], c, s);
+        g[2 * m] = c, g[2 * m + 1] = s;
+#pragma unroll
+        for (int q = 0; q < 3; q++) {
+            const double a = L6[p * 3 + q], b = L6[t * 3 + q];
+            L6[p * 3 + q] = c * a + s * b;
+            L6[t * 3 + q] = -s * a + c * b;
+        }
+        L6[t * 3 + p] = 0.0;
+    }
+}
+
+// ---- K2-64: CTA per landmark; thread o' owns observations / camera blocks o = o', o' + NT, ...
+// Householder on the scaled 2k x 3 landmark Jacobian in shared memory, compact WY, then every row
+// of the block is written from  out[a, 9o+q] = E[a, 9o+q] - V[a] . M_o[:, q]  (rows 0..2k-1), the
+// landmark / residual columns, and the damping rows by the 6 rotations of rows 0..2.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_marg64(DevProblem d, int64_t lo, double lam, double dmin, double dmax) {
+    extern __shared__ double s64[];
+    __shared__ double red[4 * (NT / 32)];
+    const int64_t j = lo + blockIdx.x;
+    const int k = d.lm_k[j], tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int W = 9 * k + 4;
+    double *SX = s64;           // 2k x 3 (scaled J_l, then R / V)
+    double *SR = SX + 6 * k;    // 2k residual column
+    double *SV = SR + 2 * k;    // 2k x 3 Householder vectors
+    const int64_t obs0 = d.lm_obs0[j];
+    const double *Xp = d.pts + 3 * j;
+    auto bsum = [&](double *v, int n) {  // CTA sum of n <= 4 values, result in every thread
+        for (int i = 0; i < n; i++) v[i] = warp_sum_d(v[i]);
+        __syncthreads();
+        if (lane == 0)
+            for (int i = 0; i < n; i++) red[4 * warp + i] = v[i];
+        __syncthreads();
+        for (int i = 0; i < n; i++) {
+            double s = 0.0;
+            for (int w = 0; w < NT / 32; w++) s += red[4 * w + i];
+            v[i] = s;
+        }
+        __syncthreads();
+    };
+    double n2[4] = {0, 0, 0, 0};
+    for (int o = tid; o < k; o += NT) {
+        double c[9], r[2], Jc[18], Jl[6];
+        load_cam(d.cams, d.obs_cam[obs0 + o], c);
+        const double2 uv = d.obs_uv[obs0 + o];
+        cam_model<double>(c, Xp[0], Xp[1], Xp[2], uv.x, uv.y, r, Jc, Jl);
+        apply_irls<double>(r, Jc, Jl, d.huber);
+        for (int q = 0; q < 3; q++) {
+            SX[6 * o + q] = Jl[q], SX[6 * o + 3 + q] = Jl[3 + q];
+            n2[q] += Jl[q] * Jl[q] + Jl[3 + q] * Jl[3 + q];
+        }
+        SR[2 * o] = r[0], SR[2 * o + 1] = r[1];
+    }
+    bsum(n2, 3);
+    double sl[3], Dl[3];
+    for (int q = 0; q < 3; q++) {
+        sl[q] = 1.0 / (1.0 + sqrt(n2[q]));
+        Dl[q] = sqrt(fmin(fmax(n2[q] * sl[q] * sl[q], dmin), dmax));
+    }
+    for (int a = tid; a < 2 * k; a += NT)
+        for (int q = 0; q < 3; q++) SX[3 * a + q] *= sl[q], SV[3 * a + q] = 0.0;
+    __syncthreads();
+    double tau[3];
+    for (int c = 0; c < 3; c++) {  // reflector c on rows c..2k-1 (reading C4 for the sign)
+        double sm[4] = {0, 0, 0, 0};
+        for (int a = c + tid; a < 2 * k; a += NT) {
+            const double x = SX[3 * a + c];
+            sm[0] += x * x;
+            if (c < 2) sm[1] += x * SX[3 * a + c + 1];
+            if (c < 1) sm[2] += x * SX[3 * a + c + 2];
+            sm[3] += x * SR[a];
+        }
+        const double x0 = SX[3 * c + c], y1 = c < 2 ? SX[3 * c + c + 1] : 0.0, y2 = c < 1 ? SX[3 * c + c + 2] : 0.0,
+                     yr = SR[c];
+        bsum(sm, 4);
+        const double sig = sqrt(sm[0]), alpha = x0 >= 0.0 ? -sig : sig;
+        const double vtv = 2.0 * sig * (sig + fabs(x0));
+        const double tc = vtv > 0.0 ? 2.0 / vtv : 0.0;
+        tau[c] = tc;
+        const double d1 = sm[1] - alpha * y1, d2 = sm[2] - alpha * y2, dr = sm[3] - alpha * yr;
+        for (int a = c + tid; a < 2 * k; a += NT) {
+            const double vv = a == c ? x0 - alpha : SX[3 * a + c];
+            SV[3 * a + c] = vv;
+            if (c < 2) SX[3 * a + c + 1] -= tc * vv * d1;
+            if (c < 1) SX[3 * a + c + 2] -= tc * vv * d2;
+            SR[a] -= tc * vv * dr;
+            SX[3 * a + c] = a == c ? alpha : 0.0;
+        }
+        __syncthreads();
+    }
+    double pv[4] = {0, 0, 0, 0};
+    for (int a = tid; a < 2 * k; a += NT) {
+        pv[0] += SV[3 * a] * SV[3 * a + 1];
+        pv[1] += SV[3 * a] * SV[3 * a + 2];
+        pv[2] += SV[3 * a + 1] * SV[3 * a + 2];
+    }
+    bsum(pv, 3);
+    const double T00 = tau[0], T11 = tau[1], T22 = tau[2];
+    const double T01 = -tau[1] * T00 * pv[0];
+    const double T02 = -tau[2] * (T00 * pv[1] + T01 * pv[2]);
+    const double T12 = -tau[2] * T11 * pv[2];
+    // damping rotations from the undamped R (rows 0..2 of SX) and sqrt(lam) D_l
+    double R[9], g[12];
+    for (int i = 0; i < 9; i++) R[i] = SX[i];
+    const double sq = sqrt(lam), sD[3] = {sq * Dl[0], sq * Dl[1], sq * Dl[2]};
+    damp64(R, sD, g);
+    double *B = blk64(d, j);
+    // pose columns of every row: thread <-> camera block o
+    for (int o = tid; o < k; o += NT) {
+        double c[9], r[2], Jc[18], Jl[6], jp[18];
+        const int cam = d.obs_cam[obs0 + o];
+        load_cam(d.cams, cam, c);
+        const double2 uv = d.obs_uv[obs0 + o];
+        cam_model<double>(c, Xp[0], Xp[1], Xp[2], uv.x, uv.y, r, Jc, Jl);
+        apply_irls<double>(r, Jc, Jl, d.huber);
+        for (int q = 0; q < 9; q++) {
+            const double s = d.sp[9 * cam + q];
+            jp[q] = Jc[q] * s, jp[9 + q] = Jc[9 + q] * s;
+        }
+        double M[27];  // M = T^T V_o^T J_o
+        const double *v0 = SV + 6 * o, *v1 = v0 + 3;
+        for (int q = 0; q < 9; q++) {
+            const double W0 = v0[0] * jp[q] + v1[0] * jp[9 + q], W1 = v0[1] * jp[q] + v1[1] * jp[9 + q],
+                         W2 = v0[2] * jp[q] + v1[2] * jp[9 + q];
+            M[q] = T00 * W0;
+            M[9 + q] = T01 * W0 + T11 * W1;
+            M[18 + q] = T02 * W0 + T12 * W1 + T22 * W2;
+        }
+        double top[27];  // undamped rows 0..2, then mixed into rows 0..2 / 2k..2k+2
+        for (int a = 0; a < 2 * k; a++) {
+            const double *va = SV + 3 * a;
+            double row[9];
+            for (int q = 0; q < 9; q++) {
+                double x = -(va[0] * M[q] + va[1] * M[9 + q] + va[2] * M[18 + q]);
+                if ((a >> 1) == o) x += jp[9 * (a & 1) + q];
+                row[q] = x;
+            }
+            if (a < 3) {
+                for (int q = 0; q < 9; q++) top[9 * a + q] = row[q];
+            } else {
+                for (int q = 0; q < 9; q++) B[(int64_t)a * W + 9 * o + q] = row[q];
+            }
+        }
+        double x6[6][9];
+        for (int q = 0; q < 9; q++) {
+            double x[6] = {top[q], top[9 + q], top[18 + q], 0.0, 0.0, 0.0};
+            for (int m = 0; m < 6; m++) {
+                const int p = damp_p(m), t = damp_t(m);
+                const double a = x[p], b = x[t];
+                x[p] = g[2 * m] * a + g[2 * m + 1] * b;
+                x[t] = -g[2 * m + 1] * a + g[2 * m] * b;
+            }
+            for (int s = 0; s < 6; s++) x6[s][q] = x[s];
+        }
+        for (int s = 0; s < 6; s++) {
+            const int row = s < 3 ? s : 2 * k + s - 3;
+            for (int q = 0; q < 9; q++) B[(int64_t)row * W + 9 * o + q] = x6[s][q];
+        }
+    }
+    // landmark and residual columns (4 per row): R / 0 and Q^T r, damping rows rotated
+    for (int a = tid; a < 2 * k + 3; a += NT) {
+        double *rw = B + (int64_t)a * W + 9 * k;
+        if (a >= 3 && a < 2 * k) {
+            rw[0] = rw[1] = rw[2] = 0.0;
+            rw[3] = SR[a];
+        }
+    }
+    if (tid == 0) {
+        double X[6][4] = {};
+        for (int i = 0; i < 3; i++) {
+            for (int q = 0; q < 3; q++) X[i][q] = R[3 * i + q];
+            X[i][3] = SR[i];
+            X[3 + i][i] = sD[i];
+        }
+        for (int m = 0; m < 6; m++) {
+            const int p = damp_p(m), t = damp_t(m);
+            for (int q = 0; q < 4; q++) {
+                const double a = X[p][q], b = X[t][q];
+                X[p][q] = g[2 * m] * a + g[2 * m + 1] * b;
+                X[t][q] = -g[2 * m + 1] * a + g[2 * m] * b;
+            }
+            X[t][p] = 0.0;
+        }
+        for (int s = 0; s < 6; s++) {
+            const int row = s < 3 ? s : 2 * k + s - 3;
+            for (int q = 0; q < 4; q++) B[(int64_t)row * W + 9 * k + q] = X[s][q];
+        }
+        double *G = B + (int64_t)(2 * k + 3) * W;
+        for (int i = 0; i < 12; i++) G[i] = g[i];
+    }
+    if (tid < 3) {
+        d.lm_s[3 * j + tid] = (float)sl[tid];
+        d.lm_D[3 * j + tid] = (float)Dl[tid];
+        d.lm_D64[3 * j + tid] = Dl[tid];
+        d.lm_s64[3 * j + tid] = sl[tid];
+    }
+}
+
+// ---- K3-64: undo the stored rotations (reverse order, transposed) and re-damp, rows {0,1,2} and
+// {2k..2k+2} over all 9k + 4 columns.  Warp per landmark.
+__global__ void __launch_bounds__(256) k_redamp64(DevProblem d, double lam) {
+    const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (j >= d.n_l) return;
+    const int k = d.lm_k[j], W = 9 * k + 4;
+    double *B = blk64(d, j);
+    double *G = B + (int64_t)(2 * k + 3) * W;
+    double g[12];
+    for (int i = 0; i < 12; i++) g[i] = G[i];
+    // R after undo: undo the 6 rotations on the landmark columns (+ damping diag) of rows 0..2
+    double X[6][3];
+    for (int s = 0; s < 6; s++) {
+        const int row = s < 3 ? s : 2 * k + s - 3;
+        for (int q = 0; q < 3; q++) X[s][q] = B[(int64_t)row * W + 9 * k + q];
+    }
+    for (int m = 5; m >= 0; m--) {
+        const int p = damp_p(m), t = damp_t(m);
+        for (int q = 0; q < 3; q++) {
+            const double a = X[p][q], b = X[t][q];
+            X[p][q] = g[2 * m] * a - g[2 * m + 1] * b;
+            X[t][q] = g[2 * m + 1] * a + g[2 * m] * b;
+        }
+    }
+    double R[9];
+    for (int i = 0; i < 3; i++)
+        for (int q = 0; q < 3; q++) R[3 * i + q] = q < i ? 0.0 : X[i][q];
+    const double sq = sqrt(lam);
+    const double sD[3] = {sq * d.lm_D64[3 * j], sq * d.lm_D64[3 * j + 1], sq * d.lm_D64[3 * j + 2]};
+    double gn[12];
+    damp64(R, sD, gn);
+    for (int c = lane; c < W; c += 32) {
+        double x[6];
+        for (int s = 0; s < 6; s++) x[s] = B[(int64_t)(s < 3 ? s : 2 * k + s - 3) * W + c];
+        for (int m = 5; m >= 0; m--) {  // undo
+            const int p = damp_p(m), t = damp_t(m);
+            const double a = x[p], b = x[t];
+            x[p] = g[2 * m] * a - g[2 * m + 1] * b;
+            x[t] = g[2 * m + 1] * a + g[2 * m] * b;
+        }
+        for (int s = 3; s < 6; s++) x[s] = 0.0;  // damping rows dropped
+        if (c >= 9 * k && c < 9 * k + 3) x[3 + (c - 9 * k)] = sD[c - 9 * k];
+        for (int m = 0; m < 6; m++) {  // re-damp
+            const int p = damp_p(m), t = damp_t(m);
+            const double a = x[p], b = x[t];
+            x[p] = gn[2 * m] * a + gn[2 * m + 1] * b;
+            x[t] = -gn[2 * m + 1] * a + gn[2 * m] * b;
+        }
+        if (c >= 9 * k && c < 9 * k + 3) x[3 + (c - 9 * k)] = 0.0;  // eliminated exactly
+        for (int s = 0; s < 6; s++) B[(int64_t)(s < 3 ? s : 2 * k + s - 3) * W + c] = x[s];
+    }
+    __syncwarp();
+    if (lane == 0) {
+        // lower-triangle entries of R^1 exactly zero
+        B[(int64_t)1 * W + 9 * k] = 0.0, B[(int64_t)2 * W + 9 * k] = 0.0, B[(int64_t)2 * W + 9 * k + 1] = 0.0;
+        for (int i = 0; i < 12; i++) G[i] = gn[i];
+    }
+}
+
+// ---- K4-64 / K5-64: CTA per landmark, rows 3..2k+2 of the block (the reduced rows A_j, q_j).
+// Product: per chunk of 8 rows, warps compute y_a = A[a] . v (lanes over columns, coalesced),
+// then thread <-> camera block accumulates out_o += A[a, block o]^T y_a (re-read from L1).
+template <int NT, int NB, bool PRE>
+__global__ void __launch_bounds__(NT) k_rcs64(DevProblem d, int64_t lo, const double *__restrict__ v,
+                                              const PcgState *__restrict__ st) {
+    if (!PRE && st && st->done) return;
+    // NB: camera blocks per thread (k <= NB * NT in this class)
+    const int64_t j = lo + blockIdx.x;
+    const int k = d.lm_k[j], W = 9 * k + 4, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const double *B = blk64(d, j);
+    const int32_t *oc = d.obs_cam + d.lm_obs0[j];
+    if (PRE) {
+        for (int o = tid; o < k; o += NT) {
+            double P[45] = {}, b[9] = {};
+            for (int a = 3; a < 2 * k + 3; a++) {
+                const double *rw = B + (int64_t)a * W;
+                double x[9];
+                for (int q = 0; q < 9; q++) x[q] = rw[9 * o + q];
+                const double qa = rw[9 * k + 3];
+                int idx = 0;
+                for (int q1 = 0; q1 < 9; q1++) {
+                    b[q1] += x[q1] * qa;
+                    for (int q2 = q1; q2 < 9; q2++) P[idx++] += x[q1] * x[q2];
+                }
+            }
+            double *acc = d.pd + 54 * (int64_t)oc[o];
+            for (int i = 0; i < 45; i++) atomicAdd(acc + i, P[i]);
+            for (int i = 0; i < 9; i++) atomicAdd(acc + 45 + i, b[i]);
+        }
+        return;
+    }
+    // thread <-> camera blocks o = tid + m NT (m < NB): its v_o in registers; per chunk of 8 rows the
+    // 8 partial dot products over its blocks are reduced across the CTA (warp shuffles, + smem for
+    // NT > 32), then out_o += A[a, o]^T y_a re-reads its 8 x 9 row segments from L1
+    __shared__ double part[8][NT / 32];
+    double acc[NB][9], vo[NB][9];
+#pragma unroll
+    for (int m = 0; m < NB; m++) {
+        const int o = tid + m * NT;
+#pragma unroll
+        for (int q = 0; q < 9; q++) {
+            acc[m][q] = 0.0;
+            vo[m][q] = o < k ? v[9 * (int64_t)oc[o] + q] : 0.0;
+        }
+    }
+    for (int a0 = 3; a0 < 2 * k + 3; a0 += 8) {
+        const int nr = min(8, 2 * k + 3 - a0);
+        double y[8];
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+            double s = 0.0;
+            if (r < nr) {
+                const double *rw = B + (int64_t)(a0 + r) * W;
+#pragma unroll
+                for (int m = 0; m < NB; m++) {
+                    const int o = tid + m * NT;
+                    if (o < k)
+#pragma unroll
+                        for (int q = 0; q < 9; q++) s += rw[9 * o + q] * vo[m][q];
+                }
+            }
+            y[r] = warp_sum_d(s);
+        }
+        if (NT > 32) {
+            if (lane == 0)
+#pragma unroll
+                for (int r = 0; r < 8; r++) part[r][warp] = y[r];
+            __syncthreads();
+#pragma unroll
+            for (int r = 0; r < 8; r++) {
+                double t = 0.0;
+#pragma unroll
+                for (int w = 0; w < NT / 32; w++) t += part[r][w];
+                y[r] = t;
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int m = 0; m < NB; m++) {
+            const int o = tid + m * NT;
+            if (o < k) {
+#pragma unroll
+                for (int r = 0; r < 8; r++) {
+                    if (r < nr) {
+                        const double *rw = B + (int64_t)(a0 + r) * W + 9 * o;
+#pragma unroll
+                        for (int q = 0; q < 9; q++) acc[m][q] += rw[q] * y[r];
+                    }
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int m = 0; m < NB; m++) {
+        const int o = tid + m * NT;
+        if (o < k) {
+            double *out = d.wd + 9 * (int64_t)oc[o];
+#pragma unroll
+            for (int q = 0; q < 9; q++) atomicAdd(out + q, acc[m][q]);
+        }
+    }
+}
+
+// ---- K7-64: dl = -R^1^-1 (Q^1^T r^ + Q^1^T J_p dp), warp per landmark (grid-stride)
+__global__ void __launch_bounds__(256) k_backsub64(DevProblem d, double lam) {
+    __shared__ double red[32];
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    double q1 = 0.0, dd = 0.0;
+    for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < d.n_l; j += nwarps) {
+        const int k = d.lm_k[j], W = 9 * k + 4;
+        const double *B = blk64(d, j);
+        const int32_t *oc = d.obs_cam + d.lm_obs0[j];
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+        for (int c = lane; c < 9 * k; c += 32) {
+            const int o = c / 9;
+            const double x = d.x[9 * (int64_t)oc[o] + (c - 9 * o)];
+            s0 += B[c] * x, s1 += B[W + c] * x, s2 += B[2 * W + c] * x;
+        }
+        s0 = warp_sum_d(s0), s1 = warp_sum_d(s1), s2 = warp_sum_d(s2);
+        if (lane == 0) {
+            const double *R0 = B + 9 * k, *R1 = B + W + 9 * k, *R2 = B + 2 * W + 9 * k;
+            const double b0 = R0[3] + s0, b1 = R1[3] + s1, b2 = R2[3] + s2;
+            const double x2 = b2 / R2[2], x1 = (b1 - R1[2] * x2) / R1[1], x0 = (b0 - R0[1] * x1 - R0[2] * x2) / R0[0];
+            const double dl[3] = {-x0, -x1, -x2};
+            q1 += R0[3] * R0[3] + R1[3] * R1[3] + R2[3] * R2[3];
+            for (int q = 0; q < 3; q++) {
+                d.dl[3 * j + q] = (float)dl[q];
+                d.pts_trial[3 * j + q] = d.pts[3 * j + q] + d.lm_s64[3 * j + q] * dl[q];
+                const double Dd = d.lm_D64[3 * j + q] * dl[q];
+                dd += Dd * Dd;
+            }
+        }
+    }
+    q1 = block_sum_d(q1, red);
+    dd = block_sum_d(dd, red);
+    if (threadIdx.x == 0) {
+        atomicAdd(d.scal + SC_Q1R2, q1);
+        atomicAdd(d.scal + SC_DAMPL, lam * dd);
+    }
+}
+
+// ============================================================================ launchers
+static inline unsigned nb64(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+__global__ void k_f2d64(const float *__restrict__ a, double *__restrict__ b, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) b[i] = a[i];
+}
+void launch_f2d64(rba_ctx *c, const float *a, double *b, int64_t n) {
+    k_f2d64<<<nb64(n, 256), 256, 0, c->stream>>>(a, b, n);
+    c->launches++;
+}
+
+template <int NT>
+static void marg64_cls(rba_ctx *c, int cls, double lam) {
+    const int64_t lo = c->s64_lo[cls], hi = c->s64_hi[cls];
+    if (hi <= lo) return;
+    const size_t sm = sizeof(double) * 14 * (size_t)c->s64_kmax[cls];  // SX 6k | SR 2k | SV 6k
+    cudaFuncSetAttribute(k_marg64<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_marg64<NT><<<(unsigned)(hi - lo), NT, sm, c->stream>>>(c->d, lo, lam, c->opt.diag_min, c->opt.diag_max);
+    c->launches++;
+}
+
+cudaError_t launch_marg64(rba_ctx *c, double lam) {
+    Prof P(c, KID_MARG, c->marg_bytes);
+    marg64_cls<32>(c, 0, lam);
+    marg64_cls<128>(c, 1, lam);
+    marg64_cls<256>(c, 2, lam);
+    P.end();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_redamp64(rba_ctx *c, double lam) {
+    if (c->d.n_l == 0) return cudaSuccess;
+    Prof P(c, KID_DAMP, 0.0);
+    k_redamp64<<<nb64(32 * c->d.n_l, 256), 256, 0, c->stream>>>(c->d, lam);
+    c->launches++;
+    P.end();
+    return cudaGetLastError();
+}
+
+template <int NT, int NB, bool PRE>
+static void rcs64_cls(rba_ctx *c, int cls, const double *v, const PcgState *st) {
+    const int64_t lo = c->s64_lo[cls], hi = c->s64_hi[cls];
+    if (hi <= lo) return;
+    k_rcs64<NT, NB, PRE><<<(unsigned)(hi - lo), NT, 0, c->stream>>>(c->d, lo, v, st);
+    c->launches++;
+}
+
+// wd = sum_j A_j^T A_j v (FP64 atomics; wd zeroed here)
+void launch_rcs64(rba_ctx *c, const double *v, const PcgState *st) {
+    cudaMemsetAsync(c->d.wd, 0, sizeof(double) * 9 * c->d.n_p, c->stream);
+    rcs64_cls<32, 1, false>(c, 0, v, st);
+    rcs64_cls<128, 1, false>(c, 1, v, st);
+    rcs64_cls<256, KMAX64 / 256, false>(c, 2, v, st);
+}
+
+void launch_pre64(rba_ctx *c) {
+    cudaMemsetAsync(c->d.pd, 0, sizeof(double) * 54 * c->d.n_p, c->stream);
+    rcs64_cls<32, 1, true>(c, 0, nullptr, nullptr);
+    rcs64_cls<128, 1, true>(c, 1, nullptr, nullptr);
+    rcs64_cls<256, KMAX64 / 256, true>(c, 2, nullptr, nullptr);
+}
+
+cudaError_t launch_backsub64(rba_ctx *c, float lam) {
+    if (c->d.n_l) {
+        const unsigned g = (unsigned)std::min<int64_t>(nb64(32 * c->d.n_l, 256), (int64_t)c->num_sms * 8);
+        k_backsub64<<<g, 256, 0, c->stream>>>(c->d, (double)lam);
+        c->launches++;
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace rba

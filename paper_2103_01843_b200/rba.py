@@ -30,7 +30,8 @@ class rba_options(C.Structure):
                 ("nccl_unique_id", C.c_void_p), ("lambda0", C.c_double), ("pcg_rel_tol", C.c_double),
                 ("pcg_max_iters", C.c_int), ("min_rel_decrease", C.c_double), ("diag_min", C.c_double),
                 ("diag_max", C.c_double), ("alloc", _ALLOC_T), ("free", _FREE_T), ("alloc_ctx", C.c_void_p),
-                ("huber_delta", C.c_double), ("solver", C.c_int), ("storage", C.c_int)]
+                ("huber_delta", C.c_double), ("solver", C.c_int), ("storage", C.c_int), ("precision", C.c_int)]
+RBA_PRECISION_FP32, RBA_PRECISION_FP64 = 0, 1
 RBA_STORAGE_DENSE, RBA_STORAGE_FACTORED = 0, 1
 RBA_SOLVER_SQRTBA, RBA_SOLVER_EXPLICIT_SC32, RBA_SOLVER_EXPLICIT_SC64 = 0, 1, 2
 
