@@ -521,6 +521,9 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     CKSC(dalloc_n(c, &d.cam_n2, 12 * n_cams));
     CKSC(dalloc_n(c, &d.sp, 9 * n_cams));
     CKSC(dalloc_n(c, &d.Dp2, 9 * n_cams));
+    CKSC(dalloc_n(c, &d.sp64, 9 * n_cams));
+    CKSC(dalloc_n(c, &d.Dp264, 9 * n_cams));
+    CKSC(dalloc_n(c, &d.cam_n2d, 9 * n_cams));
     CKSC(dalloc_n(c, &d.lm_s, 3 * nl));
     CKSC(dalloc_n(c, &d.lm_D, 3 * nl));
     if (d.s64) {
@@ -529,7 +532,7 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
         c->logical_bytes = 0;
         c->matvec_bytes = 0;
         c->marg_bytes = 0;
-        const int lim[3] = {32, 128, KMAX64};
+        const int lim[5] = {32, 128, 256, 512, KMAX64};
         int cls = 0;
         for (int64_t i = 0; i < nl; i++) {
             const int k = c->h_k[i];
@@ -544,8 +547,47 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
             c->matvec_bytes += 8.0 * 2 * k * (9 * k + 1);  // reduced rows A | q read once
             c->marg_bytes += 8.0 * (2 * k + 3) * (9 * k + 4) + 96 + 40.0 * k;
         }
-        for (int q = cls; q < 3; q++) c->s64_hi[q] = nl;
-        for (int q = cls + 1; q < 3; q++) c->s64_lo[q] = nl;
+        for (int q = cls; q < 5; q++) c->s64_hi[q] = nl;
+        for (int q = cls + 1; q < 5; q++) c->s64_lo[q] = nl;
+        // K2-64 work items: (landmark, pose-row range of ~4 MB of output); the FP32 items are unused
+        marg_items.clear();
+        for (int q = 0; q < 5; q++) {
+            c->s64_ilo[q] = (int64_t)marg_items.size();
+            for (int64_t i = c->s64_lo[q]; i < c->s64_hi[q]; i++) {
+                const int k = c->h_k[i];
+                const int rpi = (int)std::max<int64_t>(8, (int64_t)524288 / (9 * k + 4));
+                for (int r = 0; r < 2 * k; r += rpi)
+                    marg_items.push_back(LargeItem{(int32_t)i, r, std::min(2 * k, r + rpi), 0});
+            }
+            c->s64_ihi[q] = (int64_t)marg_items.size();
+        }
+        std::vector<LargeItem> rcs;  // product items: ~1 MB of the reduced rows 3..2k+2 each
+        for (int q = 0; q < 5; q++) {
+            c->s64_plo[q] = (int64_t)rcs.size();
+            for (int64_t i = c->s64_lo[q]; i < c->s64_hi[q]; i++) {
+                const int k = c->h_k[i];
+                const int rpi = (int)std::max<int64_t>(8, (int64_t)131072 / (9 * k + 4));
+                for (int r = 3; r < 2 * k + 3; r += rpi)
+                    rcs.push_back(LargeItem{(int32_t)i, r, std::min(2 * k + 3, r + rpi), 0});
+            }
+            c->s64_phi[q] = (int64_t)rcs.size();
+        }
+        {  // class 0 (k <= 32): one item per landmark, in k order; split by group size
+            const int gl[4] = {4, 8, 16, 32};
+            int64_t pos = c->s64_plo[0];
+            for (int g = 0; g < 4; g++) {
+                c->s64_glo[g] = pos;
+                while (pos < c->s64_phi[0] && c->h_k[rcs[pos].lm] <= gl[g]) pos++;
+                c->s64_ghi[g] = pos;
+                c->s64_mlo[g] = c->s64_lo[0] + (c->s64_glo[g] - c->s64_plo[0]);  // one item per landmark
+                c->s64_mhi[g] = c->s64_lo[0] + (c->s64_ghi[g] - c->s64_plo[0]);
+            }
+        }
+        CKSC(dalloc_n(c, &d.rcs_items, std::max<size_t>(1, rcs.size())));
+        if (!rcs.empty())
+            CKC(cudaMemcpyAsync(d.rcs_items, rcs.data(), sizeof(LargeItem) * rcs.size(), cudaMemcpyHostToDevice,
+                                c->stream));
+        CKC(cudaStreamSynchronize(c->stream));
         c->arena_floats = 4;
         CKSC(dalloc_n(c, &d.arena64, std::max<int64_t>(off, 1)));
         CKSC(dalloc_n(c, &d.lm_s64, 3 * std::max<int64_t>(nl, 1)));
@@ -728,9 +770,11 @@ extern "C" rba_status rba_linearize(rba_ctx *c) {
     CK(cudaSetDevice(c->device));
     DevProblem &d = c->d;
     CK(cudaMemsetAsync(d.cam_n2, 0, sizeof(float) * 12 * d.n_p, c->stream));
+    if (d.s64) CK(cudaMemsetAsync(d.cam_n2d, 0, sizeof(double) * 9 * d.n_p, c->stream));
     CK(cudaMemsetAsync(d.scal + SC_E, 0, sizeof(double) * 2, c->stream));
     CK(launch_linearize(c));
     CKS(allreduce(c, d.cam_n2, 12 * d.n_p, ncclFloat));
+    if (d.s64) CKS(allreduce(c, d.cam_n2d, 9 * d.n_p, ncclDouble));
     CKS(allreduce(c, d.scal + SC_E, 2, ncclDouble));
     CK(launch_cam_scale(c));
     CKS(read_scal(c));
@@ -992,19 +1036,26 @@ extern "C" rba_status rba_get_scaling(rba_ctx *c, double *sp, double *Dp2, doubl
     if (!c || !sp || !Dp2 || !sl || !Dl2) return fail(RBA_ERR_INVALID_ARG, "null argument");
     if (!c->linearized) return fail(RBA_ERR_STATE, "rba_get_scaling before rba_linearize");
     const int64_t n = 9 * c->d.n_p, m = 3 * std::max<int64_t>(c->d.n_l, 1);
-    std::vector<float> a(n), b(n), s(m), D(m);
-    CK(cudaMemcpyAsync(a.data(), c->d.sp, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaMemcpyAsync(b.data(), c->d.Dp2, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream));
+    std::vector<float> s(m), D(m);
+    CK(cudaMemcpyAsync(sp, c->d.sp64, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(Dp2, c->d.Dp264, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(s.data(), c->d.lm_s, sizeof(float) * 3 * c->d.n_l, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(D.data(), c->d.lm_D, sizeof(float) * 3 * c->d.n_l, cudaMemcpyDeviceToHost, c->stream));
+    std::vector<double> s64, D64;
+    if (c->d.s64) {  // the exact FP64 landmark scaling of sqrt-BA-64
+        s64.resize(m), D64.resize(m);
+        CK(cudaMemcpyAsync(s64.data(), c->d.lm_s64, sizeof(double) * 3 * c->d.n_l, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(D64.data(), c->d.lm_D64, sizeof(double) * 3 * c->d.n_l, cudaMemcpyDeviceToHost, c->stream));
+    }
     CK(cudaStreamSynchronize(c->stream));
-    for (int64_t i = 0; i < n; i++) sp[i] = a[i], Dp2[i] = b[i];
     for (int64_t i = 0; i < 3 * c->n_l_global; i++) sl[i] = 0.0, Dl2[i] = 0.0;
     if (c->marginalized)
         for (int64_t i = 0; i < c->d.n_l; i++)
             for (int q = 0; q < 3; q++) {
-                sl[3 * (int64_t)c->lm_orig[i] + q] = s[3 * i + q];
-                Dl2[3 * (int64_t)c->lm_orig[i] + q] = (double)D[3 * i + q] * D[3 * i + q];
+                const double sv = c->d.s64 ? s64[3 * i + q] : s[3 * i + q];
+                const double Dv = c->d.s64 ? D64[3 * i + q] : D[3 * i + q];
+                sl[3 * (int64_t)c->lm_orig[i] + q] = sv;
+                Dl2[3 * (int64_t)c->lm_orig[i] + q] = Dv * Dv;
             }
     return RBA_OK;
 }

@@ -119,6 +119,8 @@ struct DevProblem {
     double2 *obs_uv;
     // scaling / damping
     float *cam_n2, *sp, *Dp2;
+    double *cam_n2d;       // sqrt-BA-64: camera column norms^2 accumulated in FP64 (9 per camera)
+    double *sp64, *Dp264;  // FP64 copies of S_p and D_p^2 (exact FP64 values for sqrt-BA-64)
     float *lm_s, *lm_D;
     // arena
     float *arena;
@@ -156,6 +158,7 @@ struct DevProblem {
     // sqrt-BA-64 (f2, rba_sqrtba64.cu): row-major FP64 blocks at arena64 + lm_r2[j]
     int s64;
     double *arena64, *lm_s64, *lm_D64;
+    LargeItem *rcs_items;  // sqrt-BA-64 product / block-Jacobi items: (landmark, rows [t0, t1) of 3..2k+2)
 };
 
 struct Launch {
@@ -191,7 +194,11 @@ struct rba_ctx {
     int64_t n_huge_y = 0, n_huge_out = 0, huge_max_k = 0;  // k > KLARGE (two-pass matvec)
     int64_t fac_lo[5] = {0, 0, 0, 0, 0}, fac_hi[5] = {0, 0, 0, 0, 0};  // factored: G = 2..32 landmark ranges
     int64_t fac_big = 0;  // factored: first landmark with k > 32 (CTA-per-landmark matvec from here)
-    int64_t s64_lo[3] = {0, 0, 0}, s64_hi[3] = {0, 0, 0}, s64_kmax[3] = {2, 2, 2};  // sqrt-BA-64 classes
+    int64_t s64_lo[5] = {0, 0, 0, 0, 0}, s64_hi[5] = {0, 0, 0, 0, 0}, s64_kmax[5] = {2, 2, 2, 2, 2};  // sqrt-BA-64 classes
+    int64_t s64_ilo[5] = {0, 0, 0, 0, 0}, s64_ihi[5] = {0, 0, 0, 0, 0};  // their K2 items in marg_items
+    int64_t s64_plo[5] = {0, 0, 0, 0, 0}, s64_phi[5] = {0, 0, 0, 0, 0};  // their product items
+    int64_t s64_glo[4] = {0, 0, 0, 0}, s64_ghi[4] = {0, 0, 0, 0};  // k <= 32 items by group size 4..32
+    int64_t s64_mlo[4] = {0, 0, 0, 0}, s64_mhi[4] = {0, 0, 0, 0};  // the same as landmark ranges
     int64_t cta_off[5] = {0, 0, 0, 0, 0}, cta_n[5] = {0, 0, 0, 0, 0};    // K4/K5 CTA ranges per class
     int64_t n_chunks = 0, chunk_ctas = 0;
     int64_t n_packs = 0, max_large_k = 0;

@@ -50,14 +50,24 @@ __global__ void __launch_bounds__(256) k_linearize(DevProblem d) {
         load_cam(d.cams, cam, c);
         const double *X = d.pts + 3 * (int64_t)d.obs_lm[i];
         const double2 uv = d.obs_uv[i];
-        const double Pz = cam_model(c, X[0], X[1], X[2], uv.x, uv.y, r, Jc, Jl);
-        if (!(Pz < 0.0)) bad = 1.0;
-        e = robust_rho(r[0] * r[0] + r[1] * r[1], d.huber);
-        apply_irls(r, Jc, Jl, d.huber);
-        float n2[9];
+        if (d.s64) {  // sqrt-BA-64: FP64 Jacobians and FP64 norm sums
+            double Jcd[18], Jld[6];
+            const double Pz = cam_model<double>(c, X[0], X[1], X[2], uv.x, uv.y, r, Jcd, Jld);
+            if (!(Pz < 0.0)) bad = 1.0;
+            e = robust_rho(r[0] * r[0] + r[1] * r[1], d.huber);
+            apply_irls<double>(r, Jcd, Jld, d.huber);
 #pragma unroll
-        for (int q = 0; q < 9; q++) n2[q] = Jc[q] * Jc[q] + Jc[9 + q] * Jc[9 + q];
-        flush_cam12(d.cam_n2, cam, n2);  // camera stride 12, three float4 reductions
+            for (int q = 0; q < 9; q++) atomicAdd(d.cam_n2d + 9 * (int64_t)cam + q, Jcd[q] * Jcd[q] + Jcd[9 + q] * Jcd[9 + q]);
+        } else {
+            const double Pz = cam_model(c, X[0], X[1], X[2], uv.x, uv.y, r, Jc, Jl);
+            if (!(Pz < 0.0)) bad = 1.0;
+            e = robust_rho(r[0] * r[0] + r[1] * r[1], d.huber);
+            apply_irls(r, Jc, Jl, d.huber);
+            float n2[9];
+#pragma unroll
+            for (int q = 0; q < 9; q++) n2[q] = Jc[q] * Jc[q] + Jc[9 + q] * Jc[9 + q];
+            flush_cam12(d.cam_n2, cam, n2);  // camera stride 12, three float4 reductions
+        }
     }
     e = block_sum_d(e, red);
     bad = block_sum_d(bad, red);
@@ -71,10 +81,20 @@ __global__ void k_cam_scale(DevProblem d, float dmin, float dmax) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= 9 * d.n_p) return;
     const int64_t cam = i / 9;
+    if (d.s64) {
+        const double n2 = d.cam_n2d[i];
+        const double s = 1.0 / (1.0 + sqrt(n2));
+        const double D2 = fmin(fmax(n2 * s * s, (double)dmin), (double)dmax);
+        d.sp64[i] = s, d.Dp264[i] = D2;
+        d.sp[i] = (float)s, d.Dp2[i] = (float)D2;
+        return;
+    }
     float n2 = d.cam_n2[12 * cam + (i - 9 * cam)];
     float s = 1.f / (1.f + sqrtf(n2));
     d.sp[i] = s;
     d.Dp2[i] = fminf(fmaxf(n2 * s * s, dmin), dmax);
+    d.sp64[i] = s;
+    d.Dp264[i] = d.Dp2[i];
 }
 
 // ============================================================================ K2 emission
@@ -723,7 +743,7 @@ __global__ void k_precond_finalize(DevProblem d, float lam, double *bad) {
             idx++;
         }
     for (int a = 0; a < 9; a++) {
-        P[a * 9 + a] += (double)lam * d.Dp2[9 * i + a];
+        P[a * 9 + a] += (double)lam * d.Dp264[9 * i + a];
         d.bt[9 * i + a] = acc[45 + a];  // FP64
     }
     double L[81];
@@ -1321,7 +1341,7 @@ __global__ void __launch_bounds__(256) k_reduce_slices(float *__restrict__ sl, i
 __global__ void k_add_damping(DevProblem d, const float *v, float *out, float lam) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= 9 * d.n_p) return;
-    out[i] = (float)(d.wd[i] + (double)lam * d.Dp2[i] * v[i]);
+    out[i] = (float)(d.wd[i] + (double)lam * d.Dp264[i] * v[i]);
 }
 
 // ============================================================================ K6 PCG (single CTA)
@@ -1386,7 +1406,7 @@ __global__ void __launch_bounds__(1024) k_pcg_step(DevProblem d, float lam_f, do
     const int64_t N = 9 * d.n_p;
     double pw = 0.0;
     for (int64_t i = threadIdx.x; i < N; i += blockDim.x) {
-        const double w = d.wd[i] + lam * d.Dp2[i] * d.p[i];
+        const double w = d.wd[i] + lam * d.Dp264[i] * d.p[i];
         d.w[i] = w;
         pw += d.p[i] * w;
     }
@@ -1495,8 +1515,8 @@ __global__ void __launch_bounds__(1024) k_trial_cams(DevProblem d, float lam, in
     double m = 0.0;
     for (int64_t i = threadIdx.x; i < N; i += blockDim.x) {
         const double dp = d.x[i];
-        d.cams_trial[i] = d.cams[i] + (double)d.sp[i] * dp;
-        m += -d.bt[i] * dp + d.r[i] * dp + (double)lam * d.Dp2[i] * dp * dp;
+        d.cams_trial[i] = d.cams[i] + d.sp64[i] * dp;
+        m += -d.bt[i] * dp + d.r[i] * dp + (double)lam * d.Dp264[i] * dp * dp;
     }
     m = block_sum_d(m, red);
     if (threadIdx.x == 0) d.scal[SC_MODELP] = with_model ? m : 0.0;

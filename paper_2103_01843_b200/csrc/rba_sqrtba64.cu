@@ -54,11 +54,16 @@ __device__ __forceinline__ void damp64(const double *R, const double *sD, double
 // Householder on the scaled 2k x 3 landmark Jacobian in shared memory, compact WY, then every row
 // of the block is written from  out[a, 9o+q] = E[a, 9o+q] - V[a] . M_o[:, q]  (rows 0..2k-1), the
 // landmark / residual columns, and the damping rows by the 6 rotations of rows 0..2.
+// Work item = (landmark, rows [r0, r1) of the pose rows 0..2k-1): the O(k) prologue is recomputed
+// per item; the item with r0 == 0 also writes the special rows (0..2, 2k..2k+2) and the Givens.
 template <int NT>
-__global__ void __launch_bounds__(NT) k_marg64(DevProblem d, int64_t lo, double lam, double dmin, double dmax) {
+__global__ void __launch_bounds__(NT, NT == 32 ? 16 : 1) k_marg64(DevProblem d, const LargeItem *__restrict__ items, double lam,
+                                               double dmin, double dmax) {
     extern __shared__ double s64[];
     __shared__ double red[4 * (NT / 32)];
-    const int64_t j = lo + blockIdx.x;
+    const LargeItem it = items[blockIdx.x];
+    const int64_t j = it.lm;
+    const int r0 = it.t0, r1 = it.t1;
     const int k = d.lm_k[j], tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int W = 9 * k + 4;
     double *SX = s64;           // 2k x 3 (scaled J_l, then R / V)
@@ -146,67 +151,91 @@ __global__ void __launch_bounds__(NT) k_marg64(DevProblem d, int64_t lo, double 
     const double sq = sqrt(lam), sD[3] = {sq * Dl[0], sq * Dl[1], sq * Dl[2]};
     damp64(R, sD, g);
     double *B = blk64(d, j);
-    // pose columns of every row: thread <-> camera block o
-    for (int o = tid; o < k; o += NT) {
-        double c[9], r[2], Jc[18], Jl[6], jp[18];
-        const int cam = d.obs_cam[obs0 + o];
-        load_cam(d.cams, cam, c);
-        const double2 uv = d.obs_uv[obs0 + o];
-        cam_model<double>(c, Xp[0], Xp[1], Xp[2], uv.x, uv.y, r, Jc, Jl);
-        apply_irls<double>(r, Jc, Jl, d.huber);
-        for (int q = 0; q < 9; q++) {
-            const double s = d.sp[9 * cam + q];
-            jp[q] = Jc[q] * s, jp[9 + q] = Jc[9 + q] * s;
-        }
-        double M[27];  // M = T^T V_o^T J_o
-        const double *v0 = SV + 6 * o, *v1 = v0 + 3;
-        for (int q = 0; q < 9; q++) {
-            const double W0 = v0[0] * jp[q] + v1[0] * jp[9 + q], W1 = v0[1] * jp[q] + v1[1] * jp[9 + q],
-                         W2 = v0[2] * jp[q] + v1[2] * jp[9 + q];
-            M[q] = T00 * W0;
-            M[9 + q] = T01 * W0 + T11 * W1;
-            M[18 + q] = T02 * W0 + T12 * W1 + T22 * W2;
+    // pose columns of every row: thread <-> camera block o (warp <-> 32 consecutive blocks); each
+    // row's 9 x 32 values of a warp are staged in shared memory and stored as 9 coalesced 256-byte
+    // segments (a thread's own 9 values are 72-byte strided across the warp)
+    double *stage = SV + 6 * k + 288 * warp;  // per-warp 288 doubles
+    for (int ob = 0; ob < k; ob += NT) {
+        const int o = ob + tid;
+        const bool act = o < k;
+        const int wb = ob + 32 * warp;                       // first block of this warp
+        const int ncol = 9 * max(0, min(32, k - wb));        // valid columns of the warp's segment
+        double jp[18] = {}, M[27] = {};
+        if (act) {
+            double c[9], r[2], Jc[18], Jl[6];
+            const int cam = d.obs_cam[obs0 + o];
+            load_cam(d.cams, cam, c);
+            const double2 uv = d.obs_uv[obs0 + o];
+            cam_model<double>(c, Xp[0], Xp[1], Xp[2], uv.x, uv.y, r, Jc, Jl);
+            apply_irls<double>(r, Jc, Jl, d.huber);
+            for (int q = 0; q < 9; q++) {
+                const double sc = d.sp64[9 * cam + q];
+                jp[q] = Jc[q] * sc, jp[9 + q] = Jc[9 + q] * sc;
+            }
+            const double *v0 = SV + 6 * o, *v1 = v0 + 3;  // M = T^T V_o^T J_o
+            for (int q = 0; q < 9; q++) {
+                const double W0 = v0[0] * jp[q] + v1[0] * jp[9 + q], W1 = v0[1] * jp[q] + v1[1] * jp[9 + q],
+                             W2 = v0[2] * jp[q] + v1[2] * jp[9 + q];
+                M[q] = T00 * W0;
+                M[9 + q] = T01 * W0 + T11 * W1;
+                M[18 + q] = T02 * W0 + T12 * W1 + T22 * W2;
+            }
         }
         double top[27];  // undamped rows 0..2, then mixed into rows 0..2 / 2k..2k+2
-        for (int a = 0; a < 2 * k; a++) {
+        for (int a = r0; a < r1; a++) {
             const double *va = SV + 3 * a;
             double row[9];
+#pragma unroll
             for (int q = 0; q < 9; q++) {
                 double x = -(va[0] * M[q] + va[1] * M[9 + q] + va[2] * M[18 + q]);
                 if ((a >> 1) == o) x += jp[9 * (a & 1) + q];
                 row[q] = x;
             }
             if (a < 3) {
+#pragma unroll
                 for (int q = 0; q < 9; q++) top[9 * a + q] = row[q];
-            } else {
-                for (int q = 0; q < 9; q++) B[(int64_t)a * W + 9 * o + q] = row[q];
+                continue;
             }
+#pragma unroll
+            for (int q = 0; q < 9; q++) stage[9 * lane + q] = row[q];
+            __syncwarp();
+            double *dst = B + (int64_t)a * W + 9 * wb;
+            for (int i = lane; i < ncol; i += 32) dst[i] = stage[i];
+            __syncwarp();
         }
-        double x6[6][9];
-        for (int q = 0; q < 9; q++) {
-            double x[6] = {top[q], top[9 + q], top[18 + q], 0.0, 0.0, 0.0};
-            for (int m = 0; m < 6; m++) {
-                const int p = damp_p(m), t = damp_t(m);
-                const double a = x[p], b = x[t];
-                x[p] = g[2 * m] * a + g[2 * m + 1] * b;
-                x[t] = -g[2 * m + 1] * a + g[2 * m] * b;
+        if (r0 != 0) continue;
+        for (int s = 0; s < 6; s++) {  // the damped special rows from rows 0..2 (staged the same way)
+            double xs[9];
+#pragma unroll
+            for (int q = 0; q < 9; q++) {
+                double x[6] = {top[q], top[9 + q], top[18 + q], 0.0, 0.0, 0.0};
+#pragma unroll
+                for (int m = 0; m < 6; m++) {
+                    const int p = damp_p(m), t = damp_t(m);
+                    const double aa = x[p], bb = x[t];
+                    x[p] = g[2 * m] * aa + g[2 * m + 1] * bb;
+                    x[t] = -g[2 * m + 1] * aa + g[2 * m] * bb;
+                }
+                xs[q] = x[s];
             }
-            for (int s = 0; s < 6; s++) x6[s][q] = x[s];
-        }
-        for (int s = 0; s < 6; s++) {
+#pragma unroll
+            for (int q = 0; q < 9; q++) stage[9 * lane + q] = xs[q];
+            __syncwarp();
             const int row = s < 3 ? s : 2 * k + s - 3;
-            for (int q = 0; q < 9; q++) B[(int64_t)row * W + 9 * o + q] = x6[s][q];
+            double *dst = B + (int64_t)row * W + 9 * wb;
+            for (int i = lane; i < ncol; i += 32) dst[i] = stage[i];
+            __syncwarp();
         }
     }
     // landmark and residual columns (4 per row): R / 0 and Q^T r, damping rows rotated
-    for (int a = tid; a < 2 * k + 3; a += NT) {
+    for (int a = r0 + tid; a < r1; a += NT) {
         double *rw = B + (int64_t)a * W + 9 * k;
         if (a >= 3 && a < 2 * k) {
             rw[0] = rw[1] = rw[2] = 0.0;
             rw[3] = SR[a];
         }
     }
-    if (tid == 0) {
+    if (tid == 0 && r0 == 0) {
         double X[6][4] = {};
         for (int i = 0; i < 3; i++) {
             for (int q = 0; q < 3; q++) X[i][q] = R[3 * i + q];
@@ -229,11 +258,209 @@ __global__ void __launch_bounds__(NT) k_marg64(DevProblem d, int64_t lo, double 
         double *G = B + (int64_t)(2 * k + 3) * W;
         for (int i = 0; i < 12; i++) G[i] = g[i];
     }
-    if (tid < 3) {
+    if (tid < 3 && r0 == 0) {
         d.lm_s[3 * j + tid] = (float)sl[tid];
         d.lm_D[3 * j + tid] = (float)Dl[tid];
         d.lm_D64[3 * j + tid] = Dl[tid];
         d.lm_s64[3 * j + tid] = sl[tid];
+    }
+}
+
+// ---- K2-64 for short tracks (k <= 32): a group of G lanes per landmark (32/G landmarks per warp),
+// lane <-> observation / camera block, the Householder reductions as G-lane shuffles (the FP64 port
+// of the FP32 small-k kernel's prologue), V rows of other lanes fetched by shuffles row by row.
+template <int G>
+__device__ __forceinline__ double gsum64(double v) {
+#pragma unroll
+    for (int m = G / 2; m; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m, G);
+    return v;
+}
+
+template <int G>
+__global__ void __launch_bounds__(256) k_marg64_small(DevProblem d, int64_t lo, int64_t hi, double lam, double dmin,
+                                                      double dmax) {
+    const int lane = threadIdx.x & 31, gl = lane % G;
+    const int64_t wfirst = lo + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * (32 / G);
+    if (wfirst >= hi) return;  // warp-uniform
+    const int64_t j = wfirst + lane / G;
+    const bool valid = j < hi;
+    const int k = valid ? d.lm_k[j] : 0;
+    const bool act = gl < k;
+    double r[2] = {0.0, 0.0}, Jc[18] = {}, Jl[6] = {};
+    int cam = 0;
+    if (act) {
+        const int64_t o = d.lm_obs0[j] + gl;
+        cam = d.obs_cam[o];
+        double c[9];
+        load_cam(d.cams, cam, c);
+        const double *Xp = d.pts + 3 * j;
+        const double2 uv = d.obs_uv[o];
+        cam_model<double>(c, Xp[0], Xp[1], Xp[2], uv.x, uv.y, r, Jc, Jl);
+        apply_irls<double>(r, Jc, Jl, d.huber);
+    }
+    double sl[3], Dl[3];
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+        const double n2 = gsum64<G>(Jl[q] * Jl[q] + Jl[3 + q] * Jl[3 + q]);
+        sl[q] = 1.0 / (1.0 + sqrt(n2));
+        Dl[q] = sqrt(fmin(fmax(n2 * sl[q] * sl[q], dmin), dmax));
+    }
+    double jp[18], X[2][3], rv[2] = {r[0], r[1]};
+#pragma unroll
+    for (int q = 0; q < 9; q++) {
+        const double sc = act ? d.sp64[9 * cam + q] : 0.0;
+        jp[q] = Jc[q] * sc, jp[9 + q] = Jc[9 + q] * sc;
+    }
+#pragma unroll
+    for (int q = 0; q < 3; q++) X[0][q] = Jl[q] * sl[q], X[1][q] = Jl[3 + q] * sl[q];
+    double V[2][3], tau[3];
+#pragma unroll
+    for (int c = 0; c < 3; c++) {  // reflector c (reading C4 for the sign)
+        double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+#pragma unroll
+        for (int rr = 0; rr < 2; rr++) {
+            const int a = 2 * gl + rr;
+            const double x = (act && a >= c) ? X[rr][c] : 0.0;
+            s0 += x * x;
+            if (c + 1 < 3) s1 += x * X[rr][(c + 1) % 3];
+            if (c + 2 < 3) s2 += x * X[rr][(c + 2) % 3];
+            s3 += x * rv[rr];
+        }
+        s0 = gsum64<G>(s0), s1 = gsum64<G>(s1), s2 = gsum64<G>(s2), s3 = gsum64<G>(s3);
+        const int pl = c >> 1, pr = c & 1;
+        const double x0 = __shfl_sync(0xffffffffu, X[pr][c], pl, G);
+        const double y1 = __shfl_sync(0xffffffffu, X[pr][(c + 1) % 3], pl, G);
+        const double y2 = __shfl_sync(0xffffffffu, X[pr][(c + 2) % 3], pl, G);
+        const double yr = __shfl_sync(0xffffffffu, rv[pr], pl, G);
+        const double sig = sqrt(s0), alpha = x0 >= 0.0 ? -sig : sig;
+        const double vtv = 2.0 * sig * (sig + fabs(x0));
+        const double tc = vtv > 0.0 ? 2.0 / vtv : 0.0;
+        tau[c] = tc;
+        const double d1 = s1 - alpha * y1, d2 = s2 - alpha * y2, dr = s3 - alpha * yr;
+#pragma unroll
+        for (int rr = 0; rr < 2; rr++) {
+            const int a = 2 * gl + rr;
+            double vv = 0.0;
+            if (act && a >= c) vv = a == c ? x0 - alpha : X[rr][c];
+            V[rr][c] = vv;
+            if (c + 1 < 3) X[rr][(c + 1) % 3] -= tc * vv * d1;
+            if (c + 2 < 3) X[rr][(c + 2) % 3] -= tc * vv * d2;
+            rv[rr] -= tc * vv * dr;
+            if (a == c) X[rr][c] = alpha;
+            else if (a > c) X[rr][c] = 0.0;
+        }
+    }
+    double p01 = 0, p02 = 0, p12 = 0;
+#pragma unroll
+    for (int rr = 0; rr < 2; rr++) p01 += V[rr][0] * V[rr][1], p02 += V[rr][0] * V[rr][2], p12 += V[rr][1] * V[rr][2];
+    p01 = gsum64<G>(p01), p02 = gsum64<G>(p02), p12 = gsum64<G>(p12);
+    const double T00 = tau[0], T11 = tau[1], T22 = tau[2];
+    const double T01 = -tau[1] * T00 * p01;
+    const double T02 = -tau[2] * (T00 * p02 + T01 * p12);
+    const double T12 = -tau[2] * T11 * p12;
+    double R[9], rr3[3];
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+        R[q] = __shfl_sync(0xffffffffu, X[0][q], 0, G);
+        R[3 + q] = __shfl_sync(0xffffffffu, X[1][q], 0, G);
+        R[6 + q] = __shfl_sync(0xffffffffu, X[0][q], 1, G);
+    }
+    rr3[0] = __shfl_sync(0xffffffffu, rv[0], 0, G);
+    rr3[1] = __shfl_sync(0xffffffffu, rv[1], 0, G);
+    rr3[2] = __shfl_sync(0xffffffffu, rv[0], 1, G);
+    const double sq = sqrt(lam), sD[3] = {sq * Dl[0], sq * Dl[1], sq * Dl[2]};
+    double g[12];
+    damp64(R, sD, g);
+    double M[27];  // own block: M = T^T V_o^T J_o
+#pragma unroll
+    for (int q = 0; q < 9; q++) {
+        const double W0 = V[0][0] * jp[q] + V[1][0] * jp[9 + q], W1 = V[0][1] * jp[q] + V[1][1] * jp[9 + q],
+                     W2 = V[0][2] * jp[q] + V[1][2] * jp[9 + q];
+        M[q] = T00 * W0;
+        M[9 + q] = T01 * W0 + T11 * W1;
+        M[18 + q] = T02 * W0 + T12 * W1 + T22 * W2;
+    }
+    const int W = 9 * k + 4;
+    double *Bk = valid ? blk64(d, j) : nullptr;
+    double top[27];
+    for (int a = 0; a < 64; a++) {  // rows 0..2k-1 (V row a from lane a / 2), warp-uniform bound
+        double va[3];
+#pragma unroll
+        for (int q = 0; q < 3; q++) {
+            const double x0 = __shfl_sync(0xffffffffu, V[0][q], (a >> 1) % G, G);
+            const double x1 = __shfl_sync(0xffffffffu, V[1][q], (a >> 1) % G, G);
+            va[q] = (a & 1) ? x1 : x0;
+        }
+        if (a >= 2 * k || !act) continue;
+        double row[9];
+#pragma unroll
+        for (int q = 0; q < 9; q++) {
+            double x = -(va[0] * M[q] + va[1] * M[9 + q] + va[2] * M[18 + q]);
+            if ((a >> 1) == gl) x += jp[9 * (a & 1) + q];
+            row[q] = x;
+        }
+        if (a < 3) {
+#pragma unroll
+            for (int q = 0; q < 9; q++) top[9 * a + q] = row[q];
+        } else {
+#pragma unroll
+            for (int q = 0; q < 9; q++) Bk[(int64_t)a * W + 9 * gl + q] = row[q];
+        }
+    }
+    if (!act) return;
+#pragma unroll
+    for (int sr = 0; sr < 6; sr++) {
+        const int row = sr < 3 ? sr : 2 * k + sr - 3;
+#pragma unroll
+        for (int q = 0; q < 9; q++) {
+            double x[6] = {top[q], top[9 + q], top[18 + q], 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int m = 0; m < 6; m++) {
+                const int p = damp_p(m), t = damp_t(m);
+                const double aa = x[p], bb = x[t];
+                x[p] = g[2 * m] * aa + g[2 * m + 1] * bb;
+                x[t] = -g[2 * m + 1] * aa + g[2 * m] * bb;
+            }
+            Bk[(int64_t)row * W + 9 * gl + q] = x[sr];
+        }
+    }
+#pragma unroll
+    for (int rr = 0; rr < 2; rr++) {  // landmark / residual columns of the lane's rows >= 3
+        const int a = 2 * gl + rr;
+        if (a >= 3) {
+            double *rw = Bk + (int64_t)a * W + 9 * k;
+            rw[0] = rw[1] = rw[2] = 0.0;
+            rw[3] = rv[rr];
+        }
+    }
+    if (gl == 0) {
+        double Xs[6][4] = {};
+        for (int i = 0; i < 3; i++) {
+            for (int q = 0; q < 3; q++) Xs[i][q] = R[3 * i + q];
+            Xs[i][3] = rr3[i];
+            Xs[3 + i][i] = sD[i];
+        }
+        for (int m = 0; m < 6; m++) {
+            const int p = damp_p(m), t = damp_t(m);
+            for (int q = 0; q < 4; q++) {
+                const double aa = Xs[p][q], bb = Xs[t][q];
+                Xs[p][q] = g[2 * m] * aa + g[2 * m + 1] * bb;
+                Xs[t][q] = -g[2 * m + 1] * aa + g[2 * m] * bb;
+            }
+            Xs[t][p] = 0.0;
+        }
+        for (int sr = 0; sr < 6; sr++) {
+            const int row = sr < 3 ? sr : 2 * k + sr - 3;
+            for (int q = 0; q < 4; q++) Bk[(int64_t)row * W + 9 * k + q] = Xs[sr][q];
+        }
+        double *Gp = Bk + (int64_t)(2 * k + 3) * W;
+        for (int i = 0; i < 12; i++) Gp[i] = g[i];
+        for (int q = 0; q < 3; q++) {
+            d.lm_s[3 * j + q] = (float)sl[q];
+            d.lm_D[3 * j + q] = (float)Dl[q];
+            d.lm_s64[3 * j + q] = sl[q];
+            d.lm_D64[3 * j + q] = Dl[q];
+        }
     }
 }
 
@@ -297,22 +524,69 @@ __global__ void __launch_bounds__(256) k_redamp64(DevProblem d, double lam) {
     }
 }
 
+// ---- K5-64 for short tracks (k <= 32): a group of G lanes (G | 32) per landmark, 32/G landmarks
+// per warp, lane <-> camera block; rows looped to the warp's longest landmark so the G-wide
+// shuffles always see every lane.  One item (all reduced rows) per landmark.
+template <int G>
+__global__ void __launch_bounds__(256) k_rcs64_small(DevProblem d, const LargeItem *__restrict__ items, int64_t n_items,
+                                                     const double *__restrict__ v, const PcgState *__restrict__ st) {
+    if (st && st->done) return;
+    const int lane = threadIdx.x & 31, gl = lane % G;
+    const int64_t idx = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+    const bool valid = idx < n_items;
+    LargeItem it{0, 0, 0, 0};
+    if (valid) it = items[idx];
+    const int64_t j = it.lm;
+    const int k = valid ? d.lm_k[j] : 0;
+    const bool act = gl < k;
+    const int W = 9 * k + 4;
+    const double *B = valid ? blk64(d, j) : nullptr;
+    const int32_t *oc = d.obs_cam + (valid ? d.lm_obs0[j] : 0);
+    double vo[9], acc[9];
+#pragma unroll
+    for (int q = 0; q < 9; q++) vo[q] = act ? v[9 * (int64_t)oc[gl] + q] : 0.0, acc[q] = 0.0;
+    const int nrows = valid ? it.t1 - it.t0 : 0;
+    int maxrows = nrows;
+#pragma unroll
+    for (int m = 16; m; m >>= 1) maxrows = max(maxrows, __shfl_xor_sync(0xffffffffu, maxrows, m));
+    for (int r = 0; r < maxrows; r++) {
+        double x[9];
+        const bool live = act && r < nrows;
+        const double *rw = live ? B + (int64_t)(it.t0 + r) * W + 9 * gl : nullptr;
+#pragma unroll
+        for (int q = 0; q < 9; q++) x[q] = live ? rw[q] : 0.0;
+        double y = 0.0;
+#pragma unroll
+        for (int q = 0; q < 9; q++) y += x[q] * vo[q];
+#pragma unroll
+        for (int m = G / 2; m; m >>= 1) y += __shfl_xor_sync(0xffffffffu, y, m, G);
+#pragma unroll
+        for (int q = 0; q < 9; q++) acc[q] += x[q] * y;
+    }
+    if (act) {
+        double *out = d.wd + 9 * (int64_t)oc[gl];
+#pragma unroll
+        for (int q = 0; q < 9; q++) atomicAdd(out + q, acc[q]);
+    }
+}
+
 // ---- K4-64 / K5-64: CTA per landmark, rows 3..2k+2 of the block (the reduced rows A_j, q_j).
 // Product: per chunk of 8 rows, warps compute y_a = A[a] . v (lanes over columns, coalesced),
 // then thread <-> camera block accumulates out_o += A[a, block o]^T y_a (re-read from L1).
 template <int NT, int NB, bool PRE>
-__global__ void __launch_bounds__(NT) k_rcs64(DevProblem d, int64_t lo, const double *__restrict__ v,
-                                              const PcgState *__restrict__ st) {
+__global__ void __launch_bounds__(NT) k_rcs64(DevProblem d, const LargeItem *__restrict__ items,
+                                              const double *__restrict__ v, const PcgState *__restrict__ st) {
     if (!PRE && st && st->done) return;
     // NB: camera blocks per thread (k <= NB * NT in this class)
-    const int64_t j = lo + blockIdx.x;
+    const LargeItem it = items[blockIdx.x];  // rows [it.t0, it.t1) of the reduced rows 3..2k+2
+    const int64_t j = it.lm;
     const int k = d.lm_k[j], W = 9 * k + 4, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const double *B = blk64(d, j);
     const int32_t *oc = d.obs_cam + d.lm_obs0[j];
     if (PRE) {
         for (int o = tid; o < k; o += NT) {
             double P[45] = {}, b[9] = {};
-            for (int a = 3; a < 2 * k + 3; a++) {
+            for (int a = it.t0; a < it.t1; a++) {
                 const double *rw = B + (int64_t)a * W;
                 double x[9];
                 for (int q = 0; q < 9; q++) x[q] = rw[9 * o + q];
@@ -329,10 +603,11 @@ __global__ void __launch_bounds__(NT) k_rcs64(DevProblem d, int64_t lo, const do
         }
         return;
     }
-    // thread <-> camera blocks o = tid + m NT (m < NB): its v_o in registers; per chunk of 8 rows the
-    // 8 partial dot products over its blocks are reduced across the CTA (warp shuffles, + smem for
-    // NT > 32), then out_o += A[a, o]^T y_a re-reads its 8 x 9 row segments from L1
-    __shared__ double part[8][NT / 32];
+    // thread <-> camera blocks o = tid + m NT (m < NB): its v_o in registers; per chunk of CR rows the
+    // partial dot products over its blocks are reduced across the CTA (warp shuffles, + smem for
+    // NT > 32), then out_o += A[a, o]^T y_a re-reads its row segments (L1 hits)
+    constexpr int CR = NB == 1 ? 8 : (NB == 2 ? 4 : 2);  // rows per chunk (register budget)
+    __shared__ double part[CR][NT / 32];
     double acc[NB][9], vo[NB][9];
 #pragma unroll
     for (int m = 0; m < NB; m++) {
@@ -343,11 +618,11 @@ __global__ void __launch_bounds__(NT) k_rcs64(DevProblem d, int64_t lo, const do
             vo[m][q] = o < k ? v[9 * (int64_t)oc[o] + q] : 0.0;
         }
     }
-    for (int a0 = 3; a0 < 2 * k + 3; a0 += 8) {
-        const int nr = min(8, 2 * k + 3 - a0);
-        double y[8];
+    for (int a0 = it.t0; a0 < it.t1; a0 += CR) {
+        const int nr = min(CR, it.t1 - a0);
+        double y[CR];
 #pragma unroll
-        for (int r = 0; r < 8; r++) {
+        for (int r = 0; r < CR; r++) {
             double s = 0.0;
             if (r < nr) {
                 const double *rw = B + (int64_t)(a0 + r) * W;
@@ -364,10 +639,10 @@ __global__ void __launch_bounds__(NT) k_rcs64(DevProblem d, int64_t lo, const do
         if (NT > 32) {
             if (lane == 0)
 #pragma unroll
-                for (int r = 0; r < 8; r++) part[r][warp] = y[r];
+                for (int r = 0; r < CR; r++) part[r][warp] = y[r];
             __syncthreads();
 #pragma unroll
-            for (int r = 0; r < 8; r++) {
+            for (int r = 0; r < CR; r++) {
                 double t = 0.0;
 #pragma unroll
                 for (int w = 0; w < NT / 32; w++) t += part[r][w];
@@ -380,7 +655,7 @@ __global__ void __launch_bounds__(NT) k_rcs64(DevProblem d, int64_t lo, const do
             const int o = tid + m * NT;
             if (o < k) {
 #pragma unroll
-                for (int r = 0; r < 8; r++) {
+                for (int r = 0; r < CR; r++) {
                     if (r < nr) {
                         const double *rw = B + (int64_t)(a0 + r) * W + 9 * o;
 #pragma unroll
@@ -453,19 +728,33 @@ void launch_f2d64(rba_ctx *c, const float *a, double *b, int64_t n) {
 
 template <int NT>
 static void marg64_cls(rba_ctx *c, int cls, double lam) {
-    const int64_t lo = c->s64_lo[cls], hi = c->s64_hi[cls];
+    const int64_t lo = c->s64_ilo[cls], hi = c->s64_ihi[cls];
     if (hi <= lo) return;
-    const size_t sm = sizeof(double) * 14 * (size_t)c->s64_kmax[cls];  // SX 6k | SR 2k | SV 6k
+    const size_t sm = sizeof(double) * (14 * (size_t)c->s64_kmax[cls] + 288 * (NT / 32));  // SX | SR | SV | stage
     cudaFuncSetAttribute(k_marg64<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_marg64<NT><<<(unsigned)(hi - lo), NT, sm, c->stream>>>(c->d, lo, lam, c->opt.diag_min, c->opt.diag_max);
+    k_marg64<NT><<<(unsigned)(hi - lo), NT, sm, c->stream>>>(c->d, c->d.marg_items + lo, lam, c->opt.diag_min,
+                                                            c->opt.diag_max);
     c->launches++;
 }
 
 cudaError_t launch_marg64(rba_ctx *c, double lam) {
     Prof P(c, KID_MARG, c->marg_bytes);
-    marg64_cls<32>(c, 0, lam);
+    for (int g = 0; g < 4; g++) {  // k <= 32: grouped kernel by group size 4 / 8 / 16 / 32
+        const int64_t lo = c->s64_mlo[g], hi = c->s64_mhi[g];
+        if (hi <= lo) continue;
+        const int G = 4 << g;
+        const unsigned blocks = nb64((hi - lo) * G, 256);
+        const double dmin = c->opt.diag_min, dmax = c->opt.diag_max;
+        if (g == 0) k_marg64_small<4><<<blocks, 256, 0, c->stream>>>(c->d, lo, hi, lam, dmin, dmax);
+        else if (g == 1) k_marg64_small<8><<<blocks, 256, 0, c->stream>>>(c->d, lo, hi, lam, dmin, dmax);
+        else if (g == 2) k_marg64_small<16><<<blocks, 256, 0, c->stream>>>(c->d, lo, hi, lam, dmin, dmax);
+        else k_marg64_small<32><<<blocks, 256, 0, c->stream>>>(c->d, lo, hi, lam, dmin, dmax);
+        c->launches++;
+    }
     marg64_cls<128>(c, 1, lam);
     marg64_cls<256>(c, 2, lam);
+    marg64_cls<256>(c, 3, lam);
+    marg64_cls<256>(c, 4, lam);
     P.end();
     return cudaGetLastError();
 }
@@ -481,25 +770,40 @@ cudaError_t launch_redamp64(rba_ctx *c, double lam) {
 
 template <int NT, int NB, bool PRE>
 static void rcs64_cls(rba_ctx *c, int cls, const double *v, const PcgState *st) {
-    const int64_t lo = c->s64_lo[cls], hi = c->s64_hi[cls];
+    const int64_t lo = c->s64_plo[cls], hi = c->s64_phi[cls];
     if (hi <= lo) return;
-    k_rcs64<NT, NB, PRE><<<(unsigned)(hi - lo), NT, 0, c->stream>>>(c->d, lo, v, st);
+    k_rcs64<NT, NB, PRE><<<(unsigned)(hi - lo), NT, 0, c->stream>>>(c->d, c->d.rcs_items + lo, v, st);
     c->launches++;
 }
 
 // wd = sum_j A_j^T A_j v (FP64 atomics; wd zeroed here)
 void launch_rcs64(rba_ctx *c, const double *v, const PcgState *st) {
     cudaMemsetAsync(c->d.wd, 0, sizeof(double) * 9 * c->d.n_p, c->stream);
-    rcs64_cls<32, 1, false>(c, 0, v, st);
+    for (int g = 0; g < 4; g++) {  // k <= 32 by group size 4 / 8 / 16 / 32
+        const int64_t lo = c->s64_glo[g], hi = c->s64_ghi[g];
+        if (hi <= lo) continue;
+        const int G = 4 << g;
+        const unsigned blocks = nb64((hi - lo) * G, 256);
+        const LargeItem *itp = c->d.rcs_items + lo;
+        if (g == 0) k_rcs64_small<4><<<blocks, 256, 0, c->stream>>>(c->d, itp, hi - lo, v, st);
+        else if (g == 1) k_rcs64_small<8><<<blocks, 256, 0, c->stream>>>(c->d, itp, hi - lo, v, st);
+        else if (g == 2) k_rcs64_small<16><<<blocks, 256, 0, c->stream>>>(c->d, itp, hi - lo, v, st);
+        else k_rcs64_small<32><<<blocks, 256, 0, c->stream>>>(c->d, itp, hi - lo, v, st);
+        c->launches++;
+    }
     rcs64_cls<128, 1, false>(c, 1, v, st);
-    rcs64_cls<256, KMAX64 / 256, false>(c, 2, v, st);
+    rcs64_cls<256, 1, false>(c, 2, v, st);
+    rcs64_cls<256, 2, false>(c, 3, v, st);
+    rcs64_cls<256, KMAX64 / 256, false>(c, 4, v, st);
 }
 
 void launch_pre64(rba_ctx *c) {
     cudaMemsetAsync(c->d.pd, 0, sizeof(double) * 54 * c->d.n_p, c->stream);
     rcs64_cls<32, 1, true>(c, 0, nullptr, nullptr);
     rcs64_cls<128, 1, true>(c, 1, nullptr, nullptr);
-    rcs64_cls<256, KMAX64 / 256, true>(c, 2, nullptr, nullptr);
+    rcs64_cls<256, 1, true>(c, 2, nullptr, nullptr);
+    rcs64_cls<256, 2, true>(c, 3, nullptr, nullptr);
+    rcs64_cls<256, KMAX64 / 256, true>(c, 4, nullptr, nullptr);
 }
 
 cudaError_t launch_backsub64(rba_ctx *c, float lam) {

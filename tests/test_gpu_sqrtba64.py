@@ -1,7 +1,7 @@
 """GPU parity of sqrt-BA-64 (the paper's double-precision variant) against
-the FP64 oracle.  Blocks, QR, damping, reduced system, PCG vectors and back-substitution are FP64;
-the column scaling S and the damping diagonals D^2 are the FP32 values K1 produces for both
-precisions, so agreement is bounded by FP32 rounding of S (~1e-7), not by the FP64 arithmetic."""
+the FP64 oracle.  Jacobians, column scaling, blocks, QR, damping, reduced system, PCG vectors and
+back-substitution are all FP64, so the bars are FP64 rounding levels (the rba_matvec test hook
+returns FP32 vectors: columns of H~ read through it are bounded by FP32 output rounding)."""
 import numpy as np
 import pytest
 
@@ -45,14 +45,14 @@ def test_sqrtba64_reduced_system_and_blocks(lam):
     H, b = o.reduced_dense()
     N = 9 * o.n_p
     Hg = np.stack([_mv(s, np.eye(N)[i]) for i in range(N)], 1)
-    assert relf(Hg, H) <= 1e-6
+    assert relf(Hg, H) <= 1e-7
     for j in range(0, 200, 13):
         k = o.track_length(j)
         Bg, Bo = s.block(j), o.block(j)
         assert np.all(Bg[3:, 9 * k:9 * k + 3] == 0.0)
-        assert relf(Bg.T @ Bg, Bo.T @ Bo) <= 1e-6  # rotation invariant (reading C16)
+        assert relf(Bg.T @ Bg, Bo.T @ Bo) <= 1e-12  # rotation invariant (reading C16)
     s.pcg()
-    assert relf(s.rhs(), b) <= 1e-6
+    assert relf(s.rhs(), b) <= 1e-11
 
 
 def test_sqrtba64_redamp_and_long_tracks():
@@ -69,7 +69,7 @@ def test_sqrtba64_redamp_and_long_tracks():
         assert relf(_mv(s, v), o.matvec(v)) <= 1e-6
     for j, k in enumerate(ks[:7]):
         Bg, Bo = s.block(j), o.block(j)
-        assert relf(Bg.T @ Bg, Bo.T @ Bo) <= 1e-6
+        assert relf(Bg.T @ Bg, Bo.T @ Bo) <= 1e-11
 
 
 @pytest.mark.parametrize("cfg", [1, 2])
@@ -86,14 +86,14 @@ def test_sqrtba64_pcg_backsub_lm(cfg):
     s.backsub()
     o.backsub()
     dp, dl = s.step()
-    assert relf(dp, o.dp()) <= 1e-5
-    assert relf(dl, o.dl()) <= 1e-5
+    assert relf(dp, o.dp()) <= 1e-8
+    assert relf(dl, o.dl()) <= 1e-7  # dl is exported through the shared FP32 buffer
     s.close()
     s = _solver(p)
     o = oracle.Oracle(p)
     for i in range(5):
         rg, ro = s.lm_step(), o.lm_step()
-        assert abs(rg["cost_after"] - ro["cost_after"]) <= 1e-6 * ro["cost_after"], (i, rg, ro)
+        assert abs(rg["cost_after"] - ro["cost_after"]) <= 1e-10 * ro["cost_after"], (i, rg, ro)
 
 
 def test_sqrtba64_more_accurate_than_32():

@@ -15,9 +15,11 @@ ap.add_argument("--config", type=int, default=4)
 ap.add_argument("--matvecs", type=int, default=2)
 ap.add_argument("--storage", type=int, default=0)
 ap.add_argument("--solver", type=int, default=0)
+ap.add_argument("--precision", type=int, default=0)
 args = ap.parse_args()
 p = synth.make_problem(args.config)
-s = rba.Solver(p, pcg_max_iters=args.matvecs, pcg_rel_tol=0.0, storage=args.storage, solver=args.solver)
+s = rba.Solver(p, pcg_max_iters=args.matvecs, pcg_rel_tol=0.0, storage=args.storage, solver=args.solver,
+               precision=args.precision)
 s.linearize()
 s.marginalize(1e-4)
 st = s.pcg()
