@@ -399,7 +399,7 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     const int ntb[6] = {32, 64, 128, 256, 512, KMAX};
     static const int64_t marg_item_floats =
         getenv("RBA_MARG_ITEM_FLOATS") ? atoll(getenv("RBA_MARG_ITEM_FLOATS")) : 1048576;  // 4 MB of output per item (measured: 3.91 -> 3.34 ms on cfg4 vs 1 MB)
-    std::vector<HugeItem> huge_y, huge_out;
+    std::vector<HugeItem> huge_y, huge_out, huge_fused;
     int64_t ybuf_n = 0;
     const int64_t large_lo = pos;
     for (int64_t i = pos; i < nl; i++) {
@@ -430,6 +430,8 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
                 for (int o0 = 0; o0 < k; o0 += HUGE_NT)
                     for (int t0 = 0; t0 < T; t0 += tpo)
                         huge_out.push_back(HugeItem{(int32_t)i, o0, t0, std::min(T, t0 + tpo), ybuf_n});
+                const int tpf = std::max(1, (1 << 20) / (144 * k));
+                for (int t0 = 0; t0 < T; t0 += tpf) huge_fused.push_back(HugeItem{(int32_t)i, 0, t0, std::min(T, t0 + tpf), 0});
                 ybuf_n += 4 * (int64_t)T;
                 continue;
             }
@@ -664,6 +666,8 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     CKSC(dalloc_n(c, &d.chunk_lo, std::max<size_t>(1, chunk_lo.size())));
     c->n_huge_y = (int64_t)huge_y.size();
     c->n_huge_out = (int64_t)huge_out.size();
+    c->n_huge_fused = (int64_t)huge_fused.size();
+    CKSC(dalloc_n(c, &d.huge_fused, std::max<size_t>(1, huge_fused.size())));
     CKSC(dalloc_n(c, &d.huge_y, std::max<size_t>(1, huge_y.size())));
     CKSC(dalloc_n(c, &d.huge_out, std::max<size_t>(1, huge_out.size())));
     CKSC(dalloc_n(c, &d.ybuf, std::max<int64_t>(4, ybuf_n)));
@@ -713,6 +717,9 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
         if (!huge_y.empty())
             CKC(cudaMemcpyAsync(d.huge_y, huge_y.data(), sizeof(HugeItem) * huge_y.size(), cudaMemcpyHostToDevice,
                                 c->stream));
+        if (!huge_fused.empty())
+            CKC(cudaMemcpyAsync(d.huge_fused, huge_fused.data(), sizeof(HugeItem) * huge_fused.size(),
+                                cudaMemcpyHostToDevice, c->stream));
         if (!huge_out.empty())
             CKC(cudaMemcpyAsync(d.huge_out, huge_out.data(), sizeof(HugeItem) * huge_out.size(),
                                 cudaMemcpyHostToDevice, c->stream));

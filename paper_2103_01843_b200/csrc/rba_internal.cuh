@@ -145,6 +145,7 @@ struct DevProblem {
     int64_t *chunk_lo;      // tile-range boundaries of the persistent CTAs over the chunks
     int64_t *cta_lo;        // per class: tile range boundaries of the persistent CTAs (bytes-balanced)
     HugeItem *huge_y, *huge_out;  // k > KLARGE: y-pass items (one per tile), out/precond items
+    HugeItem *huge_fused;         // k > KLARGE: fused-product items (landmark, ~1 MB tile range)
     float *ybuf;                  // k > KLARGE: y = A v, 4 floats per 4-row tile
     // explicit Schur-complement baseline (f3, rba_sc.cu): sc = 0 off (sqrt-BA), 1 FP32, 2 FP64
     int sc;
@@ -192,6 +193,7 @@ struct rba_ctx {
     int64_t pack_lo[4] = {0, 0, 0, 0}, pack_hi[4] = {0, 0, 0, 0};  // G = 2, 4, 8, 16 pack ranges
     int64_t marg_lo[6] = {0, 0, 0, 0, 0, 0}, marg_hi[6] = {0, 0, 0, 0, 0, 0};  // K2 large items per class
     int64_t n_huge_y = 0, n_huge_out = 0, huge_max_k = 0;  // k > KLARGE (two-pass matvec)
+    int64_t n_huge_fused = 0;
     int64_t fac_lo[5] = {0, 0, 0, 0, 0}, fac_hi[5] = {0, 0, 0, 0, 0};  // factored: G = 2..32 landmark ranges
     int64_t fac_big = 0;  // factored: first landmark with k > 32 (CTA-per-landmark matvec from here)
     int64_t s64_lo[5] = {0, 0, 0, 0, 0}, s64_hi[5] = {0, 0, 0, 0, 0}, s64_kmax[5] = {2, 2, 2, 2, 2};  // sqrt-BA-64 classes

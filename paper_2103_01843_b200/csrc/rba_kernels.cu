@@ -1259,6 +1259,77 @@ __global__ void __launch_bounds__(HUGE_NT) k_huge_y(DevProblem d, const float *_
     if (threadIdx.x == 0) reinterpret_cast<float4 *>(d.ybuf + it.yoff)[t] = make_float4(y[0], y[1], y[2], y[3]);
 }
 
+// Fused variant of the two passes: CTA per (landmark, tile range), thread <-> camera blocks
+// o = tid + m HUGE_FNT (m < HUGE_NB); per tile the y partials from the tile's slabs (HBM), a CTA
+// reduction, then out_o += slab^T y from a second read of the same tile, which L2 still holds (a
+// tile is <= 144 KMAX = 442 KB), so HBM sees each tile once.
+constexpr int HUGE_FNT = 512, HUGE_NB = (KMAX + HUGE_FNT - 1) / HUGE_FNT;
+__global__ void __launch_bounds__(HUGE_FNT, 1) k_huge_fused(DevProblem d, const HugeItem *__restrict__ items,
+                                                            const float *__restrict__ v,
+                                                            const PcgState *__restrict__ st) {
+    if (st && st->done) return;
+    __shared__ float red[32 * 4];
+    const HugeItem it = items[blockIdx.x];
+    const int64_t j = it.lm;
+    const int k = d.lm_k[j], tid = threadIdx.x;
+    const float *R2 = d.arena + d.lm_r2[j];
+    const int32_t *oc = d.obs_cam + d.lm_obs0[j];
+    float acc[HUGE_NB][9];
+#pragma unroll
+    for (int m = 0; m < HUGE_NB; m++)
+#pragma unroll
+        for (int q = 0; q < 9; q++) acc[m][q] = 0.f;
+    for (int t = it.t0; t < it.t1; t++) {
+        float y[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int m = 0; m < HUGE_NB; m++) {
+            const int o = tid + m * HUGE_FNT;
+            if (o < k) {
+                const int g = o >> 5, ng = min(32, k - 32 * g);
+                const float4 *S4 = reinterpret_cast<const float4 *>(R2 + (int64_t)36 * k * t + 36 * 32 * g) + (o & 31);
+                const float *vv = v + 9 * (int64_t)oc[o];
+                float sl[36];
+#pragma unroll
+                for (int c = 0; c < 9; c++) {
+                    const float4 x = S4[c * ng];
+                    sl[4 * c] = x.x, sl[4 * c + 1] = x.y, sl[4 * c + 2] = x.z, sl[4 * c + 3] = x.w;
+                }
+#pragma unroll
+                for (int q = 0; q < 9; q++) {
+                    const float xq = __ldg(vv + q);
+#pragma unroll
+                    for (int r = 0; r < 4; r++) y[r] += sl[9 * r + q] * xq;
+                }
+            }
+        }
+        block_sum<4>(y, red);
+#pragma unroll
+        for (int m = 0; m < HUGE_NB; m++) {
+            const int o = tid + m * HUGE_FNT;
+            if (o < k) {
+                const int g = o >> 5, ng = min(32, k - 32 * g);
+                const float4 *S4 = reinterpret_cast<const float4 *>(R2 + (int64_t)36 * k * t + 36 * 32 * g) + (o & 31);
+#pragma unroll
+                for (int c = 0; c < 9; c++) {
+                    const float4 x = S4[c * ng];  // L2 hit: the tile was read just above
+                    const float e[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const int el = 4 * c + u, r = el / 9, q = el % 9;
+                        acc[m][q] += e[u] * y[r];
+                    }
+                }
+            }
+        }
+    }
+    float *out = wslice(d);
+#pragma unroll
+    for (int m = 0; m < HUGE_NB; m++) {
+        const int o = tid + m * HUGE_FNT;
+        if (o < k) flush_cam12(out, oc[o], acc[m]);
+    }
+}
+
 template <bool PRECOND>
 __global__ void __launch_bounds__(HUGE_NT) k_huge_out(DevProblem d, float *__restrict__ out,
                                                       const PcgState *__restrict__ st) {
@@ -1686,7 +1757,11 @@ static void large_pipe_cls(rba_ctx *c, int cls, const float *v, float *out, cons
 template <bool PRE>
 static void pipes_all(rba_ctx *c, const float *v, float *out12, const PcgState *st) {
     ForkJoin F(c);
-    if (c->n_huge_out > 0) {  // k > KLARGE: two passes, same stream
+    static const bool fused = !getenv("RBA_HUGE_TWOPASS");
+    if (c->n_huge_fused > 0 && !PRE && fused) {  // k > KLARGE: fused passes (second read from L2)
+        k_huge_fused<<<(unsigned)c->n_huge_fused, HUGE_FNT, 0, F.s()>>>(c->d, c->d.huge_fused, v, st);
+        c->launches++;
+    } else if (c->n_huge_out > 0) {  // k > KLARGE: two passes, same stream
         cudaStream_t hs = F.s();
         if (!PRE) {
             k_huge_y<<<(unsigned)c->n_huge_y, HUGE_NT, 0, hs>>>(c->d, v, st);
