@@ -874,10 +874,10 @@ constexpr int SP_OFF_UNIT = SP_OFF_PACK + (int)sizeof(Pack) * SP_PACKCAP;
 constexpr int SP_OFF_HDR = SP_OFF_UNIT + 2 * SP_UNITCAP;  // stage descriptor (written by the producer)
 constexpr int SP_SB = SP_OFF_HDR + 128;
 #ifndef RBA_SP_STAGES
-#define RBA_SP_STAGES 3
+#define RBA_SP_STAGES 4  // 4 stages, v read through L1 (measured 2.47 -> 2.43 ms cfg4 matvec vs 3 stages + v in smem)
 #endif
 #ifndef RBA_SP_VCAP
-#define RBA_SP_VCAP 16384
+#define RBA_SP_VCAP 0
 #endif
 #ifndef RBA_YRED_SHFL
 #define RBA_YRED_SHFL 1  // y reduction by xor butterfly (measured 2.54 -> 2.47 ms cfg4 matvec)
