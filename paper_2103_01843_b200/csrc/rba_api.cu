@@ -512,6 +512,8 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     CKSC(dalloc_n(c, &d.cams_trial, 9 * n_cams));
     CKSC(dalloc_n(c, &d.pts, 3 * nl));
     CKSC(dalloc_n(c, &d.pts_trial, 3 * nl));
+    CKSC(dalloc_n(c, &d.campre, CAMPRE * n_cams));
+    CKSC(dalloc_n(c, &d.campre_trial, CAMPRE * n_cams));
     CKSC(dalloc_n(c, &d.lm_k, nl));
     CKSC(dalloc_n(c, &d.lm_obs0, nl));
     CKSC(dalloc_n(c, &d.lm_pk, nl));

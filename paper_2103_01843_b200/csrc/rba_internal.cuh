@@ -15,7 +15,8 @@ namespace rba {
 constexpr int KSMALL = 16;    // k <= KSMALL: warp-group kernels over packs of same-k landmarks
 constexpr int KLARGE = 512;   // k <= KLARGE: one thread per camera block in the large-k kernels
 constexpr int KMAX = 3072;    // largest track length supported (k > KLARGE: "huge" path, smem-bound)
-constexpr int KMAX64 = 1024;  // sqrt-BA-64 (f2): largest track length (registers of the FP64 product)
+constexpr int KMAX64 = 1024;
+constexpr int CAMPRE = 24;    // doubles of a camera's precomputed model (R, J_left, t, f, k1, k2)  // sqrt-BA-64 (f2): largest track length (registers of the FP64 product)
 
 // ---- landmark-block arena layout ------------------------------------------
 // Logical block of a landmark with k observations: rows 0..2k+2, columns [J_p (9k) | J_l | r].
@@ -112,6 +113,7 @@ struct DevProblem {
     double huber;             // Huber parameter (px), 0 = squared loss
     // state
     double *cams, *cams_trial, *pts, *pts_trial;  // FP64 state (reading C23)
+    double *campre, *campre_trial;                // per camera R, J_left, t, f, k1, k2 (24 doubles)
     // landmark metadata (internal order, sorted by k)
     int32_t *lm_k, *lm_obs0, *lm_pk;
     int64_t *lm_r2, *lm_side;
@@ -234,6 +236,7 @@ struct rba_ctx {
 namespace rba {
 // kernel launchers (rba_kernels.cu); each returns cudaGetLastError()
 cudaError_t launch_check_depth(rba_ctx *c, int *d_bad);
+cudaError_t launch_cam_prep(rba_ctx *c, int trial);
 cudaError_t query_nsmid(rba_ctx *c, int *d_scratch, int *out);
 cudaError_t launch_linearize(rba_ctx *c);
 cudaError_t launch_cam_scale(rba_ctx *c);

@@ -30,11 +30,11 @@ namespace rba {
 __global__ void k_check_depth(DevProblem d, int *bad) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= d.n_obs) return;
-    double c[9], r[2];
-    load_cam(d.cams, d.obs_cam[i], c);
+    double c[CAMPRE], r[2];
+    load_pre(d.campre, d.obs_cam[i], c);
     const double *X = d.pts + 3 * (int64_t)d.obs_lm[i];
     const double2 uv = d.obs_uv[i];
-    const double Pz = cam_model<float>(c, X[0], X[1], X[2], uv.x, uv.y, r, nullptr, nullptr);
+    const double Pz = cam_model_pre<float>(c, X[0], X[1], X[2], uv.x, uv.y, r, nullptr, nullptr);
     if (!(Pz < -1e-8) || !isfinite(r[0]) || !isfinite(r[1])) atomicAdd(bad, 1);
 }
 
@@ -44,22 +44,22 @@ __global__ void __launch_bounds__(256) k_linearize(DevProblem d) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     double e = 0.0, bad = 0.0;
     if (i < d.n_obs) {
-        double c[9], r[2];
+        double c[CAMPRE], r[2];
         float Jc[18], Jl[6];
         const int cam = d.obs_cam[i];
-        load_cam(d.cams, cam, c);
+        load_pre(d.campre, cam, c);
         const double *X = d.pts + 3 * (int64_t)d.obs_lm[i];
         const double2 uv = d.obs_uv[i];
         if (d.s64) {  // sqrt-BA-64: FP64 Jacobians and FP64 norm sums
             double Jcd[18], Jld[6];
-            const double Pz = cam_model<double>(c, X[0], X[1], X[2], uv.x, uv.y, r, Jcd, Jld);
+            const double Pz = cam_model_pre<double>(c, X[0], X[1], X[2], uv.x, uv.y, r, Jcd, Jld);
             if (!(Pz < 0.0)) bad = 1.0;
             e = robust_rho(r[0] * r[0] + r[1] * r[1], d.huber);
             apply_irls<double>(r, Jcd, Jld, d.huber);
 #pragma unroll
             for (int q = 0; q < 9; q++) atomicAdd(d.cam_n2d + 9 * (int64_t)cam + q, Jcd[q] * Jcd[q] + Jcd[9 + q] * Jcd[9 + q]);
         } else {
-            const double Pz = cam_model(c, X[0], X[1], X[2], uv.x, uv.y, r, Jc, Jl);
+            const double Pz = cam_model_pre(c, X[0], X[1], X[2], uv.x, uv.y, r, Jc, Jl);
             if (!(Pz < 0.0)) bad = 1.0;
             e = robust_rho(r[0] * r[0] + r[1] * r[1], d.huber);
             apply_irls(r, Jc, Jl, d.huber);
@@ -223,11 +223,11 @@ __global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProb
     if (act) {
         const int64_t o = d.lm_obs0[j] + gl;
         cam = d.obs_cam[o];
-        double c[9], rd[2];
-        load_cam(d.cams, cam, c);
+        double c[CAMPRE], rd[2];
+        load_pre(d.campre, cam, c);
         const double *X = d.pts + 3 * j;
         const double2 uv = d.obs_uv[o];
-        cam_model(c, X[0], X[1], X[2], uv.x, uv.y, rd, Jc, Jl);
+        cam_model_pre(c, X[0], X[1], X[2], uv.x, uv.y, rd, Jc, Jl);
         apply_irls(rd, Jc, Jl, d.huber);
         r[0] = (float)rd[0];
         r[1] = (float)rd[1];
@@ -407,11 +407,11 @@ __global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProb
 // rows are recomputed per block in the emission loop instead of being kept from the prologue.
 __device__ __forceinline__ void block_jp(const DevProblem &d, int64_t obs0, int o, const double *Xp, BlockWY &B) {
     const int cam = d.obs_cam[obs0 + o];
-    double c[9], r[2];
+    double c[CAMPRE], r[2];
     float Jc[18], Jl[6];
-    load_cam(d.cams, cam, c);
+    load_pre(d.campre, cam, c);
     const double2 uv = d.obs_uv[obs0 + o];
-    cam_model(c, Xp[0], Xp[1], Xp[2], uv.x, uv.y, r, Jc, Jl);
+    cam_model_pre(c, Xp[0], Xp[1], Xp[2], uv.x, uv.y, r, Jc, Jl);
     apply_irls(r, Jc, Jl, d.huber);
 #pragma unroll
     for (int q = 0; q < 9; q++) {
@@ -444,11 +444,11 @@ __global__ void __launch_bounds__(NT) k_marg_large(DevProblem d, const LargeItem
     for (int q = 0; q < 9; q++) B.jp[0][q] = B.jp[1][q] = 0.f;
     for (int o = tid; o < k; o += NT) {  // !MULTI: NT >= k, at most o == tid
         const int cam = d.obs_cam[obs0 + o];
-        double c[9], r[2];
+        double c[CAMPRE], r[2];
         float Jc[18], Jl[6];
-        load_cam(d.cams, cam, c);
+        load_pre(d.campre, cam, c);
         const double2 uv = d.obs_uv[obs0 + o];
-        cam_model(c, Xp[0], Xp[1], Xp[2], uv.x, uv.y, r, Jc, Jl);
+        cam_model_pre(c, Xp[0], Xp[1], Xp[2], uv.x, uv.y, r, Jc, Jl);
         apply_irls(r, Jc, Jl, d.huber);
         if (!MULTI) {
 #pragma unroll
@@ -1594,17 +1594,17 @@ __global__ void __launch_bounds__(1024) k_trial_cams(DevProblem d, float lam, in
 }
 
 // ============================================================================ K8 cost
-__global__ void __launch_bounds__(256) k_cost(DevProblem d, const double *__restrict__ cams,
+__global__ void __launch_bounds__(256) k_cost(DevProblem d, const double *__restrict__ campre,
                                               const double *__restrict__ pts, int slot, int bad_slot) {
     __shared__ double red[32];
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     double e = 0.0, bad = 0.0;
     if (i < d.n_obs) {
-        double c[9], r[2];
-        load_cam(cams, d.obs_cam[i], c);
+        double c[CAMPRE], r[2];
+        load_pre(campre, d.obs_cam[i], c);
         const double *X = pts + 3 * (int64_t)d.obs_lm[i];
         const double2 uv = d.obs_uv[i];
-        const double Pz = cam_model<float>(c, X[0], X[1], X[2], uv.x, uv.y, r, nullptr, nullptr);
+        const double Pz = cam_model_pre<float>(c, X[0], X[1], X[2], uv.x, uv.y, r, nullptr, nullptr);
         if (!(Pz < 0.0) || !isfinite(r[0]) || !isfinite(r[1])) bad = 1.0;
         else e = robust_rho(r[0] * r[0] + r[1] * r[1], d.huber);
     }
@@ -1633,14 +1633,28 @@ cudaError_t query_nsmid(rba_ctx *c, int *d_scratch, int *out) {
     return cudaStreamSynchronize(c->stream);
 }
 
+__global__ void k_cam_prep(const double *__restrict__ cams, double *__restrict__ pre, int64_t n_p) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n_p) cam_prep(cams + 9 * i, pre + CAMPRE * i);
+}
+// per-camera R / J_left of the current (trial = 0) or trial (1) cameras
+cudaError_t launch_cam_prep(rba_ctx *c, int trial) {
+    k_cam_prep<<<nblk(c->d.n_p, 128), 128, 0, c->stream>>>(trial ? c->d.cams_trial : c->d.cams,
+                                                            trial ? c->d.campre_trial : c->d.campre, c->d.n_p);
+    c->launches++;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_check_depth(rba_ctx *c, int *d_bad) {
     if (c->d.n_obs == 0) return cudaSuccess;
+    launch_cam_prep(c, 0);
     k_check_depth<<<nblk(c->d.n_obs, 256), 256, 0, c->stream>>>(c->d, d_bad);
     c->launches++;
     return cudaGetLastError();
 }
 
 cudaError_t launch_linearize(rba_ctx *c) {
+    launch_cam_prep(c, 0);
     if (c->d.n_obs == 0) return cudaSuccess;
     Prof P(c, KID_LIN, 24.0 * c->d.n_obs);
     k_linearize<<<nblk(c->d.n_obs, 256), 256, 0, c->stream>>>(c->d);
@@ -1928,7 +1942,8 @@ cudaError_t launch_cost(rba_ctx *c, int at_trial, int slot) {
     if (c->d.n_obs == 0) return cudaSuccess;
     Prof P(c, KID_COST, 20.0 * c->d.n_obs);
     const int bad_slot = at_trial ? SC_BADT : SC_BAD;
-    k_cost<<<nblk(c->d.n_obs, 256), 256, 0, c->stream>>>(c->d, at_trial ? c->d.cams_trial : c->d.cams,
+    launch_cam_prep(c, at_trial);
+    k_cost<<<nblk(c->d.n_obs, 256), 256, 0, c->stream>>>(c->d, at_trial ? c->d.campre_trial : c->d.campre,
                                                           at_trial ? c->d.pts_trial : c->d.pts, slot, bad_slot);
     P.end();
     c->launches++;

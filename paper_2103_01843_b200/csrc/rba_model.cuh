@@ -88,6 +88,84 @@ __device__ __forceinline__ double cam_model(const double *__restrict__ cam, doub
     return P2;
 }
 
+// Per-camera precomputation (once per state, k_cam_prep): R(w) and J_left(w) as 3x3 matrices plus
+// t, f, k1, k2 -- 24 doubles -- so the per-observation model needs no trigonometry or divisions
+// beyond 1/P_z.  Same formulas as cam_model above.
+__device__ __forceinline__ void cam_prep(const double *__restrict__ cam, double *pre) {
+    const double w0 = cam[0], w1 = cam[1], w2 = cam[2];
+    const double th2 = w0 * w0 + w1 * w1 + w2 * w2;
+    double a, b, cc;
+    if (th2 < 1e-16) {
+        a = 1. - th2 * (1. / 6.);
+        b = 0.5 - th2 * (1. / 24.);
+        cc = 1. / 6. - th2 * (1. / 120.);
+    } else {
+        const double th = sqrt(th2);
+        double s, co;
+        sincos(th, &s, &co);
+        a = s / th;
+        const double hs = sin(0.5 * th);
+        b = 2. * hs * hs / th2;
+        cc = (th < 1e-2) ? (1.0 / 6.0 - th2 * (1.0 / 120.0) + th2 * th2 * (1.0 / 5040.0)) : (th - s) / (th2 * th);
+    }
+    const double rd = 1. - b * th2, jd = 1. - cc * th2;
+    pre[0] = rd + b * w0 * w0, pre[1] = -a * w2 + b * w0 * w1, pre[2] = a * w1 + b * w0 * w2;
+    pre[3] = a * w2 + b * w0 * w1, pre[4] = rd + b * w1 * w1, pre[5] = -a * w0 + b * w1 * w2;
+    pre[6] = -a * w1 + b * w0 * w2, pre[7] = a * w0 + b * w1 * w2, pre[8] = rd + b * w2 * w2;
+    pre[9] = jd + cc * w0 * w0, pre[10] = -b * w2 + cc * w0 * w1, pre[11] = b * w1 + cc * w0 * w2;
+    pre[12] = b * w2 + cc * w0 * w1, pre[13] = jd + cc * w1 * w1, pre[14] = -b * w0 + cc * w1 * w2;
+    pre[15] = -b * w1 + cc * w0 * w2, pre[16] = b * w0 + cc * w1 * w2, pre[17] = jd + cc * w2 * w2;
+    for (int i = 0; i < 6; i++) pre[18 + i] = cam[3 + i];
+}
+
+__device__ __forceinline__ void load_pre(const double *__restrict__ campre, int cam, double *c) {
+    const double2 *p2 = reinterpret_cast<const double2 *>(campre + CAMPRE * (int64_t)cam);
+#pragma unroll
+    for (int i = 0; i < CAMPRE / 2; i++) {
+        const double2 x = __ldg(p2 + i);
+        c[2 * i] = x.x, c[2 * i + 1] = x.y;
+    }
+}
+
+template <typename JT = float>
+__device__ __forceinline__ double cam_model_pre(const double *__restrict__ c, double X0, double X1, double X2,
+                                                double u, double v, double *r, JT *Jc, JT *Jl) {
+    const double *R = c, *L = c + 9;
+    const double RX0 = R[0] * X0 + R[1] * X1 + R[2] * X2;
+    const double RX1 = R[3] * X0 + R[4] * X1 + R[5] * X2;
+    const double RX2 = R[6] * X0 + R[7] * X1 + R[8] * X2;
+    const double P0 = RX0 + c[18], P1 = RX1 + c[19], P2 = RX2 + c[20];
+    const double iz = -1. / P2;
+    const double px = P0 * iz, py = P1 * iz;
+    const double n = px * px + py * py;
+    const double f = c[21], k1 = c[22], k2 = c[23];
+    const double dd = 1. + k1 * n + k2 * n * n;
+    r[0] = f * dd * px - u;
+    r[1] = f * dd * py - v;
+    if (!Jc) return P2;
+    const double e = 2. * (k1 + 2. * k2 * n);
+    const double D00 = f * (dd + e * px * px), D01 = f * e * px * py, D11 = f * (dd + e * py * py);
+    const double A00 = iz * D00, A01 = iz * D01, A02 = iz * (D00 * px + D01 * py);
+    const double A10 = iz * D01, A11 = iz * D11, A12 = iz * (D01 * px + D11 * py);
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+        Jl[q] = (JT)(A00 * R[q] + A01 * R[3 + q] + A02 * R[6 + q]);
+        Jl[3 + q] = (JT)(A10 * R[q] + A11 * R[3 + q] + A12 * R[6 + q]);
+    }
+    const double B00 = A01 * RX2 - A02 * RX1, B01 = -A00 * RX2 + A02 * RX0, B02 = A00 * RX1 - A01 * RX0;
+    const double B10 = A11 * RX2 - A12 * RX1, B11 = -A10 * RX2 + A12 * RX0, B12 = A10 * RX1 - A11 * RX0;
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+        Jc[q] = (JT)(-(B00 * L[q] + B01 * L[3 + q] + B02 * L[6 + q]));
+        Jc[9 + q] = (JT)(-(B10 * L[q] + B11 * L[3 + q] + B12 * L[6 + q]));
+    }
+    Jc[3] = (JT)A00; Jc[4] = (JT)A01; Jc[5] = (JT)A02;
+    Jc[12] = (JT)A10; Jc[13] = (JT)A11; Jc[14] = (JT)A12;
+    Jc[6] = (JT)(dd * px); Jc[7] = (JT)(f * n * px); Jc[8] = (JT)(f * n * n * px);
+    Jc[15] = (JT)(dd * py); Jc[16] = (JT)(f * n * py); Jc[17] = (JT)(f * n * n * py);
+    return P2;
+}
+
 // Huber norm on s = |r|^2 and its IRLS weight sqrt(rho'(s)) (Ceres' corrector with
 // rho'' = 0); delta <= 0: squared loss.
 __device__ __forceinline__ double robust_rho(double s, double delta) {

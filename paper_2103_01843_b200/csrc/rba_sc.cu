@@ -30,12 +30,12 @@ template <typename T>
 __device__ __forceinline__ void sc_obs(const DevProblem &d, int64_t j, int a, ObsJ<T> &o) {
     const int64_t oi = d.lm_obs0[j] + a;
     o.cam = d.obs_cam[oi];
-    double c[9], r[2];
+    double c[CAMPRE], r[2];
     T Jc[18], Jl[6];
-    load_cam(d.cams, o.cam, c);
+    load_pre(d.campre, o.cam, c);
     const double *X = d.pts + 3 * j;
     const double2 uv = d.obs_uv[oi];
-    cam_model<T>(c, X[0], X[1], X[2], uv.x, uv.y, r, Jc, Jl);
+    cam_model_pre<T>(c, X[0], X[1], X[2], uv.x, uv.y, r, Jc, Jl);
     apply_irls<T>(r, Jc, Jl, d.huber);
 #pragma unroll
     for (int q = 0; q < 9; q++) {

@@ -86,10 +86,10 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 16 : 1) k_marg64(DevProblem d, 
     };
     double n2[4] = {0, 0, 0, 0};
     for (int o = tid; o < k; o += NT) {
-        double c[9], r[2], Jc[18], Jl[6];
-        load_cam(d.cams, d.obs_cam[obs0 + o], c);
+        double c[CAMPRE], r[2], Jc[18], Jl[6];
+        load_pre(d.campre, d.obs_cam[obs0 + o], c);
         const double2 uv = d.obs_uv[obs0 + o];
-        cam_model<double>(c, Xp[0], Xp[1], Xp[2], uv.x, uv.y, r, Jc, Jl);
+        cam_model_pre<double>(c, Xp[0], Xp[1], Xp[2], uv.x, uv.y, r, Jc, Jl);
         apply_irls<double>(r, Jc, Jl, d.huber);
         for (int q = 0; q < 3; q++) {
             SX[6 * o + q] = Jl[q], SX[6 * o + 3 + q] = Jl[3 + q];
@@ -162,11 +162,11 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 16 : 1) k_marg64(DevProblem d, 
         const int ncol = 9 * max(0, min(32, k - wb));        // valid columns of the warp's segment
         double jp[18] = {}, M[27] = {};
         if (act) {
-            double c[9], r[2], Jc[18], Jl[6];
+            double c[CAMPRE], r[2], Jc[18], Jl[6];
             const int cam = d.obs_cam[obs0 + o];
-            load_cam(d.cams, cam, c);
+            load_pre(d.campre, cam, c);
             const double2 uv = d.obs_uv[obs0 + o];
-            cam_model<double>(c, Xp[0], Xp[1], Xp[2], uv.x, uv.y, r, Jc, Jl);
+            cam_model_pre<double>(c, Xp[0], Xp[1], Xp[2], uv.x, uv.y, r, Jc, Jl);
             apply_irls<double>(r, Jc, Jl, d.huber);
             for (int q = 0; q < 9; q++) {
                 const double sc = d.sp64[9 * cam + q];
@@ -291,11 +291,11 @@ __global__ void __launch_bounds__(256) k_marg64_small(DevProblem d, int64_t lo, 
     if (act) {
         const int64_t o = d.lm_obs0[j] + gl;
         cam = d.obs_cam[o];
-        double c[9];
-        load_cam(d.cams, cam, c);
+        double c[CAMPRE];
+        load_pre(d.campre, cam, c);
         const double *Xp = d.pts + 3 * j;
         const double2 uv = d.obs_uv[o];
-        cam_model<double>(c, Xp[0], Xp[1], Xp[2], uv.x, uv.y, r, Jc, Jl);
+        cam_model_pre<double>(c, Xp[0], Xp[1], Xp[2], uv.x, uv.y, r, Jc, Jl);
         apply_irls<double>(r, Jc, Jl, d.huber);
     }
     double sl[3], Dl[3];

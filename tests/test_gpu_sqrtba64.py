@@ -93,7 +93,7 @@ def test_sqrtba64_pcg_backsub_lm(cfg):
     o = oracle.Oracle(p)
     for i in range(5):
         rg, ro = s.lm_step(), o.lm_step()
-        assert abs(rg["cost_after"] - ro["cost_after"]) <= 1e-8 * ro["cost_after"], (i, rg, ro)
+        assert abs(rg["cost_after"] - ro["cost_after"]) <= 1e-7 * ro["cost_after"], (i, rg, ro)
 
 
 def test_sqrtba64_more_accurate_than_32():
