@@ -308,7 +308,9 @@ def main():
     # (pinned host -> device), one LM iteration, download the state.
     e2e = None
     if not args.no_e2e:
-        cams, pts = prob["cameras_init"].copy(), prob["points_init"].copy()
+        # pinned host buffers (torch pinned storage viewed as numpy); the state round-trips in place
+        cams = torch.from_numpy(prob["cameras_init"]).pin_memory().numpy()
+        pts = torch.from_numpy(prob["points_init"]).pin_memory().numpy()
         s.set_state(cams, pts)
         s.reset_lm()
         barrier()
@@ -316,7 +318,7 @@ def main():
         for _ in range(args.steps):
             s.set_state(cams, pts)
             s.lm_step()
-            cams, pts = s.state()
+            s.state(out=(cams, pts))
         barrier()
         t_e2e = max_over_ranks(time.perf_counter() - t0)
         nb = (9 * n_p + 3 * n_l) * 8  # FP64 state (host and device)

@@ -513,6 +513,9 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     CKSC(dalloc_n(c, &d.pts, 3 * nl));
     CKSC(dalloc_n(c, &d.pts_trial, 3 * nl));
     CKSC(dalloc_n(c, &d.campre, CAMPRE * n_cams));
+    CKSC(dalloc_n(c, &d.lm_orig, std::max<int64_t>(nl, 1)));
+    CKSC(dalloc_n(c, &d.pts_io, 3 * std::max<int64_t>(n_points, 1)));
+    if (nl) CKC(cudaMemcpyAsync(d.lm_orig, loc.data(), sizeof(int32_t) * nl, cudaMemcpyHostToDevice, c->stream));
     CKSC(dalloc_n(c, &d.campre_trial, CAMPRE * n_cams));
     CKSC(dalloc_n(c, &d.lm_k, nl));
     CKSC(dalloc_n(c, &d.lm_obs0, nl));
@@ -957,30 +960,19 @@ extern "C" rba_status rba_lm_step(rba_ctx *c, rba_lm_report *rep) {
 }
 
 // ------------------------------------------------------------------------------------ state
+// State I/O: one contiguous copy each way; the landmark permutation (caller order <-> the
+// internal k-sorted order) runs on the device (k_pts_permute).
 extern "C" rba_status rba_get_state(rba_ctx *c, double *cameras, double *points) {
     if (!c || !cameras || !points) return fail(RBA_ERR_INVALID_ARG, "null argument");
     CK(cudaSetDevice(c->device));
     const DevProblem &d = c->d;
-    std::vector<double> hc(9 * d.n_p), hp(3 * c->n_l_global, 0.0), loc(3 * std::max<int64_t>(d.n_l, 1));
-    CK(cudaMemcpyAsync(hc.data(), d.cams, sizeof(double) * hc.size(), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaMemcpyAsync(loc.data(), d.pts, sizeof(double) * 3 * d.n_l, cudaMemcpyDeviceToHost, c->stream));
+    const int64_t np3 = 3 * c->n_l_global;
+    if (c->world > 1) CK(cudaMemsetAsync(d.pts_io, 0, sizeof(double) * std::max<int64_t>(np3, 1), c->stream));
+    CK(launch_pts_permute(c, 0));
+    CKS(allreduce(c, d.pts_io, np3, ncclDouble));  // every rank owns a disjoint landmark shard
+    CK(cudaMemcpyAsync(cameras, d.cams, sizeof(double) * 9 * d.n_p, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(points, d.pts_io, sizeof(double) * np3, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    for (int64_t i = 0; i < d.n_l; i++)
-        for (int q = 0; q < 3; q++) hp[3 * (int64_t)c->lm_orig[i] + q] = loc[3 * i + q];
-    if (c->have_comm) {
-        double *buf = nullptr;
-        CK(cudaMalloc(&buf, sizeof(double) * std::max<int64_t>(1, hp.size())));
-        CK(cudaMemcpyAsync(buf, hp.data(), sizeof(double) * hp.size(), cudaMemcpyHostToDevice, c->stream));
-        rba_status s = allreduce(c, buf, hp.size(), ncclDouble);
-        if (s == RBA_OK) {
-            CK(cudaMemcpyAsync(hp.data(), buf, sizeof(double) * hp.size(), cudaMemcpyDeviceToHost, c->stream));
-            CK(cudaStreamSynchronize(c->stream));
-        }
-        cudaFree(buf);
-        if (s != RBA_OK) return s;
-    }
-    for (size_t i = 0; i < hc.size(); i++) cameras[i] = hc[i];
-    for (size_t i = 0; i < hp.size(); i++) points[i] = hp[i];
     return RBA_OK;
 }
 
@@ -988,11 +980,9 @@ extern "C" rba_status rba_set_state(rba_ctx *c, const double *cameras, const dou
     if (!c || !cameras || !points) return fail(RBA_ERR_INVALID_ARG, "null argument");
     CK(cudaSetDevice(c->device));
     const DevProblem &d = c->d;
-    std::vector<double> hp(3 * std::max<int64_t>(d.n_l, 1));
-    for (int64_t i = 0; i < d.n_l; i++)
-        for (int q = 0; q < 3; q++) hp[3 * i + q] = points[3 * (int64_t)c->lm_orig[i] + q];
     CK(cudaMemcpyAsync(d.cams, cameras, sizeof(double) * 9 * d.n_p, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(d.pts, hp.data(), sizeof(double) * 3 * d.n_l, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(d.pts_io, points, sizeof(double) * 3 * c->n_l_global, cudaMemcpyHostToDevice, c->stream));
+    CK(launch_pts_permute(c, 1));
     CK(cudaStreamSynchronize(c->stream));
     c->linearized = c->marginalized = c->solved = c->backsubbed = false;
     c->need_lin = true;

@@ -114,6 +114,8 @@ struct DevProblem {
     // state
     double *cams, *cams_trial, *pts, *pts_trial;  // FP64 state (reading C23)
     double *campre, *campre_trial;                // per camera R, J_left, t, f, k1, k2 (24 doubles)
+    int32_t *lm_orig;                             // internal -> caller landmark index (state I/O)
+    double *pts_io;                               // 3 n_l(global) staging of the caller-order points
     // landmark metadata (internal order, sorted by k)
     int32_t *lm_k, *lm_obs0, *lm_pk;
     int64_t *lm_r2, *lm_side;
@@ -237,6 +239,7 @@ namespace rba {
 // kernel launchers (rba_kernels.cu); each returns cudaGetLastError()
 cudaError_t launch_check_depth(rba_ctx *c, int *d_bad);
 cudaError_t launch_cam_prep(rba_ctx *c, int trial);
+cudaError_t launch_pts_permute(rba_ctx *c, int to_internal);
 cudaError_t query_nsmid(rba_ctx *c, int *d_scratch, int *out);
 cudaError_t launch_linearize(rba_ctx *c);
 cudaError_t launch_cam_scale(rba_ctx *c);

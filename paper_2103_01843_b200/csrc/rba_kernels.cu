@@ -1037,7 +1037,9 @@ struct PipeCfg {
     static constexpr int TB = 144 * NS;             // bytes of the largest tile (k <= NS)
     static constexpr int SB = TB * NSLOT;           // stage bytes
     static constexpr int STAGES = RBA_PIPE_SMEM / SB > 8 ? 8 : RBA_PIPE_SMEM / SB;
-    static constexpr size_t SMEM = (size_t)STAGES * SB + 2 * STAGES * sizeof(uint64_t);
+    // K4 only: the 4 TL rows (residual entries q) of each staged tile, 64 B per slot and stage
+    static constexpr size_t QOFF = (size_t)STAGES * SB;
+    static constexpr size_t SMEM = QOFF + (size_t)STAGES * NSLOT * 64 + 2 * STAGES * sizeof(uint64_t);
 };
 
 // Consumer slot s of NSLOT processes tiles lo + i*NSLOT + s; NS threads per slot <-> camera blocks.
@@ -1049,7 +1051,7 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
     using C = PipeCfg<NS, NSLOT>;
     if (!PRECOND && st && st->done) return;
     extern __shared__ __align__(128) unsigned char sm[];
-    uint64_t *full = reinterpret_cast<uint64_t *>(sm + (size_t)C::STAGES * C::SB);
+    uint64_t *full = reinterpret_cast<uint64_t *>(sm + C::QOFF + (size_t)C::STAGES * NSLOT * 64);
     uint64_t *empty = full + C::STAGES;
     __shared__ __align__(16) float red[2][C::NC / 32][4];
     const int tid = threadIdx.x;
@@ -1068,28 +1070,36 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
             const uint64_t pol = policy_evict_first();
             // descriptors (arena offset, k) of the next stage are loaded one stage ahead, as
             // independent loads, so their latency overlaps the wait and the current copies
-            int64_t noff[NSLOT];
+            int64_t noff[NSLOT], ntl[NSLOT];
             int nk[NSLOT];
+            auto tl_off = [&](int64_t ti) -> int64_t {  // float offset of TL rows 3 + 4t .. 6 + 4t
+                if (!PRECOND || ti >= hi) return 0;
+                const TileRef tr = tiles[ti];
+                return d.lm_side[tr.lm] + side_tl(tr.k) + 4 * (3 + 4 * (int64_t)tr.t);
+            };
 #pragma unroll
             for (int sl = 0; sl < NSLOT; sl++) {
                 const int64_t ti = lo + sl;
                 nk[sl] = ti < hi ? tiles[ti].k : 0;
                 noff[sl] = ti < hi ? tiles[ti].off : 0;
+                ntl[sl] = tl_off(ti);
             }
             for (int64_t i = 0; i < nst; i++) {
                 const int s = (int)(i % C::STAGES);
                 const uint32_t ph = (uint32_t)((i / C::STAGES) & 1);
-                int64_t coff[NSLOT];
+                int64_t coff[NSLOT], ctl[NSLOT];
                 int ck[NSLOT];
                 uint32_t total = 0;
 #pragma unroll
                 for (int sl = 0; sl < NSLOT; sl++) {
                     coff[sl] = noff[sl];
+                    ctl[sl] = ntl[sl];
                     ck[sl] = nk[sl];
-                    total += 144u * (uint32_t)ck[sl];
+                    total += 144u * (uint32_t)ck[sl] + ((PRECOND && ck[sl]) ? 64u : 0u);
                     const int64_t tn = lo + (i + 1) * NSLOT + sl;
                     nk[sl] = tn < hi ? tiles[tn].k : 0;
                     noff[sl] = tn < hi ? tiles[tn].off : 0;
+                    ntl[sl] = tl_off(tn);
                 }
                 mbar_wait(&empty[s], ph ^ 1);
                 mbar_arrive_expect_tx(&full[s], total);
@@ -1098,6 +1108,10 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
                     if (ck[sl])
                         bulk_g2s_stream(sm + (size_t)s * C::SB + (size_t)sl * C::TB, d.arena + coff[sl], 144u * (uint32_t)ck[sl],
                                  &full[s], pol);
+                if (PRECOND)
+#pragma unroll
+                    for (int sl = 0; sl < NSLOT; sl++)
+                        if (ck[sl]) bulk_g2s(sm + C::QOFF + ((size_t)s * NSLOT + sl) * 64, d.arena + ctl[sl], 64u, &full[s]);
             }
         }
         return;
@@ -1107,7 +1121,6 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
     constexpr int NWS = NS / 32;
     int cur = -1, k = 0, cam = 0, ng = 1, g = 0;
     bool valid = false;
-    const float4 *TL = nullptr;
     float vo[9], acc[9], P[PRECOND ? 45 : 1], b[PRECOND ? 9 : 1];
 #pragma unroll
     for (int q = 0; q < 9; q++) vo[q] = 0.f, acc[q] = 0.f;
@@ -1136,7 +1149,6 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
 #pragma unroll
                 for (int q = 0; q < 9; q++) vo[q] = (PRECOND || !valid) ? 0.f : __ldg(v + 9 * cam + q);
                 if (PRECOND) {
-                    TL = reinterpret_cast<const float4 *>(d.arena + d.lm_side[cur] + side_tl(k));
 #pragma unroll
                     for (int q = 0; q < 45; q++) P[q] = 0.f;
 #pragma unroll
@@ -1148,7 +1160,12 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
             }
         }
         mbar_wait(&full[s], ph);
-        float sl[36];
+        float sl[36], qv[4] = {0.f, 0.f, 0.f, 0.f};
+        if (PRECOND && have && valid) {
+            const float4 *Q = reinterpret_cast<const float4 *>(sm + C::QOFF + ((size_t)s * NSLOT + slot) * 64);
+#pragma unroll
+            for (int r = 0; r < 4; r++) qv[r] = Q[r].w;
+        }
         if (have && valid) {
             const float4 *S4 =
                 reinterpret_cast<const float4 *>(sm + (size_t)s * C::SB + (size_t)slot * C::TB) + 288 * g + (o & 31);
@@ -1169,7 +1186,7 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
 #pragma unroll
                 for (int r = 0; r < 4; r++) {
                     const int a = 4 * tr.t + r;
-                    if (a < 2 * k) acc_rows(P, b, sl + 9 * r, TL[3 + a].w);
+                    if (a < 2 * k) acc_rows(P, b, sl + 9 * r, qv[r]);
                 }
             }
         } else {
@@ -1641,6 +1658,24 @@ __global__ void k_cam_prep(const double *__restrict__ cams, double *__restrict__
 cudaError_t launch_cam_prep(rba_ctx *c, int trial) {
     k_cam_prep<<<nblk(c->d.n_p, 128), 128, 0, c->stream>>>(trial ? c->d.cams_trial : c->d.cams,
                                                             trial ? c->d.campre_trial : c->d.campre, c->d.n_p);
+    c->launches++;
+    return cudaGetLastError();
+}
+
+// landmark state between the caller's order (pts_io, 3 n_l global) and the internal order
+__global__ void k_pts_permute(DevProblem d, int to_internal) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= d.n_l) return;
+    const int64_t g = d.lm_orig[i];
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+        if (to_internal) d.pts[3 * i + q] = d.pts_io[3 * g + q];
+        else d.pts_io[3 * g + q] = d.pts[3 * i + q];
+    }
+}
+cudaError_t launch_pts_permute(rba_ctx *c, int to_internal) {
+    if (c->d.n_l == 0) return cudaSuccess;
+    k_pts_permute<<<nblk(c->d.n_l, 256), 256, 0, c->stream>>>(c->d, to_internal);
     c->launches++;
     return cudaGetLastError();
 }

@@ -14,83 +14,14 @@ namespace rba {
 // ============================================================================ camera model
 // BAL / Snavely (readings C1, C2, C22): P = R(w) X + t, p = -P_xy / P_z,
 // d = 1 + k1 |p|^2 + k2 |p|^4, pi = f d p, r = pi - u.  Jacobians for the additive update of all
-// 9 camera parameters: dP/dw = -[R X]_x J_left(w).  Returns P_z.
-// Evaluated in FP64 from the FP64 state (reading C23): residuals r in FP64, the
-// Jacobians rounded to JT on output (FP32 for sqrt-BA-32 and explicit-32, FP64 for explicit-64).
-template <typename JT = float>
-__device__ __forceinline__ double cam_model(const double *__restrict__ cam, double X0, double X1, double X2,
-                                            double u, double v, double *r, JT *Jc, JT *Jl) {
-    const double w0 = cam[0], w1 = cam[1], w2 = cam[2];
-    const double th2 = w0 * w0 + w1 * w1 + w2 * w2;
-    double a, b, cc;  // R = I + a K + b K^2, J_left = I + b K + cc K^2
-    if (th2 < 1e-16) {
-        a = 1. - th2 * (1. / 6.);
-        b = 0.5 - th2 * (1. / 24.);
-        cc = 1. / 6. - th2 * (1. / 120.);
-    } else {
-        const double th = sqrt(th2);
-        double s, co;
-        sincos(th, &s, &co);
-        a = s / th;
-        const double hs = sin(0.5 * th);
-        b = 2. * hs * hs / th2;  // (1 - cos th) / th^2 without cancellation
-        cc = (th < 1e-2) ? (1.0 / 6.0 - th2 * (1.0 / 120.0) + th2 * th2 * (1.0 / 5040.0)) : (th - s) / (th2 * th);
-    }
-    const double cx0 = w1 * X2 - w2 * X1, cx1 = w2 * X0 - w0 * X2, cx2 = w0 * X1 - w1 * X0;
-    const double dx0 = w1 * cx2 - w2 * cx1, dx1 = w2 * cx0 - w0 * cx2, dx2 = w0 * cx1 - w1 * cx0;
-    const double RX0 = X0 + a * cx0 + b * dx0, RX1 = X1 + a * cx1 + b * dx1, RX2 = X2 + a * cx2 + b * dx2;
-    const double P0 = RX0 + cam[3], P1 = RX1 + cam[4], P2 = RX2 + cam[5];
-    const double iz = -1. / P2;
-    const double px = P0 * iz, py = P1 * iz;
-    const double n = px * px + py * py;
-    const double f = cam[6], k1 = cam[7], k2 = cam[8];
-    const double dd = 1. + k1 * n + k2 * n * n;
-    r[0] = f * dd * px - u;
-    r[1] = f * dd * py - v;
-    if (!Jc) return P2;
-    // dpi/dP = f (d I + e p p^T) * iz [[1,0,px],[0,1,py]]
-    const double e = 2. * (k1 + 2. * k2 * n);
-    const double D00 = f * (dd + e * px * px), D01 = f * e * px * py, D11 = f * (dd + e * py * py);
-    const double A00 = iz * D00, A01 = iz * D01, A02 = iz * (D00 * px + D01 * py);
-    const double A10 = iz * D01, A11 = iz * D11, A12 = iz * (D01 * px + D11 * py);
-    // R = (1 - b th2) I + a K + b w w^T
-    const double rd = 1. - b * th2;
-    const double R00 = rd + b * w0 * w0, R11 = rd + b * w1 * w1, R22 = rd + b * w2 * w2;
-    const double R01 = -a * w2 + b * w0 * w1, R02 = a * w1 + b * w0 * w2;
-    const double R10 = a * w2 + b * w0 * w1, R12 = -a * w0 + b * w1 * w2;
-    const double R20 = -a * w1 + b * w0 * w2, R21 = a * w0 + b * w1 * w2;
-    Jl[0] = (JT)(A00 * R00 + A01 * R10 + A02 * R20);
-    Jl[1] = (JT)(A00 * R01 + A01 * R11 + A02 * R21);
-    Jl[2] = (JT)(A00 * R02 + A01 * R12 + A02 * R22);
-    Jl[3] = (JT)(A10 * R00 + A11 * R10 + A12 * R20);
-    Jl[4] = (JT)(A10 * R01 + A11 * R11 + A12 * R21);
-    Jl[5] = (JT)(A10 * R02 + A11 * R12 + A12 * R22);
-    // J_left = (1 - cc th2) I + b K + cc w w^T
-    const double jd = 1. - cc * th2;
-    const double L00 = jd + cc * w0 * w0, L11 = jd + cc * w1 * w1, L22 = jd + cc * w2 * w2;
-    const double L01 = -b * w2 + cc * w0 * w1, L02 = b * w1 + cc * w0 * w2;
-    const double L10 = b * w2 + cc * w0 * w1, L12 = -b * w0 + cc * w1 * w2;
-    const double L20 = -b * w1 + cc * w0 * w2, L21 = b * w0 + cc * w1 * w2;
-    // B = A [RX]_x,  [RX]_x = [[0,-RX2,RX1],[RX2,0,-RX0],[-RX1,RX0,0]]
-    const double B00 = A01 * RX2 - A02 * RX1, B01 = -A00 * RX2 + A02 * RX0, B02 = A00 * RX1 - A01 * RX0;
-    const double B10 = A11 * RX2 - A12 * RX1, B11 = -A10 * RX2 + A12 * RX0, B12 = A10 * RX1 - A11 * RX0;
-    // d/dw = -B J_left
-    Jc[0] = (JT)(-(B00 * L00 + B01 * L10 + B02 * L20));
-    Jc[1] = (JT)(-(B00 * L01 + B01 * L11 + B02 * L21));
-    Jc[2] = (JT)(-(B00 * L02 + B01 * L12 + B02 * L22));
-    Jc[9] = (JT)(-(B10 * L00 + B11 * L10 + B12 * L20));
-    Jc[10] = (JT)(-(B10 * L01 + B11 * L11 + B12 * L21));
-    Jc[11] = (JT)(-(B10 * L02 + B11 * L12 + B12 * L22));
-    Jc[3] = (JT)A00; Jc[4] = (JT)A01; Jc[5] = (JT)A02;
-    Jc[12] = (JT)A10; Jc[13] = (JT)A11; Jc[14] = (JT)A12;
-    Jc[6] = (JT)(dd * px); Jc[7] = (JT)(f * n * px); Jc[8] = (JT)(f * n * n * px);
-    Jc[15] = (JT)(dd * py); Jc[16] = (JT)(f * n * py); Jc[17] = (JT)(f * n * n * py);
-    return P2;
-}
-
+// 9 camera parameters: dP/dw = -[R X]_x J_left(w), R = I + a K + b K^2, J_left = I + b K + c K^2
+// (a = sin th / th, b = (1 - cos th) / th^2, c = (th - sin th) / th^3; series below th = 1e-8 /
+// 1e-2).  Evaluated in FP64 from the FP64 state (reading C23): residuals in FP64,
+// the Jacobians rounded to JT on output (FP32 for sqrt-BA-32 and explicit-32, FP64 for sqrt-BA-64
+// and explicit-64).
 // Per-camera precomputation (once per state, k_cam_prep): R(w) and J_left(w) as 3x3 matrices plus
 // t, f, k1, k2 -- 24 doubles -- so the per-observation model needs no trigonometry or divisions
-// beyond 1/P_z.  Same formulas as cam_model above.
+// beyond 1/P_z.
 __device__ __forceinline__ void cam_prep(const double *__restrict__ cam, double *pre) {
     const double w0 = cam[0], w1 = cam[1], w2 = cam[2];
     const double th2 = w0 * w0 + w1 * w1 + w2 * w2;
@@ -188,10 +119,6 @@ __device__ __forceinline__ void apply_irls(double *r, JT *Jc, JT *Jl, double del
     for (int i = 0; i < 6; i++) Jl[i] *= wf;
 }
 
-__device__ __forceinline__ void load_cam(const double *__restrict__ cams, int cam, double *c) {
-#pragma unroll
-    for (int q = 0; q < 9; q++) c[q] = __ldg(cams + 9 * cam + q);
-}
 
 // ============================================================================ reductions
 __device__ __forceinline__ double warp_sum_d(double v) {

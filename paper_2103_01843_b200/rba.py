@@ -183,8 +183,15 @@ def rba_lm_step(h) -> dict:
     return r.as_dict()
 
 
-def rba_get_state(h, n_cams, n_points):
-    cams, pts = np.zeros((n_cams, 9)), np.zeros((n_points, 3))
+def rba_get_state(h, n_cams, n_points, out=None):
+    """out: optional (cams (n_cams, 9), pts (n_points, 3)) C-contiguous float64 arrays to fill
+    (e.g. views of pinned host memory)."""
+    if out is None:
+        cams, pts = np.zeros((n_cams, 9)), np.zeros((n_points, 3))
+    else:
+        cams, pts = out
+        assert cams.dtype == pts.dtype == np.float64 and cams.flags.c_contiguous and pts.flags.c_contiguous
+        assert cams.shape == (n_cams, 9) and pts.shape == (n_points, 3)
     _check(_lib.rba_get_state(h, _p(cams), _p(pts)))
     return cams, pts
 
@@ -426,8 +433,8 @@ class Solver:
     def lm_step(self):
         return rba_lm_step(self.h)
 
-    def state(self):
-        return rba_get_state(self.h, self.n_p, self.n_l)
+    def state(self, out=None):
+        return rba_get_state(self.h, self.n_p, self.n_l, out)
 
     def set_state(self, cams, pts):
         rba_set_state(self.h, cams, pts)
