@@ -548,11 +548,16 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
                 c->s64_lo[++cls] = i;
             }
             c->s64_kmax[cls] = std::max<int64_t>(c->s64_kmax[cls], k);
-            c->h_r2[i] = off;
-            off += (int64_t)(2 * k + 3) * (9 * k + 4) + 12;
+            c->h_r2[i] = off;  // rows 3..2k+2 (the reduced rows A | q), consecutive over landmarks
+            off += (int64_t)(2 * k) * (9 * k + 4);
             c->logical_bytes += (int64_t)(2 * k + 3) * (9 * k + 4) * 8 + 96;
             c->matvec_bytes += 8.0 * 2 * k * (9 * k + 1);  // reduced rows A | q read once
             c->marg_bytes += 8.0 * (2 * k + 3) * (9 * k + 4) + 96 + 40.0 * k;
+        }
+        for (int64_t i = 0; i < nl; i++) {  // rows 0..2 and the 12 Givens doubles after all reduced rows
+            const int k = c->h_k[i];
+            c->h_side[i] = off;
+            off += (int64_t)3 * (9 * k + 4) + 12;
         }
         for (int q = cls; q < 5; q++) c->s64_hi[q] = nl;
         for (int q = cls + 1; q < 5; q++) c->s64_lo[q] = nl;
@@ -589,6 +594,46 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
                 c->s64_mlo[g] = c->s64_lo[0] + (c->s64_glo[g] - c->s64_plo[0]);  // one item per landmark
                 c->s64_mhi[g] = c->s64_lo[0] + (c->s64_ghi[g] - c->s64_plo[0]);
             }
+        }
+        {  // k <= 16 (groups of 4 / 8 / 16 lanes): TMA batches of consecutive landmarks; their reduced
+           // rows are contiguous, so one 16-byte-aligned copy per batch (offsets in doubles; arena64
+           // is 16-byte aligned); at most 48 KB, 256 / G landmarks and 256 observations per batch
+            std::vector<int4> bat, rec;
+            for (int g = 0; g < 3; g++) {
+                const int NG = 256 / (4 << g);  // = the consumer groups of k_rcs64_ws (8 warps)
+                c->s64_blo[g] = (int64_t)bat.size();
+                int64_t i = c->s64_mlo[g];
+                while (i < c->s64_mhi[g]) {
+                    int n = 0, nob = 0;
+                    const int64_t ob0 = h_obs0[i], c_lo = ob0 & ~(int64_t)3, lo = c->h_r2[i] & ~(int64_t)1;
+                    int64_t hi = lo;
+                    const size_t r0 = rec.size();
+                    rec.resize(r0 + 64, int4{0, 0, 0, 0});
+                    while (i < c->s64_mhi[g] && n < NG) {
+                        const int64_t k = c->h_k[i], W = 9 * k + 4, end = (c->h_r2[i] + 2 * k * W + 1) & ~(int64_t)1;
+                        if (end - lo > S64_STAGE_DBL || nob + k > 256) break;
+                        rec[r0 + n] = int4{(int)k, (int)(c->h_r2[i] - lo), (int)(h_obs0[i] - c_lo), 0};
+                        hi = end;
+                        nob += (int)k;
+                        n++;
+                        i++;
+                    }
+                    const int64_t c_hi = (ob0 + nob + 3) & ~(int64_t)3;
+                    bat.push_back(int4{n, (int)(hi - lo), (int)c_lo, (int)(c_hi - c_lo)});
+                    rec.push_back(int4{(int)(lo & 0xffffffff), (int)(lo >> 32), 0, 0});  // slot 64: source
+                    rec.resize(r0 + 66, int4{0, 0, 0, 0});
+                }
+                c->s64_bhi[g] = (int64_t)bat.size();
+            }
+            CKSC(dalloc_n(c, &d.s64_batches, std::max<size_t>(1, bat.size())));
+            CKSC(dalloc_n(c, &d.s64_brec, std::max<size_t>(1, rec.size())));
+            if (!bat.empty()) {
+                CKC(cudaMemcpyAsync(d.s64_batches, bat.data(), sizeof(int4) * bat.size(), cudaMemcpyHostToDevice,
+                                    c->stream));
+                CKC(cudaMemcpyAsync(d.s64_brec, rec.data(), sizeof(int4) * rec.size(), cudaMemcpyHostToDevice,
+                                    c->stream));
+            }
+            CKC(cudaStreamSynchronize(c->stream));
         }
         CKSC(dalloc_n(c, &d.rcs_items, std::max<size_t>(1, rcs.size())));
         if (!rcs.empty())
@@ -1073,7 +1118,9 @@ extern "C" rba_status rba_export_block(rba_ctx *c, int64_t landmark, double *buf
         const int64_t R = 2 * k + 3, C = 9 * k + 4;
         *rows = R, *cols = C;
         if (cap < R * C) return fail(RBA_ERR_INVALID_ARG, "buffer too small");
-        CK(cudaMemcpyAsync(buf, c->d.arena64 + c->h_r2[j], sizeof(double) * R * C, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(buf, c->d.arena64 + c->h_side[j], sizeof(double) * 3 * C, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(buf + 3 * C, c->d.arena64 + c->h_r2[j], sizeof(double) * (R - 3) * C, cudaMemcpyDeviceToHost,
+                           c->stream));
         CK(cudaStreamSynchronize(c->stream));
         return RBA_OK;
     }

@@ -16,6 +16,7 @@ constexpr int KSMALL = 16;    // k <= KSMALL: warp-group kernels over packs of s
 constexpr int KLARGE = 512;   // k <= KLARGE: one thread per camera block in the large-k kernels
 constexpr int KMAX = 3072;    // largest track length supported (k > KLARGE: "huge" path, smem-bound)
 constexpr int KMAX64 = 1024;
+constexpr int S64_STAGE_DBL = 6144;  // sqrt-BA-64 small-k TMA stage: 48 KB
 constexpr int CAMPRE = 24;    // doubles of a camera's precomputed model (R, J_left, t, f, k1, k2)  // sqrt-BA-64 (f2): largest track length (registers of the FP64 product)
 
 // ---- landmark-block arena layout ------------------------------------------
@@ -164,6 +165,10 @@ struct DevProblem {
     int s64;
     double *arena64, *lm_s64, *lm_D64;
     LargeItem *rcs_items;  // sqrt-BA-64 product / block-Jacobi items: (landmark, rows [t0, t1) of 3..2k+2)
+    int4 *s64_batches;     // sqrt-BA-64, k <= 16: TMA batches {count, stage doubles, first camera index (16-B
+                           // aligned), camera indices staged}
+    int4 *s64_brec;        // ... and per batch 64 x 2 landmark records {arena offset lo, hi, bytes, stage
+                           // offset}, {k, row-3 offset in the stage, camera offset, 0}
 };
 
 struct Launch {
@@ -205,6 +210,7 @@ struct rba_ctx {
     int64_t s64_plo[5] = {0, 0, 0, 0, 0}, s64_phi[5] = {0, 0, 0, 0, 0};  // their product items
     int64_t s64_glo[4] = {0, 0, 0, 0}, s64_ghi[4] = {0, 0, 0, 0};  // k <= 32 items by group size 4..32
     int64_t s64_mlo[4] = {0, 0, 0, 0}, s64_mhi[4] = {0, 0, 0, 0};  // the same as landmark ranges
+    int64_t s64_blo[3] = {0, 0, 0}, s64_bhi[3] = {0, 0, 0};  // k <= 4 / 8 / 16: their TMA batches
     int64_t cta_off[5] = {0, 0, 0, 0, 0}, cta_n[5] = {0, 0, 0, 0, 0};    // K4/K5 CTA ranges per class
     int64_t n_chunks = 0, chunk_ctas = 0;
     int64_t n_packs = 0, max_large_k = 0;

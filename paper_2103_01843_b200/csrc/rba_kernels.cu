@@ -130,6 +130,19 @@ __device__ __forceinline__ void wy_row(const BlockWY &B, const float4 *VR, const
         out9[q] = c0 * B.jp[0][q] + c1 * B.jp[1][q] - (V.x * B.m[0][q] + V.y * B.m[1][q] + V.z * B.m[2][q]);
 }
 
+// Fast path for the plain rows L in [3, 2k) (no damping rotation involved): the J_p term is
+// nonzero only in the 2 rows of the lane's own observation, so every other lane spends 3 FMA per
+// output (same rounding as wy_row: -(V.M) then + the J_p entry).
+__device__ __forceinline__ void wy_row_plain(const BlockWY &B, const float4 V, int L, int o, float *out9) {
+#pragma unroll
+    for (int q = 0; q < 9; q++) out9[q] = fmaf(-V.z, B.m[2][q], fmaf(-V.y, B.m[1][q], -V.x * B.m[0][q]));
+    if (o == (L >> 1)) {
+        const bool odd = L & 1;
+#pragma unroll
+        for (int q = 0; q < 9; q++) out9[q] += odd ? B.jp[1][q] : B.jp[0][q];
+    }
+}
+
 // M column block from V rows 2o, 2o+1 and T (upper 3x3, entries T00..T22)
 __device__ __forceinline__ void wy_m(BlockWY &B, float4 v0, float4 v1, float T00, float T01, float T02, float T11,
                                      float T12, float T22) {
@@ -207,7 +220,7 @@ __global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProb
     const Pack pack = d.packs[pi];
     const bool valid = grp < pack.np;
     const int64_t j = pack.lm0 + (valid ? grp : 0);
-    const int k = d.lm_k[pack.lm0];
+    const int k = pack.k;  // (the pack's observations are contiguous: no per-landmark index loads)
     const bool act = valid && gl < k;
     float *tab = smem + (warp * NG + grp) * TB::FLOATS;
     float4 *VR = reinterpret_cast<float4 *>(tab);
@@ -220,9 +233,12 @@ __global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProb
 #pragma unroll
     for (int i = 0; i < 6; i++) Jl[i] = 0.f;
     int cam = 0;
+    float spc[9];
     if (act) {
-        const int64_t o = d.lm_obs0[j] + gl;
-        cam = d.obs_cam[o];
+        const int64_t o = (int64_t)pack.obs0 + grp * k + gl;
+        cam = __ldg(d.obs_cam + o);
+#pragma unroll
+        for (int q = 0; q < 9; q++) spc[q] = __ldg(d.sp + 9 * cam + q);  // issued with the camera loads
         double c[CAMPRE], rd[2];
         load_pre(d.campre, cam, c);
         const double *X = d.pts + 3 * j;
@@ -244,7 +260,7 @@ __global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProb
     float X[2][3], rv[2] = {r[0], r[1]};
 #pragma unroll
     for (int q = 0; q < 9; q++) {
-        const float s = act ? d.sp[9 * cam + q] : 0.f;
+        const float s = act ? spc[q] : 0.f;
         B.jp[0][q] = Jc[q] * s;
         B.jp[1][q] = Jc[9 + q] * s;
     }
@@ -362,12 +378,18 @@ __global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProb
     float *blk_side = d.arena + d.lm_side[j];
     float2 *A = reinterpret_cast<float2 *>(d.arena + pack.base);
     const int npk = pack.np * k, mo = grp * k + gl;
-    for (int p = 0; p < k; p++) {
+    float2 *Ap = A + mo;
+    for (int p = 0; p < k; p++, Ap += 9 * npk) {
         float v18[18];
-        wy_row(B, VR, GM, k, 2 * p + 3, gl, v18);
-        wy_row(B, VR, GM, k, 2 * p + 4, gl, v18 + 9);
+        if (p < k - 2) {  // rows 2p+3, 2p+4 < 2k: no damping rows
+            wy_row_plain(B, VR[2 * p + 3], 2 * p + 3, gl, v18);
+            wy_row_plain(B, VR[2 * p + 4], 2 * p + 4, gl, v18 + 9);
+        } else {
+            wy_row(B, VR, GM, k, 2 * p + 3, gl, v18);
+            wy_row(B, VR, GM, k, 2 * p + 4, gl, v18 + 9);
+        }
 #pragma unroll
-        for (int c = 0; c < 9; c++) A[(p * 9 + c) * npk + mo] = make_float2(v18[2 * c], v18[2 * c + 1]);
+        for (int c = 0; c < 9; c++) Ap[c * npk] = make_float2(v18[2 * c], v18[2 * c + 1]);
     }
 #pragma unroll
     for (int s = 0; s < 3; s++) {
@@ -581,14 +603,19 @@ __global__ void __launch_bounds__(NT) k_marg_large(DevProblem d, const LargeItem
         for (int t = it.t0; t < it.t1; t++) {
             float4 *S = reinterpret_cast<float4 *>(R2 + (int64_t)36 * k * t + 36 * 32 * g_) + (o & 31);
             float v36[36];
+            if (4 * t + 6 < 2 * k) {  // logical rows 4t+3 .. 4t+6 are plain rows (< 2k)
 #pragma unroll
-            for (int rr = 0; rr < 4; rr++) {
-                const int a = 4 * t + rr;
-                if (a < 2 * k) {
-                    wy_row(B, VR, GM, k, a + 3, o, v36 + 9 * rr);
-                } else {
+                for (int rr = 0; rr < 4; rr++) wy_row_plain(B, VR[4 * t + rr + 3], 4 * t + rr + 3, o, v36 + 9 * rr);
+            } else {
 #pragma unroll
-                    for (int q = 0; q < 9; q++) v36[9 * rr + q] = 0.f;
+                for (int rr = 0; rr < 4; rr++) {
+                    const int a = 4 * t + rr;
+                    if (a < 2 * k) {
+                        wy_row(B, VR, GM, k, a + 3, o, v36 + 9 * rr);
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 9; q++) v36[9 * rr + q] = 0.f;
+                    }
                 }
             }
 #pragma unroll
@@ -812,50 +839,6 @@ __device__ __forceinline__ float group_sum_rt(float v, int G) {
 }
 __device__ __forceinline__ int group_of(int k) { return k == 2 ? 2 : (k <= 4 ? 4 : (k <= 8 ? 8 : 16)); }
 
-// ---- TMA bulk-copy pipeline for large k (B200: cp.async.bulk + mbarrier, one CTA per SM).
-__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-// streaming variant for the landmark blocks: L2 evict-first, so the read-once R2 stream does not
-// evict the L2-resident camera vectors and per-SM accumulation slices
-__device__ __forceinline__ uint64_t policy_evict_first() {
-    uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ void bulk_g2s_stream(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
-                                                uint64_t pol) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
-        : "memory");
-}
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

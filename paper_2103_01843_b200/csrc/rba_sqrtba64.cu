@@ -9,14 +9,25 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "rba_internal.cuh"
 #include "rba_model.cuh"
 
 namespace rba {
 
-// block of landmark j: B + row * W + col, W = 9k + 4; Givens after the (2k+3) rows
-__device__ __forceinline__ double *blk64(const DevProblem &d, int64_t j) { return d.arena64 + d.lm_r2[j]; }
+// Block of landmark j, rows of W = 9k + 4 doubles: rows 3..2k+2 (the reduced rows A_j | q_j) at
+// lm_r2[j], consecutive over landmarks so the product streams them back to back; rows 0..2 and the 12
+// Givens doubles at lm_side[j] (a second region after all reduced rows).
+struct Blk64 {
+    double *r2, *side;
+    int64_t W;
+    __device__ __forceinline__ double *row(int a) const { return a < 3 ? side + a * W : r2 + (a - 3) * W; }
+    __device__ __forceinline__ double *givens() const { return side + 3 * W; }
+};
+__device__ __forceinline__ Blk64 blk64(const DevProblem &d, int64_t j, int k) {
+    return Blk64{d.arena64 + d.lm_r2[j], d.arena64 + d.lm_side[j], 9 * (int64_t)k + 4};
+}
 
 __device__ __forceinline__ void givens64(double a, double b, double &c, double &s) {
     if (b == 0.0) {
@@ -65,7 +76,6 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 16 : 1) k_marg64(DevProblem d, 
     const int64_t j = it.lm;
     const int r0 = it.t0, r1 = it.t1;
     const int k = d.lm_k[j], tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int W = 9 * k + 4;
     double *SX = s64;           // 2k x 3 (scaled J_l, then R / V)
     double *SR = SX + 6 * k;    // 2k residual column
     double *SV = SR + 2 * k;    // 2k x 3 Householder vectors
@@ -150,7 +160,7 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 16 : 1) k_marg64(DevProblem d, 
     for (int i = 0; i < 9; i++) R[i] = SX[i];
     const double sq = sqrt(lam), sD[3] = {sq * Dl[0], sq * Dl[1], sq * Dl[2]};
     damp64(R, sD, g);
-    double *B = blk64(d, j);
+    const Blk64 B = blk64(d, j, k);
     // pose columns of every row: thread <-> camera block o (warp <-> 32 consecutive blocks); each
     // row's 9 x 32 values of a warp are staged in shared memory and stored as 9 coalesced 256-byte
     // segments (a thread's own 9 values are 72-byte strided across the warp)
@@ -199,7 +209,7 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 16 : 1) k_marg64(DevProblem d, 
 #pragma unroll
             for (int q = 0; q < 9; q++) stage[9 * lane + q] = row[q];
             __syncwarp();
-            double *dst = B + (int64_t)a * W + 9 * wb;
+            double *dst = B.row(a) + 9 * wb;
             for (int i = lane; i < ncol; i += 32) dst[i] = stage[i];
             __syncwarp();
         }
@@ -222,14 +232,14 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 16 : 1) k_marg64(DevProblem d, 
             for (int q = 0; q < 9; q++) stage[9 * lane + q] = xs[q];
             __syncwarp();
             const int row = s < 3 ? s : 2 * k + s - 3;
-            double *dst = B + (int64_t)row * W + 9 * wb;
+            double *dst = B.row(row) + 9 * wb;
             for (int i = lane; i < ncol; i += 32) dst[i] = stage[i];
             __syncwarp();
         }
     }
     // landmark and residual columns (4 per row): R / 0 and Q^T r, damping rows rotated
     for (int a = r0 + tid; a < r1; a += NT) {
-        double *rw = B + (int64_t)a * W + 9 * k;
+        double *rw = B.row(a) + 9 * k;
         if (a >= 3 && a < 2 * k) {
             rw[0] = rw[1] = rw[2] = 0.0;
             rw[3] = SR[a];
@@ -253,9 +263,9 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 16 : 1) k_marg64(DevProblem d, 
         }
         for (int s = 0; s < 6; s++) {
             const int row = s < 3 ? s : 2 * k + s - 3;
-            for (int q = 0; q < 4; q++) B[(int64_t)row * W + 9 * k + q] = X[s][q];
+            for (int q = 0; q < 4; q++) B.row(row)[9 * k + q] = X[s][q];
         }
-        double *G = B + (int64_t)(2 * k + 3) * W;
+        double *G = B.givens();
         for (int i = 0; i < 12; i++) G[i] = g[i];
     }
     if (tid < 3 && r0 == 0) {
@@ -380,8 +390,7 @@ __global__ void __launch_bounds__(256) k_marg64_small(DevProblem d, int64_t lo, 
         M[9 + q] = T01 * W0 + T11 * W1;
         M[18 + q] = T02 * W0 + T12 * W1 + T22 * W2;
     }
-    const int W = 9 * k + 4;
-    double *Bk = valid ? blk64(d, j) : nullptr;
+    const Blk64 Bk = blk64(d, valid ? j : 0, valid ? k : 2);
     double top[27];
     for (int a = 0; a < 64; a++) {  // rows 0..2k-1 (V row a from lane a / 2), warp-uniform bound
         double va[3];
@@ -404,7 +413,7 @@ __global__ void __launch_bounds__(256) k_marg64_small(DevProblem d, int64_t lo, 
             for (int q = 0; q < 9; q++) top[9 * a + q] = row[q];
         } else {
 #pragma unroll
-            for (int q = 0; q < 9; q++) Bk[(int64_t)a * W + 9 * gl + q] = row[q];
+            for (int q = 0; q < 9; q++) Bk.row(a)[9 * gl + q] = row[q];
         }
     }
     if (!act) return;
@@ -421,14 +430,14 @@ __global__ void __launch_bounds__(256) k_marg64_small(DevProblem d, int64_t lo, 
                 x[p] = g[2 * m] * aa + g[2 * m + 1] * bb;
                 x[t] = -g[2 * m + 1] * aa + g[2 * m] * bb;
             }
-            Bk[(int64_t)row * W + 9 * gl + q] = x[sr];
+            Bk.row(row)[9 * gl + q] = x[sr];
         }
     }
 #pragma unroll
     for (int rr = 0; rr < 2; rr++) {  // landmark / residual columns of the lane's rows >= 3
         const int a = 2 * gl + rr;
         if (a >= 3) {
-            double *rw = Bk + (int64_t)a * W + 9 * k;
+            double *rw = Bk.row(a) + 9 * k;
             rw[0] = rw[1] = rw[2] = 0.0;
             rw[3] = rv[rr];
         }
@@ -451,9 +460,9 @@ __global__ void __launch_bounds__(256) k_marg64_small(DevProblem d, int64_t lo, 
         }
         for (int sr = 0; sr < 6; sr++) {
             const int row = sr < 3 ? sr : 2 * k + sr - 3;
-            for (int q = 0; q < 4; q++) Bk[(int64_t)row * W + 9 * k + q] = Xs[sr][q];
+            for (int q = 0; q < 4; q++) Bk.row(row)[9 * k + q] = Xs[sr][q];
         }
-        double *Gp = Bk + (int64_t)(2 * k + 3) * W;
+        double *Gp = Bk.givens();
         for (int i = 0; i < 12; i++) Gp[i] = g[i];
         for (int q = 0; q < 3; q++) {
             d.lm_s[3 * j + q] = (float)sl[q];
@@ -471,15 +480,15 @@ __global__ void __launch_bounds__(256) k_redamp64(DevProblem d, double lam) {
     const int lane = threadIdx.x & 31;
     if (j >= d.n_l) return;
     const int k = d.lm_k[j], W = 9 * k + 4;
-    double *B = blk64(d, j);
-    double *G = B + (int64_t)(2 * k + 3) * W;
+    const Blk64 B = blk64(d, j, k);
+    double *G = B.givens();
     double g[12];
     for (int i = 0; i < 12; i++) g[i] = G[i];
     // R after undo: undo the 6 rotations on the landmark columns (+ damping diag) of rows 0..2
     double X[6][3];
     for (int s = 0; s < 6; s++) {
         const int row = s < 3 ? s : 2 * k + s - 3;
-        for (int q = 0; q < 3; q++) X[s][q] = B[(int64_t)row * W + 9 * k + q];
+        for (int q = 0; q < 3; q++) X[s][q] = B.row(row)[9 * k + q];
     }
     for (int m = 5; m >= 0; m--) {
         const int p = damp_p(m), t = damp_t(m);
@@ -498,7 +507,7 @@ __global__ void __launch_bounds__(256) k_redamp64(DevProblem d, double lam) {
     damp64(R, sD, gn);
     for (int c = lane; c < W; c += 32) {
         double x[6];
-        for (int s = 0; s < 6; s++) x[s] = B[(int64_t)(s < 3 ? s : 2 * k + s - 3) * W + c];
+        for (int s = 0; s < 6; s++) x[s] = B.row(s < 3 ? s : 2 * k + s - 3)[c];
         for (int m = 5; m >= 0; m--) {  // undo
             const int p = damp_p(m), t = damp_t(m);
             const double a = x[p], b = x[t];
@@ -514,12 +523,12 @@ __global__ void __launch_bounds__(256) k_redamp64(DevProblem d, double lam) {
             x[t] = -gn[2 * m + 1] * a + gn[2 * m] * b;
         }
         if (c >= 9 * k && c < 9 * k + 3) x[3 + (c - 9 * k)] = 0.0;  // eliminated exactly
-        for (int s = 0; s < 6; s++) B[(int64_t)(s < 3 ? s : 2 * k + s - 3) * W + c] = x[s];
+        for (int s = 0; s < 6; s++) B.row(s < 3 ? s : 2 * k + s - 3)[c] = x[s];
     }
     __syncwarp();
     if (lane == 0) {
         // lower-triangle entries of R^1 exactly zero
-        B[(int64_t)1 * W + 9 * k] = 0.0, B[(int64_t)2 * W + 9 * k] = 0.0, B[(int64_t)2 * W + 9 * k + 1] = 0.0;
+        B.row(1)[9 * k] = 0.0, B.row(2)[9 * k] = 0.0, B.row(2)[9 * k + 1] = 0.0;
         for (int i = 0; i < 12; i++) G[i] = gn[i];
     }
 }
@@ -539,8 +548,7 @@ __global__ void __launch_bounds__(256) k_rcs64_small(DevProblem d, const LargeIt
     const int64_t j = it.lm;
     const int k = valid ? d.lm_k[j] : 0;
     const bool act = gl < k;
-    const int W = 9 * k + 4;
-    const double *B = valid ? blk64(d, j) : nullptr;
+    const Blk64 B = blk64(d, valid ? j : 0, k > 0 ? k : 2);
     const int32_t *oc = d.obs_cam + (valid ? d.lm_obs0[j] : 0);
     double vo[9], acc[9];
 #pragma unroll
@@ -552,7 +560,7 @@ __global__ void __launch_bounds__(256) k_rcs64_small(DevProblem d, const LargeIt
     for (int r = 0; r < maxrows; r++) {
         double x[9];
         const bool live = act && r < nrows;
-        const double *rw = live ? B + (int64_t)(it.t0 + r) * W + 9 * gl : nullptr;
+        const double *rw = live ? B.row(it.t0 + r) + 9 * gl : nullptr;
 #pragma unroll
         for (int q = 0; q < 9; q++) x[q] = live ? rw[q] : 0.0;
         double y = 0.0;
@@ -580,14 +588,14 @@ __global__ void __launch_bounds__(NT) k_rcs64(DevProblem d, const LargeItem *__r
     // NB: camera blocks per thread (k <= NB * NT in this class)
     const LargeItem it = items[blockIdx.x];  // rows [it.t0, it.t1) of the reduced rows 3..2k+2
     const int64_t j = it.lm;
-    const int k = d.lm_k[j], W = 9 * k + 4, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const double *B = blk64(d, j);
+    const int k = d.lm_k[j], tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const Blk64 B = blk64(d, j, k);
     const int32_t *oc = d.obs_cam + d.lm_obs0[j];
     if (PRE) {
         for (int o = tid; o < k; o += NT) {
             double P[45] = {}, b[9] = {};
             for (int a = it.t0; a < it.t1; a++) {
-                const double *rw = B + (int64_t)a * W;
+                const double *rw = B.row(a);
                 double x[9];
                 for (int q = 0; q < 9; q++) x[q] = rw[9 * o + q];
                 const double qa = rw[9 * k + 3];
@@ -625,7 +633,7 @@ __global__ void __launch_bounds__(NT) k_rcs64(DevProblem d, const LargeItem *__r
         for (int r = 0; r < CR; r++) {
             double s = 0.0;
             if (r < nr) {
-                const double *rw = B + (int64_t)(a0 + r) * W;
+                const double *rw = B.row(a0 + r);
 #pragma unroll
                 for (int m = 0; m < NB; m++) {
                     const int o = tid + m * NT;
@@ -657,13 +665,299 @@ __global__ void __launch_bounds__(NT) k_rcs64(DevProblem d, const LargeItem *__r
 #pragma unroll
                 for (int r = 0; r < CR; r++) {
                     if (r < nr) {
-                        const double *rw = B + (int64_t)(a0 + r) * W + 9 * o;
+                        const double *rw = B.row(a0 + r) + 9 * o;
 #pragma unroll
                         for (int q = 0; q < 9; q++) acc[m][q] += rw[q] * y[r];
                     }
                 }
             }
         }
+    }
+#pragma unroll
+    for (int m = 0; m < NB; m++) {
+        const int o = tid + m * NT;
+        if (o < k) {
+            double *out = d.wd + 9 * (int64_t)oc[o];
+#pragma unroll
+            for (int q = 0; q < 9; q++) atomicAdd(out + q, acc[m][q]);
+        }
+    }
+}
+
+// ---- K4-64 / K5-64 for k <= 16, TMA-staged and warp-specialized: persistent CTA (one per SM) of
+// 8 consumer warps + 1 producer warp, ring of 4 stages of 48 KB.  A stage holds a batch of
+// consecutive landmarks (<= 256 / G): each landmark's reduced rows 3..2k+2 (one cp.async.bulk per
+// landmark, 16-byte-aligned superset), the batch's camera indices (one copy), and a table written
+// by the producer {k, row-3 offset, camera offset}.  Consumers: groups of G lanes <-> landmark
+// (assigned round-robin over the CTA's landmark sequence, so consecutive one-landmark stages go to
+// different warps), lane <-> camera block (72-byte lane stride in shared memory), two rows per
+// step with G-lane shuffle reductions; a warp releases a stage as soon as it is done with it (no
+// CTA-wide barrier).  PRE: block-Jacobi blocks and b~ instead of the product.
+constexpr int WS_CW = 8, WS_S = 4, WS_CAMS = 264;  // consumer warps, stages, camera slots per stage
+template <int G, bool PRE>
+__global__ void __launch_bounds__(32 * (WS_CW + 1), 1) k_rcs64_ws(DevProblem d, const int4 *__restrict__ batches,
+                                                                  const int4 *__restrict__ brec, int nbat,
+                                                                  const double *__restrict__ v,
+                                                                  const PcgState *__restrict__ st) {
+    if (!PRE && st && st->done) return;
+    constexpr int NG = 32 * WS_CW / G, S = WS_S;
+    extern __shared__ __align__(16) double sm64[];  // S x S64_STAGE_DBL
+    __shared__ __align__(16) int32_t cams[S][WS_CAMS];
+    __shared__ int4 tab[S][NG];  // {k, row-3 offset in the stage, camera offset, 0}
+    __shared__ uint64_t full[S], empty[S];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        for (int s = 0; s < S; s++) mbar_init(&full[s], 1), mbar_init(&empty[s], WS_CW);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int nmine = nbat > (int)blockIdx.x ? (nbat - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+    if (warp == WS_CW) {  // ---- producer: batch headers and records prefetched one batch ahead
+        const uint64_t pol = policy_evict_first();
+        constexpr int RL = (NG + 31) / 32;  // records per lane
+        int4 h_nx = make_int4(0, 0, 0, 0), rb_nx[RL], src_nx = make_int4(0, 0, 0, 0);
+        auto fetch = [&](int c) {
+            const int64_t bi = blockIdx.x + (int64_t)c * gridDim.x;
+            h_nx = batches[bi];
+            src_nx = brec[bi * 66 + 64];
+#pragma unroll
+            for (int u = 0; u < RL; u++) {
+                const int i = lane + 32 * u;
+                rb_nx[u] = i < NG ? brec[bi * 66 + i] : make_int4(0, 0, 0, 0);
+            }
+        };
+        if (nmine > 0) fetch(0);
+        for (int c = 0; c < nmine; c++) {
+            const int s = c % S;
+            const int4 h = h_nx, src = src_nx;  // {n, doubles, first camera index, cameras}, {source lo}
+            int4 rb[RL];
+#pragma unroll
+            for (int u = 0; u < RL; u++) rb[u] = rb_nx[u];
+            if (c + 1 < nmine) fetch(c + 1);
+            if (c >= S) mbar_wait(&empty[s], (uint32_t)(((c / S) - 1) & 1));
+#pragma unroll
+            for (int u = 0; u < RL; u++) {
+                const int i = lane + 32 * u;
+                if (i < h.x) tab[s][i] = rb[u];
+            }
+            __syncwarp();
+            if (lane == 0) {
+                const int64_t lo = (int64_t)(uint32_t)src.x | ((int64_t)src.y << 32);
+                mbar_arrive_expect_tx(&full[s], 8u * (uint32_t)h.y + 4u * (uint32_t)h.w);
+                bulk_g2s(cams[s], d.obs_cam + h.z, 4u * (uint32_t)h.w, &full[s]);
+                bulk_g2s_stream(sm64 + (size_t)s * S64_STAGE_DBL, d.arena64 + lo, 8u * (uint32_t)h.y, &full[s], pol);
+            }
+        }
+        return;
+    }
+    // ---- consumers.  A batch has at most NG landmarks, so a group owns at most one landmark per
+    // stage (assigned round-robin over the CTA's landmark sequence).
+    const int gl = lane % G, g = tid / G;  // my group (0 .. NG-1)
+    constexpr int U = G >= 8 ? 4 : 2;      // rows per step
+    int base = 0;                          // landmarks of this CTA's earlier stages
+    for (int c = 0; c < nmine; c++) {
+        const int s = c % S;
+        const int n = batches[blockIdx.x + (int64_t)c * gridDim.x].x;  // (load issued before the wait)
+        mbar_wait(&full[s], (uint32_t)((c / S) & 1));
+        const int m = ((g - base) % NG + NG) % NG;
+        base += n;
+        const int4 e = m < n ? tab[s][m] : make_int4(0, 0, 0, 0);
+        const int cam = gl < e.x ? cams[s][e.z + gl] : 0;
+        double vo[9];
+#pragma unroll
+        for (int q = 0; q < 9; q++) vo[q] = (!PRE && gl < e.x) ? v[9 * (int64_t)cam + q] : 0.0;
+        const double *stg = sm64 + (size_t)s * S64_STAGE_DBL;
+        const int k = e.x, W = 9 * k + 4;
+        const bool act = gl < k;
+        const double *rows = stg + e.y;
+        if (PRE) {
+            double P[45], bb[9];
+#pragma unroll
+            for (int i = 0; i < 45; i++) P[i] = 0.0;
+#pragma unroll
+            for (int i = 0; i < 9; i++) bb[i] = 0.0;
+            if (act)
+                for (int r = 0; r < 2 * k; r++) {
+                    const double *x = rows + r * W + 9 * gl;
+                    const double qa = rows[r * W + 9 * k + 3];
+                    int idx = 0;
+#pragma unroll
+                    for (int q1 = 0; q1 < 9; q1++) {
+                        const double x1 = x[q1];
+                        bb[q1] = fma(x1, qa, bb[q1]);
+#pragma unroll
+                        for (int q2 = q1; q2 < 9; q2++, idx++) P[idx] = fma(x1, x[q2], P[idx]);
+                    }
+                }
+            if (act) {
+                double *acc = d.pd + 54 * (int64_t)cam;
+#pragma unroll
+                for (int i = 0; i < 45; i++) atomicAdd(acc + i, P[i]);
+#pragma unroll
+                for (int i = 0; i < 9; i++) atomicAdd(acc + 45 + i, bb[i]);
+            }
+        } else {
+            double acc[9];
+#pragma unroll
+            for (int q = 0; q < 9; q++) acc[q] = 0.0;
+            int maxrows = 2 * k;
+#pragma unroll
+            for (int sh = 16; sh; sh >>= 1) maxrows = max(maxrows, __shfl_xor_sync(0xffffffffu, maxrows, sh));
+            for (int r = 0; r < maxrows; r += U) {  // U rows per step
+                double x[U][9], y[U];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const bool live = act && r + u < 2 * k;
+                    const double *p = rows + (r + u) * W + 9 * gl;
+                    y[u] = 0.0;
+#pragma unroll
+                    for (int q = 0; q < 9; q++) {
+                        x[u][q] = live ? p[q] : 0.0;
+                        y[u] = fma(x[u][q], vo[q], y[u]);
+                    }
+                }
+#pragma unroll
+                for (int sh = G / 2; sh; sh >>= 1)
+#pragma unroll
+                    for (int u = 0; u < U; u++) y[u] += __shfl_xor_sync(0xffffffffu, y[u], sh, G);
+#pragma unroll
+                for (int u = 0; u < U; u++)
+#pragma unroll
+                    for (int q = 0; q < 9; q++) acc[q] = fma(x[u][q], y[u], acc[q]);
+            }
+            if (act) {
+                double *out = d.wd + 9 * (int64_t)cam;
+#pragma unroll
+                for (int q = 0; q < 9; q++) atomicAdd(out + q, acc[q]);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+}
+
+// ---- K5-64 for k > 32, TMA-staged: CTA per item (rows [t0, t1) of the reduced rows 3..2k+2 of one
+// landmark, ~1 MB).  The rows are contiguous in the row-major block, so chunks of CR rows go
+// HBM -> shared memory with one cp.async.bulk each (16-byte-aligned superset; the 8-byte offset of
+// odd-k rows is skipped in shared memory) through an S-stage mbarrier ring, L2 evict-first.  Thread
+// <-> camera blocks o = tid + m NT: per chunk, partial dots over its 9-column segments (shared-memory
+// reads at a 72-byte lane stride: conflict-free per half-warp), y_a reduced across the CTA, then
+// out_o += A[a, o]^T y_a from the same staged rows.  One HBM read of A_j per product.
+template <int NT, int NB, bool PRE>
+__global__ void __launch_bounds__(NT) k_rcs64_tma(DevProblem d, const LargeItem *__restrict__ items,
+                                                  const double *__restrict__ v, const PcgState *__restrict__ st,
+                                                  int CRMAX, int S, int stage_dbl) {
+    static_assert(!PRE || NB == 1, "block-Jacobi blocks: one camera block per thread");
+    if (!PRE && st && st->done) return;
+    extern __shared__ __align__(16) double sm64[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(sm64 + (size_t)S * stage_dbl);
+    double *part = reinterpret_cast<double *>(full + S);  // CRMAX x (NT / 32)
+    const LargeItem it = items[blockIdx.x];
+    const int64_t j = it.lm;
+    const int k = d.lm_k[j], W = 9 * k + 4, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int CR = CRMAX;  // rows per stage (sized for the class's longest track)
+    const double *B = d.arena64 + d.lm_r2[j] - 3 * (int64_t)W;  // row a at B + a W for a >= 3
+    const int nrows = it.t1 - it.t0, nch = (nrows + CR - 1) / CR;
+    if (tid == 0) {
+        for (int s = 0; s < S; s++) mbar_init(&full[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const uint64_t pol = policy_evict_first();
+    auto issue = [&](int c) {  // thread 0: chunk c -> stage c % S
+        const int a0 = it.t0 + c * CR, nr = min(CR, it.t1 - a0);
+        const uintptr_t lo = reinterpret_cast<uintptr_t>(B + (int64_t)a0 * W) & ~(uintptr_t)15;
+        const uintptr_t hi = (reinterpret_cast<uintptr_t>(B + (int64_t)(a0 + nr) * W) + 15) & ~(uintptr_t)15;
+        uint64_t *bar = &full[c % S];
+        mbar_arrive_expect_tx(bar, (uint32_t)(hi - lo));
+        bulk_g2s_stream(sm64 + (size_t)(c % S) * stage_dbl, reinterpret_cast<const void *>(lo), (uint32_t)(hi - lo),
+                        bar, pol);
+    };
+    if (tid == 0)
+        for (int c = 0; c < min(S, nch); c++) issue(c);
+    const int32_t *oc = d.obs_cam + d.lm_obs0[j];
+    if (PRE) {
+        double P[45], bb[9];
+#pragma unroll
+        for (int i = 0; i < 45; i++) P[i] = 0.0;
+#pragma unroll
+        for (int i = 0; i < 9; i++) bb[i] = 0.0;
+        for (int c = 0; c < nch; c++) {
+            const int s = c % S, a0 = it.t0 + c * CR, nr = min(CR, it.t1 - a0);
+            mbar_wait(&full[s], (uint32_t)((c / S) & 1));
+            const double *rows =
+                sm64 + (size_t)s * stage_dbl + ((reinterpret_cast<uintptr_t>(B + (int64_t)a0 * W) >> 3) & 1);
+            if (tid < k)
+                for (int r = 0; r < nr; r++) {
+                    const double *x = rows + r * W + 9 * tid;
+                    const double qa = rows[r * W + 9 * k + 3];
+                    int idx = 0;
+#pragma unroll
+                    for (int q1 = 0; q1 < 9; q1++) {
+                        const double x1 = x[q1];
+                        bb[q1] = fma(x1, qa, bb[q1]);
+#pragma unroll
+                        for (int q2 = q1; q2 < 9; q2++, idx++) P[idx] = fma(x1, x[q2], P[idx]);
+                    }
+                }
+            __syncthreads();
+            if (tid == 0 && c + S < nch) issue(c + S);
+        }
+        if (tid < k) {
+            double *acc = d.pd + 54 * (int64_t)oc[tid];
+#pragma unroll
+            for (int i = 0; i < 45; i++) atomicAdd(acc + i, P[i]);
+#pragma unroll
+            for (int i = 0; i < 9; i++) atomicAdd(acc + 45 + i, bb[i]);
+        }
+        return;
+    }
+    double acc[NB][9], vo[NB][9];
+#pragma unroll
+    for (int m = 0; m < NB; m++) {
+        const int o = tid + m * NT;
+#pragma unroll
+        for (int q = 0; q < 9; q++) {
+            acc[m][q] = 0.0;
+            vo[m][q] = o < k ? v[9 * (int64_t)oc[o] + q] : 0.0;
+        }
+    }
+    constexpr int NW = NT / 32;
+    for (int c = 0; c < nch; c++) {
+        const int s = c % S, a0 = it.t0 + c * CR, nr = min(CR, it.t1 - a0);
+        mbar_wait(&full[s], (uint32_t)((c / S) & 1));
+        const double *rows = sm64 + (size_t)s * stage_dbl + ((reinterpret_cast<uintptr_t>(B + (int64_t)a0 * W) >> 3) & 1);
+        for (int r = 0; r < nr; r++) {
+            double y = 0.0;
+#pragma unroll
+            for (int m = 0; m < NB; m++) {
+                const int o = tid + m * NT;
+                if (o < k) {
+                    const double *x = rows + r * W + 9 * o;
+#pragma unroll
+                    for (int q = 0; q < 9; q++) y = fma(x[q], vo[m][q], y);
+                }
+            }
+            y = warp_sum_d(y);
+            if (lane == 0) part[r * NW + warp] = y;
+        }
+        __syncthreads();
+        for (int r = 0; r < nr; r++) {
+            double y = 0.0;
+#pragma unroll
+            for (int w = 0; w < NW; w++) y += part[r * NW + w];
+#pragma unroll
+            for (int m = 0; m < NB; m++) {
+                const int o = tid + m * NT;
+                if (o < k) {
+                    const double *x = rows + r * W + 9 * o;
+#pragma unroll
+                    for (int q = 0; q < 9; q++) acc[m][q] = fma(x[q], y, acc[m][q]);
+                }
+            }
+        }
+        __syncthreads();  // stage s and part free
+        if (tid == 0 && c + S < nch) issue(c + S);
     }
 #pragma unroll
     for (int m = 0; m < NB; m++) {
@@ -684,7 +978,7 @@ __global__ void __launch_bounds__(256) k_backsub64(DevProblem d, double lam) {
     double q1 = 0.0, dd = 0.0;
     for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < d.n_l; j += nwarps) {
         const int k = d.lm_k[j], W = 9 * k + 4;
-        const double *B = blk64(d, j);
+        const double *B = d.arena64 + d.lm_side[j];  // rows 0..2
         const int32_t *oc = d.obs_cam + d.lm_obs0[j];
         double s0 = 0.0, s1 = 0.0, s2 = 0.0;
         for (int c = lane; c < 9 * k; c += 32) {
@@ -776,9 +1070,64 @@ static void rcs64_cls(rba_ctx *c, int cls, const double *v, const PcgState *st) 
     c->launches++;
 }
 
+// TMA-staged product / block-Jacobi blocks for the rcs items [lo, hi) (tracks up to kmax): stages
+// of CR rows (~32 KB, at least one row), S <= 3
+template <int NT, int NB, bool PRE>
+static void rcs64_tma_range(rba_ctx *c, int64_t lo, int64_t hi, int64_t kmax, const double *v, const PcgState *st) {
+    if (hi <= lo) return;
+    const int64_t W = 9 * kmax + 4;
+    // stages of ~32 KB (at least one row of the class's longest track); S = 3 keeps 2 CTAs per SM
+    // (1 CTA per SM measured 2x slower: the per-item start-up is then exposed)
+    const int CRMAX = (int)std::max<int64_t>(1, 4096 / W);
+    const int stage_dbl = (int)((CRMAX * W + 2 + 1) & ~(int64_t)1);
+    const size_t fixed = 8 * 4 + sizeof(double) * CRMAX * (NT / 32);
+    int S = 3;
+    while (S > 2 && sizeof(double) * S * (size_t)stage_dbl + fixed > 200 * 1024) S--;
+    const size_t sm = sizeof(double) * S * (size_t)stage_dbl + fixed;
+    cudaFuncSetAttribute(k_rcs64_tma<NT, NB, PRE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_rcs64_tma<NT, NB, PRE><<<(unsigned)(hi - lo), NT, sm, c->stream>>>(c->d, c->d.rcs_items + lo, v, st, CRMAX,
+                                                                         S, stage_dbl);
+    c->launches++;
+}
+template <int NT, int NB, bool PRE>
+static void rcs64_tma_cls(rba_ctx *c, int cls, const double *v, const PcgState *st) {
+    rcs64_tma_range<NT, NB, PRE>(c, c->s64_plo[cls], c->s64_phi[cls], c->s64_kmax[cls], v, st);
+}
+// k <= 16 by group size 4 / 8 / 16: persistent warp-specialized TMA-batch kernel
+template <bool PRE>
+static void rcs64_small_tma(rba_ctx *c, const double *v, const PcgState *st) {
+    const size_t sm = sizeof(double) * WS_S * (size_t)S64_STAGE_DBL;
+    for (int g = 0; g < 3; g++) {
+        const int64_t lo = c->s64_blo[g], n = c->s64_bhi[g] - lo;
+        if (n <= 0) continue;
+        const unsigned grid = (unsigned)std::min<int64_t>(n, c->num_sms);
+        const int4 *bp = c->d.s64_batches + lo, *rp = c->d.s64_brec + 66 * lo;
+#define RBA_WS64(GG)                                                                                       \
+    do {                                                                                                   \
+        cudaFuncSetAttribute(k_rcs64_ws<GG, PRE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+        k_rcs64_ws<GG, PRE><<<grid, 32 * (WS_CW + 1), sm, c->stream>>>(c->d, bp, rp, (int)n, v, st);     \
+    } while (0)
+        if (g == 0) RBA_WS64(4);
+        else if (g == 1) RBA_WS64(8);
+        else RBA_WS64(16);
+#undef RBA_WS64
+        c->launches++;
+    }
+}
+
 // wd = sum_j A_j^T A_j v (FP64 atomics; wd zeroed here)
 void launch_rcs64(rba_ctx *c, const double *v, const PcgState *st) {
     cudaMemsetAsync(c->d.wd, 0, sizeof(double) * 9 * c->d.n_p, c->stream);
+    static const bool ldg = getenv("RBA_RCS64_LDG") != nullptr;  // the direct-load kernels (A/B timing)
+    if (!ldg) {
+        rcs64_small_tma<false>(c, v, st);
+        rcs64_tma_range<32, 1, false>(c, c->s64_glo[3], c->s64_ghi[3], 32, v, st);  // 16 < k <= 32
+        rcs64_tma_cls<128, 1, false>(c, 1, v, st);
+        rcs64_tma_cls<256, 1, false>(c, 2, v, st);
+        rcs64_tma_cls<256, 2, false>(c, 3, v, st);
+        rcs64_tma_cls<256, KMAX64 / 256, false>(c, 4, v, st);
+        return;
+    }
     for (int g = 0; g < 4; g++) {  // k <= 32 by group size 4 / 8 / 16 / 32
         const int64_t lo = c->s64_glo[g], hi = c->s64_ghi[g];
         if (hi <= lo) continue;
@@ -799,9 +1148,17 @@ void launch_rcs64(rba_ctx *c, const double *v, const PcgState *st) {
 
 void launch_pre64(rba_ctx *c) {
     cudaMemsetAsync(c->d.pd, 0, sizeof(double) * 54 * c->d.n_p, c->stream);
-    rcs64_cls<32, 1, true>(c, 0, nullptr, nullptr);
-    rcs64_cls<128, 1, true>(c, 1, nullptr, nullptr);
-    rcs64_cls<256, 1, true>(c, 2, nullptr, nullptr);
+    static const bool ldg = getenv("RBA_RCS64_LDG") != nullptr;
+    if (!ldg) {
+        rcs64_small_tma<true>(c, nullptr, nullptr);
+        rcs64_tma_range<32, 1, true>(c, c->s64_glo[3], c->s64_ghi[3], 32, nullptr, nullptr);
+        rcs64_tma_cls<128, 1, true>(c, 1, nullptr, nullptr);
+        rcs64_tma_cls<256, 1, true>(c, 2, nullptr, nullptr);
+    } else {
+        rcs64_cls<32, 1, true>(c, 0, nullptr, nullptr);
+        rcs64_cls<128, 1, true>(c, 1, nullptr, nullptr);
+        rcs64_cls<256, 1, true>(c, 2, nullptr, nullptr);
+    }
     rcs64_cls<256, 2, true>(c, 3, nullptr, nullptr);
     rcs64_cls<256, KMAX64 / 256, true>(c, 4, nullptr, nullptr);
 }
