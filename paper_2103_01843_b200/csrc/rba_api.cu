@@ -690,7 +690,9 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
         CKSC(dalloc_n(c, &d.pcg, 1));
         CKC(query_nsmid(c, reinterpret_cast<int *>(d.pcg), &nsm));
         d.nslice = std::max(nsm, 1);
+        CKC(cudaMemsetAsync(d.pcg, 0, sizeof(PcgState), c->stream));
     }
+    CKSC(dalloc_n(c, &d.pcg_part, 2 * ((9 * n_cams + 31) / 32) + 64));
     CKSC(dalloc_n(c, &d.psl, (int64_t)d.nslice * PACC_STRIDE * n_cams));
     CKSC(dalloc_n(c, &d.wsl, (int64_t)d.nslice * 12 * n_cams));
     CKC(cudaMemsetAsync(d.psl, 0, sizeof(float) * d.nslice * PACC_STRIDE * n_cams, c->stream));

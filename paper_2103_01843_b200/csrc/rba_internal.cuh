@@ -82,6 +82,8 @@ struct PcgState {
     double r0;  // |rho_0|
     double rn;  // |rho_k|
     int it, done, reason, active;
+    double alpha, beta;       // step lengths of the current iteration (multi-CTA update kernels)
+    unsigned int ctr_a, ctr_b;  // last-CTA-done counters of k_pcg_a / k_pcg_b (reset by that CTA)
 };
 
 // double scalars on the device (single buffer so one all-reduce covers them)
@@ -142,6 +144,7 @@ struct DevProblem {
     float *dl;
     double *scal;
     PcgState *pcg;
+    double *pcg_part;  // per-CTA partial dot products of the PCG update kernels (fixed-order sums)
     Pack *packs;            // small-k packs, classes G = 2, 4, 8, 16 back to back
     uint16_t *units;        // small-k work units per stage
     LargeItem *marg_items;  // K2 work items (~1 MB of output each), classes NT = 64, 128, 256, 512
@@ -235,6 +238,7 @@ struct rba_ctx {
     cudaGraphExec_t pcg_exec = nullptr;
     bool pcg_graph_failed = false;
     int64_t graph_body_kernels = 0;  // kernels per PCG-graph iteration (launch accounting)
+    bool pcg_fused = false;          // the last PCG product left its sum in the per-SM slices
     bool profiling = false;
     int64_t prof_real_matvecs = 0;  // matvecs that did work (PCG iterations + hook calls) since rba_profile
     std::vector<rba::Launch> prof;

@@ -1430,6 +1430,156 @@ __device__ __forceinline__ void precond_apply(const DevProblem &d, const double 
     }
 }
 
+// ---- one PCG iteration as three multi-CTA kernels (the single-CTA k_pcg_step is latency-bound at
+// ~60 us on config 4).  Dots are per-CTA partials summed in a fixed order by the last CTA to finish
+// (threadfence + counter), so the result does not depend on CTA scheduling.
+__device__ __forceinline__ bool last_cta(unsigned int *ctr) {
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(ctr, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last) __threadfence();
+    return last;
+}
+__device__ __forceinline__ double sum_parts(const double *part, int n, int stride, double *red) {
+    double t = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) t += __ldcg(part + (int64_t)i * stride);  // (L2: other CTAs' writes)
+    return block_sum_d(t, red);
+}
+
+// A: w = wd + lambda D_p^2 p, with wd = the sum of the per-SM slices (fused: 32 outputs x 8 slice
+// phases per CTA, slices zeroed for the next product) or already in wd (all-reduced / other
+// storage); then alpha = rho^T z / p^T w, or done with "indefinite" if p^T w <= 0.
+__global__ void __launch_bounds__(256) k_pcg_a(DevProblem d, float lam_f, int fuse, cudaGraphConditionalHandle h,
+                                               int use_h) {
+    __shared__ double part[8][33];
+    __shared__ double red[32];
+    PcgState *st = d.pcg;
+    if (st->done) {
+        if (use_h && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(h, 0);
+        return;
+    }
+    const double lam = lam_f < 0.f ? d.scal[SC_LAM] : (double)lam_f;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int64_t N = 9 * d.n_p, i = (int64_t)blockIdx.x * 32 + tx;
+    double s = 0.0;
+    if (i < N) {
+        if (fuse) {
+            const int64_t cam = i / 9, e = 12 * cam + (i - 9 * cam), S = 12 * d.n_p;
+            float a[24];
+#pragma unroll
+            for (int u = 0; u < 24; u++) {  // all loads first (nslice <= 192 here), then the zeroing
+                const int k = ty + 8 * u;
+                a[u] = k < d.nslice ? d.wsl[k * S + e] : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < 24; u++) {
+                const int k = ty + 8 * u;
+                if (k < d.nslice) d.wsl[k * S + e] = 0.f;
+            }
+            for (int k = ty + 8 * 24; k < d.nslice; k += 8) {  // (more than 192 SMs)
+                s += (double)d.wsl[k * S + e];
+                d.wsl[k * S + e] = 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < 24; u += 4) s += ((double)a[u] + (double)a[u + 1]) + ((double)a[u + 2] + (double)a[u + 3]);
+        } else if (ty == 0) {
+            s = d.wd[i];
+        }
+    }
+    part[ty][tx] = s;
+    __syncthreads();
+    double pw = 0.0;
+    if (ty == 0 && i < N) {
+        double t = 0.0;
+#pragma unroll
+        for (int y = 0; y < 8; y++) t += part[y][tx];
+        if (fuse) d.wd[i] = t;
+        const double w = t + lam * d.Dp264[i] * d.p[i];
+        d.w[i] = w;
+        pw = d.p[i] * w;
+    }
+    pw = block_sum_d(pw, red);
+    if (threadIdx.x == 0) d.pcg_part[blockIdx.x] = pw;
+    if (!last_cta(&st->ctr_a)) return;
+    pw = sum_parts(d.pcg_part, gridDim.x, 1, red);
+    if (threadIdx.x == 0) {
+        st->ctr_a = 0;
+        if (!(pw > 0.0)) {
+            st->done = 1, st->reason = 2;
+            if (use_h) cudaGraphSetConditional(h, 0);
+        } else {
+            st->alpha = st->rz / pw;
+        }
+    }
+}
+
+// B: thread <-> camera: x += alpha p, rho -= alpha w, z = M^-1 rho (9 x 9 block); |rho|, rho^T z;
+// the last CTA decides convergence (C11) / max iterations and forms beta.
+__global__ void __launch_bounds__(128) k_pcg_b(DevProblem d, double tol, int max_iters, cudaGraphConditionalHandle h,
+                                               int use_h) {
+    __shared__ double red[32];
+    PcgState *st = d.pcg;
+    if (st->done) return;  // (A already cleared the condition)
+    const double alpha = st->alpha;
+    const int64_t cam = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double rr = 0.0, rz = 0.0;
+    if (cam < d.n_p) {
+        double r[9];
+#pragma unroll
+        for (int q = 0; q < 9; q++) {
+            const int64_t i = 9 * cam + q;
+            d.x[i] += alpha * d.p[i];
+            r[q] = d.r[i] - alpha * d.w[i];
+            d.r[i] = r[q];
+            rr += r[q] * r[q];
+        }
+        const double *M = d.Minv + 81 * cam;
+#pragma unroll
+        for (int a = 0; a < 9; a++) {
+            double z = 0.0;
+#pragma unroll
+            for (int b = 0; b < 9; b++) z += M[9 * a + b] * r[b];
+            d.z[9 * cam + a] = z;
+            rz += r[a] * z;
+        }
+    }
+    rr = block_sum_d(rr, red);
+    rz = block_sum_d(rz, red);
+    if (threadIdx.x == 0) d.pcg_part[2 * blockIdx.x] = rr, d.pcg_part[2 * blockIdx.x + 1] = rz;
+    if (!last_cta(&st->ctr_b)) return;
+    rr = sum_parts(d.pcg_part, gridDim.x, 2, red);
+    rz = sum_parts(d.pcg_part + 1, gridDim.x, 2, red);
+    if (threadIdx.x == 0) {
+        st->ctr_b = 0;
+        const int it = st->it + 1;
+        st->it = it;
+        st->rn = sqrt(rr);
+        int stop = 0;
+        if (sqrt(rr) <= tol * st->r0) stop = 1, st->reason = 0;
+        else if (it >= max_iters) stop = 1, st->reason = 1;
+        if (stop) st->done = 1;
+        if (use_h) cudaGraphSetConditional(h, stop ? 0 : 1);
+        st->beta = rz / st->rz;
+        st->rz = rz;
+    }
+}
+
+// C: p = z + beta p (and its FP32 copy for the product)
+__global__ void __launch_bounds__(256) k_pcg_c(DevProblem d) {
+    const PcgState *st = d.pcg;
+    if (st->done) return;
+    const double beta = st->beta;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 9 * d.n_p) return;
+    const double pn = d.z[i] + beta * d.p[i];
+    d.p[i] = pn;
+    d.p32[i] = (float)pn;
+}
+
 // PCG vectors (x, rho, z, p, w) are FP64 (9 n_p each, reading C24); the matvec reads p as FP32 (p32).
 __global__ void __launch_bounds__(1024) k_pcg_init(DevProblem d) {
     __shared__ double red[32];
@@ -1844,11 +1994,13 @@ cudaError_t launch_precond_finalize(rba_ctx *c, float lam) {
     return cudaGetLastError();
 }
 
-// wd = (H~ - lambda D_p^2) v: sqrt-BA product (Eq. cg_mult) or, in explicit-SC mode, the BSR SpMV
-static void matvec_body(rba_ctx *c, const float *v, const PcgState *st) {
+// wd = (H~ - lambda D_p^2) v: sqrt-BA product (Eq. cg_mult) or, in explicit-SC mode, the BSR SpMV.
+// reduce = false: leave the sum in the per-SM slices (k_pcg_a reduces them); returns whether the
+// product went to the slices.
+static bool matvec_body(rba_ctx *c, const float *v, const PcgState *st, bool reduce = true) {
     if (c->d.sc) {
         launch_sc_spmv(c, st, st ? nullptr : v);
-        return;
+        return false;
     }
     if (c->d.s64) {  // sqrt-BA-64: FP64 product straight into wd
         const double *v64 = c->d.p;
@@ -1857,11 +2009,12 @@ static void matvec_body(rba_ctx *c, const float *v, const PcgState *st) {
             v64 = c->d.z;
         }
         launch_rcs64(c, v64, st);
-        return;
+        return false;
     }
     if (c->d.fac) launch_fac_matvec(c, v, st);
     else pipes_all<false>(c, v, c->d.wsl, st);
-    reduce_slices(c, c->d.wsl, 12, 9, c->d.wd, st);
+    if (reduce) reduce_slices(c, c->d.wsl, 12, 9, c->d.wd, st);
+    return true;
 }
 
 static cudaError_t matvec_impl(rba_ctx *c, const float *v, const PcgState *st) {
@@ -1873,7 +2026,13 @@ static cudaError_t matvec_impl(rba_ctx *c, const float *v, const PcgState *st) {
 
 // wd = sum_j A_j^T (A_j v_j) in FP64 (callers all-reduce it afterwards)
 cudaError_t launch_matvec(rba_ctx *c, const float *v, float *) { return matvec_impl(c, v, nullptr); }
-cudaError_t launch_matvec_pcg(rba_ctx *c) { return matvec_impl(c, c->d.p32, c->d.pcg); }
+// PCG iteration product: the slices are reduced by k_pcg_a unless the result is all-reduced first
+cudaError_t launch_matvec_pcg(rba_ctx *c) {
+    Prof P(c, KID_MATVEC, plan_matvec_bytes(c));
+    c->pcg_fused = matvec_body(c, c->d.p32, c->d.pcg, c->have_comm);
+    P.end();
+    return cudaGetLastError();
+}
 
 cudaError_t launch_add_damping(rba_ctx *c, const float *v, float *out, float lam) {
     k_add_damping<<<nblk(9 * c->d.n_p, 256), 256, 0, c->stream>>>(c->d, v, out, lam);
@@ -1887,11 +2046,27 @@ cudaError_t launch_pcg_init(rba_ctx *c, float, int) {
     return cudaGetLastError();
 }
 
+static void pcg_update(rba_ctx *c, cudaStream_t s, float lam, double tol, int max_iters, bool fuse,
+                       cudaGraphConditionalHandle h, int use_h) {
+    const int64_t N = 9 * c->d.n_p;
+    k_pcg_a<<<(unsigned)((N + 31) / 32), 256, 0, s>>>(c->d, lam, fuse ? 1 : 0, h, use_h);
+    k_pcg_b<<<nblk(c->d.n_p, 128), 128, 0, s>>>(c->d, tol, max_iters, h, use_h);
+    k_pcg_c<<<nblk(N, 256), 256, 0, s>>>(c->d);
+    c->launches += 3;
+}
+
 cudaError_t launch_pcg_step(rba_ctx *c, float lam, float tol, int max_iters) {
     Prof P(c, KID_PCG, 0.0);
-    k_pcg_step<<<1, 1024, 0, c->stream>>>(c->d, lam, (double)tol, max_iters, 0, 0);
+    static const bool single = getenv("RBA_PCG_SINGLE_CTA") != nullptr;  // the single-CTA step (A/B)
+    if (single) {
+        if (c->pcg_fused) reduce_slices(c, c->d.wsl, 12, 9, c->d.wd, c->d.pcg);
+        k_pcg_step<<<1, 1024, 0, c->stream>>>(c->d, lam, (double)tol, max_iters, 0, 0);
+        c->launches++;
+    } else {
+        pcg_update(c, c->stream, lam, tol, max_iters, c->pcg_fused, 0, 0);
+    }
+    c->pcg_fused = false;
     P.end();
-    c->launches++;
     return cudaGetLastError();
 }
 
@@ -1919,11 +2094,18 @@ cudaError_t build_pcg_graph(rba_ctx *c) {
     const int64_t nl = c->launches;
     c->stream = cs;
     c->profiling = false;
-    matvec_body(c, c->d.p32, c->d.pcg);
-    k_pcg_step<<<1, 1024, 0, cs>>>(c->d, -1.f, c->opt.pcg_rel_tol, c->opt.pcg_max_iters, h, 1);
+    static const bool single = getenv("RBA_PCG_SINGLE_CTA") != nullptr;
+    if (single) {
+        matvec_body(c, c->d.p32, c->d.pcg);
+        k_pcg_step<<<1, 1024, 0, cs>>>(c->d, -1.f, c->opt.pcg_rel_tol, c->opt.pcg_max_iters, h, 1);
+        c->launches++;
+    } else {
+        const bool fuse = matvec_body(c, c->d.p32, c->d.pcg, false);
+        pcg_update(c, cs, -1.f, c->opt.pcg_rel_tol, c->opt.pcg_max_iters, fuse, h, 1);
+    }
     c->stream = saved;
     c->profiling = prof;
-    c->graph_body_kernels = c->launches - nl + 1;  // kernel nodes per loop iteration
+    c->graph_body_kernels = c->launches - nl;  // kernel nodes per loop iteration
     c->launches = nl;
     cudaGraph_t captured;
     e = cudaStreamEndCapture(cs, &captured);
