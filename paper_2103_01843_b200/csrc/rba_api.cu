@@ -319,7 +319,8 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     // ---- R2 arena: packs of same-k small landmarks (classes G = 2, 4, 8, 16), then large ones
     std::vector<Pack> packs;
     const int bounds[4] = {2, 4, 8, 16};
-    int64_t r2_total = 0, pos = 0;
+    int64_t r2_total = 0, pos = 0, q_total = 0;
+    c->h_q.assign(nl, -1);
     for (int cls = 0; cls < 4; cls++) {
         const int NG = 32 / bounds[cls];
         c->pack_lo[cls] = (int64_t)packs.size();
@@ -327,11 +328,13 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
             const int k = c->h_k[pos];
             int np = 0;
             while (pos + np < nl && np < NG && c->h_k[pos + np] == k) np++;
-            packs.push_back(Pack{(int32_t)pos, np, r2_total, h_obs0[pos], k, 0, 0});
+            packs.push_back(Pack{(int32_t)pos, np, r2_total, h_obs0[pos], k, (int32_t)q_total, 0});
             for (int m = 0; m < np; m++) {
                 c->h_r2[pos + m] = r2_total;
                 c->h_pk[pos + m] = m | (np << 8);
+                c->h_q[pos + m] = (int32_t)(q_total + 2 * k * m);
             }
+            q_total += 2 * k * np;
             r2_total += pad4(small_pack_floats(k, np));
             pos += np;
         }
@@ -353,13 +356,18 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
         while (q < c->n_packs) {
             const int64_t pb = 4 * pad4(small_pack_floats(packs[q].k, packs[q].np));
             const int32_t ce = (packs[q].obs0 + packs[q].np * packs[q].k + 3) & ~3;
-            if (q > p0 && (bytes + pb > SMALL_STAGE_BYTES || ce - cam0 > 320 || q - p0 >= 64)) break;
+            const int32_t qe = (packs[q].q0 + 2 * packs[q].np * packs[q].k + 3) & ~3;
+            if (q > p0 && (bytes + pb > SMALL_STAGE_BYTES || ce - cam0 > 320 || q - p0 >= 64 ||
+                           qe - (packs[p0].q0 & ~3) > SP_QCAP))
+                break;
             bytes += pb;
             cam_end = ce;
             q++;
         }
         ch.np = (int32_t)(q - p0);
         ch.bytes = (int32_t)bytes;
+        ch.q0 = packs[p0].q0 & ~3;
+        ch.nq = ((packs[q - 1].q0 + 2 * packs[q - 1].np * packs[q - 1].k + 3) & ~3) - ch.q0;
         ch.cam0 = cam0;
         ch.ncam = cam_end - cam0;
         ch.unit0 = (int32_t)units.size();
@@ -520,6 +528,8 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     CKSC(dalloc_n(c, &d.lm_k, nl));
     CKSC(dalloc_n(c, &d.lm_obs0, nl));
     CKSC(dalloc_n(c, &d.lm_pk, nl));
+    CKSC(dalloc_n(c, &d.lm_q, nl));
+    CKSC(dalloc_n(c, &d.qpk, q_total + 8));
     CKSC(dalloc_n(c, &d.lm_r2, nl));
     CKSC(dalloc_n(c, &d.lm_side, nl));
     CKSC(dalloc_n(c, &d.obs_cam, nobs_loc + 8));  // +8: 16-byte aligned camera-index bulk copies
@@ -753,6 +763,7 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
         CKC(cudaMemcpyAsync(d.obs_lm, olm.data(), sizeof(int32_t) * nobs_loc, cudaMemcpyHostToDevice, c->stream));
         CKC(cudaMemcpyAsync(d.obs_uv, ouv.data(), sizeof(double2) * nobs_loc, cudaMemcpyHostToDevice, c->stream));
         CKC(cudaMemcpyAsync(d.lm_pk, c->h_pk.data(), sizeof(int32_t) * nl, cudaMemcpyHostToDevice, c->stream));
+        CKC(cudaMemcpyAsync(d.lm_q, c->h_q.data(), sizeof(int32_t) * nl, cudaMemcpyHostToDevice, c->stream));
         if (!packs.empty())
             CKC(cudaMemcpyAsync(d.packs, packs.data(), sizeof(Pack) * packs.size(), cudaMemcpyHostToDevice, c->stream));
         if (!marg_items.empty())

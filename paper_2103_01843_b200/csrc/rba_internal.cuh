@@ -61,7 +61,7 @@ struct Pack {
     int32_t lm0, np;  // first landmark (internal index) and number of landmarks (same k)
     int64_t base;     // float offset of the pack's R2 region
     int32_t obs0, k;  // first observation of the pack (its observations are contiguous) and k
-    int32_t pad0, pad1;
+    int32_t q0, pad1; // offset of the first landmark's q in qpk (landmark m: q0 + 2 k m)
 };
 
 // A stage of the small-k pipeline: consecutive packs whose R2 regions are contiguous, their
@@ -72,10 +72,13 @@ struct SmallChunk {
     int32_t bytes;           // R2 bytes (multiple of 16)
     int32_t cam0, ncam;      // obs_cam[cam0 .. cam0 + ncam): 16-byte aligned superset of the packs' cameras
     int32_t unit0;           // units[unit0 .. unit0 + nunit) (nunit a multiple of 8, 0xFFFF = none)
-    int32_t nunit, pad0, pad1, pad2;
+    int32_t nunit;
+    int32_t q0, nq;          // qpk[q0 .. q0 + nq): 16-byte aligned superset of the packs' q (K4 only)
+    int32_t pad2;
 };
 constexpr int PACC_STRIDE = 56;             // per-camera slot of the preconditioner accumulator
 constexpr int SMALL_STAGE_BYTES = 40 * 1024;  // >= largest pack (k = 16, np = 2: 36,864 B)
+constexpr int SP_QCAP = 640;                   // q floats per small-pipe stage (K4; host guarantees)
 
 struct PcgState {
     double rz;  // rho^T z
@@ -121,6 +124,8 @@ struct DevProblem {
     double *pts_io;                               // 3 n_l(global) staging of the caller-order points
     // landmark metadata (internal order, sorted by k)
     int32_t *lm_k, *lm_obs0, *lm_pk;
+    int32_t *lm_q;  // small landmarks: offset of their residual entries q (rows 3..2k+2) in qpk; -1 else
+    float *qpk;     // copy of q of the small landmarks, consecutive (TMA-staged by the small K4 pipe)
     int64_t *lm_r2, *lm_side;
     int32_t *obs_cam, *obs_lm;
     double2 *obs_uv;
@@ -201,7 +206,7 @@ struct rba_ctx {
     std::vector<int32_t> orig_to_int; // caller landmark -> internal (-1 if not owned)
     std::vector<int32_t> h_k;
     std::vector<int64_t> h_r2, h_side;
-    std::vector<int32_t> h_pk;
+    std::vector<int32_t> h_pk, h_q;
     int64_t pack_lo[4] = {0, 0, 0, 0}, pack_hi[4] = {0, 0, 0, 0};  // G = 2, 4, 8, 16 pack ranges
     int64_t marg_lo[6] = {0, 0, 0, 0, 0, 0}, marg_hi[6] = {0, 0, 0, 0, 0, 0};  // K2 large items per class
     int64_t n_huge_y = 0, n_huge_out = 0, huge_max_k = 0;  // k > KLARGE (two-pass matvec)

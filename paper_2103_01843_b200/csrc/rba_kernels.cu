@@ -399,16 +399,18 @@ __global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProb
         for (int q = 0; q < 9; q++) blk_side[s * 9 * k + 9 * gl + q] = v9[q];
     }
     float4 *TL = reinterpret_cast<float4 *>(blk_side + side_tl(k));
+    float *qc = d.qpk + pack.q0 + 2 * k * grp - 3;  // q copy, row a at qc[a] (a >= 3)
 #pragma unroll
     for (int rr = 0; rr < 2; rr++) {
         const int a = 2 * gl + rr;
-        if (a >= 3) TL[a] = make_float4(0.f, 0.f, 0.f, rv[rr]);
+        if (a >= 3) TL[a] = make_float4(0.f, 0.f, 0.f, rv[rr]), qc[a] = rv[rr];
     }
     if (gl == 0) {
 #pragma unroll
         for (int s = 0; s < 3; s++) {
             TL[s] = make_float4(L6[s * 3], L6[s * 3 + 1], L6[s * 3 + 2], rr6[s]);
             TL[2 * k + s] = make_float4(0.f, 0.f, 0.f, rr6[3 + s]);
+            qc[2 * k + s] = rr6[3 + s];
         }
         float *gp = blk_side + side_g(k);
 #pragma unroll
@@ -727,6 +729,10 @@ __global__ void __launch_bounds__(256) k_redamp(DevProblem d, float lam) {
             TL[s] = make_float4(L6[s * 3], L6[s * 3 + 1], L6[s * 3 + 2], rr6[s]);
             TL[2 * k + s] = make_float4(0.f, 0.f, 0.f, rr6[3 + s]);
         }
+        const int32_t qo = d.lm_q[j];  // small landmarks: the q copy of the damping rows too
+        if (qo >= 0)
+#pragma unroll
+            for (int s = 0; s < 3; s++) d.qpk[qo + 2 * k - 3 + s] = rr6[3 + s];
 #pragma unroll
         for (int i = 0; i < 12; i++) gp[i] = gn[i];
     }
@@ -854,7 +860,8 @@ constexpr int SP_UNITCAP = 4 * SP_PACKCAP;          // work units per stage
 constexpr int SP_OFF_CAM = SMALL_STAGE_BYTES;
 constexpr int SP_OFF_PACK = SP_OFF_CAM + 4 * SP_CAMCAP;
 constexpr int SP_OFF_UNIT = SP_OFF_PACK + (int)sizeof(Pack) * SP_PACKCAP;
-constexpr int SP_OFF_HDR = SP_OFF_UNIT + 2 * SP_UNITCAP;  // stage descriptor (written by the producer)
+constexpr int SP_OFF_Q = SP_OFF_UNIT + 2 * SP_UNITCAP;     // K4: the packs' q (SP_QCAP floats)
+constexpr int SP_OFF_HDR = SP_OFF_Q + 4 * SP_QCAP;         // stage descriptor (written by the producer)
 constexpr int SP_SB = SP_OFF_HDR + 128;
 #ifndef RBA_SP_STAGES
 #define RBA_SP_STAGES 4  // 4 stages, v read through L1 (measured 2.47 -> 2.43 ms cfg4 matvec vs 3 stages + v in smem)
@@ -875,7 +882,7 @@ constexpr size_t SP_SMEM = (size_t)SP_STAGES * SP_SB + 4 * SP_VCAP + 2 * SP_STAG
 // one work unit: NRP row pairs starting at p0 of the lane's (landmark, camera block)
 template <int NRP, bool PRECOND>
 __device__ __forceinline__ void small_unit(const DevProblem &d, const float2 *A, int npk, int p0, int k, int G,
-                                           bool valid, int cam, const float *vo, const float4 *TL,
+                                           bool valid, int cam, const float *vo, const float *qs,
                                            float *__restrict__ out12) {
     float sl[NRP][18];
 #pragma unroll
@@ -895,8 +902,8 @@ __device__ __forceinline__ void small_unit(const DevProblem &d, const float2 *A,
         for (int q = 0; q < 9; q++) b[q] = 0.f;
 #pragma unroll
         for (int u = 0; u < NRP; u++) {
-            acc_rows(P, b, sl[u], TL[3 + 2 * (p0 + u)].w);
-            acc_rows(P, b, sl[u] + 9, TL[4 + 2 * (p0 + u)].w);
+            acc_rows(P, b, sl[u], qs[2 * (p0 + u)]);
+            acc_rows(P, b, sl[u] + 9, qs[2 * (p0 + u) + 1]);
         }
         flush54(pslice(d) + PACC_STRIDE * (int64_t)cam, P, b);
     } else {
@@ -965,12 +972,14 @@ __global__ void __launch_bounds__(SP_WARPS * 32 + 32, 1)
                 mbar_wait(&empty[s], ph ^ 1);
                 *reinterpret_cast<SmallChunk *>(sm + (size_t)s * SP_SB + SP_OFF_HDR) = ch;
                 mbar_arrive_expect_tx(&full[s], (uint32_t)ch.bytes + 4u * (uint32_t)ch.ncam +
-                                                    (uint32_t)sizeof(Pack) * (uint32_t)ch.np + 2u * (uint32_t)ch.nunit);
+                                                    (uint32_t)sizeof(Pack) * (uint32_t)ch.np + 2u * (uint32_t)ch.nunit +
+                                                    (PRECOND ? 4u * (uint32_t)ch.nq : 0u));
                 unsigned char *dst = sm + (size_t)s * SP_SB;
                 bulk_g2s_stream(dst, d.arena + ch.base, (uint32_t)ch.bytes, &full[s], pol);
                 bulk_g2s(dst + SP_OFF_CAM, d.obs_cam + ch.cam0, 4u * (uint32_t)ch.ncam, &full[s]);
                 bulk_g2s(dst + SP_OFF_PACK, d.packs + ch.p0, (uint32_t)sizeof(Pack) * ch.np, &full[s]);
                 bulk_g2s(dst + SP_OFF_UNIT, d.units + ch.unit0, 2u * (uint32_t)ch.nunit, &full[s]);
+                if (PRECOND) bulk_g2s_stream(dst + SP_OFF_Q, d.qpk + ch.q0, 4u * (uint32_t)ch.nq, &full[s], pol);
             }
         }
         return;
@@ -999,14 +1008,13 @@ __global__ void __launch_bounds__(SP_WARPS * 32 + 32, 1)
             float vo[9];
 #pragma unroll
             for (int q = 0; q < 9; q++) vo[q] = (valid && !PRECOND) ? vv[9 * cam + q] : 0.f;
-            const float4 *TL = (PRECOND && valid)
-                                   ? reinterpret_cast<const float4 *>(d.arena + d.lm_side[pack.lm0 + m] + side_tl(k))
-                                   : nullptr;
+            // K4: the landmark's q from the staged copy, row a at qs[a - 3]
+            const float *qs = reinterpret_cast<const float *>(stg + SP_OFF_Q) + (pack.q0 - ch.q0) + 2 * k * m;
             switch (min(4, k - p0)) {
-                case 1: small_unit<1, PRECOND>(d, A, npk, p0, k, G, valid, cam, vo, TL, out12); break;
-                case 2: small_unit<2, PRECOND>(d, A, npk, p0, k, G, valid, cam, vo, TL, out12); break;
-                case 3: small_unit<3, PRECOND>(d, A, npk, p0, k, G, valid, cam, vo, TL, out12); break;
-                default: small_unit<4, PRECOND>(d, A, npk, p0, k, G, valid, cam, vo, TL, out12); break;
+                case 1: small_unit<1, PRECOND>(d, A, npk, p0, k, G, valid, cam, vo, qs, out12); break;
+                case 2: small_unit<2, PRECOND>(d, A, npk, p0, k, G, valid, cam, vo, qs, out12); break;
+                case 3: small_unit<3, PRECOND>(d, A, npk, p0, k, G, valid, cam, vo, qs, out12); break;
+                default: small_unit<4, PRECOND>(d, A, npk, p0, k, G, valid, cam, vo, qs, out12); break;
             }
         }
         __syncwarp();
@@ -1143,6 +1151,27 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
             }
         }
         mbar_wait(&full[s], ph);
+        if (PRECOND && NS == 512) {  // 544 threads: <= 120 registers; one row at a time (no spills)
+            if (have && valid) {
+                const float4 *Q = reinterpret_cast<const float4 *>(sm + C::QOFF + ((size_t)s * NSLOT + slot) * 64);
+                const float *S1 = reinterpret_cast<const float *>(
+                    reinterpret_cast<const float4 *>(sm + (size_t)s * C::SB + (size_t)slot * C::TB) + 288 * g + (o & 31));
+#pragma unroll
+                for (int r = 0; r < 4; r++) {
+                    float row[9];
+#pragma unroll
+                    for (int q = 0; q < 9; q++) {
+                        const int f = 9 * r + q;  // float f of the thread's 36: float4 f / 4, lane f % 4
+                        row[q] = S1[4 * (f >> 2) * ng + (f & 3)];
+                    }
+                    const float qa = Q[r].w;
+                    if (4 * tr.t + r < 2 * k) acc_rows(P, b, row, qa);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            continue;
+        }
         float sl[36], qv[4] = {0.f, 0.f, 0.f, 0.f};
         if (PRECOND && have && valid) {
             const float4 *Q = reinterpret_cast<const float4 *>(sm + C::QOFF + ((size_t)s * NSLOT + slot) * 64);
@@ -1517,35 +1546,35 @@ __global__ void __launch_bounds__(256) k_pcg_a(DevProblem d, float lam_f, int fu
     }
 }
 
-// B: thread <-> camera: x += alpha p, rho -= alpha w, z = M^-1 rho (9 x 9 block); |rho|, rho^T z;
-// the last CTA decides convergence (C11) / max iterations and forms beta.
-__global__ void __launch_bounds__(128) k_pcg_b(DevProblem d, double tol, int max_iters, cudaGraphConditionalHandle h,
+// B: thread <-> one entry (32 cameras x 9 per CTA): x += alpha p, rho -= alpha w, then z = M^-1 rho
+// with the camera's 9 updated rho entries exchanged through shared memory; |rho|, rho^T z.  The
+// last CTA decides convergence (C11) / max iterations and forms beta.
+__global__ void __launch_bounds__(288) k_pcg_b(DevProblem d, double tol, int max_iters, cudaGraphConditionalHandle h,
                                                int use_h) {
     __shared__ double red[32];
+    __shared__ double rs[288];
     PcgState *st = d.pcg;
     if (st->done) return;  // (A already cleared the condition)
     const double alpha = st->alpha;
-    const int64_t cam = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    double rr = 0.0, rz = 0.0;
-    if (cam < d.n_p) {
-        double r[9];
+    const int tid = threadIdx.x, cl = tid / 9, a = tid - 9 * cl;
+    const int64_t cam = (int64_t)blockIdx.x * 32 + cl, i = 9 * cam + a;
+    const bool valid = cam < d.n_p;
+    double r = 0.0;
+    if (valid) {
+        d.x[i] += alpha * d.p[i];
+        r = d.r[i] - alpha * d.w[i];
+        d.r[i] = r;
+    }
+    rs[tid] = r;
+    __syncthreads();
+    double rr = r * r, rz = 0.0;
+    if (valid) {
+        const double *M = d.Minv + 81 * cam + 9 * a;
+        double z = 0.0;
 #pragma unroll
-        for (int q = 0; q < 9; q++) {
-            const int64_t i = 9 * cam + q;
-            d.x[i] += alpha * d.p[i];
-            r[q] = d.r[i] - alpha * d.w[i];
-            d.r[i] = r[q];
-            rr += r[q] * r[q];
-        }
-        const double *M = d.Minv + 81 * cam;
-#pragma unroll
-        for (int a = 0; a < 9; a++) {
-            double z = 0.0;
-#pragma unroll
-            for (int b = 0; b < 9; b++) z += M[9 * a + b] * r[b];
-            d.z[9 * cam + a] = z;
-            rz += r[a] * z;
-        }
+        for (int q = 0; q < 9; q++) z += M[q] * rs[9 * cl + q];
+        d.z[i] = z;
+        rz = r * z;
     }
     rr = block_sum_d(rr, red);
     rz = block_sum_d(rz, red);
@@ -2050,7 +2079,7 @@ static void pcg_update(rba_ctx *c, cudaStream_t s, float lam, double tol, int ma
                        cudaGraphConditionalHandle h, int use_h) {
     const int64_t N = 9 * c->d.n_p;
     k_pcg_a<<<(unsigned)((N + 31) / 32), 256, 0, s>>>(c->d, lam, fuse ? 1 : 0, h, use_h);
-    k_pcg_b<<<nblk(c->d.n_p, 128), 128, 0, s>>>(c->d, tol, max_iters, h, use_h);
+    k_pcg_b<<<nblk(c->d.n_p, 32), 288, 0, s>>>(c->d, tol, max_iters, h, use_h);
     k_pcg_c<<<nblk(N, 256), 256, 0, s>>>(c->d);
     c->launches += 3;
 }
