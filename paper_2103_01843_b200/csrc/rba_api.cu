@@ -535,7 +535,6 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     CKSC(dalloc_n(c, &d.obs_cam, nobs_loc + 8));  // +8: 16-byte aligned camera-index bulk copies
     CKSC(dalloc_n(c, &d.obs_lm, nobs_loc));
     CKSC(dalloc_n(c, &d.obs_uv, nobs_loc));
-    CKSC(dalloc_n(c, &d.cam_n2, 12 * n_cams));
     CKSC(dalloc_n(c, &d.sp, 9 * n_cams));
     CKSC(dalloc_n(c, &d.Dp2, 9 * n_cams));
     CKSC(dalloc_n(c, &d.sp64, 9 * n_cams));
@@ -839,12 +838,11 @@ extern "C" rba_status rba_linearize(rba_ctx *c) {
     if (!c) return fail(RBA_ERR_INVALID_ARG, "null ctx");
     CK(cudaSetDevice(c->device));
     DevProblem &d = c->d;
-    CK(cudaMemsetAsync(d.cam_n2, 0, sizeof(float) * 12 * d.n_p, c->stream));
     if (d.s64) CK(cudaMemsetAsync(d.cam_n2d, 0, sizeof(double) * 9 * d.n_p, c->stream));
     CK(cudaMemsetAsync(d.scal + SC_E, 0, sizeof(double) * 2, c->stream));
     CK(launch_linearize(c));
-    CKS(allreduce(c, d.cam_n2, 12 * d.n_p, ncclFloat));
-    if (d.s64) CKS(allreduce(c, d.cam_n2d, 9 * d.n_p, ncclDouble));
+    CK(launch_reduce_cam_norms(c));
+    CKS(allreduce(c, d.cam_n2d, 9 * d.n_p, ncclDouble));
     CKS(allreduce(c, d.scal + SC_E, 2, ncclDouble));
     CK(launch_cam_scale(c));
     CKS(read_scal(c));

@@ -130,8 +130,8 @@ struct DevProblem {
     int32_t *obs_cam, *obs_lm;
     double2 *obs_uv;
     // scaling / damping
-    float *cam_n2, *sp, *Dp2;
-    double *cam_n2d;       // sqrt-BA-64: camera column norms^2 accumulated in FP64 (9 per camera)
+    float *sp, *Dp2;
+    double *cam_n2d;       // camera column norms^2 in FP64 (9 per camera): FP32 slices summed, or FP64 sums (sqrt-BA-64)
     double *sp64, *Dp264;  // FP64 copies of S_p and D_p^2 (exact FP64 values for sqrt-BA-64)
     float *lm_s, *lm_D;
     // arena
@@ -254,6 +254,7 @@ namespace rba {
 // kernel launchers (rba_kernels.cu); each returns cudaGetLastError()
 cudaError_t launch_check_depth(rba_ctx *c, int *d_bad);
 cudaError_t launch_cam_prep(rba_ctx *c, int trial);
+cudaError_t launch_reduce_cam_norms(rba_ctx *c);
 cudaError_t launch_pts_permute(rba_ctx *c, int to_internal);
 cudaError_t query_nsmid(rba_ctx *c, int *d_scratch, int *out);
 cudaError_t launch_linearize(rba_ctx *c);

@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(256) k_linearize(DevProblem d) {
             float n2[9];
 #pragma unroll
             for (int q = 0; q < 9; q++) n2[q] = Jc[q] * Jc[q] + Jc[9 + q] * Jc[9 + q];
-            flush_cam12(d.cam_n2, cam, n2);  // camera stride 12, three float4 reductions
+            flush_cam12(wslice(d), cam, n2);  // per-SM slice (k_reduce_slices sums them in FP64)
         }
     }
     e = block_sum_d(e, red);
@@ -89,7 +89,7 @@ __global__ void k_cam_scale(DevProblem d, float dmin, float dmax) {
         d.sp[i] = (float)s, d.Dp2[i] = (float)D2;
         return;
     }
-    float n2 = d.cam_n2[12 * cam + (i - 9 * cam)];
+    float n2 = (float)d.cam_n2d[i];
     float s = 1.f / (1.f + sqrtf(n2));
     d.sp[i] = s;
     d.Dp2[i] = fminf(fmaxf(n2 * s * s, dmin), dmax);
@@ -1414,18 +1414,23 @@ __global__ void __launch_bounds__(256) k_reduce_slices(float *__restrict__ sl, i
         const int64_t cam = i / nv;
         const int64_t e = stride * cam + (i - nv * cam);
         const int64_t S = (int64_t)stride * n_p;
-        int k = ty;
-        for (; k + 24 < nslice; k += 32) {
-            float *q0 = sl + k * S + e, *q1 = q0 + 8 * S, *q2 = q0 + 16 * S, *q3 = q0 + 24 * S;
-            const float a0 = *q0, a1 = *q1, a2 = *q2, a3 = *q3;
-            *q0 = 0.f, *q1 = 0.f, *q2 = 0.f, *q3 = 0.f;
-            s += ((double)a0 + (double)a1) + ((double)a2 + (double)a3);
+        float a[24];
+#pragma unroll
+        for (int u = 0; u < 24; u++) {  // all loads in flight first (nslice <= 192), then the zeroing
+            const int k = ty + 8 * u;
+            a[u] = k < nslice ? sl[k * S + e] : 0.f;
         }
-        for (; k < nslice; k += 8) {
-            float *q = sl + k * S + e;
-            s += (double)*q;
-            *q = 0.f;
+#pragma unroll
+        for (int u = 0; u < 24; u++) {
+            const int k = ty + 8 * u;
+            if (k < nslice) sl[k * S + e] = 0.f;
         }
+        for (int k = ty + 8 * 24; k < nslice; k += 8) {  // (more than 192 SMs)
+            s += (double)sl[k * S + e];
+            sl[k * S + e] = 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 24; u += 4) s += ((double)a[u] + (double)a[u + 1]) + ((double)a[u + 2] + (double)a[u + 3]);
     }
     part[ty][tx] = s;
     __syncthreads();
@@ -2001,6 +2006,12 @@ static void pipes_all(rba_ctx *c, const float *v, float *out12, const PcgState *
 static void reduce_slices(rba_ctx *c, float *sl, int stride, int nv, double *out, const PcgState *st) {
     k_reduce_slices<<<nblk(nv * c->d.n_p, 32), 256, 0, c->stream>>>(sl, c->d.n_p, stride, nv, c->d.nslice, out, st);
     c->launches++;
+}
+
+// K1 camera column norms^2: the per-SM slices into cam_n2d (FP32 path; sqrt-BA-64 adds FP64 directly)
+cudaError_t launch_reduce_cam_norms(rba_ctx *c) {
+    if (!c->d.s64) reduce_slices(c, c->d.wsl, 12, 9, c->d.cam_n2d, nullptr);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_precond_rhs(rba_ctx *c) {
