@@ -39,11 +39,13 @@ __global__ void k_check_depth(DevProblem d, int *bad) {
 }
 
 // K1: residuals, E and camera column norms^2 (sum over the camera's observations).
+// Grid-stride (a few CTAs per SM): the per-CTA FP64 sums of E go to one address, so fewer CTAs
+// means fewer serialized same-address atomics.
 __global__ void __launch_bounds__(256) k_linearize(DevProblem d) {
     __shared__ double red[32];
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     double e = 0.0, bad = 0.0;
-    if (i < d.n_obs) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d.n_obs;
+         i += (int64_t)gridDim.x * blockDim.x) {
         double c[CAMPRE], r[2];
         float Jc[18], Jl[6];
         const int cam = d.obs_cam[i];
@@ -53,15 +55,15 @@ __global__ void __launch_bounds__(256) k_linearize(DevProblem d) {
         if (d.s64) {  // sqrt-BA-64: FP64 Jacobians and FP64 norm sums
             double Jcd[18], Jld[6];
             const double Pz = cam_model_pre<double>(c, X[0], X[1], X[2], uv.x, uv.y, r, Jcd, Jld);
-            if (!(Pz < 0.0)) bad = 1.0;
-            e = robust_rho(r[0] * r[0] + r[1] * r[1], d.huber);
+            if (!(Pz < 0.0)) bad += 1.0;
+            e += robust_rho(r[0] * r[0] + r[1] * r[1], d.huber);
             apply_irls<double>(r, Jcd, Jld, d.huber);
 #pragma unroll
             for (int q = 0; q < 9; q++) atomicAdd(d.cam_n2d + 9 * (int64_t)cam + q, Jcd[q] * Jcd[q] + Jcd[9 + q] * Jcd[9 + q]);
         } else {
             const double Pz = cam_model_pre(c, X[0], X[1], X[2], uv.x, uv.y, r, Jc, Jl);
-            if (!(Pz < 0.0)) bad = 1.0;
-            e = robust_rho(r[0] * r[0] + r[1] * r[1], d.huber);
+            if (!(Pz < 0.0)) bad += 1.0;
+            e += robust_rho(r[0] * r[0] + r[1] * r[1], d.huber);
             apply_irls(r, Jc, Jl, d.huber);
             float n2[9];
 #pragma unroll
@@ -1781,16 +1783,16 @@ __global__ void __launch_bounds__(1024) k_trial_cams(DevProblem d, float lam, in
 __global__ void __launch_bounds__(256) k_cost(DevProblem d, const double *__restrict__ campre,
                                               const double *__restrict__ pts, int slot, int bad_slot) {
     __shared__ double red[32];
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     double e = 0.0, bad = 0.0;
-    if (i < d.n_obs) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d.n_obs;
+         i += (int64_t)gridDim.x * blockDim.x) {  // grid-stride (see k_linearize)
         double c[CAMPRE], r[2];
         load_pre(campre, d.obs_cam[i], c);
         const double *X = pts + 3 * (int64_t)d.obs_lm[i];
         const double2 uv = d.obs_uv[i];
         const double Pz = cam_model_pre<float>(c, X[0], X[1], X[2], uv.x, uv.y, r, nullptr, nullptr);
-        if (!(Pz < 0.0) || !isfinite(r[0]) || !isfinite(r[1])) bad = 1.0;
-        else e = robust_rho(r[0] * r[0] + r[1] * r[1], d.huber);
+        if (!(Pz < 0.0) || !isfinite(r[0]) || !isfinite(r[1])) bad += 1.0;
+        else e += robust_rho(r[0] * r[0] + r[1] * r[1], d.huber);
     }
     e = block_sum_d(e, red);
     bad = block_sum_d(bad, red);
@@ -1859,7 +1861,7 @@ cudaError_t launch_linearize(rba_ctx *c) {
     launch_cam_prep(c, 0);
     if (c->d.n_obs == 0) return cudaSuccess;
     Prof P(c, KID_LIN, 24.0 * c->d.n_obs);
-    k_linearize<<<nblk(c->d.n_obs, 256), 256, 0, c->stream>>>(c->d);
+    k_linearize<<<(unsigned)std::min<int64_t>(nblk(c->d.n_obs, 256), 8 * (int64_t)c->num_sms), 256, 0, c->stream>>>(c->d);
     P.end();
     c->launches++;
     return cudaGetLastError();
@@ -2183,7 +2185,7 @@ cudaError_t launch_cost(rba_ctx *c, int at_trial, int slot) {
     Prof P(c, KID_COST, 20.0 * c->d.n_obs);
     const int bad_slot = at_trial ? SC_BADT : SC_BAD;
     launch_cam_prep(c, at_trial);
-    k_cost<<<nblk(c->d.n_obs, 256), 256, 0, c->stream>>>(c->d, at_trial ? c->d.campre_trial : c->d.campre,
+    k_cost<<<(unsigned)std::min<int64_t>(nblk(c->d.n_obs, 256), 8 * (int64_t)c->num_sms), 256, 0, c->stream>>>(c->d, at_trial ? c->d.campre_trial : c->d.campre,
                                                           at_trial ? c->d.pts_trial : c->d.pts, slot, bad_slot);
     P.end();
     c->launches++;
