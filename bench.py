@@ -56,8 +56,8 @@ def peaks():
 
 
 MATVEC_KERNELS = re.compile(r"k_large_pipe<\d+, \d+, (0|false)>|k_small_pipe<(0|false)>|k_huge_y|k_huge_out<(0|false)>|"
-                            r"k_fac_matvec|k_sc_spmv|k_reduce_slices")
-MARG_KERNELS = re.compile(r"k_marg_(small|large)<")
+                            r"k_huge_fused|k_fac_matvec|k_sc_spmv|k_rcs64_(ws|tma)<[^>]*(0|false)>|k_pcg_a")
+MARG_KERNELS = re.compile(r"k_marg_(small|large)<|k_marg64")
 
 
 def ncu_traffic(cfg, variant=""):
@@ -348,9 +348,9 @@ def main():
         roof_mv["traffic"] = tr_mv
         roof_mv["traffic_source"] = tr_src
         roof_mv["kernel"] = {
-            "": "matvec (K5: k_small_pipe + k_large_pipe<NS> + k_huge_*, then k_reduce_slices), algorithmic 72k^2 B/landmark",
-            "_factored": "factored matvec (k_fac_matvec<G> + k_reduce_slices), algorithmic 176+112k B/landmark",
-            "_fp64": "sqrt-BA-64 product (k_rcs64), algorithmic 8 x 2k(9k+1) B/landmark",
+            "": "matvec (K5: k_small_pipe + k_large_pipe<NS> + k_huge_*, slices summed in k_pcg_a), algorithmic 72k^2 B/landmark",
+            "_factored": "factored matvec (k_fac_matvec<G>, slices summed in k_pcg_a), algorithmic 176+112k B/landmark",
+            "_fp64": "sqrt-BA-64 product (k_rcs64_ws<G> + k_rcs64_tma<NT>), algorithmic 8 x 2k(9k+1) B/landmark",
         }.get(variant, "explicit-SC SpMV (k_sc_spmv), algorithmic 81 x sizeof(T) B per 9x9 block")
     roof_mg = roof(*mprof)
     if roof_mg:
