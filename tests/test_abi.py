@@ -74,6 +74,29 @@ def test_create_rejects_bad_problems(mutate, status):
     assert ei.value.status == status
 
 
+def _one_track(k):
+    """One landmark seen by k distinct cameras (the track-length limits)."""
+    rng = np.random.default_rng(k)
+    cams = np.zeros((k, 9))
+    cams[:, 3:6] = rng.normal(0, 1, (k, 3))
+    cams[:, 5] = 10.0
+    cams[:, 6] = 500.0
+    return (cams, np.zeros((1, 3)), np.arange(k, dtype=np.int32), np.zeros(k, np.int32),
+            rng.normal(0, 1, (k, 2)))
+
+
+@pytest.mark.parametrize("k,precision", [(3073, 0), (1025, 1)])
+def test_create_rejects_tracks_beyond_kmax(k, precision):
+    """Track lengths above KMAX (3072) / KMAX64 (1024, sqrt-BA-64) are BAD_PROBLEM, checked on the
+    host before any device work."""
+    o = rba.rba_default_options()
+    o.precision = precision
+    with pytest.raises(rba.RBAError) as ei:
+        rba.rba_create(*_one_track(k), o)
+    assert ei.value.status == rba.RBA_ERR_BAD_PROBLEM
+    assert str(k) in str(ei.value)
+
+
 def test_create_rejects_bad_options():
     p = _prob()
     o = rba.rba_default_options()
