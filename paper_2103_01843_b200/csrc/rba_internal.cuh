@@ -32,7 +32,7 @@ constexpr int CAMPRE = 24;    // doubles of a camera's precomputed model (R, J_l
 //    9 float4 chunks:  float4 index (36*32*g)/4 + c*n_g + (o & 31)
 // Side region per landmark (16-byte aligned):  R1 = logical rows 0..2 pose columns (3 x 9k
 // row-major) | pad4 | TL: (2k+3) float4 [J_l row | residual] of every logical row | G: 6 x (c, s).
-__host__ __device__ inline int64_t pad4(int64_t x) { return (x + 3) & ~int64_t(3); }
+__host__ __device__ constexpr int64_t pad4(int64_t x) { return (x + 3) & ~int64_t(3); }
 __host__ __device__ inline int large_tiles(int k) { return (k + 1) >> 1; }  // ceil(2k / 4)
 __host__ __device__ inline int64_t small_pack_floats(int k, int np) { return (int64_t)18 * k * k * np; }
 __host__ __device__ inline int64_t large_r2_floats(int k) { return (int64_t)36 * k * large_tiles(k); }
@@ -49,8 +49,8 @@ __host__ __device__ inline int64_t large_index(int k, int a, int o, int q) {
 __host__ __device__ inline int64_t r2_index(int k, int32_t pk, int a, int o, int q) {
     return k <= KSMALL ? small_index(k, pk >> 8, pk & 255, a, o, q) : large_index(k, a, o, q);
 }
-__host__ __device__ inline int64_t side_r1_floats(int k) { return pad4(27 * (int64_t)k); }
-__host__ __device__ inline int64_t side_floats(int k) { return side_r1_floats(k) + 4 * (2 * (int64_t)k + 3) + 12; }
+__host__ __device__ constexpr int64_t side_r1_floats(int k) { return pad4(27 * (int64_t)k); }
+__host__ __device__ constexpr int64_t side_floats(int k) { return side_r1_floats(k) + 4 * (2 * (int64_t)k + 3) + 12; }
 __host__ __device__ inline int64_t side_tl(int k) { return side_r1_floats(k); }
 __host__ __device__ inline int64_t side_g(int k) { return side_r1_floats(k) + 4 * (2 * (int64_t)k + 3); }
 

@@ -203,6 +203,9 @@ template <int G>
 struct SmallTab {
     static constexpr int VR = 4 * (2 * G + 3);
     static constexpr int FLOATS = VR + 20;
+    // the pack's side regions (R1 | TL | G of its <= 32/G landmarks, consecutive in the arena) are
+    // assembled in shared memory and written with one bulk store (k <= G; k = 2 for G = 2)
+    static constexpr int SIDE = (32 / G) * (int)side_floats(G);
 };
 
 template <int G>
@@ -225,6 +228,7 @@ __global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProb
     const int k = pack.k;  // (the pack's observations are contiguous: no per-landmark index loads)
     const bool act = valid && gl < k;
     float *tab = smem + (warp * NG + grp) * TB::FLOATS;
+    float *sside = smem + 4 * NG * TB::FLOATS + warp * TB::SIDE;  // this warp's pack side regions
     float4 *VR = reinterpret_cast<float4 *>(tab);
     float *GM = tab + TB::VR;
 
@@ -362,8 +366,8 @@ __global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProb
         for (int i = 0; i < 18; i++) GM[i] = Gm[i];
     }
     __syncwarp();
-    if (!act) return;
     if (d.fac) {  // factored storage: the factors instead of the dense block
+        if (!act) return;
         float *base = d.arena + d.lm_r2[j];
         fac_write_obs(base + 44 + 28 * gl, B, V[0], V[1], rv[0], rv[1]);
         if (gl == 0) {
@@ -376,8 +380,9 @@ __global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProb
         }
         return;
     }
-    // ---- emission (write-only stream, Fig. 2c) in the pack layout
-    float *blk_side = d.arena + d.lm_side[j];
+    // ---- emission (write-only stream, Fig. 2c) in the pack layout; side regions via smem
+    float *blk_side = sside + grp * (int)side_floats(k);
+    if (act) {
     float2 *A = reinterpret_cast<float2 *>(d.arena + pack.base);
     const int npk = pack.np * k, mo = grp * k + gl;
     float2 *Ap = A + mo;
@@ -423,6 +428,12 @@ __global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProb
             d.lm_D[3 * j + q] = Dl[q];
         }
     }
+    }  // act
+    fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk copy
+    __syncwarp();
+    if (lane == 0)
+        bulk_s2g(d.arena + d.lm_side[pack.lm0], sside, 4u * (uint32_t)(pack.np * side_floats(k))),
+            bulk_commit_wait_read();
 }
 
 // ============================================================================ K2 large (k > 32)
@@ -1901,7 +1912,7 @@ template <int G>
 static cudaError_t marg_small_cls(rba_ctx *c, int cls, float lam, cudaStream_t st) {
     const int64_t lo = c->pack_lo[cls], hi = c->pack_hi[cls];
     if (hi <= lo) return cudaSuccess;
-    const size_t sm = (size_t)4 * (32 / G) * SmallTab<G>::FLOATS * sizeof(float);
+    const size_t sm = (size_t)4 * ((32 / G) * SmallTab<G>::FLOATS + SmallTab<G>::SIDE) * sizeof(float);
     k_marg_small<G><<<nblk(hi - lo, 4), 128, sm, st>>>(c->d, lo, hi, lam, (float)c->opt.diag_min,
                                                               (float)c->opt.diag_max);
     c->launches++;
