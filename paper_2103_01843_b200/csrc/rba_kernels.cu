@@ -1731,25 +1731,33 @@ __global__ void __launch_bounds__(256) k_backsub(DevProblem d, float lam) {
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     double q1 = 0.0, dd = 0.0;
-    for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < d.n_l; j += nwarps) {
-        const int k = d.lm_k[j];
-        const float *side = d.arena + d.lm_side[j];
+    constexpr int G = 8;  // lanes per landmark: 4 landmarks per warp and sweep
+    const int gl = lane % G;
+    for (int64_t jb = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * (32 / G); jb < d.n_l;
+         jb += nwarps * (32 / G)) {
+        const int64_t j = jb + lane / G;
+        const bool valid = j < d.n_l;
+        const int k = valid ? d.lm_k[j] : 0;
+        const float *side = d.arena + (valid ? d.lm_side[j] : 0);
         const int W = 9 * k;
-        const int32_t *oc = d.obs_cam + d.lm_obs0[j];
+        const int32_t *oc = d.obs_cam + (valid ? d.lm_obs0[j] : 0);
         // FP64 arithmetic on the stored FP32 R^1 | Q^1^T J_p rows (the 3x3 solve amplifies errors by
         // cond(R^1), large for far / short-baseline landmarks)
         double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-        for (int c = lane; c < W; c += 32) {
+        for (int c = gl; c < W; c += G) {
             const int o = c / 9, q = c - 9 * o;
             const double v = d.x[9 * (int64_t)oc[o] + q];
             s0 += (double)side[c] * v;
             s1 += (double)side[W + c] * v;
             s2 += (double)side[2 * W + c] * v;
         }
-        s0 = warp_sum_d(s0);
-        s1 = warp_sum_d(s1);
-        s2 = warp_sum_d(s2);
-        if (lane == 0) {
+#pragma unroll
+        for (int m = G / 2; m; m >>= 1) {
+            s0 += __shfl_xor_sync(0xffffffffu, s0, m, G);
+            s1 += __shfl_xor_sync(0xffffffffu, s1, m, G);
+            s2 += __shfl_xor_sync(0xffffffffu, s2, m, G);
+        }
+        if (valid && gl == 0) {
             const float4 *TL = reinterpret_cast<const float4 *>(side + side_tl(k));
             const float4 t0 = TL[0], t1 = TL[1], t2 = TL[2];
             const double b0 = t0.w + s0, b1 = t1.w + s1, b2 = t2.w + s2;
