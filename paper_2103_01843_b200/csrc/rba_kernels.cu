@@ -44,13 +44,16 @@ __global__ void k_check_depth(DevProblem d, int *bad) {
 __global__ void __launch_bounds__(256) k_linearize(DevProblem d) {
     __shared__ double red[32];
     double e = 0.0, bad = 0.0;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d.n_obs;
-         i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int cam_n = i < d.n_obs ? __ldg(d.obs_cam + i) : 0, lm_n = i < d.n_obs ? __ldg(d.obs_lm + i) : 0;
+    for (; i < d.n_obs; i += stride) {
         double c[CAMPRE], r[2];
         float Jc[18], Jl[6];
-        const int cam = d.obs_cam[i];
+        const int cam = cam_n, lm = lm_n;  // indices of the next observation are loaded one ahead
+        if (i + stride < d.n_obs) cam_n = __ldg(d.obs_cam + i + stride), lm_n = __ldg(d.obs_lm + i + stride);
         load_pre(d.campre, cam, c);
-        const double *X = d.pts + 3 * (int64_t)d.obs_lm[i];
+        const double *X = d.pts + 3 * (int64_t)lm;
         const double2 uv = d.obs_uv[i];
         if (d.s64) {  // sqrt-BA-64: FP64 Jacobians and FP64 norm sums
             double Jcd[18], Jld[6];
