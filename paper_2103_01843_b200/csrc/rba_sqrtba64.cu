@@ -847,7 +847,6 @@ template <int NT, int NB, bool PRE>
 __global__ void __launch_bounds__(NT) k_rcs64_tma(DevProblem d, const LargeItem *__restrict__ items,
                                                   const double *__restrict__ v, const PcgState *__restrict__ st,
                                                   int CRMAX, int S, int stage_dbl) {
-    static_assert(!PRE || NB == 1, "block-Jacobi blocks: one camera block per thread");
     if (!PRE && st && st->done) return;
     extern __shared__ __align__(16) double sm64[];
     uint64_t *full = reinterpret_cast<uint64_t *>(sm64 + (size_t)S * stage_dbl);
@@ -864,32 +863,39 @@ __global__ void __launch_bounds__(NT) k_rcs64_tma(DevProblem d, const LargeItem 
     }
     __syncthreads();
     const uint64_t pol = policy_evict_first();
-    auto issue = [&](int c) {  // thread 0: chunk c -> stage c % S
+    // PRE streams the item once per camera-block pass m < NB (54 accumulators per thread and
+    // pass; the repeated reads of the ~1 MB item mostly hit L2): chunk sequence c = m nch + chunk
+    const int ntot = PRE ? NB * nch : nch;
+    auto issue = [&](int cc) {  // thread 0: chunk cc -> stage cc % S
+        const int c = cc % nch;
         const int a0 = it.t0 + c * CR, nr = min(CR, it.t1 - a0);
         const uintptr_t lo = reinterpret_cast<uintptr_t>(B + (int64_t)a0 * W) & ~(uintptr_t)15;
         const uintptr_t hi = (reinterpret_cast<uintptr_t>(B + (int64_t)(a0 + nr) * W) + 15) & ~(uintptr_t)15;
-        uint64_t *bar = &full[c % S];
+        uint64_t *bar = &full[cc % S];
         mbar_arrive_expect_tx(bar, (uint32_t)(hi - lo));
-        bulk_g2s_stream(sm64 + (size_t)(c % S) * stage_dbl, reinterpret_cast<const void *>(lo), (uint32_t)(hi - lo),
+        bulk_g2s_stream(sm64 + (size_t)(cc % S) * stage_dbl, reinterpret_cast<const void *>(lo), (uint32_t)(hi - lo),
                         bar, pol);
     };
     if (tid == 0)
-        for (int c = 0; c < min(S, nch); c++) issue(c);
+        for (int c = 0; c < min(S, ntot); c++) issue(c);
     const int32_t *oc = d.obs_cam + d.lm_obs0[j];
     if (PRE) {
         double P[45], bb[9];
+        for (int cc = 0; cc < ntot; cc++) {
+            const int c = cc % nch, o = tid + (cc / nch) * NT;
+            if (c == 0) {
 #pragma unroll
-        for (int i = 0; i < 45; i++) P[i] = 0.0;
+                for (int i = 0; i < 45; i++) P[i] = 0.0;
 #pragma unroll
-        for (int i = 0; i < 9; i++) bb[i] = 0.0;
-        for (int c = 0; c < nch; c++) {
-            const int s = c % S, a0 = it.t0 + c * CR, nr = min(CR, it.t1 - a0);
-            mbar_wait(&full[s], (uint32_t)((c / S) & 1));
+                for (int i = 0; i < 9; i++) bb[i] = 0.0;
+            }
+            const int s = cc % S, a0 = it.t0 + c * CR, nr = min(CR, it.t1 - a0);
+            mbar_wait(&full[s], (uint32_t)((cc / S) & 1));
             const double *rows =
                 sm64 + (size_t)s * stage_dbl + ((reinterpret_cast<uintptr_t>(B + (int64_t)a0 * W) >> 3) & 1);
-            if (tid < k)
+            if (o < k)
                 for (int r = 0; r < nr; r++) {
-                    const double *x = rows + r * W + 9 * tid;
+                    const double *x = rows + r * W + 9 * o;
                     const double qa = rows[r * W + 9 * k + 3];
                     int idx = 0;
 #pragma unroll
@@ -901,14 +907,14 @@ __global__ void __launch_bounds__(NT) k_rcs64_tma(DevProblem d, const LargeItem 
                     }
                 }
             __syncthreads();
-            if (tid == 0 && c + S < nch) issue(c + S);
-        }
-        if (tid < k) {
-            double *acc = d.pd + 54 * (int64_t)oc[tid];
+            if (tid == 0 && cc + S < ntot) issue(cc + S);
+            if (c == nch - 1 && o < k) {  // end of pass: block o's sums
+                double *acc = d.pd + 54 * (int64_t)oc[o];
 #pragma unroll
-            for (int i = 0; i < 45; i++) atomicAdd(acc + i, P[i]);
+                for (int i = 0; i < 45; i++) atomicAdd(acc + i, P[i]);
 #pragma unroll
-            for (int i = 0; i < 9; i++) atomicAdd(acc + 45 + i, bb[i]);
+                for (int i = 0; i < 9; i++) atomicAdd(acc + 45 + i, bb[i]);
+            }
         }
         return;
     }
@@ -1154,6 +1160,9 @@ void launch_pre64(rba_ctx *c) {
         rcs64_tma_range<32, 1, true>(c, c->s64_glo[3], c->s64_ghi[3], 32, nullptr, nullptr);
         rcs64_tma_cls<128, 1, true>(c, 1, nullptr, nullptr);
         rcs64_tma_cls<256, 1, true>(c, 2, nullptr, nullptr);
+        rcs64_tma_cls<256, 2, true>(c, 3, nullptr, nullptr);
+        rcs64_tma_cls<256, KMAX64 / 256, true>(c, 4, nullptr, nullptr);
+        return;
     } else {
         rcs64_cls<32, 1, true>(c, 0, nullptr, nullptr);
         rcs64_cls<128, 1, true>(c, 1, nullptr, nullptr);
