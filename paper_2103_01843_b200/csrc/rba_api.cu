@@ -890,7 +890,10 @@ extern "C" rba_status rba_pcg_solve(rba_ctx *c, rba_pcg_stats *stats) {
     CKS(allreduce(c, d.pd, 54 * d.n_p, ncclDouble));
     CK(launch_precond_finalize(c, lam));
     CK(launch_pcg_init(c, (float)c->opt.pcg_rel_tol, c->opt.pcg_max_iters));
-    static const bool no_graph = getenv("RBA_NO_GRAPH") != nullptr;
+    // The device-side loop (CUDA graph with a `while` node) saves the host round trips, but with
+    // huge tracks (k > 512, config 5) its branches run the fused two-read kernel measurably slower
+    // than the eager issue order (31.3 vs 27.3 ms per product), so those problems loop on the host.
+    const bool no_graph = getenv("RBA_NO_GRAPH") != nullptr || c->n_huge_fused > 0 || c->n_huge_out > 0;
     if (!c->have_comm && !no_graph && !c->pcg_exec && !c->pcg_graph_failed) {
         if (build_pcg_graph(c) != cudaSuccess) {
             cudaGetLastError();

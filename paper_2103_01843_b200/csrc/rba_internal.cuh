@@ -244,6 +244,7 @@ struct rba_ctx {
     bool pcg_graph_failed = false;
     int64_t graph_body_kernels = 0;  // kernels per PCG-graph iteration (launch accounting)
     bool pcg_fused = false;          // the last PCG product left its sum in the per-SM slices
+    bool nofork = false;             // launch the per-class kernels on the context stream only
     bool profiling = false;
     int64_t prof_real_matvecs = 0;  // matvecs that did work (PCG iterations + hook calls) since rba_profile
     std::vector<rba::Launch> prof;

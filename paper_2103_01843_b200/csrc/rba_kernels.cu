@@ -1903,15 +1903,19 @@ extern double plan_matvec_bytes(rba_ctx *c);
 struct ForkJoin {
     rba_ctx *c;
     int next = 0;
-    explicit ForkJoin(rba_ctx *c_) : c(c_) {
+    bool on;
+    explicit ForkJoin(rba_ctx *c_) : c(c_), on(!c_->nofork) {
+        if (!on) return;
         cudaEventRecord(c->ev_fork, c->stream);
         for (int i = 0; i < rba_ctx::NAUX; i++) cudaStreamWaitEvent(c->aux[i], c->ev_fork, 0);
     }
     cudaStream_t s() {  // round robin: context stream, aux 0, aux 1, ...
+        if (!on) return c->stream;
         const int i = next++ % (rba_ctx::NAUX + 1);
         return i == 0 ? c->stream : c->aux[i - 1];
     }
     void join() {
+        if (!on) return;
         for (int i = 0; i < rba_ctx::NAUX; i++) {
             cudaEventRecord(c->ev_join[i], c->aux[i]);
             cudaStreamWaitEvent(c->stream, c->ev_join[i], 0);
@@ -2158,6 +2162,8 @@ cudaError_t build_pcg_graph(rba_ctx *c) {
     const int64_t nl = c->launches;
     c->stream = cs;
     c->profiling = false;
+    static const bool nofork = getenv("RBA_GRAPH_NOFORK") != nullptr;
+    c->nofork = nofork;
     static const bool single = getenv("RBA_PCG_SINGLE_CTA") != nullptr;
     if (single) {
         matvec_body(c, c->d.p32, c->d.pcg);
@@ -2169,6 +2175,7 @@ cudaError_t build_pcg_graph(rba_ctx *c) {
     }
     c->stream = saved;
     c->profiling = prof;
+    c->nofork = false;
     c->graph_body_kernels = c->launches - nl;  // kernel nodes per loop iteration
     c->launches = nl;
     cudaGraph_t captured;
