@@ -1324,7 +1324,13 @@ __global__ void __launch_bounds__(HUGE_FNT, 1) k_huge_fused(DevProblem d, const 
     for (int m = 0; m < HUGE_NB; m++)
 #pragma unroll
         for (int q = 0; q < 9; q++) acc[m][q] = 0.f;
+    // the tiles of the item stream into L2 two ahead of the one being processed (TMA prefetch), so
+    // HBM stays busy during the CTA reduction and the second (L2) read of the current tile
+    const uint32_t tb = 144u * (uint32_t)k;  // bytes of one 4 x 9k tile
+    if (tid == 0)
+        for (int t = it.t0; t < min(it.t1, it.t0 + 2); t++) bulk_prefetch_l2(R2 + (int64_t)36 * k * t, tb);
     for (int t = it.t0; t < it.t1; t++) {
+        if (tid == 0 && t + 2 < it.t1) bulk_prefetch_l2(R2 + (int64_t)36 * k * (t + 2), tb);
         float y[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int m = 0; m < HUGE_NB; m++) {

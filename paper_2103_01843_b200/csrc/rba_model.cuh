@@ -296,6 +296,10 @@ __device__ __forceinline__ void bulk_g2s_stream(void *dst, const void *src, uint
         : "memory");
 }
 
+// TMA prefetch of a global range into L2 (no shared memory, no completion tracking)
+__device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 // shared -> global bulk store (TMA), its commit and the wait until the shared source was read
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t bytes) {
