@@ -444,7 +444,7 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
                 continue;
             }
             for (int t = 0; t < T; t++)
-                tiles.push_back(TileRef{(int32_t)i, t, c->h_r2[i] + (int64_t)36 * k * t, k, 0});
+                tiles.push_back(TileRef{(int32_t)i, t, c->h_r2[i] + (int64_t)36 * k * t, k, h_obs0[i]});
             bytes += 144.0 * k * T;
         }
         c->marg_hi[cls] = (int64_t)marg_items.size();

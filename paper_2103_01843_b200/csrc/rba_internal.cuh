@@ -98,7 +98,7 @@ enum { KID_LIN = 0, KID_MARG, KID_DAMP, KID_PRE, KID_MATVEC, KID_PCG, KID_BACKSU
 struct TileRef {
     int32_t lm, t;   // landmark (internal index) and 4-row tile index
     int64_t off;     // float offset of the tile in the arena
-    int32_t k, pad;  // track length (tile bytes = 144 k)
+    int32_t k, obs0;  // track length (tile bytes = 144 k) and the landmark's first observation
 };
 
 struct LargeItem {

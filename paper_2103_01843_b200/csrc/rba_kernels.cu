@@ -1152,7 +1152,7 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
                 valid = o < k;
                 g = o >> 5;
                 ng = valid ? min(32, k - 32 * g) : 1;
-                if (valid) cam = d.obs_cam[d.lm_obs0[cur] + o];
+                if (valid) cam = __ldg(d.obs_cam + tr.obs0 + o);  // (first observation carried by the tile)
 #pragma unroll
                 for (int q = 0; q < 9; q++) vo[q] = (PRECOND || !valid) ? 0.f : __ldg(v + 9 * cam + q);
                 if (PRECOND) {
@@ -1402,7 +1402,14 @@ __global__ void __launch_bounds__(HUGE_NT) k_huge_out(DevProblem d, float *__res
     }
     const float4 *TL = reinterpret_cast<const float4 *>(d.arena + d.lm_side[j] + side_tl(k));
     const float4 *Y = reinterpret_cast<const float4 *>(d.ybuf + it.yoff);
+    // this CTA's camera blocks [o0, o0 + 256) are one contiguous range of each tile: TMA-prefetch
+    // it into L2 two tiles ahead (thread 0; the threads are otherwise independent)
+    const uint32_t span = 144u * (uint32_t)(min(it.o0 + HUGE_NT, k) - it.o0);
+    const int64_t soff = (int64_t)36 * it.o0;
+    if (threadIdx.x == 0)
+        for (int t = it.t0; t < min(it.t1, it.t0 + 2); t++) bulk_prefetch_l2(R2 + (int64_t)36 * k * t + soff, span);
     for (int t = it.t0; t < it.t1; t++) {
+        if (threadIdx.x == 0 && t + 2 < it.t1) bulk_prefetch_l2(R2 + (int64_t)36 * k * (t + 2) + soff, span);
         float sl[36];
         huge_slab(R2, k, t, o, sl);
         if (PRECOND) {
