@@ -814,6 +814,7 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
         }
         c->have_comm = true;
     }
+    c->emulate_comm = getenv("RBA_EMULATE_COMM") != nullptr;  // test hook (tests/test_gpu_parity.py)
     *out = c;
     return RBA_OK;
 #undef CKC
@@ -894,13 +895,13 @@ extern "C" rba_status rba_pcg_solve(rba_ctx *c, rba_pcg_stats *stats) {
     // huge tracks (k > 512, config 5) its branches run the fused two-read kernel measurably slower
     // than the eager issue order (31.3 vs 27.3 ms per product), so those problems loop on the host.
     const bool no_graph = getenv("RBA_NO_GRAPH") != nullptr || c->n_huge_fused > 0 || c->n_huge_out > 0;
-    if (!c->have_comm && !no_graph && !c->pcg_exec && !c->pcg_graph_failed) {
+    if (!c->host_reduce_path() && !no_graph && !c->pcg_exec && !c->pcg_graph_failed) {
         if (build_pcg_graph(c) != cudaSuccess) {
             cudaGetLastError();
             c->pcg_graph_failed = true;
         }
     }
-    if (!c->have_comm && c->pcg_exec && !no_graph) {
+    if (!c->host_reduce_path() && c->pcg_exec && !no_graph) {
         // device-side loop: no host round trip per iteration, no post-convergence launches
         c->h_scal[SC_LAM] = lam;
         CK(cudaMemcpyAsync(d.scal + SC_LAM, c->h_scal + SC_LAM, sizeof(double), cudaMemcpyHostToDevice, c->stream));
@@ -913,7 +914,7 @@ extern "C" rba_status rba_pcg_solve(rba_ctx *c, rba_pcg_stats *stats) {
         c->launches += c->graph_body_kernels * std::max(1, c->h_pcg->it);
     }
     int batch = 2;
-    for (; !(!c->have_comm && c->pcg_exec && !no_graph);) {
+    for (; !(!c->host_reduce_path() && c->pcg_exec && !no_graph);) {
         CK(cudaMemcpyAsync(c->h_pcg, d.pcg, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
         if (c->h_pcg->done || c->h_pcg->it >= c->opt.pcg_max_iters) break;

@@ -245,6 +245,9 @@ struct rba_ctx {
     int64_t graph_body_kernels = 0;  // kernels per PCG-graph iteration (launch accounting)
     bool pcg_fused = false;          // the last PCG product left its sum in the per-SM slices
     bool nofork = false;             // launch the per-class kernels on the context stream only
+    bool emulate_comm = false;       // RBA_EMULATE_COMM: the multi-GPU PCG path (host loop, product
+                                     // reduced before the update) on one GPU, all-reduces skipped
+    bool host_reduce_path() const { return have_comm || emulate_comm; }
     bool profiling = false;
     int64_t prof_real_matvecs = 0;  // matvecs that did work (PCG iterations + hook calls) since rba_profile
     std::vector<rba::Launch> prof;

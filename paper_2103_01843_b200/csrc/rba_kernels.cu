@@ -2110,7 +2110,10 @@ cudaError_t launch_matvec(rba_ctx *c, const float *v, float *) { return matvec_i
 // PCG iteration product: the slices are reduced by k_pcg_a unless the result is all-reduced first
 cudaError_t launch_matvec_pcg(rba_ctx *c) {
     Prof P(c, KID_MATVEC, plan_matvec_bytes(c));
-    c->pcg_fused = matvec_body(c, c->d.p32, c->d.pcg, c->have_comm);
+    // with an all-reduce between product and update (multi-GPU), reduce the slices into wd here
+    // and let the update kernels read wd; otherwise the first update kernel sums the slices
+    const bool reduce_now = c->host_reduce_path();
+    c->pcg_fused = matvec_body(c, c->d.p32, c->d.pcg, reduce_now) && !reduce_now;
     P.end();
     return cudaGetLastError();
 }

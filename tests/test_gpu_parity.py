@@ -163,6 +163,21 @@ def test_lm_cost_trajectory(cfg, iters):
         assert abs(rg["cost_after"] - ro["cost_after"]) <= 1e-4 * ro["cost_after"], (i, rg, ro)
 
 
+@pytest.mark.parametrize("storage", [0, 1])
+def test_lm_on_the_multi_gpu_pcg_path(monkeypatch, storage):
+    """The PCG path a sharded run takes (host loop, product reduced into wd before the update
+    kernels, where the NCCL all-reduce sits), emulated on one GPU (RBA_EMULATE_COMM): same cost
+    trajectory as the oracle."""
+    monkeypatch.setenv("RBA_EMULATE_COMM", "1")
+    p = synth.make_problem(2)
+    s = _solver(p, storage=storage)
+    o = oracle.Oracle(p)
+    for i in range(4):
+        rg, ro = s.lm_step(), o.lm_step()
+        assert rg["pcg_reason"] != 2
+        assert abs(rg["cost_after"] - ro["cost_after"]) <= 1e-4 * ro["cost_after"], (i, rg, ro)
+
+
 def test_state_io_round_trip_and_lm_state():
     """rba_set_state / rba_get_state (the device-side landmark permutation between the caller's
     order and the internal k-sorted order) are exact, including on landmark shards; after LM
