@@ -681,7 +681,6 @@ __global__ void k_fac_redamp(DevProblem d, float lam) {
 
 // ============================================================================ launchers
 static inline unsigned nbk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
-static const int FAC_G[5] = {2, 4, 8, 16, 32};
 
 template <int G>
 static void fac_cls(rba_ctx *c, int cls, int what, const float *v, const PcgState *st, float lam, cudaStream_t s) {

@@ -85,7 +85,6 @@ __global__ void __launch_bounds__(256) k_linearize(DevProblem d) {
 __global__ void k_cam_scale(DevProblem d, float dmin, float dmax) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= 9 * d.n_p) return;
-    const int64_t cam = i / 9;
     if (d.s64) {
         const double n2 = d.cam_n2d[i];
         const double s = 1.0 / (1.0 + sqrt(n2));

@@ -533,157 +533,6 @@ __global__ void __launch_bounds__(256) k_redamp64(DevProblem d, double lam) {
     }
 }
 
-// ---- K5-64 for short tracks (k <= 32): a group of G lanes (G | 32) per landmark, 32/G landmarks
-// per warp, lane <-> camera block; rows looped to the warp's longest landmark so the G-wide
-// shuffles always see every lane.  One item (all reduced rows) per landmark.
-template <int G>
-__global__ void __launch_bounds__(256) k_rcs64_small(DevProblem d, const LargeItem *__restrict__ items, int64_t n_items,
-                                                     const double *__restrict__ v, const PcgState *__restrict__ st) {
-    if (st && st->done) return;
-    const int lane = threadIdx.x & 31, gl = lane % G;
-    const int64_t idx = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
-    const bool valid = idx < n_items;
-    LargeItem it{0, 0, 0, 0};
-    if (valid) it = items[idx];
-    const int64_t j = it.lm;
-    const int k = valid ? d.lm_k[j] : 0;
-    const bool act = gl < k;
-    const Blk64 B = blk64(d, valid ? j : 0, k > 0 ? k : 2);
-    const int32_t *oc = d.obs_cam + (valid ? d.lm_obs0[j] : 0);
-    double vo[9], acc[9];
-#pragma unroll
-    for (int q = 0; q < 9; q++) vo[q] = act ? v[9 * (int64_t)oc[gl] + q] : 0.0, acc[q] = 0.0;
-    const int nrows = valid ? it.t1 - it.t0 : 0;
-    int maxrows = nrows;
-#pragma unroll
-    for (int m = 16; m; m >>= 1) maxrows = max(maxrows, __shfl_xor_sync(0xffffffffu, maxrows, m));
-    for (int r = 0; r < maxrows; r++) {
-        double x[9];
-        const bool live = act && r < nrows;
-        const double *rw = live ? B.row(it.t0 + r) + 9 * gl : nullptr;
-#pragma unroll
-        for (int q = 0; q < 9; q++) x[q] = live ? rw[q] : 0.0;
-        double y = 0.0;
-#pragma unroll
-        for (int q = 0; q < 9; q++) y += x[q] * vo[q];
-#pragma unroll
-        for (int m = G / 2; m; m >>= 1) y += __shfl_xor_sync(0xffffffffu, y, m, G);
-#pragma unroll
-        for (int q = 0; q < 9; q++) acc[q] += x[q] * y;
-    }
-    if (act) {
-        double *out = d.wd + 9 * (int64_t)oc[gl];
-#pragma unroll
-        for (int q = 0; q < 9; q++) atomicAdd(out + q, acc[q]);
-    }
-}
-
-// ---- K4-64 / K5-64: CTA per landmark, rows 3..2k+2 of the block (the reduced rows A_j, q_j).
-// Product: per chunk of 8 rows, warps compute y_a = A[a] . v (lanes over columns, coalesced),
-// then thread <-> camera block accumulates out_o += A[a, block o]^T y_a (re-read from L1).
-template <int NT, int NB, bool PRE>
-__global__ void __launch_bounds__(NT) k_rcs64(DevProblem d, const LargeItem *__restrict__ items,
-                                              const double *__restrict__ v, const PcgState *__restrict__ st) {
-    if (!PRE && st && st->done) return;
-    // NB: camera blocks per thread (k <= NB * NT in this class)
-    const LargeItem it = items[blockIdx.x];  // rows [it.t0, it.t1) of the reduced rows 3..2k+2
-    const int64_t j = it.lm;
-    const int k = d.lm_k[j], tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const Blk64 B = blk64(d, j, k);
-    const int32_t *oc = d.obs_cam + d.lm_obs0[j];
-    if (PRE) {
-        for (int o = tid; o < k; o += NT) {
-            double P[45] = {}, b[9] = {};
-            for (int a = it.t0; a < it.t1; a++) {
-                const double *rw = B.row(a);
-                double x[9];
-                for (int q = 0; q < 9; q++) x[q] = rw[9 * o + q];
-                const double qa = rw[9 * k + 3];
-                int idx = 0;
-                for (int q1 = 0; q1 < 9; q1++) {
-                    b[q1] += x[q1] * qa;
-                    for (int q2 = q1; q2 < 9; q2++) P[idx++] += x[q1] * x[q2];
-                }
-            }
-            double *acc = d.pd + 54 * (int64_t)oc[o];
-            for (int i = 0; i < 45; i++) atomicAdd(acc + i, P[i]);
-            for (int i = 0; i < 9; i++) atomicAdd(acc + 45 + i, b[i]);
-        }
-        return;
-    }
-    // thread <-> camera blocks o = tid + m NT (m < NB): its v_o in registers; per chunk of CR rows the
-    // partial dot products over its blocks are reduced across the CTA (warp shuffles, + smem for
-    // NT > 32), then out_o += A[a, o]^T y_a re-reads its row segments (L1 hits)
-    constexpr int CR = NB == 1 ? 8 : (NB == 2 ? 4 : 2);  // rows per chunk (register budget)
-    __shared__ double part[CR][NT / 32];
-    double acc[NB][9], vo[NB][9];
-#pragma unroll
-    for (int m = 0; m < NB; m++) {
-        const int o = tid + m * NT;
-#pragma unroll
-        for (int q = 0; q < 9; q++) {
-            acc[m][q] = 0.0;
-            vo[m][q] = o < k ? v[9 * (int64_t)oc[o] + q] : 0.0;
-        }
-    }
-    for (int a0 = it.t0; a0 < it.t1; a0 += CR) {
-        const int nr = min(CR, it.t1 - a0);
-        double y[CR];
-#pragma unroll
-        for (int r = 0; r < CR; r++) {
-            double s = 0.0;
-            if (r < nr) {
-                const double *rw = B.row(a0 + r);
-#pragma unroll
-                for (int m = 0; m < NB; m++) {
-                    const int o = tid + m * NT;
-                    if (o < k)
-#pragma unroll
-                        for (int q = 0; q < 9; q++) s += rw[9 * o + q] * vo[m][q];
-                }
-            }
-            y[r] = warp_sum_d(s);
-        }
-        if (NT > 32) {
-            if (lane == 0)
-#pragma unroll
-                for (int r = 0; r < CR; r++) part[r][warp] = y[r];
-            __syncthreads();
-#pragma unroll
-            for (int r = 0; r < CR; r++) {
-                double t = 0.0;
-#pragma unroll
-                for (int w = 0; w < NT / 32; w++) t += part[r][w];
-                y[r] = t;
-            }
-            __syncthreads();
-        }
-#pragma unroll
-        for (int m = 0; m < NB; m++) {
-            const int o = tid + m * NT;
-            if (o < k) {
-#pragma unroll
-                for (int r = 0; r < CR; r++) {
-                    if (r < nr) {
-                        const double *rw = B.row(a0 + r) + 9 * o;
-#pragma unroll
-                        for (int q = 0; q < 9; q++) acc[m][q] += rw[q] * y[r];
-                    }
-                }
-            }
-        }
-    }
-#pragma unroll
-    for (int m = 0; m < NB; m++) {
-        const int o = tid + m * NT;
-        if (o < k) {
-            double *out = d.wd + 9 * (int64_t)oc[o];
-#pragma unroll
-            for (int q = 0; q < 9; q++) atomicAdd(out + q, acc[m][q]);
-        }
-    }
-}
-
 // ---- K4-64 / K5-64 for k <= 16, TMA-staged and warp-specialized: persistent CTA (one per SM) of
 // 8 consumer warps + 1 producer warp, ring of 4 stages of 48 KB.  A stage holds a batch of
 // consecutive landmarks (<= 256 / G): each landmark's reduced rows 3..2k+2 (one cp.async.bulk per
@@ -843,11 +692,11 @@ __global__ void __launch_bounds__(32 * (WS_CW + 1), 1) k_rcs64_ws(DevProblem d, 
 // <-> camera blocks o = tid + m NT: per chunk, partial dots over its 9-column segments (shared-memory
 // reads at a 72-byte lane stride: conflict-free per half-warp), y_a reduced across the CTA, then
 // out_o += A[a, o]^T y_a from the same staged rows.  One HBM read of A_j per product.
-template <int NT, int NB, bool PRE>
+template <int NT, int NB>
 __global__ void __launch_bounds__(NT) k_rcs64_tma(DevProblem d, const LargeItem *__restrict__ items,
                                                   const double *__restrict__ v, const PcgState *__restrict__ st,
                                                   int CRMAX, int S, int stage_dbl) {
-    if (!PRE && st && st->done) return;
+    if (st && st->done) return;
     extern __shared__ __align__(16) double sm64[];
     uint64_t *full = reinterpret_cast<uint64_t *>(sm64 + (size_t)S * stage_dbl);
     double *part = reinterpret_cast<double *>(full + S);  // CRMAX x (NT / 32)
@@ -863,61 +712,18 @@ __global__ void __launch_bounds__(NT) k_rcs64_tma(DevProblem d, const LargeItem 
     }
     __syncthreads();
     const uint64_t pol = policy_evict_first();
-    // PRE streams the item once per camera-block pass m < NB (54 accumulators per thread and
-    // pass; the repeated reads of the ~1 MB item mostly hit L2): chunk sequence c = m nch + chunk
-    const int ntot = PRE ? NB * nch : nch;
-    auto issue = [&](int cc) {  // thread 0: chunk cc -> stage cc % S
-        const int c = cc % nch;
+    auto issue = [&](int c) {  // thread 0: chunk c -> stage c % S
         const int a0 = it.t0 + c * CR, nr = min(CR, it.t1 - a0);
         const uintptr_t lo = reinterpret_cast<uintptr_t>(B + (int64_t)a0 * W) & ~(uintptr_t)15;
         const uintptr_t hi = (reinterpret_cast<uintptr_t>(B + (int64_t)(a0 + nr) * W) + 15) & ~(uintptr_t)15;
-        uint64_t *bar = &full[cc % S];
+        uint64_t *bar = &full[c % S];
         mbar_arrive_expect_tx(bar, (uint32_t)(hi - lo));
-        bulk_g2s_stream(sm64 + (size_t)(cc % S) * stage_dbl, reinterpret_cast<const void *>(lo), (uint32_t)(hi - lo),
+        bulk_g2s_stream(sm64 + (size_t)(c % S) * stage_dbl, reinterpret_cast<const void *>(lo), (uint32_t)(hi - lo),
                         bar, pol);
     };
     if (tid == 0)
-        for (int c = 0; c < min(S, ntot); c++) issue(c);
+        for (int c = 0; c < min(S, nch); c++) issue(c);
     const int32_t *oc = d.obs_cam + d.lm_obs0[j];
-    if (PRE) {
-        double P[45], bb[9];
-        for (int cc = 0; cc < ntot; cc++) {
-            const int c = cc % nch, o = tid + (cc / nch) * NT;
-            if (c == 0) {
-#pragma unroll
-                for (int i = 0; i < 45; i++) P[i] = 0.0;
-#pragma unroll
-                for (int i = 0; i < 9; i++) bb[i] = 0.0;
-            }
-            const int s = cc % S, a0 = it.t0 + c * CR, nr = min(CR, it.t1 - a0);
-            mbar_wait(&full[s], (uint32_t)((cc / S) & 1));
-            const double *rows =
-                sm64 + (size_t)s * stage_dbl + ((reinterpret_cast<uintptr_t>(B + (int64_t)a0 * W) >> 3) & 1);
-            if (o < k)
-                for (int r = 0; r < nr; r++) {
-                    const double *x = rows + r * W + 9 * o;
-                    const double qa = rows[r * W + 9 * k + 3];
-                    int idx = 0;
-#pragma unroll
-                    for (int q1 = 0; q1 < 9; q1++) {
-                        const double x1 = x[q1];
-                        bb[q1] = fma(x1, qa, bb[q1]);
-#pragma unroll
-                        for (int q2 = q1; q2 < 9; q2++, idx++) P[idx] = fma(x1, x[q2], P[idx]);
-                    }
-                }
-            __syncthreads();
-            if (tid == 0 && cc + S < ntot) issue(cc + S);
-            if (c == nch - 1 && o < k) {  // end of pass: block o's sums
-                double *acc = d.pd + 54 * (int64_t)oc[o];
-#pragma unroll
-                for (int i = 0; i < 45; i++) atomicAdd(acc + i, P[i]);
-#pragma unroll
-                for (int i = 0; i < 9; i++) atomicAdd(acc + 45 + i, bb[i]);
-            }
-        }
-        return;
-    }
     double acc[NB][9], vo[NB][9];
 #pragma unroll
     for (int m = 0; m < NB; m++) {
@@ -972,6 +778,83 @@ __global__ void __launch_bounds__(NT) k_rcs64_tma(DevProblem d, const LargeItem 
             double *out = d.wd + 9 * (int64_t)oc[o];
 #pragma unroll
             for (int q = 0; q < 9; q++) atomicAdd(out + q, acc[m][q]);
+        }
+    }
+}
+
+// ---- K4-64 for k > 16, TMA-staged like k_rcs64_tma: 54 FP64 accumulators per thread, so the item
+// is streamed once per camera-block pass m < NB (the repeated reads of the ~1 MB item mostly hit
+// L2); chunk sequence c = m nch + chunk.
+template <int NT, int NB>
+__global__ void __launch_bounds__(NT) k_pre64_tma(DevProblem d, const LargeItem *__restrict__ items, int CRMAX,
+                                                  int S, int stage_dbl) {
+    constexpr bool PRE = true;
+    extern __shared__ __align__(16) double sm64[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(sm64 + (size_t)S * stage_dbl);
+    const LargeItem it = items[blockIdx.x];
+    const int64_t j = it.lm;
+    const int k = d.lm_k[j], W = 9 * k + 4, tid = threadIdx.x;
+    const int CR = CRMAX;  // rows per stage (sized for the class's longest track)
+    const double *B = d.arena64 + d.lm_r2[j] - 3 * (int64_t)W;  // row a at B + a W for a >= 3
+    const int nrows = it.t1 - it.t0, nch = (nrows + CR - 1) / CR;
+    if (tid == 0) {
+        for (int s = 0; s < S; s++) mbar_init(&full[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const uint64_t pol = policy_evict_first();
+    // PRE streams the item once per camera-block pass m < NB (54 accumulators per thread and
+    // pass; the repeated reads of the ~1 MB item mostly hit L2): chunk sequence c = m nch + chunk
+    const int ntot = PRE ? NB * nch : nch;
+    auto issue = [&](int cc) {  // thread 0: chunk cc -> stage cc % S
+        const int c = cc % nch;
+        const int a0 = it.t0 + c * CR, nr = min(CR, it.t1 - a0);
+        const uintptr_t lo = reinterpret_cast<uintptr_t>(B + (int64_t)a0 * W) & ~(uintptr_t)15;
+        const uintptr_t hi = (reinterpret_cast<uintptr_t>(B + (int64_t)(a0 + nr) * W) + 15) & ~(uintptr_t)15;
+        uint64_t *bar = &full[cc % S];
+        mbar_arrive_expect_tx(bar, (uint32_t)(hi - lo));
+        bulk_g2s_stream(sm64 + (size_t)(cc % S) * stage_dbl, reinterpret_cast<const void *>(lo), (uint32_t)(hi - lo),
+                        bar, pol);
+    };
+    if (tid == 0)
+        for (int c = 0; c < min(S, ntot); c++) issue(c);
+    const int32_t *oc = d.obs_cam + d.lm_obs0[j];
+    {
+        double P[45], bb[9];
+        for (int cc = 0; cc < ntot; cc++) {
+            const int c = cc % nch, o = tid + (cc / nch) * NT;
+            if (c == 0) {
+#pragma unroll
+                for (int i = 0; i < 45; i++) P[i] = 0.0;
+#pragma unroll
+                for (int i = 0; i < 9; i++) bb[i] = 0.0;
+            }
+            const int s = cc % S, a0 = it.t0 + c * CR, nr = min(CR, it.t1 - a0);
+            mbar_wait(&full[s], (uint32_t)((cc / S) & 1));
+            const double *rows =
+                sm64 + (size_t)s * stage_dbl + ((reinterpret_cast<uintptr_t>(B + (int64_t)a0 * W) >> 3) & 1);
+            if (o < k)
+                for (int r = 0; r < nr; r++) {
+                    const double *x = rows + r * W + 9 * o;
+                    const double qa = rows[r * W + 9 * k + 3];
+                    int idx = 0;
+#pragma unroll
+                    for (int q1 = 0; q1 < 9; q1++) {
+                        const double x1 = x[q1];
+                        bb[q1] = fma(x1, qa, bb[q1]);
+#pragma unroll
+                        for (int q2 = q1; q2 < 9; q2++, idx++) P[idx] = fma(x1, x[q2], P[idx]);
+                    }
+                }
+            __syncthreads();
+            if (tid == 0 && cc + S < ntot) issue(cc + S);
+            if (c == nch - 1 && o < k) {  // end of pass: block o's sums
+                double *acc = d.pd + 54 * (int64_t)oc[o];
+#pragma unroll
+                for (int i = 0; i < 45; i++) atomicAdd(acc + i, P[i]);
+#pragma unroll
+                for (int i = 0; i < 9; i++) atomicAdd(acc + 45 + i, bb[i]);
+            }
         }
     }
 }
@@ -1068,13 +951,6 @@ cudaError_t launch_redamp64(rba_ctx *c, double lam) {
     return cudaGetLastError();
 }
 
-template <int NT, int NB, bool PRE>
-static void rcs64_cls(rba_ctx *c, int cls, const double *v, const PcgState *st) {
-    const int64_t lo = c->s64_plo[cls], hi = c->s64_phi[cls];
-    if (hi <= lo) return;
-    k_rcs64<NT, NB, PRE><<<(unsigned)(hi - lo), NT, 0, c->stream>>>(c->d, c->d.rcs_items + lo, v, st);
-    c->launches++;
-}
 
 // TMA-staged product / block-Jacobi blocks for the rcs items [lo, hi) (tracks up to kmax): stages
 // of CR rows (~32 KB, at least one row), S <= 3
@@ -1090,9 +966,14 @@ static void rcs64_tma_range(rba_ctx *c, int64_t lo, int64_t hi, int64_t kmax, co
     int S = 3;
     while (S > 2 && sizeof(double) * S * (size_t)stage_dbl + fixed > 200 * 1024) S--;
     const size_t sm = sizeof(double) * S * (size_t)stage_dbl + fixed;
-    cudaFuncSetAttribute(k_rcs64_tma<NT, NB, PRE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_rcs64_tma<NT, NB, PRE><<<(unsigned)(hi - lo), NT, sm, c->stream>>>(c->d, c->d.rcs_items + lo, v, st, CRMAX,
-                                                                         S, stage_dbl);
+    if constexpr (PRE) {
+        cudaFuncSetAttribute(k_pre64_tma<NT, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k_pre64_tma<NT, NB><<<(unsigned)(hi - lo), NT, sm, c->stream>>>(c->d, c->d.rcs_items + lo, CRMAX, S, stage_dbl);
+    } else {
+        cudaFuncSetAttribute(k_rcs64_tma<NT, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k_rcs64_tma<NT, NB><<<(unsigned)(hi - lo), NT, sm, c->stream>>>(c->d, c->d.rcs_items + lo, v, st, CRMAX, S,
+                                                                        stage_dbl);
+    }
     c->launches++;
 }
 template <int NT, int NB, bool PRE>
@@ -1124,52 +1005,22 @@ static void rcs64_small_tma(rba_ctx *c, const double *v, const PcgState *st) {
 // wd = sum_j A_j^T A_j v (FP64 atomics; wd zeroed here)
 void launch_rcs64(rba_ctx *c, const double *v, const PcgState *st) {
     cudaMemsetAsync(c->d.wd, 0, sizeof(double) * 9 * c->d.n_p, c->stream);
-    static const bool ldg = getenv("RBA_RCS64_LDG") != nullptr;  // the direct-load kernels (A/B timing)
-    if (!ldg) {
-        rcs64_small_tma<false>(c, v, st);
-        rcs64_tma_range<32, 1, false>(c, c->s64_glo[3], c->s64_ghi[3], 32, v, st);  // 16 < k <= 32
-        rcs64_tma_cls<128, 1, false>(c, 1, v, st);
-        rcs64_tma_cls<256, 1, false>(c, 2, v, st);
-        rcs64_tma_cls<256, 2, false>(c, 3, v, st);
-        rcs64_tma_cls<256, KMAX64 / 256, false>(c, 4, v, st);
-        return;
-    }
-    for (int g = 0; g < 4; g++) {  // k <= 32 by group size 4 / 8 / 16 / 32
-        const int64_t lo = c->s64_glo[g], hi = c->s64_ghi[g];
-        if (hi <= lo) continue;
-        const int G = 4 << g;
-        const unsigned blocks = nb64((hi - lo) * G, 256);
-        const LargeItem *itp = c->d.rcs_items + lo;
-        if (g == 0) k_rcs64_small<4><<<blocks, 256, 0, c->stream>>>(c->d, itp, hi - lo, v, st);
-        else if (g == 1) k_rcs64_small<8><<<blocks, 256, 0, c->stream>>>(c->d, itp, hi - lo, v, st);
-        else if (g == 2) k_rcs64_small<16><<<blocks, 256, 0, c->stream>>>(c->d, itp, hi - lo, v, st);
-        else k_rcs64_small<32><<<blocks, 256, 0, c->stream>>>(c->d, itp, hi - lo, v, st);
-        c->launches++;
-    }
-    rcs64_cls<128, 1, false>(c, 1, v, st);
-    rcs64_cls<256, 1, false>(c, 2, v, st);
-    rcs64_cls<256, 2, false>(c, 3, v, st);
-    rcs64_cls<256, KMAX64 / 256, false>(c, 4, v, st);
+    rcs64_small_tma<false>(c, v, st);
+    rcs64_tma_range<32, 1, false>(c, c->s64_glo[3], c->s64_ghi[3], 32, v, st);  // 16 < k <= 32
+    rcs64_tma_cls<128, 1, false>(c, 1, v, st);
+    rcs64_tma_cls<256, 1, false>(c, 2, v, st);
+    rcs64_tma_cls<256, 2, false>(c, 3, v, st);
+    rcs64_tma_cls<256, KMAX64 / 256, false>(c, 4, v, st);
 }
 
 void launch_pre64(rba_ctx *c) {
     cudaMemsetAsync(c->d.pd, 0, sizeof(double) * 54 * c->d.n_p, c->stream);
-    static const bool ldg = getenv("RBA_RCS64_LDG") != nullptr;
-    if (!ldg) {
-        rcs64_small_tma<true>(c, nullptr, nullptr);
-        rcs64_tma_range<32, 1, true>(c, c->s64_glo[3], c->s64_ghi[3], 32, nullptr, nullptr);
-        rcs64_tma_cls<128, 1, true>(c, 1, nullptr, nullptr);
-        rcs64_tma_cls<256, 1, true>(c, 2, nullptr, nullptr);
-        rcs64_tma_cls<256, 2, true>(c, 3, nullptr, nullptr);
-        rcs64_tma_cls<256, KMAX64 / 256, true>(c, 4, nullptr, nullptr);
-        return;
-    } else {
-        rcs64_cls<32, 1, true>(c, 0, nullptr, nullptr);
-        rcs64_cls<128, 1, true>(c, 1, nullptr, nullptr);
-        rcs64_cls<256, 1, true>(c, 2, nullptr, nullptr);
-    }
-    rcs64_cls<256, 2, true>(c, 3, nullptr, nullptr);
-    rcs64_cls<256, KMAX64 / 256, true>(c, 4, nullptr, nullptr);
+    rcs64_small_tma<true>(c, nullptr, nullptr);
+    rcs64_tma_range<32, 1, true>(c, c->s64_glo[3], c->s64_ghi[3], 32, nullptr, nullptr);
+    rcs64_tma_cls<128, 1, true>(c, 1, nullptr, nullptr);
+    rcs64_tma_cls<256, 1, true>(c, 2, nullptr, nullptr);
+    rcs64_tma_cls<256, 2, true>(c, 3, nullptr, nullptr);
+    rcs64_tma_cls<256, KMAX64 / 256, true>(c, 4, nullptr, nullptr);
 }
 
 cudaError_t launch_backsub64(rba_ctx *c, float lam) {

@@ -14,4 +14,4 @@ torch.cuda.synchronize()
 rba.rba_profile(s.h, True)
 for _ in range(a.reps): s.matvec(v)
 ms, n, by = rba.rba_profile_get(s.h, "matvec")
-print(f"cfg{a.config} matvec {ms/n:.3f} ms  {by/n/(ms/n*1e-3)/1e9:.0f} GB/s  precision={a.precision} ldg={os.environ.get('RBA_RCS64_LDG','0')}")
+print(f"cfg{a.config} matvec {ms/n:.3f} ms  {by/n/(ms/n*1e-3)/1e9:.0f} GB/s  precision={a.precision}")
