@@ -324,6 +324,23 @@ def test_huber_reduced_system_and_lm(cfg):
         assert abs(rg["cost_after"] - ro["cost_after"]) <= 1e-4 * ro["cost_after"], (i, rg, ro)
 
 
+@pytest.mark.parametrize("kw,bar", [(dict(storage=1), 1e-4), (dict(precision=1), 1e-6),
+                                    (dict(solver=2), 1e-5)])
+def test_huber_with_other_paths(kw, bar):
+    """f1 combined with f4 (factored), f2 (sqrt-BA-64) and f3 (explicit-64): LM costs with Huber
+    (delta = 1 px) vs the oracle's (the §8c bar 1e-4 for FP32 storage; tighter for the FP64 paths:
+    1e-6 for sqrt-BA-64, whose column scaling is FP64, 1e-5 for explicit-64, which shares the FP32
+    column scaling S_p, D_p^2 of K1 -- seen: 3e-6 at the third iteration)."""
+    p = synth.make_problem(2)
+    s = _solver(p, huber_delta=1.0, **kw)
+    o = oracle.Oracle(p)
+    o.set_huber(1.0)
+    for i in range(4):
+        rg, ro = s.lm_step(), o.lm_step()
+        assert rg["pcg_reason"] != 2
+        assert abs(rg["cost_after"] - ro["cost_after"]) <= bar * ro["cost_after"], (i, rg, ro)
+
+
 def test_bal_ingest_end_to_end(tmp_path):
     """f1 end to end: a BAL file written from a synthetic problem, read back with the paper's
     preprocessing (gauge normalization to MAD 100, seeded perturbation, z-filter), solved
