@@ -960,7 +960,10 @@ static void rcs64_tma_range(rba_ctx *c, int64_t lo, int64_t hi, int64_t kmax, co
     const int64_t W = 9 * kmax + 4;
     // stages of ~32 KB (at least one row of the class's longest track); S = 3 keeps 2 CTAs per SM
     // (1 CTA per SM measured 2x slower: the per-item start-up is then exposed)
-    const int CRMAX = (int)std::max<int64_t>(1, 4096 / W);
+    // narrow CTAs get smaller stages so that more of them fit per SM (latency hiding)
+    static const int64_t tgt_env = getenv("RBA_RCS64_STAGE_DBL") ? atoll(getenv("RBA_RCS64_STAGE_DBL")) : 0;
+    const int64_t tgt = tgt_env > 0 ? tgt_env : (NT >= 256 ? 4096 : (NT >= 128 ? 2048 : 1024));
+    const int CRMAX = (int)std::max<int64_t>(1, tgt / W);
     const int stage_dbl = (int)((CRMAX * W + 2 + 1) & ~(int64_t)1);
     const size_t fixed = 8 * 4 + sizeof(double) * CRMAX * (NT / 32);
     int S = 3;
