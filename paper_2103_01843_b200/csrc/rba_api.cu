@@ -706,6 +706,10 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     CKSC(dalloc_n(c, &d.wsl, (int64_t)d.nslice * 12 * n_cams));
     CKC(cudaMemsetAsync(d.psl, 0, sizeof(float) * d.nslice * PACC_STRIDE * n_cams, c->stream));
     CKC(cudaMemsetAsync(d.wsl, 0, sizeof(float) * d.nslice * 12 * n_cams, c->stream));
+    if (d.s64) {
+        CKSC(dalloc_n(c, &d.wsl64, (int64_t)d.nslice * 9 * n_cams));
+        CKC(cudaMemsetAsync(d.wsl64, 0, sizeof(double) * d.nslice * 9 * n_cams, c->stream));
+    }
     CKSC(dalloc_n(c, &d.pd, 54 * n_cams));
     CKSC(dalloc_n(c, &d.wd, 9 * n_cams));
     CKSC(dalloc_n(c, &d.p32, 9 * n_cams));

@@ -173,6 +173,7 @@ struct DevProblem {
     int s64;
     double *arena64, *lm_s64, *lm_D64;
     LargeItem *rcs_items;  // sqrt-BA-64 product / block-Jacobi items: (landmark, rows [t0, t1) of 3..2k+2)
+    double *wsl64;         // sqrt-BA-64: per-SM FP64 slices of the product (nslice x 9 n_p), summed into wd
     int4 *s64_batches;     // sqrt-BA-64, k <= 16: TMA batches {count, stage doubles, first camera index (16-B
                            // aligned), camera indices staged}
     int4 *s64_brec;        // ... and per batch 64 x 2 landmark records {arena offset lo, hi, bytes, stage

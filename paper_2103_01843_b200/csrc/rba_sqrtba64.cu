@@ -675,7 +675,7 @@ __global__ void __launch_bounds__(32 * (WS_CW + 1), 1) k_rcs64_ws(DevProblem d, 
                     for (int q = 0; q < 9; q++) acc[q] = fma(x[u][q], y[u], acc[q]);
             }
             if (act) {
-                double *out = d.wd + 9 * (int64_t)cam;
+                double *out = d.wsl64 + ((int64_t)smid() * d.n_p + cam) * 9;  // this SM's slice
 #pragma unroll
                 for (int q = 0; q < 9; q++) atomicAdd(out + q, acc[q]);
             }
@@ -775,7 +775,7 @@ __global__ void __launch_bounds__(NT) k_rcs64_tma(DevProblem d, const LargeItem 
     for (int m = 0; m < NB; m++) {
         const int o = tid + m * NT;
         if (o < k) {
-            double *out = d.wd + 9 * (int64_t)oc[o];
+            double *out = d.wsl64 + ((int64_t)smid() * d.n_p + oc[o]) * 9;  // this SM's slice
 #pragma unroll
             for (int q = 0; q < 9; q++) atomicAdd(out + q, acc[m][q]);
         }
@@ -856,6 +856,43 @@ __global__ void __launch_bounds__(NT) k_pre64_tma(DevProblem d, const LargeItem 
                 for (int i = 0; i < 9; i++) atomicAdd(acc + 45 + i, bb[i]);
             }
         }
+    }
+}
+
+// wd = sum of the per-SM FP64 product slices (32 outputs x 8 slice phases per CTA, all loads in
+// flight first), zeroing them for the next product
+__global__ void __launch_bounds__(256) k_reduce_slices64(DevProblem d, const PcgState *__restrict__ st) {
+    if (st && st->done) return;
+    __shared__ double part[8][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int64_t N = 9 * d.n_p, i = (int64_t)blockIdx.x * 32 + tx;
+    double s = 0.0;
+    if (i < N) {
+        double a[24];
+#pragma unroll
+        for (int u = 0; u < 24; u++) {
+            const int k = ty + 8 * u;
+            a[u] = k < d.nslice ? d.wsl64[k * N + i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 24; u++) {
+            const int k = ty + 8 * u;
+            if (k < d.nslice) d.wsl64[k * N + i] = 0.0;
+        }
+        for (int k = ty + 8 * 24; k < d.nslice; k += 8) {
+            s += d.wsl64[k * N + i];
+            d.wsl64[k * N + i] = 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 24; u++) s += a[u];
+    }
+    part[ty][tx] = s;
+    __syncthreads();
+    if (ty == 0 && i < N) {
+        double t = 0.0;
+#pragma unroll
+        for (int y = 0; y < 8; y++) t += part[y][tx];
+        d.wd[i] = t;
     }
 }
 
@@ -1005,15 +1042,16 @@ static void rcs64_small_tma(rba_ctx *c, const double *v, const PcgState *st) {
     }
 }
 
-// wd = sum_j A_j^T A_j v (FP64 atomics; wd zeroed here)
+// wd = sum_j A_j^T A_j v: FP64 atomics into per-SM slices, summed into wd by k_reduce_slices64
 void launch_rcs64(rba_ctx *c, const double *v, const PcgState *st) {
-    cudaMemsetAsync(c->d.wd, 0, sizeof(double) * 9 * c->d.n_p, c->stream);
     rcs64_small_tma<false>(c, v, st);
     rcs64_tma_range<32, 1, false>(c, c->s64_glo[3], c->s64_ghi[3], 32, v, st);  // 16 < k <= 32
     rcs64_tma_cls<128, 1, false>(c, 1, v, st);
     rcs64_tma_cls<256, 1, false>(c, 2, v, st);
     rcs64_tma_cls<256, 2, false>(c, 3, v, st);
     rcs64_tma_cls<256, KMAX64 / 256, false>(c, 4, v, st);
+    k_reduce_slices64<<<nb64(9 * c->d.n_p, 32), 256, 0, c->stream>>>(c->d, st);
+    c->launches++;
 }
 
 void launch_pre64(rba_ctx *c) {
