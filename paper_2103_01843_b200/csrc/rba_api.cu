@@ -843,7 +843,6 @@ extern "C" rba_status rba_linearize(rba_ctx *c) {
     if (!c) return fail(RBA_ERR_INVALID_ARG, "null ctx");
     CK(cudaSetDevice(c->device));
     DevProblem &d = c->d;
-    if (d.s64) CK(cudaMemsetAsync(d.cam_n2d, 0, sizeof(double) * 9 * d.n_p, c->stream));
     CK(cudaMemsetAsync(d.scal + SC_E, 0, sizeof(double) * 2, c->stream));
     CK(launch_linearize(c));
     CK(launch_reduce_cam_norms(c));

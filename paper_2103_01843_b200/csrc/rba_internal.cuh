@@ -260,6 +260,7 @@ namespace rba {
 cudaError_t launch_check_depth(rba_ctx *c, int *d_bad);
 cudaError_t launch_cam_prep(rba_ctx *c, int trial);
 cudaError_t launch_reduce_cam_norms(rba_ctx *c);
+void launch_reduce_slices64(rba_ctx *c, double *out);
 cudaError_t launch_pts_permute(rba_ctx *c, int to_internal);
 cudaError_t query_nsmid(rba_ctx *c, int *d_scratch, int *out);
 cudaError_t launch_linearize(rba_ctx *c);

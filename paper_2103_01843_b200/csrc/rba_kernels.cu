@@ -61,8 +61,9 @@ __global__ void __launch_bounds__(256) k_linearize(DevProblem d) {
             if (!(Pz < 0.0)) bad += 1.0;
             e += robust_rho(r[0] * r[0] + r[1] * r[1], d.huber);
             apply_irls<double>(r, Jcd, Jld, d.huber);
+            double *sl = d.wsl64 + ((int64_t)smid() * d.n_p + cam) * 9;  // this SM's FP64 slice
 #pragma unroll
-            for (int q = 0; q < 9; q++) atomicAdd(d.cam_n2d + 9 * (int64_t)cam + q, Jcd[q] * Jcd[q] + Jcd[9 + q] * Jcd[9 + q]);
+            for (int q = 0; q < 9; q++) atomicAdd(sl + q, Jcd[q] * Jcd[q] + Jcd[9 + q] * Jcd[9 + q]);
         } else {
             const double Pz = cam_model_pre(c, X[0], X[1], X[2], uv.x, uv.y, r, Jc, Jl);
             if (!(Pz < 0.0)) bad += 1.0;
@@ -2050,7 +2051,8 @@ static void reduce_slices(rba_ctx *c, float *sl, int stride, int nv, double *out
 
 // K1 camera column norms^2: the per-SM slices into cam_n2d (FP32 path; sqrt-BA-64 adds FP64 directly)
 cudaError_t launch_reduce_cam_norms(rba_ctx *c) {
-    if (!c->d.s64) reduce_slices(c, c->d.wsl, 12, 9, c->d.cam_n2d, nullptr);
+    if (c->d.s64) launch_reduce_slices64(c, c->d.cam_n2d);
+    else reduce_slices(c, c->d.wsl, 12, 9, c->d.cam_n2d, nullptr);
     return cudaGetLastError();
 }
 

@@ -861,7 +861,8 @@ __global__ void __launch_bounds__(NT) k_pre64_tma(DevProblem d, const LargeItem 
 
 // wd = sum of the per-SM FP64 product slices (32 outputs x 8 slice phases per CTA, all loads in
 // flight first), zeroing them for the next product
-__global__ void __launch_bounds__(256) k_reduce_slices64(DevProblem d, const PcgState *__restrict__ st) {
+__global__ void __launch_bounds__(256) k_reduce_slices64(DevProblem d, double *__restrict__ out,
+                                                         const PcgState *__restrict__ st) {
     if (st && st->done) return;
     __shared__ double part[8][33];
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -892,8 +893,12 @@ __global__ void __launch_bounds__(256) k_reduce_slices64(DevProblem d, const Pcg
         double t = 0.0;
 #pragma unroll
         for (int y = 0; y < 8; y++) t += part[y][tx];
-        d.wd[i] = t;
+        out[i] = t;
     }
+}
+void launch_reduce_slices64(rba_ctx *c, double *out) {
+    k_reduce_slices64<<<(unsigned)((9 * c->d.n_p + 31) / 32), 256, 0, c->stream>>>(c->d, out, nullptr);
+    c->launches++;
 }
 
 // ---- K7-64: dl = -R^1^-1 (Q^1^T r^ + Q^1^T J_p dp), warp per landmark (grid-stride)
@@ -1050,7 +1055,7 @@ void launch_rcs64(rba_ctx *c, const double *v, const PcgState *st) {
     rcs64_tma_cls<256, 1, false>(c, 2, v, st);
     rcs64_tma_cls<256, 2, false>(c, 3, v, st);
     rcs64_tma_cls<256, KMAX64 / 256, false>(c, 4, v, st);
-    k_reduce_slices64<<<nb64(9 * c->d.n_p, 32), 256, 0, c->stream>>>(c->d, st);
+    k_reduce_slices64<<<nb64(9 * c->d.n_p, 32), 256, 0, c->stream>>>(c->d, c->d.wd, st);
     c->launches++;
 }
 
