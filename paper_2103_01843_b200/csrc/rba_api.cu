@@ -684,7 +684,7 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
         const size_t ts = d.sc == 2 ? sizeof(double) : sizeof(float);
         CKSC(dalloc_n(c, &d.bsr_ptr, n_cams + 1));
         CKSC(dalloc_n(c, &d.bsr_col, d.nnzb));
-        CKSC(dalloc(c, &d.bsr_val, ts * 81 * (size_t)d.nnzb));
+        CKSC(dalloc(c, &d.bsr_val, ts * SC_BS * (size_t)d.nnzb));
         CKSC(dalloc(c, &d.sc_b, ts * 9 * (size_t)n_cams));
         CKSC(dalloc(c, &d.sc_scratch, ts * 54 * (size_t)std::max<int64_t>(nobs_loc, 1)));
         CKC(cudaMemcpyAsync(d.bsr_ptr, bptr.data(), sizeof(int32_t) * bptr.size(), cudaMemcpyHostToDevice, c->stream));
@@ -1169,7 +1169,8 @@ extern "C" rba_status rba_export_block(rba_ctx *c, int64_t landmark, double *buf
 extern "C" rba_status rba_arena_bytes(rba_ctx *c, int64_t *logical, int64_t *physical) {
     if (!c || !logical || !physical) return fail(RBA_ERR_INVALID_ARG, "null argument");
     if (c->d.sc) {  // explicit SC: the block-sparse H~
-        *logical = *physical = (int64_t)(c->d.sc == 2 ? 8 : 4) * 81 * c->d.nnzb;
+        *logical = (int64_t)(c->d.sc == 2 ? 8 : 4) * 81 * c->d.nnzb;
+        *physical = (int64_t)(c->d.sc == 2 ? 8 : 4) * SC_BS * c->d.nnzb;
         return RBA_OK;
     }
     *logical = c->logical_bytes;

@@ -17,6 +17,7 @@ constexpr int KLARGE = 512;   // k <= KLARGE: one thread per camera block in the
 constexpr int KMAX = 3072;    // largest track length supported (k > KLARGE: "huge" path, smem-bound)
 constexpr int KMAX64 = 1024;
 constexpr int S64_STAGE_DBL = 6144;  // sqrt-BA-64 small-k TMA stage: 48 KB
+constexpr int SC_BS = 84;            // explicit SC: stored elements per 9 x 9 block (81 + 3 pad: 16-byte rows of float4)
 constexpr int CAMPRE = 24;    // doubles of a camera's precomputed model (R, J_left, t, f, k1, k2)  // sqrt-BA-64 (f2): largest track length (registers of the FP64 product)
 
 // ---- landmark-block arena layout ------------------------------------------

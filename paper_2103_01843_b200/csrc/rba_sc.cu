@@ -122,6 +122,56 @@ __device__ __forceinline__ int64_t bsr_find(const DevProblem &d, int r, int c) {
 __device__ __forceinline__ void atomic_add_t(float *p, float v) { atomicAdd(p, v); }
 __device__ __forceinline__ void atomic_add_t(double *p, double v) { atomicAdd(p, v); }
 
+// one (a, b) contribution -L_a^T G_b (+ J_a^T J_a on the diagonal) to a stored 9 x 9 block:
+// FP32 as 21 float4 reductions over the 84-element block, FP64 as 81 scalar ones
+template <typename O>
+__device__ __forceinline__ void sc_block_add(float *B, const float *L, const float *gv, const O &o, bool diag) {
+    float v[SC_BS];
+#pragma unroll
+    for (int q1 = 0; q1 < 9; q1++)
+#pragma unroll
+        for (int q2 = 0; q2 < 9; q2++) {
+            float x = -(L[3 * q1] * gv[3 * q2] + L[3 * q1 + 1] * gv[3 * q2 + 1] + L[3 * q1 + 2] * gv[3 * q2 + 2]);
+            if (diag) x += o.jp[0][q1] * o.jp[0][q2] + o.jp[1][q1] * o.jp[1][q2];
+            v[9 * q1 + q2] = x;
+        }
+#pragma unroll
+    for (int i = 81; i < SC_BS; i++) v[i] = 0.f;
+    float4 *B4 = reinterpret_cast<float4 *>(B);
+#pragma unroll
+    for (int i = 0; i < SC_BS / 4; i++) atomicAdd(B4 + i, make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
+}
+template <typename O>
+__device__ __forceinline__ void sc_block_add(double *B, const double *L, const double *gv, const O &o, bool diag) {
+#pragma unroll 1
+    for (int q1 = 0; q1 < 9; q1++)
+#pragma unroll
+        for (int q2 = 0; q2 < 9; q2++) {
+            double x = -(L[3 * q1] * gv[3 * q2] + L[3 * q1 + 1] * gv[3 * q2 + 1] + L[3 * q1 + 2] * gv[3 * q2 + 2]);
+            if (diag) x += o.jp[0][q1] * o.jp[0][q2] + o.jp[1][q1] * o.jp[1][q2];
+            atomicAdd(B + 9 * q1 + q2, x);
+        }
+}
+
+// lower blocks of H~ from the upper ones: block (r, c), c < r, = block (c, r)^T.  Warp per block row.
+template <typename T>
+__global__ void __launch_bounds__(256) k_sc_mirror(DevProblem d) {
+    T *val = reinterpret_cast<T *>(d.bsr_val);
+    const int lane = threadIdx.x & 31;
+    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (r >= d.n_p) return;
+    for (int e = d.bsr_ptr[r] + lane; e < d.bsr_ptr[r + 1]; e += 32) {
+        const int c = d.bsr_col[e];
+        if (c >= r) continue;
+        const T *U = val + SC_BS * bsr_find(d, c, (int)r);
+        T *B = val + SC_BS * (int64_t)e;
+#pragma unroll
+        for (int q1 = 0; q1 < 9; q1++)
+#pragma unroll
+            for (int q2 = 0; q2 < 9; q2++) B[9 * q1 + q2] = U[9 * q2 + q1];
+    }
+}
+
 // ---- build: warp per landmark (grid-stride).  Phase 1: per observation a, G_a = J_p,a^T J_l,a
 // (9x3, the H_pl block) and L_a = G_a H_ll^-1 go to a per-observation scratch; b~ contributions
 // J_p,a^T r_a - L_a b_l are added.  Phase 2: lane a adds block (a, b), b >= a:
@@ -171,21 +221,16 @@ __global__ void __launch_bounds__(256) k_sc_build(DevProblem d, T lam, float dmi
             T L[27];
 #pragma unroll
             for (int i = 0; i < 27; i++) L[i] = la[i];
+            // upper triangle only (observations are camera-sorted, so cam_a <= cam_b); the lower
+            // blocks are filled by k_sc_mirror
             for (int b = a; b < k; b++) {
                 const int cb = d.obs_cam[obs0 + b];
                 const T *gb = scr + 54 * (obs0 + b);
-                T *B = val + 81 * bsr_find(d, o.cam, cb);
-                T *Bt = b != a ? val + 81 * bsr_find(d, cb, o.cam) : nullptr;
-#pragma unroll 1
-                for (int q1 = 0; q1 < 9; q1++) {
+                T *B = val + SC_BS * bsr_find(d, o.cam, cb);
+                T gv[27];
 #pragma unroll
-                    for (int q2 = 0; q2 < 9; q2++) {
-                        T v = -(L[3 * q1] * gb[3 * q2] + L[3 * q1 + 1] * gb[3 * q2 + 1] + L[3 * q1 + 2] * gb[3 * q2 + 2]);
-                        if (b == a) v += o.jp[0][q1] * o.jp[0][q2] + o.jp[1][q1] * o.jp[1][q2];
-                        atomic_add_t(B + 9 * q1 + q2, v);
-                        if (Bt) atomic_add_t(Bt + 9 * q2 + q1, v);
-                    }
-                }
+                for (int i = 0; i < 27; i++) gv[i] = gb[i];
+                sc_block_add(B, L, gv, o, b == a);
             }
         }
         __syncwarp();
@@ -204,7 +249,7 @@ __global__ void __launch_bounds__(256) k_sc_spmv(DevProblem d, const T *__restri
     const T *val = reinterpret_cast<const T *>(d.bsr_val);
     T s = 0;
     for (int e = d.bsr_ptr[c]; e < d.bsr_ptr[c + 1]; e++) {
-        const T *B = val + 81 * (int64_t)e + 9 * i;
+        const T *B = val + SC_BS * (int64_t)e + 9 * i;
         const T *x = v + 9 * (int64_t)d.bsr_col[e];
 #pragma unroll
         for (int q = 0; q < 9; q++) s += B[q] * x[q];
@@ -217,7 +262,7 @@ template <typename T>
 __global__ void k_sc_precond(DevProblem d) {
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= d.n_p) return;
-    const T *B = reinterpret_cast<const T *>(d.bsr_val) + 81 * bsr_find(d, (int)c, (int)c);
+    const T *B = reinterpret_cast<const T *>(d.bsr_val) + SC_BS * bsr_find(d, (int)c, (int)c);
     const T *bsc = reinterpret_cast<const T *>(d.sc_b);
     double *o = d.pd + 54 * c;
     int idx = 0;
@@ -289,12 +334,13 @@ static inline unsigned nb(int64_t n, int b) { return (unsigned)((n + b - 1) / b)
 template <typename T>
 static cudaError_t sc_build_t(rba_ctx *c, float lam) {
     DevProblem &d = c->d;
-    cudaMemsetAsync(d.bsr_val, 0, sizeof(T) * 81 * (size_t)d.nnzb, c->stream);
+    cudaMemsetAsync(d.bsr_val, 0, sizeof(T) * SC_BS * (size_t)d.nnzb, c->stream);
     cudaMemsetAsync(d.sc_b, 0, sizeof(T) * 9 * (size_t)d.n_p, c->stream);
     if (d.n_l) {
         const unsigned g = (unsigned)std::min<int64_t>(nb(32 * d.n_l, 256), (int64_t)c->num_sms * 16);
         k_sc_build<T><<<g, 256, 0, c->stream>>>(d, (T)lam, (float)c->opt.diag_min, (float)c->opt.diag_max);
-        c->launches++;
+        k_sc_mirror<T><<<nb(32 * d.n_p, 256), 256, 0, c->stream>>>(d);
+        c->launches += 2;
     }
     return cudaGetLastError();
 }
