@@ -237,24 +237,54 @@ __global__ void __launch_bounds__(256) k_sc_build(DevProblem d, T lam, float dmi
     }
 }
 
-// ---- SpMV on the explicit H~ (without lambda D_p^2, added by the PCG update): thread per row
-// (camera c, parameter i) sums over the row's blocks in T; out in FP64.
+// ---- SpMV on the explicit H~ (without lambda D_p^2, added by the PCG update); out in FP64.
+// SpMV, CTA per camera row: threads stride over the row's blocks (each block read once, as 16-byte
+// vectors), 9 partial sums per thread reduced across the CTA (warp shuffles + shared memory).
 template <typename T>
-__global__ void __launch_bounds__(256) k_sc_spmv(DevProblem d, const T *__restrict__ v, double *__restrict__ out,
-                                                 const PcgState *__restrict__ st) {
+__global__ void __launch_bounds__(128) k_sc_spmv_row(DevProblem d, const T *__restrict__ v, double *__restrict__ out,
+                                                     const PcgState *__restrict__ st) {
     if (st && st->done) return;
-    const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (row >= 9 * d.n_p) return;
-    const int c = (int)(row / 9), i = (int)(row - 9 * (int64_t)c);
+    __shared__ double red[4][9];
+    const int c = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const T *val = reinterpret_cast<const T *>(d.bsr_val);
-    T s = 0;
-    for (int e = d.bsr_ptr[c]; e < d.bsr_ptr[c + 1]; e++) {
-        const T *B = val + SC_BS * (int64_t)e + 9 * i;
-        const T *x = v + 9 * (int64_t)d.bsr_col[e];
+    T acc[9];
 #pragma unroll
-        for (int q = 0; q < 9; q++) s += B[q] * x[q];
+    for (int i = 0; i < 9; i++) acc[i] = 0;
+    for (int e = d.bsr_ptr[c] + tid; e < d.bsr_ptr[c + 1]; e += 128) {
+        const T *x = v + 9 * (int64_t)__ldg(d.bsr_col + e);
+        T xv[9];
+#pragma unroll
+        for (int q = 0; q < 9; q++) xv[q] = __ldg(x + q);
+        T b[SC_BS];
+        if constexpr (sizeof(T) == 4) {
+            const float4 *B4 = reinterpret_cast<const float4 *>(val + SC_BS * (int64_t)e);
+#pragma unroll
+            for (int u = 0; u < SC_BS / 4; u++) {
+                const float4 w = __ldcs(B4 + u);
+                b[4 * u] = w.x, b[4 * u + 1] = w.y, b[4 * u + 2] = w.z, b[4 * u + 3] = w.w;
+            }
+        } else {
+            const double2 *B2 = reinterpret_cast<const double2 *>(val + SC_BS * (int64_t)e);
+#pragma unroll
+            for (int u = 0; u < SC_BS / 2; u++) {
+                const double2 w = __ldcs(B2 + u);
+                b[2 * u] = w.x, b[2 * u + 1] = w.y;
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 9; i++)
+#pragma unroll
+            for (int q = 0; q < 9; q++) acc[i] += b[9 * i + q] * xv[q];
     }
-    out[row] = (double)s;
+#pragma unroll
+    for (int i = 0; i < 9; i++) {
+        double t = (double)acc[i];
+#pragma unroll
+        for (int m = 16; m; m >>= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
+        if (lane == 0) red[warp][i] = t;
+    }
+    __syncthreads();
+    if (tid < 9) out[9 * (int64_t)c + tid] = red[0][tid] + red[1][tid] + red[2][tid] + red[3][tid];
 }
 
 // preconditioner blocks (the diagonal blocks of H~, 45 upper entries) and b~ into pd (FP64)
@@ -371,9 +401,9 @@ void launch_sc_spmv(rba_ctx *c, const PcgState *st, const float *v32) {
             c->launches++;
             v = d.z;
         }
-        k_sc_spmv<double><<<nb(9 * d.n_p, 256), 256, 0, c->stream>>>(d, v, d.wd, st);
+        k_sc_spmv_row<double><<<(unsigned)d.n_p, 128, 0, c->stream>>>(d, v, d.wd, st);
     } else {
-        k_sc_spmv<float><<<nb(9 * d.n_p, 256), 256, 0, c->stream>>>(d, v32 ? v32 : d.p32, d.wd, st);
+        k_sc_spmv_row<float><<<(unsigned)d.n_p, 128, 0, c->stream>>>(d, v32 ? v32 : d.p32, d.wd, st);
     }
     c->launches++;
 }
