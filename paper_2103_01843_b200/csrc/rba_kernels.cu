@@ -1,18 +1,24 @@
 // rba_kernels.cu -- sm_100a kernels of the FP32 sqrt-BA hot path (product path; no oracle code).
 //
 //  K0 k_check_depth       validation: every observation in front of its camera
-//  K1 k_linearize         residuals, E, camera Jacobian column norms (P:348 scaling)
+//     k_cam_prep          per camera R(w), J_left(w), t, f, k1, k2 once per state
+//  K1 k_linearize         residuals, E, camera Jacobian column norms into per-SM slices
 //  K1b k_cam_scale        s = 1/(1+|c|), D^2 = clamp(|c|^2 s^2) (C7, C8)
-//  K2 k_marg_small<G>     k <= 32: warp-group per landmark: Jacobians, 3 Householder reflectors
-//     k_marg_large        k > 32: CTA per (landmark, tile range); compact-WY emission of
+//  K2 k_marg_small<G>     k <= 16: G-lane group per landmark: Jacobians, 3 Householder reflectors,
+//                         compact-WY emission, side regions written by one TMA bulk store
+//     k_marg_large<NT>    k > 16: CTA per (landmark, ~4 MB of tiles); compact-WY emission of
 //                         Q^T [J_p | J_l | r] with the 6 damping Givens rotations folded in
 //
 //  K3 k_redamp            undo / re-apply the 6 damping rotations in place (Fig. 3)
-//  K4 k_precond_rhs       block-Jacobi blocks + b~ = sum A^T q
+//  K4 k_small_pipe<1>,    block-Jacobi blocks + b~ = sum A^T q
+//     k_large_pipe<..,1>
 //     k_precond_finalize  + lambda D_p^2, Cholesky inverse per camera (C12)
-//  K5 k_matvec_small<G>,  H~ v = sum_j A_j^T (A_j v_j) (Eq. cg_mult), one HBM pass
-//     k_matvec_large
-//  K6 k_pcg_init/step     PCG vector updates, dots in FP64, device-side termination flag
+//  K5 k_small_pipe<0>,    H~ v = sum_j A_j^T (A_j v_j) (Eq. cg_mult), one HBM pass:
+//     k_large_pipe<..,0>  TMA (cp.async.bulk) + mbarrier pipelines, persistent CTAs;
+//     k_huge_*            k > 512: fused two-read product with TMA L2 prefetch
+//     k_reduce_slices     FP64 sum of the per-SM FP32 slices (C24)
+//  K6 k_pcg_init, k_pcg_a/b/c   one PCG iteration as three multi-CTA kernels (fixed-order dots);
+//                         the loop is a CUDA graph with a device-side while node
 //  K7 k_backsub           dl = -R^_1^-1 (Q^_1^T r^ + Q^_1^T J_p dp), trial point
 //  K8 k_cost              E at the current or trial state (Eq. ba_energy; C14, C17)
 #include <cuda_runtime.h>

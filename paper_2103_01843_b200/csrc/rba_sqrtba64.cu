@@ -2,8 +2,10 @@
 // Table 1): the same QR nullspace marginalization (Householder + compact WY, 6 damping Givens),
 // reduced-camera-system product, block-Jacobi blocks and back-substitution as the FP32 path, with
 // the landmark blocks stored and all their arithmetic done in FP64.  Storage is the paper's logical
-// block itself: (2k+3) x (9k+4) doubles per landmark, row-major (Fig. 2c), followed by the 6
-// Givens pairs.  Camera-space sums use FP64 atomics directly (no FP32 slices).
+// block, (2k+3) x (9k+4) doubles per landmark in row-major rows (Fig. 2c): the reduced rows
+// 3..2k+2 consecutive over landmarks, rows 0..2 and the 6 Givens pairs in a second region.  The
+// product and block-Jacobi passes are TMA-staged (k_rcs64_ws / k_rcs64_tma / k_pre64_tma); the
+// product's camera-space sums go to per-SM FP64 slices (k_reduce_slices64).
 // Product path only (no oracle code).
 #include <cuda_runtime.h>
 
