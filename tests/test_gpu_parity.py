@@ -209,6 +209,28 @@ def test_state_io_round_trip_and_lm_state():
     assert relf(cg - c0, co - c0) <= 1e-3 and relf(pg - p0, po - p0) <= 1e-3
 
 
+@pytest.mark.parametrize("kw", [dict(storage=1), dict(precision=1)])
+def test_virtual_shards_other_storage(kw):
+    """The landmark-sharded decomposition with factored storage (f4) and sqrt-BA-64 (f2): two
+    world=2 contexts on one GPU (no NCCL) hold disjoint shards whose camera-unscaled partial
+    products and costs add up to the full context's."""
+    p = synth.make_tracks(22, list(np.random.default_rng(4).integers(2, 12, 200)) + [40, 60], n_p=64)
+    full = _solver(p, **kw)
+    parts = [_solver(p, world=2, rank=r, **kw) for r in (0, 1)]
+    for s in [full] + parts:
+        s.linearize()
+        s.marginalize(0.0)
+    w = np.random.default_rng(6).normal(size=9 * full.n_p)
+
+    def unscaled(s):
+        sp = s.scaling()[0]
+        v = torch.tensor(w / sp, dtype=torch.float32, device="cuda")
+        return s.matvec(v).double().cpu().numpy() / sp
+
+    assert relf(unscaled(parts[0]) + unscaled(parts[1]), unscaled(full)) <= 1e-5
+    assert abs(sum(s.cost() for s in parts) - full.cost()) <= 1e-6 * full.cost()
+
+
 def test_virtual_shards_sum_to_full():
     """Landmark sharding on one GPU: two contexts (world=2, no NCCL) hold disjoint
     landmark shards and compute only partial sums.  Without the all-reduce each shard scales the
