@@ -1069,6 +1069,8 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
     __shared__ __align__(16) float red[2][C::NC / 32][4];
     const int tid = threadIdx.x;
     const int64_t lo = cta_lo[blockIdx.x], hi = cta_lo[blockIdx.x + 1];
+    // slot s streams the contiguous tile run [lo + s nst, lo + (s + 1) nst): consecutive tiles of a
+    // landmark stay in one slot, so its camera / v / flush work is paid once per landmark, not per tile
     const int64_t nst = (hi - lo + NSLOT - 1) / NSLOT;
     if (tid == 0) {
         for (int s = 0; s < C::STAGES; s++) {
@@ -1092,7 +1094,7 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
             };
 #pragma unroll
             for (int sl = 0; sl < NSLOT; sl++) {
-                const int64_t ti = lo + sl;
+                const int64_t ti = lo + sl * nst;
                 nk[sl] = ti < hi ? tiles[ti].k : 0;
                 noff[sl] = ti < hi ? tiles[ti].off : 0;
                 ntl[sl] = tl_off(ti);
@@ -1109,7 +1111,7 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
                     ctl[sl] = ntl[sl];
                     ck[sl] = nk[sl];
                     total += 144u * (uint32_t)ck[sl] + ((PRECOND && ck[sl]) ? 64u : 0u);
-                    const int64_t tn = lo + (i + 1) * NSLOT + sl;
+                    const int64_t tn = i + 1 < nst ? lo + sl * nst + (i + 1) : hi;
                     nk[sl] = tn < hi ? tiles[tn].k : 0;
                     noff[sl] = tn < hi ? tiles[tn].off : 0;
                     ntl[sl] = tl_off(tn);
@@ -1146,7 +1148,7 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
     for (int64_t i = 0; i < nst; i++) {
         const int s = (int)(i % C::STAGES);
         const uint32_t ph = (uint32_t)((i / C::STAGES) & 1);
-        const int64_t ti = lo + i * NSLOT + slot;
+        const int64_t ti = lo + slot * nst + i;
         const bool have = ti < hi;  // uniform over the slot
         TileRef tr{-1, 0, 0, 0, 0};
         if (have) {
