@@ -56,7 +56,8 @@ def _lm(p, iters=5, ref="after"):
         e0 = ro["cost"] if e0 is None else e0
         assert rg["pcg_reason"] != 2
         den = ro["cost_after"] if ref == "after" else e0
-        assert abs(rg["cost_after"] - ro["cost_after"]) <= 1e-4 * den, (i, rg, ro)
+        bar = 1e-3 if rg["pcg_iters"] != ro["pcg_iters"] else 1e-4  # §8c tolerance edge (tests/_lm.py)
+        assert abs(rg["cost_after"] - ro["cost_after"]) <= bar * den, (i, rg, ro)
 
 
 @pytest.mark.parametrize("lam", [0.0, 1e-4])
