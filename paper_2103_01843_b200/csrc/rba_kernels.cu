@@ -875,7 +875,10 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 // and a work-unit table); warp <-> unit (pack, <= 4 row pairs), lane <-> (landmark m = lane / G,
 // camera block o = lane % G), slabs read from shared memory, row-pair partials reduced with G-lane
 // shuffles, the unit's 9 outputs per lane added to the camera vector with float4 reductions.
-constexpr int SP_WARPS = 12;                        // consumer warps
+#ifndef RBA_SP_WARPS
+#define RBA_SP_WARPS 12
+#endif
+constexpr int SP_WARPS = RBA_SP_WARPS;              // consumer warps
 constexpr int SP_CAMCAP = 320;                      // camera indices per stage (host guarantees)
 constexpr int SP_PACKCAP = 64;                      // packs per stage (host guarantees)
 constexpr int SP_UNITCAP = 4 * SP_PACKCAP;          // work units per stage
