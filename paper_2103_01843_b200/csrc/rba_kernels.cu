@@ -1035,6 +1035,26 @@ __global__ void __launch_bounds__(SP_WARPS * 32 + 32, 1)
             for (int q = 0; q < 9; q++) vo[q] = (valid && !PRECOND) ? vv[9 * cam + q] : 0.f;
             // K4: the landmark's q from the staged copy, row a at qs[a - 3]
             const float *qs = reinterpret_cast<const float *>(stg + SP_OFF_Q) + (pack.q0 - ch.q0) + 2 * k * m;
+            if (PRECOND) {  // the pack's first unit takes all its row pairs: one flush per (landmark, camera)
+                if (p0 != 0 || !valid) continue;
+                float P[45], b[9];
+#pragma unroll
+                for (int q = 0; q < 45; q++) P[q] = 0.f;
+#pragma unroll
+                for (int q = 0; q < 9; q++) b[q] = 0.f;
+                for (int pp = 0; pp < k; pp++) {
+                    float sl[18];
+#pragma unroll
+                    for (int c = 0; c < 9; c++) {
+                        const float2 x = A[(pp * 9 + c) * npk];
+                        sl[2 * c] = x.x, sl[2 * c + 1] = x.y;
+                    }
+                    acc_rows(P, b, sl, qs[2 * pp]);
+                    acc_rows(P, b, sl + 9, qs[2 * pp + 1]);
+                }
+                flush54(pslice(d) + PACC_STRIDE * (int64_t)cam, P, b);
+                continue;
+            }
             switch (min(4, k - p0)) {
                 case 1: small_unit<1, PRECOND>(d, A, npk, p0, k, G, valid, cam, vo, qs, out12); break;
                 case 2: small_unit<2, PRECOND>(d, A, npk, p0, k, G, valid, cam, vo, qs, out12); break;
