@@ -918,20 +918,8 @@ __device__ __forceinline__ void small_unit(const DevProblem &d, const float2 *A,
             sl[u][2 * c] = x.x;
             sl[u][2 * c + 1] = x.y;
         }
-    if (PRECOND) {
-        if (!valid) return;
-        float P[45], b[9];
-#pragma unroll
-        for (int q = 0; q < 45; q++) P[q] = 0.f;
-#pragma unroll
-        for (int q = 0; q < 9; q++) b[q] = 0.f;
-#pragma unroll
-        for (int u = 0; u < NRP; u++) {
-            acc_rows(P, b, sl[u], qs[2 * (p0 + u)]);
-            acc_rows(P, b, sl[u] + 9, qs[2 * (p0 + u) + 1]);
-        }
-        flush54(pslice(d) + PACC_STRIDE * (int64_t)cam, P, b);
-    } else {
+    static_assert(!PRECOND, "K4 accumulates whole landmarks in k_small_pipe");
+    {
         float y[2 * NRP];
 #pragma unroll
         for (int u = 0; u < NRP; u++) {
@@ -1055,11 +1043,13 @@ __global__ void __launch_bounds__(SP_WARPS * 32 + 32, 1)
                 flush54(pslice(d) + PACC_STRIDE * (int64_t)cam, P, b);
                 continue;
             }
-            switch (min(4, k - p0)) {
-                case 1: small_unit<1, PRECOND>(d, A, npk, p0, k, G, valid, cam, vo, qs, out12); break;
-                case 2: small_unit<2, PRECOND>(d, A, npk, p0, k, G, valid, cam, vo, qs, out12); break;
-                case 3: small_unit<3, PRECOND>(d, A, npk, p0, k, G, valid, cam, vo, qs, out12); break;
-                default: small_unit<4, PRECOND>(d, A, npk, p0, k, G, valid, cam, vo, qs, out12); break;
+            if constexpr (!PRECOND) {
+                switch (min(4, k - p0)) {
+                    case 1: small_unit<1, false>(d, A, npk, p0, k, G, valid, cam, vo, qs, out12); break;
+                    case 2: small_unit<2, false>(d, A, npk, p0, k, G, valid, cam, vo, qs, out12); break;
+                    case 3: small_unit<3, false>(d, A, npk, p0, k, G, valid, cam, vo, qs, out12); break;
+                    default: small_unit<4, false>(d, A, npk, p0, k, G, valid, cam, vo, qs, out12); break;
+                }
             }
         }
         __syncwarp();
