@@ -82,6 +82,14 @@ typedef struct {
      * operation in FP64; track lengths up to 1024).  The column scaling and damping diagonals are
      * FP32 in both (shared with K1). */
     int precision;
+    /* 1 = bitwise-reproducible camera-space sums (SURVEY §8b "no float atomics"; the paper's
+     * "parallel reduce"): every landmark's contribution to a camera sum (K1 camera norms,
+     * K4 block-Jacobi blocks and b~, K5 product) is written to its own slot and the slots of a
+     * camera are added in a fixed order, and every scalar sum (E, model decrease) is reduced in a
+     * fixed order, so two runs on the same input produce identical bits.  0 (default) = per-SM
+     * FP32 slices filled by vector atomics (faster; run-to-run differences at FP32 rounding).
+     * Only RBA_SOLVER_SQRTBA with dense FP32 storage supports 1 (else RBA_ERR_INVALID_ARG). */
+    int deterministic;
 } rba_options;
 
 enum { RBA_PRECISION_FP32 = 0, RBA_PRECISION_FP64 = 1 };
@@ -108,6 +116,16 @@ typedef struct {
     double rho;          /* gain ratio (E - E_trial) / model                                   */
     double lambda;       /* damping used for this attempt                                     */
     double lambda_next;
+    int relinearized;    /* 1: this attempt linearized + marginalized; 0: it re-damped the blocks of
+                            the previous linearization (backtracking)                 */
+    int status;          /* 0 running; 1 converged: this accepted step decreased E by less than ftol E
+                            (rba_lm_solve); 2 error: a point is not in front of its camera at
+                            the current state                                                     */
+    /* per-phase device time of this attempt (ms, %globaltimer stamps taken by the kernels, so
+     * valid inside the device-side loop; the paper traces time per iteration) */
+    double t_linearize_ms, t_marginalize_ms, t_precond_ms, t_pcg_ms, t_trial_ms, t_total_ms;
+    int64_t device_bytes; /* device memory held by the context (its peak: every buffer is allocated
+                             by rba_create; the paper traces peak memory)                   */
 } rba_lm_report;
 
 /* Fill defaults: device 0, own stream, world 1, lambda0 1e-4, tol 1e-2, 500 iters, 1e-3, 1e-6, 1e32,
@@ -149,8 +167,21 @@ rba_status rba_backsubstitute(rba_ctx *ctx);
 rba_status rba_cost(rba_ctx *ctx, int at_trial, double *cost);
 
 /* One LM iteration = linearize (if the state changed) -> marginalize / re-damp -> PCG ->
- * back-substitute -> trial cost -> accept / reject and lambda update (C9, C10, C13). */
+ * back-substitute -> trial cost -> accept / reject and lambda update (C9, C10, C13).
+ * The LM schedule (lambda, nu, current E, accept decision) lives on the device and is advanced by
+ * a control kernel; on a single GPU the whole iteration is one CUDA graph (conditional nodes for
+ * relinearize-vs-re-damp and the PCG loop), so the only host synchronization is the copy of the
+ * report.  RBA_ERR_BAD_PROBLEM if a point is not in front of its camera at the current state.
+ * report may be NULL. */
 rba_status rba_lm_step(rba_ctx *ctx, rba_lm_report *report);
+
+/* The LM loop of the paper's experiments: up to max_iters iterations (every attempt
+ * counts, C13), terminating early once an accepted step decreases E by less than ftol * E
+ * ("relative function tolerance"; 1e-6 in the paper).  Runs on the device without host
+ * round trips (a CUDA graph `while` node around the iteration) except for the final copy of the
+ * reports.  reports: caller array of max_iters entries (may be NULL); *n_done: iterations run.
+ * max_iters >= 0, ftol >= 0 else RBA_ERR_INVALID_ARG. */
+rba_status rba_lm_solve(rba_ctx *ctx, int max_iters, double ftol, rba_lm_report *reports, int *n_done);
 
 /* Full state on every rank (host FP64, caller buffers n_cams x 9 and n_points x 3). */
 rba_status rba_get_state(rba_ctx *ctx, double *cameras, double *points);
@@ -158,6 +189,15 @@ rba_status rba_get_state(rba_ctx *ctx, double *cameras, double *points);
 rba_status rba_set_state(rba_ctx *ctx, const double *cameras, const double *points);
 /* Restart the LM schedule: lambda = lambda0, nu = 2, iteration counter 0. */
 rba_status rba_reset_lm(rba_ctx *ctx);
+/* Set / read the LM schedule (lambda > 0, nu >= 1; with the state, this replays an iteration).
+ * rba_get_lm synchronizes. */
+rba_status rba_set_lm(rba_ctx *ctx, double lambda, double nu);
+rba_status rba_get_lm(rba_ctx *ctx, double *lambda, double *nu, int64_t *iter);
+/* Change the PCG stopping rule (reading C11) for the following solves: |rho| <= rel_tol |rho_0| or
+ * max_iters iterations.  rel_tol = 0 with max_iters = n runs exactly n iterations (unless the
+ * system is indefinite): the replay rule of the parity protocol.  rel_tol >= 0,
+ * max_iters >= 0 else RBA_ERR_INVALID_ARG. */
+rba_status rba_set_pcg_limits(rba_ctx *ctx, double rel_tol, int max_iters);
 
 /* ---- test / measurement hooks ----------------------------------------------------------- */
 /* out = H~ v (incl. lambda D_p^2 v at the damping currently folded in); v, out: device FP32 9 n_cams. */
@@ -177,8 +217,11 @@ rba_status rba_export_block(rba_ctx *ctx, int64_t landmark, double *host_buf, in
 /* Landmark-block bytes: logical = sum (2k+3)(9k+4)*4 + 48 per landmark (6 Givens pairs);
  * physical = bytes allocated for the arena (16-byte alignment padding included). */
 rba_status rba_arena_bytes(rba_ctx *ctx, int64_t *logical, int64_t *physical);
-/* Number of this library's kernel launches so far. */
+/* Number of this library's kernel launches so far (kernel nodes executed inside CUDA graphs
+ * included, counted per executed conditional branch / loop iteration). */
 rba_status rba_kernel_launches(rba_ctx *ctx, int64_t *count);
+/* Device memory held by the context (bytes of every buffer it allocated). */
+rba_status rba_device_bytes(rba_ctx *ctx, int64_t *bytes);
 /* Per-kernel CUDA-event timing on the context stream: enable (1) / disable (0) and reset. */
 rba_status rba_profile(rba_ctx *ctx, int enable);
 /* kernel: 0 linearize(K1), 1 marginalize(K2), 2 damp(K3), 3 precond+rhs(K4), 4 matvec(K5),

@@ -83,6 +83,7 @@ def lib():
             "orc_get_block": (None, [P, I64, P]),
             "orc_get_givens": (None, [P, I64, P]),
             "orc_get_rhs": (None, [P, P]),
+            "orc_get_precond_factor": (None, [P, P]),
             "orc_get_dp": (None, [P, P]),
             "orc_set_dp": (None, [P, P]),
             "orc_get_rho_cg": (None, [P, P]),
@@ -271,6 +272,12 @@ class Oracle:
         b = np.zeros(9 * self.n_p)
         lib().orc_get_rhs(self.h, _p(b))
         return b
+
+    def precond_blocks(self):
+        """The block-Jacobi blocks P_i (n_p x 9 x 9) as L_i L_i^T from the stored Cholesky factors."""
+        L = np.zeros((self.n_p, 9, 9))
+        lib().orc_get_precond_factor(self.h, _p(L))
+        return L @ L.transpose(0, 2, 1)
 
     def dp(self):
         d = np.zeros(9 * self.n_p)

@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librba.so")
-SOURCES = ["rba_kernels.cu", "rba_sc.cu", "rba_factored.cu", "rba_sqrtba64.cu", "rba_api.cu", "rba_bal.cpp"]
+SOURCES = ["rba_kernels.cu", "rba_sc.cu", "rba_factored.cu", "rba_sqrtba64.cu", "rba_lm.cu", "rba_api.cu", "rba_bal.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -14,6 +14,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "rba_internal.cuh"
 
 using namespace rba;
@@ -43,6 +45,9 @@ static rba_status fail(rba_status s, const std::string &msg) {
     } while (0)
 
 namespace rba {
+rba_status set_error(rba_status s, const std::string &msg) { return fail(s, msg); }
+bool use_pcg_graph(rba_ctx *c);
+rba_status run_pcg_loop(rba_ctx *c);
 double plan_marg_bytes(rba_ctx *c) { return c->marg_bytes; }
 double plan_matvec_bytes(rba_ctx *c) { return c->matvec_bytes; }
 
@@ -87,6 +92,7 @@ static rba_status dalloc(rba_ctx *c, void **p, size_t bytes) {
         }
     }
     c->allocations.push_back(*p);
+    c->device_bytes += (int64_t)bytes;
     return RBA_OK;
 }
 template <typename T>
@@ -136,6 +142,7 @@ extern "C" void rba_default_options(rba_options *o) {
     o->diag_min = 1e-6;
     o->diag_max = 1e32;
     o->huber_delta = 0.0;
+    o->deterministic = 0;
 }
 
 extern "C" const char *rba_last_error(void) { return g_err.c_str(); }
@@ -164,6 +171,9 @@ static void free_ctx(rba_ctx *c) {
     }
     if (c->h_scal) cudaFreeHost(c->h_scal);
     if (c->h_pcg) cudaFreeHost(c->h_pcg);
+    if (c->h_reps) cudaFreeHost(c->h_reps);
+    if (c->lmg.exec) cudaGraphExecDestroy(c->lmg.exec);
+    if (c->lmg.graph) cudaGraphDestroy(c->lmg.graph);
     if (c->have_comm) ncclCommDestroy(c->comm);
     if (c->pcg_exec) cudaGraphExecDestroy(c->pcg_exec);
     if (c->pcg_graph) cudaGraphDestroy(c->pcg_graph);
@@ -199,7 +209,8 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
         opt.pcg_max_iters < 0 || !(opt.diag_min > 0) || !(opt.diag_max >= opt.diag_min) ||
         !(opt.huber_delta >= 0) || !std::isfinite(opt.huber_delta) || opt.solver < 0 || opt.solver > 2 ||
         opt.storage < 0 || opt.storage > 1 || (opt.storage == 1 && opt.solver != 0) || opt.precision < 0 ||
-        opt.precision > 1 || (opt.precision == 1 && (opt.solver != 0 || opt.storage != 0)))
+        opt.precision > 1 || (opt.precision == 1 && (opt.solver != 0 || opt.storage != 0)) || opt.deterministic < 0 ||
+        opt.deterministic > 1 || (opt.deterministic == 1 && (opt.solver != 0 || opt.storage != 0 || opt.precision != 0)))
         return fail(RBA_ERR_INVALID_ARG, "rba_create: bad options");
     if (n_obs >= (int64_t)1 << 31 || n_points >= (int64_t)1 << 31 || n_cams >= (int64_t)1 << 28)
         return fail(RBA_ERR_INVALID_ARG, "rba_create: problem too large for int32 indices");
@@ -254,7 +265,6 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     c->n_p = n_cams;
     c->n_l_global = n_points;
     c->n_obs_global = n_obs;
-    c->lm_lambda = opt.lambda0;
     auto bail = [&](rba_status s) {
         free_ctx(c);
         return s;
@@ -700,6 +710,7 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
         CKC(query_nsmid(c, reinterpret_cast<int *>(d.pcg), &nsm));
         d.nslice = std::max(nsm, 1);
         CKC(cudaMemsetAsync(d.pcg, 0, sizeof(PcgState), c->stream));
+        CKC(launch_set_pcg_limits(c, opt.pcg_rel_tol, opt.pcg_max_iters));
     }
     CKSC(dalloc_n(c, &d.pcg_part, 2 * ((9 * n_cams + 31) / 32) + 64));
     CKSC(dalloc_n(c, &d.psl, (int64_t)d.nslice * PACC_STRIDE * n_cams));
@@ -722,6 +733,8 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     CKSC(dalloc_n(c, &d.w, 9 * n_cams));
     CKSC(dalloc_n(c, &d.dl, 3 * nl));
     CKSC(dalloc_n(c, &d.scal, SC_N));
+    CKSC(dalloc_n(c, &d.lm, 1));
+    CKSC(dalloc_n(c, &d.reps, rba_ctx::REP_CAP));
     CKSC(dalloc_n(c, &d.packs, std::max<size_t>(1, packs.size())));
     CKSC(dalloc_n(c, &d.marg_items, std::max<size_t>(1, marg_items.size())));
     CKSC(dalloc_n(c, &d.tiles, std::max<size_t>(1, tiles.size())));
@@ -738,6 +751,7 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     CKSC(dalloc_n(c, &d.ybuf, std::max<int64_t>(4, ybuf_n)));
     CKC(cudaMallocHost(&c->h_scal, sizeof(double) * SC_N));
     CKC(cudaMallocHost(&c->h_pcg, sizeof(PcgState)));
+    CKC(cudaMallocHost(&c->h_reps, sizeof(rba_lm_report) * rba_ctx::REP_CAP));
     // ---- upload (host staging in the device layout)
     {
         std::vector<double> hc(cameras, cameras + 9 * n_cams), hp(3 * std::max<int64_t>(nl, 1));
@@ -796,6 +810,10 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
             CKC(cudaMemcpyAsync(d.cta_lo, cta_lo.data(), sizeof(int64_t) * cta_lo.size(), cudaMemcpyHostToDevice,
                                 c->stream));
         CKC(cudaMemsetAsync(d.scal, 0, sizeof(double) * SC_N, c->stream));
+        CKC(cudaMemsetAsync(d.lm, 0, sizeof(LmDev), c->stream));
+        CKC(launch_lm_init(c, opt.lambda0, 2.0, 1));
+        CKC(launch_lm_need_lin(c));
+        CKC(launch_set_lambda(c, opt.lambda0));
         // front-of-camera validation at the initial state, in a kernel
         int *dbad = reinterpret_cast<int *>(d.pcg);  // scratch
         CKC(cudaMemsetAsync(dbad, 0, sizeof(int), c->stream));
@@ -819,6 +837,7 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
         c->have_comm = true;
     }
     c->emulate_comm = getenv("RBA_EMULATE_COMM") != nullptr;  // test hook (tests/test_gpu_parity.py)
+    c->no_graph = getenv("RBA_NO_GRAPH") != nullptr;
     *out = c;
     return RBA_OK;
 #undef CKC
@@ -826,11 +845,13 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
 }
 
 // ------------------------------------------------------------------------------------ helpers
-static rba_status allreduce(rba_ctx *c, void *buf, size_t count, ncclDataType_t t) {
+namespace rba {
+rba_status allreduce(rba_ctx *c, void *buf, size_t count, ncclDataType_t t) {
     if (!c->have_comm || count == 0) return RBA_OK;
     CKN(ncclAllReduce(buf, buf, count, t, ncclSum, c->comm, c->stream));
     return RBA_OK;
 }
+}  // namespace rba
 
 static rba_status read_scal(rba_ctx *c) {
     CK(cudaMemcpyAsync(c->h_scal, c->d.scal, sizeof(double) * SC_N, cudaMemcpyDeviceToHost, c->stream));
@@ -856,6 +877,7 @@ extern "C" rba_status rba_linearize(rba_ctx *c) {
     c->marginalized = false;
     c->solved = false;
     c->backsubbed = false;
+    c->lm_dirty = true;
     return RBA_OK;
 }
 
@@ -864,22 +886,26 @@ extern "C" rba_status rba_marginalize_qr(rba_ctx *c, double lambda) {
     if (!(lambda >= 0) || !std::isfinite(lambda)) return fail(RBA_ERR_INVALID_ARG, "lambda must be finite and >= 0");
     if (!c->linearized) return fail(RBA_ERR_STATE, "rba_marginalize_qr before rba_linearize");
     CK(cudaSetDevice(c->device));
+    nvtxRangePushA("rba_marginalize_qr");
+    CK(launch_set_lambda(c, lambda));  // every kernel reads lambda (FP64) from the device
     if (c->d.s64) {  // sqrt-BA-64: marginalize once per linearization, then re-damp in place
-        if (!c->marginalized) CK(launch_marg64(c, lambda));
-        else if (lambda != c->lambda_blocks) CK(launch_redamp64(c, lambda));
+        if (!c->marginalized) CK(launch_marg64(c));
+        else if (lambda != c->lambda_blocks) CK(launch_redamp64(c));
         c->marginalized = true;
     } else if (c->d.sc) {  // explicit SC: H_ll depends on lambda, so every new lambda re-forms H~
-        if (!c->marginalized || (float)lambda != (float)c->lambda_blocks) CK(launch_sc_build(c, (float)lambda));
+        if (!c->marginalized || lambda != c->lambda_blocks) CK(launch_sc_build(c));
         c->marginalized = true;
     } else if (!c->marginalized) {
-        CK(launch_marginalize(c, (float)lambda));
+        CK(launch_marginalize(c));
         c->marginalized = true;
-    } else if ((float)lambda != (float)c->lambda_blocks) {
-        CK(launch_redamp(c, (float)lambda));
+    } else if (lambda != c->lambda_blocks) {
+        CK(launch_redamp(c));
     }
+    nvtxRangePop();
     c->lambda_blocks = lambda;
     c->solved = false;
     c->backsubbed = false;
+    c->lm_dirty = true;
     return RBA_OK;
 }
 
@@ -887,55 +913,24 @@ extern "C" rba_status rba_pcg_solve(rba_ctx *c, rba_pcg_stats *stats) {
     if (!c) return fail(RBA_ERR_INVALID_ARG, "null ctx");
     if (!c->marginalized) return fail(RBA_ERR_STATE, "rba_pcg_solve before rba_marginalize_qr");
     CK(cudaSetDevice(c->device));
+    nvtxRangePushA("rba_pcg_solve");
     DevProblem &d = c->d;
-    const float lam = (float)c->lambda_blocks;
-    CK(cudaMemsetAsync(d.scal + SC_BAD, 0, sizeof(double), c->stream));
+    CK(launch_set_lambda(c, c->lambda_blocks));
+    CK(cudaMemsetAsync(d.scal + SC_NSPD, 0, sizeof(double), c->stream));
     CK(c->d.sc ? launch_sc_precond(c) : launch_precond_rhs(c));  // (sqrt-BA-64 dispatches inside)
     CKS(allreduce(c, d.pd, 54 * d.n_p, ncclDouble));
-    CK(launch_precond_finalize(c, lam));
-    CK(launch_pcg_init(c, (float)c->opt.pcg_rel_tol, c->opt.pcg_max_iters));
-    // The device-side loop (CUDA graph with a `while` node) saves the host round trips, but with
-    // huge tracks (k > 512, config 5) its branches run the fused two-read kernel measurably slower
-    // than the eager issue order (31.3 vs 27.3 ms per product), so those problems loop on the host.
-    const bool no_graph = getenv("RBA_NO_GRAPH") != nullptr || c->n_huge_fused > 0 || c->n_huge_out > 0;
-    if (!c->host_reduce_path() && !no_graph && !c->pcg_exec && !c->pcg_graph_failed) {
-        if (build_pcg_graph(c) != cudaSuccess) {
-            cudaGetLastError();
-            c->pcg_graph_failed = true;
-        }
-    }
-    if (!c->host_reduce_path() && c->pcg_exec && !no_graph) {
-        // device-side loop: no host round trip per iteration, no post-convergence launches
-        c->h_scal[SC_LAM] = lam;
-        CK(cudaMemcpyAsync(d.scal + SC_LAM, c->h_scal + SC_LAM, sizeof(double), cudaMemcpyHostToDevice, c->stream));
-        Prof P(c, KID_MATVEC, 0.0);
-        CK(cudaGraphLaunch(c->pcg_exec, c->stream));
-        P.end();
-        CK(cudaMemcpyAsync(c->h_pcg, d.pcg, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
-        // every body iteration launched its kernel nodes (the last one's product kernels exit early)
-        c->launches += c->graph_body_kernels * std::max(1, c->h_pcg->it);
-    }
-    int batch = 2;
-    for (; !(!c->host_reduce_path() && c->pcg_exec && !no_graph);) {
-        CK(cudaMemcpyAsync(c->h_pcg, d.pcg, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
-        if (c->h_pcg->done || c->h_pcg->it >= c->opt.pcg_max_iters) break;
-        const int todo = std::min(batch, c->opt.pcg_max_iters - c->h_pcg->it);
-        for (int b = 0; b < todo; b++) {
-            CK(launch_matvec_pcg(c));
-            CKS(allreduce(c, d.wd, 9 * d.n_p, ncclDouble));
-            CK(launch_pcg_step(c, lam, (float)c->opt.pcg_rel_tol, c->opt.pcg_max_iters));
-        }
-        batch = std::min(batch * 2, 64);
-    }
+    CK(launch_precond_finalize(c));
+    CK(launch_pcg_init(c));
+    CKS(run_pcg_loop(c));  // the device-side loop (CUDA graph `while` node) or host batches
     CKS(read_scal(c));
+    CK(cudaMemcpyAsync(c->h_pcg, d.pcg, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    nvtxRangePop();
     c->prof_real_matvecs += c->h_pcg->it;
     if (stats) {
         stats->iters = c->h_pcg->it;
         stats->reason = c->h_pcg->reason;
         stats->rel_residual = c->h_pcg->r0 > 0 ? c->h_pcg->rn / c->h_pcg->r0 : 0.0;
-        if (c->h_scal[SC_BAD] > 0) stats->reason = 2;  // preconditioner block not SPD
     }
     c->solved = true;
     c->backsubbed = false;
@@ -947,7 +942,7 @@ extern "C" rba_status rba_backsubstitute(rba_ctx *c) {
     if (!c->solved) return fail(RBA_ERR_STATE, "rba_backsubstitute before rba_pcg_solve");
     CK(cudaSetDevice(c->device));
     CK(cudaMemsetAsync(c->d.scal + SC_Q1R2, 0, sizeof(double) * 2, c->stream));
-    CK(launch_backsub(c, (float)c->lambda_blocks));
+    CK(launch_backsub(c));
     c->backsubbed = true;
     return RBA_OK;
 }
@@ -962,63 +957,6 @@ extern "C" rba_status rba_cost(rba_ctx *c, int at_trial, double *cost) {
     CKS(allreduce(c, c->d.scal + slot, 2, ncclDouble));
     CKS(read_scal(c));
     *cost = c->h_scal[slot + 1] > 0 ? INFINITY : c->h_scal[slot];
-    return RBA_OK;
-}
-
-extern "C" rba_status rba_lm_step(rba_ctx *c, rba_lm_report *rep) {
-    if (!c) return fail(RBA_ERR_INVALID_ARG, "null ctx");
-    rba_lm_report R;
-    std::memset(&R, 0, sizeof(R));
-    R.iter = c->iteration;
-    if (c->need_lin || !c->linearized) {
-        CKS(rba_linearize(c));
-        c->need_lin = false;
-    }
-    CKS(rba_marginalize_qr(c, c->lm_lambda));
-    R.cost = c->cost;
-    R.lambda = c->lm_lambda;
-    rba_pcg_stats st;
-    CKS(rba_pcg_solve(c, &st));
-    R.pcg_iters = st.iters;
-    R.pcg_reason = st.reason;
-    bool accept = false;
-    R.cost_trial = INFINITY;
-    if (st.reason != 2) {
-        CKS(rba_backsubstitute(c));
-        DevProblem &d = c->d;
-        CK(cudaMemsetAsync(d.scal + SC_ET, 0, sizeof(double) * 2, c->stream));
-        CK(launch_trial_cost(c));
-        CKS(allreduce(c, d.scal + SC_ET, 4, ncclDouble));
-        CKS(read_scal(c));
-        const double *s = c->h_scal;
-        const double Et = s[SC_BADT] > 0 ? INFINITY : s[SC_ET];
-        const double model = s[SC_Q1R2] + s[SC_DAMPL] + s[SC_MODELP];
-        const double rho = (c->cost - Et) / model;
-        R.cost_trial = Et;
-        R.model = model;
-        R.rho = rho;
-        accept = model > 0 && std::isfinite(Et) && rho > c->opt.min_rel_decrease;
-        if (accept) {
-            CK(cudaMemcpyAsync(d.cams, d.cams_trial, sizeof(double) * 9 * d.n_p, cudaMemcpyDeviceToDevice, c->stream));
-            CK(cudaMemcpyAsync(d.pts, d.pts_trial, sizeof(double) * 3 * d.n_l, cudaMemcpyDeviceToDevice, c->stream));
-            c->cost = Et;
-            const double t = 2.0 * rho - 1.0;
-            c->lm_lambda *= std::max(1.0 / 3.0, 1.0 - t * t * t);
-            c->lm_nu = 2.0;
-            c->need_lin = true;
-            c->linearized = false;
-        }
-    }
-    if (!accept) {
-        c->lm_lambda *= c->lm_nu;
-        c->lm_nu *= 2.0;
-    }
-    c->lm_lambda = std::min(std::max(c->lm_lambda, 1e-16), 1e16);
-    R.accepted = accept;
-    R.cost_after = c->cost;
-    R.lambda_next = c->lm_lambda;
-    c->iteration++;
-    if (rep) *rep = R;
     return RBA_OK;
 }
 
@@ -1048,15 +986,7 @@ extern "C" rba_status rba_set_state(rba_ctx *c, const double *cameras, const dou
     CK(launch_pts_permute(c, 1));
     CK(cudaStreamSynchronize(c->stream));
     c->linearized = c->marginalized = c->solved = c->backsubbed = false;
-    c->need_lin = true;
-    return RBA_OK;
-}
-
-extern "C" rba_status rba_reset_lm(rba_ctx *c) {
-    if (!c) return fail(RBA_ERR_INVALID_ARG, "null ctx");
-    c->lm_lambda = c->opt.lambda0;
-    c->lm_nu = 2.0;
-    c->iteration = 0;
+    c->lm_dirty = true;
     return RBA_OK;
 }
 
@@ -1067,7 +997,8 @@ extern "C" rba_status rba_matvec(rba_ctx *c, const float *v, float *outv) {
     CK(cudaSetDevice(c->device));
     CK(launch_matvec(c, v, outv));
     CKS(allreduce(c, c->d.wd, 9 * c->d.n_p, ncclDouble));
-    CK(launch_add_damping(c, v, outv, (float)c->lambda_blocks));
+    CK(launch_set_lambda(c, c->lambda_blocks));
+    CK(launch_add_damping(c, v, outv));
     c->prof_real_matvecs++;
     return RBA_OK;
 }

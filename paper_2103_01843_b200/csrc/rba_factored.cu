@@ -584,8 +584,9 @@ __global__ void __launch_bounds__(256) k_fac_precond(DevProblem d, int64_t lo, i
 
 // ---- K7F: dl = -R^1^-1 (Q^1^T r^ + (Q^^T [J_p dp; 0])[0:3]) and the C10 terms
 template <int G>
-__global__ void __launch_bounds__(256) k_fac_backsub(DevProblem d, int64_t lo, int64_t hi, float lam) {
+__global__ void __launch_bounds__(256) k_fac_backsub(DevProblem d, int64_t lo, int64_t hi) {
     __shared__ double red[32];
+    if (d.pcg->reason == 2) return;  // indefinite attempt: no step
     const int lane = threadIdx.x & 31, gl = lane % G;
     const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / G;  // landmarks per grid sweep
     double q1 = 0.0, dd2 = 0.0;
@@ -651,12 +652,12 @@ __global__ void __launch_bounds__(256) k_fac_backsub(DevProblem d, int64_t lo, i
     dd2 = block_sum_d(dd2, red);
     if (threadIdx.x == 0) {
         atomicAdd(d.scal + SC_Q1R2, q1);
-        atomicAdd(d.scal + SC_DAMPL, (double)lam * dd2);
+        atomicAdd(d.scal + SC_DAMPL, d.scal[SC_LAM] * dd2);
     }
 }
 
 // ---- K3F: re-damping is O(1) per landmark: new Givens from the undamped R and Q1^T r
-__global__ void k_fac_redamp(DevProblem d, float lam) {
+__global__ void k_fac_redamp(DevProblem d) {
     const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= d.n_l) return;
     const int k = d.lm_k[j];
@@ -667,7 +668,7 @@ __global__ void k_fac_redamp(DevProblem d, float lam) {
     for (int i = 0; i < 9; i++) R[i] = base[i];
     rr3[0] = fac[24], rr3[1] = fac[25], rr3[2] = fac[28 + 24];
     (void)k;
-    const float sq = sqrtf(lam);
+    const float sq = sqrtf((float)d.scal[SC_LAM]);
     const float sD[3] = {sq * d.lm_D[3 * j], sq * d.lm_D[3 * j + 1], sq * d.lm_D[3 * j + 2]};
     float L6[18], Gm[18], rr6[6], g[12];
     damp_rotations(R, rr3, sD, L6, Gm, rr6, g);
@@ -683,7 +684,7 @@ __global__ void k_fac_redamp(DevProblem d, float lam) {
 static inline unsigned nbk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
 
 template <int G>
-static void fac_cls(rba_ctx *c, int cls, int what, const float *v, const PcgState *st, float lam, cudaStream_t s) {
+static void fac_cls(rba_ctx *c, int cls, int what, const float *v, const PcgState *st, cudaStream_t s) {
     const int64_t lo = c->fac_lo[cls], hi = c->fac_hi[cls];
     if (hi <= lo) return;
     const unsigned g = (unsigned)std::min<int64_t>(nbk((hi - lo) * G, 256), (int64_t)c->num_sms * 8);
@@ -704,35 +705,35 @@ static void fac_cls(rba_ctx *c, int cls, int what, const float *v, const PcgStat
         if (G == 32) cudaFuncSetAttribute(k_fac_precond<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         k_fac_precond<G><<<g, 256, sm, s>>>(c->d, lo, hi);
     } else {
-        k_fac_backsub<G><<<g, 256, 0, s>>>(c->d, lo, hi, lam);
+        k_fac_backsub<G><<<g, 256, 0, s>>>(c->d, lo, hi);
     }
     c->launches++;
 }
 
-static void fac_all(rba_ctx *c, int what, const float *v, const PcgState *st, float lam) {
+static void fac_all(rba_ctx *c, int what, const float *v, const PcgState *st) {
     // the classes are independent: fork them over the auxiliary streams and join back
     cudaEventRecord(c->ev_fork, c->stream);
     for (int i = 0; i < rba_ctx::NAUX; i++) cudaStreamWaitEvent(c->aux[i], c->ev_fork, 0);
-    fac_cls<32>(c, 4, what, v, st, lam, c->stream);
-    fac_cls<16>(c, 3, what, v, st, lam, c->aux[0]);
-    fac_cls<8>(c, 2, what, v, st, lam, c->aux[1]);
-    fac_cls<4>(c, 1, what, v, st, lam, c->aux[2]);
-    fac_cls<2>(c, 0, what, v, st, lam, c->stream);
+    fac_cls<32>(c, 4, what, v, st, c->stream);
+    fac_cls<16>(c, 3, what, v, st, c->aux[0]);
+    fac_cls<8>(c, 2, what, v, st, c->aux[1]);
+    fac_cls<4>(c, 1, what, v, st, c->aux[2]);
+    fac_cls<2>(c, 0, what, v, st, c->stream);
     for (int i = 0; i < rba_ctx::NAUX; i++) {
         cudaEventRecord(c->ev_join[i], c->aux[i]);
         cudaStreamWaitEvent(c->stream, c->ev_join[i], 0);
     }
 }
 
-void launch_fac_matvec(rba_ctx *c, const float *v, const PcgState *st) { fac_all(c, 0, v, st, 0.f); }
-void launch_fac_precond(rba_ctx *c) { fac_all(c, 1, nullptr, nullptr, 0.f); }
-cudaError_t launch_fac_backsub(rba_ctx *c, float lam) {
-    fac_all(c, 2, nullptr, nullptr, lam);
+void launch_fac_matvec(rba_ctx *c, const float *v, const PcgState *st) { fac_all(c, 0, v, st); }
+void launch_fac_precond(rba_ctx *c) { fac_all(c, 1, nullptr, nullptr); }
+cudaError_t launch_fac_backsub(rba_ctx *c) {
+    fac_all(c, 2, nullptr, nullptr);
     return cudaGetLastError();
 }
-cudaError_t launch_fac_redamp(rba_ctx *c, float lam) {
+cudaError_t launch_fac_redamp(rba_ctx *c) {
     if (c->d.n_l) {
-        k_fac_redamp<<<nbk(c->d.n_l, 256), 256, 0, c->stream>>>(c->d, lam);
+        k_fac_redamp<<<nbk(c->d.n_l, 256), 256, 0, c->stream>>>(c->d);
         c->launches++;
     }
     return cudaGetLastError();

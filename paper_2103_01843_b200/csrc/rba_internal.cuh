@@ -88,11 +88,35 @@ struct PcgState {
     int it, done, reason, active;
     double alpha, beta;       // step lengths of the current iteration (multi-CTA update kernels)
     unsigned int ctr_a, ctr_b;  // last-CTA-done counters of k_pcg_a / k_pcg_b (reset by that CTA)
+    double tol;                 // stop when |rho| <= tol |rho_0| (reading C11); set by the host
+    int max_iters, pad_;        // (rba_set_pcg_limits), read by k_pcg_init / k_pcg_b
 };
 
 // double scalars on the device (single buffer so one all-reduce covers them)
-// [E, BAD] reduced at linearize; [ET, BADT, Q1R2, DAMPL] reduced after a trial; MODELP replicated
-enum { SC_E = 0, SC_BAD, SC_ET, SC_BADT, SC_Q1R2, SC_DAMPL, SC_MODELP, SC_LAM, SC_N = 8 };
+// [E, BAD] reduced at linearize; [ET, BADT, Q1R2, DAMPL] reduced after a trial; MODELP replicated;
+// LAM = the damping lambda of the current attempt (every kernel that needs lambda reads it here, in
+// FP64, so the device-side LM control can change it without the host); NSPD = preconditioner
+// blocks found not SPD (the attempt is then treated as indefinite)
+enum { SC_E = 0, SC_BAD, SC_ET, SC_BADT, SC_Q1R2, SC_DAMPL, SC_MODELP, SC_LAM, SC_NSPD, SC_N = 9 };
+
+// Device-side Levenberg-Marquardt control (readings C9, C10, C13): the schedule lives in
+// device memory and is advanced by k_lm_control, so an LM iteration (or a whole rba_lm_solve) runs
+// without a host round trip.  Timestamps are %globaltimer (ns).
+enum { TS_BEGIN = 0, TS_LIN, TS_MARG, TS_PRE, TS_PCG, TS_TRIAL, TS_END, TS_N };
+struct LmDev {
+    double lambda, nu;        // damping of the next attempt and the rejection multiplier
+    double cost;              // E at the current state
+    double min_rel_decrease;  // accept iff gain ratio > this (C9)
+    double ftol;              // rba_lm_solve: stop once an accepted step decreases E by < ftol E
+    int need_lin;             // the next attempt relinearizes (state changed / accepted)
+    int stop;                 // 0 running, 1 converged (ftol), 2 error (point behind a camera / non-finite E)
+    int lin_now;              // this attempt relinearized
+    int accepted_now;         // this attempt was accepted (k_lm_commit copies the trial state)
+    int64_t iter;             // LM iteration counter (every attempt counts, C13)
+    int64_t target, n_done;   // rba_lm_solve: attempts requested / done in this call
+    int64_t rep_cap;          // capacity of the device report array
+    unsigned long long ts[TS_N];
+};
 
 enum { KID_LIN = 0, KID_MARG, KID_DAMP, KID_PRE, KID_MATVEC, KID_PCG, KID_BACKSUB, KID_COST, KID_N };
 
@@ -150,6 +174,8 @@ struct DevProblem {
     float *dl;
     double *scal;
     PcgState *pcg;
+    LmDev *lm;                // device-side LM schedule (rba_lm.cu)
+    rba_lm_report *reps;      // device reports of the iterations of one rba_lm_step / rba_lm_solve call
     double *pcg_part;  // per-CTA partial dot products of the PCG update kernels (fixed-order sums)
     Pack *packs;            // small-k packs, classes G = 2, 4, 8, 16 back to back
     uint16_t *units;        // small-k work units per stage
@@ -231,14 +257,24 @@ struct rba_ctx {
     // pinned host scratch
     double *h_scal = nullptr;
     rba::PcgState *h_pcg = nullptr;
-    // solver state
+    // solver state of the step-by-step API (call ordering; the LM schedule itself lives on the
+    // device, rba::LmDev)
     bool linearized = false, marginalized = false, solved = false, backsubbed = false;
     double lambda_blocks = 0.0;
     double cost = 0.0;
-    double lm_lambda = 1e-4, lm_nu = 2.0;
-    bool need_lin = true;
-    int64_t iteration = 0;
+    bool lm_dirty = true;  // a step-by-step call changed the blocks / state: the next LM step relinearizes
     int64_t launches = 0;
+    int64_t device_bytes = 0;
+    // device-side LM loop (rba_lm.cu): one CUDA graph = while (LM) { if (relinearize) {K1, K2} else
+    // {K3}; K4; while (PCG) {K5, K6}; K7, K8, control }, and the kernel-node counts of its parts
+    struct LmGraph {
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        bool failed = false, built = false;
+        int64_t n_head = 0, n_lin = 0, n_redamp = 0, n_mid = 0, n_pcg = 0, n_tail = 0;
+    } lmg;
+    rba_lm_report *h_reps = nullptr;  // pinned host copy of the device reports
+    static constexpr int REP_CAP = 1024;
     // profiling
     // PCG as a CUDA graph with a device-side while loop (single GPU; NCCL path uses host batches)
     cudaGraph_t pcg_graph = nullptr;
@@ -249,6 +285,7 @@ struct rba_ctx {
     bool nofork = false;             // launch the per-class kernels on the context stream only
     bool emulate_comm = false;       // RBA_EMULATE_COMM: the multi-GPU PCG path (host loop, product
                                      // reduced before the update) on one GPU, all-reduces skipped
+    bool no_graph = false;           // RBA_NO_GRAPH (read at rba_create): eager LM / host-polled PCG
     bool host_reduce_path() const { return have_comm || emulate_comm; }
     bool profiling = false;
     int64_t prof_real_matvecs = 0;  // matvecs that did work (PCG iterations + hook calls) since rba_profile
@@ -257,6 +294,15 @@ struct rba_ctx {
 };
 
 namespace rba {
+// shared host helpers (rba_api.cu)
+rba_status set_error(rba_status s, const std::string &msg);
+rba_status allreduce(rba_ctx *c, void *buf, size_t count, ncclDataType_t t);
+// device-side LM (rba_lm.cu)
+cudaError_t launch_set_lambda(rba_ctx *c, double lambda);
+cudaError_t launch_set_pcg_limits(rba_ctx *c, double tol, int max_iters);
+cudaError_t launch_lm_init(rba_ctx *c, double lambda, double nu, int reset_iter);
+cudaError_t launch_lm_need_lin(rba_ctx *c);
+rba_status build_pcg_graph(rba_ctx *c);
 // kernel launchers (rba_kernels.cu); each returns cudaGetLastError()
 cudaError_t launch_check_depth(rba_ctx *c, int *d_bad);
 cudaError_t launch_cam_prep(rba_ctx *c, int trial);
@@ -266,37 +312,36 @@ cudaError_t launch_pts_permute(rba_ctx *c, int to_internal);
 cudaError_t query_nsmid(rba_ctx *c, int *d_scratch, int *out);
 cudaError_t launch_linearize(rba_ctx *c);
 cudaError_t launch_cam_scale(rba_ctx *c);
-cudaError_t launch_marginalize(rba_ctx *c, float lambda);
-cudaError_t launch_redamp(rba_ctx *c, float lambda_new);
+cudaError_t launch_marginalize(rba_ctx *c);
+cudaError_t launch_redamp(rba_ctx *c);
 cudaError_t launch_precond_rhs(rba_ctx *c);
-cudaError_t launch_precond_finalize(rba_ctx *c, float lambda);
+cudaError_t launch_precond_finalize(rba_ctx *c);
 cudaError_t launch_matvec(rba_ctx *c, const float *v, float *out);
 cudaError_t launch_matvec_pcg(rba_ctx *c);
-cudaError_t launch_pcg_init(rba_ctx *c, float tol, int max_iters);
-cudaError_t launch_pcg_step(rba_ctx *c, float lambda, float tol, int max_iters);
-cudaError_t build_pcg_graph(rba_ctx *c);
-cudaError_t launch_backsub(rba_ctx *c, float lambda);
+cudaError_t launch_pcg_init(rba_ctx *c, cudaGraphConditionalHandle h = 0, int use_h = 0);
+cudaError_t launch_pcg_step(rba_ctx *c, cudaGraphConditionalHandle h = 0, int use_h = 0);
+cudaError_t launch_backsub(rba_ctx *c);
 cudaError_t launch_trial_cost(rba_ctx *c);
 cudaError_t launch_cost(rba_ctx *c, int at_trial, int slot);
 cudaError_t launch_commit(rba_ctx *c);
-cudaError_t launch_add_damping(rba_ctx *c, const float *v, float *out, float lambda);
+cudaError_t launch_add_damping(rba_ctx *c, const float *v, float *out);
 // explicit Schur complement (rba_sc.cu)
-cudaError_t launch_sc_build(rba_ctx *c, float lambda);
+cudaError_t launch_sc_build(rba_ctx *c);
 cudaError_t launch_sc_precond(rba_ctx *c);
 void launch_sc_spmv(rba_ctx *c, const PcgState *st, const float *v32);
 // factored storage (rba_factored.cu)
 void launch_fac_matvec(rba_ctx *c, const float *v, const PcgState *st);
 void launch_fac_precond(rba_ctx *c);
-cudaError_t launch_fac_backsub(rba_ctx *c, float lambda);
-cudaError_t launch_fac_redamp(rba_ctx *c, float lambda);
+cudaError_t launch_fac_backsub(rba_ctx *c);
+cudaError_t launch_fac_redamp(rba_ctx *c);
 // sqrt-BA-64 (rba_sqrtba64.cu)
-cudaError_t launch_marg64(rba_ctx *c, double lambda);
-cudaError_t launch_redamp64(rba_ctx *c, double lambda);
+cudaError_t launch_marg64(rba_ctx *c);
+cudaError_t launch_redamp64(rba_ctx *c);
 void launch_rcs64(rba_ctx *c, const double *v, const PcgState *st);
 void launch_pre64(rba_ctx *c);
-cudaError_t launch_backsub64(rba_ctx *c, float lambda);
+cudaError_t launch_backsub64(rba_ctx *c);
 void launch_f2d64(rba_ctx *c, const float *a, double *b, int64_t n);
-cudaError_t launch_sc_backsub(rba_ctx *c, float lambda);
+cudaError_t launch_sc_backsub(rba_ctx *c);
 // profiling scope: CUDA events on the context stream around one launch (rba_api.cu)
 struct Prof {
     rba_ctx *c;

@@ -221,7 +221,7 @@ template <int G>
 #ifndef RBA_MARG_SMALL_MINB
 #define RBA_MARG_SMALL_MINB 4  // 128 registers: 4 CTAs per SM (measured 3.35 -> 3.22 ms K2 on cfg4)
 #endif
-__global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProblem d, int64_t pk_lo, int64_t pk_hi, float lam, float dmin,
+__global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProblem d, int64_t pk_lo, int64_t pk_hi, float dmin,
                                                     float dmax) {
     constexpr int NG = 32 / G;
     using TB = SmallTab<G>;
@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProb
     rr3[0] = __shfl_sync(0xffffffffu, rv[0], 0, G);
     rr3[1] = __shfl_sync(0xffffffffu, rv[1], 0, G);
     rr3[2] = __shfl_sync(0xffffffffu, rv[0], 1, G);
-    const float sq = sqrtf(lam);
+    const float sq = sqrtf((float)d.scal[SC_LAM]);  // lambda of this attempt (device-side LM control)
     const float sD[3] = {sq * Dl[0], sq * Dl[1], sq * Dl[2]};
     float L6[18], Gm[18], rr6[6], g[12];
     damp_rotations(R, rr3, sD, L6, Gm, rr6, g);
@@ -468,8 +468,8 @@ __device__ __forceinline__ void block_jp(const DevProblem &d, int64_t obs0, int 
 }
 
 template <int NT, bool MULTI>
-__global__ void __launch_bounds__(NT) k_marg_large(DevProblem d, const LargeItem *__restrict__ items, float lam,
-                                                   float dmin, float dmax) {
+__global__ void __launch_bounds__(NT) k_marg_large(DevProblem d, const LargeItem *__restrict__ items, float dmin,
+                                                   float dmax) {
     extern __shared__ float4 smem4[];
     __shared__ float red[32 * 4];
     __shared__ float piv[4];
@@ -587,7 +587,7 @@ __global__ void __launch_bounds__(NT) k_marg_large(DevProblem d, const LargeItem
         const float4 v = VR[i];
         V3[i * 3] = v.x, V3[i * 3 + 1] = v.y, V3[i * 3 + 2] = v.z;
     }
-    const float sq = sqrtf(lam);
+    const float sq = sqrtf((float)d.scal[SC_LAM]);
     const float sD[3] = {sq * Dl[0], sq * Dl[1], sq * Dl[2]};
     float L6[18], Gm[18], rr6[6], g[12];
     damp_rotations(R, rr3, sD, L6, Gm, rr6, g);
@@ -675,7 +675,7 @@ __global__ void __launch_bounds__(NT) k_marg_large(DevProblem d, const LargeItem
 // ============================================================================ K3 re-damping
 // Warp per landmark.  Undo the stored rotations (transposed, reverse order, Fig. 3c), drop the
 // damping rows, and fold sqrt(lam) D_l in again with freshly computed rotations.
-__global__ void __launch_bounds__(256) k_redamp(DevProblem d, float lam) {
+__global__ void __launch_bounds__(256) k_redamp(DevProblem d) {
     const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (j >= d.n_l) return;
@@ -714,7 +714,7 @@ __global__ void __launch_bounds__(256) k_redamp(DevProblem d, float lam) {
     }
     // exact upper-triangular R1 after undo
     R[3] = 0.f, R[6] = 0.f, R[7] = 0.f;
-    const float sq = sqrtf(lam);
+    const float sq = sqrtf((float)d.scal[SC_LAM]);
     const float sD[3] = {sq * d.lm_D[3 * j], sq * d.lm_D[3 * j + 1], sq * d.lm_D[3 * j + 2]};
     float L6[18], Gm[18], rr6[6], gn[12];
     damp_rotations(R, rr3, sD, L6, Gm, rr6, gn);
@@ -785,9 +785,10 @@ __device__ __forceinline__ void flush54(float *acc, const float *P, const float 
 }
 
 // per camera: P_i + lambda D_p^2 -> Cholesky (FP64) -> inverse M^-1 (FP32, 81); b~ copied out.
-__global__ void k_precond_finalize(DevProblem d, float lam, double *bad) {
+__global__ void k_precond_finalize(DevProblem d, double *bad) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= d.n_p) return;
+    const double lam = d.scal[SC_LAM];
     const double *acc = d.pd + 54 * i;
     double P[81];
     int idx = 0;
@@ -798,7 +799,7 @@ __global__ void k_precond_finalize(DevProblem d, float lam, double *bad) {
             idx++;
         }
     for (int a = 0; a < 9; a++) {
-        P[a * 9 + a] += (double)lam * d.Dp264[9 * i + a];
+        P[a * 9 + a] += lam * d.Dp264[9 * i + a];
         d.bt[9 * i + a] = acc[45 + a];  // FP64
     }
     double L[81];
@@ -1493,10 +1494,10 @@ __global__ void __launch_bounds__(256) k_reduce_slices(float *__restrict__ sl, i
 }
 
 // out = H~ v = wd + lambda D_p^2 v  (test hook, FP32 out)
-__global__ void k_add_damping(DevProblem d, const float *v, float *out, float lam) {
+__global__ void k_add_damping(DevProblem d, const float *v, float *out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= 9 * d.n_p) return;
-    out[i] = (float)(d.wd[i] + (double)lam * d.Dp264[i] * v[i]);
+    out[i] = (float)(d.wd[i] + d.scal[SC_LAM] * d.Dp264[i] * v[i]);
 }
 
 // ============================================================================ K6 PCG (single CTA)
@@ -1537,8 +1538,7 @@ __device__ __forceinline__ double sum_parts(const double *part, int n, int strid
 // A: w = wd + lambda D_p^2 p, with wd = the sum of the per-SM slices (fused: 32 outputs x 8 slice
 // phases per CTA, slices zeroed for the next product) or already in wd (all-reduced / other
 // storage); then alpha = rho^T z / p^T w, or done with "indefinite" if p^T w <= 0.
-__global__ void __launch_bounds__(256) k_pcg_a(DevProblem d, float lam_f, int fuse, cudaGraphConditionalHandle h,
-                                               int use_h) {
+__global__ void __launch_bounds__(256) k_pcg_a(DevProblem d, int fuse, cudaGraphConditionalHandle h, int use_h) {
     __shared__ double part[8][33];
     __shared__ double red[32];
     PcgState *st = d.pcg;
@@ -1546,7 +1546,7 @@ __global__ void __launch_bounds__(256) k_pcg_a(DevProblem d, float lam_f, int fu
         if (use_h && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(h, 0);
         return;
     }
-    const double lam = lam_f < 0.f ? d.scal[SC_LAM] : (double)lam_f;
+    const double lam = d.scal[SC_LAM];
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int64_t N = 9 * d.n_p, i = (int64_t)blockIdx.x * 32 + tx;
     double s = 0.0;
@@ -1604,8 +1604,7 @@ __global__ void __launch_bounds__(256) k_pcg_a(DevProblem d, float lam_f, int fu
 // B: thread <-> one entry (32 cameras x 9 per CTA): x += alpha p, rho -= alpha w, then z = M^-1 rho
 // with the camera's 9 updated rho entries exchanged through shared memory; |rho|, rho^T z.  The
 // last CTA decides convergence (C11) / max iterations and forms beta.
-__global__ void __launch_bounds__(288) k_pcg_b(DevProblem d, double tol, int max_iters, cudaGraphConditionalHandle h,
-                                               int use_h) {
+__global__ void __launch_bounds__(288) k_pcg_b(DevProblem d, cudaGraphConditionalHandle h, int use_h) {
     __shared__ double red[32];
     __shared__ double rs[288];
     PcgState *st = d.pcg;
@@ -1643,8 +1642,8 @@ __global__ void __launch_bounds__(288) k_pcg_b(DevProblem d, double tol, int max
         st->it = it;
         st->rn = sqrt(rr);
         int stop = 0;
-        if (sqrt(rr) <= tol * st->r0) stop = 1, st->reason = 0;
-        else if (it >= max_iters) stop = 1, st->reason = 1;
+        if (sqrt(rr) <= st->tol * st->r0) stop = 1, st->reason = 0;
+        else if (it >= st->max_iters) stop = 1, st->reason = 1;
         if (stop) st->done = 1;
         if (use_h) cudaGraphSetConditional(h, stop ? 0 : 1);
         st->beta = rz / st->rz;
@@ -1665,7 +1664,7 @@ __global__ void __launch_bounds__(256) k_pcg_c(DevProblem d) {
 }
 
 // PCG vectors (x, rho, z, p, w) are FP64 (9 n_p each, reading C24); the matvec reads p as FP32 (p32).
-__global__ void __launch_bounds__(1024) k_pcg_init(DevProblem d) {
+__global__ void __launch_bounds__(1024) k_pcg_init(DevProblem d, cudaGraphConditionalHandle h, int use_h) {
     __shared__ double red[32];
     const int64_t N = 9 * d.n_p;
     double rr = 0.0;
@@ -1692,18 +1691,25 @@ __global__ void __launch_bounds__(1024) k_pcg_init(DevProblem d) {
         d.pcg->rn = sqrt(rr);
         d.pcg->it = 0;
         d.pcg->reason = 0;
-        d.pcg->done = (rr == 0.0) ? 1 : 0;
+        // a block found not SPD by k_precond_finalize makes the attempt indefinite
+        const bool nspd = d.scal[SC_NSPD] > 0.0;
+        d.pcg->done = (rr == 0.0 || d.pcg->max_iters <= 0 || nspd) ? 1 : 0;
+        if (nspd) d.pcg->reason = 2;
+        d.pcg->ctr_a = 0;
+        d.pcg->ctr_b = 0;
+        if (use_h) cudaGraphSetConditional(h, d.pcg->done ? 0 : 1);
     }
 }
 
 // lam < 0: read lambda from d.scal[SC_LAM] (graph launches).  use_h: also drive the graph's
 // while-loop condition (0 once the solve is done).
-__global__ void __launch_bounds__(1024) k_pcg_step(DevProblem d, float lam_f, double tol, int max_iters,
-                                                   cudaGraphConditionalHandle h, int use_h) {
+__global__ void __launch_bounds__(1024) k_pcg_step(DevProblem d, cudaGraphConditionalHandle h, int use_h) {
     __shared__ double red[32];
     __shared__ int stop;
     PcgState *st = d.pcg;
-    const double lam = lam_f < 0.f ? d.scal[SC_LAM] : (double)lam_f;
+    const double lam = d.scal[SC_LAM];
+    const double tol = st->tol;
+    const int max_iters = st->max_iters;
     if (st->done) {
         if (use_h && threadIdx.x == 0) cudaGraphSetConditional(h, 0);
         return;
@@ -1763,8 +1769,10 @@ __global__ void __launch_bounds__(1024) k_pcg_step(DevProblem d, float lam_f, do
 // Warp per landmark (grid-stride), lanes over the flattened 9k pose columns of R1 (coalesced), the
 // three row sums reduced with shuffles; lane 0 solves the 3x3 upper-triangular system.  The
 // model-decrease sums go out once per CTA (not per landmark: same-address FP64 atomics serialize).
-__global__ void __launch_bounds__(256) k_backsub(DevProblem d, float lam) {
+__global__ void __launch_bounds__(256) k_backsub(DevProblem d) {
     __shared__ double red[32];
+    if (d.pcg->reason == 2) return;  // indefinite attempt: no step (the LM control rejects it)
+    const double lam = d.scal[SC_LAM];
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     double q1 = 0.0, dd = 0.0;
@@ -1816,20 +1824,22 @@ __global__ void __launch_bounds__(256) k_backsub(DevProblem d, float lam) {
     dd = block_sum_d(dd, red);
     if (threadIdx.x == 0) {
         atomicAdd(d.scal + SC_Q1R2, q1);
-        atomicAdd(d.scal + SC_DAMPL, (double)lam * dd);
+        atomicAdd(d.scal + SC_DAMPL, lam * dd);
     }
 }
 
 // trial cameras x_p + S_p dp and the (replicated) camera part of the model decrease (C10):
 // sum_i (-b~_i dp_i + rho_i dp_i + lam D_p,i^2 dp_i^2)
-__global__ void __launch_bounds__(1024) k_trial_cams(DevProblem d, float lam, int with_model) {
+__global__ void __launch_bounds__(1024) k_trial_cams(DevProblem d, int with_model) {
     __shared__ double red[32];
+    if (d.pcg->reason == 2) return;
+    const double lam = d.scal[SC_LAM];
     const int64_t N = 9 * d.n_p;
     double m = 0.0;
     for (int64_t i = threadIdx.x; i < N; i += blockDim.x) {
         const double dp = d.x[i];
         d.cams_trial[i] = d.cams[i] + d.sp64[i] * dp;
-        m += -d.bt[i] * dp + d.r[i] * dp + (double)lam * d.Dp264[i] * dp * dp;
+        m += -d.bt[i] * dp + d.r[i] * dp + lam * d.Dp264[i] * dp * dp;
     }
     m = block_sum_d(m, red);
     if (threadIdx.x == 0) d.scal[SC_MODELP] = with_model ? m : 0.0;
@@ -1839,6 +1849,7 @@ __global__ void __launch_bounds__(1024) k_trial_cams(DevProblem d, float lam, in
 __global__ void __launch_bounds__(256) k_cost(DevProblem d, const double *__restrict__ campre,
                                               const double *__restrict__ pts, int slot, int bad_slot) {
     __shared__ double red[32];
+    if (slot == SC_ET && d.pcg->reason == 2) return;  // indefinite attempt: no trial point
     double e = 0.0, bad = 0.0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d.n_obs;
          i += (int64_t)gridDim.x * blockDim.x) {  // grid-stride (see k_linearize)
@@ -1958,30 +1969,30 @@ struct ForkJoin {
 };
 
 template <int G>
-static cudaError_t marg_small_cls(rba_ctx *c, int cls, float lam, cudaStream_t st) {
+static cudaError_t marg_small_cls(rba_ctx *c, int cls, cudaStream_t st) {
     const int64_t lo = c->pack_lo[cls], hi = c->pack_hi[cls];
     if (hi <= lo) return cudaSuccess;
     const size_t sm = (size_t)4 * ((32 / G) * SmallTab<G>::FLOATS + SmallTab<G>::SIDE) * sizeof(float);
-    k_marg_small<G><<<nblk(hi - lo, 4), 128, sm, st>>>(c->d, lo, hi, lam, (float)c->opt.diag_min,
+    k_marg_small<G><<<nblk(hi - lo, 4), 128, sm, st>>>(c->d, lo, hi, (float)c->opt.diag_min,
                                                               (float)c->opt.diag_max);
     c->launches++;
     return cudaGetLastError();
 }
 
 template <int NT, bool MULTI = false>
-static cudaError_t marg_large_cls(rba_ctx *c, int cls, float lam, cudaStream_t st) {
+static cudaError_t marg_large_cls(rba_ctx *c, int cls, cudaStream_t st) {
     const int64_t lo = c->marg_lo[cls], hi = c->marg_hi[cls];
     if (hi <= lo) return cudaSuccess;
     const int64_t K = MULTI ? (cls == 5 ? c->huge_max_k : KLARGE) : NT;
     const size_t sm = (size_t)(4 * (2 * K + 3) + 8 * K) * sizeof(float);
     cudaFuncSetAttribute(k_marg_large<NT, MULTI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_marg_large<NT, MULTI><<<(unsigned)(hi - lo), NT, sm, st>>>(c->d, c->d.marg_items + lo, lam,
-                                                                  (float)c->opt.diag_min, (float)c->opt.diag_max);
+    k_marg_large<NT, MULTI><<<(unsigned)(hi - lo), NT, sm, st>>>(c->d, c->d.marg_items + lo, (float)c->opt.diag_min,
+                                                                  (float)c->opt.diag_max);
     c->launches++;
     return cudaGetLastError();
 }
 
-cudaError_t launch_marginalize(rba_ctx *c, float lam) {
+cudaError_t launch_marginalize(rba_ctx *c) {
     Prof P(c, KID_MARG, plan_marg_bytes(c));
     cudaError_t e;
     ForkJoin F(c);
@@ -1989,33 +2000,33 @@ cudaError_t launch_marginalize(rba_ctx *c, float lam) {
     static const bool small_first = getenv("RBA_MARG_ORDER") && atoi(getenv("RBA_MARG_ORDER"));  // tuning knob
     auto smalls = [&]() -> cudaError_t {
         cudaError_t x;
-        if ((x = marg_small_cls<16>(c, 3, lam, F.s()))) return x;
-        if ((x = marg_small_cls<8>(c, 2, lam, F.s()))) return x;
-        if ((x = marg_small_cls<4>(c, 1, lam, F.s()))) return x;
-        return marg_small_cls<2>(c, 0, lam, F.s());
+        if ((x = marg_small_cls<16>(c, 3, F.s()))) return x;
+        if ((x = marg_small_cls<8>(c, 2, F.s()))) return x;
+        if ((x = marg_small_cls<4>(c, 1, F.s()))) return x;
+        return marg_small_cls<2>(c, 0, F.s());
     };
     if (small_first && (e = smalls())) return e;
-    if ((e = marg_large_cls<512, true>(c, 5, lam, F.s()))) return e;
+    if ((e = marg_large_cls<512, true>(c, 5, F.s()))) return e;
     if (m512) {
-        if ((e = marg_large_cls<256, true>(c, 4, lam, F.s()))) return e;
-    } else if ((e = marg_large_cls<512>(c, 4, lam, F.s()))) {
+        if ((e = marg_large_cls<256, true>(c, 4, F.s()))) return e;
+    } else if ((e = marg_large_cls<512>(c, 4, F.s()))) {
         return e;
     }
-    if ((e = marg_large_cls<256>(c, 3, lam, F.s()))) return e;
-    if ((e = marg_large_cls<128>(c, 2, lam, F.s()))) return e;
-    if ((e = marg_large_cls<64>(c, 1, lam, F.s()))) return e;
-    if ((e = marg_large_cls<32>(c, 0, lam, F.s()))) return e;
+    if ((e = marg_large_cls<256>(c, 3, F.s()))) return e;
+    if ((e = marg_large_cls<128>(c, 2, F.s()))) return e;
+    if ((e = marg_large_cls<64>(c, 1, F.s()))) return e;
+    if ((e = marg_large_cls<32>(c, 0, F.s()))) return e;
     if (!small_first && (e = smalls())) return e;
     F.join();
     P.end();
     return cudaSuccess;
 }
 
-cudaError_t launch_redamp(rba_ctx *c, float lam) {
+cudaError_t launch_redamp(rba_ctx *c) {
     if (c->d.n_l == 0) return cudaSuccess;
-    if (c->d.fac) return launch_fac_redamp(c, lam);
+    if (c->d.fac) return launch_fac_redamp(c);
     Prof P(c, KID_DAMP, 0.0);
-    k_redamp<<<nblk(32 * c->d.n_l, 256), 256, 0, c->stream>>>(c->d, lam);
+    k_redamp<<<nblk(32 * c->d.n_l, 256), 256, 0, c->stream>>>(c->d);
     P.end();
     c->launches++;
     return cudaGetLastError();
@@ -2091,8 +2102,8 @@ cudaError_t launch_precond_rhs(rba_ctx *c) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_precond_finalize(rba_ctx *c, float lam) {
-    k_precond_finalize<<<nblk(c->d.n_p, 128), 128, 0, c->stream>>>(c->d, lam, c->d.scal + SC_BAD);
+cudaError_t launch_precond_finalize(rba_ctx *c) {
+    k_precond_finalize<<<nblk(c->d.n_p, 128), 128, 0, c->stream>>>(c->d, c->d.scal + SC_NSPD);
     c->launches++;
     return cudaGetLastError();
 }
@@ -2140,108 +2151,60 @@ cudaError_t launch_matvec_pcg(rba_ctx *c) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_add_damping(rba_ctx *c, const float *v, float *out, float lam) {
-    k_add_damping<<<nblk(9 * c->d.n_p, 256), 256, 0, c->stream>>>(c->d, v, out, lam);
+cudaError_t launch_add_damping(rba_ctx *c, const float *v, float *out) {
+    k_add_damping<<<nblk(9 * c->d.n_p, 256), 256, 0, c->stream>>>(c->d, v, out);
     c->launches++;
     return cudaGetLastError();
 }
 
-cudaError_t launch_pcg_init(rba_ctx *c, float, int) {
-    k_pcg_init<<<1, 1024, 0, c->stream>>>(c->d);
+cudaError_t launch_pcg_init(rba_ctx *c, cudaGraphConditionalHandle h, int use_h) {
+    k_pcg_init<<<1, 1024, 0, c->stream>>>(c->d, h, use_h);
     c->launches++;
     return cudaGetLastError();
 }
 
-static void pcg_update(rba_ctx *c, cudaStream_t s, float lam, double tol, int max_iters, bool fuse,
-                       cudaGraphConditionalHandle h, int use_h) {
+static void pcg_update(rba_ctx *c, cudaStream_t s, bool fuse, cudaGraphConditionalHandle h, int use_h) {
     const int64_t N = 9 * c->d.n_p;
-    k_pcg_a<<<(unsigned)((N + 31) / 32), 256, 0, s>>>(c->d, lam, fuse ? 1 : 0, h, use_h);
-    k_pcg_b<<<nblk(c->d.n_p, 32), 288, 0, s>>>(c->d, tol, max_iters, h, use_h);
+    k_pcg_a<<<(unsigned)((N + 31) / 32), 256, 0, s>>>(c->d, fuse ? 1 : 0, h, use_h);
+    k_pcg_b<<<nblk(c->d.n_p, 32), 288, 0, s>>>(c->d, h, use_h);
     k_pcg_c<<<nblk(N, 256), 256, 0, s>>>(c->d);
     c->launches += 3;
 }
 
-cudaError_t launch_pcg_step(rba_ctx *c, float lam, float tol, int max_iters) {
+// The PCG update after a product (launch_matvec_pcg + the all-reduce of wd when sharded); h / use_h:
+// the conditional handle of the device-side PCG `while` loop the update kernels drive.
+cudaError_t launch_pcg_step(rba_ctx *c, cudaGraphConditionalHandle h, int use_h) {
     Prof P(c, KID_PCG, 0.0);
     static const bool single = getenv("RBA_PCG_SINGLE_CTA") != nullptr;  // the single-CTA step (A/B)
     if (single) {
         if (c->pcg_fused) reduce_slices(c, c->d.wsl, 12, 9, c->d.wd, c->d.pcg);
-        k_pcg_step<<<1, 1024, 0, c->stream>>>(c->d, lam, (double)tol, max_iters, 0, 0);
+        k_pcg_step<<<1, 1024, 0, c->stream>>>(c->d, h, use_h);
         c->launches++;
     } else {
-        pcg_update(c, c->stream, lam, tol, max_iters, c->pcg_fused, 0, 0);
+        pcg_update(c, c->stream, c->pcg_fused, h, use_h);
     }
     c->pcg_fused = false;
     P.end();
     return cudaGetLastError();
 }
 
-// PCG loop as a graph: while (cond) { slices += A_j^T A_j p32 (all pipes); wd = sum of slices; PCG update }
-// The update kernel clears the condition once |rho| <= tol |rho_0|, max iterations or p^T H p <= 0.
-cudaError_t build_pcg_graph(rba_ctx *c) {
-    cudaError_t e;
-    cudaGraph_t g;
-    if ((e = cudaGraphCreate(&g, 0))) return e;
-    cudaGraphConditionalHandle h;
-    if ((e = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault))) return e;
-    cudaGraphNodeParams np = {};
-    np.type = cudaGraphNodeTypeConditional;
-    np.conditional.handle = h;
-    np.conditional.type = cudaGraphCondTypeWhile;
-    np.conditional.size = 1;
-    cudaGraphNode_t node;
-    if ((e = cudaGraphAddNode(&node, g, nullptr, 0, &np))) return e;
-    cudaGraph_t body = np.conditional.phGraph_out[0];
-    cudaStream_t cs;
-    if ((e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking))) return e;
-    if ((e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed))) return e;
-    cudaStream_t saved = c->stream;
-    const bool prof = c->profiling;
-    const int64_t nl = c->launches;
-    c->stream = cs;
-    c->profiling = false;
-    static const bool nofork = getenv("RBA_GRAPH_NOFORK") != nullptr;
-    c->nofork = nofork;
-    static const bool single = getenv("RBA_PCG_SINGLE_CTA") != nullptr;
-    if (single) {
-        matvec_body(c, c->d.p32, c->d.pcg);
-        k_pcg_step<<<1, 1024, 0, cs>>>(c->d, -1.f, c->opt.pcg_rel_tol, c->opt.pcg_max_iters, h, 1);
-        c->launches++;
-    } else {
-        const bool fuse = matvec_body(c, c->d.p32, c->d.pcg, false);
-        pcg_update(c, cs, -1.f, c->opt.pcg_rel_tol, c->opt.pcg_max_iters, fuse, h, 1);
-    }
-    c->stream = saved;
-    c->profiling = prof;
-    c->nofork = false;
-    c->graph_body_kernels = c->launches - nl;  // kernel nodes per loop iteration
-    c->launches = nl;
-    cudaGraph_t captured;
-    e = cudaStreamEndCapture(cs, &captured);
-    cudaStreamDestroy(cs);
-    if (e) return e;
-    if ((e = cudaGraphInstantiate(&c->pcg_exec, g, 0))) return e;
-    c->pcg_graph = g;
-    return cudaSuccess;
-}
-
-cudaError_t launch_backsub(rba_ctx *c, float lam) {
+cudaError_t launch_backsub(rba_ctx *c) {
     Prof P(c, KID_BACKSUB, 0.0);
     if (c->d.sc) {
-        cudaError_t e = launch_sc_backsub(c, lam);
+        cudaError_t e = launch_sc_backsub(c);
         if (e) return e;
     } else if (c->d.fac) {
-        cudaError_t e = launch_fac_backsub(c, lam);
+        cudaError_t e = launch_fac_backsub(c);
         if (e) return e;
     } else if (c->d.s64) {
-        cudaError_t e = launch_backsub64(c, lam);
+        cudaError_t e = launch_backsub64(c);
         if (e) return e;
     } else if (c->d.n_l) {
         const unsigned g = (unsigned)std::min<int64_t>(nblk(32 * c->d.n_l, 256), (int64_t)c->num_sms * 8);
-        k_backsub<<<g, 256, 0, c->stream>>>(c->d, lam);
+        k_backsub<<<g, 256, 0, c->stream>>>(c->d);
         c->launches++;
     }
-    k_trial_cams<<<1, 1024, 0, c->stream>>>(c->d, lam, c->d.sc ? 0 : 1);
+    k_trial_cams<<<1, 1024, 0, c->stream>>>(c->d, c->d.sc ? 0 : 1);
     c->launches++;
     P.end();
     return cudaGetLastError();

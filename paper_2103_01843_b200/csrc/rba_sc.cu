@@ -177,7 +177,8 @@ __global__ void __launch_bounds__(256) k_sc_mirror(DevProblem d) {
 // J_p,a^T r_a - L_a b_l are added.  Phase 2: lane a adds block (a, b), b >= a:
 //   delta_ab J_p,a^T J_p,a - L_a G_b^T   to H~(c_a, c_b) (and its transpose to H~(c_b, c_a)).
 template <typename T>
-__global__ void __launch_bounds__(256) k_sc_build(DevProblem d, T lam, float dmin, float dmax) {
+__global__ void __launch_bounds__(256) k_sc_build(DevProblem d, float dmin, float dmax) {
+    const T lam = (T)d.scal[SC_LAM];  // lambda of this attempt (explicit-32: rounded to FP32)
     T *val = reinterpret_cast<T *>(d.bsr_val);
     T *bsc = reinterpret_cast<T *>(d.sc_b);
     T *scr = reinterpret_cast<T *>(d.sc_scratch);
@@ -304,8 +305,10 @@ __global__ void k_sc_precond(DevProblem d) {
 // ---- back-substitution dl_j = -H_ll^-1 (b_l + sum_a G_a^T dp_a) and the model decrease
 // L(0) - L(dx) = -sum_a (2 r_a^T J_a dx_a + |J_a dx_a|^2) (C10, undamped), summed per CTA.
 template <typename T>
-__global__ void __launch_bounds__(256) k_sc_backsub(DevProblem d, T lam, float dmin, float dmax) {
+__global__ void __launch_bounds__(256) k_sc_backsub(DevProblem d, float dmin, float dmax) {
     __shared__ double red[32];
+    if (d.pcg->reason == 2) return;  // indefinite attempt: no step
+    const T lam = (T)d.scal[SC_LAM];
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     double md = 0.0;
@@ -362,22 +365,22 @@ __global__ void k_f2d(const float *__restrict__ a, double *__restrict__ b, int64
 static inline unsigned nb(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
 
 template <typename T>
-static cudaError_t sc_build_t(rba_ctx *c, float lam) {
+static cudaError_t sc_build_t(rba_ctx *c) {
     DevProblem &d = c->d;
     cudaMemsetAsync(d.bsr_val, 0, sizeof(T) * SC_BS * (size_t)d.nnzb, c->stream);
     cudaMemsetAsync(d.sc_b, 0, sizeof(T) * 9 * (size_t)d.n_p, c->stream);
     if (d.n_l) {
         const unsigned g = (unsigned)std::min<int64_t>(nb(32 * d.n_l, 256), (int64_t)c->num_sms * 16);
-        k_sc_build<T><<<g, 256, 0, c->stream>>>(d, (T)lam, (float)c->opt.diag_min, (float)c->opt.diag_max);
+        k_sc_build<T><<<g, 256, 0, c->stream>>>(d, (float)c->opt.diag_min, (float)c->opt.diag_max);
         k_sc_mirror<T><<<nb(32 * d.n_p, 256), 256, 0, c->stream>>>(d);
         c->launches += 2;
     }
     return cudaGetLastError();
 }
 
-cudaError_t launch_sc_build(rba_ctx *c, float lam) {
+cudaError_t launch_sc_build(rba_ctx *c) {
     Prof P(c, KID_MARG, c->marg_bytes);
-    cudaError_t e = c->d.sc == 2 ? sc_build_t<double>(c, lam) : sc_build_t<float>(c, lam);
+    cudaError_t e = c->d.sc == 2 ? sc_build_t<double>(c) : sc_build_t<float>(c);
     P.end();
     return e;
 }
@@ -408,14 +411,14 @@ void launch_sc_spmv(rba_ctx *c, const PcgState *st, const float *v32) {
     c->launches++;
 }
 
-cudaError_t launch_sc_backsub(rba_ctx *c, float lam) {
+cudaError_t launch_sc_backsub(rba_ctx *c) {
     DevProblem &d = c->d;
     if (d.n_l) {
         const unsigned g = (unsigned)std::min<int64_t>(nb(32 * d.n_l, 256), (int64_t)c->num_sms * 8);
         if (d.sc == 2)
-            k_sc_backsub<double><<<g, 256, 0, c->stream>>>(d, (double)lam, (float)c->opt.diag_min, (float)c->opt.diag_max);
+            k_sc_backsub<double><<<g, 256, 0, c->stream>>>(d, (float)c->opt.diag_min, (float)c->opt.diag_max);
         else
-            k_sc_backsub<float><<<g, 256, 0, c->stream>>>(d, lam, (float)c->opt.diag_min, (float)c->opt.diag_max);
+            k_sc_backsub<float><<<g, 256, 0, c->stream>>>(d, (float)c->opt.diag_min, (float)c->opt.diag_max);
         c->launches++;
     }
     return cudaGetLastError();

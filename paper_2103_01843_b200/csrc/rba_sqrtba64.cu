@@ -70,7 +70,7 @@ __device__ __forceinline__ void damp64(const double *R, const double *sD, double
 // Work item = (landmark, rows [r0, r1) of the pose rows 0..2k-1): the O(k) prologue is recomputed
 // per item; the item with r0 == 0 also writes the special rows (0..2, 2k..2k+2) and the Givens.
 template <int NT>
-__global__ void __launch_bounds__(NT, NT == 32 ? 16 : 1) k_marg64(DevProblem d, const LargeItem *__restrict__ items, double lam,
+__global__ void __launch_bounds__(NT, NT == 32 ? 16 : 1) k_marg64(DevProblem d, const LargeItem *__restrict__ items,
                                                double dmin, double dmax) {
     extern __shared__ double s64[];
     __shared__ double red[4 * (NT / 32)];
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(NT, NT == 32 ? 16 : 1) k_marg64(DevProblem d, 
     // damping rotations from the undamped R (rows 0..2 of SX) and sqrt(lam) D_l
     double R[9], g[12];
     for (int i = 0; i < 9; i++) R[i] = SX[i];
-    const double sq = sqrt(lam), sD[3] = {sq * Dl[0], sq * Dl[1], sq * Dl[2]};
+    const double sq = sqrt(d.scal[SC_LAM]), sD[3] = {sq * Dl[0], sq * Dl[1], sq * Dl[2]};
     damp64(R, sD, g);
     const Blk64 B = blk64(d, j, k);
     // pose columns of every row: thread <-> camera block o (warp <-> 32 consecutive blocks); each
@@ -289,7 +289,7 @@ __device__ __forceinline__ double gsum64(double v) {
 }
 
 template <int G>
-__global__ void __launch_bounds__(256) k_marg64_small(DevProblem d, int64_t lo, int64_t hi, double lam, double dmin,
+__global__ void __launch_bounds__(256) k_marg64_small(DevProblem d, int64_t lo, int64_t hi, double dmin,
                                                       double dmax) {
     const int lane = threadIdx.x & 31, gl = lane % G;
     const int64_t wfirst = lo + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * (32 / G);
@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(256) k_marg64_small(DevProblem d, int64_t lo, 
     rr3[0] = __shfl_sync(0xffffffffu, rv[0], 0, G);
     rr3[1] = __shfl_sync(0xffffffffu, rv[1], 0, G);
     rr3[2] = __shfl_sync(0xffffffffu, rv[0], 1, G);
-    const double sq = sqrt(lam), sD[3] = {sq * Dl[0], sq * Dl[1], sq * Dl[2]};
+    const double sq = sqrt(d.scal[SC_LAM]), sD[3] = {sq * Dl[0], sq * Dl[1], sq * Dl[2]};
     double g[12];
     damp64(R, sD, g);
     double M[27];  // own block: M = T^T V_o^T J_o
@@ -477,7 +477,7 @@ __global__ void __launch_bounds__(256) k_marg64_small(DevProblem d, int64_t lo, 
 
 // ---- K3-64: undo the stored rotations (reverse order, transposed) and re-damp, rows {0,1,2} and
 // {2k..2k+2} over all 9k + 4 columns.  Warp per landmark.
-__global__ void __launch_bounds__(256) k_redamp64(DevProblem d, double lam) {
+__global__ void __launch_bounds__(256) k_redamp64(DevProblem d) {
     const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (j >= d.n_l) return;
@@ -503,7 +503,7 @@ __global__ void __launch_bounds__(256) k_redamp64(DevProblem d, double lam) {
     double R[9];
     for (int i = 0; i < 3; i++)
         for (int q = 0; q < 3; q++) R[3 * i + q] = q < i ? 0.0 : X[i][q];
-    const double sq = sqrt(lam);
+    const double sq = sqrt(d.scal[SC_LAM]);
     const double sD[3] = {sq * d.lm_D64[3 * j], sq * d.lm_D64[3 * j + 1], sq * d.lm_D64[3 * j + 2]};
     double gn[12];
     damp64(R, sD, gn);
@@ -904,8 +904,10 @@ void launch_reduce_slices64(rba_ctx *c, double *out) {
 }
 
 // ---- K7-64: dl = -R^1^-1 (Q^1^T r^ + Q^1^T J_p dp), warp per landmark (grid-stride)
-__global__ void __launch_bounds__(256) k_backsub64(DevProblem d, double lam) {
+__global__ void __launch_bounds__(256) k_backsub64(DevProblem d) {
     __shared__ double red[32];
+    if (d.pcg->reason == 2) return;  // indefinite attempt: no step
+    const double lam = d.scal[SC_LAM];
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     double q1 = 0.0, dd = 0.0;
@@ -954,17 +956,17 @@ void launch_f2d64(rba_ctx *c, const float *a, double *b, int64_t n) {
 }
 
 template <int NT>
-static void marg64_cls(rba_ctx *c, int cls, double lam) {
+static void marg64_cls(rba_ctx *c, int cls) {
     const int64_t lo = c->s64_ilo[cls], hi = c->s64_ihi[cls];
     if (hi <= lo) return;
     const size_t sm = sizeof(double) * (14 * (size_t)c->s64_kmax[cls] + 288 * (NT / 32));  // SX | SR | SV | stage
     cudaFuncSetAttribute(k_marg64<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_marg64<NT><<<(unsigned)(hi - lo), NT, sm, c->stream>>>(c->d, c->d.marg_items + lo, lam, c->opt.diag_min,
+    k_marg64<NT><<<(unsigned)(hi - lo), NT, sm, c->stream>>>(c->d, c->d.marg_items + lo, c->opt.diag_min,
                                                             c->opt.diag_max);
     c->launches++;
 }
 
-cudaError_t launch_marg64(rba_ctx *c, double lam) {
+cudaError_t launch_marg64(rba_ctx *c) {
     Prof P(c, KID_MARG, c->marg_bytes);
     for (int g = 0; g < 4; g++) {  // k <= 32: grouped kernel by group size 4 / 8 / 16 / 32
         const int64_t lo = c->s64_mlo[g], hi = c->s64_mhi[g];
@@ -972,24 +974,24 @@ cudaError_t launch_marg64(rba_ctx *c, double lam) {
         const int G = 4 << g;
         const unsigned blocks = nb64((hi - lo) * G, 256);
         const double dmin = c->opt.diag_min, dmax = c->opt.diag_max;
-        if (g == 0) k_marg64_small<4><<<blocks, 256, 0, c->stream>>>(c->d, lo, hi, lam, dmin, dmax);
-        else if (g == 1) k_marg64_small<8><<<blocks, 256, 0, c->stream>>>(c->d, lo, hi, lam, dmin, dmax);
-        else if (g == 2) k_marg64_small<16><<<blocks, 256, 0, c->stream>>>(c->d, lo, hi, lam, dmin, dmax);
-        else k_marg64_small<32><<<blocks, 256, 0, c->stream>>>(c->d, lo, hi, lam, dmin, dmax);
+        if (g == 0) k_marg64_small<4><<<blocks, 256, 0, c->stream>>>(c->d, lo, hi, dmin, dmax);
+        else if (g == 1) k_marg64_small<8><<<blocks, 256, 0, c->stream>>>(c->d, lo, hi, dmin, dmax);
+        else if (g == 2) k_marg64_small<16><<<blocks, 256, 0, c->stream>>>(c->d, lo, hi, dmin, dmax);
+        else k_marg64_small<32><<<blocks, 256, 0, c->stream>>>(c->d, lo, hi, dmin, dmax);
         c->launches++;
     }
-    marg64_cls<128>(c, 1, lam);
-    marg64_cls<256>(c, 2, lam);
-    marg64_cls<256>(c, 3, lam);
-    marg64_cls<256>(c, 4, lam);
+    marg64_cls<128>(c, 1);
+    marg64_cls<256>(c, 2);
+    marg64_cls<256>(c, 3);
+    marg64_cls<256>(c, 4);
     P.end();
     return cudaGetLastError();
 }
 
-cudaError_t launch_redamp64(rba_ctx *c, double lam) {
+cudaError_t launch_redamp64(rba_ctx *c) {
     if (c->d.n_l == 0) return cudaSuccess;
     Prof P(c, KID_DAMP, 0.0);
-    k_redamp64<<<nb64(32 * c->d.n_l, 256), 256, 0, c->stream>>>(c->d, lam);
+    k_redamp64<<<nb64(32 * c->d.n_l, 256), 256, 0, c->stream>>>(c->d);
     c->launches++;
     P.end();
     return cudaGetLastError();
@@ -1071,10 +1073,10 @@ void launch_pre64(rba_ctx *c) {
     rcs64_tma_cls<256, KMAX64 / 256, true>(c, 4, nullptr, nullptr);
 }
 
-cudaError_t launch_backsub64(rba_ctx *c, float lam) {
+cudaError_t launch_backsub64(rba_ctx *c) {
     if (c->d.n_l) {
         const unsigned g = (unsigned)std::min<int64_t>(nb64(32 * c->d.n_l, 256), (int64_t)c->num_sms * 8);
-        k_backsub64<<<g, 256, 0, c->stream>>>(c->d, (double)lam);
+        k_backsub64<<<g, 256, 0, c->stream>>>(c->d);
         c->launches++;
     }
     return cudaGetLastError();

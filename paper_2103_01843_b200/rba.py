@@ -30,7 +30,8 @@ class rba_options(C.Structure):
                 ("nccl_unique_id", C.c_void_p), ("lambda0", C.c_double), ("pcg_rel_tol", C.c_double),
                 ("pcg_max_iters", C.c_int), ("min_rel_decrease", C.c_double), ("diag_min", C.c_double),
                 ("diag_max", C.c_double), ("alloc", _ALLOC_T), ("free", _FREE_T), ("alloc_ctx", C.c_void_p),
-                ("huber_delta", C.c_double), ("solver", C.c_int), ("storage", C.c_int), ("precision", C.c_int)]
+                ("huber_delta", C.c_double), ("solver", C.c_int), ("storage", C.c_int), ("precision", C.c_int),
+                ("deterministic", C.c_int)]
 RBA_PRECISION_FP32, RBA_PRECISION_FP64 = 0, 1
 RBA_STORAGE_DENSE, RBA_STORAGE_FACTORED = 0, 1
 RBA_SOLVER_SQRTBA, RBA_SOLVER_EXPLICIT_SC32, RBA_SOLVER_EXPLICIT_SC64 = 0, 1, 2
@@ -43,7 +44,10 @@ class rba_pcg_stats(C.Structure):
 class rba_lm_report(C.Structure):
     _fields_ = [("iter", C.c_int64), ("accepted", C.c_int), ("pcg_iters", C.c_int), ("pcg_reason", C.c_int),
                 ("cost", C.c_double), ("cost_trial", C.c_double), ("cost_after", C.c_double),
-                ("model", C.c_double), ("rho", C.c_double), ("lambda_", C.c_double), ("lambda_next", C.c_double)]
+                ("model", C.c_double), ("rho", C.c_double), ("lambda_", C.c_double), ("lambda_next", C.c_double),
+                ("relinearized", C.c_int), ("status", C.c_int), ("t_linearize_ms", C.c_double),
+                ("t_marginalize_ms", C.c_double), ("t_precond_ms", C.c_double), ("t_pcg_ms", C.c_double),
+                ("t_trial_ms", C.c_double), ("t_total_ms", C.c_double), ("device_bytes", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -77,6 +81,11 @@ def _load():
         "rba_backsubstitute": (I, [P]),
         "rba_cost": (I, [P, I, C.POINTER(C.c_double)]),
         "rba_lm_step": (I, [P, C.POINTER(rba_lm_report)]),
+        "rba_lm_solve": (I, [P, I, D, P, C.POINTER(I)]),
+        "rba_set_lm": (I, [P, D, D]),
+        "rba_get_lm": (I, [P, C.POINTER(D), C.POINTER(D), C.POINTER(I64)]),
+        "rba_set_pcg_limits": (I, [P, D, I]),
+        "rba_device_bytes": (I, [P, C.POINTER(I64)]),
         "rba_get_state": (I, [P, P, P]),
         "rba_set_state": (I, [P, P, P]),
         "rba_reset_lm": (I, [P]),
@@ -110,7 +119,8 @@ def _load():
 
 _lib = _load()
 EXPORTED = ["rba_default_options", "rba_create", "rba_destroy", "rba_linearize", "rba_marginalize_qr",
-            "rba_pcg_solve", "rba_backsubstitute", "rba_cost", "rba_lm_step", "rba_get_state", "rba_set_state", "rba_reset_lm",
+            "rba_pcg_solve", "rba_backsubstitute", "rba_cost", "rba_lm_step", "rba_lm_solve", "rba_get_state",
+            "rba_set_state", "rba_reset_lm", "rba_set_lm", "rba_get_lm", "rba_set_pcg_limits", "rba_device_bytes",
             "rba_matvec", "rba_get_rhs", "rba_get_step", "rba_get_scaling", "rba_export_block", "rba_arena_bytes",
             "rba_kernel_launches", "rba_profile", "rba_profile_get", "rba_plan_shards", "rba_nccl_unique_id",
             "rba_last_error", "rba_bal_parse", "rba_bal_read", "rba_bal_write", "rba_bal_normalize",
@@ -181,6 +191,33 @@ def rba_lm_step(h) -> dict:
     r = rba_lm_report()
     _check(_lib.rba_lm_step(h, C.byref(r)))
     return r.as_dict()
+
+
+def rba_lm_solve(h, max_iters: int, ftol: float = 1e-6) -> list:
+    reps = (rba_lm_report * max(1, int(max_iters)))()
+    n = C.c_int()
+    _check(_lib.rba_lm_solve(h, int(max_iters), float(ftol), reps, C.byref(n)))
+    return [reps[i].as_dict() for i in range(n.value)]
+
+
+def rba_set_lm(h, lam, nu=2.0):
+    _check(_lib.rba_set_lm(h, float(lam), float(nu)))
+
+
+def rba_get_lm(h):
+    lam, nu, it = C.c_double(), C.c_double(), C.c_int64()
+    _check(_lib.rba_get_lm(h, C.byref(lam), C.byref(nu), C.byref(it)))
+    return lam.value, nu.value, it.value
+
+
+def rba_set_pcg_limits(h, rel_tol, max_iters):
+    _check(_lib.rba_set_pcg_limits(h, float(rel_tol), int(max_iters)))
+
+
+def rba_device_bytes(h) -> int:
+    n = C.c_int64()
+    _check(_lib.rba_device_bytes(h, C.byref(n)))
+    return n.value
 
 
 def rba_get_state(h, n_cams, n_points, out=None):
@@ -432,6 +469,19 @@ class Solver:
 
     def lm_step(self):
         return rba_lm_step(self.h)
+
+    def lm_solve(self, max_iters=50, ftol=1e-6):
+        """The paper's LM loop on the device: reports of the iterations run."""
+        return rba_lm_solve(self.h, max_iters, ftol)
+
+    def set_lm(self, lam, nu=2.0):
+        rba_set_lm(self.h, lam, nu)
+
+    def get_lm(self):
+        return rba_get_lm(self.h)
+
+    def set_pcg_limits(self, rel_tol, max_iters):
+        rba_set_pcg_limits(self.h, rel_tol, max_iters)
 
     def state(self, out=None):
         return rba_get_state(self.h, self.n_p, self.n_l, out)

@@ -1,12 +1,31 @@
-"""LM cost parity helper: cost after each iteration within `bar` (1e-4) relative of
-the oracle's.  PCG stops at a relative residual of 1e-2; where its iteration count differs from the
-oracle's (the stop is decided by FP32 summation order, which varies run to run with the
-camera-slice reductions, and on ill-conditioned iterations -- 130 to 260 PCG iterations on
-configs 2 and 3 -- counts drift by a few), the steps differ by up to the tolerance.  §8c re-runs
-both at the oracle's count, which the C ABI cannot replay, so in that case the bar is 1e-3."""
+"""LM cost parity: the cost after each LM iteration within `bar` (1e-4) relative of
+the oracle's, with no relaxation.  PCG stops at a relative residual of 1e-2 (reading C11); where the
+GPU's FP32 solve stops at a different iteration count than the oracle's FP64 solve (the tolerance
+edge), §8c re-runs the iteration with the oracle's count fixed: the GPU state and LM schedule from
+before the iteration are restored through the C ABI (rba_set_state, rba_set_lm) and the iteration
+is replayed with rba_set_pcg_limits(0, n_oracle), which runs exactly that many PCG iterations."""
 
 
-def check_lm_step(i, rg, ro, bar=1e-4, edge_bar=1e-3):
-    assert rg["pcg_reason"] != 2, (i, rg)
-    b = max(bar, edge_bar) if rg["pcg_iters"] != ro["pcg_iters"] else bar
-    assert abs(rg["cost_after"] - ro["cost_after"]) <= b * ro["cost_after"], (i, rg, ro)
+def lm_parity(s, o, iters, bar=1e-4, pcg_tol=1e-2, pcg_max=500, allow_indefinite=False):
+    """Run `iters` LM iterations on the GPU solver `s` and the oracle `o` from their current states;
+    returns the list of (gpu_report, oracle_report, replayed)."""
+    out = []
+    for i in range(iters):
+        cams, pts = s.state()
+        lam, nu, _ = s.get_lm()
+        rg = s.lm_step()
+        ro = o.lm_step(pcg_tol, pcg_max)
+        replayed = False
+        if rg["pcg_iters"] != ro["pcg_iters"]:
+            s.set_state(cams, pts)
+            s.set_lm(lam, nu)
+            s.set_pcg_limits(0.0, ro["pcg_iters"])
+            rg = s.lm_step()
+            s.set_pcg_limits(pcg_tol, pcg_max)
+            replayed = True
+            assert rg["pcg_iters"] == ro["pcg_iters"] or rg["pcg_reason"] == 2, (i, rg, ro)
+        if not allow_indefinite:
+            assert rg["pcg_reason"] != 2 and ro["pcg_reason"] != 2, (i, rg, ro)  # never indefinite
+        assert abs(rg["cost_after"] - ro["cost_after"]) <= bar * ro["cost_after"], (i, replayed, rg, ro)
+        out.append((rg, ro, replayed))
+    return out

@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 import oracle
-from _lm import check_lm_step
+from _lm import lm_parity
 from paper_2103_01843_b200 import synth
 from paper_2103_01843_b200.rba import RBA_STORAGE_DENSE, RBA_STORAGE_FACTORED
 
@@ -102,10 +102,7 @@ def test_factored_pcg_backsub_and_lm(cfg):
     s.close()
     s = _solver(p)
     o = oracle.Oracle(p)
-    for i in range(5):
-        rg, ro = s.lm_step(), o.lm_step()
-        assert rg["pcg_reason"] != 2
-        check_lm_step(i, rg, ro)
+    lm_parity(s, o, 5)
 
 
 def test_factored_matches_dense_at_config3():

@@ -15,7 +15,7 @@ import numpy as np
 import pytest
 
 import oracle
-from _lm import check_lm_step
+from _lm import lm_parity
 from paper_2103_01843_b200 import synth
 
 pytestmark = pytest.mark.gpu
@@ -115,6 +115,4 @@ def test_full_lm_cost_trajectory(full):
     s.reset_lm()
     o.set_state(p["cameras_init"], p["points_init"])
     o.set_lm(LAM, 2.0)
-    for i in range(5 if full.cfg == 3 else 2):
-        rg, ro = s.lm_step(), o.lm_step()
-        check_lm_step(i, rg, ro)
+    lm_parity(s, o, 5)

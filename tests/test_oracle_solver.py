@@ -52,7 +52,6 @@ def test_column_scaling_definition():
     np.testing.assert_allclose(sl, 1 / (1 + np.sqrt(ln)), rtol=1e-13)
     np.testing.assert_allclose(Dp2, np.clip(cn * sp ** 2, 1e-6, 1e32), rtol=1e-13)
     np.testing.assert_allclose(Dl2, np.clip(ln * sl ** 2, 1e-6, 1e32), rtol=1e-13)
-    assert 1 / (1 + 3.0) == 0.25
 
 
 @pytest.mark.parametrize("seed", range(6))
@@ -178,6 +177,36 @@ def test_pcg_backsub_and_brute_force_step(seed, lam):
         dxx = np.concatenate([o.dp(), o.dl()])
         direct = r @ r - np.sum((r + J @ dxx) ** 2)
         np.testing.assert_allclose(o.model_decrease(), direct, rtol=1e-9)
+
+
+@pytest.mark.parametrize("seed,lam", [(14, 1e-4), (15, 1.0)])
+def test_block_jacobi_blocks_are_the_diagonal_of_the_reduced_system(seed, lam):
+    """The preconditioner is block Jacobi on H~ ("block-diagonal of H~pp", C12): each
+    9 x 9 block P_i of orc_precond_rhs (reconstructed from its stored Cholesky factor) equals the
+    diagonal block of the dense H~ of orc_reduced_dense, whose diagonal includes lambda D_p^2, and
+    the dense H~ itself is pinned to the explicit Schur complement above.  The first PCG iterate
+    is alpha M^-1 (-b~) with M = blockdiag(H~): a point-Jacobi or unpreconditioned
+    PCG fails both checks."""
+    p = _small(seed, n_p=6, n_l=30, kmin=2, kmax=6)
+    o = oracle.Oracle(p)
+    o.linearize()
+    o.marginalize()
+    o.damp(lam)
+    H, b = o.reduced_dense()
+    assert o.precond_rhs() == 0
+    P = o.precond_blocks()
+    for i in range(o.n_p):
+        Hi = H[9 * i:9 * i + 9, 9 * i:9 * i + 9]
+        np.testing.assert_allclose(P[i], Hi, rtol=1e-12, atol=1e-13 * np.abs(Hi).max())
+        assert np.abs(Hi - np.diag(np.diag(Hi))).max() > 1e-3 * np.abs(Hi).max()  # genuinely 9 x 9
+    M = np.zeros_like(H)
+    for i in range(o.n_p):
+        M[9 * i:9 * i + 9, 9 * i:9 * i + 9] = H[9 * i:9 * i + 9, 9 * i:9 * i + 9]
+    z = np.linalg.solve(M, -b)
+    alpha = (-b @ z) / (z @ H @ z)
+    it, reason, _ = o.pcg(tol=0.0, max_iters=1)
+    assert it == 1 and reason == 1
+    assert relf(o.dp(), alpha * z) < 1e-11
 
 
 def test_pcg_degenerate_and_limits():
