@@ -222,6 +222,9 @@ rba_status rba_arena_bytes(rba_ctx *ctx, int64_t *logical, int64_t *physical);
 rba_status rba_kernel_launches(rba_ctx *ctx, int64_t *count);
 /* Device memory held by the context (bytes of every buffer it allocated). */
 rba_status rba_device_bytes(rba_ctx *ctx, int64_t *bytes);
+/* Algorithmic bytes of one marginalization (K2: the landmark blocks written + the
+ * observations read) and of one reduced-camera-system product (K5: the reduced rows read once). */
+rba_status rba_plan_bytes(rba_ctx *ctx, double *marginalize_bytes, double *matvec_bytes);
 /* Per-kernel CUDA-event timing on the context stream: enable (1) / disable (0) and reset. */
 rba_status rba_profile(rba_ctx *ctx, int enable);
 /* kernel: 0 linearize(K1), 1 marginalize(K2), 2 damp(K3), 3 precond+rhs(K4), 4 matvec(K5),

@@ -444,12 +444,13 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
                 // blocks, ~1 MB of tiles)
                 c->huge_max_k = std::max<int64_t>(c->huge_max_k, k);
                 for (int t = 0; t < T; t++) huge_y.push_back(HugeItem{(int32_t)i, 0, t, t + 1, ybuf_n});
-                const int tpo = std::max(1, (1 << 20) / (144 * HUGE_NT));
                 for (int o0 = 0; o0 < k; o0 += HUGE_NT)
-                    for (int t0 = 0; t0 < T; t0 += tpo)
-                        huge_out.push_back(HugeItem{(int32_t)i, o0, t0, std::min(T, t0 + tpo), ybuf_n});
+                    for (int t0 = 0; t0 < T; t0 += HUGE_TPO)
+                        huge_out.push_back(HugeItem{(int32_t)i, o0, t0, std::min(T, t0 + HUGE_TPO), ybuf_n});
+                // fused product items; yoff = the item's index within its landmark (deterministic mode)
                 const int tpf = std::max(1, (1 << 20) / (144 * k));
-                for (int t0 = 0; t0 < T; t0 += tpf) huge_fused.push_back(HugeItem{(int32_t)i, 0, t0, std::min(T, t0 + tpf), 0});
+                for (int t0 = 0; t0 < T; t0 += tpf)
+                    huge_fused.push_back(HugeItem{(int32_t)i, 0, t0, std::min(T, t0 + tpf), (int64_t)(t0 / tpf)});
                 ybuf_n += 4 * (int64_t)T;
                 continue;
             }
@@ -516,6 +517,69 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
                 break;
             }
         c->arena_floats = std::max<int64_t>(off, 4);
+    }
+    // ---- deterministic mode: slot numbering of the camera-space contributions.  Parts per
+    // observation: K5 small-k pack units (row-pair groups of 4), large-pipe consumer runs a track's
+    // tiles span (shared by K4 and K5), huge-track tile-range items (separately for K4 and K5).
+    // Slots are camera-major: camera i owns [camptrF[i], camptrF[i+1]), its observations in
+    // landmark order, each with its parts consecutive.
+    std::vector<int32_t> h_slot[3], h_run0;
+    std::vector<int64_t> h_cp[3];
+    int64_t n_slots[3] = {0, 0, 0};
+    if (opt.deterministic) {
+        std::vector<int32_t> p4(nl, 1), p5(nl, 1);
+        for (int64_t i = 0; i < large_lo; i++) p5[i] = (c->h_k[i] + 3) / 4;
+        // consumer runs (CTA b, slot sl) of the large-pipe classes: a run's landmarks other than its
+        // first start in it (part 0); its first landmark's part = the runs of that landmark before it
+        std::vector<int32_t> cnt(nl, 0);
+        for (int cls = 0; cls < 5; cls++) {
+            const int NS = PIPE_NSLOT[cls];
+            c->run_off[cls] = (int64_t)h_run0.size();
+            for (int64_t b = 0; b < c->cta_n[cls]; b++) {
+                const int64_t lo = cta_lo[c->cta_off[cls] + b], hi = cta_lo[c->cta_off[cls] + b + 1];
+                const int64_t nst = (hi - lo + NS - 1) / NS;
+                for (int sl = 0; sl < NS; sl++) {
+                    const int64_t a = lo + sl * nst, e = std::min(hi, lo + (sl + 1) * nst);
+                    h_run0.push_back(a < e ? cnt[tiles[a].lm] : 0);
+                    int32_t prev = -1;
+                    for (int64_t t = a; t < e; t++)
+                        if (tiles[t].lm != prev) prev = tiles[t].lm, cnt[prev]++;
+                }
+            }
+        }
+        for (int64_t i = large_lo; i < nl; i++)
+            if (cnt[i] > 0) p5[i] = p4[i] = cnt[i];
+        for (auto &it : huge_fused) p5[it.lm] = std::max<int32_t>(p5[it.lm], (int32_t)it.yoff + 1);
+        for (auto &it : huge_out) p4[it.lm] = std::max<int32_t>(p4[it.lm], it.t0 / HUGE_TPO + 1);
+        std::vector<int32_t> ocam(nobs_loc), olm(nobs_loc);
+        for (int64_t i = 0; i < nl; i++)
+            for (int o = 0; o < c->h_k[i]; o++) {
+                ocam[h_obs0[i] + o] = obs_cam[ord[gptr[loc[i]] + o]];
+                olm[h_obs0[i] + o] = (int32_t)i;
+            }
+        std::vector<int64_t> first(n_cams + 1, 0);  // observations by camera (stable: landmarks ascending)
+        for (int64_t ob = 0; ob < nobs_loc; ob++) first[ocam[ob] + 1]++;
+        for (int64_t q = 0; q < n_cams; q++) first[q + 1] += first[q];
+        std::vector<int64_t> bycam(nobs_loc), fill(first.begin(), first.end() - 1);
+        for (int64_t ob = 0; ob < nobs_loc; ob++) bycam[fill[ocam[ob]]++] = ob;
+        for (int F = 0; F < 3; F++) {
+            const std::vector<int32_t> *parts = F == 1 ? &p4 : (F == 2 ? &p5 : nullptr);
+            h_slot[F].assign(std::max<int64_t>(nobs_loc, 1), 0);
+            h_cp[F].assign(n_cams + 1, 0);
+            int64_t pos = 0;
+            for (int64_t q = 0; q < n_cams; q++) {
+                h_cp[F][q] = pos;
+                for (int64_t m = first[q]; m < first[q + 1]; m++) {
+                    const int64_t ob = bycam[m];
+                    h_slot[F][ob] = (int32_t)pos;
+                    pos += parts ? (*parts)[olm[ob]] : 1;
+                }
+            }
+            h_cp[F][n_cams] = pos;
+            n_slots[F] = pos;
+            if (pos >= ((int64_t)1 << 31))
+                return bail(fail(RBA_ERR_INVALID_ARG, "deterministic mode: too many camera-sum slots for int32"));
+        }
     }
     // ---- device buffers
     DevProblem &d = c->d;
@@ -734,6 +798,30 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     CKSC(dalloc_n(c, &d.dl, 3 * nl));
     CKSC(dalloc_n(c, &d.scal, SC_N));
     CKSC(dalloc_n(c, &d.lm, 1));
+    d.det = opt.deterministic;
+    if (d.det) {
+        const int64_t of = std::max({56 * n_slots[1], 12 * n_slots[2], 12 * n_slots[0], (int64_t)16});
+        CKSC(dalloc_n(c, &d.obuf, of));
+        CKC(cudaMemsetAsync(d.obuf, 0, sizeof(float) * of, c->stream));
+        int32_t **sl[3] = {&d.slot1, &d.slot4, &d.slot5};
+        int64_t **cp[3] = {&d.camptr1, &d.camptr4, &d.camptr5};
+        for (int F = 0; F < 3; F++) {
+            CKSC(dalloc_n(c, sl[F], (int64_t)h_slot[F].size()));
+            CKSC(dalloc_n(c, cp[F], n_cams + 1));
+            CKC(cudaMemcpyAsync(*sl[F], h_slot[F].data(), sizeof(int32_t) * h_slot[F].size(), cudaMemcpyHostToDevice,
+                                c->stream));
+            CKC(cudaMemcpyAsync(*cp[F], h_cp[F].data(), sizeof(int64_t) * (n_cams + 1), cudaMemcpyHostToDevice,
+                                c->stream));
+        }
+        CKSC(dalloc_n(c, &d.run_part, std::max<int64_t>((int64_t)h_run0.size(), 1)));
+        if (!h_run0.empty())
+            CKC(cudaMemcpyAsync(d.run_part, h_run0.data(), sizeof(int32_t) * h_run0.size(), cudaMemcpyHostToDevice,
+                                c->stream));
+        CKSC(dalloc_n(c, &d.det_part, (int64_t)DS_N * DET_PART));
+        CKSC(dalloc_n(c, &d.det_ctr, DS_N));
+        CKC(cudaMemsetAsync(d.det_ctr, 0, sizeof(unsigned int) * DS_N, c->stream));
+        CKC(cudaStreamSynchronize(c->stream));  // host staging vectors go out of scope
+    }
     CKSC(dalloc_n(c, &d.reps, rba_ctx::REP_CAP));
     CKSC(dalloc_n(c, &d.packs, std::max<size_t>(1, packs.size())));
     CKSC(dalloc_n(c, &d.marg_items, std::max<size_t>(1, marg_items.size())));

@@ -138,6 +138,10 @@ struct HugeItem {
     int64_t yoff;
 };
 constexpr int HUGE_NT = 256;  // threads per CTA of the huge-k passes (camera blocks per out item)
+constexpr int HUGE_TPO = (1 << 20) / (144 * HUGE_NT);  // tiles per out / preconditioner item (~1 MB)
+constexpr int PIPE_NSLOT[5] = {8, 4, 2, 1, 1};          // consumer slots per CTA of the large-pipe classes
+constexpr int DET_PART = 2048;  // deterministic scalar sums: per-CTA partials per sum (>= any grid used)
+enum { DS_E = 0, DS_ET, DS_Q1R2, DS_DAMPL, DS_N };
 
 struct DevProblem {
     int64_t n_p, n_l, n_obs;  // local counts (landmarks / observations of this shard)
@@ -205,6 +209,21 @@ struct DevProblem {
                            // aligned), camera indices staged}
     int4 *s64_brec;        // ... and per batch 64 x 2 landmark records {arena offset lo, hi, bytes, stage
                            // offset}, {k, row-3 offset in the stage, camera offset, 0}
+    // deterministic mode (rba_options.deterministic): every contribution to a camera-space sum is
+    // stored in its own slot of obuf; the slots of a camera are consecutive (camera-major) and are
+    // added in a fixed order by k_det_reduce.  Family 1 = K1 camera norms (one slot per
+    // observation), 4 = K4 block-Jacobi + b~, 5 = K5 product; a family's slots of observation `ob`
+    // are slotF[ob] + part (the parts of one observation come from different work items: the
+    // row-pair units of a small-k pack, the consumer runs a long track's tiles are split over, the
+    // tile ranges of a huge track).  Scalar FP64 sums use per-CTA partials summed in CTA order.
+    int det;
+    float *obuf;
+    int32_t *slot1, *slot4, *slot5;
+    int64_t *camptr1, *camptr4, *camptr5;
+    int32_t *run_part;     // large-pipe consumer runs (class offset + CTA * NSLOT + slot): the part index
+                           // of the run's first landmark (its other landmarks start in it: part 0)
+    double *det_part;      // DS_N x DET_PART per-CTA partials
+    unsigned int *det_ctr; // DS_N last-CTA counters
 };
 
 struct Launch {
@@ -248,6 +267,7 @@ struct rba_ctx {
     int64_t s64_mlo[4] = {0, 0, 0, 0}, s64_mhi[4] = {0, 0, 0, 0};  // the same as landmark ranges
     int64_t s64_blo[3] = {0, 0, 0}, s64_bhi[3] = {0, 0, 0};  // k <= 4 / 8 / 16: their TMA batches
     int64_t cta_off[5] = {0, 0, 0, 0, 0}, cta_n[5] = {0, 0, 0, 0, 0};    // K4/K5 CTA ranges per class
+    int64_t run_off[5] = {0, 0, 0, 0, 0};  // deterministic mode: per class offset into d.run_part
     int64_t n_chunks = 0, chunk_ctas = 0;
     int64_t n_packs = 0, max_large_k = 0;
     int num_sms = 148;

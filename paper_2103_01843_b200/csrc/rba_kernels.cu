@@ -32,6 +32,86 @@
 
 namespace rba {
 
+// ============================================================================ deterministic mode
+// (rba_options.deterministic).  A camera-space contribution goes to its own slot
+// (plain stores, no atomics); k_det_reduce adds the slots of a camera in a fixed order.
+__device__ __forceinline__ void det_store12(const DevProblem &d, int64_t slot, const float *acc) {
+    float4 *o4 = reinterpret_cast<float4 *>(d.obuf + 12 * slot);
+    o4[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    o4[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+    o4[2] = make_float4(acc[8], 0.f, 0.f, 0.f);
+}
+__device__ __forceinline__ void det_store54(const DevProblem &d, int64_t slot, const float *P, const float *b) {
+    float4 *a4 = reinterpret_cast<float4 *>(d.obuf + (int64_t)PACC_STRIDE * slot);
+#pragma unroll
+    for (int i = 0; i < 11; i++) a4[i] = make_float4(P[4 * i], P[4 * i + 1], P[4 * i + 2], P[4 * i + 3]);
+    a4[11] = make_float4(P[44], b[0], b[1], b[2]);
+    a4[12] = make_float4(b[3], b[4], b[5], b[6]);
+    a4[13] = make_float4(b[7], b[8], 0.f, 0.f);
+}
+
+// out[NV cam + e] = sum over the camera's slots m (ascending) of obuf[stride m + e], FP64: thread t
+// takes slots t, t + 256, ... in order, then a fixed warp butterfly and a fixed order over warps.
+template <int NV>
+__global__ void __launch_bounds__(256) k_det_reduce(const float *__restrict__ obuf, const int64_t *__restrict__ camptr,
+                                                    int stride, double *__restrict__ out,
+                                                    const PcgState *__restrict__ st) {
+    if (st && st->done) return;  // PCG graph: no product ran
+    __shared__ double part[8][NV];
+    const int64_t cam = blockIdx.x;
+    const int64_t a = camptr[cam], b = camptr[cam + 1];
+    double acc[NV];
+#pragma unroll
+    for (int e = 0; e < NV; e++) acc[e] = 0.0;
+    for (int64_t m = a + threadIdx.x; m < b; m += 256) {
+        const float4 *row = reinterpret_cast<const float4 *>(obuf + (int64_t)stride * m);
+#pragma unroll
+        for (int q = 0; q < (NV + 3) / 4; q++) {
+            const float4 x = __ldcs(row + q);
+            const float v[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+                if (4 * q + u < NV) acc[4 * q + u] += (double)v[u];
+        }
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int e = 0; e < NV; e++) {
+        double v = acc[e];
+#pragma unroll
+        for (int m = 16; m; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+        if (lane == 0) part[warp][e] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < NV) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; w++) t += part[w][threadIdx.x];
+        out[NV * cam + threadIdx.x] = t;
+    }
+}
+
+// Grid-wide FP64 sum in a fixed order: the block total v (valid in every thread) goes to
+// parts[blockIdx.x]; the last CTA to finish adds the parts in CTA order into *out.
+__device__ void det_grid_sum(double v, double *parts, unsigned int *ctr, double *out) {
+    __shared__ bool last;
+    if (threadIdx.x == 0) parts[blockIdx.x] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(ctr, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (unsigned int b = 0; b < gridDim.x; b++) t += __ldcg(parts + b);
+        *out = t;
+        *ctr = 0;
+    }
+}
+
 // ============================================================================ K0 / K1
 __global__ void k_check_depth(DevProblem d, int *bad) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -78,15 +158,15 @@ __global__ void __launch_bounds__(256) k_linearize(DevProblem d) {
             float n2[9];
 #pragma unroll
             for (int q = 0; q < 9; q++) n2[q] = Jc[q] * Jc[q] + Jc[9 + q] * Jc[9 + q];
-            flush_cam12(wslice(d), cam, n2);  // per-SM slice (k_reduce_slices sums them in FP64)
+            if (d.det) det_store12(d, d.slot1[i], n2);  // own slot (k_det_reduce)
+            else flush_cam12(wslice(d), cam, n2);     // per-SM slice (k_reduce_slices sums them in FP64)
         }
     }
     e = block_sum_d(e, red);
     bad = block_sum_d(bad, red);
-    if (threadIdx.x == 0) {
-        atomicAdd(d.scal + SC_E, e);
-        if (bad > 0) atomicAdd(d.scal + SC_BAD, bad);
-    }
+    if (threadIdx.x == 0 && bad > 0) atomicAdd(d.scal + SC_BAD, bad);  // an integer count: exact
+    if (d.det) det_grid_sum(e, d.det_part + DS_E * DET_PART, d.det_ctr + DS_E, d.scal + SC_E);
+    else if (threadIdx.x == 0) atomicAdd(d.scal + SC_E, e);
 }
 
 __global__ void k_cam_scale(DevProblem d, float dmin, float dmax) {
@@ -909,7 +989,7 @@ constexpr size_t SP_SMEM = (size_t)SP_STAGES * SP_SB + 4 * SP_VCAP + 2 * SP_STAG
 template <int NRP, bool PRECOND>
 __device__ __forceinline__ void small_unit(const DevProblem &d, const float2 *A, int npk, int p0, int k, int G,
                                            bool valid, int cam, const float *vo, const float *qs,
-                                           float *__restrict__ out12) {
+                                           float *__restrict__ out12, int64_t slot) {
     float sl[NRP][18];
 #pragma unroll
     for (int u = 0; u < NRP; u++)
@@ -946,7 +1026,8 @@ __device__ __forceinline__ void small_unit(const DevProblem &d, const float2 *A,
             for (int u = 0; u < NRP; u++) a_ += sl[u][q] * y[2 * u] + sl[u][9 + q] * y[2 * u + 1];
             acc[q] = a_;
         }
-        flush_cam12(wslice(d), cam, acc);
+        if (d.det) det_store12(d, slot, acc);
+        else flush_cam12(wslice(d), cam, acc);
     }
 }
 
@@ -1041,15 +1122,18 @@ __global__ void __launch_bounds__(SP_WARPS * 32 + 32, 1)
                     acc_rows(P, b, sl, qs[2 * pp]);
                     acc_rows(P, b, sl + 9, qs[2 * pp + 1]);
                 }
-                flush54(pslice(d) + PACC_STRIDE * (int64_t)cam, P, b);
+                if (d.det) det_store54(d, d.slot4[pack.obs0 + mo], P, b);
+                else flush54(pslice(d) + PACC_STRIDE * (int64_t)cam, P, b);
                 continue;
             }
             if constexpr (!PRECOND) {
+                // deterministic mode: the unit's own slot (part = its row-pair group)
+                const int64_t slot = (d.det && valid) ? (int64_t)d.slot5[pack.obs0 + mo] + (code >> 8) : 0;
                 switch (min(4, k - p0)) {
-                    case 1: small_unit<1, false>(d, A, npk, p0, k, G, valid, cam, vo, qs, out12); break;
-                    case 2: small_unit<2, false>(d, A, npk, p0, k, G, valid, cam, vo, qs, out12); break;
-                    case 3: small_unit<3, false>(d, A, npk, p0, k, G, valid, cam, vo, qs, out12); break;
-                    default: small_unit<4, false>(d, A, npk, p0, k, G, valid, cam, vo, qs, out12); break;
+                    case 1: small_unit<1, false>(d, A, npk, p0, k, G, valid, cam, vo, qs, out12, slot); break;
+                    case 2: small_unit<2, false>(d, A, npk, p0, k, G, valid, cam, vo, qs, out12, slot); break;
+                    case 3: small_unit<3, false>(d, A, npk, p0, k, G, valid, cam, vo, qs, out12, slot); break;
+                    default: small_unit<4, false>(d, A, npk, p0, k, G, valid, cam, vo, qs, out12, slot); break;
                 }
             }
         }
@@ -1074,7 +1158,8 @@ struct PipeCfg {
 template <int NS, int NSLOT, bool PRECOND>
 __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
     k_large_pipe(DevProblem d, const TileRef *__restrict__ tiles, const int64_t *__restrict__ cta_lo,
-                 const float *__restrict__ v, float *__restrict__ out, const PcgState *__restrict__ st) {
+                 const float *__restrict__ v, float *__restrict__ out, const PcgState *__restrict__ st,
+                 const int32_t *__restrict__ run_part) {
     using C = PipeCfg<NS, NSLOT>;
     if (!PRECOND && st && st->done) return;
     extern __shared__ __align__(128) unsigned char sm[];
@@ -1148,15 +1233,23 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
     // ---------------- consumers
     const int slot = tid / NS, o = tid % NS, lane = tid & 31, warp = tid >> 5;
     constexpr int NWS = NS / 32;
-    int cur = -1, k = 0, cam = 0, ng = 1, g = 0;
+    int cur = -1, k = 0, cam = 0, ng = 1, g = 0, cur_obs0 = 0;
     bool valid = false;
     float vo[9], acc[9], P[PRECOND ? 45 : 1], b[PRECOND ? 9 : 1];
 #pragma unroll
     for (int q = 0; q < 9; q++) vo[q] = 0.f, acc[q] = 0.f;
+    // deterministic mode: the part index of this consumer run's first landmark (later ones: 0)
+    int part = (d.det && run_part) ? run_part[(int)blockIdx.x * NSLOT + slot] : 0;
     auto flush = [&]() {
         if (cur < 0 || !valid) return;
-        if (PRECOND) flush54(pslice(d) + PACC_STRIDE * (int64_t)cam, P, b);
-        else flush_cam12(wslice(d), cam, acc);
+        if (d.det) {
+            if (PRECOND) det_store54(d, (int64_t)d.slot4[cur_obs0 + o] + part, P, b);
+            else det_store12(d, (int64_t)d.slot5[cur_obs0 + o] + part, acc);
+        } else if (PRECOND) {
+            flush54(pslice(d) + PACC_STRIDE * (int64_t)cam, P, b);
+        } else {
+            flush_cam12(wslice(d), cam, acc);
+        }
     };
     int buf = 0;
     for (int64_t i = 0; i < nst; i++) {
@@ -1169,7 +1262,9 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
             tr = tiles[ti];
             if (tr.lm != cur) {
                 flush();
+                if (cur >= 0) part = 0;  // a landmark that starts in this run
                 cur = tr.lm;
+                cur_obs0 = tr.obs0;
                 k = tr.k;
                 valid = o < k;
                 g = o >> 5;
@@ -1395,11 +1490,15 @@ __global__ void __launch_bounds__(HUGE_FNT, 1) k_huge_fused(DevProblem d, const 
             }
         }
     }
-    float *out = wslice(d);
+    float *out = d.det ? nullptr : wslice(d);
+    const int64_t ob0 = d.lm_obs0[j];
 #pragma unroll
     for (int m = 0; m < HUGE_NB; m++) {
         const int o = tid + m * HUGE_FNT;
-        if (o < k) flush_cam12(out, oc[o], acc[m]);
+        if (o < k) {
+            if (d.det) det_store12(d, (int64_t)d.slot5[ob0 + o] + it.yoff, acc[m]);  // part = item within landmark
+            else flush_cam12(out, oc[o], acc[m]);
+        }
     }
 }
 
@@ -1446,8 +1545,9 @@ __global__ void __launch_bounds__(HUGE_NT) k_huge_out(DevProblem d, float *__res
             for (int q = 0; q < 9; q++) acc[q] += sl[q] * y.x + sl[9 + q] * y.y + sl[18 + q] * y.z + sl[27 + q] * y.w;
         }
     }
-    if (PRECOND) flush54(pslice(d) + PACC_STRIDE * (int64_t)cam, P, b);
-    else flush_cam12(wslice(d), cam, acc);
+    if (PRECOND && d.det) det_store54(d, (int64_t)d.slot4[d.lm_obs0[j] + o] + it.t0 / HUGE_TPO, P, b);
+    else if (PRECOND) flush54(pslice(d) + PACC_STRIDE * (int64_t)cam, P, b);
+    else flush_cam12(wslice(d), cam, acc);  // (two-pass product: not used in deterministic mode)
 }
 
 // FP64 sum over the SM slices (stride `stride` floats per camera, `nv` values used), zeroing them
@@ -1822,7 +1922,10 @@ __global__ void __launch_bounds__(256) k_backsub(DevProblem d) {
     }
     q1 = block_sum_d(q1, red);
     dd = block_sum_d(dd, red);
-    if (threadIdx.x == 0) {
+    if (d.det) {
+        det_grid_sum(q1, d.det_part + DS_Q1R2 * DET_PART, d.det_ctr + DS_Q1R2, d.scal + SC_Q1R2);
+        det_grid_sum(lam * dd, d.det_part + DS_DAMPL * DET_PART, d.det_ctr + DS_DAMPL, d.scal + SC_DAMPL);
+    } else if (threadIdx.x == 0) {
         atomicAdd(d.scal + SC_Q1R2, q1);
         atomicAdd(d.scal + SC_DAMPL, lam * dd);
     }
@@ -1863,10 +1966,9 @@ __global__ void __launch_bounds__(256) k_cost(DevProblem d, const double *__rest
     }
     e = block_sum_d(e, red);
     bad = block_sum_d(bad, red);
-    if (threadIdx.x == 0) {
-        atomicAdd(d.scal + slot, e);
-        if (bad > 0) atomicAdd(d.scal + bad_slot, bad);
-    }
+    if (threadIdx.x == 0 && bad > 0) atomicAdd(d.scal + bad_slot, bad);
+    if (d.det) det_grid_sum(e, d.det_part + DS_ET * DET_PART, d.det_ctr + DS_ET, d.scal + slot);
+    else if (threadIdx.x == 0) atomicAdd(d.scal + slot, e);
 }
 
 // ============================================================================ launchers
@@ -2039,14 +2141,15 @@ static void large_pipe_cls(rba_ctx *c, int cls, const float *v, float *out, cons
     using Cf = PipeCfg<NS, NSLOT>;
     cudaFuncSetAttribute(k_large_pipe<NS, NSLOT, PRE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
     k_large_pipe<NS, NSLOT, PRE><<<(unsigned)n, Cf::NC + 32, Cf::SMEM, ss>>>(
-        c->d, c->d.tiles, c->d.cta_lo + c->cta_off[cls], v, out, st);
+        c->d, c->d.tiles, c->d.cta_lo + c->cta_off[cls], v, out, st, c->d.det ? c->d.run_part + c->run_off[cls] : nullptr);
     c->launches++;
 }
 
 template <bool PRE>
 static void pipes_all(rba_ctx *c, const float *v, float *out12, const PcgState *st) {
     ForkJoin F(c);
-    static const bool fused = !getenv("RBA_HUGE_TWOPASS");
+    static const bool fused_env = !getenv("RBA_HUGE_TWOPASS");
+    const bool fused = fused_env || c->d.det;  // (the two-pass product has no deterministic slots)
     if (c->n_huge_fused > 0 && !PRE && fused) {  // k > KLARGE: fused passes (second read from L2)
         k_huge_fused<<<(unsigned)c->n_huge_fused, HUGE_FNT, 0, F.s()>>>(c->d, c->d.huge_fused, v, st);
         c->launches++;
@@ -2077,6 +2180,14 @@ static void pipes_all(rba_ctx *c, const float *v, float *out12, const PcgState *
 }
 
 static void reduce_slices(rba_ctx *c, float *sl, int stride, int nv, double *out, const PcgState *st) {
+    if (c->d.det) {  // deterministic mode: the camera-major slots, fixed order (family by stride / nv)
+        if (c->d.n_p == 0) return;
+        if (nv == 54) k_det_reduce<54><<<(unsigned)c->d.n_p, 256, 0, c->stream>>>(c->d.obuf, c->d.camptr4, PACC_STRIDE, out, st);
+        else k_det_reduce<9><<<(unsigned)c->d.n_p, 256, 0, c->stream>>>(c->d.obuf, sl == nullptr ? c->d.camptr1 : c->d.camptr5,
+                                                                          12, out, st);
+        c->launches++;
+        return;
+    }
     k_reduce_slices<<<nblk(nv * c->d.n_p, 32), 256, 0, c->stream>>>(sl, c->d.n_p, stride, nv, c->d.nslice, out, st);
     c->launches++;
 }
@@ -2084,7 +2195,7 @@ static void reduce_slices(rba_ctx *c, float *sl, int stride, int nv, double *out
 // K1 camera column norms^2: the per-SM slices into cam_n2d (FP32 path; sqrt-BA-64 adds FP64 directly)
 cudaError_t launch_reduce_cam_norms(rba_ctx *c) {
     if (c->d.s64) launch_reduce_slices64(c, c->d.cam_n2d);
-    else reduce_slices(c, c->d.wsl, 12, 9, c->d.cam_n2d, nullptr);
+    else reduce_slices(c, c->d.det ? nullptr : c->d.wsl, 12, 9, c->d.cam_n2d, nullptr);  // (det: family 1)
     return cudaGetLastError();
 }
 
@@ -2127,6 +2238,10 @@ static bool matvec_body(rba_ctx *c, const float *v, const PcgState *st, bool red
     }
     if (c->d.fac) launch_fac_matvec(c, v, st);
     else pipes_all<false>(c, v, c->d.wsl, st);
+    if (c->d.det) {  // the slots are always reduced here (k_pcg_a then reads wd)
+        reduce_slices(c, c->d.wsl, 12, 9, c->d.wd, st);
+        return false;
+    }
     if (reduce) reduce_slices(c, c->d.wsl, 12, 9, c->d.wd, st);
     return true;
 }

@@ -644,3 +644,10 @@ extern "C" rba_status rba_device_bytes(rba_ctx *c, int64_t *bytes) {
     *bytes = c->device_bytes;
     return RBA_OK;
 }
+
+extern "C" rba_status rba_plan_bytes(rba_ctx *c, double *marginalize_bytes, double *matvec_bytes) {
+    if (!c || !marginalize_bytes || !matvec_bytes) return set_error(RBA_ERR_INVALID_ARG, "null argument");
+    *marginalize_bytes = c->marg_bytes;
+    *matvec_bytes = c->matvec_bytes;
+    return RBA_OK;
+}

@@ -86,6 +86,7 @@ def _load():
         "rba_get_lm": (I, [P, C.POINTER(D), C.POINTER(D), C.POINTER(I64)]),
         "rba_set_pcg_limits": (I, [P, D, I]),
         "rba_device_bytes": (I, [P, C.POINTER(I64)]),
+        "rba_plan_bytes": (I, [P, C.POINTER(D), C.POINTER(D)]),
         "rba_get_state": (I, [P, P, P]),
         "rba_set_state": (I, [P, P, P]),
         "rba_reset_lm": (I, [P]),
@@ -120,7 +121,7 @@ def _load():
 _lib = _load()
 EXPORTED = ["rba_default_options", "rba_create", "rba_destroy", "rba_linearize", "rba_marginalize_qr",
             "rba_pcg_solve", "rba_backsubstitute", "rba_cost", "rba_lm_step", "rba_lm_solve", "rba_get_state",
-            "rba_set_state", "rba_reset_lm", "rba_set_lm", "rba_get_lm", "rba_set_pcg_limits", "rba_device_bytes",
+            "rba_set_state", "rba_reset_lm", "rba_set_lm", "rba_get_lm", "rba_set_pcg_limits", "rba_device_bytes", "rba_plan_bytes",
             "rba_matvec", "rba_get_rhs", "rba_get_step", "rba_get_scaling", "rba_export_block", "rba_arena_bytes",
             "rba_kernel_launches", "rba_profile", "rba_profile_get", "rba_plan_shards", "rba_nccl_unique_id",
             "rba_last_error", "rba_bal_parse", "rba_bal_read", "rba_bal_write", "rba_bal_normalize",
@@ -218,6 +219,12 @@ def rba_device_bytes(h) -> int:
     n = C.c_int64()
     _check(_lib.rba_device_bytes(h, C.byref(n)))
     return n.value
+
+
+def rba_plan_bytes(h):
+    a, b = C.c_double(), C.c_double()
+    _check(_lib.rba_plan_bytes(h, C.byref(a), C.byref(b)))
+    return a.value, b.value
 
 
 def rba_get_state(h, n_cams, n_points, out=None):

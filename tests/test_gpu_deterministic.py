@@ -1,0 +1,95 @@
+"""Deterministic mode (rba_options.deterministic; SURVEY §8b "no float atomics", the paper's
+"parallel reduce"): every camera-space contribution (K1 camera norms, K4 block-Jacobi blocks
+and b~, K5 product) is stored in its own slot and the slots of a camera are summed in a fixed
+order; scalar sums go through per-CTA partials in CTA order.  Two fresh contexts on the same input
+then produce bitwise-identical LM trajectories, and the results match the oracle like the default
+mode does."""
+import numpy as np
+import pytest
+
+import oracle
+from _lm import lm_parity
+from paper_2103_01843_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _solver(p, **kw):
+    from paper_2103_01843_b200.rba import Solver
+    return Solver(p, **kw)
+
+
+def relf(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
+
+
+def _problem(cfg):
+    if cfg == 0:  # every kernel bucket incl. a huge (k > 512) track, whose product and block-Jacobi
+        rng = np.random.default_rng(41)  # pass split into several tile-range items (parts)
+        ks = [2, 3, 4, 5, 8, 9, 16, 17, 33, 65, 129, 257, 600] + list(rng.integers(2, 12, 400))
+        return synth.make_tracks(41, ks, n_p=700)
+    return synth.make_problem(cfg)
+
+
+@pytest.mark.parametrize("cfg", [0, 2, 3])
+def test_bitwise_reproducible_lm(cfg):
+    """Three LM iterations in two fresh deterministic contexts: identical reports and states."""
+    p = _problem(cfg)
+    runs = []
+    for _ in range(2):
+        s = _solver(p, deterministic=1)
+        reps = s.lm_solve(3, 0.0)
+        cams, pts = s.state()
+        runs.append(([(r["cost_after"], r["pcg_iters"], r["rho"], r["lambda_next"]) for r in reps], cams, pts))
+        s.close()
+    assert runs[0][0] == runs[1][0]
+    assert np.array_equal(runs[0][1], runs[1][1]) and np.array_equal(runs[0][2], runs[1][2])
+
+
+@pytest.mark.parametrize("cfg", [0, 2])
+def test_deterministic_reduced_system_matches_oracle(cfg):
+    """H~ probes and b~ of the deterministic path vs the oracle (<= 1e-4), and vs the default path."""
+    p = _problem(cfg)
+    s = _solver(p, deterministic=1)
+    s.linearize()
+    s.marginalize(1e-4)
+    q = _solver(p)
+    q.linearize()
+    q.marginalize(1e-4)
+    o = oracle.Oracle(p)
+    o.linearize()
+    o.marginalize()
+    o.damp(1e-4)
+    sp_d, sp_q = s.scaling()[0], q.scaling()[0]
+    assert relf(sp_d, o.scaling()[0]) <= 1e-5 and relf(sp_d, sp_q) <= 1e-6
+    assert abs(s.cost() - o.cost()) <= 1e-6 * o.cost()
+    rng = np.random.default_rng(cfg)
+    for _ in range(3):
+        v = rng.normal(size=9 * o.n_p)
+        vt = torch.tensor(v, dtype=torch.float32, device="cuda")
+        g = s.matvec(vt).double().cpu().numpy()
+        assert relf(g, o.matvec(v)) <= 1e-4
+        assert relf(g, q.matvec(vt).double().cpu().numpy()) <= 1e-5
+        g2 = s.matvec(vt).double().cpu().numpy()
+        assert np.array_equal(g, g2)  # same context, same input: same bits
+    s.pcg()
+    assert o.precond_rhs() == 0
+    assert relf(s.rhs(), o.rhs()) <= 1e-4
+
+
+def test_deterministic_lm_parity():
+    """Cost after each of 5 LM iterations within 1e-4 of the oracle's (config 2)."""
+    p = synth.make_problem(2)
+    s = _solver(p, deterministic=1)
+    lm_parity(s, oracle.Oracle(p), 5)
+
+
+def test_deterministic_only_for_dense_fp32():
+    from paper_2103_01843_b200.rba import RBAError, RBA_ERR_INVALID_ARG
+    p = synth.make_problem(1)
+    for kw in (dict(storage=1), dict(precision=1), dict(solver=1)):
+        with pytest.raises(RBAError) as e:
+            _solver(p, deterministic=1, **kw)
+        assert e.value.status == RBA_ERR_INVALID_ARG
