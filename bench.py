@@ -180,9 +180,9 @@ def compose_oracle(t, iters):
 
 
 def oracle_trajectory(cfg):
-    """The oracle's own LM trajectory on this config (profiles/oracle_cfg<C>_lm*.json, written by
+    """The oracle's own LM trajectory on this config (tests/oracle_data/cfg<C>_lm*.json, written by
     tools/oracle_trajectory.py, which calls only oracle/)."""
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"oracle_cfg{cfg}_lm*.json")))
+    files = sorted(glob.glob(os.path.join(ROOT, "tests", "oracle_data", f"cfg{cfg}_lm*.json")))
     if not files:
         return None
     d = json.load(open(files[-1]))

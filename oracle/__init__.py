@@ -84,6 +84,7 @@ def lib():
             "orc_get_givens": (None, [P, I64, P]),
             "orc_get_rhs": (None, [P, P]),
             "orc_get_precond_factor": (None, [P, P]),
+            "orc_block_arena": (None, [P, C.POINTER(C.c_void_p), P]),
             "orc_get_dp": (None, [P, P]),
             "orc_set_dp": (None, [P, P]),
             "orc_get_rho_cg": (None, [P, P]),
@@ -272,6 +273,19 @@ class Oracle:
         b = np.zeros(9 * self.n_p)
         lib().orc_get_rhs(self.h, _p(b))
         return b
+
+    def block_arena(self):
+        """(arena, offsets): a zero-copy read-only numpy view of every landmark block (landmark j at
+        arena[offsets[j]:offsets[j+1]], row-major (2k+3) x (9k+4)); valid until the next
+        linearization and while this Oracle lives."""
+        ptr = C.c_void_p()
+        off = np.zeros(self.n_l + 1, np.int64)
+        lib().orc_block_arena(self.h, C.byref(ptr), _p(off))
+        if not ptr.value:
+            raise RuntimeError("oracle: no landmark blocks (linearize first)")
+        arr = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_double)), shape=(int(off[-1]),))
+        arr.flags.writeable = False
+        return arr, off
 
     def precond_blocks(self):
         """The block-Jacobi blocks P_i (n_p x 9 x 9) as L_i L_i^T from the stored Cholesky factors."""

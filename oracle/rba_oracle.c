@@ -858,6 +858,12 @@ void orc_get_block(orc_ctx *c, int64_t j, double *buf) {
 }
 void orc_get_givens(orc_ctx *c, int64_t j, double *g) { memcpy(g, c->giv + 12 * j, sizeof(double) * 12); }
 void orc_get_rhs(orc_ctx *c, double *b) { memcpy(b, c->bt, sizeof(double) * DP * c->n_p); }
+/* Read-only view of the landmark-block arena: *ptr = first double, offsets[j] = start of landmark j
+ * (n_l + 1 entries, caller buffer); valid until the next linearization. */
+void orc_block_arena(orc_ctx *c, const double **ptr, int64_t *offsets) {
+    *ptr = c->blk;
+    memcpy(offsets, c->blk_off, sizeof(int64_t) * (c->n_l + 1));
+}
 /* Cholesky factors L_i (lower, row-major, 81 per camera) of the block-Jacobi blocks of orc_precond_rhs */
 void orc_get_precond_factor(orc_ctx *c, double *L) { memcpy(L, c->Lp, sizeof(double) * 81 * c->n_p); }
 void orc_get_dp(orc_ctx *c, double *dp) { memcpy(dp, c->dp, sizeof(double) * DP * c->n_p); }

@@ -71,3 +71,40 @@ def _blocks_bar(errs):
 
 def _lm_sp(sp, cams):
     return np.concatenate([sp[9 * c:9 * c + 9] for c in cams])
+
+
+def oracle_reduced_dense(o, lam):
+    """H~ = sum_j A_j^T A_j + lam D_p^2 and b~ = sum_j A_j^T q_j (Eq. cg_mult; the
+    definition), assembled with numpy BLAS from the oracle's marginalized + damped landmark blocks
+    (a read-only view of its block arena), landmarks of equal track length batched.  The oracle's
+    own orc_reduced_dense is the same sum, pinned on small problems against the explicit Schur
+    complement, but too slow for configs 3-4."""
+    N = 9 * o.n_p
+    H = np.zeros((N, N))
+    b = np.zeros(N)
+    arena, off = o.block_arena()
+    lp, cc = o.lm_ptr, o.csr_cam
+    k_all = np.diff(lp)
+    for k in np.unique(k_all):
+        k = int(k)
+        js = np.flatnonzero(k_all == k)
+        R, W = 2 * k + 3, 9 * k + 4
+        for c0 in range(0, js.size, max(1, (1 << 27) // (R * W))):  # chunks of <= 1 GB
+            jj = js[c0:c0 + max(1, (1 << 27) // (R * W))]
+            X = arena[off[jj][:, None] + np.arange(R * W)[None, :]].reshape(jj.size, R, W)
+            A, q = np.ascontiguousarray(X[:, 3:, :9 * k]), np.ascontiguousarray(X[:, 3:, -1])
+            G = np.matmul(A.transpose(0, 2, 1), A)  # (contiguous operands: one BLAS call per landmark)
+            g = np.matmul(A.transpose(0, 2, 1), q[:, :, None])[:, :, 0]
+            cams = cc[lp[jj][:, None] + np.arange(k)[None, :]]
+            for n in range(jj.size):
+                c = cams[n]
+                if c[-1] - c[0] == k - 1:  # consecutive cameras (the street geometry): a dense slice
+                    s0 = 9 * int(c[0])
+                    H[s0:s0 + 9 * k, s0:s0 + 9 * k] += G[n]
+                    b[s0:s0 + 9 * k] += g[n]
+                else:
+                    idx = (9 * c[:, None] + np.arange(9)).ravel()
+                    H[np.ix_(idx, idx)] += G[n]
+                    b[idx] += g[n]
+    H[np.diag_indices(N)] += lam * o.scaling()[1]
+    return H, b

@@ -1,9 +1,10 @@
 """The FP64 oracle's own LM trajectory on a full BASELINE config (test / measurement infrastructure:
 calls only oracle/ and the seeded generator).  Writes, after every iteration, the oracle's report
 (cost after the decision, PCG iterations and reason, accept, lambda) to
-profiles/oracle_cfg<C>_lm<N>.json.  bench.py's reference arm composes the oracle's per-phase times
-measured on the full workload with these iteration counts, and the full-size parity
-notes compare the GPU's trajectory with it.
+tests/oracle_data/cfg<C>_lm<N>.json.  The full-size GPU parity test replays these iterations at the
+oracle's PCG counts and compares the costs (tests/test_gpu_fullsize.py), and bench.py's reference
+arm composes the oracle's per-phase times measured on the full workload with these iteration
+counts.
 
     OMP_NUM_THREADS=6 nice -n 19 python tools/oracle_trajectory.py --config 4 --iters 20
 """
@@ -23,7 +24,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=4)
 ap.add_argument("--iters", type=int, default=20)
 a = ap.parse_args()
-out = os.path.join(ROOT, "profiles", f"oracle_cfg{a.config}_lm{a.iters}.json")
+out = os.path.join(ROOT, "tests", "oracle_data", f"cfg{a.config}_lm{a.iters}.json")
 p = synth.make_problem(a.config)
 o = oracle.Oracle(p)
 rec = {"config": a.config, "digest": synth.digest(p), "lambda0": 1e-4, "pcg_tol": 1e-2, "pcg_max": 500,
