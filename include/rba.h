@@ -220,6 +220,22 @@ rba_status rba_arena_bytes(rba_ctx *ctx, int64_t *logical, int64_t *physical);
 /* Number of this library's kernel launches so far (kernel nodes executed inside CUDA graphs
  * included, counted per executed conditional branch / loop iteration). */
 rba_status rba_kernel_launches(rba_ctx *ctx, int64_t *count);
+/* Execution facts of a context (for tests and the benchmark line). */
+typedef struct {
+    int lm_graph;          /* 1: LM iterations run as one CUDA graph; 0: eager (host-driven); -1: the
+                              graph failed to build / instantiate and the eager path is used     */
+    int pcg_graph;         /* the same for the step-by-step rba_pcg_solve                          */
+    int nccl;              /* 1: an NCCL communicator is attached (all-reduces issued)              */
+    int deterministic;
+    int64_t n_landmarks;   /* landmarks of this rank's shard                                       */
+    int64_t n_observations;
+} rba_info;
+rba_status rba_get_info(rba_ctx *ctx, rba_info *info);
+/* 64-bit FNV-1a checksums of the bit patterns of the camera-space vectors every rank must hold
+ * identically after their all-reduces (SURVEY §8e lockstep): [0] the camera column norms^2 of the
+ * last linearization, [1] the block-Jacobi partials + b~ of the last preconditioner pass, [2] the
+ * last product wd, [3] the PCG solution dp.  Synchronizes. */
+rba_status rba_checksums(rba_ctx *ctx, uint64_t out[4]);
 /* Device memory held by the context (bytes of every buffer it allocated). */
 rba_status rba_device_bytes(rba_ctx *ctx, int64_t *bytes);
 /* Algorithmic bytes of one marginalization (K2: the landmark blocks written + the

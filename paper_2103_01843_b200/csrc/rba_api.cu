@@ -385,6 +385,7 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
             const int nr = (packs[p0 + sl].k + 3) / 4;
             for (int r = 0; r < nr; r++) units.push_back((uint16_t)(sl | (r << 8)));
         }
+        ch.nreal = (int32_t)(units.size() - ch.unit0);
         while ((units.size() - ch.unit0) % 8) units.push_back(0xFFFF);
         ch.nunit = (int32_t)(units.size() - ch.unit0);
         chunks.push_back(ch);
@@ -768,6 +769,8 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
         c->marg_bytes = (double)ts * 81 * d.nnzb + 48.0 * nobs_loc;
     }
     CKSC(dalloc_n(c, &d.arena, c->arena_floats));
+    d.arena_n = c->arena_floats;
+    for (int F = 0; F < 3; F++) d.n_slots[F] = n_slots[F];
     {
         int nsm = 0;
         CKSC(dalloc_n(c, &d.pcg, 1));
@@ -914,7 +917,9 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
             return bail(RBA_ERR_BAD_PROBLEM);
         }
     }
-    if (opt.world > 1 && opt.nccl_unique_id) {
+    // world == 1 with an id: a one-rank communicator, so the sharded code path (all-reduces between
+    // product and update, captured into the LM graph) runs for real on one GPU
+    if (opt.nccl_unique_id) {
         ncclUniqueId id;
         std::memcpy(&id, opt.nccl_unique_id, sizeof(id));
         ncclResult_t r = ncclCommInitRank(&c->comm, opt.world, id, opt.rank);

@@ -12,6 +12,20 @@
 
 namespace rba {
 
+// RBA_CHECKS build (tools/checked_build.py): device-side bounds checks on the staged / indexed
+// accesses of the kernels (compute-sanitizer is closed on this pool); a failed check traps, the
+// context's next call reports a CUDA error.
+#ifdef RBA_CHECKS
+#define RBA_CHECK(cond)              \
+    do {                             \
+        if (!(cond)) __trap();       \
+    } while (0)
+#else
+#define RBA_CHECK(cond) \
+    do {                \
+    } while (0)
+#endif
+
 constexpr int KSMALL = 16;    // k <= KSMALL: warp-group kernels over packs of same-k landmarks
 constexpr int KLARGE = 512;   // k <= KLARGE: one thread per camera block in the large-k kernels
 constexpr int KMAX = 3072;    // largest track length supported (k > KLARGE: "huge" path, smem-bound)
@@ -75,10 +89,13 @@ struct SmallChunk {
     int32_t unit0;           // units[unit0 .. unit0 + nunit) (nunit a multiple of 8, 0xFFFF = none)
     int32_t nunit;
     int32_t q0, nq;          // qpk[q0 .. q0 + nq): 16-byte aligned superset of the packs' q (K4 only)
-    int32_t pad2;
+    int32_t nreal;           // units before the 0xFFFF padding
 };
 constexpr int PACC_STRIDE = 56;             // per-camera slot of the preconditioner accumulator
-constexpr int SMALL_STAGE_BYTES = 40 * 1024;  // >= largest pack (k = 16, np = 2: 36,864 B)
+#ifndef RBA_SP_STAGE_KB
+#define RBA_SP_STAGE_KB 40
+#endif
+constexpr int SMALL_STAGE_BYTES = RBA_SP_STAGE_KB * 1024;  // >= largest pack (k = 16, np = 2: 36,864 B)
 constexpr int SP_QCAP = 640;                   // q floats per small-pipe stage (K4; host guarantees)
 
 struct PcgState {
@@ -217,6 +234,8 @@ struct DevProblem {
     // row-pair units of a small-k pack, the consumer runs a long track's tiles are split over, the
     // tile ranges of a huge track).  Scalar FP64 sums use per-CTA partials summed in CTA order.
     int det;
+    int64_t arena_n;         // floats of the arena (bounds checks of the RBA_CHECKS build)
+    int64_t n_slots[3];      // deterministic mode: slots of families 1, 4, 5
     float *obuf;
     int32_t *slot1, *slot4, *slot5;
     int64_t *camptr1, *camptr4, *camptr5;

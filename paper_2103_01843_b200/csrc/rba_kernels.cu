@@ -36,12 +36,14 @@ namespace rba {
 // (rba_options.deterministic).  A camera-space contribution goes to its own slot
 // (plain stores, no atomics); k_det_reduce adds the slots of a camera in a fixed order.
 __device__ __forceinline__ void det_store12(const DevProblem &d, int64_t slot, const float *acc) {
+    RBA_CHECK(slot >= 0 && 12 * slot + 12 <= 56 * d.n_slots[1] + 12 * (d.n_slots[2] + d.n_slots[0]));
     float4 *o4 = reinterpret_cast<float4 *>(d.obuf + 12 * slot);
     o4[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
     o4[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
     o4[2] = make_float4(acc[8], 0.f, 0.f, 0.f);
 }
 __device__ __forceinline__ void det_store54(const DevProblem &d, int64_t slot, const float *P, const float *b) {
+    RBA_CHECK(slot >= 0 && slot < d.n_slots[1]);
     float4 *a4 = reinterpret_cast<float4 *>(d.obuf + (int64_t)PACC_STRIDE * slot);
 #pragma unroll
     for (int i = 0; i < 11; i++) a4[i] = make_float4(P[4 * i], P[4 * i + 1], P[4 * i + 2], P[4 * i + 3]);
@@ -473,6 +475,8 @@ __global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProb
     float *blk_side = sside + grp * (int)side_floats(k);
     if (act) {
     float2 *A = reinterpret_cast<float2 *>(d.arena + pack.base);
+    RBA_CHECK(pack.base >= 0 && pack.base + small_pack_floats(k, pack.np) <= d.arena_n && d.lm_side[pack.lm0] +
+              pack.np * side_floats(k) <= d.arena_n);
     const int npk = pack.np * k, mo = grp * k + gl;
     float2 *Ap = A + mo;
     for (int p = 0; p < k; p++, Ap += 9 * npk) {
@@ -978,6 +982,9 @@ constexpr int SP_SB = SP_OFF_HDR + 128;
 #ifndef RBA_YRED_SHFL
 #define RBA_YRED_SHFL 1  // y reduction by xor butterfly (measured 2.54 -> 2.47 ms cfg4 matvec)
 #endif
+#ifndef RBA_PF_AHEAD
+#define RBA_PF_AHEAD 0  // stages prefetched into L2 beyond the shared-memory ring (measured: slower, 0.29 -> 0.52 ms cfg3)
+#endif
 #ifndef RBA_PIPE_SMEM
 #define RBA_PIPE_SMEM 225000  // 3 stages of 4 x 512 x 36-byte tiles (measured +2.3% over 200 KB)
 #endif
@@ -1059,11 +1066,27 @@ __global__ void __launch_bounds__(SP_WARPS * 32 + 32, 1)
             const uint64_t pol = policy_evict_first();
             SmallChunk nxc{};
             if (lo < hi) nxc = d.chunks[lo];
+            // the consumers wait on the TMA data (ncu: the full-barrier wait is the top stall): keep
+            // RBA_PF_AHEAD more stages in flight as L2 prefetches beyond the shared-memory ring
+            int64_t pf_base = 0;
+            int pf_bytes = 0;
+            if (RBA_PF_AHEAD && lo + RBA_PF_AHEAD < hi) pf_base = d.chunks[lo + RBA_PF_AHEAD].base, pf_bytes = d.chunks[lo + RBA_PF_AHEAD].bytes;
             for (int64_t i = lo; i < hi; i++) {
                 const int s = (int)((i - lo) % SP_STAGES);
                 const uint32_t ph = (uint32_t)(((i - lo) / SP_STAGES) & 1);
                 const SmallChunk ch = nxc;
                 if (i + 1 < hi) nxc = d.chunks[i + 1];  // prefetch the next stage's descriptor
+                RBA_CHECK(ch.bytes <= SMALL_STAGE_BYTES && ch.ncam <= SP_CAMCAP && ch.np <= SP_PACKCAP &&
+                          ch.nunit <= SP_UNITCAP && (!PRECOND || ch.nq <= SP_QCAP) && ch.base >= 0 &&
+                          ch.base + ch.bytes / 4 <= d.arena_n && ch.cam0 >= 0 && ch.cam0 + ch.ncam <= d.n_obs + 8);
+                if (RBA_PF_AHEAD && pf_bytes) {
+                    bulk_prefetch_l2(d.arena + pf_base, (uint32_t)pf_bytes);
+                    pf_bytes = 0;
+                    if (i + 1 + RBA_PF_AHEAD < hi) {
+                        const SmallChunk &pc = d.chunks[i + 1 + RBA_PF_AHEAD];
+                        pf_base = pc.base, pf_bytes = pc.bytes;
+                    }
+                }
                 mbar_wait(&empty[s], ph ^ 1);
                 *reinterpret_cast<SmallChunk *>(sm + (size_t)s * SP_SB + SP_OFF_HDR) = ch;
                 mbar_arrive_expect_tx(&full[s], (uint32_t)ch.bytes + 4u * (uint32_t)ch.ncam +
@@ -1079,6 +1102,11 @@ __global__ void __launch_bounds__(SP_WARPS * 32 + 32, 1)
         }
         return;
     }
+    // Work items (K5: the units of a stage; K4: its packs) are dealt to the consumer warps round
+    // robin over the concatenation of all stages (item n of the sequence -> warp n mod SP_WARPS), so
+    // every warp has work although a stage holds only a few items (1-8 for k >= 8); warps run up
+    // to SP_STAGES stages apart.
+    int base = 0;  // items of the previous stages, mod SP_WARPS
     for (int64_t i = lo; i < hi; i++) {
         const int s = (int)((i - lo) % SP_STAGES);
         const uint32_t ph = (uint32_t)(((i - lo) / SP_STAGES) & 1);
@@ -1088,25 +1116,31 @@ __global__ void __launch_bounds__(SP_WARPS * 32 + 32, 1)
         const uint16_t *sun = reinterpret_cast<const uint16_t *>(stg + SP_OFF_UNIT);
         mbar_wait(&full[s], ph);
         const SmallChunk ch = *reinterpret_cast<const SmallChunk *>(stg + SP_OFF_HDR);
-        for (int ui = warp; ui < (dbg == 1 ? 0 : ch.nunit); ui += SP_WARPS) {
-            const int code = sun[ui];
-            if (code == 0xFFFF) continue;
+        const int nitems = dbg == 1 ? 0 : (PRECOND ? ch.np : ch.nreal);
+        int first = warp - base;
+        if (first < 0) first += SP_WARPS;
+        base = (base + nitems) % SP_WARPS;
+        for (int wi = first; wi < nitems; wi += SP_WARPS) {
+            const int code = PRECOND ? wi : sun[wi];
             const Pack pack = spk[code & 255];
-            const int p0 = 4 * (code >> 8);
+            const int p0 = PRECOND ? 0 : 4 * (code >> 8);
             const int k = pack.k;
             const int G = group_of(k);
             const int m = lane / G, o = lane % G;
             const bool valid = m < pack.np && o < k;
             const int npk = pack.np * k, mo = m * k + o;
             const float2 *A = reinterpret_cast<const float2 *>(stg + 4 * (pack.base - ch.base)) + mo;
+            RBA_CHECK(pack.base >= ch.base && 4 * (pack.base - ch.base + small_pack_floats(k, pack.np)) <= ch.bytes);
+            RBA_CHECK(!valid || (pack.obs0 - ch.cam0 + mo >= 0 && pack.obs0 - ch.cam0 + mo < ch.ncam));
+            RBA_CHECK(!PRECOND || !valid || (pack.q0 - ch.q0 + 2 * k * m >= 0 && pack.q0 - ch.q0 + 2 * k * (m + 1) <= ch.nq));
             const int cam = valid ? scam[pack.obs0 - ch.cam0 + mo] : 0;
             float vo[9];
 #pragma unroll
             for (int q = 0; q < 9; q++) vo[q] = (valid && !PRECOND) ? vv[9 * cam + q] : 0.f;
             // K4: the landmark's q from the staged copy, row a at qs[a - 3]
             const float *qs = reinterpret_cast<const float *>(stg + SP_OFF_Q) + (pack.q0 - ch.q0) + 2 * k * m;
-            if (PRECOND) {  // the pack's first unit takes all its row pairs: one flush per (landmark, camera)
-                if (p0 != 0 || !valid) continue;
+            if (PRECOND) {  // a warp takes all row pairs of a pack: one flush per (landmark, camera)
+                if (!valid) continue;
                 float P[45], b[9];
 #pragma unroll
                 for (int q = 0; q < 45; q++) P[q] = 0.f;
@@ -1191,16 +1225,31 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
                 const TileRef tr = tiles[ti];
                 return d.lm_side[tr.lm] + side_tl(tr.k) + 4 * (3 + 4 * (int64_t)tr.t);
             };
+            // tiles of stage i + RBA_PF_AHEAD (per slot), prefetched into L2 beyond the ring
+            int64_t poff[NSLOT];
+            int pk[NSLOT];
 #pragma unroll
             for (int sl = 0; sl < NSLOT; sl++) {
                 const int64_t ti = lo + sl * nst;
                 nk[sl] = ti < hi ? tiles[ti].k : 0;
                 noff[sl] = ti < hi ? tiles[ti].off : 0;
                 ntl[sl] = tl_off(ti);
+                const int64_t tp = ti + RBA_PF_AHEAD;
+                pk[sl] = (RBA_PF_AHEAD && RBA_PF_AHEAD < nst && tp < hi) ? tiles[tp].k : 0;
+                poff[sl] = pk[sl] ? tiles[tp].off : 0;
             }
             for (int64_t i = 0; i < nst; i++) {
                 const int s = (int)(i % C::STAGES);
                 const uint32_t ph = (uint32_t)((i / C::STAGES) & 1);
+                if (RBA_PF_AHEAD) {
+#pragma unroll
+                    for (int sl = 0; sl < NSLOT; sl++) {
+                        if (pk[sl]) bulk_prefetch_l2(d.arena + poff[sl], 144u * (uint32_t)pk[sl]);
+                        const int64_t tp = lo + sl * nst + i + 1 + RBA_PF_AHEAD;
+                        pk[sl] = (i + 1 + RBA_PF_AHEAD < nst && tp < hi) ? tiles[tp].k : 0;
+                        poff[sl] = pk[sl] ? tiles[tp].off : 0;
+                    }
+                }
                 int64_t coff[NSLOT], ctl[NSLOT];
                 int ck[NSLOT];
                 uint32_t total = 0;
@@ -1216,6 +1265,8 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
                     ntl[sl] = tl_off(tn);
                 }
                 mbar_wait(&empty[s], ph ^ 1);
+#pragma unroll
+                for (int sl = 0; sl < NSLOT; sl++) RBA_CHECK(ck[sl] <= NS && coff[sl] >= 0 && coff[sl] + 36 * ck[sl] <= d.arena_n);
                 mbar_arrive_expect_tx(&full[s], total);
 #pragma unroll
                 for (int sl = 0; sl < NSLOT; sl++)

@@ -28,6 +28,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "rba_internal.cuh"
 
@@ -649,5 +650,37 @@ extern "C" rba_status rba_plan_bytes(rba_ctx *c, double *marginalize_bytes, doub
     if (!c || !marginalize_bytes || !matvec_bytes) return set_error(RBA_ERR_INVALID_ARG, "null argument");
     *marginalize_bytes = c->marg_bytes;
     *matvec_bytes = c->matvec_bytes;
+    return RBA_OK;
+}
+
+extern "C" rba_status rba_get_info(rba_ctx *c, rba_info *info) {
+    if (!c || !info) return set_error(RBA_ERR_INVALID_ARG, "null argument");
+    memset(info, 0, sizeof(*info));
+    info->lm_graph = c->lmg.failed ? -1 : (c->lmg.exec ? 1 : 0);
+    info->pcg_graph = c->pcg_graph_failed ? -1 : (c->pcg_exec ? 1 : 0);
+    info->nccl = c->have_comm ? 1 : 0;
+    info->deterministic = c->d.det;
+    info->n_landmarks = c->d.n_l;
+    info->n_observations = c->d.n_obs;
+    return RBA_OK;
+}
+
+static uint64_t fnv1a(const void *p, size_t n, uint64_t h = 1469598103934665603ull) {
+    const unsigned char *b = static_cast<const unsigned char *>(p);
+    for (size_t i = 0; i < n; i++) h = (h ^ b[i]) * 1099511628211ull;
+    return h;
+}
+
+extern "C" rba_status rba_checksums(rba_ctx *c, uint64_t out[4]) {
+    if (!c || !out) return set_error(RBA_ERR_INVALID_ARG, "null argument");
+    const int64_t np = c->d.n_p;
+    std::vector<double> buf(54 * std::max<int64_t>(np, 1));
+    const double *src[4] = {c->d.cam_n2d, c->d.pd, c->d.wd, c->d.x};
+    const int64_t cnt[4] = {9 * np, 54 * np, 9 * np, 9 * np};
+    for (int i = 0; i < 4; i++) {
+        CKE(cudaMemcpyAsync(buf.data(), src[i], sizeof(double) * cnt[i], cudaMemcpyDeviceToHost, c->stream));
+        CKE(cudaStreamSynchronize(c->stream));
+        out[i] = fnv1a(buf.data(), sizeof(double) * cnt[i]);
+    }
     return RBA_OK;
 }

@@ -37,6 +37,11 @@ RBA_STORAGE_DENSE, RBA_STORAGE_FACTORED = 0, 1
 RBA_SOLVER_SQRTBA, RBA_SOLVER_EXPLICIT_SC32, RBA_SOLVER_EXPLICIT_SC64 = 0, 1, 2
 
 
+class rba_info(C.Structure):
+    _fields_ = [("lm_graph", C.c_int), ("pcg_graph", C.c_int), ("nccl", C.c_int), ("deterministic", C.c_int),
+                ("n_landmarks", C.c_int64), ("n_observations", C.c_int64)]
+
+
 class rba_pcg_stats(C.Structure):
     _fields_ = [("iters", C.c_int), ("reason", C.c_int), ("rel_residual", C.c_double)]
 
@@ -87,6 +92,8 @@ def _load():
         "rba_set_pcg_limits": (I, [P, D, I]),
         "rba_device_bytes": (I, [P, C.POINTER(I64)]),
         "rba_plan_bytes": (I, [P, C.POINTER(D), C.POINTER(D)]),
+        "rba_get_info": (I, [P, C.POINTER(rba_info)]),
+        "rba_checksums": (I, [P, C.POINTER(C.c_uint64)]),
         "rba_get_state": (I, [P, P, P]),
         "rba_set_state": (I, [P, P, P]),
         "rba_reset_lm": (I, [P]),
@@ -121,7 +128,7 @@ def _load():
 _lib = _load()
 EXPORTED = ["rba_default_options", "rba_create", "rba_destroy", "rba_linearize", "rba_marginalize_qr",
             "rba_pcg_solve", "rba_backsubstitute", "rba_cost", "rba_lm_step", "rba_lm_solve", "rba_get_state",
-            "rba_set_state", "rba_reset_lm", "rba_set_lm", "rba_get_lm", "rba_set_pcg_limits", "rba_device_bytes", "rba_plan_bytes",
+            "rba_set_state", "rba_reset_lm", "rba_set_lm", "rba_get_lm", "rba_set_pcg_limits", "rba_device_bytes", "rba_plan_bytes", "rba_get_info", "rba_checksums",
             "rba_matvec", "rba_get_rhs", "rba_get_step", "rba_get_scaling", "rba_export_block", "rba_arena_bytes",
             "rba_kernel_launches", "rba_profile", "rba_profile_get", "rba_plan_shards", "rba_nccl_unique_id",
             "rba_last_error", "rba_bal_parse", "rba_bal_read", "rba_bal_write", "rba_bal_normalize",
@@ -225,6 +232,18 @@ def rba_plan_bytes(h):
     a, b = C.c_double(), C.c_double()
     _check(_lib.rba_plan_bytes(h, C.byref(a), C.byref(b)))
     return a.value, b.value
+
+
+def rba_get_info(h) -> dict:
+    i = rba_info()
+    _check(_lib.rba_get_info(h, C.byref(i)))
+    return {k: getattr(i, k) for k, _ in i._fields_}
+
+
+def rba_checksums(h) -> list:
+    out = (C.c_uint64 * 4)()
+    _check(_lib.rba_checksums(h, out))
+    return list(out)
 
 
 def rba_get_state(h, n_cams, n_points, out=None):
@@ -489,6 +508,12 @@ class Solver:
 
     def set_pcg_limits(self, rel_tol, max_iters):
         rba_set_pcg_limits(self.h, rel_tol, max_iters)
+
+    def info(self):
+        return rba_get_info(self.h)
+
+    def checksums(self):
+        return rba_checksums(self.h)
 
     def state(self, out=None):
         return rba_get_state(self.h, self.n_p, self.n_l, out)

@@ -93,3 +93,25 @@ def test_deterministic_only_for_dense_fp32():
         with pytest.raises(RBAError) as e:
             _solver(p, deterministic=1, **kw)
         assert e.value.status == RBA_ERR_INVALID_ARG
+
+
+@pytest.mark.parametrize("cfg", [0, 2])
+def test_no_reads_of_unwritten_memory(cfg):
+    """Stale-memory check (compute-sanitizer's initcheck is closed on this pool): every device
+    allocation of a second context comes from torch's caching allocator right after 8 GB of it
+    were filled with NaN; in deterministic mode its LM trajectory, state and the checksums of the
+    camera-space vectors must equal a first run's bit for bit, so no kernel reads memory it did not
+    write (a NaN would propagate, any other stale value would change the bits)."""
+    p = _problem(cfg)
+    runs = []
+    for poison in (False, True):
+        if poison:
+            x = torch.full((2 << 30,), float("nan"), device="cuda", dtype=torch.float32)
+            del x
+        s = _solver(p, deterministic=1)
+        reps = s.lm_solve(3, 0.0)
+        runs.append(([r["cost_after"] for r in reps], s.state(), s.checksums()))
+        s.close()
+    assert runs[0][0] == runs[1][0] and all(np.isfinite(runs[1][0]))
+    assert np.array_equal(runs[0][1][0], runs[1][1][0]) and np.array_equal(runs[0][1][1], runs[1][1][1])
+    assert runs[0][2] == runs[1][2]

@@ -248,6 +248,30 @@ def test_lm_on_the_multi_gpu_pcg_path(monkeypatch, storage, graph):
     lm_parity(s, o, 4)
 
 
+@pytest.mark.parametrize("det", [0, 1])
+def test_lm_with_one_rank_nccl(det):
+    """The sharded code path with a real NCCL communicator on one GPU (a one-rank communicator:
+    every all-reduce of SURVEY §8e is issued through NCCL -- camera norms, preconditioner partials,
+    the product of every PCG iteration, the trial scalars -- inside the device-side LM graph when
+    NCCL captures into its conditional bodies, else eagerly): costs of 4 LM iterations within 1e-4
+    of the oracle's; the all-reduced vectors' checksums are reproducible in deterministic mode."""
+    from paper_2103_01843_b200 import rba
+    p = synth.make_problem(2)
+    s = _solver(p, world=1, nccl_id=rba.rba_nccl_unique_id(), deterministic=det)
+    assert s.info()["nccl"] == 1
+    lm_parity(s, oracle.Oracle(p), 4)
+    info = s.info()
+    assert info["lm_graph"] in (1, -1), info
+    print("one-rank NCCL: LM graph", info["lm_graph"])
+    if det:
+        q = _solver(p, world=1, nccl_id=rba.rba_nccl_unique_id(), deterministic=1)
+        s.set_state(p["cameras_init"], p["points_init"])
+        s.reset_lm()
+        a = [s.lm_step()["cost_after"] for _ in range(2)]
+        b = [q.lm_step()["cost_after"] for _ in range(2)]
+        assert a == b and s.checksums() == q.checksums()
+
+
 def test_state_io_round_trip_and_lm_state():
     """rba_set_state / rba_get_state (the device-side landmark permutation between the caller's
     order and the internal k-sorted order) are exact, including on landmark shards; after LM
