@@ -204,6 +204,11 @@ rba_status rba_set_pcg_limits(rba_ctx *ctx, double rel_tol, int max_iters);
 rba_status rba_matvec(rba_ctx *ctx, const float *v_dev, float *out_dev);
 /* b~ = sum_j A_j^T q_j (host FP64, 9 n_cams), valid after rba_pcg_solve. */
 rba_status rba_get_rhs(rba_ctx *ctx, double *b);
+/* The camera-space sums of the last preconditioner pass (host FP64, n_cams x 54): the 45 upper-
+ * triangle entries (row-major, i <= j) of sum_j A_j[:,i]^T A_j[:,i] (the block-Jacobi block of
+ * camera i without lambda D_p^2) followed by the 9 entries of b~_i.  Valid after
+ * rba_pcg_solve. */
+rba_status rba_get_precond(rba_ctx *ctx, double *blocks);
 /* scaled steps dp (9 n_cams) and dl (3 n_points, caller's landmark order; entries of landmarks
  * owned by other ranks are 0). */
 rba_status rba_get_step(rba_ctx *ctx, double *dp, double *dl);

@@ -85,6 +85,8 @@ def lib():
             "orc_get_rhs": (None, [P, P]),
             "orc_get_precond_factor": (None, [P, P]),
             "orc_block_arena": (None, [P, C.POINTER(C.c_void_p), P]),
+            "orc_set_streaming": (None, [P, I]),
+            "orc_products": (None, [P, I, P, P]),
             "orc_get_dp": (None, [P, P]),
             "orc_set_dp": (None, [P, P]),
             "orc_get_rho_cg": (None, [P, P]),
@@ -273,6 +275,18 @@ class Oracle:
         b = np.zeros(9 * self.n_p)
         lib().orc_get_rhs(self.h, _p(b))
         return b
+
+    def set_streaming(self, on=True):
+        """Streaming mode (no block arena: every block is recomputed, O3-O5, where it is read) for
+        problems whose FP64 blocks do not fit in host memory (config 5).  Relinearizes next."""
+        lib().orc_set_streaming(self.h, int(bool(on)))
+
+    def products(self, V):
+        """H~ v for the rows v of V (nvec x 9 n_p) in one pass over the landmarks."""
+        V = np.ascontiguousarray(np.atleast_2d(V), np.float64)
+        out = np.zeros_like(V)
+        lib().orc_products(self.h, V.shape[0], _p(V), _p(out))
+        return out
 
     def block_arena(self):
         """(arena, offsets): a zero-copy read-only numpy view of every landmark block (landmark j at

@@ -77,6 +77,12 @@ typedef struct {
     double huber;
     int need_linearize;
     int64_t iteration;
+    /* streaming mode (SURVEY §8c "Oracle capacity"): no block arena; every operation that reads a
+     * landmark block re-assembles, re-factorizes and re-damps it (O3-O5) in a per-thread scratch,
+     * identical arithmetic, O(threads) memory -- for problems whose FP64 blocks do not fit in host
+     * memory (config 5: 263 GB). */
+    int streaming;
+    int64_t max_block; /* doubles of the largest block */
 } orc_ctx;
 
 typedef struct {
@@ -303,6 +309,7 @@ orc_ctx *orc_create(const double *cams, int64_t n_p, const double *pts, int64_t 
     for (int64_t j = 0; j < n_l; j++) {
         int64_t k = c->lm_ptr[j + 1] - c->lm_ptr[j];
         c->blk_off[j + 1] = c->blk_off[j] + (2 * k + 3) * (DP * k + 4); /* P:645 */
+        if ((2 * k + 3) * (DP * k + 4) > c->max_block) c->max_block = (2 * k + 3) * (DP * k + 4);
     }
     c->blk = NULL; /* allocated by the first orc_linearize (orc_scaling needs no blocks) */
     c->giv = calloc(12 * n_l, sizeof(double));
@@ -409,33 +416,115 @@ int orc_scaling(orc_ctx *c) {
     return 0;
 }
 
+/* O3 for one landmark: block (Fig. 2b): rows 2i,2i+1 = obs i; pose cols 9i..9i+8;
+ * landmark cols 9k..9k+2; residual col 9k+3; 3 zero damping rows at the bottom. */
+static void block_assemble(const orc_ctx *c, int64_t j, double *B) {
+    int64_t k = c->lm_ptr[j + 1] - c->lm_ptr[j];
+    int64_t W = DP * k + 4;
+    memset(B, 0, sizeof(double) * (2 * k + 3) * W);
+    for (int64_t i = 0; i < k; i++) {
+        int64_t o = c->lm_ptr[j] + i;
+        int cam = c->o_cam[o];
+        for (int rr = 0; rr < 2; rr++) {
+            double *row = B + (2 * i + rr) * W;
+            for (int q = 0; q < DP; q++) row[DP * i + q] = c->Jc[18 * o + 9 * rr + q] * c->sp[DP * cam + q];
+            for (int q = 0; q < 3; q++) row[DP * k + q] = c->Jl[6 * o + 3 * rr + q] * c->sl[3 * j + q];
+            row[DP * k + 3] = c->r[2 * o + rr];
+        }
+    }
+}
+
+/* O4 for one landmark: in-place Givens QR of the landmark columns (Appendix A.1; C5,
+ * C6): column l = 0..2, target rows i = 2k-1 down to l+1 against pivot row l: 6k-6 rotations. */
+static void block_qr(int64_t k, double *B) {
+    int64_t W = DP * k + 4;
+    for (int l = 0; l < 3; l++)
+        for (int64_t i = 2 * k - 1; i > l; i--) {
+            double cs, sn, rho;
+            orc_givens(B[l * W + DP * k + l], B[i * W + DP * k + l], &cs, &sn, &rho);
+            if (sn == 0.0) continue;
+            rot_rows(B + l * W, B + i * W, W, cs, sn);
+            B[i * W + DP * k + l] = 0.0; /* exact zero below the diagonal (Fig. 2c) */
+        }
+}
+
+/* O5 for one landmark (Fig. 3): damping rows 2k+q get sqrt(lambda) D_l,q in landmark
+ * column q; 6 rotations (pivot,target) = (0,2k),(1,2k),(2,2k),(1,2k+1),(2,2k+1),(2,2k+2) eliminate
+ * them; the (c,s) pairs go to g (12 doubles) to undo later. */
+static const int DAMP_P[6] = {0, 1, 2, 1, 2, 2};
+static const int DAMP_T[6] = {0, 0, 0, 1, 1, 2}; /* target = 2k + DAMP_T */
+static void block_damp(const orc_ctx *c, int64_t j, double *B, double lambda, double *g) {
+    int64_t k = c->lm_ptr[j + 1] - c->lm_ptr[j];
+    int64_t W = DP * k + 4;
+    double sl = sqrt(lambda);
+    for (int q = 0; q < 3; q++) B[(2 * k + q) * W + DP * k + q] = sl * sqrt(c->Dl2[3 * j + q]);
+    for (int m = 0; m < 6; m++) {
+        int p = DAMP_P[m];
+        double *rp = B + p * W, *rt = B + (2 * k + DAMP_T[m]) * W;
+        double cs, sn, rho;
+        orc_givens(rp[DP * k + p], rt[DP * k + p], &cs, &sn, &rho);
+        g[2 * m] = cs;
+        g[2 * m + 1] = sn;
+        if (sn != 0.0) {
+            rot_rows(rp, rt, W, cs, sn);
+            rt[DP * k + p] = 0.0;
+        }
+    }
+}
+
+/* undo (Fig. 3c): transposed rotations in reverse order, then zero the damping rows */
+static void block_undamp(int64_t k, double *B, const double *g) {
+    int64_t W = DP * k + 4;
+    for (int m = 5; m >= 0; m--) rot_rows(B + DAMP_P[m] * W, B + (2 * k + DAMP_T[m]) * W, W, g[2 * m], -g[2 * m + 1]);
+    memset(B + 2 * k * W, 0, sizeof(double) * 3 * W);
+}
+
+/* The current block of landmark j: the arena's, or (streaming mode) O3-O5 recomputed into
+ * `scratch` (max_block doubles) at the damping currently in force; g receives its rotations. */
+static const double *lm_block(orc_ctx *c, int64_t j, double *scratch, double *g) {
+    if (!c->streaming) {
+        if (g) memcpy(g, c->giv + 12 * j, sizeof(double) * 12);
+        return c->blk + c->blk_off[j];
+    }
+    int64_t k = c->lm_ptr[j + 1] - c->lm_ptr[j];
+    double gl[12];
+    block_assemble(c, j, scratch);
+    block_qr(k, scratch);
+    if (c->damped) block_damp(c, j, scratch, c->lambda, gl);
+    else for (int m = 0; m < 6; m++) gl[2 * m] = 1.0, gl[2 * m + 1] = 0.0;
+    if (g) memcpy(g, gl, sizeof(gl));
+    return scratch;
+}
+
+/* per-thread scratch for lm_block (streaming mode); NULL otherwise */
+static double *lm_scratch(orc_ctx *c) { return c->streaming ? malloc(sizeof(double) * (size_t)c->max_block) : NULL; }
+
+/* Streaming mode on (1) / off (0).  Takes effect at the next linearization. */
+void orc_set_streaming(orc_ctx *c, int on) {
+    c->streaming = on;
+    c->need_linearize = 1;
+    c->linearized = c->marginalized = c->damped = 0;
+    c->lambda = 0;
+    if (on && c->blk) { free(c->blk); c->blk = NULL; }
+}
+
 /* O1-O3: orc_scaling, then assemble the (undamped, unmarginalized) landmark blocks.
  * Returns 1 on a degenerate projection, 3 if the blocks cannot be allocated. */
 int orc_linearize(orc_ctx *c) {
     if (orc_scaling(c)) return 1;
+    if (c->streaming) {
+        c->linearized = 1;
+        c->marginalized = 0;
+        c->damped = 0;
+        c->lambda = 0;
+        return 0;
+    }
     if (!c->blk) {
         c->blk = malloc(sizeof(double) * (size_t)c->blk_off[c->n_l]);
         if (!c->blk) return 3;
     }
 #pragma omp parallel for schedule(dynamic, 256)
-    for (int64_t j = 0; j < c->n_l; j++) {
-        /* O3: landmark block (Fig. 2b): rows 2i,2i+1 = obs i; pose cols 9i..9i+8;
-         * landmark cols 9k..9k+2; residual col 9k+3; 3 zero damping rows at the bottom. */
-        int64_t k = c->lm_ptr[j + 1] - c->lm_ptr[j];
-        int64_t W = DP * k + 4;
-        double *B = c->blk + c->blk_off[j];
-        memset(B, 0, sizeof(double) * (2 * k + 3) * W);
-        for (int64_t i = 0; i < k; i++) {
-            int64_t o = c->lm_ptr[j] + i;
-            int cam = c->o_cam[o];
-            for (int rr = 0; rr < 2; rr++) {
-                double *row = B + (2 * i + rr) * W;
-                for (int q = 0; q < DP; q++) row[DP * i + q] = c->Jc[18 * o + 9 * rr + q] * c->sp[DP * cam + q];
-                for (int q = 0; q < 3; q++) row[DP * k + q] = c->Jl[6 * o + 3 * rr + q] * c->sl[3 * j + q];
-                row[DP * k + 3] = c->r[2 * o + rr];
-            }
-        }
-    }
+    for (int64_t j = 0; j < c->n_l; j++) block_assemble(c, j, c->blk + c->blk_off[j]);
     c->linearized = 1;
     c->marginalized = 0;
     c->damped = 0;
@@ -447,42 +536,22 @@ int orc_linearize(orc_ctx *c) {
  * column l = 0..2, target rows i = 2k-1 down to l+1 against pivot row l: 6k-6 rotations. */
 int orc_marginalize(orc_ctx *c) {
     if (!c->linearized || c->marginalized) return 2;
+    if (!c->streaming) {
 #pragma omp parallel for schedule(dynamic, 64)
-    for (int64_t j = 0; j < c->n_l; j++) {
-        int64_t k = c->lm_ptr[j + 1] - c->lm_ptr[j];
-        int64_t W = DP * k + 4;
-        double *B = c->blk + c->blk_off[j];
-        for (int l = 0; l < 3; l++)
-            for (int64_t i = 2 * k - 1; i > l; i--) {
-                double cs, sn, rho;
-                orc_givens(B[l * W + DP * k + l], B[i * W + DP * k + l], &cs, &sn, &rho);
-                if (sn == 0.0) continue;
-                rot_rows(B + l * W, B + i * W, W, cs, sn);
-                B[i * W + DP * k + l] = 0.0; /* exact zero below the diagonal (Fig. 2c) */
-            }
+        for (int64_t j = 0; j < c->n_l; j++) block_qr(c->lm_ptr[j + 1] - c->lm_ptr[j], c->blk + c->blk_off[j]);
     }
     c->marginalized = 1;
     return 0;
 }
 
-/* O5: landmark damping (Fig. 3).  Damping rows 2k+q get sqrt(lambda) D_l,q in landmark
- * column q; 6 rotations (pivot,target) = (0,2k),(1,2k),(2,2k),(1,2k+1),(2,2k+1),(2,2k+2) eliminate
- * them; the (c,s) pairs are stored to undo later. */
-static const int DAMP_P[6] = {0, 1, 2, 1, 2, 2};
-static const int DAMP_T[6] = {0, 0, 0, 1, 1, 2}; /* target = 2k + DAMP_T */
-
+/* O5: landmark damping (Fig. 3) of every block (block_damp); undo (block_undamp). */
 int orc_undamp(orc_ctx *c) {
     if (!c->marginalized) return 2;
     if (!c->damped) return 0;
+    if (!c->streaming) {
 #pragma omp parallel for schedule(dynamic, 64)
-    for (int64_t j = 0; j < c->n_l; j++) {
-        int64_t k = c->lm_ptr[j + 1] - c->lm_ptr[j];
-        int64_t W = DP * k + 4;
-        double *B = c->blk + c->blk_off[j];
-        const double *g = c->giv + 12 * j;
-        for (int m = 5; m >= 0; m--) /* transposed rotations in reverse order (Fig. 3c) */
-            rot_rows(B + DAMP_P[m] * W, B + (2 * k + DAMP_T[m]) * W, W, g[2 * m], -g[2 * m + 1]);
-        memset(B + 2 * k * W, 0, sizeof(double) * 3 * W); /* then zero the damping rows */
+        for (int64_t j = 0; j < c->n_l; j++)
+            block_undamp(c->lm_ptr[j + 1] - c->lm_ptr[j], c->blk + c->blk_off[j], c->giv + 12 * j);
     }
     c->damped = 0;
     c->lambda = 0;
@@ -493,26 +562,9 @@ int orc_damp(orc_ctx *c, double lambda) {
     if (!c->marginalized) return 2;
     if (!(lambda >= 0)) return 1;
     if (c->damped) orc_undamp(c);
-    double sl = sqrt(lambda);
+    if (!c->streaming) {
 #pragma omp parallel for schedule(dynamic, 64)
-    for (int64_t j = 0; j < c->n_l; j++) {
-        int64_t k = c->lm_ptr[j + 1] - c->lm_ptr[j];
-        int64_t W = DP * k + 4;
-        double *B = c->blk + c->blk_off[j];
-        for (int q = 0; q < 3; q++) B[(2 * k + q) * W + DP * k + q] = sl * sqrt(c->Dl2[3 * j + q]);
-        double *g = c->giv + 12 * j;
-        for (int m = 0; m < 6; m++) {
-            int p = DAMP_P[m];
-            double *rp = B + p * W, *rt = B + (2 * k + DAMP_T[m]) * W;
-            double cs, sn, rho;
-            orc_givens(rp[DP * k + p], rt[DP * k + p], &cs, &sn, &rho);
-            g[2 * m] = cs;
-            g[2 * m + 1] = sn;
-            if (sn != 0.0) {
-                rot_rows(rp, rt, W, cs, sn);
-                rt[DP * k + p] = 0.0;
-            }
-        }
+        for (int64_t j = 0; j < c->n_l; j++) block_damp(c, j, c->blk + c->blk_off[j], lambda, c->giv + 12 * j);
     }
     c->damped = 1;
     c->lambda = lambda;
@@ -525,7 +577,7 @@ int orc_damp(orc_ctx *c, double lambda) {
 /* O6: dense reduced system (test-sized problems only): H~ = sum_j A_j^T A_j + lambda D_p^2 and
  * b~ = sum_j A_j^T q_j.  H is (9 n_p)^2 row-major. */
 int orc_reduced_dense(orc_ctx *c, double *H, double *b) {
-    if (!c->marginalized) return 2;
+    if (!c->marginalized || c->streaming) return 2;
     int64_t N = DP * c->n_p;
     memset(H, 0, sizeof(double) * N * N);
     memset(b, 0, sizeof(double) * N);
@@ -557,7 +609,13 @@ int orc_reduced_dense(orc_ctx *c, double *H, double *b) {
 /* O6 implicit: out = H~ v = sum_j A_j^T (A_j v_j) + lambda D_p^2 v  (Eq. cg_mult).
  * Pass 1 (per landmark): y_j = A_j v_j.  Pass 2 (per camera, landmarks ascending): gather
  * A_j[:,o]^T y_j.  Fixed summation order. */
+void orc_products(orc_ctx *c, int nvec, const double *V, double *out);
+
 void orc_matvec(orc_ctx *c, const double *v, double *out) {
+    if (c->streaming) {
+        orc_products(c, 1, v, out);
+        return;
+    }
 #pragma omp parallel for schedule(dynamic, 256)
     for (int64_t j = 0; j < c->n_l; j++) {
         int64_t k = c->lm_ptr[j + 1] - c->lm_ptr[j];
@@ -593,15 +651,132 @@ void orc_matvec(orc_ctx *c, const double *v, double *out) {
     }
 }
 
+/* O6 for several vectors in one pass over the landmarks (each block read / recomputed once):
+ * out[t] = sum_j A_j^T (A_j v_t) + lambda D_p^2 v_t for the nvec vectors V[t] (9 n_p each).  Every
+ * thread owns a contiguous landmark range and accumulates into its own buffer; the buffers are
+ * added in thread order (a fixed order for a fixed thread count).  Used by the streaming mode's
+ * product and by batched probes. */
+void orc_products(orc_ctx *c, int nvec, const double *V, double *out) {
+    const int64_t N = DP * c->n_p;
+    int T = 1;
+#ifdef _OPENMP
+    T = omp_get_max_threads();
+#endif
+    double *acc = calloc((size_t)T * nvec * N, sizeof(double));
+#pragma omp parallel num_threads(T)
+    {
+        int t = 0;
+#ifdef _OPENMP
+        t = omp_get_thread_num();
+#endif
+        double *mine = acc + (size_t)t * nvec * N;
+        double *scratch = lm_scratch(c);
+        double *y = malloc(sizeof(double) * 2 * (size_t)(c->max_block > 0 ? c->max_block : 1));
+        const int64_t j0 = c->n_l * t / T, j1 = c->n_l * (t + 1) / T;
+        for (int64_t j = j0; j < j1; j++) {
+            int64_t k = c->lm_ptr[j + 1] - c->lm_ptr[j];
+            int64_t W = DP * k + 4;
+            const double *B = lm_block(c, j, scratch, NULL);
+            for (int v = 0; v < nvec; v++) {
+                const double *vv = V + (size_t)v * N;
+                for (int64_t a = 0; a < 2 * k; a++) {
+                    double s = 0;
+                    for (int64_t o = 0; o < k; o++) {
+                        const double *vc = vv + DP * c->o_cam[c->lm_ptr[j] + o];
+                        for (int q = 0; q < DP; q++) s += AJ(B, W, a, DP * o + q) * vc[q];
+                    }
+                    y[a] = s;
+                }
+                double *dst = mine + (size_t)v * N;
+                for (int64_t o = 0; o < k; o++) {
+                    double *oc = dst + DP * c->o_cam[c->lm_ptr[j] + o];
+                    for (int q = 0; q < DP; q++) {
+                        double s = 0;
+                        for (int64_t a = 0; a < 2 * k; a++) s += AJ(B, W, a, DP * o + q) * y[a];
+                        oc[q] += s;
+                    }
+                }
+            }
+        }
+        free(scratch);
+        free(y);
+    }
+    for (int v = 0; v < nvec; v++)
+        for (int64_t i = 0; i < N; i++) {
+            double s = 0;
+            for (int t = 0; t < T; t++) s += acc[((size_t)t * nvec + v) * N + i];
+            out[(size_t)v * N + i] = s + c->lambda * c->Dp2[i] * V[(size_t)v * N + i];
+        }
+    free(acc);
+}
+
+/* streaming mode: sum_j A_j[:,o]^T A_j[:,o] and A_j[:,o]^T q_j per camera (81 + 9 per camera),
+ * per-thread buffers over contiguous landmark ranges, added in thread order */
+static void stream_precond_sums(orc_ctx *c, double *Pall, double *ball) {
+    int T = 1;
+#ifdef _OPENMP
+    T = omp_get_max_threads();
+#endif
+    const size_t per = (size_t)90 * c->n_p;
+    double *acc = calloc((size_t)T * per, sizeof(double));
+#pragma omp parallel num_threads(T)
+    {
+        int t = 0;
+#ifdef _OPENMP
+        t = omp_get_thread_num();
+#endif
+        double *mine = acc + (size_t)t * per;
+        double *scratch = lm_scratch(c);
+        const int64_t j0 = c->n_l * t / T, j1 = c->n_l * (t + 1) / T;
+        for (int64_t j = j0; j < j1; j++) {
+            int64_t k = c->lm_ptr[j + 1] - c->lm_ptr[j];
+            int64_t W = DP * k + 4;
+            const double *B = lm_block(c, j, scratch, NULL);
+            for (int64_t o = 0; o < k; o++) {
+                double *P = mine + 90 * (size_t)c->o_cam[c->lm_ptr[j] + o], *bb = P + 81;
+                for (int q1 = 0; q1 < DP; q1++) {
+                    double sb = 0;
+                    for (int64_t a = 0; a < 2 * k; a++) sb += AJ(B, W, a, DP * o + q1) * AJ(B, W, a, DP * k + 3);
+                    bb[q1] += sb;
+                    for (int q2 = 0; q2 < DP; q2++) {
+                        double s = 0;
+                        for (int64_t a = 0; a < 2 * k; a++) s += AJ(B, W, a, DP * o + q1) * AJ(B, W, a, DP * o + q2);
+                        P[DP * q1 + q2] += s;
+                    }
+                }
+            }
+        }
+        free(scratch);
+    }
+    for (int64_t i = 0; i < c->n_p; i++)
+        for (int e = 0; e < 90; e++) {
+            double s = 0;
+            for (int t = 0; t < T; t++) s += acc[(size_t)t * per + 90 * (size_t)i + e];
+            if (e < 81) Pall[81 * i + e] = s;
+            else ball[DP * i + e - 81] = s;
+        }
+    free(acc);
+}
+
 /* O6/O7: b~ and the block-Jacobi preconditioner P_i = sum_j A_j[:,i]^T A_j[:,i] + lambda D_p,i^2
  * (C12), factored by Cholesky.  Returns 0, or 3 if a block is not SPD. */
 int orc_precond_rhs(orc_ctx *c) {
     if (!c->marginalized) return 2;
     int bad = 0;
+    double *Ps = NULL, *bs = NULL;
+    if (c->streaming) {
+        Ps = malloc(sizeof(double) * 81 * c->n_p);
+        bs = malloc(sizeof(double) * DP * c->n_p);
+        stream_precond_sums(c, Ps, bs);
+    }
 #pragma omp parallel for schedule(dynamic, 4) reduction(| : bad)
     for (int64_t i = 0; i < c->n_p; i++) {
         double P[81] = {0}, bb[DP] = {0};
-        for (int64_t m = c->cam_ptr[i]; m < c->cam_ptr[i + 1]; m++) {
+        if (c->streaming) {
+            memcpy(P, Ps + 81 * i, sizeof(P));
+            memcpy(bb, bs + DP * i, sizeof(bb));
+        }
+        for (int64_t m = c->streaming ? c->cam_ptr[i + 1] : c->cam_ptr[i]; m < c->cam_ptr[i + 1]; m++) {
             int64_t pos = c->cam_obs[m];
             int64_t j = c->o_lm[pos], o = pos - c->lm_ptr[j];
             int64_t k = c->lm_ptr[j + 1] - c->lm_ptr[j];
@@ -637,6 +812,8 @@ int orc_precond_rhs(orc_ctx *c) {
                 }
             }
     }
+    free(Ps);
+    free(bs);
     return bad ? 3 : 0;
 }
 
@@ -706,11 +883,14 @@ done:
 int orc_backsub(orc_ctx *c) {
     if (!c->marginalized) return 2;
     double *q1 = malloc(sizeof(double) * c->n_l), *dd = malloc(sizeof(double) * c->n_l);
-#pragma omp parallel for schedule(dynamic, 256)
+#pragma omp parallel
+    {
+    double *scratch = lm_scratch(c);
+#pragma omp for schedule(dynamic, 256)
     for (int64_t j = 0; j < c->n_l; j++) {
         int64_t k = c->lm_ptr[j + 1] - c->lm_ptr[j];
         int64_t W = DP * k + 4;
-        const double *B = c->blk + c->blk_off[j];
+        const double *B = lm_block(c, j, scratch, NULL);
         double rhs[3];
         double s2 = 0;
         for (int a = 0; a < 3; a++) {
@@ -735,6 +915,8 @@ int orc_backsub(orc_ctx *c) {
         }
         q1[j] = s2;
         dd[j] = dsum;
+    }
+    free(scratch);
     }
     double s1 = 0, s2 = 0;
     for (int64_t j = 0; j < c->n_l; j++) { s1 += q1[j]; s2 += dd[j]; }
@@ -854,9 +1036,21 @@ void orc_get_scaling(orc_ctx *c, double *sp, double *Dp2, double *sl, double *Dl
     memcpy(Dl2, c->Dl2, sizeof(double) * 3 * c->n_l);
 }
 void orc_get_block(orc_ctx *c, int64_t j, double *buf) {
+    if (c->streaming) {  /* recomputed (O3-O5) at the damping in force */
+        lm_block(c, j, buf, NULL);
+        return;
+    }
     memcpy(buf, c->blk + c->blk_off[j], sizeof(double) * (c->blk_off[j + 1] - c->blk_off[j]));
 }
-void orc_get_givens(orc_ctx *c, int64_t j, double *g) { memcpy(g, c->giv + 12 * j, sizeof(double) * 12); }
+void orc_get_givens(orc_ctx *c, int64_t j, double *g) {
+    if (c->streaming) {
+        double *scratch = lm_scratch(c);
+        lm_block(c, j, scratch, g);
+        free(scratch);
+        return;
+    }
+    memcpy(g, c->giv + 12 * j, sizeof(double) * 12);
+}
 void orc_get_rhs(orc_ctx *c, double *b) { memcpy(b, c->bt, sizeof(double) * DP * c->n_p); }
 /* Read-only view of the landmark-block arena: *ptr = first double, offsets[j] = start of landmark j
  * (n_l + 1 entries, caller buffer); valid until the next linearization. */

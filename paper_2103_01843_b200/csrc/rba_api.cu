@@ -1104,6 +1104,15 @@ extern "C" rba_status rba_get_rhs(rba_ctx *c, double *b) {
     return RBA_OK;
 }
 
+extern "C" rba_status rba_get_precond(rba_ctx *c, double *blocks) {
+    if (!c || !blocks) return fail(RBA_ERR_INVALID_ARG, "null argument");
+    if (!c->solved) return fail(RBA_ERR_STATE, "rba_get_precond before rba_pcg_solve");
+    if (c->d.sc) return fail(RBA_ERR_STATE, "rba_get_precond: not kept in explicit-SC mode");
+    CK(cudaMemcpyAsync(blocks, c->d.pd, sizeof(double) * 54 * c->d.n_p, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return RBA_OK;
+}
+
 extern "C" rba_status rba_get_step(rba_ctx *c, double *dp, double *dl) {
     if (!c || !dp || !dl) return fail(RBA_ERR_INVALID_ARG, "null argument");
     if (!c->solved) return fail(RBA_ERR_STATE, "rba_get_step before rba_pcg_solve");

@@ -99,6 +99,7 @@ def _load():
         "rba_reset_lm": (I, [P]),
         "rba_matvec": (I, [P, P, P]),
         "rba_get_rhs": (I, [P, P]),
+        "rba_get_precond": (I, [P, P]),
         "rba_get_step": (I, [P, P, P]),
         "rba_get_scaling": (I, [P, P, P, P, P]),
         "rba_export_block": (I, [P, I64, P, I64, C.POINTER(I64), C.POINTER(I64)]),
@@ -129,7 +130,7 @@ _lib = _load()
 EXPORTED = ["rba_default_options", "rba_create", "rba_destroy", "rba_linearize", "rba_marginalize_qr",
             "rba_pcg_solve", "rba_backsubstitute", "rba_cost", "rba_lm_step", "rba_lm_solve", "rba_get_state",
             "rba_set_state", "rba_reset_lm", "rba_set_lm", "rba_get_lm", "rba_set_pcg_limits", "rba_device_bytes", "rba_plan_bytes", "rba_get_info", "rba_checksums",
-            "rba_matvec", "rba_get_rhs", "rba_get_step", "rba_get_scaling", "rba_export_block", "rba_arena_bytes",
+            "rba_matvec", "rba_get_rhs", "rba_get_precond", "rba_get_step", "rba_get_scaling", "rba_export_block", "rba_arena_bytes",
             "rba_kernel_launches", "rba_profile", "rba_profile_get", "rba_plan_shards", "rba_nccl_unique_id",
             "rba_last_error", "rba_bal_parse", "rba_bal_read", "rba_bal_write", "rba_bal_normalize",
             "rba_bal_perturb", "rba_bal_filter", "rba_bal_free", "rba_bal_last_error"]
@@ -277,6 +278,12 @@ def rba_get_rhs(h, n_cams):
     b = np.zeros(9 * n_cams)
     _check(_lib.rba_get_rhs(h, _p(b)))
     return b
+
+
+def rba_get_precond(h, n_cams):
+    out = np.zeros((n_cams, 54))
+    _check(_lib.rba_get_precond(h, _p(out)))
+    return out
 
 
 def rba_get_step(h, n_cams, n_points):
@@ -539,6 +546,10 @@ class Solver:
 
     def rhs(self):
         return rba_get_rhs(self.h, self.n_p)
+
+    def precond_sums(self):
+        """(n_p, 54): upper triangles of sum_j A_j[:,i]^T A_j[:,i] and b~_i (last PCG solve)."""
+        return rba_get_precond(self.h, self.n_p)
 
     def step(self):
         return rba_get_step(self.h, self.n_p, self.n_l)
