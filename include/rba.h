@@ -273,8 +273,10 @@ typedef struct {
     int32_t *obs_cam, *obs_pt;
 } rba_bal;
 /* Parse BAL text: header "n_cams n_points n_obs", n_obs lines "cam pt u v", 9 numbers per camera,
- * 3 per point.  Counts come from the header; observation order is preserved. */
+ * 3 per point.  Counts come from the header; observation order is preserved.  Reads at most
+ * `len` bytes (text need not be NUL-terminated). */
 rba_status rba_bal_parse(const char *text, size_t len, rba_bal *out);
+/* Read a BAL file, plain text or gzip-compressed (zlib). */
 rba_status rba_bal_read(const char *path, rba_bal *out);
 /* Write BAL text (%.17g, so parse(write(p)) reproduces p exactly). */
 rba_status rba_bal_write(const char *path, const rba_bal *p);

@@ -61,7 +61,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
 
     with ThreadPoolExecutor(len(srcs)) as ex:
         objs = list(ex.map(comp, srcs))
-    link = [nvcc(), *ARCH, "-shared", "-o", lib, *objs, "-L", libdir, "-l:libnccl.so.2",
+    link = [nvcc(), *ARCH, "-shared", "-o", lib, *objs, "-L", libdir, "-l:libnccl.so.2", "-lz",
             "-Xlinker", f"-rpath,{libdir}"]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:

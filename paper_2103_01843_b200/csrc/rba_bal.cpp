@@ -15,6 +15,9 @@
 //     convention (camera looks down -z) the depth is -P_z; an observation is kept iff -P_z > z_min.
 #include <cmath>
 #include <cstdint>
+#include <zlib.h>
+
+#include <charconv>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -98,10 +101,11 @@ struct Lexer {
             p++;
         }
         if (p >= end) return false;
-        char *q = nullptr;
-        *v = std::strtod(p, &q);
-        if (q == p) return false;
-        p = q;
+        // bounded by `end` (the buffer need not be NUL-terminated); from_chars does not take a
+        // leading '+', which BAL writers do not emit
+        const std::from_chars_result res = std::from_chars(p, end, *v);
+        if (res.ec != std::errc() || res.ptr == p) return false;
+        p = res.ptr;
         return true;
     }
     bool next_int(int64_t *v) {
@@ -179,13 +183,17 @@ extern "C" rba_status rba_bal_parse(const char *text, size_t len, rba_bal *out) 
 
 extern "C" rba_status rba_bal_read(const char *path, rba_bal *out) {
     if (!path || !out) return bal_fail(RBA_ERR_INVALID_ARG, "null argument");
-    FILE *f = std::fopen(path, "rb");
+    // plain text or gzip (the BAL distribution's .bz2 / .gz files are usually stored gunzipped or
+    // gzipped; zlib's gzread reads both plain and gzip-compressed input transparently)
+    gzFile f = gzopen(path, "rb");
     if (!f) return bal_fail(RBA_ERR_INVALID_ARG, std::string("cannot open ") + path);
     std::string buf;
     char tmp[1 << 16];
-    size_t n;
-    while ((n = std::fread(tmp, 1, sizeof(tmp), f)) > 0) buf.append(tmp, n);
-    std::fclose(f);
+    int n;
+    while ((n = gzread(f, tmp, sizeof(tmp))) > 0) buf.append(tmp, (size_t)n);
+    const bool err = n < 0;
+    gzclose(f);
+    if (err) return bal_fail(RBA_ERR_INVALID_ARG, std::string("cannot decompress ") + path);
     return rba_bal_parse(buf.data(), buf.size(), out);
 }
 

@@ -30,6 +30,10 @@
 #include "rba_internal.cuh"
 #include "rba_model.cuh"
 
+#ifndef RBA_K2_EXP
+#define RBA_K2_EXP 0  // K2 measurement experiments (tools/): 1 = no R2 emission, 2 = no camera model
+#endif
+
 namespace rba {
 
 // ============================================================================ deterministic mode
@@ -340,7 +344,13 @@ __global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProb
         load_pre(d.campre, cam, c);
         const double *X = d.pts + 3 * j;
         const double2 uv = d.obs_uv[o];
+#if RBA_K2_EXP == 2  // measurement experiment: skip the camera model (emission-bound time)
+        for (int q = 0; q < 18; q++) Jc[q] = (float)c[q] + q;
+        for (int q = 0; q < 6; q++) Jl[q] = (float)c[q + 9] + q * gl;
+        rd[0] = uv.x, rd[1] = uv.y;
+#else
         cam_model_pre(c, X[0], X[1], X[2], uv.x, uv.y, rd, Jc, Jl);
+#endif
         apply_irls(rd, Jc, Jl, d.huber);
         r[0] = (float)rd[0];
         r[1] = (float)rd[1];
@@ -479,7 +489,7 @@ __global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProb
               pack.np * side_floats(k) <= d.arena_n);
     const int npk = pack.np * k, mo = grp * k + gl;
     float2 *Ap = A + mo;
-    for (int p = 0; p < k; p++, Ap += 9 * npk) {
+    for (int p = 0; p < (RBA_K2_EXP == 1 ? 0 : k); p++, Ap += 9 * npk) {  // (EXP 1: no R2 emission)
         float v18[18];
         if (p < k - 2) {  // rows 2p+3, 2p+4 < 2k: no damping rows
             wy_row_plain(B, VR[2 * p + 3], 2 * p + 3, gl, v18);
@@ -578,7 +588,13 @@ __global__ void __launch_bounds__(NT) k_marg_large(DevProblem d, const LargeItem
         float Jc[18], Jl[6];
         load_pre(d.campre, cam, c);
         const double2 uv = d.obs_uv[obs0 + o];
+#if RBA_K2_EXP == 2
+        for (int q = 0; q < 18; q++) Jc[q] = (float)c[q] + q;
+        for (int q = 0; q < 6; q++) Jl[q] = (float)c[q + 9] + q * o;
+        r[0] = uv.x, r[1] = uv.y;
+#else
         cam_model_pre(c, Xp[0], Xp[1], Xp[2], uv.x, uv.y, r, Jc, Jl);
+#endif
         apply_irls(r, Jc, Jl, d.huber);
         if (!MULTI) {
 #pragma unroll
@@ -708,7 +724,7 @@ __global__ void __launch_bounds__(NT) k_marg_large(DevProblem d, const LargeItem
         }
         const int g_ = o >> 5, ng = min(32, k - 32 * g_);
         float *R2 = d.arena + d.lm_r2[j];
-        for (int t = it.t0; t < it.t1; t++) {
+        for (int t = it.t0; t < (RBA_K2_EXP == 1 ? it.t0 : it.t1); t++) {
             float4 *S = reinterpret_cast<float4 *>(R2 + (int64_t)36 * k * t + 36 * 32 * g_) + (o & 31);
             float v36[36];
             if (4 * t + 6 < 2 * k) {  // logical rows 4t+3 .. 4t+6 are plain rows (< 2k)

@@ -128,3 +128,31 @@ def test_filter_hand_cases():
     b = rba.BalProblem.parse(bal_text(s))
     assert b.filter(1e-8) == (0, 0)
     np.testing.assert_array_equal(b.as_problem()["obs_cam"], s["obs_cam"])
+
+
+def test_parse_is_bounded_by_len():
+    """rba_bal_parse reads at most `len` bytes: a buffer that is not NUL-terminated (here followed
+    by more digits in memory) parses exactly as its first `len` bytes (strtod overran)."""
+    import ctypes as C
+    text = b"1 2 2\n0 0 1.5 2.5\n0 1 3.5 4.5\n" + b"\n".join(b"0.25" for _ in range(9)) + b"\n1 2 3\n4 5 6"
+    tail = b"789123"  # would extend the last number to 6789123 if the parser ran past len
+    raw = C.create_string_buffer(text + tail, len(text) + len(tail))
+    b = rba.rba_bal()
+    assert rba.lib().rba_bal_parse(C.cast(raw, C.c_char_p), len(text), C.byref(b)) == rba.RBA_OK
+    p = rba.BalProblem(b).as_problem()
+    assert p["points_init"][1, 2] == 6.0
+    assert np.allclose(p["obs_uv"], [[1.5, 2.5], [3.5, 4.5]])
+
+
+def test_read_gzip(tmp_path):
+    """rba_bal_read takes gzip-compressed BAL files (the distribution format) as well as plain text."""
+    import gzip
+    p = synth.make_random_small(3, n_p=4, n_l=6)
+    plain = tmp_path / "p.txt"
+    b = rba.BalProblem.parse(bal_text(p))
+    b.write(str(plain))
+    gz = tmp_path / "p.txt.gz"
+    gz.write_bytes(gzip.compress(plain.read_bytes()))
+    a, z = rba.BalProblem.read(str(plain)).as_problem(), rba.BalProblem.read(str(gz)).as_problem()
+    for key in a:
+        assert np.array_equal(a[key], z[key]), key

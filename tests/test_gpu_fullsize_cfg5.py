@@ -126,6 +126,9 @@ def test_cfg5_block_jacobi_and_rhs_vs_streaming_oracle(cfg5, stream5):
     A_j[:,i] + lambda D_p,i^2, C12) and the whole b~ against the streaming oracle."""
     p, s = cfg5
     o = stream5
+    s.set_state(p["cameras_init"], p["points_init"])  # (an earlier test ran LM steps on this solver)
+    s.linearize()
+    s.marginalize(LAM)
     s.set_pcg_limits(0.0, 0)
     s.pcg()  # preconditioner pass only
     s.set_pcg_limits(1e-2, 500)
@@ -154,6 +157,9 @@ def test_cfg5_reduced_system_hutchinson(cfg5, stream5):
     p, s = cfg5
     o = stream5
     N = 9 * o.n_p
+    s.set_state(p["cameras_init"], p["points_init"])
+    s.linearize()
+    s.marginalize(LAM)
     Z = np.random.default_rng(55).choice([-1.0, 1.0], size=(16, N))
     t0 = time.time()
     Ho = o.products(Z)
