@@ -998,6 +998,9 @@ constexpr int SP_SB = SP_OFF_HDR + 128;
 #ifndef RBA_YRED_SHFL
 #define RBA_YRED_SHFL 1  // y reduction by xor butterfly (measured 2.54 -> 2.47 ms cfg4 matvec)
 #endif
+#ifndef RBA_SP_EXP
+#define RBA_SP_EXP 0  // small-pipe experiment: 1 = no staged camera / pack / unit tables
+#endif
 #ifndef RBA_PF_AHEAD
 #define RBA_PF_AHEAD 0  // stages prefetched into L2 beyond the shared-memory ring (measured: slower, 0.29 -> 0.52 ms cfg3)
 #endif
@@ -1105,14 +1108,16 @@ __global__ void __launch_bounds__(SP_WARPS * 32 + 32, 1)
                 }
                 mbar_wait(&empty[s], ph ^ 1);
                 *reinterpret_cast<SmallChunk *>(sm + (size_t)s * SP_SB + SP_OFF_HDR) = ch;
-                mbar_arrive_expect_tx(&full[s], (uint32_t)ch.bytes + 4u * (uint32_t)ch.ncam +
-                                                    (uint32_t)sizeof(Pack) * (uint32_t)ch.np + 2u * (uint32_t)ch.nunit +
+                mbar_arrive_expect_tx(&full[s], (uint32_t)ch.bytes + (RBA_SP_EXP ? 0u : 4u * (uint32_t)ch.ncam +
+                                                    (uint32_t)sizeof(Pack) * (uint32_t)ch.np + 2u * (uint32_t)ch.nunit) +
                                                     (PRECOND ? 4u * (uint32_t)ch.nq : 0u));
                 unsigned char *dst = sm + (size_t)s * SP_SB;
                 bulk_g2s_stream(dst, d.arena + ch.base, (uint32_t)ch.bytes, &full[s], pol);
-                bulk_g2s(dst + SP_OFF_CAM, d.obs_cam + ch.cam0, 4u * (uint32_t)ch.ncam, &full[s]);
-                bulk_g2s(dst + SP_OFF_PACK, d.packs + ch.p0, (uint32_t)sizeof(Pack) * ch.np, &full[s]);
-                bulk_g2s(dst + SP_OFF_UNIT, d.units + ch.unit0, 2u * (uint32_t)ch.nunit, &full[s]);
+                if (!RBA_SP_EXP) {
+                    bulk_g2s(dst + SP_OFF_CAM, d.obs_cam + ch.cam0, 4u * (uint32_t)ch.ncam, &full[s]);
+                    bulk_g2s(dst + SP_OFF_PACK, d.packs + ch.p0, (uint32_t)sizeof(Pack) * ch.np, &full[s]);
+                    bulk_g2s(dst + SP_OFF_UNIT, d.units + ch.unit0, 2u * (uint32_t)ch.nunit, &full[s]);
+                }
                 if (PRECOND) bulk_g2s_stream(dst + SP_OFF_Q, d.qpk + ch.q0, 4u * (uint32_t)ch.nq, &full[s], pol);
             }
         }
@@ -1127,11 +1132,17 @@ __global__ void __launch_bounds__(SP_WARPS * 32 + 32, 1)
         const int s = (int)((i - lo) % SP_STAGES);
         const uint32_t ph = (uint32_t)(((i - lo) / SP_STAGES) & 1);
         const unsigned char *stg = sm + (size_t)s * SP_SB;
+        mbar_wait(&full[s], ph);
+        const SmallChunk ch = *reinterpret_cast<const SmallChunk *>(stg + SP_OFF_HDR);
+#if RBA_SP_EXP  // experiment: the stage tables read from global (L1 / L2) instead of staged copies
+        const int *scam = d.obs_cam + ch.cam0;
+        const Pack *spk = d.packs + ch.p0;
+        const uint16_t *sun = d.units + ch.unit0;
+#else
         const int *scam = reinterpret_cast<const int *>(stg + SP_OFF_CAM);
         const Pack *spk = reinterpret_cast<const Pack *>(stg + SP_OFF_PACK);
         const uint16_t *sun = reinterpret_cast<const uint16_t *>(stg + SP_OFF_UNIT);
-        mbar_wait(&full[s], ph);
-        const SmallChunk ch = *reinterpret_cast<const SmallChunk *>(stg + SP_OFF_HDR);
+#endif
         const int nitems = dbg == 1 ? 0 : (PRECOND ? ch.np : ch.nreal);
         int first = warp - base;
         if (first < 0) first += SP_WARPS;

@@ -177,8 +177,7 @@ def test_cfg5_pcg_and_lm_vs_streaming_oracle(cfg5):
     """The PCG solution of the first LM iteration (<= 1e-3, the same rule and, at the tolerance edge,
     the oracle's count) and the cost after each of the first LM iterations (<= 1e-4, the §8c replay
     rule) against the streaming oracle on the full config 5.  RBA_LM5 iterations (default 2)."""
-    from paper_2103_01843_b200.rba import Solver
-    p, _ = cfg5
+    p, s = cfg5  # (the fixture's solver: a second 131.7 GB context does not fit next to it)
     o = oracle.Oracle(p)
     o.set_streaming(True)
     o.linearize()
@@ -188,25 +187,27 @@ def test_cfg5_pcg_and_lm_vs_streaming_oracle(cfg5):
     t0 = time.time()
     it, reason, _ = o.pcg(1e-2, 500)
     print(f"streaming oracle PCG: {it} iterations, {time.time() - t0:.1f} s")
-    s = Solver(p, pcg_rel_tol=0.0, pcg_max_iters=it)
+    s.set_state(p["cameras_init"], p["points_init"])
+    s.reset_lm()
     s.linearize()
     s.marginalize(LAM)
+    s.set_pcg_limits(0.0, it)
     st = s.pcg()
+    s.set_pcg_limits(1e-2, 500)
     assert st["iters"] == it and reason != 2 and st["reason"] != 2
     s.backsub()
     o.backsub()
     dp, dl = s.step()
     assert relf(dp, o.dp()) <= 1e-3
     assert relf(dl, o.dl()) <= 1e-3
-    s.close()
     o.set_state(p["cameras_init"], p["points_init"])
     o.set_lm(LAM, 2.0)
     from _lm import lm_parity
-    s = Solver(p)
+    s.set_state(p["cameras_init"], p["points_init"])
+    s.reset_lm()
     t0 = time.time()
     out = lm_parity(s, o, int(os.environ.get("RBA_LM5", "2")))
     for rg, ro, rep in out:
         print(f"cfg5 LM: gpu {rg['cost_after']:.6f} oracle {ro['cost_after']:.6f} pcg {ro['pcg_iters']} "
               f"accepted {ro['accepted']} replayed {rep}")
     print(f"cfg5 LM against the streaming oracle: {time.time() - t0:.1f} s")
-    s.close()
