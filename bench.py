@@ -214,6 +214,12 @@ def bench_reference(args, prob, rank):
     traj = oracle_trajectory(args.config)
     if traj is not None and len(traj[0]) >= args.steps:
         iters, src = traj[0][:args.steps], traj[1]
+    elif traj is not None and traj[0]:
+        # the recorded trajectory is shorter than K: its last iterations already run PCG to its
+        # 500-iteration cap; the remaining steps are taken at the cap, relinearizing
+        n_rec = len(traj[0])
+        iters = traj[0] + [(True, 500)] * (args.steps - n_rec)
+        src = f"{traj[1]}: {n_rec} recorded iterations, the other {args.steps - n_rec} at the PCG cap of 500"
     else:  # no recorded trajectory: the GPU-independent lower bound of one PCG iteration per step
         iters, src = [(True, 1)] * args.steps, "none (1 PCG iteration per step assumed)"
     sec = compose_oracle(t, iters)

@@ -998,6 +998,12 @@ constexpr int SP_SB = SP_OFF_HDR + 128;
 #ifndef RBA_YRED_SHFL
 #define RBA_YRED_SHFL 1  // y reduction by xor butterfly (measured 2.54 -> 2.47 ms cfg4 matvec)
 #endif
+#ifndef RBA_SP_AGG
+#define RBA_SP_AGG 1  // small pipe: add a pack's per-camera partials over its landmarks before the reductions
+#endif
+#ifndef RBA_STRIPE
+#define RBA_STRIPE 1  // large-pipe product, NSLOT > 1: one bulk copy of NSLOT consecutive tiles per stage
+#endif
 #ifndef RBA_SP_EXP
 #define RBA_SP_EXP 0  // small-pipe experiment: 1 = no staged camera / pack / unit tables
 #endif
@@ -1043,8 +1049,7 @@ __device__ __forceinline__ void small_unit(const DevProblem &d, const float2 *A,
 #pragma unroll
             for (int i = 0; i < 2 * NRP; i++) y[i] += __shfl_xor_sync(0xffffffffu, y[i], mm, G);
         }
-        if (!valid) return;
-        float acc[9];
+        float acc[9];  // (0 on invalid lanes: their slab is 0)
 #pragma unroll
         for (int q = 0; q < 9; q++) {
             float a_ = 0.f;
@@ -1052,8 +1057,25 @@ __device__ __forceinline__ void small_unit(const DevProblem &d, const float2 *A,
             for (int u = 0; u < NRP; u++) a_ += sl[u][q] * y[2 * u] + sl[u][9 + q] * y[2 * u + 1];
             acc[q] = a_;
         }
-        if (d.det) det_store12(d, slot, acc);
-        else flush_cam12(wslice(d), cam, acc);
+        if (d.det) {
+            if (valid) det_store12(d, slot, acc);
+            return;
+        }
+        if (RBA_SP_AGG && G < 32) {
+            // the pack's landmarks are sorted by first camera and observe windows of cameras, so
+            // usually every landmark of the pack has the same camera in block o: add their partials
+            // over m with shuffles and issue one set of reductions per o instead of one per lane
+            const int lane = threadIdx.x & 31, o = lane % G;
+            const int cam0 = __shfl_sync(0xffffffffu, cam, o);
+            if (__all_sync(0xffffffffu, !valid || cam == cam0)) {
+                for (int mm = G; mm < 32; mm <<= 1)
+#pragma unroll
+                    for (int q = 0; q < 9; q++) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], mm);
+                if (lane < G && o < k) flush_cam12(wslice(d), cam0, acc);
+                return;
+            }
+        }
+        if (valid) flush_cam12(wslice(d), cam, acc);
     }
 }
 
@@ -1167,13 +1189,12 @@ __global__ void __launch_bounds__(SP_WARPS * 32 + 32, 1)
             // K4: the landmark's q from the staged copy, row a at qs[a - 3]
             const float *qs = reinterpret_cast<const float *>(stg + SP_OFF_Q) + (pack.q0 - ch.q0) + 2 * k * m;
             if (PRECOND) {  // a warp takes all row pairs of a pack: one flush per (landmark, camera)
-                if (!valid) continue;
                 float P[45], b[9];
 #pragma unroll
                 for (int q = 0; q < 45; q++) P[q] = 0.f;
 #pragma unroll
                 for (int q = 0; q < 9; q++) b[q] = 0.f;
-                for (int pp = 0; pp < k; pp++) {
+                for (int pp = 0; pp < (valid ? k : 0); pp++) {
                     float sl[18];
 #pragma unroll
                     for (int c = 0; c < 9; c++) {
@@ -1183,8 +1204,24 @@ __global__ void __launch_bounds__(SP_WARPS * 32 + 32, 1)
                     acc_rows(P, b, sl, qs[2 * pp]);
                     acc_rows(P, b, sl + 9, qs[2 * pp + 1]);
                 }
-                if (d.det) det_store54(d, d.slot4[pack.obs0 + mo], P, b);
-                else flush54(pslice(d) + PACC_STRIDE * (int64_t)cam, P, b);
+                if (d.det) {
+                    if (valid) det_store54(d, d.slot4[pack.obs0 + mo], P, b);
+                    continue;
+                }
+                if (RBA_SP_AGG && G < 32) {  // same camera across the pack's landmarks: see small_unit
+                    const int cam0 = __shfl_sync(0xffffffffu, cam, o);
+                    if (__all_sync(0xffffffffu, !valid || cam == cam0)) {
+                        for (int mm = G; mm < 32; mm <<= 1) {
+#pragma unroll
+                            for (int q = 0; q < 45; q++) P[q] += __shfl_xor_sync(0xffffffffu, P[q], mm);
+#pragma unroll
+                            for (int q = 0; q < 9; q++) b[q] += __shfl_xor_sync(0xffffffffu, b[q], mm);
+                        }
+                        if (lane < G && o < k) flush54(pslice(d) + PACC_STRIDE * (int64_t)cam0, P, b);
+                        continue;
+                    }
+                }
+                if (valid) flush54(pslice(d) + PACC_STRIDE * (int64_t)cam, P, b);
                 continue;
             }
             if constexpr (!PRECOND) {
@@ -1229,8 +1266,14 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
     __shared__ __align__(16) float red[2][C::NC / 32][4];
     const int tid = threadIdx.x;
     const int64_t lo = cta_lo[blockIdx.x], hi = cta_lo[blockIdx.x + 1];
-    // slot s streams the contiguous tile run [lo + s nst, lo + (s + 1) nst): consecutive tiles of a
-    // landmark stay in one slot, so its camera / v / flush work is paid once per landmark, not per tile
+    // Run mode: slot s streams the contiguous tile run [lo + s nst, lo + (s + 1) nst): consecutive
+    // tiles of a landmark stay in one slot, so its camera / v / flush work is paid once per
+    // landmark; a stage is NSLOT separate bulk copies of one tile each.
+    // Stripe mode (the product with NSLOT > 1, not deterministic): stage i = the NSLOT consecutive
+    // tiles lo + i NSLOT .. (one contiguous range of the arena: ONE bulk copy of NSLOT tiles, so the
+    // copies are as large as the big-k classes'), slot s takes tile lo + i NSLOT + s; a landmark's
+    // partial sums are flushed once per slot that saw it.
+    const bool stripe = RBA_STRIPE && !PRECOND && NSLOT > 1 && !d.det;
     const int64_t nst = (hi - lo + NSLOT - 1) / NSLOT;
     if (tid == 0) {
         for (int s = 0; s < C::STAGES; s++) {
@@ -1241,7 +1284,27 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
     }
     __syncthreads();
     if (tid >= C::NC) {  // ---------------- producer warp: one elected lane streams the tiles
-        if (tid == C::NC) {
+        if (tid == C::NC && stripe) {
+            const uint64_t pol = policy_evict_first();
+            int64_t n_off = 0, n_bytes = 0;  // the next stage's source range (loaded one ahead)
+            auto range = [&](int64_t i, int64_t &off, int64_t &bytes) {
+                const int64_t first = lo + i * NSLOT, last = min(hi, first + NSLOT) - 1;
+                const TileRef a = tiles[first], z = tiles[last];
+                off = a.off;
+                bytes = 4 * (z.off - a.off + 36 * (int64_t)z.k);
+            };
+            if (nst > 0) range(0, n_off, n_bytes);
+            for (int64_t i = 0; i < nst; i++) {
+                const int s = (int)(i % C::STAGES);
+                const uint32_t ph = (uint32_t)((i / C::STAGES) & 1);
+                const int64_t c_off = n_off, c_bytes = n_bytes;
+                if (i + 1 < nst) range(i + 1, n_off, n_bytes);
+                mbar_wait(&empty[s], ph ^ 1);
+                RBA_CHECK(c_bytes > 0 && c_bytes <= C::SB && c_off >= 0 && c_off + c_bytes / 4 <= d.arena_n);
+                mbar_arrive_expect_tx(&full[s], (uint32_t)c_bytes);
+                bulk_g2s_stream(sm + (size_t)s * C::SB, d.arena + c_off, (uint32_t)c_bytes, &full[s], pol);
+            }
+        } else if (tid == C::NC) {
             const uint64_t pol = policy_evict_first();
             // descriptors (arena offset, k) of the next stage are loaded one stage ahead, as
             // independent loads, so their latency overlaps the wait and the current copies
@@ -1333,9 +1396,11 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
     for (int64_t i = 0; i < nst; i++) {
         const int s = (int)(i % C::STAGES);
         const uint32_t ph = (uint32_t)((i / C::STAGES) & 1);
-        const int64_t ti = lo + slot * nst + i;
+        const int64_t ti = stripe ? lo + i * NSLOT + slot : lo + slot * nst + i;
         const bool have = ti < hi;  // uniform over the slot
         TileRef tr{-1, 0, 0, 0, 0};
+        int64_t stage_off = 0;  // stripe mode: arena offset of the stage's first tile
+        if (stripe) stage_off = tiles[lo + i * NSLOT].off;
         if (have) {
             tr = tiles[ti];
             if (tr.lm != cur) {
@@ -1391,7 +1456,9 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
         }
         if (have && valid) {
             const float4 *S4 =
-                reinterpret_cast<const float4 *>(sm + (size_t)s * C::SB + (size_t)slot * C::TB) + 288 * g + (o & 31);
+                reinterpret_cast<const float4 *>(sm + (size_t)s * C::SB +
+                                                 (stripe ? (size_t)4 * (tr.off - stage_off) : (size_t)slot * C::TB)) +
+                288 * g + (o & 31);
 #pragma unroll
             for (int c = 0; c < 9; c++) {
                 const float4 x = S4[c * ng];

@@ -115,3 +115,47 @@ def test_no_reads_of_unwritten_memory(cfg):
     assert runs[0][0] == runs[1][0] and all(np.isfinite(runs[1][0]))
     assert np.array_equal(runs[0][1][0], runs[1][1][0]) and np.array_equal(runs[0][1][1], runs[1][1][1])
     assert runs[0][2] == runs[1][2]
+
+
+@pytest.mark.parametrize("cfg", [0, 2])
+def test_graph_eager_step_and_solve_bitwise_equal(cfg, monkeypatch):
+    """The device-side LM loop (one CUDA graph: conditional if/else for relinearize vs re-damp,
+    nested while loops for PCG and LM) runs exactly the kernels of the eager path: in
+    deterministic mode rba_lm_solve(4), four rba_lm_step calls, and the eager path (RBA_NO_GRAPH:
+    host-driven branches, host-polled PCG batches) give bit-identical trajectories and states."""
+    p = _problem(cfg)
+    out = {}
+    for name in ("solve", "steps", "eager"):
+        if name == "eager":
+            monkeypatch.setenv("RBA_NO_GRAPH", "1")
+        s = _solver(p, deterministic=1)
+        reps = s.lm_solve(4, 0.0) if name == "solve" else [s.lm_step() for _ in range(4)]
+        info = s.info()
+        assert info["lm_graph"] == (0 if name == "eager" or cfg == 0 else 1), (name, info)  # (cfg 0: a k > 512 track runs eagerly)
+        out[name] = ([(r["cost_after"], r["pcg_iters"], r["accepted"], r["relinearized"]) for r in reps], s.state())
+        s.close()
+    for name in ("steps", "eager"):
+        assert out[name][0] == out["solve"][0], name
+        assert np.array_equal(out[name][1][0], out["solve"][1][0]) and np.array_equal(out[name][1][1], out["solve"][1][1])
+
+
+def test_lm_solve_terminates_like_the_oracle():
+    """rba_lm_solve's termination (at most max_iters attempts, stop once an accepted step
+    decreases E by less than ftol E) against the same rule applied to the oracle's iterations:
+    same number of iterations, same accept sequence, costs within 1e-4 (config 1)."""
+    p = synth.make_problem(1)
+    s = _solver(p)
+    reps = s.lm_solve(50, 1e-6)
+    o = oracle.Oracle(p)
+    ref = []
+    for _ in range(50):
+        r = o.lm_step()
+        ref.append(r)
+        if r["accepted"] and (r["cost"] - r["cost_after"]) < 1e-6 * r["cost"]:
+            break
+    assert len(reps) == len(ref) < 50, (len(reps), len(ref))
+    assert reps[-1]["status"] == 1 and all(r["status"] == 0 for r in reps[:-1])
+    assert [r["accepted"] for r in reps] == [r["accepted"] for r in ref]
+    for rg, ro in zip(reps, ref):
+        assert abs(rg["cost_after"] - ro["cost_after"]) <= 1e-4 * ro["cost_after"], (rg, ro)
+    assert all(r["t_total_ms"] > 0 and r["device_bytes"] > 0 for r in reps)
