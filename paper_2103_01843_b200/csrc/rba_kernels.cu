@@ -1002,7 +1002,7 @@ constexpr int SP_SB = SP_OFF_HDR + 128;
 #define RBA_SP_AGG 1  // small pipe: add a pack's per-camera partials over its landmarks before the reductions
 #endif
 #ifndef RBA_STRIPE
-#define RBA_STRIPE 1  // large-pipe product, NSLOT > 1: one bulk copy of NSLOT consecutive tiles per stage
+#define RBA_STRIPE 0  // 1: large-pipe product, NSLOT > 1: one bulk copy of NSLOT consecutive tiles per stage (measured slower: cfg3 0.266 -> 0.298 ms)
 #endif
 #ifndef RBA_SP_EXP
 #define RBA_SP_EXP 0  // small-pipe experiment: 1 = no staged camera / pack / unit tables
