@@ -191,6 +191,17 @@ extern "C" rba_status rba_destroy(rba_ctx *c) {
     return RBA_OK;
 }
 
+// Persistent CTAs of a product / preconditioner class kernel (one per SM at most: their smem
+// rings take the SM): every class kernel gets all SMs.  RBA_PROP_GRID=1: SMs in proportion to the
+// class's bytes of the product, so that the classes, forked over separate streams, could run side
+// by side -- measured 1.8x slower (cfg 4 product 2.22 -> 4.01 ms): the class kernels do not share
+// the GPU that way.
+static int64_t prop_ctas(const rba_ctx *c, double bytes) {
+    static const bool prop = getenv("RBA_PROP_GRID") && atoi(getenv("RBA_PROP_GRID")) != 0;
+    if (!prop || c->matvec_bytes <= 0) return c->num_sms;
+    return std::max<int64_t>(1, std::min<int64_t>(c->num_sms, std::llround(c->num_sms * bytes / c->matvec_bytes)));
+}
+
 // ------------------------------------------------------------------------------------ create
 extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const double *points, int64_t n_points,
                                  const int32_t *obs_cam, const int32_t *obs_pt, const double *obs_uv,
@@ -394,10 +405,10 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     c->n_chunks = (int64_t)chunks.size();
     std::vector<int64_t> chunk_lo;
     {
-        const int64_t G = std::min<int64_t>(c->num_sms, c->n_chunks);
-        c->chunk_ctas = G;
         double tot = 0;
         for (auto &ch : chunks) tot += ch.bytes;
+        const int64_t G = std::min<int64_t>(prop_ctas(c, tot), c->n_chunks);
+        c->chunk_ctas = G;
         chunk_lo.push_back(0);
         double accb = 0;
         int64_t next = 1;
@@ -465,7 +476,7 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
         // persistent CTAs (one per SM) over contiguous tile ranges balanced by bytes
         c->cta_off[cls] = (int64_t)cta_lo.size();
         const int64_t ntl = t_hi - t_lo;
-        const int64_t G = std::min<int64_t>(c->num_sms, ntl);
+        const int64_t G = std::min<int64_t>(prop_ctas(c, bytes), ntl);
         c->cta_n[cls] = G;
         if (G > 0) {
             cta_lo.push_back(t_lo);

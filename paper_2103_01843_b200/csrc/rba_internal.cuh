@@ -259,9 +259,9 @@ struct rba_ctx {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     // auxiliary streams: independent per-class kernels fork off the context stream and join back
-    static constexpr int NAUX = 3;
-    cudaStream_t aux[NAUX] = {nullptr, nullptr, nullptr};
-    cudaEvent_t ev_fork = nullptr, ev_join[NAUX] = {nullptr, nullptr, nullptr};
+    static constexpr int NAUX = 5;
+    cudaStream_t aux[NAUX] = {};
+    cudaEvent_t ev_fork = nullptr, ev_join[NAUX] = {};
     int world = 1, rank = 0;
     ncclComm_t comm = nullptr;
     bool have_comm = false;
