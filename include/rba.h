@@ -79,8 +79,10 @@ typedef struct {
     /* arithmetic of the landmark blocks for RBA_SOLVER_SQRTBA with dense storage (SURVEY §8f row
      * f2): RBA_PRECISION_FP32 (default, the paper's sqrt-BA-32) or RBA_PRECISION_FP64 (sqrt-BA-64:
      * the (2k+3) x (9k+4) blocks stored row-major in FP64 and every QR / product / back-substitution
-     * operation in FP64; track lengths up to 1024).  The column scaling and damping diagonals are
-     * FP32 in both (shared with K1). */
+     * operation in FP64; track lengths up to 1024).  sqrt-BA-64 computes the camera column norms,
+     * the scaling S_p / S_l and the damping diagonals D_p^2 / D_l^2 in FP64 as well (sqrt-BA-32:
+     * FP32 values, kept beside FP64 copies of S_p and D_p^2 for the FP64 PCG vectors), and every
+     * kernel reads the damping lambda in FP64. */
     int precision;
     /* 1 = bitwise-reproducible camera-space sums (SURVEY §8b "no float atomics"; the paper's
      * "parallel reduce"): every landmark's contribution to a camera sum (K1 camera norms,

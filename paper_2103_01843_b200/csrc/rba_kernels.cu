@@ -998,6 +998,9 @@ constexpr int SP_SB = SP_OFF_HDR + 128;
 #ifndef RBA_YRED_SHFL
 #define RBA_YRED_SHFL 1  // y reduction by xor butterfly (measured 2.54 -> 2.47 ms cfg4 matvec)
 #endif
+#ifndef RBA_LP_AHEAD
+#define RBA_LP_AHEAD 0  // 1: large pipe loads the next tile descriptor and the next landmark's camera / v ahead (measured neutral)
+#endif
 #ifndef RBA_SP_AGG
 #define RBA_SP_AGG 1  // small pipe: add a pack's per-camera partials over its landmarks before the reductions
 #endif
@@ -1393,16 +1396,29 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
         }
     };
     int buf = 0;
+    // The next stage's tile descriptor and the next landmark's camera / v block are loaded ahead
+    // (RBA_LP_AHEAD): at a landmark change the slot would otherwise wait on two dependent L2 round
+    // trips (camera index, then v) -- for k <= 64 that stall was longer than the landmark's tiles.
+    constexpr bool LPA = RBA_LP_AHEAD && NS <= 128;  // (NS >= 256: landmark changes are rare, registers tight)
+    auto tile_of = [&](int64_t i) -> int64_t { return stripe ? lo + i * NSLOT + slot : lo + slot * nst + i; };
+    TileRef tr_n{-1, 0, 0, 0, 0};
+    if (nst > 0 && tile_of(0) < hi) tr_n = tiles[tile_of(0)];
+    int pf_state = 0, pf_cam = 0;  // 0 none, 1 camera index loaded, 2 camera and v loaded
+    int64_t pf_obs0 = -1;
+    float pf_v[9];
+#pragma unroll
+    for (int q = 0; q < 9; q++) pf_v[q] = 0.f;
     for (int64_t i = 0; i < nst; i++) {
         const int s = (int)(i % C::STAGES);
         const uint32_t ph = (uint32_t)((i / C::STAGES) & 1);
-        const int64_t ti = stripe ? lo + i * NSLOT + slot : lo + slot * nst + i;
+        const int64_t ti = tile_of(i);
         const bool have = ti < hi;  // uniform over the slot
-        TileRef tr{-1, 0, 0, 0, 0};
+        TileRef tr = have ? tr_n : TileRef{-1, 0, 0, 0, 0};
+        if (LPA && i + 1 < nst && tile_of(i + 1) < hi) tr_n = tiles[tile_of(i + 1)];
+        else if (!LPA && have) tr = tiles[ti];
         int64_t stage_off = 0;  // stripe mode: arena offset of the stage's first tile
         if (stripe) stage_off = tiles[lo + i * NSLOT].off;
         if (have) {
-            tr = tiles[ti];
             if (tr.lm != cur) {
                 flush();
                 if (cur >= 0) part = 0;  // a landmark that starts in this run
@@ -1412,9 +1428,20 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
                 valid = o < k;
                 g = o >> 5;
                 ng = valid ? min(32, k - 32 * g) : 1;
-                if (valid) cam = __ldg(d.obs_cam + tr.obs0 + o);  // (first observation carried by the tile)
+                if (LPA && pf_state > 0 && pf_obs0 == tr.obs0) {
+                    cam = pf_cam;
 #pragma unroll
-                for (int q = 0; q < 9; q++) vo[q] = (PRECOND || !valid) ? 0.f : __ldg(v + 9 * cam + q);
+                    for (int q = 0; q < 9; q++)
+                        vo[q] = (PRECOND || !valid) ? 0.f : (pf_state == 2 ? pf_v[q] : __ldg(v + 9 * cam + q));
+                } else {
+                    if (valid) cam = __ldg(d.obs_cam + tr.obs0 + o);  // (first observation carried by the tile)
+#pragma unroll
+                    for (int q = 0; q < 9; q++) vo[q] = (PRECOND || !valid) ? 0.f : __ldg(v + 9 * cam + q);
+                }
+                // the following landmark of the class starts at observation obs0 + k
+                pf_state = 0;
+                pf_obs0 = tr.obs0 + k;
+                if (LPA && pf_obs0 + o < d.n_obs) pf_cam = __ldg(d.obs_cam + pf_obs0 + o), pf_state = 1;
                 if (PRECOND) {
 #pragma unroll
                     for (int q = 0; q < 45; q++) P[q] = 0.f;
@@ -1424,6 +1451,10 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
 #pragma unroll
                     for (int q = 0; q < 9; q++) acc[q] = 0.f;
                 }
+            } else if (LPA && !PRECOND && pf_state == 1) {  // second step of the prefetch: v of that camera
+#pragma unroll
+                for (int q = 0; q < 9; q++) pf_v[q] = __ldg(v + 9 * pf_cam + q);
+                pf_state = 2;
             }
         }
         mbar_wait(&full[s], ph);
