@@ -337,7 +337,11 @@ __global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProb
     float spc[9];
     if (act) {
         const int64_t o = (int64_t)pack.obs0 + grp * k + gl;
+#if RBA_K2_EXP == 5  // measurement experiment: no dependent camera-index load
+        cam = (int)(o % d.n_p);
+#else
         cam = __ldg(d.obs_cam + o);
+#endif
 #pragma unroll
         for (int q = 0; q < 9; q++) spc[q] = __ldg(d.sp + 9 * cam + q);  // issued with the camera loads
         double c[CAMPRE], rd[2];
@@ -378,6 +382,12 @@ __global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProb
     }
     // ---- Householder QR of the 2k x 3 landmark Jacobian, reading C4 for the sign
     float V[2][3], tau[3];
+#if RBA_K2_EXP == 3  // measurement experiment: no Householder reductions (trivial reflectors)
+    for (int c = 0; c < 3; c++) {
+        tau[c] = 1.f;
+        for (int rr = 0; rr < 2; rr++) V[rr][c] = X[rr][c];
+    }
+#else
 #pragma unroll
     for (int c = 0; c < 3; c++) {
         float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
@@ -418,6 +428,7 @@ __global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProb
             else if (a > c) X[rr][c] = 0.f;
         }
     }
+#endif
     // ---- compact WY: T upper 3x3 (Q = I - V T V^T, Q^T = I - V T^T V^T)
     float p01 = 0.f, p02 = 0.f, p12 = 0.f;
 #pragma unroll
@@ -534,7 +545,7 @@ __global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProb
     }  // act
     fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk copy
     __syncwarp();
-    if (lane == 0)
+    if (lane == 0 && RBA_K2_EXP != 4)  // (EXP 4: measurement experiment, no side-region store)
         bulk_s2g(d.arena + d.lm_side[pack.lm0], sside, 4u * (uint32_t)(pack.np * side_floats(k))),
             bulk_commit_wait_read();
 }
