@@ -492,62 +492,69 @@ __global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProb
         }
         return;
     }
-    // ---- emission (write-only stream, Fig. 2c) in the pack layout; side regions via smem
+    // ---- side regions first (R1 rows, TL, q copy, Givens, scaling: the damping values die here,
+    // which frees their registers for the emission), assembled in shared memory and written by one
+    // bulk store that overlaps the emission; then the emission (write-only stream, Fig. 2c)
+    // in the pack layout
     float *blk_side = sside + grp * (int)side_floats(k);
     if (act) {
-    float2 *A = reinterpret_cast<float2 *>(d.arena + pack.base);
-    RBA_CHECK(pack.base >= 0 && pack.base + small_pack_floats(k, pack.np) <= d.arena_n && d.lm_side[pack.lm0] +
-              pack.np * side_floats(k) <= d.arena_n);
-    const int npk = pack.np * k, mo = grp * k + gl;
-    float2 *Ap = A + mo;
-    for (int p = 0; p < (RBA_K2_EXP == 1 ? 0 : k); p++, Ap += 9 * npk) {  // (EXP 1: no R2 emission)
-        float v18[18];
-        if (p < k - 2) {  // rows 2p+3, 2p+4 < 2k: no damping rows
-            wy_row_plain(B, VR[2 * p + 3], 2 * p + 3, gl, v18);
-            wy_row_plain(B, VR[2 * p + 4], 2 * p + 4, gl, v18 + 9);
-        } else {
-            wy_row(B, VR, GM, k, 2 * p + 3, gl, v18);
-            wy_row(B, VR, GM, k, 2 * p + 4, gl, v18 + 9);
-        }
-#pragma unroll
-        for (int c = 0; c < 9; c++) Ap[c * npk] = make_float2(v18[2 * c], v18[2 * c + 1]);
-    }
-#pragma unroll
-    for (int s = 0; s < 3; s++) {
-        float v9[9];
-        wy_row(B, VR, GM, k, s, gl, v9);
-#pragma unroll
-        for (int q = 0; q < 9; q++) blk_side[s * 9 * k + 9 * gl + q] = v9[q];
-    }
-    float4 *TL = reinterpret_cast<float4 *>(blk_side + side_tl(k));
-    float *qc = d.qpk + pack.q0 + 2 * k * grp - 3;  // q copy, row a at qc[a] (a >= 3)
-#pragma unroll
-    for (int rr = 0; rr < 2; rr++) {
-        const int a = 2 * gl + rr;
-        if (a >= 3) TL[a] = make_float4(0.f, 0.f, 0.f, rv[rr]), qc[a] = rv[rr];
-    }
-    if (gl == 0) {
 #pragma unroll
         for (int s = 0; s < 3; s++) {
-            TL[s] = make_float4(L6[s * 3], L6[s * 3 + 1], L6[s * 3 + 2], rr6[s]);
-            TL[2 * k + s] = make_float4(0.f, 0.f, 0.f, rr6[3 + s]);
-            qc[2 * k + s] = rr6[3 + s];
+            float v9[9];
+            wy_row(B, VR, GM, k, s, gl, v9);
+#pragma unroll
+            for (int q = 0; q < 9; q++) blk_side[s * 9 * k + 9 * gl + q] = v9[q];
         }
-        float *gp = blk_side + side_g(k);
+        float4 *TL = reinterpret_cast<float4 *>(blk_side + side_tl(k));
+        float *qc = d.qpk + pack.q0 + 2 * k * grp - 3;  // q copy, row a at qc[a] (a >= 3)
 #pragma unroll
-        for (int i = 0; i < 12; i++) gp[i] = g[i];
+        for (int rr = 0; rr < 2; rr++) {
+            const int a = 2 * gl + rr;
+            if (a >= 3) TL[a] = make_float4(0.f, 0.f, 0.f, rv[rr]), qc[a] = rv[rr];
+        }
+        if (gl == 0) {
 #pragma unroll
-        for (int q = 0; q < 3; q++) {
-            d.lm_s[3 * j + q] = sl[q];
-            d.lm_D[3 * j + q] = Dl[q];
+            for (int s = 0; s < 3; s++) {
+                TL[s] = make_float4(L6[s * 3], L6[s * 3 + 1], L6[s * 3 + 2], rr6[s]);
+                TL[2 * k + s] = make_float4(0.f, 0.f, 0.f, rr6[3 + s]);
+                qc[2 * k + s] = rr6[3 + s];
+            }
+            float *gp = blk_side + side_g(k);
+#pragma unroll
+            for (int i = 0; i < 12; i++) gp[i] = g[i];
+#pragma unroll
+            for (int q = 0; q < 3; q++) {
+                d.lm_s[3 * j + q] = sl[q];
+                d.lm_D[3 * j + q] = Dl[q];
+            }
         }
     }
-    }  // act
     fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk copy
     __syncwarp();
-    if (lane == 0 && RBA_K2_EXP != 4)  // (EXP 4: measurement experiment, no side-region store)
-        bulk_s2g(d.arena + d.lm_side[pack.lm0], sside, 4u * (uint32_t)(pack.np * side_floats(k))),
-            bulk_commit_wait_read();
+    if (lane == 0 && RBA_K2_EXP != 4) {  // (EXP 4: measurement experiment, no side-region store)
+        bulk_s2g(d.arena + d.lm_side[pack.lm0], sside, 4u * (uint32_t)(pack.np * side_floats(k)));
+        bulk_commit();
+    }
+    if (act) {
+        float2 *A = reinterpret_cast<float2 *>(d.arena + pack.base);
+        RBA_CHECK(pack.base >= 0 && pack.base + small_pack_floats(k, pack.np) <= d.arena_n && d.lm_side[pack.lm0] +
+                  pack.np * side_floats(k) <= d.arena_n);
+        const int npk = pack.np * k, mo = grp * k + gl;
+        float2 *Ap = A + mo;
+        for (int p = 0; p < (RBA_K2_EXP == 1 ? 0 : k); p++, Ap += 9 * npk) {  // (EXP 1: no R2 emission)
+            float v18[18];
+            if (p < k - 2) {  // rows 2p+3, 2p+4 < 2k: no damping rows
+                wy_row_plain(B, VR[2 * p + 3], 2 * p + 3, gl, v18);
+                wy_row_plain(B, VR[2 * p + 4], 2 * p + 4, gl, v18 + 9);
+            } else {
+                wy_row(B, VR, GM, k, 2 * p + 3, gl, v18);
+                wy_row(B, VR, GM, k, 2 * p + 4, gl, v18 + 9);
+            }
+#pragma unroll
+            for (int c = 0; c < 9; c++) Ap[c * npk] = make_float2(v18[2 * c], v18[2 * c + 1]);
+        }
+    }
+    if (lane == 0 && RBA_K2_EXP != 4) bulk_wait_read();  // the side buffer is read before the CTA exits
 }
 
 // ============================================================================ K2 large (k > 32)
@@ -573,7 +580,7 @@ __device__ __forceinline__ void block_jp(const DevProblem &d, int64_t obs0, int 
 }
 
 template <int NT, bool MULTI>
-__global__ void __launch_bounds__(NT) k_marg_large(DevProblem d, const LargeItem *__restrict__ items, float dmin,
+__global__ void __launch_bounds__(NT, (NT < 512 ? 512 / NT : 1)) k_marg_large(DevProblem d, const LargeItem *__restrict__ items, float dmin,
                                                    float dmax) {
     extern __shared__ float4 smem4[];
     __shared__ float red[32 * 4];
@@ -703,8 +710,14 @@ __global__ void __launch_bounds__(NT) k_marg_large(DevProblem d, const LargeItem
     float L6[18], Gm[18], rr6[6], g[12];
     damp_rotations(R, rr3, sD, L6, Gm, rr6, g);
     __syncthreads();  // all reads of VR rows 0..2 done
-    if (tid < 6) VR[tid < 3 ? tid : 2 * k + tid - 3] = veff(Gm, V3, tid);
-    if (tid < 18) GM[tid] = Gm[tid];
+    // (compile-time indices only: a thread-indexed access would put Gm / L6 / g / sl / Dl in local
+    // memory -- round 1 had a 288-byte stack frame here)
+    if (tid == 0) {
+#pragma unroll
+        for (int s6 = 0; s6 < 6; s6++) VR[s6 < 3 ? s6 : 2 * k + s6 - 3] = veff(Gm, V3, s6);
+#pragma unroll
+        for (int i = 0; i < 18; i++) GM[i] = Gm[i];
+    }
     __syncthreads();
     if (d.fac) {  // factored storage: the factors instead of the dense block (one item per landmark)
         float *base = d.arena + d.lm_r2[j];
@@ -719,11 +732,28 @@ __global__ void __launch_bounds__(NT) k_marg_large(DevProblem d, const LargeItem
             fac_write_obs(base + 44 + 28 * o, B, v0, v1, SR[2 * o], SR[2 * o + 1]);
         }
         if (tid == 0) fac_write_hdr(base, R, T00, T01, T02, T11, T12, T22, g, L6, rr6);
-        if (tid < 3) {
-            d.lm_s[3 * j + tid] = sl[tid];
-            d.lm_D[3 * j + tid] = Dl[tid];
-        }
+        if (tid == 0)
+#pragma unroll
+            for (int q = 0; q < 3; q++) d.lm_s[3 * j + q] = sl[q], d.lm_D[3 * j + q] = Dl[q];
         return;
+    }
+    // the landmark and residual columns, the Givens and the scaling first: the damping values die
+    // here, freeing their registers for the emission
+    if (it.t0 == 0) {
+        float *side = d.arena + d.lm_side[j];
+        float4 *TL = reinterpret_cast<float4 *>(side + side_tl(k));
+        for (int a = 3 + tid; a < 2 * k; a += NT) TL[a] = make_float4(0.f, 0.f, 0.f, SR[a]);
+        if (tid == 0) {
+#pragma unroll
+            for (int s = 0; s < 3; s++) {
+                TL[s] = make_float4(L6[s * 3], L6[s * 3 + 1], L6[s * 3 + 2], rr6[s]);
+                TL[2 * k + s] = make_float4(0.f, 0.f, 0.f, rr6[3 + s]);
+                d.lm_s[3 * j + s] = sl[s];
+                d.lm_D[3 * j + s] = Dl[s];
+            }
+#pragma unroll
+            for (int i = 0; i < 12; i++) side[side_g(k) + i] = g[i];
+        }
     }
     for (int o = tid; o < k; o += NT) {
         if (MULTI) {  // raw V rows 2o, 2o+1 (VR rows 0..2 now hold V_eff of the damped rows)
@@ -767,19 +797,6 @@ __global__ void __launch_bounds__(NT) k_marg_large(DevProblem d, const LargeItem
                 for (int q = 0; q < 9; q++) side[s * 9 * k + 9 * o + q] = v9[q];
             }
         }
-    }
-    if (it.t0 == 0) {
-        float *side = d.arena + d.lm_side[j];
-        float4 *TL = reinterpret_cast<float4 *>(side + side_tl(k));
-        for (int a = 3 + tid; a < 2 * k; a += NT) TL[a] = make_float4(0.f, 0.f, 0.f, SR[a]);
-        if (tid < 3) {
-            const int s = tid;
-            TL[s] = make_float4(L6[s * 3], L6[s * 3 + 1], L6[s * 3 + 2], rr6[s]);
-            TL[2 * k + s] = make_float4(0.f, 0.f, 0.f, rr6[3 + s]);
-            d.lm_s[3 * j + s] = sl[s];
-            d.lm_D[3 * j + s] = Dl[s];
-        }
-        if (tid < 12) side[side_g(k) + tid] = g[tid];
     }
 }
 
