@@ -469,3 +469,29 @@ def test_bal_ingest_end_to_end(tmp_path):
     o = oracle.Oracle(q)
     o.set_huber(1.0)
     lm_parity(s, o, 5)
+
+
+def test_lm_report_phases_and_launch_accounting():
+    """rba_lm_report (time, trust region, #CG, memory per iteration): the device-timed
+    phases of an attempt add up to its total, relinearized attempts spend time in K1 and re-damped
+    ones do not, the memory field is the context's device bytes; kernel launches are counted for
+    the graph's executed kernel nodes."""
+    from paper_2103_01843_b200 import rba
+    rng = np.random.default_rng(33)
+    ks = REDAMP_KS[:12] + list(rng.integers(2, 10, 300))
+    p = synth.make_tracks(33, ks, n_p=120, pt_noise=1.0, cam_noise=0.05)  # (rejections first)
+    s = _solver(p)
+    l0 = s.launches()
+    reps = s.lm_solve(6, 0.0)
+    assert s.launches() - l0 > 20 * len(reps)
+    mem = rba.rba_device_bytes(s.h)
+    for r in reps:
+        parts = r["t_linearize_ms"] + r["t_marginalize_ms"] + r["t_precond_ms"] + r["t_pcg_ms"] + r["t_trial_ms"]
+        assert 0 < parts <= r["t_total_ms"] * (1 + 1e-9) and parts >= 0.5 * r["t_total_ms"], r
+        assert r["device_bytes"] == mem > 0
+        if r["relinearized"]:
+            assert r["t_linearize_ms"] > 0
+        else:
+            assert r["t_linearize_ms"] == 0
+    assert any(not r["relinearized"] for r in reps) and reps[0]["relinearized"]
+    assert [r["iter"] for r in reps] == list(range(6))
