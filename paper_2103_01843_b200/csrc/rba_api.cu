@@ -348,7 +348,9 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
         while (pos < nl && c->h_k[pos] <= bounds[cls]) {
             const int k = c->h_k[pos];
             int np = 0;
-            while (pos + np < nl && np < NG && c->h_k[pos + np] == k) np++;
+            while (pos + np < nl && np < NG && c->h_k[pos + np] == k &&
+                   4 * small_pack_floats(k, np + 1) <= SMALL_STAGE_BYTES)  // (a pack fits a pipeline stage)
+                np++;
             packs.push_back(Pack{(int32_t)pos, np, r2_total, h_obs0[pos], k, (int32_t)q_total, 0});
             for (int m = 0; m < np; m++) {
                 c->h_r2[pos + m] = r2_total;
