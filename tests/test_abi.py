@@ -117,3 +117,33 @@ def test_layout_constants_match_paper_block_size():
         logical = (2 * k + 3) * (9 * k + 4) + 12
         extra = r2 + side - logical
         assert 0 <= extra <= 3 + (18 * k if (k > 32 and k % 2) else 0)
+
+
+def test_null_context_and_bad_arguments_are_rejected_without_a_gpu():
+    """Every entry point added for the device-side LM loop, the replay rule and the measurement
+    hooks validates its arguments on the host: a null context / null output is INVALID_ARG."""
+    import ctypes as C
+    L = rba.lib()
+    d, i64, n = C.c_double(), C.c_int64(), C.c_int()
+    assert L.rba_lm_step(None, None) == rba.RBA_ERR_INVALID_ARG
+    assert L.rba_lm_solve(None, 5, 1e-6, None, C.byref(n)) == rba.RBA_ERR_INVALID_ARG
+    assert L.rba_set_lm(None, 1e-4, 2.0) == rba.RBA_ERR_INVALID_ARG
+    assert L.rba_get_lm(None, C.byref(d), C.byref(d), C.byref(i64)) == rba.RBA_ERR_INVALID_ARG
+    assert L.rba_set_pcg_limits(None, 1e-2, 500) == rba.RBA_ERR_INVALID_ARG
+    assert L.rba_device_bytes(None, C.byref(i64)) == rba.RBA_ERR_INVALID_ARG
+    assert L.rba_plan_bytes(None, C.byref(d), C.byref(d)) == rba.RBA_ERR_INVALID_ARG
+    assert L.rba_get_info(None, C.byref(rba.rba_info())) == rba.RBA_ERR_INVALID_ARG
+    assert L.rba_checksums(None, (C.c_uint64 * 4)()) == rba.RBA_ERR_INVALID_ARG
+    assert L.rba_get_precond(None, None) == rba.RBA_ERR_INVALID_ARG
+
+
+def test_deterministic_option_validated_on_the_host():
+    """deterministic = 1 only for dense FP32 sqrt-BA (rba.h), rejected before any device work."""
+    p = _prob()
+    for field, value in (("storage", 1), ("precision", 1), ("solver", 1)):
+        o = rba.rba_default_options()
+        o.deterministic = 1
+        setattr(o, field, value)
+        with pytest.raises(rba.RBAError) as ei:
+            rba.rba_create(p["cameras_init"], p["points_init"], p["obs_cam"], p["obs_pt"], p["obs_uv"], o)
+        assert ei.value.status == rba.RBA_ERR_INVALID_ARG
