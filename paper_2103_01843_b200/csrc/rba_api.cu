@@ -445,12 +445,19 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
         c->marg_lo[cls] = (int64_t)marg_items.size();
         const int64_t t_lo = (int64_t)tiles.size();
         double bytes = 0;
+        // K2 work item: ~item_floats of emitted output (the O(k) prologue is recomputed per item):
+        // 4 MB, but at least ~2 items per SM for a class too small to fill the GPU otherwise (a
+        // single 2.8-MB item of a k = 196 track on one CTA was the tail of config 3's K2)
+        double cls_floats = 0;
+        for (int64_t i = large_lo; i < nl; i++)
+            if (in_cls(c->h_k[i])) cls_floats += large_r2_floats(c->h_k[i]);
+        const int64_t item_floats = getenv("RBA_MARG_ITEM_FLOATS") ? marg_item_floats :
+            std::min<int64_t>(marg_item_floats, std::max<int64_t>(131072, (int64_t)(cls_floats / (2.0 * c->num_sms))));
         for (int64_t i = large_lo; i < nl; i++) {
             const int k = c->h_k[i];
             if (!in_cls(k)) continue;
             const int T = large_tiles(k);
-            // K2 work item: ~marg_item_floats of emitted output (the O(k) prologue is recomputed per item)
-            const int tpi2 = opt.storage ? T : (int)std::max<int64_t>(1, marg_item_floats / (36 * k));
+            const int tpi2 = opt.storage ? T : (int)std::max<int64_t>(1, item_floats / (36 * k));
             for (int t0 = 0; t0 < T; t0 += tpi2)
                 marg_items.push_back(LargeItem{(int32_t)i, t0, std::min(T, t0 + tpi2), 0});
             if (cls == 5) {
@@ -840,6 +847,17 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     }
     CKSC(dalloc_n(c, &d.reps, rba_ctx::REP_CAP));
     CKSC(dalloc_n(c, &d.packs, std::max<size_t>(1, packs.size())));
+    {  // 17 <= k <= 32 with dense FP32 storage: K2 warp per landmark (k_marg_small<32>, tile layout)
+        std::vector<Pack> mid;
+        if (!opt.storage && !opt.precision && !opt.solver && !getenv("RBA_NO_MID_K2"))
+            for (int64_t i = large_lo; i < nl; i++)
+                if (c->h_k[i] <= 32) mid.push_back(Pack{(int32_t)i, 1, c->h_r2[i], h_obs0[i], c->h_k[i], 0, 0});
+        c->n_mid_packs = (int64_t)mid.size();
+        CKSC(dalloc_n(c, &d.mid_packs, std::max<size_t>(1, mid.size())));
+        if (!mid.empty())
+            CKC(cudaMemcpyAsync(d.mid_packs, mid.data(), sizeof(Pack) * mid.size(), cudaMemcpyHostToDevice, c->stream));
+        CKC(cudaStreamSynchronize(c->stream));
+    }
     CKSC(dalloc_n(c, &d.marg_items, std::max<size_t>(1, marg_items.size())));
     CKSC(dalloc_n(c, &d.tiles, std::max<size_t>(1, tiles.size())));
     CKSC(dalloc_n(c, &d.cta_lo, std::max<size_t>(1, cta_lo.size())));

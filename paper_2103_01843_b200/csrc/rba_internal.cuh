@@ -199,6 +199,7 @@ struct DevProblem {
     rba_lm_report *reps;      // device reports of the iterations of one rba_lm_step / rba_lm_solve call
     double *pcg_part;  // per-CTA partial dot products of the PCG update kernels (fixed-order sums)
     Pack *packs;            // small-k packs, classes G = 2, 4, 8, 16 back to back
+    Pack *mid_packs;        // 17 <= k <= 32 (dense FP32): one landmark per "pack" for k_marg_small<32>
     uint16_t *units;        // small-k work units per stage
     LargeItem *marg_items;  // K2 work items (~1 MB of output each), classes NT = 64, 128, 256, 512
     TileRef *tiles;         // K4/K5 tile stream of the large landmarks, classes k <= 32, 64, 128, 256, 512
@@ -289,6 +290,7 @@ struct rba_ctx {
     int64_t run_off[5] = {0, 0, 0, 0, 0};  // deterministic mode: per class offset into d.run_part
     int64_t n_chunks = 0, chunk_ctas = 0;
     int64_t n_packs = 0, max_large_k = 0;
+    int64_t n_mid_packs = 0;  // landmarks marginalized by the warp-per-landmark K2 (17 <= k <= 32)
     int num_sms = 148;
     int64_t arena_floats = 0, logical_bytes = 0;
     double marg_bytes = 0, matvec_bytes = 0;  // algorithmic bytes per launch

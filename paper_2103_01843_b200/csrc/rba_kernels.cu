@@ -194,6 +194,10 @@ __global__ void k_cam_scale(DevProblem d, float dmin, float dmax) {
     d.Dp264[i] = d.Dp2[i];
 }
 
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 // ============================================================================ K2 emission
 // Compact-WY form of the marginalized block (Householder): Q^T = I - V T^T V^T, so every
 // output row L of the pose columns of camera block o is
@@ -307,7 +311,7 @@ template <int G>
 #ifndef RBA_MARG_SMALL_MINB
 #define RBA_MARG_SMALL_MINB 4  // 128 registers: 4 CTAs per SM (measured 3.35 -> 3.22 ms K2 on cfg4)
 #endif
-__global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProblem d, int64_t pk_lo, int64_t pk_hi, float dmin,
+__global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProblem d, const Pack *__restrict__ packs, int64_t pk_lo, int64_t pk_hi, float dmin,
                                                     float dmax) {
     constexpr int NG = 32 / G;
     using TB = SmallTab<G>;
@@ -317,7 +321,7 @@ __global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProb
     const int grp = lane / G, gl = lane % G;
     const int64_t pi = pk_lo + (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
     if (pi >= pk_hi) return;  // warp-uniform
-    const Pack pack = d.packs[pi];
+    const Pack pack = packs[pi];  // (G = 32: one landmark of 17..32 observations, tile layout)
     const bool valid = grp < pack.np;
     const int64_t j = pack.lm0 + (valid ? grp : 0);
     const int k = pack.k;  // (the pack's observations are contiguous: no per-landmark index loads)
@@ -506,18 +510,23 @@ __global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProb
             for (int q = 0; q < 9; q++) blk_side[s * 9 * k + 9 * gl + q] = v9[q];
         }
         float4 *TL = reinterpret_cast<float4 *>(blk_side + side_tl(k));
-        float *qc = d.qpk + pack.q0 + 2 * k * grp - 3;  // q copy, row a at qc[a] (a >= 3)
+        // q copy of the small-k preconditioner pass, row a at qc[a] (a >= 3); G = 32 (tile layout):
+        // the large pipe reads q from TL
+        float *qc = G < 32 ? d.qpk + pack.q0 + 2 * k * grp - 3 : nullptr;
 #pragma unroll
         for (int rr = 0; rr < 2; rr++) {
             const int a = 2 * gl + rr;
-            if (a >= 3) TL[a] = make_float4(0.f, 0.f, 0.f, rv[rr]), qc[a] = rv[rr];
+            if (a >= 3) {
+                TL[a] = make_float4(0.f, 0.f, 0.f, rv[rr]);
+                if (G < 32) qc[a] = rv[rr];
+            }
         }
         if (gl == 0) {
 #pragma unroll
             for (int s = 0; s < 3; s++) {
                 TL[s] = make_float4(L6[s * 3], L6[s * 3 + 1], L6[s * 3 + 2], rr6[s]);
                 TL[2 * k + s] = make_float4(0.f, 0.f, 0.f, rr6[3 + s]);
-                qc[2 * k + s] = rr6[3 + s];
+                if (G < 32) qc[2 * k + s] = rr6[3 + s];
             }
             float *gp = blk_side + side_g(k);
 #pragma unroll
@@ -535,7 +544,33 @@ __global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProb
         bulk_s2g(d.arena + d.lm_side[pack.lm0], sside, 4u * (uint32_t)(pack.np * side_floats(k)));
         bulk_commit();
     }
-    if (act) {
+    if (G == 32 && act) {  // 17 <= k <= 32: the 4-row tile layout of the large pipes (g = 0, n_g = k)
+        float *R2 = d.arena + pack.base;
+        RBA_CHECK(pack.base >= 0 && pack.base + large_r2_floats(k) <= d.arena_n);
+        const int T = large_tiles(k);
+        for (int t = 0; t < (RBA_K2_EXP == 1 ? 0 : T); t++) {
+            float4 *S = reinterpret_cast<float4 *>(R2 + (int64_t)36 * k * t) + gl;
+            float v36[36];
+            if (4 * t + 6 < 2 * k) {  // logical rows 4t+3 .. 4t+6 are plain rows (< 2k)
+#pragma unroll
+                for (int rr = 0; rr < 4; rr++) wy_row_plain(B, VR[4 * t + rr + 3], 4 * t + rr + 3, gl, v36 + 9 * rr);
+            } else {
+#pragma unroll
+                for (int rr = 0; rr < 4; rr++) {
+                    const int a = 4 * t + rr;
+                    if (a < 2 * k) {
+                        wy_row(B, VR, GM, k, a + 3, gl, v36 + 9 * rr);
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 9; q++) v36[9 * rr + q] = 0.f;
+                    }
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < 9; c++)
+                S[c * k] = make_float4(v36[4 * c], v36[4 * c + 1], v36[4 * c + 2], v36[4 * c + 3]);
+        }
+    } else if (G < 32 && act) {
         float2 *A = reinterpret_cast<float2 *>(d.arena + pack.base);
         RBA_CHECK(pack.base >= 0 && pack.base + small_pack_floats(k, pack.np) <= d.arena_n && d.lm_side[pack.lm0] +
                   pack.np * side_floats(k) <= d.arena_n);
@@ -579,19 +614,45 @@ __device__ __forceinline__ void block_jp(const DevProblem &d, int64_t obs0, int 
     }
 }
 
-template <int NT, bool MULTI>
-__global__ void __launch_bounds__(NT, (NT < 512 ? 512 / NT : 1)) k_marg_large(DevProblem d, const LargeItem *__restrict__ items, float dmin,
-                                                   float dmax) {
+// LPC > 1: LPC items (landmarks) per CTA, each on its own NT-thread sub-block synchronized by a
+// named barrier (mid k: more resident landmarks per SM than NT-thread CTAs allow, measured below).
+template <int NT, bool MULTI, int LPC = 1>
+__global__ void __launch_bounds__(NT *LPC, (NT * LPC < 512 ? 512 / (NT * LPC) : 1))
+    k_marg_large(DevProblem d, const LargeItem *__restrict__ items, int64_t n_items, int64_t sub_floats, float dmin,
+                 float dmax) {
     extern __shared__ float4 smem4[];
-    __shared__ float red[32 * 4];
-    __shared__ float piv[4];
-    __shared__ float GM[20];
-    const LargeItem it = items[blockIdx.x];
+    __shared__ float red_all[LPC][32 * 4];
+    __shared__ float piv_all[LPC][4];
+    __shared__ float GM_all[LPC][20];
+    const int sub = LPC > 1 ? (int)threadIdx.x / NT : 0;
+    const int tid = LPC > 1 ? (int)threadIdx.x % NT : (int)threadIdx.x;
+    const int64_t item = (int64_t)blockIdx.x * LPC + sub;
+    if (item >= n_items) return;  // (a whole sub-block: its named barrier is its own)
+    float *red = red_all[sub], *piv = piv_all[sub], *GM = GM_all[sub];
+    auto sync = [&]() {
+        if (LPC > 1) named_sync(1 + sub, NT);
+        else __syncthreads();
+    };
+    // block_sum over the sub-block (warp shuffles, then one value per warp through shared memory)
+    auto sub_sum = [&](float *v, int nv) {
+        const int lane = tid & 31, w = tid >> 5;
+        for (int i = 0; i < nv; i++) v[i] = warp_sum_f(v[i]);
+        sync();
+        if (lane == 0)
+            for (int i = 0; i < nv; i++) red[i * 32 + w] = v[i];
+        sync();
+        for (int i = 0; i < nv; i++) {
+            float s_ = 0.f;
+            for (int w2 = 0; w2 < NT / 32; w2++) s_ += red[i * 32 + w2];
+            v[i] = s_;
+        }
+        sync();
+    };
+    const LargeItem it = items[item];
     const int64_t j = it.lm;
     const int k = d.lm_k[j];
-    const int tid = threadIdx.x;
     const bool own = tid < k;
-    float4 *VR = smem4;                                         // 2k+3
+    float4 *VR = smem4 + (LPC > 1 ? sub * (sub_floats / 4) : 0);  // 2k+3
     float *SX = reinterpret_cast<float *>(VR + (2 * k + 3));    // 2k x 3 landmark Jacobian
     float *SR = SX + 6 * k;                                     // 2k residuals
     const int64_t obs0 = d.lm_obs0[j];
@@ -631,7 +692,7 @@ __global__ void __launch_bounds__(NT, (NT < 512 ? 512 / NT : 1)) k_marg_large(De
         SR[2 * o] = (float)r[0];
         SR[2 * o + 1] = (float)r[1];
     }
-    block_sum<3>(n2, red);
+    sub_sum(n2, 3);
     float sl[3], Dl[3];
 #pragma unroll
     for (int q = 0; q < 3; q++) {
@@ -641,7 +702,7 @@ __global__ void __launch_bounds__(NT, (NT < 512 ? 512 / NT : 1)) k_marg_large(De
     for (int a = tid; a < 2 * k; a += NT)
 #pragma unroll
         for (int q = 0; q < 3; q++) SX[a * 3 + q] *= sl[q];
-    __syncthreads();
+    sync();
     // Householder, 3 reflectors; V kept in VR rows (all rows 0..2k-1 during the prologue)
     float tau[3];
 #pragma unroll
@@ -660,7 +721,7 @@ __global__ void __launch_bounds__(NT, (NT < 512 ? 512 / NT : 1)) k_marg_large(De
             piv[2] = (c + 2 < 3) ? SX[c * 3 + c + 2] : 0.f;
             piv[3] = SR[c];
         }
-        block_sum<4>(s, red);  // contains __syncthreads
+        sub_sum(s, 4);  // (synchronizes)
         const float x0 = piv[0], y1 = piv[1], y2 = piv[2], yr = piv[3];
         const float sig = sqrtf(s[0]);
         const float alpha = x0 >= 0.f ? -sig : sig;
@@ -680,7 +741,7 @@ __global__ void __launch_bounds__(NT, (NT < 512 ? 512 / NT : 1)) k_marg_large(De
             if (a == c) SX[a * 3 + c] = alpha;
             else if (a > c) SX[a * 3 + c] = 0.f;
         }
-        __syncthreads();
+        sync();
     }
     float p[3] = {0.f, 0.f, 0.f};
     for (int a = tid; a < 2 * k; a += NT) {
@@ -689,7 +750,7 @@ __global__ void __launch_bounds__(NT, (NT < 512 ? 512 / NT : 1)) k_marg_large(De
         p[1] += v.x * v.z;
         p[2] += v.y * v.z;
     }
-    block_sum<3>(p, red);
+    sub_sum(p, 3);
     const float T00 = tau[0], T11 = tau[1], T22 = tau[2];
     const float T01 = -tau[1] * T00 * p[0];
     const float T02 = -tau[2] * (T00 * p[1] + T01 * p[2]);
@@ -709,7 +770,7 @@ __global__ void __launch_bounds__(NT, (NT < 512 ? 512 / NT : 1)) k_marg_large(De
     const float sD[3] = {sq * Dl[0], sq * Dl[1], sq * Dl[2]};
     float L6[18], Gm[18], rr6[6], g[12];
     damp_rotations(R, rr3, sD, L6, Gm, rr6, g);
-    __syncthreads();  // all reads of VR rows 0..2 done
+    sync();  // all reads of VR rows 0..2 done
     // (compile-time indices only: a thread-indexed access would put Gm / L6 / g / sl / Dl in local
     // memory -- round 1 had a 288-byte stack frame here)
     if (tid == 0) {
@@ -718,7 +779,7 @@ __global__ void __launch_bounds__(NT, (NT < 512 ? 512 / NT : 1)) k_marg_large(De
 #pragma unroll
         for (int i = 0; i < 18; i++) GM[i] = Gm[i];
     }
-    __syncthreads();
+    sync();
     if (d.fac) {  // factored storage: the factors instead of the dense block (one item per landmark)
         float *base = d.arena + d.lm_r2[j];
         for (int o = tid; o < k; o += NT) {
@@ -996,9 +1057,6 @@ __device__ __forceinline__ float group_sum_rt(float v, int G) {
 }
 __device__ __forceinline__ int group_of(int k) { return k == 2 ? 2 : (k <= 4 ? 4 : (k <= 8 ? 8 : 16)); }
 
-__device__ __forceinline__ void named_sync(int id, int nthreads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
 
 // ---- small k (<= KSMALL): TMA stages of consecutive packs (+ their camera indices, pack headers
 // and a work-unit table); warp <-> unit (pack, <= 4 row pairs), lane <-> (landmark m = lane / G,
@@ -1037,6 +1095,9 @@ constexpr int SP_SB = SP_OFF_HDR + 128;
 #endif
 #ifndef RBA_SP_EXP
 #define RBA_SP_EXP 0  // small-pipe experiment: 1 = no staged camera / pack / unit tables
+#endif
+#ifndef RBA_MARG_LPC64
+#define RBA_MARG_LPC64 1  // K2, 33 <= k <= 64: landmarks per CTA (64-thread sub-blocks, named barriers; measured 2: 74, 4: 83 vs 1: 69 us on cfg 3)
 #endif
 #ifndef RBA_PF_AHEAD
 #define RBA_PF_AHEAD 0  // stages prefetched into L2 beyond the shared-memory ring (measured: slower, 0.29 -> 0.52 ms cfg3)
@@ -2276,24 +2337,25 @@ struct ForkJoin {
 
 template <int G>
 static cudaError_t marg_small_cls(rba_ctx *c, int cls, cudaStream_t st) {
-    const int64_t lo = c->pack_lo[cls], hi = c->pack_hi[cls];
+    const int64_t lo = G == 32 ? 0 : c->pack_lo[cls], hi = G == 32 ? c->n_mid_packs : c->pack_hi[cls];
     if (hi <= lo) return cudaSuccess;
     const size_t sm = (size_t)4 * ((32 / G) * SmallTab<G>::FLOATS + SmallTab<G>::SIDE) * sizeof(float);
-    k_marg_small<G><<<nblk(hi - lo, 4), 128, sm, st>>>(c->d, lo, hi, (float)c->opt.diag_min,
-                                                              (float)c->opt.diag_max);
+    k_marg_small<G><<<nblk(hi - lo, 4), 128, sm, st>>>(c->d, G == 32 ? c->d.mid_packs : c->d.packs, lo, hi,
+                                                              (float)c->opt.diag_min, (float)c->opt.diag_max);
     c->launches++;
     return cudaGetLastError();
 }
 
-template <int NT, bool MULTI = false>
+template <int NT, bool MULTI = false, int LPC = 1>
 static cudaError_t marg_large_cls(rba_ctx *c, int cls, cudaStream_t st) {
     const int64_t lo = c->marg_lo[cls], hi = c->marg_hi[cls];
     if (hi <= lo) return cudaSuccess;
     const int64_t K = MULTI ? (cls == 5 ? c->huge_max_k : KLARGE) : NT;
-    const size_t sm = (size_t)(4 * (2 * K + 3) + 8 * K) * sizeof(float);
-    cudaFuncSetAttribute(k_marg_large<NT, MULTI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k_marg_large<NT, MULTI><<<(unsigned)(hi - lo), NT, sm, st>>>(c->d, c->d.marg_items + lo, (float)c->opt.diag_min,
-                                                                  (float)c->opt.diag_max);
+    const int64_t sub_floats = pad4(4 * (2 * K + 3) + 8 * K);  // per item (sub-block)
+    const size_t sm = (size_t)LPC * sub_floats * sizeof(float);
+    cudaFuncSetAttribute(k_marg_large<NT, MULTI, LPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_marg_large<NT, MULTI, LPC><<<(unsigned)((hi - lo + LPC - 1) / LPC), NT * LPC, sm, st>>>(
+        c->d, c->d.marg_items + lo, hi - lo, sub_floats, (float)c->opt.diag_min, (float)c->opt.diag_max);
     c->launches++;
     return cudaGetLastError();
 }
@@ -2320,8 +2382,13 @@ cudaError_t launch_marginalize(rba_ctx *c) {
     }
     if ((e = marg_large_cls<256>(c, 3, F.s()))) return e;
     if ((e = marg_large_cls<128>(c, 2, F.s()))) return e;
-    if ((e = marg_large_cls<64>(c, 1, F.s()))) return e;
-    if ((e = marg_large_cls<32>(c, 0, F.s()))) return e;
+    if ((e = marg_large_cls<64, false, RBA_MARG_LPC64>(c, 1, F.s()))) return e;
+    // 17 <= k <= 32: warp per landmark (shuffle reductions, 4 landmarks per CTA) when dense FP32
+    if (c->n_mid_packs > 0) {
+        if ((e = marg_small_cls<32>(c, 0, F.s()))) return e;
+    } else if ((e = marg_large_cls<32>(c, 0, F.s()))) {
+        return e;
+    }
     if (!small_first && (e = smalls())) return e;
     F.join();
     P.end();
