@@ -973,52 +973,64 @@ __device__ __forceinline__ void flush54(float *acc, const float *P, const float 
     atomicAdd(a4 + 13, make_float4(b[7], b[8], 0.f, 0.f));
 }
 
-// per camera: P_i + lambda D_p^2 -> Cholesky (FP64) -> inverse M^-1 (FP32, 81); b~ copied out.
-__global__ void k_precond_finalize(DevProblem d, double *bad) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= d.n_p) return;
+// per camera (one warp): P_i + lambda D_p^2 -> Cholesky (FP64) -> inverse M^-1 (FP64, 81); b~
+// copied out.  The block sits in shared memory; column b of L is formed by lanes b..8 (the same
+// left-looking sums, in the same order, as a serial Cholesky), and column c of the inverse by lane c.
+constexpr int FIN_WARPS = 8;
+__global__ void __launch_bounds__(32 * FIN_WARPS) k_precond_finalize(DevProblem d, double *bad) {
+    __shared__ double sP[FIN_WARPS][81];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t i = (int64_t)blockIdx.x * FIN_WARPS + w;
+    if (i >= d.n_p) return;  // (warp-uniform)
+    double *P = sP[w];
     const double lam = d.scal[SC_LAM];
     const double *acc = d.pd + 54 * i;
-    double P[81];
-    int idx = 0;
-    for (int a = 0; a < 9; a++)
-        for (int b = a; b < 9; b++) {
-            P[a * 9 + b] = acc[idx];
-            P[b * 9 + a] = acc[idx];
-            idx++;
-        }
-    for (int a = 0; a < 9; a++) {
-        P[a * 9 + a] += lam * d.Dp264[9 * i + a];
-        d.bt[9 * i + a] = acc[45 + a];  // FP64
+    for (int t = lane; t < 45; t += 32) {  // upper-triangle entry t = (a, b), b >= a, row-major
+        int a = 0, r = t;
+        while (r >= 9 - a) r -= 9 - a, a++;
+        const int b = a + r;
+        double v = acc[t];
+        if (a == b) v += lam * d.Dp264[9 * i + a];
+        P[a * 9 + b] = v;
+        P[b * 9 + a] = v;
     }
-    double L[81];
-    for (int a = 0; a < 81; a++) L[a] = 0.0;
-    bool ok = true;
-    for (int a = 0; a < 9; a++)
-        for (int b = 0; b <= a; b++) {
-            double s = P[a * 9 + b];
-            for (int m = 0; m < b; m++) s -= L[a * 9 + m] * L[b * 9 + m];
-            if (a == b) {
-                if (!(s > 0.0)) ok = false, s = 1.0;
-                L[a * 9 + a] = sqrt(s);
-            } else {
-                L[a * 9 + b] = s / L[b * 9 + b];
-            }
+    if (lane < 9) d.bt[9 * i + lane] = acc[45 + lane];  // FP64
+    __syncwarp();
+    bool ok = true;  // L overwrites the lower triangle of P
+    for (int b = 0; b < 9; b++) {
+        if (lane == b) {
+            double s = P[b * 9 + b];
+            for (int m = 0; m < b; m++) s -= P[b * 9 + m] * P[b * 9 + m];
+            if (!(s > 0.0)) ok = false, s = 1.0;
+            P[b * 9 + b] = sqrt(s);
         }
-    if (!ok) atomicAdd(bad, 1.0);
-    // inverse: solve L L^T X = I column by column
-    for (int col = 0; col < 9; col++) {
+        __syncwarp();
+        if (lane > b && lane < 9) {
+            double s = P[lane * 9 + b];
+            for (int m = 0; m < b; m++) s -= P[lane * 9 + m] * P[b * 9 + m];
+            P[lane * 9 + b] = s / P[b * 9 + b];
+        }
+        __syncwarp();
+    }
+    if (__any_sync(0xffffffffu, !ok) && lane == 0) atomicAdd(bad, 1.0);
+    if (lane < 9) {  // solve L L^T x = e_lane
+        const int col = lane;
         double y[9], x[9];
+#pragma unroll
         for (int a = 0; a < 9; a++) {
             double s = (a == col) ? 1.0 : 0.0;
-            for (int m = 0; m < a; m++) s -= L[a * 9 + m] * y[m];
-            y[a] = s / L[a * 9 + a];
+#pragma unroll
+            for (int m = 0; m < a; m++) s -= P[a * 9 + m] * y[m];
+            y[a] = s / P[a * 9 + a];
         }
+#pragma unroll
         for (int a = 8; a >= 0; a--) {
             double s = y[a];
-            for (int m = a + 1; m < 9; m++) s -= L[m * 9 + a] * x[m];
-            x[a] = s / L[a * 9 + a];
+#pragma unroll
+            for (int m = a + 1; m < 9; m++) s -= P[m * 9 + a] * x[m];
+            x[a] = s / P[a * 9 + a];
         }
+#pragma unroll
         for (int a = 0; a < 9; a++) d.Minv[81 * i + a * 9 + col] = x[a];
     }
 }
@@ -2485,7 +2497,7 @@ cudaError_t launch_precond_rhs(rba_ctx *c) {
 }
 
 cudaError_t launch_precond_finalize(rba_ctx *c) {
-    k_precond_finalize<<<nblk(c->d.n_p, 128), 128, 0, c->stream>>>(c->d, c->d.scal + SC_NSPD);
+    k_precond_finalize<<<nblk(c->d.n_p, FIN_WARPS), 32 * FIN_WARPS, 0, c->stream>>>(c->d, c->d.scal + SC_NSPD);
     c->launches++;
     return cudaGetLastError();
 }
