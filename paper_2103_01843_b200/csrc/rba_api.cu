@@ -91,6 +91,18 @@ static rba_status dalloc(rba_ctx *c, void **p, size_t bytes) {
                                          cudaGetErrorString(e));
         }
     }
+    // stale-memory check (test switch): RBA_POISON_ALLOC=<byte>[:lo:hi] fills every new allocation
+    // (allocation indices lo..hi-1) with that byte, so a kernel that reads memory before writing it
+    // changes the results (tests/test_gpu_deterministic.py compares two poison patterns bitwise)
+    if (const char *pz = getenv("RBA_POISON_ALLOC")) {  // <byte>[:lo:hi[:other byte]]
+        int byte = 0, other = -1;
+        long long plo = 0, phi = -1;
+        const int n = sscanf(pz, "%d:%lld:%lld:%d", &byte, &plo, &phi, &other);
+        const long long idx = (long long)c->allocations.size();
+        const bool in = n >= 1 && idx >= plo && (n < 3 || idx < phi);
+        if (in || other >= 0) cudaMemset(*p, (in ? byte : other) & 255, bytes), cudaDeviceSynchronize();
+        if (getenv("RBA_ALLOC_TRACE")) fprintf(stderr, "rba alloc %lld: %zu bytes\n", idx, bytes);
+    }
     c->allocations.push_back(*p);
     c->device_bytes += (int64_t)bytes;
     return RBA_OK;
@@ -476,7 +488,7 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
                 continue;
             }
             for (int t = 0; t < T; t++)
-                tiles.push_back(TileRef{(int32_t)i, t, c->h_r2[i] + (int64_t)36 * k * t, k, h_obs0[i]});
+                tiles.push_back(TileRef{(int32_t)i, t, c->h_r2[i] + (int64_t)36 * k * t, k, h_obs0[i], 0});
             bytes += 144.0 * k * T;
         }
         c->marg_hi[cls] = (int64_t)marg_items.size();
@@ -925,6 +937,7 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
         if (!huge_out.empty())
             CKC(cudaMemcpyAsync(d.huge_out, huge_out.data(), sizeof(HugeItem) * huge_out.size(),
                                 cudaMemcpyHostToDevice, c->stream));
+        for (TileRef &tr : tiles) tr.tl = c->h_side[tr.lm] + side_tl(tr.k) + 4 * (3 + 4 * (int64_t)tr.t);
         if (!tiles.empty())
             CKC(cudaMemcpyAsync(d.tiles, tiles.data(), sizeof(TileRef) * tiles.size(), cudaMemcpyHostToDevice,
                                 c->stream));

@@ -141,6 +141,7 @@ struct TileRef {
     int32_t lm, t;   // landmark (internal index) and 4-row tile index
     int64_t off;     // float offset of the tile in the arena
     int32_t k, obs0;  // track length (tile bytes = 144 k) and the landmark's first observation
+    int64_t tl;      // float offset of the tile's 4 TL rows 3 + 4t .. 6 + 4t (K4's residual entries)
 };
 
 struct LargeItem {

@@ -589,7 +589,9 @@ __global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProb
             for (int c = 0; c < 9; c++) Ap[c * npk] = make_float2(v18[2 * c], v18[2 * c + 1]);
         }
     }
-    if (lane == 0 && RBA_K2_EXP != 4) bulk_wait_read();  // the side buffer is read before the CTA exits
+    // the side regions must be in global memory before the kernel ends (K4's large pipe, K7 and the
+    // re-damp read them): wait for the bulk store's completion, not only for its source reads
+    if (lane == 0 && RBA_K2_EXP != 4) bulk_wait_all();
 }
 
 // ============================================================================ K2 large (k > 32)
@@ -1111,6 +1113,21 @@ constexpr int SP_SB = SP_OFF_HDR + 128;
 #ifndef RBA_MARG_LPC64
 #define RBA_MARG_LPC64 1  // K2, 33 <= k <= 64: landmarks per CTA (64-thread sub-blocks, named barriers; measured 2: 74, 4: 83 vs 1: 69 us on cfg 3)
 #endif
+#ifndef RBA_LP_EARLY_RELEASE
+// 1: a large-pipe consumer releases its stage right after issuing its shared-memory loads.  Measured
+// WRONG on B200: the TMA refill of the stage (async proxy) can overwrite it before those loads have
+// read it, although mbarrier.arrive is a release -- a warp's contribution then comes from the wrong
+// tile now and then (tools/det_classes.py: k = 150 / 256 tracks, 7-8 of 15 repeated passes differ).
+// 0 (default): release once the loaded values are in use.
+#define RBA_LP_EARLY_RELEASE 0
+#endif
+#ifndef RBA_LP_LANES
+// large pipes: one producer lane per slot, its tile descriptors loaded a batch ahead, lane 0 arms
+// the stage's full barrier with the bytes of all slots (one arrival; an arrival per lane measured
+// the same).  0: one producer thread for all slots (cfg3 K4 0.33 -> 0.28 ms, K5 0.263 -> 0.245 ms
+// with 1)
+#define RBA_LP_LANES 1
+#endif
 #ifndef RBA_PF_AHEAD
 #define RBA_PF_AHEAD 0  // stages prefetched into L2 beyond the shared-memory ring (measured: slower, 0.29 -> 0.52 ms cfg3)
 #endif
@@ -1378,6 +1395,7 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
     // copies are as large as the big-k classes'), slot s takes tile lo + i NSLOT + s; a landmark's
     // partial sums are flushed once per slot that saw it.
     const bool stripe = RBA_STRIPE && !PRECOND && NSLOT > 1 && !d.det;
+    constexpr bool LANES = RBA_LP_LANES != 0;
     const int64_t nst = (hi - lo + NSLOT - 1) / NSLOT;
     if (tid == 0) {
         for (int s = 0; s < C::STAGES; s++) {
@@ -1408,16 +1426,61 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
                 mbar_arrive_expect_tx(&full[s], (uint32_t)c_bytes);
                 bulk_g2s_stream(sm + (size_t)s * C::SB, d.arena + c_off, (uint32_t)c_bytes, &full[s], pol);
             }
-        } else if (tid == C::NC) {
+        } else if (LANES && !stripe && tid < C::NC + NSLOT) {
+            // run mode: producer lane sl streams slot sl's tile run [r0, r1) (one arrival per lane
+            // on the full barrier); its tile descriptors (arena offset, k, TL offset) are loaded in
+            // batches of PD, one batch ahead, so no copy waits on a descriptor load
+            const int sl = tid - C::NC;
+            const uint64_t pol = policy_evict_first();
+            const int64_t r0 = lo + sl * nst, r1 = min(hi, r0 + nst);
+            constexpr int PD = 4;
+            int64_t coff[PD], ctl[PD], noff[PD], ntl[PD];
+            int ck[PD], nk[PD];
+            auto load = [&](int64_t i0) {
+#pragma unroll
+                for (int u = 0; u < PD; u++) {
+                    const int64_t ti = r0 + i0 + u;
+                    nk[u] = 0, noff[u] = 0, ntl[u] = 0;
+                    if (ti < r1) {
+                        const TileRef tr = tiles[ti];
+                        nk[u] = tr.k, noff[u] = tr.off, ntl[u] = PRECOND ? tr.tl : 0;
+                    }
+                }
+            };
+            load(0);
+            for (int64_t i0 = 0; i0 < nst; i0 += PD) {
+#pragma unroll
+                for (int u = 0; u < PD; u++) coff[u] = noff[u], ctl[u] = ntl[u], ck[u] = nk[u];
+                load(i0 + PD);
+#pragma unroll
+                for (int u = 0; u < PD; u++) {
+                    const int64_t i = i0 + u;
+                    if (i >= nst) break;
+                    const int s = (int)(i % C::STAGES);
+                    const uint32_t ph = (uint32_t)((i / C::STAGES) & 1);
+                    mbar_wait(&empty[s], ph ^ 1);
+                    RBA_CHECK(ck[u] <= NS && coff[u] >= 0 && coff[u] + 36 * ck[u] <= d.arena_n);
+                    // one arrival per stage: lane 0 announces the bytes of all slots (a copy that
+                    // lands first only drives the transaction count negative meanwhile)
+                    uint32_t nb = ck[u] ? 144u * (uint32_t)ck[u] + (PRECOND ? 64u : 0u) : 0u;
+#pragma unroll
+                    for (int m = 1; m < NSLOT; m <<= 1) nb += __shfl_xor_sync((1u << NSLOT) - 1u, nb, m);
+                    if (sl == 0) mbar_arrive_expect_tx(&full[s], nb);
+                    if (ck[u]) {
+                        bulk_g2s_stream(sm + (size_t)s * C::SB + (size_t)sl * C::TB, d.arena + coff[u],
+                                        144u * (uint32_t)ck[u], &full[s], pol);
+                        if (PRECOND) bulk_g2s(sm + C::QOFF + ((size_t)s * NSLOT + sl) * 64, d.arena + ctl[u], 64u, &full[s]);
+                    }
+                }
+            }
+        } else if (!LANES && tid == C::NC) {
             const uint64_t pol = policy_evict_first();
             // descriptors (arena offset, k) of the next stage are loaded one stage ahead, as
             // independent loads, so their latency overlaps the wait and the current copies
             int64_t noff[NSLOT], ntl[NSLOT];
             int nk[NSLOT];
             auto tl_off = [&](int64_t ti) -> int64_t {  // float offset of TL rows 3 + 4t .. 6 + 4t
-                if (!PRECOND || ti >= hi) return 0;
-                const TileRef tr = tiles[ti];
-                return d.lm_side[tr.lm] + side_tl(tr.k) + 4 * (3 + 4 * (int64_t)tr.t);
+                return (PRECOND && ti < hi) ? tiles[ti].tl : 0;
             };
             // tiles of stage i + RBA_PF_AHEAD (per slot), prefetched into L2 beyond the ring
             int64_t poff[NSLOT];
@@ -1502,7 +1565,7 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
     // trips (camera index, then v) -- for k <= 64 that stall was longer than the landmark's tiles.
     constexpr bool LPA = RBA_LP_AHEAD && NS <= 128;  // (NS >= 256: landmark changes are rare, registers tight)
     auto tile_of = [&](int64_t i) -> int64_t { return stripe ? lo + i * NSLOT + slot : lo + slot * nst + i; };
-    TileRef tr_n{-1, 0, 0, 0, 0};
+    TileRef tr_n{-1, 0, 0, 0, 0, 0};
     if (nst > 0 && tile_of(0) < hi) tr_n = tiles[tile_of(0)];
     int pf_state = 0, pf_cam = 0;  // 0 none, 1 camera index loaded, 2 camera and v loaded
     int64_t pf_obs0 = -1;
@@ -1514,7 +1577,7 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
         const uint32_t ph = (uint32_t)((i / C::STAGES) & 1);
         const int64_t ti = tile_of(i);
         const bool have = ti < hi;  // uniform over the slot
-        TileRef tr = have ? tr_n : TileRef{-1, 0, 0, 0, 0};
+        TileRef tr = have ? tr_n : TileRef{-1, 0, 0, 0, 0, 0};
         if (LPA && i + 1 < nst && tile_of(i + 1) < hi) tr_n = tiles[tile_of(i + 1)];
         else if (!LPA && have) tr = tiles[ti];
         int64_t stage_off = 0;  // stripe mode: arena offset of the stage's first tile
@@ -1600,8 +1663,13 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
 #pragma unroll
             for (int c = 0; c < 36; c++) sl[c] = 0.f;
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
+        // the stage is released once the values read from it are in use (RBA_LP_EARLY_RELEASE = 1:
+        // right after the loads were issued)
+        auto release = [&]() {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        };
+        if (RBA_LP_EARLY_RELEASE || !have) release();
         if (!have) continue;
         if (PRECOND) {
             if (valid) {
@@ -1611,6 +1679,7 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
                     if (a < 2 * k) acc_rows(P, b, sl + 9 * r, qv[r]);
                 }
             }
+            if (!RBA_LP_EARLY_RELEASE) release();
         } else {
             float y[4];
 #pragma unroll
@@ -1620,6 +1689,7 @@ __global__ void __launch_bounds__(NS *NSLOT + 32, 1)
                 for (int q = 0; q < 9; q++) sacc += sl[9 * r + q] * vo[q];
                 y[r] = sacc;
             }
+            if (!RBA_LP_EARLY_RELEASE) release();
             const float yr = warp_sum4(y[0], y[1], y[2], y[3], lane);
             if ((lane & 7) == 0) red[buf][warp][lane >> 3] = yr;
             if (NS == 32) {
@@ -2324,11 +2394,16 @@ extern double plan_marg_bytes(rba_ctx *c);
 extern double plan_matvec_bytes(rba_ctx *c);
 
 // fork the context stream into the auxiliary streams (independent class kernels) and join back
+// (RBA_NOFORK: everything on the context stream, a diagnostic switch)
+static bool nofork_env() {
+    static const bool v = getenv("RBA_NOFORK") != nullptr;
+    return v;
+}
 struct ForkJoin {
     rba_ctx *c;
     int next = 0;
     bool on;
-    explicit ForkJoin(rba_ctx *c_) : c(c_), on(!c_->nofork) {
+    explicit ForkJoin(rba_ctx *c_) : c(c_), on(!c_->nofork && !nofork_env()) {
         if (!on) return;
         cudaEventRecord(c->ev_fork, c->stream);
         for (int i = 0; i < rba_ctx::NAUX; i++) cudaStreamWaitEvent(c->aux[i], c->ev_fork, 0);
