@@ -879,6 +879,11 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     c->n_huge_y = (int64_t)huge_y.size();
     c->n_huge_out = (int64_t)huge_out.size();
     c->n_huge_fused = (int64_t)huge_fused.size();
+    // the register-resident fused product takes the items of k <= 1024 (2 camera blocks per thread)
+    std::stable_partition(huge_fused.begin(), huge_fused.end(),
+                          [&](const HugeItem &it) { return c->h_k[it.lm] <= 1024; });
+    c->n_huge_reg = std::count_if(huge_fused.begin(), huge_fused.end(),
+                                  [&](const HugeItem &it) { return c->h_k[it.lm] <= 1024; });
     CKSC(dalloc_n(c, &d.huge_fused, std::max<size_t>(1, huge_fused.size())));
     CKSC(dalloc_n(c, &d.huge_y, std::max<size_t>(1, huge_y.size())));
     CKSC(dalloc_n(c, &d.huge_out, std::max<size_t>(1, huge_out.size())));

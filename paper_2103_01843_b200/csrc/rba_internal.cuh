@@ -278,7 +278,7 @@ struct rba_ctx {
     int64_t pack_lo[4] = {0, 0, 0, 0}, pack_hi[4] = {0, 0, 0, 0};  // G = 2, 4, 8, 16 pack ranges
     int64_t marg_lo[6] = {0, 0, 0, 0, 0, 0}, marg_hi[6] = {0, 0, 0, 0, 0, 0};  // K2 large items per class
     int64_t n_huge_y = 0, n_huge_out = 0, huge_max_k = 0;  // k > KLARGE (two-pass matvec)
-    int64_t n_huge_fused = 0;
+    int64_t n_huge_fused = 0, n_huge_reg = 0;  // (items of k <= 1024 first: k_huge_fused<2, true>)
     int64_t fac_lo[5] = {0, 0, 0, 0, 0}, fac_hi[5] = {0, 0, 0, 0, 0};  // factored: G = 2..32 landmark ranges
     int64_t fac_big = 0;  // factored: first landmark with k > 32 (CTA-per-landmark matvec from here)
     int64_t s64_lo[5] = {0, 0, 0, 0, 0}, s64_hi[5] = {0, 0, 0, 0, 0}, s64_kmax[5] = {2, 2, 2, 2, 2};  // sqrt-BA-64 classes

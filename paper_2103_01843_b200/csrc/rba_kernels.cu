@@ -1773,78 +1773,112 @@ __global__ void __launch_bounds__(HUGE_NT) k_huge_y(DevProblem d, const float *_
 // reduction, then out_o += slab^T y from a second read of the same tile, which L2 still holds (a
 // tile is <= 144 KMAX = 442 KB), so HBM sees each tile once.
 constexpr int HUGE_FNT = 512, HUGE_NB = (KMAX + HUGE_FNT - 1) / HUGE_FNT;
+constexpr int HUGE_REG_K = 2 * HUGE_FNT;  // k <= this: the tile stays in registers (NB = 2)
+// Persistent: CTA b takes items b, b + grid, ...; thread 0 keeps the tile two ahead in the CTA's
+// tile sequence (across item boundaries) prefetching into L2.  REG (k <= HUGE_REG_K): the thread's
+// two slabs stay in registers through the CTA reduction, so the second half of the product reads
+// no memory; otherwise they are read again from L2.
+template <int NB, bool REG>
 __global__ void __launch_bounds__(HUGE_FNT, 1) k_huge_fused(DevProblem d, const HugeItem *__restrict__ items,
-                                                            const float *__restrict__ v,
+                                                            int64_t n_items, const float *__restrict__ v,
                                                             const PcgState *__restrict__ st) {
     if (st && st->done) return;
     __shared__ float red[32 * 4];
-    const HugeItem it = items[blockIdx.x];
-    const int64_t j = it.lm;
-    const int k = d.lm_k[j], tid = threadIdx.x;
-    const float *R2 = d.arena + d.lm_r2[j];
-    const int32_t *oc = d.obs_cam + d.lm_obs0[j];
-    float acc[HUGE_NB][9];
+    const int tid = threadIdx.x;
+    // prefetch cursor (thread 0): item pi, tile pt of it
+    int64_t pi = blockIdx.x;
+    int pt = 0, pk = 0, pt1 = 0;
+    const float *pr = nullptr;
+    auto pf_load = [&]() {
+        if (pi < n_items) {
+            const HugeItem q = items[pi];
+            pk = d.lm_k[q.lm], pr = d.arena + d.lm_r2[q.lm], pt = q.t0, pt1 = q.t1;
+        }
+    };
+    auto pf_next = [&]() {  // prefetch the cursor's tile, then advance it
+        if (pi >= n_items) return;
+        bulk_prefetch_l2(pr + (int64_t)36 * pk * pt, 144u * (uint32_t)pk);
+        if (++pt >= pt1) {
+            pi += gridDim.x;
+            pf_load();
+        }
+    };
+    if (tid == 0) {
+        pf_load();
+        pf_next();
+        pf_next();
+    }
+    for (int64_t ii = blockIdx.x; ii < n_items; ii += gridDim.x) {
+        const HugeItem it = items[ii];
+        const int64_t j = it.lm;
+        const int k = d.lm_k[j];
+        const float *R2 = d.arena + d.lm_r2[j];
+        const int32_t *oc = d.obs_cam + d.lm_obs0[j];
+        float acc[NB][9];
 #pragma unroll
-    for (int m = 0; m < HUGE_NB; m++)
+        for (int m = 0; m < NB; m++)
 #pragma unroll
-        for (int q = 0; q < 9; q++) acc[m][q] = 0.f;
-    // the tiles of the item stream into L2 two ahead of the one being processed (TMA prefetch), so
-    // HBM stays busy during the CTA reduction and the second (L2) read of the current tile
-    const uint32_t tb = 144u * (uint32_t)k;  // bytes of one 4 x 9k tile
-    if (tid == 0)
-        for (int t = it.t0; t < min(it.t1, it.t0 + 2); t++) bulk_prefetch_l2(R2 + (int64_t)36 * k * t, tb);
-    for (int t = it.t0; t < it.t1; t++) {
-        if (tid == 0 && t + 2 < it.t1) bulk_prefetch_l2(R2 + (int64_t)36 * k * (t + 2), tb);
-        float y[4] = {0.f, 0.f, 0.f, 0.f};
+            for (int q = 0; q < 9; q++) acc[m][q] = 0.f;
+        for (int t = it.t0; t < it.t1; t++) {
+            if (tid == 0) pf_next();
+            float y[4] = {0.f, 0.f, 0.f, 0.f};
+            float sl[REG ? NB : 1][36];
 #pragma unroll
-        for (int m = 0; m < HUGE_NB; m++) {
-            const int o = tid + m * HUGE_FNT;
-            if (o < k) {
-                const int g = o >> 5, ng = min(32, k - 32 * g);
-                const float4 *S4 = reinterpret_cast<const float4 *>(R2 + (int64_t)36 * k * t + 36 * 32 * g) + (o & 31);
-                const float *vv = v + 9 * (int64_t)oc[o];
-                float sl[36];
+            for (int m = 0; m < NB; m++) {
+                const int o = tid + m * HUGE_FNT;
+                if (o < k) {
+                    const int g = o >> 5, ng = min(32, k - 32 * g);
+                    const float4 *S4 = reinterpret_cast<const float4 *>(R2 + (int64_t)36 * k * t + 36 * 32 * g) + (o & 31);
+                    float *x36 = sl[REG ? m : 0];
 #pragma unroll
-                for (int c = 0; c < 9; c++) {
-                    const float4 x = S4[c * ng];
-                    sl[4 * c] = x.x, sl[4 * c + 1] = x.y, sl[4 * c + 2] = x.z, sl[4 * c + 3] = x.w;
-                }
+                    for (int c = 0; c < 9; c++) {
+                        const float4 x = S4[c * ng];
+                        x36[4 * c] = x.x, x36[4 * c + 1] = x.y, x36[4 * c + 2] = x.z, x36[4 * c + 3] = x.w;
+                    }
+                    const float *vv = v + 9 * (int64_t)oc[o];
 #pragma unroll
-                for (int q = 0; q < 9; q++) {
-                    const float xq = __ldg(vv + q);
+                    for (int q = 0; q < 9; q++) {
+                        const float xq = __ldg(vv + q);
 #pragma unroll
-                    for (int r = 0; r < 4; r++) y[r] += sl[9 * r + q] * xq;
+                        for (int r = 0; r < 4; r++) y[r] += x36[9 * r + q] * xq;
+                    }
                 }
             }
-        }
-        block_sum<4>(y, red);
+            block_sum<4>(y, red);
 #pragma unroll
-        for (int m = 0; m < HUGE_NB; m++) {
-            const int o = tid + m * HUGE_FNT;
-            if (o < k) {
-                const int g = o >> 5, ng = min(32, k - 32 * g);
-                const float4 *S4 = reinterpret_cast<const float4 *>(R2 + (int64_t)36 * k * t + 36 * 32 * g) + (o & 31);
+            for (int m = 0; m < NB; m++) {
+                const int o = tid + m * HUGE_FNT;
+                if (o < k) {
+                    if (REG) {
 #pragma unroll
-                for (int c = 0; c < 9; c++) {
-                    const float4 x = S4[c * ng];  // L2 hit: the tile was read just above
-                    const float e[4] = {x.x, x.y, x.z, x.w};
+                        for (int e = 0; e < 36; e++) acc[m][e % 9] += sl[REG ? m : 0][e] * y[e / 9];
+                    } else {
+                        const int g = o >> 5, ng = min(32, k - 32 * g);
+                        const float4 *S4 =
+                            reinterpret_cast<const float4 *>(R2 + (int64_t)36 * k * t + 36 * 32 * g) + (o & 31);
 #pragma unroll
-                    for (int u = 0; u < 4; u++) {
-                        const int el = 4 * c + u, r = el / 9, q = el % 9;
-                        acc[m][q] += e[u] * y[r];
+                        for (int c = 0; c < 9; c++) {
+                            const float4 x = S4[c * ng];  // L2 hit: the tile was read just above
+                            const float e4[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                            for (int u = 0; u < 4; u++) {
+                                const int el = 4 * c + u, r = el / 9, q = el % 9;
+                                acc[m][q] += e4[u] * y[r];
+                            }
+                        }
                     }
                 }
             }
         }
-    }
-    float *out = d.det ? nullptr : wslice(d);
-    const int64_t ob0 = d.lm_obs0[j];
+        float *out = d.det ? nullptr : wslice(d);
+        const int64_t ob0 = d.lm_obs0[j];
 #pragma unroll
-    for (int m = 0; m < HUGE_NB; m++) {
-        const int o = tid + m * HUGE_FNT;
-        if (o < k) {
-            if (d.det) det_store12(d, (int64_t)d.slot5[ob0 + o] + it.yoff, acc[m]);  // part = item within landmark
-            else flush_cam12(out, oc[o], acc[m]);
+        for (int m = 0; m < NB; m++) {
+            const int o = tid + m * HUGE_FNT;
+            if (o < k) {
+                if (d.det) det_store12(d, (int64_t)d.slot5[ob0 + o] + it.yoff, acc[m]);  // part = item within landmark
+                else flush_cam12(out, oc[o], acc[m]);
+            }
         }
     }
 }
@@ -2509,8 +2543,20 @@ static void pipes_all(rba_ctx *c, const float *v, float *out12, const PcgState *
     static const bool fused_env = !getenv("RBA_HUGE_TWOPASS");
     const bool fused = fused_env || c->d.det;  // (the two-pass product has no deterministic slots)
     if (c->n_huge_fused > 0 && !PRE && fused) {  // k > KLARGE: fused passes (second read from L2)
-        k_huge_fused<<<(unsigned)c->n_huge_fused, HUGE_FNT, 0, F.s()>>>(c->d, c->d.huge_fused, v, st);
-        c->launches++;
+        // items of k <= HUGE_REG_K first; RBA_HUGE_PERSIST: one CTA per SM looping over the items
+        // (default: CTA per item, the block scheduler balances)
+        static const bool persist = getenv("RBA_HUGE_PERSIST") != nullptr;
+        static const bool noreg = getenv("RBA_HUGE_NOREG") != nullptr;
+        const int64_t nr = noreg ? 0 : c->n_huge_reg, ng = c->n_huge_fused - nr;
+        auto grid = [&](int64_t n) { return (unsigned)(persist ? std::min<int64_t>(n, c->num_sms) : n); };
+        if (nr > 0) {
+            k_huge_fused<2, true><<<grid(nr), HUGE_FNT, 0, F.s()>>>(c->d, c->d.huge_fused, nr, v, st);
+            c->launches++;
+        }
+        if (ng > 0) {
+            k_huge_fused<HUGE_NB, false><<<grid(ng), HUGE_FNT, 0, F.s()>>>(c->d, c->d.huge_fused + nr, ng, v, st);
+            c->launches++;
+        }
     } else if (c->n_huge_out > 0) {  // k > KLARGE: two passes, same stream
         cudaStream_t hs = F.s();
         if (!PRE) {
