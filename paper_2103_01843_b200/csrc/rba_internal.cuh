@@ -42,6 +42,9 @@ constexpr int CAMPRE = 24;    // doubles of a camera's precomputed model (R, J_l
 //    per landmark).  A pack is row-pair major: for row pair p (rows 2p, 2p+1), slab chunk c (9
 //    float2 of the 2 x 9 slab of camera block o), landmark m, block o:
 //       float2 index ((p*9 + c)*np*k + m*k + o)
+//    The slab's 18 values (row r, column q) sit in the chunks as: c = 0..3 row 0 (q, q+1) pairs,
+//    c = 4..7 row 1 pairs, c = 8 (row 0 q 8, row 1 q 8) -- so K2 emits each pair with one packed
+//    FP32 FMA (FFMA2) per term and the product reads whole rows (slab_elem below).
 //  * large k (> KSMALL): tiles of 4 rows (rows >= 2k are zero padding), tile t at 36 k t; in a
 //    tile, camera blocks in groups of 32 (n_g = min(32, k - 32 g)); the 4 x 9 slab of block o is
 //    9 float4 chunks:  float4 index (36*32*g)/4 + c*n_g + (o & 31)
@@ -51,9 +54,12 @@ __host__ __device__ constexpr int64_t pad4(int64_t x) { return (x + 3) & ~int64_
 __host__ __device__ inline int large_tiles(int k) { return (k + 1) >> 1; }  // ceil(2k / 4)
 __host__ __device__ inline int64_t small_pack_floats(int k, int np) { return (int64_t)18 * k * k * np; }
 __host__ __device__ inline int64_t large_r2_floats(int k) { return (int64_t)36 * k * large_tiles(k); }
+// slab element (9 r + q) held by half h of small-k chunk c (see above)
+__host__ __device__ constexpr int slab_elem(int c, int h) { return c < 4 ? 2 * c + h : (c < 8 ? 2 * c + 1 + h : 8 + 9 * h); }
 __host__ __device__ inline int64_t small_index(int k, int np, int m, int a, int o, int q) {
-    const int p = a >> 1, e = 9 * (a & 1) + q, c = e >> 1;
-    return ((int64_t)((p * 9 + c) * np + m) * k + o) * 2 + (e & 1);
+    const int p = a >> 1, r = a & 1;
+    const int c = q < 8 ? 4 * r + (q >> 1) : 8, h = q < 8 ? (q & 1) : r;
+    return ((int64_t)((p * 9 + c) * np + m) * k + o) * 2 + h;
 }
 __host__ __device__ inline int64_t large_index(int k, int a, int o, int q) {
     const int t = a >> 2, e = 9 * (a & 3) + q, c = e >> 2;

@@ -244,6 +244,56 @@ __device__ __forceinline__ void wy_row_plain(const BlockWY &B, const float4 V, i
     }
 }
 
+// Packed forms of wy_row_plain / wy_row for the small-k pack layout (rba_internal.cuh): a row's 9
+// values as 4 (q, q+1) pairs + q = 8, each pair one FFMA2 (sm_100 packed FP32 FMA) per term, in
+// the same operation order (so the same rounding) as the scalar plain row.
+struct Row9 {
+    float2 p[4];
+    float e;
+};
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ Row9 wy_negvm(const BlockWY &B, const float4 V) {  // -(V . M[:, q])
+    const float nx = -V.x, ny = -V.y, nz = -V.z;
+    Row9 r;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        const int q = 2 * i;
+        float2 t = __fmul2_rn(f2(nx, nx), f2(B.m[0][q], B.m[0][q + 1]));
+        t = __ffma2_rn(f2(ny, ny), f2(B.m[1][q], B.m[1][q + 1]), t);
+        r.p[i] = __ffma2_rn(f2(nz, nz), f2(B.m[2][q], B.m[2][q + 1]), t);
+    }
+    r.e = fmaf(nz, B.m[2][8], fmaf(ny, B.m[1][8], nx * B.m[0][8]));
+    return r;
+}
+__device__ __forceinline__ void row9_add_jp(Row9 &r, const BlockWY &B, int i) {  // += J_p row i
+#pragma unroll
+    for (int j = 0; j < 4; j++) r.p[j] = __fadd2_rn(r.p[j], f2(B.jp[i][2 * j], B.jp[i][2 * j + 1]));
+    r.e += B.jp[i][8];
+}
+__device__ __forceinline__ Row9 wy_row_plain2(const BlockWY &B, const float4 V, int L, int o) {
+    Row9 r = wy_negvm(B, V);
+    if (o == (L >> 1)) row9_add_jp(r, B, L & 1);
+    return r;
+}
+// damped rows (L < 3 or L >= 2k): V_eff from VR, J_p rows 0..2 mixed by Gm (blocks 0 and 1 only)
+__device__ __forceinline__ Row9 wy_row2(const BlockWY &B, const float4 *VR, const float *GM, int k, int L, int o) {
+    Row9 r = wy_negvm(B, VR[L]);
+    if (L >= 3 && L < 2 * k) {
+        if (o == (L >> 1)) row9_add_jp(r, B, L & 1);
+    } else if (o < 2) {
+        const int s = L < 3 ? L : L - 2 * k + 3;
+        const float c0 = o == 0 ? GM[3 * s] : GM[3 * s + 2], c1 = o == 0 ? GM[3 * s + 1] : 0.f;
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const float2 u = __ffma2_rn(f2(c1, c1), f2(B.jp[1][2 * j], B.jp[1][2 * j + 1]),
+                                        __fmul2_rn(f2(c0, c0), f2(B.jp[0][2 * j], B.jp[0][2 * j + 1])));
+            r.p[j] = __fadd2_rn(r.p[j], u);
+        }
+        r.e += fmaf(c1, B.jp[1][8], c0 * B.jp[0][8]);
+    }
+    return r;
+}
+
 // M column block from V rows 2o, 2o+1 and T (upper 3x3, entries T00..T22)
 __device__ __forceinline__ void wy_m(BlockWY &B, float4 v0, float4 v1, float T00, float T01, float T02, float T11,
                                      float T12, float T22) {
@@ -504,10 +554,11 @@ __global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProb
     if (act) {
 #pragma unroll
         for (int s = 0; s < 3; s++) {
-            float v9[9];
-            wy_row(B, VR, GM, k, s, gl, v9);
+            const Row9 v = wy_row2(B, VR, GM, k, s, gl);
+            float *dst = blk_side + s * 9 * k + 9 * gl;
 #pragma unroll
-            for (int q = 0; q < 9; q++) blk_side[s * 9 * k + 9 * gl + q] = v9[q];
+            for (int j = 0; j < 4; j++) dst[2 * j] = v.p[j].x, dst[2 * j + 1] = v.p[j].y;
+            dst[8] = v.e;
         }
         float4 *TL = reinterpret_cast<float4 *>(blk_side + side_tl(k));
         // q copy of the small-k preconditioner pass, row a at qc[a] (a >= 3); G = 32 (tile layout):
@@ -551,20 +602,28 @@ __global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProb
         for (int t = 0; t < (RBA_K2_EXP == 1 ? 0 : T); t++) {
             float4 *S = reinterpret_cast<float4 *>(R2 + (int64_t)36 * k * t) + gl;
             float v36[36];
+            Row9 rw[4];
             if (4 * t + 6 < 2 * k) {  // logical rows 4t+3 .. 4t+6 are plain rows (< 2k)
 #pragma unroll
-                for (int rr = 0; rr < 4; rr++) wy_row_plain(B, VR[4 * t + rr + 3], 4 * t + rr + 3, gl, v36 + 9 * rr);
+                for (int rr = 0; rr < 4; rr++) rw[rr] = wy_row_plain2(B, VR[4 * t + rr + 3], 4 * t + rr + 3, gl);
             } else {
 #pragma unroll
                 for (int rr = 0; rr < 4; rr++) {
                     const int a = 4 * t + rr;
                     if (a < 2 * k) {
-                        wy_row(B, VR, GM, k, a + 3, gl, v36 + 9 * rr);
+                        rw[rr] = wy_row2(B, VR, GM, k, a + 3, gl);
                     } else {
 #pragma unroll
-                        for (int q = 0; q < 9; q++) v36[9 * rr + q] = 0.f;
+                        for (int j = 0; j < 4; j++) rw[rr].p[j] = make_float2(0.f, 0.f);
+                        rw[rr].e = 0.f;
                     }
                 }
+            }
+#pragma unroll
+            for (int rr = 0; rr < 4; rr++) {
+#pragma unroll
+                for (int j = 0; j < 4; j++) v36[9 * rr + 2 * j] = rw[rr].p[j].x, v36[9 * rr + 2 * j + 1] = rw[rr].p[j].y;
+                v36[9 * rr + 8] = rw[rr].e;
             }
 #pragma unroll
             for (int c = 0; c < 9; c++)
@@ -577,16 +636,22 @@ __global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProb
         const int npk = pack.np * k, mo = grp * k + gl;
         float2 *Ap = A + mo;
         for (int p = 0; p < (RBA_K2_EXP == 1 ? 0 : k); p++, Ap += 9 * npk) {  // (EXP 1: no R2 emission)
-            float v18[18];
+            Row9 r0, r1;
             if (p < k - 2) {  // rows 2p+3, 2p+4 < 2k: no damping rows
-                wy_row_plain(B, VR[2 * p + 3], 2 * p + 3, gl, v18);
-                wy_row_plain(B, VR[2 * p + 4], 2 * p + 4, gl, v18 + 9);
+                r0 = wy_row_plain2(B, VR[2 * p + 3], 2 * p + 3, gl);
+                r1 = wy_row_plain2(B, VR[2 * p + 4], 2 * p + 4, gl);
             } else {
-                wy_row(B, VR, GM, k, 2 * p + 3, gl, v18);
-                wy_row(B, VR, GM, k, 2 * p + 4, gl, v18 + 9);
+                r0 = wy_row2(B, VR, GM, k, 2 * p + 3, gl);
+                r1 = wy_row2(B, VR, GM, k, 2 * p + 4, gl);
             }
+            // chunk order of the pack layout: row 0 pairs, row 1 pairs, (row 0, row 1) q = 8
+            // (32-bit chunk offsets: one IMAD.WIDE per store address instead of a 64-bit add)
+            const unsigned S = (unsigned)npk;
 #pragma unroll
-            for (int c = 0; c < 9; c++) Ap[c * npk] = make_float2(v18[2 * c], v18[2 * c + 1]);
+            for (int c = 0; c < 4; c++) Ap[c * S] = r0.p[c];
+#pragma unroll
+            for (int c = 0; c < 4; c++) Ap[(4 + c) * S] = r1.p[c];
+            Ap[8 * S] = make_float2(r0.e, r1.e);
         }
     }
     // the side regions must be in global memory before the kernel ends (K4's large pipe, K7 and the
@@ -1149,8 +1214,8 @@ __device__ __forceinline__ void small_unit(const DevProblem &d, const float2 *A,
 #pragma unroll
         for (int c = 0; c < 9; c++) {
             const float2 x = valid ? A[((p0 + u) * 9 + c) * npk] : make_float2(0.f, 0.f);
-            sl[u][2 * c] = x.x;
-            sl[u][2 * c + 1] = x.y;
+            sl[u][slab_elem(c, 0)] = x.x;
+            sl[u][slab_elem(c, 1)] = x.y;
         }
     static_assert(!PRECOND, "K4 accumulates whole landmarks in k_small_pipe");
     {
@@ -1320,7 +1385,7 @@ __global__ void __launch_bounds__(SP_WARPS * 32 + 32, 1)
 #pragma unroll
                     for (int c = 0; c < 9; c++) {
                         const float2 x = A[(pp * 9 + c) * npk];
-                        sl[2 * c] = x.x, sl[2 * c + 1] = x.y;
+                        sl[slab_elem(c, 0)] = x.x, sl[slab_elem(c, 1)] = x.y;
                     }
                     acc_rows(P, b, sl, qs[2 * pp]);
                     acc_rows(P, b, sl + 9, qs[2 * pp + 1]);
