@@ -896,20 +896,28 @@ __global__ void __launch_bounds__(NT *LPC, (NT * LPC < 512 ? 512 / (NT * LPC) : 
         for (int t = it.t0; t < (RBA_K2_EXP == 1 ? it.t0 : it.t1); t++) {
             float4 *S = reinterpret_cast<float4 *>(R2 + (int64_t)36 * k * t + 36 * 32 * g_) + (o & 31);
             float v36[36];
+            Row9 rw[4];
             if (4 * t + 6 < 2 * k) {  // logical rows 4t+3 .. 4t+6 are plain rows (< 2k)
 #pragma unroll
-                for (int rr = 0; rr < 4; rr++) wy_row_plain(B, VR[4 * t + rr + 3], 4 * t + rr + 3, o, v36 + 9 * rr);
+                for (int rr = 0; rr < 4; rr++) rw[rr] = wy_row_plain2(B, VR[4 * t + rr + 3], 4 * t + rr + 3, o);
             } else {
 #pragma unroll
                 for (int rr = 0; rr < 4; rr++) {
                     const int a = 4 * t + rr;
                     if (a < 2 * k) {
-                        wy_row(B, VR, GM, k, a + 3, o, v36 + 9 * rr);
+                        rw[rr] = wy_row2(B, VR, GM, k, a + 3, o);
                     } else {
 #pragma unroll
-                        for (int q = 0; q < 9; q++) v36[9 * rr + q] = 0.f;
+                        for (int jj = 0; jj < 4; jj++) rw[rr].p[jj] = make_float2(0.f, 0.f);
+                        rw[rr].e = 0.f;
                     }
                 }
+            }
+#pragma unroll
+            for (int rr = 0; rr < 4; rr++) {
+#pragma unroll
+                for (int jj = 0; jj < 4; jj++) v36[9 * rr + 2 * jj] = rw[rr].p[jj].x, v36[9 * rr + 2 * jj + 1] = rw[rr].p[jj].y;
+                v36[9 * rr + 8] = rw[rr].e;
             }
 #pragma unroll
             for (int c = 0; c < 9; c++)
@@ -919,10 +927,11 @@ __global__ void __launch_bounds__(NT *LPC, (NT * LPC < 512 ? 512 / (NT * LPC) : 
             float *side = d.arena + d.lm_side[j];
 #pragma unroll
             for (int s = 0; s < 3; s++) {
-                float v9[9];
-                wy_row(B, VR, GM, k, s, o, v9);
+                const Row9 v = wy_row2(B, VR, GM, k, s, o);
+                float *dst = side + s * 9 * k + 9 * o;
 #pragma unroll
-                for (int q = 0; q < 9; q++) side[s * 9 * k + 9 * o + q] = v9[q];
+                for (int jj = 0; jj < 4; jj++) dst[2 * jj] = v.p[jj].x, dst[2 * jj + 1] = v.p[jj].y;
+                dst[8] = v.e;
             }
         }
     }
