@@ -80,6 +80,29 @@ def test_blocks_all_buckets(lam):
         _check_block(s.block(j), o.block(j), k)
 
 
+def test_blocks_extreme_damping():
+    """lambda D_l^2 >= 1e30 (the damping Givens' a^2 + b^2 leaves the range of the rsqrt path and
+    K2 takes its hypotf fallback, rba_model.cuh `givens`): every bucket's damped R^1 satisfies
+    R^1^T R^1 = J_l^T J_l + lambda D_l^2 and the reduced rows (A | q) have the oracle's
+    Gram matrix; the reduced product and b~ match the oracle's at the same lambda."""
+    lam = 1e36
+    ks = [2, 3, 4, 5, 8, 9, 12, 16, 17, 31, 32, 33, 40, 63, 64, 100]
+    p = synth.make_tracks(7, ks, n_p=120)
+    s, o = _pair(p, lam)
+    for j, k in enumerate(ks):
+        Bg, Bo = s.block(j), o.block(j)
+        assert np.all(Bg[3:, 9 * k:9 * k + 3] == 0.0)
+        R1g, R1o = Bg[:3, 9 * k:9 * k + 3], Bo[:3, 9 * k:9 * k + 3]
+        assert relf(R1g.T @ R1g, R1o.T @ R1o) <= 1e-4
+        A_g = np.concatenate([Bg[3:, :9 * k], Bg[3:, -1:]], 1)
+        A_o = np.concatenate([Bo[3:, :9 * k], Bo[3:, -1:]], 1)
+        assert relf(A_g.T @ A_g, A_o.T @ A_o) <= 1e-4
+    # b~ = sum_j A_j^T q_j (it does not see lambda D_p^2, which would swamp the product at this lambda)
+    s.pcg()
+    assert o.precond_rhs() == 0
+    assert relf(s.rhs(), o.rhs()) <= 1e-4
+
+
 def test_block_config1():
     p = synth.make_problem(1)
     s, o = _pair(p)
