@@ -25,5 +25,7 @@ for _ in range(a.reps):
     s.linearize()
     s.marginalize(1e-4)
 ms, n, by = rba.rba_profile_get(s.h, "marginalize")
+ms1, n1, _ = rba.rba_profile_get(s.h, "linearize")
+print(f"cfg{a.config} linearize {ms1 / max(n1, 1):.3f} ms; linearize + marginalize {ms1 / max(n1, 1) + ms / n:.3f} ms")
 print(f"cfg{a.config} marginalize {ms / n:.3f} ms  {by / n / (ms / n * 1e-3) / 1e9:.0f} GB/s  "
       f"item_floats={os.environ.get('RBA_MARG_ITEM_FLOATS', 'default')}")
