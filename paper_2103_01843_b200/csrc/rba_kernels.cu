@@ -498,8 +498,6 @@ __global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProb
     const float T01 = -tau[1] * T00 * p01;
     const float T02 = -tau[2] * (T00 * p02 + T01 * p12);
     const float T12 = -tau[2] * T11 * p12;
-    wy_m(B, make_float4(V[0][0], V[0][1], V[0][2], 0.f), make_float4(V[1][0], V[1][1], V[1][2], 0.f), T00, T01,
-         T02, T11, T12, T22);
     if (act) {
 #pragma unroll
         for (int rr = 0; rr < 2; rr++) {
@@ -546,6 +544,10 @@ __global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProb
         }
         return;
     }
+    // M = T^T V^T J_p only now: through the damping its 27 values would be live next to the
+    // rotations' (the kernel's register peak)
+    wy_m(B, make_float4(V[0][0], V[0][1], V[0][2], 0.f), make_float4(V[1][0], V[1][1], V[1][2], 0.f), T00, T01,
+         T02, T11, T12, T22);
     // ---- side regions first (R1 rows, TL, q copy, Givens, scaling: the damping values die here,
     // which frees their registers for the emission), assembled in shared memory and written by one
     // bulk store that overlaps the emission; then the emission (write-only stream, Fig. 2c)
@@ -822,7 +824,7 @@ __global__ void __launch_bounds__(NT *LPC, (NT * LPC < 512 ? 512 / (NT * LPC) : 
     const float T01 = -tau[1] * T00 * p[0];
     const float T02 = -tau[2] * (T00 * p[1] + T01 * p[2]);
     const float T12 = -tau[2] * T11 * p[2];
-    if (!MULTI && own) wy_m(B, VR[2 * tid], VR[2 * tid + 1], T00, T01, T02, T11, T12, T22);
+    // (M = T^T V^T J_p is formed after the damping, below: its 27 values would be live through it)
     // damping (every thread computes the 6 rotations redundantly from smem values)
     float R[9], rr3[3], V3[9];
 #pragma unroll
@@ -884,8 +886,8 @@ __global__ void __launch_bounds__(NT *LPC, (NT * LPC < 512 ? 512 / (NT * LPC) : 
         }
     }
     for (int o = tid; o < k; o += NT) {
-        if (MULTI) {  // raw V rows 2o, 2o+1 (VR rows 0..2 now hold V_eff of the damped rows)
-            block_jp(d, obs0, o, Xp, B);
+        {  // raw V rows 2o, 2o+1 (VR rows 0..2 now hold V_eff of the damped rows)
+            if (MULTI) block_jp(d, obs0, o, Xp, B);
             const float4 v0 = o == 0 ? make_float4(V3[0], V3[1], V3[2], 0.f)
                                      : (o == 1 ? make_float4(V3[6], V3[7], V3[8], 0.f) : VR[2 * o]);
             const float4 v1 = o == 0 ? make_float4(V3[3], V3[4], V3[5], 0.f) : VR[2 * o + 1];
@@ -1846,6 +1848,9 @@ __global__ void __launch_bounds__(HUGE_NT) k_huge_y(DevProblem d, const float *_
 // o = tid + m HUGE_FNT (m < HUGE_NB); per tile the y partials from the tile's slabs (HBM), a CTA
 // reduction, then out_o += slab^T y from a second read of the same tile, which L2 still holds (a
 // tile is <= 144 KMAX = 442 KB), so HBM sees each tile once.
+#ifndef RBA_HUGE_PF_DEFAULT
+#define RBA_HUGE_PF_DEFAULT 0  // 0: two tiles ahead (round-2 measured default)
+#endif
 constexpr int HUGE_FNT = 512, HUGE_NB = (KMAX + HUGE_FNT - 1) / HUGE_FNT;
 constexpr int HUGE_REG_K = 2 * HUGE_FNT;  // k <= this: the tile stays in registers (NB = 2)
 // Persistent: CTA b takes items b, b + grid, ...; thread 0 keeps the tile two ahead in the CTA's
@@ -1855,7 +1860,7 @@ constexpr int HUGE_REG_K = 2 * HUGE_FNT;  // k <= this: the tile stays in regist
 template <int NB, bool REG>
 __global__ void __launch_bounds__(HUGE_FNT, 1) k_huge_fused(DevProblem d, const HugeItem *__restrict__ items,
                                                             int64_t n_items, const float *__restrict__ v,
-                                                            const PcgState *__restrict__ st) {
+                                                            const PcgState *__restrict__ st, int pf_bytes) {
     if (st && st->done) return;
     __shared__ float red[32 * 4];
     const int tid = threadIdx.x;
@@ -1877,10 +1882,10 @@ __global__ void __launch_bounds__(HUGE_FNT, 1) k_huge_fused(DevProblem d, const 
             pf_load();
         }
     };
-    if (tid == 0) {
+    if (tid == 0) {  // keep ~pf_bytes of this CTA's tiles on their way into L2 (at least 2 tiles)
         pf_load();
-        pf_next();
-        pf_next();
+        const int ahead = pk > 0 ? max(2, min(16, pf_bytes / (144 * pk))) : 2;
+        for (int a = 0; a < ahead; a++) pf_next();
     }
     for (int64_t ii = blockIdx.x; ii < n_items; ii += gridDim.x) {
         const HugeItem it = items[ii];
@@ -2621,14 +2626,16 @@ static void pipes_all(rba_ctx *c, const float *v, float *out12, const PcgState *
         // (default: CTA per item, the block scheduler balances)
         static const bool persist = getenv("RBA_HUGE_PERSIST") != nullptr;
         static const bool noreg = getenv("RBA_HUGE_NOREG") != nullptr;
+        // L2 prefetch distance of the fused kernel in bytes per CTA (tuning knob RBA_HUGE_PF)
+        static const int huge_pf = getenv("RBA_HUGE_PF") ? atoi(getenv("RBA_HUGE_PF")) : RBA_HUGE_PF_DEFAULT;
         const int64_t nr = noreg ? 0 : c->n_huge_reg, ng = c->n_huge_fused - nr;
         auto grid = [&](int64_t n) { return (unsigned)(persist ? std::min<int64_t>(n, c->num_sms) : n); };
         if (nr > 0) {
-            k_huge_fused<2, true><<<grid(nr), HUGE_FNT, 0, F.s()>>>(c->d, c->d.huge_fused, nr, v, st);
+            k_huge_fused<2, true><<<grid(nr), HUGE_FNT, 0, F.s()>>>(c->d, c->d.huge_fused, nr, v, st, huge_pf);
             c->launches++;
         }
         if (ng > 0) {
-            k_huge_fused<HUGE_NB, false><<<grid(ng), HUGE_FNT, 0, F.s()>>>(c->d, c->d.huge_fused + nr, ng, v, st);
+            k_huge_fused<HUGE_NB, false><<<grid(ng), HUGE_FNT, 0, F.s()>>>(c->d, c->d.huge_fused + nr, ng, v, st, huge_pf);
             c->launches++;
         }
     } else if (c->n_huge_out > 0) {  // k > KLARGE: two passes, same stream
