@@ -375,6 +375,9 @@ __global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProb
     const bool valid = grp < pack.np;
     const int64_t j = pack.lm0 + (valid ? grp : 0);
     const int k = pack.k;  // (the pack's observations are contiguous: no per-landmark index loads)
+    // the pack's side-region offset, loaded now so the bulk store after the prologue does not wait on it
+    int64_t side_off = 0;
+    if (lane == 0) side_off = __ldg(d.lm_side + pack.lm0);
     const bool act = valid && gl < k;
     float *tab = smem + (warp * NG + grp) * TB::FLOATS;
     float *sside = smem + 4 * NG * TB::FLOATS + warp * TB::SIDE;  // this warp's pack side regions
@@ -594,7 +597,7 @@ __global__ void __launch_bounds__(128, RBA_MARG_SMALL_MINB) k_marg_small(DevProb
     fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk copy
     __syncwarp();
     if (lane == 0 && RBA_K2_EXP != 4) {  // (EXP 4: measurement experiment, no side-region store)
-        bulk_s2g(d.arena + d.lm_side[pack.lm0], sside, 4u * (uint32_t)(pack.np * side_floats(k)));
+        bulk_s2g(d.arena + side_off, sside, 4u * (uint32_t)(pack.np * side_floats(k)));
         bulk_commit();
     }
     if (G == 32 && act) {  // 17 <= k <= 32: the 4-row tile layout of the large pipes (g = 0, n_g = k)
