@@ -1865,8 +1865,15 @@ __global__ void __launch_bounds__(HUGE_FNT, 1) k_huge_fused(DevProblem d, const 
                                                             int64_t n_items, const float *__restrict__ v,
                                                             const PcgState *__restrict__ st, int pf_bytes) {
     if (st && st->done) return;
-    __shared__ float red[32 * 4];
-    const int tid = threadIdx.x;
+    // y partials of the 16 warps, double-buffered so one barrier per tile suffices (a warp can only
+    // rewrite a buffer after the next tile's barrier, i.e. after every warp has read it)
+    __shared__ __align__(16) float red[2][HUGE_FNT / 32][4];
+    // the item's v blocks of this thread's camera blocks, [m][q][tid] (conflict-free), loaded once
+    // per item instead of once per tile
+    extern __shared__ float sv_dyn[];  // [NB][9][HUGE_FNT] (dynamic: NB = 6 exceeds 48 KB)
+    float(*sv)[9][HUGE_FNT] = reinterpret_cast<float(*)[9][HUGE_FNT]>(sv_dyn);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int nt = 0;  // tiles processed (reduction buffer parity)
     // prefetch cursor (thread 0): item pi, tile pt of it
     int64_t pi = blockIdx.x;
     int pt = 0, pk = 0, pt1 = 0;
@@ -1898,9 +1905,16 @@ __global__ void __launch_bounds__(HUGE_FNT, 1) k_huge_fused(DevProblem d, const 
         const int32_t *oc = d.obs_cam + d.lm_obs0[j];
         float acc[NB][9];
 #pragma unroll
-        for (int m = 0; m < NB; m++)
+        for (int m = 0; m < NB; m++) {
 #pragma unroll
             for (int q = 0; q < 9; q++) acc[m][q] = 0.f;
+            const int o = tid + m * HUGE_FNT;
+            if (o < k) {
+                const float *vv = v + 9 * (int64_t)oc[o];
+#pragma unroll
+                for (int q = 0; q < 9; q++) sv[m][q][tid] = __ldg(vv + q);
+            }
+        }
         for (int t = it.t0; t < it.t1; t++) {
             if (tid == 0) pf_next();
             float y[4] = {0.f, 0.f, 0.f, 0.f};
@@ -1917,16 +1931,29 @@ __global__ void __launch_bounds__(HUGE_FNT, 1) k_huge_fused(DevProblem d, const 
                         const float4 x = S4[c * ng];
                         x36[4 * c] = x.x, x36[4 * c + 1] = x.y, x36[4 * c + 2] = x.z, x36[4 * c + 3] = x.w;
                     }
-                    const float *vv = v + 9 * (int64_t)oc[o];
 #pragma unroll
                     for (int q = 0; q < 9; q++) {
-                        const float xq = __ldg(vv + q);
+                        const float xq = sv[m][q][tid];
 #pragma unroll
                         for (int r = 0; r < 4; r++) y[r] += x36[9 * r + q] * xq;
                     }
                 }
             }
-            block_sum<4>(y, red);
+            {  // CTA sum of the 4 row dot products: warp transpose-reduce, one barrier, 16-lane butterfly
+                const float yr = warp_sum4(y[0], y[1], y[2], y[3], lane);
+                const int buf = nt++ & 1;
+                if ((lane & 7) == 0) red[buf][warp][lane >> 3] = yr;
+                __syncthreads();
+                float4 pv = *reinterpret_cast<const float4 *>(&red[buf][lane & (HUGE_FNT / 32 - 1)][0]);
+#pragma unroll
+                for (int mm = HUGE_FNT / 64; mm; mm >>= 1) {
+                    pv.x += __shfl_xor_sync(0xffffffffu, pv.x, mm);
+                    pv.y += __shfl_xor_sync(0xffffffffu, pv.y, mm);
+                    pv.z += __shfl_xor_sync(0xffffffffu, pv.z, mm);
+                    pv.w += __shfl_xor_sync(0xffffffffu, pv.w, mm);
+                }
+                y[0] = pv.x, y[1] = pv.y, y[2] = pv.z, y[3] = pv.w;
+            }
 #pragma unroll
             for (int m = 0; m < NB; m++) {
                 const int o = tid + m * HUGE_FNT;
@@ -2634,11 +2661,15 @@ static void pipes_all(rba_ctx *c, const float *v, float *out12, const PcgState *
         const int64_t nr = noreg ? 0 : c->n_huge_reg, ng = c->n_huge_fused - nr;
         auto grid = [&](int64_t n) { return (unsigned)(persist ? std::min<int64_t>(n, c->num_sms) : n); };
         if (nr > 0) {
-            k_huge_fused<2, true><<<grid(nr), HUGE_FNT, 0, F.s()>>>(c->d, c->d.huge_fused, nr, v, st, huge_pf);
+            constexpr size_t sm2 = (size_t)2 * 9 * HUGE_FNT * sizeof(float);
+            cudaFuncSetAttribute(k_huge_fused<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+            k_huge_fused<2, true><<<grid(nr), HUGE_FNT, sm2, F.s()>>>(c->d, c->d.huge_fused, nr, v, st, huge_pf);
             c->launches++;
         }
         if (ng > 0) {
-            k_huge_fused<HUGE_NB, false><<<grid(ng), HUGE_FNT, 0, F.s()>>>(c->d, c->d.huge_fused + nr, ng, v, st, huge_pf);
+            constexpr size_t smn = (size_t)HUGE_NB * 9 * HUGE_FNT * sizeof(float);
+            cudaFuncSetAttribute(k_huge_fused<HUGE_NB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smn);
+            k_huge_fused<HUGE_NB, false><<<grid(ng), HUGE_FNT, smn, F.s()>>>(c->d, c->d.huge_fused + nr, ng, v, st, huge_pf);
             c->launches++;
         }
     } else if (c->n_huge_out > 0) {  // k > KLARGE: two passes, same stream
