@@ -693,23 +693,26 @@ __global__ void __launch_bounds__(NT *LPC, (NT * LPC < 512 ? 512 / (NT * LPC) : 
     k_marg_large(DevProblem d, const LargeItem *__restrict__ items, int64_t n_items, int64_t sub_floats, float dmin,
                  float dmax) {
     extern __shared__ float4 smem4[];
-    __shared__ float red_all[LPC][32 * 4];
+    __shared__ float red_all[LPC][2][32 * 4];
     __shared__ float piv_all[LPC][4];
     __shared__ float GM_all[LPC][20];
     const int sub = LPC > 1 ? (int)threadIdx.x / NT : 0;
     const int tid = LPC > 1 ? (int)threadIdx.x % NT : (int)threadIdx.x;
     const int64_t item = (int64_t)blockIdx.x * LPC + sub;
     if (item >= n_items) return;  // (a whole sub-block: its named barrier is its own)
-    float *red = red_all[sub], *piv = piv_all[sub], *GM = GM_all[sub];
+    float *piv = piv_all[sub], *GM = GM_all[sub];
+    int nred = 0;  // sub_sum calls (partials buffer parity)
     auto sync = [&]() {
         if (LPC > 1) named_sync(1 + sub, NT);
         else __syncthreads();
     };
-    // block_sum over the sub-block (warp shuffles, then one value per warp through shared memory)
+    // block_sum over the sub-block (warp shuffles, then one value per warp through shared memory);
+    // the partials alternate between two buffers, so one barrier per call suffices (a buffer is
+    // rewritten two calls later, after the intervening call's barrier every thread has passed)
     auto sub_sum = [&](float *v, int nv) {
         const int lane = tid & 31, w = tid >> 5;
+        float *red = red_all[sub][nred++ & 1];
         for (int i = 0; i < nv; i++) v[i] = warp_sum_f(v[i]);
-        sync();
         if (lane == 0)
             for (int i = 0; i < nv; i++) red[i * 32 + w] = v[i];
         sync();
@@ -718,7 +721,6 @@ __global__ void __launch_bounds__(NT *LPC, (NT * LPC < 512 ? 512 / (NT * LPC) : 
             for (int w2 = 0; w2 < NT / 32; w2++) s_ += red[i * 32 + w2];
             v[i] = s_;
         }
-        sync();
     };
     const LargeItem it = items[item];
     const int64_t j = it.lm;
