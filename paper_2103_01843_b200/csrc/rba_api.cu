@@ -443,6 +443,9 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
     const int ntb[6] = {32, 64, 128, 256, 512, KMAX};
     static const int64_t marg_item_floats =
         getenv("RBA_MARG_ITEM_FLOATS") ? atoll(getenv("RBA_MARG_ITEM_FLOATS")) : 1048576;  // 4 MB of output per item (measured: 3.91 -> 3.34 ms on cfg4 vs 1 MB)
+#ifndef RBA_HUGE_ITEM_DEFAULT
+#define RBA_HUGE_ITEM_DEFAULT (1 << 20)  // bytes of tiles per fused huge-product item (tuning knob RBA_HUGE_ITEM_BYTES)
+#endif
     std::vector<HugeItem> huge_y, huge_out, huge_fused;
     int64_t ybuf_n = 0;
     const int64_t large_lo = pos;
@@ -481,7 +484,8 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
                     for (int t0 = 0; t0 < T; t0 += HUGE_TPO)
                         huge_out.push_back(HugeItem{(int32_t)i, o0, t0, std::min(T, t0 + HUGE_TPO), ybuf_n});
                 // fused product items; yoff = the item's index within its landmark (deterministic mode)
-                const int tpf = std::max(1, (1 << 20) / (144 * k));
+                static const int64_t huge_item = getenv("RBA_HUGE_ITEM_BYTES") ? atoll(getenv("RBA_HUGE_ITEM_BYTES")) : RBA_HUGE_ITEM_DEFAULT;
+                const int tpf = (int)std::max<int64_t>(1, huge_item / (144 * k));
                 for (int t0 = 0; t0 < T; t0 += tpf)
                     huge_fused.push_back(HugeItem{(int32_t)i, 0, t0, std::min(T, t0 + tpf), (int64_t)(t0 / tpf)});
                 ybuf_n += 4 * (int64_t)T;
