@@ -1224,41 +1224,51 @@ template <int NRP, bool PRECOND>
 __device__ __forceinline__ void small_unit(const DevProblem &d, const float2 *A, int npk, int p0, int k, int G,
                                            bool valid, int cam, const float *vo, const float *qs,
                                            float *__restrict__ out12, int64_t slot) {
-    float sl[NRP][18];
+    // the slab chunks as stored (rba_internal.cuh): c = 0..3 row-0 (q, q+1) pairs, 4..7 row-1 pairs,
+    // 8 = (row 0, row 1) at q = 8 -- so both products run on packed FP32 FMAs (FFMA2)
+    float2 ch[NRP][9];
 #pragma unroll
     for (int u = 0; u < NRP; u++)
 #pragma unroll
-        for (int c = 0; c < 9; c++) {
-            const float2 x = valid ? A[((p0 + u) * 9 + c) * npk] : make_float2(0.f, 0.f);
-            sl[u][slab_elem(c, 0)] = x.x;
-            sl[u][slab_elem(c, 1)] = x.y;
-        }
+        for (int c = 0; c < 9; c++) ch[u][c] = valid ? A[((p0 + u) * 9 + c) * npk] : make_float2(0.f, 0.f);
     static_assert(!PRECOND, "K4 accumulates whole landmarks in k_small_pipe");
     {
+        float2 v2[4];
+#pragma unroll
+        for (int c = 0; c < 4; c++) v2[c] = make_float2(vo[2 * c], vo[2 * c + 1]);
+        const float v8 = vo[8];
         float y[2 * NRP];
 #pragma unroll
-        for (int u = 0; u < NRP; u++) {
-            float y0 = 0.f, y1 = 0.f;
+        for (int u = 0; u < NRP; u++) {  // y = A v on the unit's 2 rows
+            float2 t0 = make_float2(0.f, 0.f), t1 = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int q = 0; q < 9; q++) {
-                y0 += sl[u][q] * vo[q];
-                y1 += sl[u][9 + q] * vo[q];
+            for (int c = 0; c < 4; c++) {
+                t0 = __ffma2_rn(ch[u][c], v2[c], t0);
+                t1 = __ffma2_rn(ch[u][4 + c], v2[c], t1);
             }
-            y[2 * u] = y0;
-            y[2 * u + 1] = y1;
+            const float2 t8 = __fmul2_rn(ch[u][8], make_float2(v8, v8));
+            y[2 * u] = (t0.x + t0.y) + t8.x;
+            y[2 * u + 1] = (t1.x + t1.y) + t8.y;
         }
         for (int mm = G >> 1; mm; mm >>= 1) {
 #pragma unroll
             for (int i = 0; i < 2 * NRP; i++) y[i] += __shfl_xor_sync(0xffffffffu, y[i], mm, G);
         }
+        float2 a2[4];
+        float a8 = 0.f;
+#pragma unroll
+        for (int c = 0; c < 4; c++) a2[c] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < NRP; u++) {  // out += A^T y
+            const float2 y0 = make_float2(y[2 * u], y[2 * u]), y1 = make_float2(y[2 * u + 1], y[2 * u + 1]);
+#pragma unroll
+            for (int c = 0; c < 4; c++) a2[c] = __ffma2_rn(ch[u][4 + c], y1, __ffma2_rn(ch[u][c], y0, a2[c]));
+            a8 = fmaf(ch[u][8].y, y[2 * u + 1], fmaf(ch[u][8].x, y[2 * u], a8));
+        }
         float acc[9];  // (0 on invalid lanes: their slab is 0)
 #pragma unroll
-        for (int q = 0; q < 9; q++) {
-            float a_ = 0.f;
-#pragma unroll
-            for (int u = 0; u < NRP; u++) a_ += sl[u][q] * y[2 * u] + sl[u][9 + q] * y[2 * u + 1];
-            acc[q] = a_;
-        }
+        for (int c = 0; c < 4; c++) acc[2 * c] = a2[c].x, acc[2 * c + 1] = a2[c].y;
+        acc[8] = a8;
         if (d.det) {
             if (valid) det_store12(d, slot, acc);
             return;
