@@ -49,6 +49,7 @@ rba_status set_error(rba_status s, const std::string &msg) { return fail(s, msg)
 bool use_pcg_graph(rba_ctx *c);
 rba_status run_pcg_loop(rba_ctx *c);
 double plan_marg_bytes(rba_ctx *c) { return c->marg_bytes; }
+double plan_backsub_bytes(rba_ctx *c) { return c->backsub_bytes; }
 double plan_matvec_bytes(rba_ctx *c) { return c->matvec_bytes; }
 
 Prof::Prof(rba_ctx *c_, int kid_, double bytes_) : c(c_), kid(kid_), bytes(bytes_) {
@@ -348,6 +349,11 @@ extern "C" rba_status rba_create(const double *cameras, int64_t n_cams, const do
         c->logical_bytes += (int64_t)(2 * k + 3) * (9 * k + 4) * 4 + 48;
         c->marg_bytes += (double)(2 * k + 3) * (9 * k + 4) * 4 + 48 + 20.0 * k;
         c->matvec_bytes += 72.0 * k * k;
+        // K7: R^1 rows, TL, camera indices, landmark header / point / scaling / D reads, dl + trial writes
+        c->backsub_bytes += 112.0 * k + 148;
+        const int rg = k <= 16 ? 0 : k <= 256 ? 1 : 2;  // K7 regimes (landmarks sorted by k)
+        c->bs_bytes[rg] += 112.0 * k + 148;
+        c->bs_hi[rg] = i + 1;
     }
     // ---- R2 arena: packs of same-k small landmarks (classes G = 2, 4, 8, 16), then large ones
     std::vector<Pack> packs;

@@ -300,7 +300,9 @@ struct rba_ctx {
     int64_t n_mid_packs = 0;  // landmarks marginalized by the warp-per-landmark K2 (17 <= k <= 32)
     int num_sms = 148;
     int64_t arena_floats = 0, logical_bytes = 0;
-    double marg_bytes = 0, matvec_bytes = 0;  // algorithmic bytes per launch
+    double marg_bytes = 0, matvec_bytes = 0, backsub_bytes = 0;
+    double bs_bytes[3] = {0, 0, 0};  // K7 regimes k <= 16 | 16 < k <= 256 | k > 256: bytes, end landmark
+    int64_t bs_hi[3] = {0, 0, 0};  // algorithmic bytes per launch
     std::vector<void *> allocations;
     // pinned host scratch
     double *h_scal = nullptr;

@@ -2368,60 +2368,120 @@ __global__ void __launch_bounds__(1024) k_pcg_step(DevProblem d, cudaGraphCondit
 }
 
 // ============================================================================ K7 back-substitution
-// Warp per landmark (grid-stride), lanes over the flattened 9k pose columns of R1 (coalesced), the
-// three row sums reduced with shuffles; lane 0 solves the 3x3 upper-triangular system.  The
-// model-decrease sums go out once per CTA (not per landmark: same-address FP64 atomics serialize).
-__global__ void __launch_bounds__(256) k_backsub(DevProblem d) {
-    __shared__ double red[32];
-    if (d.pcg->reason == 2) return;  // indefinite attempt: no step (the LM control rejects it)
-    const double lam = d.scal[SC_LAM];
-    const int lane = threadIdx.x & 31;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    double q1 = 0.0, dd = 0.0;
-    constexpr int G = 8;  // lanes per landmark: 4 landmarks per warp and sweep
-    const int gl = lane % G;
-    for (int64_t jb = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * (32 / G); jb < d.n_l;
-         jb += nwarps * (32 / G)) {
-        const int64_t j = jb + lane / G;
-        const bool valid = j < d.n_l;
-        const int k = valid ? d.lm_k[j] : 0;
-        const float *side = d.arena + (valid ? d.lm_side[j] : 0);
+// Landmarks are stored sorted by k, so K7 splits them into three regimes by lanes per landmark,
+// each a block-uniform role of one grid (one wave; blocks per regime in proportion to its bytes):
+// L = 8 for k <= 16 (4 landmarks per warp and sweep), a warp (L = 32) for 16 < k <= 256, a CTA
+// (L = 256) for k > 256.  Lane gl <-> observations o = gl, gl + L, ...: one camera-index load, then
+// the observation's 9 FP64 dp entries and its 3 x 9 R^1 | Q^1^T J_p entries (the lanes of a group
+// read contiguous 36-byte row segments) are independent loads in flight; the three row sums are
+// reduced with shuffles (+ shared memory for L = 256); every lane of the group solves the 3x3
+// upper-triangular system, lanes 0..2 write one component each (their point / scaling entries
+// and the TL rows are loaded with the R^1 rows; the next sweep's header one sweep ahead).  (Round
+// 1: 8 lanes over the flattened 9k columns of every landmark, a division and a dependent
+// camera-index load per element, the longest tracks last on 8 lanes: 0.16 ms on config 3.)  The
+// model-decrease sums go out once per CTA (same-address FP64 atomics serialize).
+#ifndef RBA_BACKSUB_MINB
+#define RBA_BACKSUB_MINB 3
+#endif
+struct BsRange {
+    int64_t lo, hi;  // landmarks of the regime
+    int nb;          // its blocks
+};
+template <int L>
+__device__ __forceinline__ void bs_regime(const DevProblem &d, const BsRange R, int b0, double &q1, double &dd,
+                                          double (*sw)[3]) {
+    constexpr int PB = 256 / L;  // landmarks per block and sweep
+    const int gl = threadIdx.x % L;
+    const int64_t step = (int64_t)R.nb * PB;
+    int64_t j = R.lo + (int64_t)(blockIdx.x - b0) * PB + threadIdx.x / L;
+    int k = 0;
+    int64_t soff = 0, obs0 = 0;
+    if (j < R.hi) k = __ldg(d.lm_k + j), soff = __ldg(d.lm_side + j), obs0 = __ldg(d.lm_obs0 + j);
+    // the loop test is on the warp's first landmark (L = 8) / j itself (L >= 32): warp- resp. block-uniform
+    for (; j - (int64_t)((threadIdx.x & 31) / L) < R.hi; j += step) {
+        const bool valid = j < R.hi;
+        const int qc = gl < 3 ? gl : 0;
+        double pt = 0.0;
+        float lsq = 0.f, lDq = 0.f;
+        if (valid && gl < 3) pt = d.pts[3 * j + qc], lsq = __ldg(d.lm_s + 3 * j + qc), lDq = __ldg(d.lm_D + 3 * j + qc);
+        const float *side = d.arena + soff;
         const int W = 9 * k;
-        const int32_t *oc = d.obs_cam + (valid ? d.lm_obs0[j] : 0);
+        const int32_t *oc = d.obs_cam + obs0;
+        const int kc = valid ? k : 0;
+        {  // next sweep's header
+            const int64_t jn = j + step;
+            k = 0, soff = 0, obs0 = 0;
+            if (jn < R.hi) k = __ldg(d.lm_k + jn), soff = __ldg(d.lm_side + jn), obs0 = __ldg(d.lm_obs0 + jn);
+        }
+        float4 t0 = make_float4(1.f, 0.f, 0.f, 0.f), t1 = make_float4(0.f, 1.f, 0.f, 0.f), t2 = make_float4(0.f, 0.f, 1.f, 0.f);
+        if (valid && gl < 3) {
+            const float4 *TL = reinterpret_cast<const float4 *>(side + side_tl(kc));
+            t0 = __ldg(TL), t1 = __ldg(TL + 1), t2 = __ldg(TL + 2);
+        }
         // FP64 arithmetic on the stored FP32 R^1 | Q^1^T J_p rows (the 3x3 solve amplifies errors by
         // cond(R^1), large for far / short-baseline landmarks)
         double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-        for (int c = gl; c < W; c += G) {
-            const int o = c / 9, q = c - 9 * o;
-            const double v = d.x[9 * (int64_t)oc[o] + q];
-            s0 += (double)side[c] * v;
-            s1 += (double)side[W + c] * v;
-            s2 += (double)side[2 * W + c] * v;
-        }
+        for (int o = gl; o < kc; o += L) {
+            const double *x = d.x + 9 * (int64_t)__ldg(oc + o);
+            const float *r0 = side + 9 * o;
+            float a0[9], a1[9], a2[9];
+            double xv[9];
 #pragma unroll
-        for (int m = G / 2; m; m >>= 1) {
-            s0 += __shfl_xor_sync(0xffffffffu, s0, m, G);
-            s1 += __shfl_xor_sync(0xffffffffu, s1, m, G);
-            s2 += __shfl_xor_sync(0xffffffffu, s2, m, G);
+            for (int q = 0; q < 9; q++) {
+                xv[q] = x[q];
+                a0[q] = __ldg(r0 + q);
+                a1[q] = __ldg(r0 + W + q);
+                a2[q] = __ldg(r0 + 2 * W + q);
+            }
+#pragma unroll
+            for (int q = 0; q < 9; q++) {
+                s0 += (double)a0[q] * xv[q];
+                s1 += (double)a1[q] * xv[q];
+                s2 += (double)a2[q] * xv[q];
+            }
         }
-        if (valid && gl == 0) {
-            const float4 *TL = reinterpret_cast<const float4 *>(side + side_tl(k));
-            const float4 t0 = TL[0], t1 = TL[1], t2 = TL[2];
+        constexpr int WL = L < 32 ? L : 32;
+#pragma unroll
+        for (int m = WL / 2; m; m >>= 1) {
+            s0 += __shfl_xor_sync(0xffffffffu, s0, m, WL);
+            s1 += __shfl_xor_sync(0xffffffffu, s1, m, WL);
+            s2 += __shfl_xor_sync(0xffffffffu, s2, m, WL);
+        }
+        if (L == 256) {  // the 8 warp sums, added in warp order by threads 0..2
+            if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5][0] = s0, sw[threadIdx.x >> 5][1] = s1, sw[threadIdx.x >> 5][2] = s2;
+            __syncthreads();
+            if (threadIdx.x < 3) {
+                s0 = s1 = s2 = 0.0;
+#pragma unroll
+                for (int w = 0; w < 8; w++) s0 += sw[w][0], s1 += sw[w][1], s2 += sw[w][2];
+            }
+            __syncthreads();
+        }
+        if (valid && gl < 3) {  // lanes 0..2 solve and write one component each
             const double b0 = t0.w + s0, b1 = t1.w + s1, b2 = t2.w + s2;
             const double x2 = b2 / t2.z;
             const double x1 = (b1 - t1.z * x2) / t1.y;
             const double x0 = (b0 - t0.y * x1 - (double)t0.z * x2) / t0.x;
-            const float dl[3] = {(float)-x0, (float)-x1, (float)-x2};
-            q1 += (double)t0.w * t0.w + (double)t1.w * t1.w + (double)t2.w * t2.w;
-#pragma unroll
-            for (int q = 0; q < 3; q++) {
-                d.dl[3 * j + q] = dl[q];
-                d.pts_trial[3 * j + q] = d.pts[3 * j + q] + (double)(d.lm_s[3 * j + q] * dl[q]);
-                const double Dd = (double)d.lm_D[3 * j + q] * dl[q];
-                dd += Dd * Dd;
-            }
+            const float dlq = (float)-(qc == 0 ? x0 : qc == 1 ? x1 : x2);
+            if (gl == 0) q1 += (double)t0.w * t0.w + (double)t1.w * t1.w + (double)t2.w * t2.w;
+            d.dl[3 * j + qc] = dlq;
+            d.pts_trial[3 * j + qc] = pt + (double)(lsq * dlq);
+            const double Dd = (double)lDq * dlq;
+            dd += Dd * Dd;
         }
     }
+}
+
+__global__ void __launch_bounds__(256, RBA_BACKSUB_MINB) k_backsub(DevProblem d, BsRange r8, BsRange r32, BsRange r256) {
+    __shared__ double red[32];
+    __shared__ double sw[8][3];
+    if (d.pcg->reason == 2) return;  // indefinite attempt: no step (the LM control rejects it)
+    const double lam = d.scal[SC_LAM];
+    double q1 = 0.0, dd = 0.0;
+    const int b = blockIdx.x;
+    if (b < r8.nb) bs_regime<8>(d, r8, 0, q1, dd, sw);
+    else if (b < r8.nb + r32.nb) bs_regime<32>(d, r32, r8.nb, q1, dd, sw);
+    else bs_regime<256>(d, r256, r8.nb + r32.nb, q1, dd, sw);
     q1 = block_sum_d(q1, red);
     dd = block_sum_d(dd, red);
     if (d.det) {
@@ -2546,6 +2606,7 @@ cudaError_t launch_cam_scale(rba_ctx *c) {
 }
 
 extern double plan_marg_bytes(rba_ctx *c);
+extern double plan_backsub_bytes(rba_ctx *c);
 extern double plan_matvec_bytes(rba_ctx *c);
 
 // fork the context stream into the auxiliary streams (independent class kernels) and join back
@@ -2835,7 +2896,7 @@ cudaError_t launch_pcg_step(rba_ctx *c, cudaGraphConditionalHandle h, int use_h)
 }
 
 cudaError_t launch_backsub(rba_ctx *c) {
-    Prof P(c, KID_BACKSUB, 0.0);
+    Prof P(c, KID_BACKSUB, c->d.sc || c->d.fac || c->d.s64 ? 0.0 : plan_backsub_bytes(c));
     if (c->d.sc) {
         cudaError_t e = launch_sc_backsub(c);
         if (e) return e;
@@ -2846,8 +2907,23 @@ cudaError_t launch_backsub(rba_ctx *c) {
         cudaError_t e = launch_backsub64(c);
         if (e) return e;
     } else if (c->d.n_l) {
-        const unsigned g = (unsigned)std::min<int64_t>(nblk(32 * c->d.n_l, 256), (int64_t)c->num_sms * 8);
-        k_backsub<<<g, 256, 0, c->stream>>>(c->d);
+        // one wave; blocks per regime in proportion to its bytes, capped by its landmark count
+        static int per_sm = 0;
+        if (!per_sm && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_backsub, 256, 0) || per_sm < 1)) per_sm = 3;
+        const int64_t G = std::min<int64_t>((int64_t)c->num_sms * per_sm, DET_PART);
+        BsRange r[3];
+        int64_t lo = 0;
+        const double tot = c->bs_bytes[0] + c->bs_bytes[1] + c->bs_bytes[2];
+        constexpr int per_block[3] = {32, 8, 1};  // landmarks per block and sweep
+        for (int i = 0; i < 3; i++) {
+            const int64_t hi = std::max(lo, c->bs_hi[i]), n = hi - lo;
+            int64_t nb = n ? std::max<int64_t>(1, (int64_t)(G * c->bs_bytes[i] / tot)) : 0;
+            nb = std::min<int64_t>(nb, (n + per_block[i] - 1) / per_block[i]);
+            r[i] = BsRange{lo, hi, (int)nb};
+            lo = hi;
+        }
+        const unsigned g = (unsigned)(r[0].nb + r[1].nb + r[2].nb);
+        k_backsub<<<g, 256, 0, c->stream>>>(c->d, r[0], r[1], r[2]);
         c->launches++;
     }
     k_trial_cams<<<1, 1024, 0, c->stream>>>(c->d, c->d.sc ? 0 : 1);

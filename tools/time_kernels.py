@@ -19,10 +19,10 @@ torch.cuda.synchronize()
 rba.rba_profile(s.h, True)
 for _ in range(a.reps):
     s.set_state(p["cameras_init"], p["points_init"]); s.linearize(); s.marginalize(1e-4)
-    s.set_pcg_limits(0.0, 0); s.pcg()
+    s.set_pcg_limits(0.0, 0); s.pcg(); s.backsub()
     s.matvec(v)
 out = {"config": a.config, "det": a.det}
-for k in ("marginalize", "precond", "matvec"):
+for k in ("marginalize", "precond", "matvec", "backsub"):
     ms, n, by = rba.rba_profile_get(s.h, k)
     out[k] = {"ms": ms / n, "GBs": by / n / (ms / n * 1e-3) / 1e9, "bytes": by / n}
 print(json.dumps(out))
