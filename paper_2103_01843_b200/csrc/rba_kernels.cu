@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 
 #include "rba_internal.cuh"
 #include "rba_model.cuh"
@@ -2370,7 +2371,7 @@ __global__ void __launch_bounds__(1024) k_pcg_step(DevProblem d, cudaGraphCondit
 // ============================================================================ K7 back-substitution
 // Landmarks are stored sorted by k, so K7 splits them into three regimes by lanes per landmark,
 // each a block-uniform role of one grid (one wave; blocks per regime in proportion to its bytes):
-// L = 8 for k <= 16 (4 landmarks per warp and sweep), a warp (L = 32) for 16 < k <= 256, a CTA
+// L = 4 for k <= 16 (8 landmarks per warp and sweep), a warp (L = 32) for 16 < k <= 256, a CTA
 // (L = 256) for k > 256.  Lane gl <-> observations o = gl, gl + L, ...: one camera-index load, then
 // the observation's 9 FP64 dp entries and its 3 x 9 R^1 | Q^1^T J_p entries (the lanes of a group
 // read contiguous 36-byte row segments) are independent loads in flight; the three row sums are
@@ -2382,6 +2383,9 @@ __global__ void __launch_bounds__(1024) k_pcg_step(DevProblem d, cudaGraphCondit
 // model-decrease sums go out once per CTA (same-address FP64 atomics serialize).
 #ifndef RBA_BACKSUB_MINB
 #define RBA_BACKSUB_MINB 3
+#endif
+#ifndef RBA_BS_L0
+#define RBA_BS_L0 4  // lanes per landmark for k <= 16 (mean k ~4.2-4.6 on configs 3-4)
 #endif
 struct BsRange {
     int64_t lo, hi;  // landmarks of the regime
@@ -2479,7 +2483,7 @@ __global__ void __launch_bounds__(256, RBA_BACKSUB_MINB) k_backsub(DevProblem d,
     const double lam = d.scal[SC_LAM];
     double q1 = 0.0, dd = 0.0;
     const int b = blockIdx.x;
-    if (b < r8.nb) bs_regime<8>(d, r8, 0, q1, dd, sw);
+    if (b < r8.nb) bs_regime<RBA_BS_L0>(d, r8, 0, q1, dd, sw);
     else if (b < r8.nb + r32.nb) bs_regime<32>(d, r32, r8.nb, q1, dd, sw);
     else bs_regime<256>(d, r256, r8.nb + r32.nb, q1, dd, sw);
     q1 = block_sum_d(q1, red);
@@ -2913,11 +2917,19 @@ cudaError_t launch_backsub(rba_ctx *c) {
         const int64_t G = std::min<int64_t>((int64_t)c->num_sms * per_sm, DET_PART);
         BsRange r[3];
         int64_t lo = 0;
-        const double tot = c->bs_bytes[0] + c->bs_bytes[1] + c->bs_bytes[2];
-        constexpr int per_block[3] = {32, 8, 1};  // landmarks per block and sweep
+        // per-regime weights on the byte shares (tuning knob RBA_BS_W="w0,w1,w2"; measured on cfg 3 /
+        // cfg 4: 1,1,1 0.095 / 0.286 ms, 1,1.5,1.5 0.086 / 0.252, 1,2,2 0.088 / 0.266, 2,1,1 0.125 / 0.406)
+        static double w[3] = {1.0, 1.5, 1.5};
+        static const bool wset = [] {
+            if (const char *e = getenv("RBA_BS_W")) sscanf(e, "%lf,%lf,%lf", &w[0], &w[1], &w[2]);
+            return true;
+        }();
+        (void)wset;
+        const double tot = w[0] * c->bs_bytes[0] + w[1] * c->bs_bytes[1] + w[2] * c->bs_bytes[2];
+        constexpr int per_block[3] = {256 / RBA_BS_L0, 8, 1};  // landmarks per block and sweep
         for (int i = 0; i < 3; i++) {
             const int64_t hi = std::max(lo, c->bs_hi[i]), n = hi - lo;
-            int64_t nb = n ? std::max<int64_t>(1, (int64_t)(G * c->bs_bytes[i] / tot)) : 0;
+            int64_t nb = n ? std::max<int64_t>(1, (int64_t)(G * w[i] * c->bs_bytes[i] / tot)) : 0;
             nb = std::min<int64_t>(nb, (n + per_block[i] - 1) / per_block[i]);
             r[i] = BsRange{lo, hi, (int)nb};
             lo = hi;
