@@ -63,12 +63,19 @@ MATVEC_KERNELS = re.compile(r"k_large_pipe<\d+, \d+, (0|false)>|k_small_pipe<(0|
 MARG_KERNELS = re.compile(r"k_marg_(small|large)<|k_marg64")
 
 
+def _round_key(f):
+    """Sort key of a profiles/ capture name r<round>[<letter>]_...: (round, refresh letter); names
+    that do not follow the pattern sort first."""
+    m = re.search(r"/r(\d+)([a-z]?)_[^/]*$", f)
+    return (int(m.group(1)), m.group(2)) if m else (-1, "")
+
+
 def ncu_traffic(cfg, variant=""):
     """DRAM bytes (read + write) of ONE launch of the matvec and of the marginalization, summed over
     their per-class kernels, from the newest committed `ncu --set full` summary of this config
     (profiles/r*_cfg<cfg>_ncu_full.json, written by tools/ncu_summary.py).  None if absent."""
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_cfg{cfg}{variant}_ncu_full.json")),
-                   key=lambda f: int(re.search(r"/r(\d+)_", f).group(1)))
+                   key=_round_key)
     if not files:
         return None, None, None
     rows = json.load(open(files[-1]))
